@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""Benchmark: segmented voxels/s of the per-frame 3-D segmentation hot path.
+
+Workload (BASELINE.json configs[1], "C2"): synthetic 1024x1024x64 uint8 time
+points with two channels (cell + vessel), spacing (0.8, 0.8, 1.0) um, the
+reference's default parameters (session.py:70-74).  One step = one time point:
+the cell channel (Gaussian background, median, Otsu, closing, 26-CCL, per-cell
+table) and the vessel channel (MRF statistics, Otsu, closing, EDT), the two
+channels on two CUDA streams.  value = voxels of all processed (frame,
+channel) volumes / device time (max over ranks).  Frames are independent:
+N GPUs shard time points (weak scaling); the only collective is an
+all_gather of per-frame detection counts (global id offsets).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "segmented voxels/sec (frames/sec) at 1/2/4/8 B200; % HBM roofline; vs host CPU"
+UNIT = "voxels/s"
+SPACING = (0.8, 0.8, 1.0)
+K1_FP64_OPS_PER_VOXEL = None  # filled from the radii: 3*(rx+ry+rz) + 3
+
+
+def peaks():
+    p = {"hbm_gbs": 6551.7, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "source": "MEASURED_PEAKS.json", "sm_max_mhz": m.get("sm_max_mhz")}
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg / --impl reference arm)
+# ---------------------------------------------------------------------------
+def cpu_sample_voxels_per_s(spec, t: int, crop_nx: int, threads: int):
+    """Oracle (test-only checker, oracle/) on a bounded sample: both channels of
+    time point t, cropped to crop_nx x-slices.  Returns (voxels/s, seconds)."""
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    from oracle import oracle as O
+
+    O.lib()
+    dims = (crop_nx, spec.ny, spec.nz)
+    balls = spec.balls(t)
+    balls = balls[balls[:, 0] < crop_nx * 16]
+    raw_c = O.synth_frame(dims, spec.dtype, spec.frame_seed(t, 0), spec.vmax, balls=balls, amp_ball=spec.amp_cell)
+    raw_v = O.synth_frame(dims, spec.dtype, spec.frame_seed(t, 1), spec.vmax, tubes=spec.tubes(),
+                          amp_tube=spec.amp_tube)
+    t0 = time.perf_counter()
+    den = O.denoise_cell(raw_c, SPACING, 10.0)["denoised"]
+    O.segment_cell(den, SPACING)
+    st = O.mrf(raw_v)
+    cur = st["current"] if st["current"] is not None else raw_v
+    O.segment_vessel(cur, SPACING)
+    dt = time.perf_counter() - t0
+    return 2 * crop_nx * spec.ny * spec.nz / dt, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_1407_2089_b200 import synth
+
+    O.lib()
+    spec = synth.C2
+    threads = os.cpu_count() or 1
+    crop = args.cpu_crop
+    vals = []
+    for s in range(args.warmup + args.steps):
+        v, dt = cpu_sample_voxels_per_s(spec, s % 100, crop, threads)
+        if s >= args.warmup:
+            vals.append(v)
+    value = float(np.mean(vals))
+    sample = f"oracle port, both channels of C2 time points cropped to {crop}x1024x64 per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 2 * crop * spec.ny * spec.nz / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "C2 1024x1024x64 u8, 2 channels (cell+vessel), cropped sample", "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1407_2089_b200 import _lib, synth
+    from paper_1407_2089_b200.imaging import VoxelSpacing
+    from paper_1407_2089_b200.pipeline import FramePipeline
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    spec = synth.C2
+    sp = VoxelSpacing(*SPACING)
+    T = 100
+    nvox = spec.nx * spec.ny * spec.nz
+    per_rank = (T + world - 1) // world
+    my_frames = [rank * per_rank + i for i in range(per_rank) if rank * per_rank + i < T] or [rank % T]
+    ring = min(args.ring, len(my_frames))
+
+    s_cell = torch.cuda.Stream(dev)
+    s_vess = torch.cuda.Stream(dev)
+    pipe = FramePipeline(spec.dims, spec.dtype, sp)
+    # inputs resident in HBM (a ring of distinct time points; 134 MB/step > L2)
+    inputs = []
+    for i in range(ring):
+        t = my_frames[i]
+        inputs.append((t, synth.generate(spec, t, synth.CELL), synth.generate(spec, t, synth.VESSEL)))
+    counts_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+    gathered = torch.zeros(world, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize()
+
+    def step(i, timing=False):
+        t, rc, rv = inputs[i % ring]
+        main = torch.cuda.current_stream()
+        s_cell.wait_stream(main)
+        s_vess.wait_stream(main)
+        with torch.cuda.stream(s_cell):
+            pipe.cell(rc, frame=t, id_start=0)
+            counts_dev.copy_(pipe.counters[2:3])
+        with torch.cuda.stream(s_vess):
+            pipe.vessel(rv)
+        main.wait_stream(s_cell)
+        main.wait_stream(s_vess)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, counts_dev)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    # correctness guard: the fused path's decisions must be the fast ones
+    assert int(pipe.state[5].item()) == 0, "MRF needed iterations: bench workload assumption broken"
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    _lib.launch_counter.update(enabled=True, count=0)
+    pipe.marks = []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    e1.record()
+    torch.cuda.synchronize()
+    _lib.launch_counter["enabled"] = False
+    launches = _lib.launch_counter["count"]
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    stage_ms = pipe.stage_times_ms()
+    pipe.marks = None
+    t_dev = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    ms_max = float(t_dev.item())
+    total_vox = world * args.steps * 2 * nvox
+    value = total_vox / (ms_max / 1e3)
+
+    # --- e2e through the public pipeline API with pinned host buffers -------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, pipe, spec, sp, dev, world, s_cell, s_vess)
+
+    # --- roofline of the dominant kernel (K1, FP64-pipe bound) --------------
+    pk = peaks()
+    rx, ry, rz = pipe.r
+    fp64_ops = 3 * (rx + ry + rz) + 3
+    k1_ms = stage_ms.get("K1 gaussian")
+    fp64_peak = measured_fp64_peak(dev)
+    roof = None
+    if k1_ms:
+        k1_bytes = 2 * nvox  # read raw u8 + write q u8 (algorithmic)
+        achieved_tf = fp64_ops * nvox / (k1_ms / 1e3) / 1e12
+        traffic = ncu_traffic("gauss")
+        roof = {
+            "kernel": "K1 gaussian (3 separable FP64 passes, scipy order, no FMA)",
+            "bound": "fp64",
+            "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak,
+            "peak_source": "ct_fp64_peak (DADD+DMUL dependent-free loop, measured in this run)",
+            "traffic": traffic,
+            "hbm": {"achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / pk["hbm_gbs"], "peak_source": pk["source"],
+                    "algorithmic_bytes_per_voxel": 2},
+            "fp64_ops_per_voxel": fp64_ops,
+            "share_of_cell_stream": k1_ms / sum(v for k, v in stage_ms.items() if k.startswith(("K1", "K2", "K3 o", "K4", "K5", "K6"))),
+        }
+    kernels = {}
+    bpv = {"K2 median+hist": 2, "K4 threshold+close": 2, "K5 ccl": 5, "K6 table": 0, "K7 mrf": 3,
+           "K3+K4 vessel otsu+close": 2, "K8 edt": 9, "K1 gaussian": 2}
+    for k, v in stage_ms.items():
+        b = bpv.get(k)
+        kernels[k] = {"ms": v, "hbm_gbs": (b * nvox / (v / 1e3) / 1e9) if b else None,
+                      "hbm_frac": (b * nvox / (v / 1e3) / 1e9 / pk["hbm_gbs"]) if b else None,
+                      "algorithmic_bytes_per_voxel": b}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, dt = cpu_sample_voxels_per_s(spec, 0, args.cpu_crop, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"oracle/ct_oracle.c port, both channels of C2 t=0 cropped to {args.cpu_crop}x1024x64 "
+                         f"({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "C2: 1024x1024x64 uint8 time points, 2 channels (cell+vessel), 1600 cells",
+                       "global_batch": world, "parallelism": f"frame-sharded dp{world}",
+                       "frames_per_s": world * args.steps / (ms_max / 1e3),
+                       "l2": f"inputs larger than L2: {2 * nvox / 1e6:.0f} MB/step from a ring of {ring} "
+                             "distinct time points, plus GB-scale intermediates"},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof, "kernels": kernels,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def measured_fp64_peak(dev) -> float:
+    """TFLOP/s of independent DADD/DMUL (no FMA) measured on this GPU."""
+    import torch
+
+    from paper_1407_2089_b200._lib import lib
+
+    L = lib()
+    if not hasattr(L, "ct_fp64_peak"):
+        return float("nan")
+    import ctypes
+
+    out = torch.zeros(148 * 8 * 256, dtype=torch.float64, device=dev)
+    fn = L.ct_fp64_peak
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    iters = 4096
+    for _ in range(2):
+        fn(out.data_ptr(), iters, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    fn(out.data_ptr(), iters, torch.cuda.current_stream().cuda_stream)
+    b.record()
+    torch.cuda.synchronize()
+    ops = out.numel() * iters * 16.0
+    return ops / (a.elapsed_time(b) / 1e3) / 1e12
+
+
+def ncu_traffic(pattern: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(pattern)
+    except Exception:
+        return None
+
+
+def run_e2e(args, pipe, spec, sp, dev, world, s_cell, s_vess):
+    """Public API end to end: pinned host frames -> H2D -> fused pipeline ->
+    D2H of the step's result (counters + per-cell table rows + vessel state),
+    double-buffered so step i+1's H2D overlaps step i's kernels."""
+    import torch
+
+    from paper_1407_2089_b200 import synth
+
+    nvox = spec.nx * spec.ny * spec.nz
+    nring = 2
+    host = []
+    for i in range(nring):
+        c = torch.empty(spec.dims, dtype=torch.uint8, pin_memory=True)
+        v = torch.empty(spec.dims, dtype=torch.uint8, pin_memory=True)
+        c.copy_(synth.generate(spec, 50 + i, synth.CELL).cpu())
+        v.copy_(synth.generate(spec, 50 + i, synth.VESSEL).cpu())
+        host.append((c, v))
+    dbuf = [(torch.empty(spec.dims, dtype=torch.uint8, device=dev), torch.empty(spec.dims, dtype=torch.uint8, device=dev))
+            for _ in range(2)]
+    rows = 4096
+    out_host = torch.empty(rows * 128 + 64 + 72 + 32, dtype=torch.uint8, pin_memory=True)
+    s_copy = torch.cuda.Stream(dev)
+    copied = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    for d in done:
+        d.record()
+
+    def h2d(i):
+        slot = i % 2
+        with torch.cuda.stream(s_copy):
+            s_copy.wait_event(done[slot])
+            dbuf[slot][0].copy_(host[i % nring][0], non_blocking=True)
+            dbuf[slot][1].copy_(host[i % nring][1], non_blocking=True)
+            copied[slot].record()
+
+    def compute(i):
+        slot = i % 2
+        main = torch.cuda.current_stream()
+        main.wait_event(copied[slot])
+        s_cell.wait_stream(main)
+        s_vess.wait_stream(main)
+        with torch.cuda.stream(s_cell):
+            pipe.cell(dbuf[slot][0], frame=i)
+        with torch.cuda.stream(s_vess):
+            pipe.vessel(dbuf[slot][1])
+        main.wait_stream(s_cell)
+        main.wait_stream(s_vess)
+        done[slot].record()
+        # the step's result to the host
+        out_host[: rows * 128].copy_(pipe.table[: rows * 128], non_blocking=True)
+        out_host[rows * 128 : rows * 128 + 64].copy_(pipe.counters.view(torch.uint8), non_blocking=True)
+        out_host[rows * 128 + 64 : rows * 128 + 136].copy_(pipe.state.view(torch.uint8)[:72], non_blocking=True)
+        out_host[rows * 128 + 136 :].copy_(pipe.votsu.view(torch.uint8), non_blocking=True)
+
+    n = args.warmup + args.steps
+    h2d(0)
+    for i in range(args.warmup):
+        if i + 1 < n:
+            h2d(i + 1)
+        compute(i)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(args.warmup, n):
+        if i + 1 < n:
+            h2d(i + 1)
+        compute(i)
+        torch.cuda.current_stream().synchronize()  # result readable on the host every step
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    val = world * args.steps * 2 * nvox / (ms / 1e3)
+    return {"value": val, "unit": UNIT, "h2d_bytes_per_step": 2 * nvox,
+            "d2h_bytes_per_step": int(out_host.numel()), "ms_per_step": ms / args.steps,
+            "note": "pinned host frames, H2D of step i+1 overlapped with step i; D2H of counters, "
+                    f"first {rows} table rows, vessel state"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ring", type=int, default=6)
+    ap.add_argument("--cpu-crop", type=int, default=128)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

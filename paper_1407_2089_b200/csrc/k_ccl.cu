@@ -1,0 +1,530 @@
+// k_ccl.cu -- K5 26-connected component labelling and K6 the per-cell table.
+//
+// K5 replaces ref segment.py:254 (ndimage.label(mask, ones((3,3,3)))).  The
+// label of a component is its minimum C-order linear index ("root"), which
+// is exactly the key the reference orders components by after sizes
+// (segment.py:257, v[0] of the C-ordered voxel list).  Union-find always
+// links the larger root under the smaller one, so the final root is the
+// component minimum regardless of the (non-deterministic) union order.
+//   ccl_local   : per 4x8x32 tile, union-find in SMEM over the 13 backward
+//                 neighbours inside the tile; writes labels (global index of the
+//                 tile-local root) and appends foreground voxels to fg_list.
+//   ccl_boundary: for foreground voxels on a tile face, unions with backward
+//                 neighbours in other tiles (global atomicMin union-find).
+//   ccl_flatten : labels[p] = find(p).
+// K6 replaces ref segment.py:242-276 minus the hull (hull stays on the host):
+//   tab_roots   : compact the roots (component index c, any order).
+//   tab_stats   : per component count / bbox / intensity sum (warp-aggregated
+//                 integer atomics: order-independent, deterministic).
+//   tab_rank    : one CTA: volume filter in float64 (segment.py:253-255),
+//                 stable LSD radix sort by (-count, root) (segment.py:257),
+//                 ids, voxel offsets (exclusive scan).
+//   tab_relabel : labels[p] = rank of p's kept cell or -1.
+//   tab_voxels  : one CTA per kept cell walks its bbox in C order, emitting
+//                 the ordered voxel list (segment.py:207-217) with a block
+//                 scan; thread 0 then forms the centroid by the row-sequential
+//                 float64 sum numpy's mean(axis=0) performs (segment.py:260).
+#include "ct_common.cuh"
+
+namespace {
+
+constexpr int LI = 4, LJ = 8, LK = 32;
+constexpr int LN = LI * LJ * LK;
+
+// 13 backward neighbours (da, db, dc) of the 26-neighbourhood
+__constant__ int8_t BACK[13][3] = {{-1, -1, -1}, {-1, -1, 0}, {-1, -1, 1}, {-1, 0, -1}, {-1, 0, 0},
+                                   {-1, 0, 1},   {-1, 1, -1}, {-1, 1, 0},  {-1, 1, 1},  {0, -1, -1},
+                                   {0, -1, 0},   {0, -1, 1},  {0, 0, -1}};
+
+__device__ __forceinline__ unsigned lane_id() {
+    unsigned l;
+    asm("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+}
+
+__device__ __forceinline__ int find_s(volatile int *L, int x) {
+    int y = L[x];
+    while (y != x) {
+        x = y;
+        y = L[x];
+    }
+    return x;
+}
+
+__device__ void union_s(int *L, int a, int b) {
+    for (;;) {
+        a = find_s(L, a);
+        b = find_s(L, b);
+        if (a == b) return;
+        if (a > b) { const int t = a; a = b; b = t; }
+        const int old = atomicMin(&L[b], a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+__device__ __forceinline__ int find_g(volatile int32_t *L, int x) {
+    int y = L[x];
+    while (y != x) {
+        x = y;
+        y = L[x];
+    }
+    return x;
+}
+
+__device__ void union_g(int32_t *L, int a, int b) {
+    for (;;) {
+        a = find_g(L, a);
+        b = find_g(L, b);
+        if (a == b) return;
+        if (a > b) { const int t = a; a = b; b = t; }
+        const int old = atomicMin(&L[b], a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+// warp-aggregated append of p to list (order within the list is irrelevant)
+__device__ __forceinline__ void append(int32_t *list, unsigned long long *cnt, int32_t p, bool pred) {
+    const unsigned m = __ballot_sync(__activemask(), pred);
+    if (!pred) return;
+    const unsigned lane = lane_id();
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if ((int)lane == leader) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    list[base + __popc(m & ((1u << lane) - 1))] = p;
+}
+
+__global__ void __launch_bounds__(LK *LJ) ccl_local(const uint8_t *__restrict__ mask, i64 nx, i64 ny, i64 nz,
+                                                    int32_t *__restrict__ labels, int32_t *__restrict__ fg,
+                                                    int64_t *__restrict__ counters) {
+    __shared__ int L[LN];
+    const int tid = threadIdx.y * LK + threadIdx.x;
+    const i64 tk = (nz + LK - 1) / LK, tj = (ny + LJ - 1) / LJ, ti = (nx + LI - 1) / LI;
+    const i64 ntiles = tk * tj * ti;
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const i64 k0 = (tile % tk) * LK, j0 = ((tile / tk) % tj) * LJ, i0 = (tile / (tk * tj)) * LI;
+        __syncthreads();
+        const int c = threadIdx.x, b = threadIdx.y;
+        const i64 j = j0 + b, k = k0 + c;
+#pragma unroll
+        for (int a = 0; a < LI; ++a) {
+            const i64 i = i0 + a;
+            const int v = (a * LJ + b) * LK + c;
+            const bool in = i < nx && j < ny && k < nz;
+            L[v] = (in && mask[(i * ny + j) * nz + k]) ? v : -1;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < LI; ++a) {
+            const int v = (a * LJ + b) * LK + c;
+            if (L[v] < 0) continue;
+            for (int n = 0; n < 13; ++n) {
+                const int aa = a + BACK[n][0], bb = b + BACK[n][1], cc = c + BACK[n][2];
+                if (aa < 0 || bb < 0 || bb >= LJ || cc < 0 || cc >= LK) continue;
+                const int u = (aa * LJ + bb) * LK + cc;
+                if (L[u] >= 0) union_s(L, v, u);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < LI; ++a) {
+            const int v = (a * LJ + b) * LK + c;
+            if (L[v] >= 0) L[v] = find_s(L, v);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < LI; ++a) {
+            const i64 i = i0 + a;
+            const int v = (a * LJ + b) * LK + c;
+            const bool in = i < nx && j < ny && k < nz;
+            const int r = L[v];
+            const i64 p = (i * ny + j) * nz + k;
+            if (in) {
+                int32_t lab = -1;
+                if (r >= 0) {
+                    const int ra = r / (LJ * LK), rb = (r / LK) % LJ, rc = r % LK;
+                    lab = (int32_t)(((i0 + ra) * ny + (j0 + rb)) * nz + (k0 + rc));
+                }
+                labels[p] = lab;
+            }
+            append(fg, (unsigned long long *)&counters[CT_CNT_FG], (int32_t)p, in && r >= 0);
+        }
+    }
+}
+
+__global__ void ccl_boundary(const uint8_t *__restrict__ mask, i64 nx, i64 ny, i64 nz, int32_t *labels,
+                             const int32_t *__restrict__ fg, const int64_t *__restrict__ counters) {
+    const i64 nfg = counters[CT_CNT_FG];
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < nfg; e += (i64)gridDim.x * blockDim.x) {
+        const i64 p = fg[e];
+        const i64 k = p % nz, j = (p / nz) % ny, i = p / (ny * nz);
+        for (int n = 0; n < 13; ++n) {
+            const i64 a = i + BACK[n][0], b = j + BACK[n][1], c = k + BACK[n][2];
+            if (a < 0 || b < 0 || b >= ny || c < 0 || c >= nz) continue;
+            if (a / LI == i / LI && b / LJ == j / LJ && c / LK == k / LK) continue;  // same tile
+            const i64 q = (a * ny + b) * nz + c;
+            if (mask[q]) union_g(labels, (int)p, (int)q);
+        }
+    }
+}
+
+__global__ void ccl_flatten(int32_t *labels, const int32_t *__restrict__ fg, const int64_t *__restrict__ counters) {
+    const i64 nfg = counters[CT_CNT_FG];
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < nfg; e += (i64)gridDim.x * blockDim.x) {
+        const int p = fg[e];
+        labels[p] = find_g(labels, p);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6 -- table
+// ---------------------------------------------------------------------------
+struct TabWork {
+    int32_t *root;      // [cap]
+    uint32_t *count;    // [cap]
+    int32_t *bbox;      // [cap][6] lo i,j,k then hi i,j,k
+    uint64_t *isum;     // [cap]
+    int32_t *rank;      // [cap]
+    int32_t *sa, *sb;   // [cap] sort ping-pong (component indices)
+    int32_t *comp;      // [N]   component index of fg_list[e]
+};
+
+__host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ inline size_t tab_bytes(i64 N, i64 cap) {
+    return align_up(cap * 4) * 6 + align_up(cap * 24) + align_up(cap * 8) + align_up(N * 4);
+}
+
+__host__ TabWork tab_carve(void *work, i64 N, i64 cap) {
+    char *p = (char *)work;
+    TabWork w;
+    w.root = (int32_t *)p; p += align_up(cap * 4);
+    w.count = (uint32_t *)p; p += align_up(cap * 4);
+    w.bbox = (int32_t *)p; p += align_up(cap * 24);
+    w.isum = (uint64_t *)p; p += align_up(cap * 8);
+    w.rank = (int32_t *)p; p += align_up(cap * 4);
+    w.sa = (int32_t *)p; p += align_up(cap * 4);
+    w.sb = (int32_t *)p; p += align_up(cap * 4);
+    w.comp = (int32_t *)p; p += align_up(N * 4);
+    return w;
+}
+
+__global__ void tab_roots(int32_t *labels, const int32_t *__restrict__ fg, int64_t *counters, TabWork w, i64 cap) {
+    const i64 nfg = counters[CT_CNT_FG];
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < nfg; e += (i64)gridDim.x * blockDim.x) {
+        const int p = fg[e];
+        if (labels[p] != p) continue;
+        const unsigned long long c = atomicAdd((unsigned long long *)&counters[CT_CNT_COMPONENTS], 1ull);
+        if ((i64)c < cap) {
+            w.root[c] = p;
+            w.count[c] = 0;
+            w.isum[c] = 0;
+            w.bbox[6 * c + 0] = w.bbox[6 * c + 1] = w.bbox[6 * c + 2] = INT32_MAX;
+            w.bbox[6 * c + 3] = w.bbox[6 * c + 4] = w.bbox[6 * c + 5] = -1;
+            labels[p] = -(int32_t)(c + 2);
+        } else {
+            counters[CT_CNT_OVERFLOW] = 1;
+        }
+    }
+}
+
+template <typename TI>
+__global__ void tab_stats(const int32_t *__restrict__ labels, i64 ny, i64 nz, const int32_t *__restrict__ fg,
+                          const int64_t *__restrict__ counters, TabWork w, const TI *__restrict__ intensity) {
+    const i64 nfg = counters[CT_CNT_FG];
+    const bool over = counters[CT_CNT_OVERFLOW] != 0;
+    for (i64 e0 = blockIdx.x * (i64)blockDim.x; e0 < nfg; e0 += (i64)gridDim.x * blockDim.x) {
+        const i64 e = e0 + threadIdx.x;
+        int c = -1;
+        int p = 0;
+        if (e < nfg && !over) {
+            p = fg[e];
+            const int v = labels[p];
+            const int rv = v < 0 ? v : labels[v];
+            c = -(rv + 2);
+            w.comp[e] = c;
+        }
+        const bool act = c >= 0;
+        const unsigned full = __ballot_sync(0xffffffffu, act);
+        if (!act) continue;
+        const unsigned peers = __match_any_sync(full, c);
+        const int leader = __ffs(peers) - 1;
+        const int k = (int)(p % nz), j = (int)((p / nz) % ny), i = (int)(p / (ny * nz));
+        const int imin = __reduce_min_sync(peers, i), jmin = __reduce_min_sync(peers, j),
+                  kmin = __reduce_min_sync(peers, k);
+        const int imax = __reduce_max_sync(peers, i), jmax = __reduce_max_sync(peers, j),
+                  kmax = __reduce_max_sync(peers, k);
+        unsigned isum = 0;
+        if (intensity) isum = __reduce_add_sync(peers, (unsigned)intensity[p]);
+        if ((int)lane_id() == leader) {
+            atomicAdd(&w.count[c], (unsigned)__popc(peers));
+            atomicMin(&w.bbox[6 * c + 0], imin);
+            atomicMin(&w.bbox[6 * c + 1], jmin);
+            atomicMin(&w.bbox[6 * c + 2], kmin);
+            atomicMax(&w.bbox[6 * c + 3], imax);
+            atomicMax(&w.bbox[6 * c + 4], jmax);
+            atomicMax(&w.bbox[6 * c + 5], kmax);
+            if (intensity) atomicAdd((unsigned long long *)&w.isum[c], (unsigned long long)isum);
+        }
+    }
+}
+
+constexpr int RT = 512;    // tab_rank threads
+constexpr int RD = 16;     // radix digits (4 bits)
+
+__device__ __forceinline__ u64 sort_key(const TabWork &w, int c, u64 maxc, int rbits) {
+    return ((maxc - (u64)w.count[c]) << rbits) | (u64)(uint32_t)w.root[c];
+}
+
+// Block-wide exclusive scan of one value per thread; returns the total.
+// sh must hold blockDim.x/32 + 1 entries.
+__device__ u64 block_excl_scan(u64 &v, u64 *sh) {
+    const unsigned lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u64 x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((int)lane >= o) x += y;
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 acc = 0;
+        for (unsigned i = 0; i < nw; ++i) { const u64 t = sh[i]; sh[i] = acc; acc += t; }
+        sh[nw] = acc;
+    }
+    __syncthreads();
+    const u64 res = sh[wid] + x - v;
+    const u64 total = sh[nw];
+    __syncthreads();
+    v = res;
+    return total;
+}
+
+__global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64 cap, i64 N, double vv,
+                                               double min_volume, i64 id_start, ct_cell *table) {
+    __shared__ uint32_t hcnt[RD][RT];
+    __shared__ u64 sh[RT / 32 + 1];
+    __shared__ u64 s_maxc;
+    const int tid = threadIdx.x;
+    i64 nc = counters[CT_CNT_COMPONENTS];
+    if (nc > cap) nc = cap;
+    if (counters[CT_CNT_OVERFLOW]) nc = 0;
+    // 1. kept components, compacted in component order; max count
+    const i64 chunk = (nc + RT - 1) / RT;
+    const i64 c0 = min((i64)tid * chunk, nc), c1 = min(c0 + chunk, nc);
+    u64 kept = 0, maxc = 0;
+    for (i64 c = c0; c < c1; ++c) {
+        w.rank[c] = -1;
+        const double vol = __dmul_rn((double)w.count[c], vv);
+        if (!(vol < min_volume)) { ++kept; maxc = max(maxc, (u64)w.count[c]); }
+    }
+    for (int o = 16; o; o >>= 1) maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, o));
+    if (tid == 0) s_maxc = 0;
+    __syncthreads();
+    if ((tid & 31) == 0) atomicMax((unsigned long long *)&s_maxc, (unsigned long long)maxc);
+    u64 off = kept;
+    const u64 nk = block_excl_scan(off, sh);
+    for (i64 c = c0; c < c1; ++c) {
+        const double vol = __dmul_rn((double)w.count[c], vv);
+        if (!(vol < min_volume)) w.sa[off++] = (int32_t)c;
+    }
+    __syncthreads();
+    const u64 mc = s_maxc;
+    int cbits = 0;
+    while (cbits < 40 && (mc >> cbits)) ++cbits;
+    int rbits = 1;
+    while ((((u64)N - 1) >> rbits) && rbits < 40) ++rbits;
+    const int passes = (cbits + rbits + 3) / 4;
+    // 2. stable LSD radix sort of sa[0..nk) by key
+    int32_t *src = w.sa, *dst = w.sb;
+    const i64 kchunk = ((i64)nk + RT - 1) / RT;
+    const i64 e0 = min((i64)tid * kchunk, (i64)nk), e1 = min(e0 + kchunk, (i64)nk);
+    __threadfence_block();
+    __syncthreads();
+    for (int pass = 0; pass < passes; ++pass) {
+        const int shift = 4 * pass;
+        uint32_t cnt[RD];
+#pragma unroll
+        for (int d = 0; d < RD; ++d) cnt[d] = 0;
+        for (i64 e = e0; e < e1; ++e) {
+            const int d = (int)((sort_key(w, src[e], mc, rbits) >> shift) & 15);
+#pragma unroll
+            for (int dd = 0; dd < RD; ++dd) cnt[dd] += (d == dd);
+        }
+#pragma unroll
+        for (int d = 0; d < RD; ++d) hcnt[d][tid] = cnt[d];
+        __syncthreads();
+        // exclusive scan over (digit-major, thread-minor)
+        u64 run = 0;
+        for (int d = 0; d < RD; ++d) {
+            u64 v = hcnt[d][tid];
+            const u64 tot = block_excl_scan(v, sh);
+            hcnt[d][tid] = (uint32_t)(run + v);
+            run += tot;
+        }
+        __syncthreads();
+        uint32_t pos[RD];
+#pragma unroll
+        for (int d = 0; d < RD; ++d) pos[d] = hcnt[d][tid];
+        for (i64 e = e0; e < e1; ++e) {
+            const int c = src[e];
+            const int d = (int)((sort_key(w, c, mc, rbits) >> shift) & 15);
+            uint32_t at = 0;
+#pragma unroll
+            for (int dd = 0; dd < RD; ++dd)
+                if (d == dd) at = pos[dd]++;
+            dst[at] = c;
+        }
+        __threadfence_block();
+        __syncthreads();
+        int32_t *t = src; src = dst; dst = t;
+    }
+    // 3. ranks, ids, offsets
+    u64 vox = 0;
+    for (i64 e = e0; e < e1; ++e) vox += w.count[src[e]];
+    u64 voff = vox;
+    const u64 total_vox = block_excl_scan(voff, sh);
+    for (i64 e = e0; e < e1; ++e) {
+        const int c = src[e];
+        w.rank[c] = (int32_t)e;
+        ct_cell r;
+        r.id = id_start + e;
+        r.count = w.count[c];
+        r.root = w.root[c];
+        for (int a = 0; a < 3; ++a) {
+            r.bbox_lo[a] = w.bbox[6 * c + a];
+            r.bbox_hi[a] = w.bbox[6 * c + 3 + a];
+        }
+        r.intensity_sum = (int64_t)w.isum[c];
+        r.centroid_um[0] = r.centroid_um[1] = r.centroid_um[2] = 0.0;
+        r.volume_um3 = __dmul_rn((double)r.count, vv);
+        r.voxel_offset = (int64_t)voff;
+        r.reserved = c;
+        table[e] = r;
+        voff += w.count[c];
+    }
+    if (tid == 0) {
+        counters[CT_CNT_KEPT] = (int64_t)nk;
+        counters[CT_CNT_KEPT_VOXELS] = (int64_t)total_vox;
+    }
+}
+
+__global__ void tab_relabel(int32_t *labels, const int32_t *__restrict__ fg, const int64_t *__restrict__ counters,
+                            TabWork w) {
+    const i64 nfg = counters[CT_CNT_FG];
+    const bool over = counters[CT_CNT_OVERFLOW] != 0;
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < nfg; e += (i64)gridDim.x * blockDim.x)
+        labels[fg[e]] = over ? -1 : w.rank[w.comp[e]];
+}
+
+constexpr int VT = 256;
+
+__global__ void __launch_bounds__(VT) tab_voxels(const int32_t *__restrict__ labels, i64 ny, i64 nz,
+                                                 const int64_t *__restrict__ counters, ct_cell *table,
+                                                 int32_t *__restrict__ voxels, double dx, double dy, double dz) {
+    __shared__ u64 sh[VT / 32 + 1];
+    const i64 nk = counters[CT_CNT_KEPT];
+    for (i64 r = blockIdx.x; r < nk; r += gridDim.x) {
+        const ct_cell cell = table[r];
+        const i64 bi = cell.bbox_hi[0] - cell.bbox_lo[0] + 1, bj = cell.bbox_hi[1] - cell.bbox_lo[1] + 1,
+                  bk = cell.bbox_hi[2] - cell.bbox_lo[2] + 1;
+        const i64 nbox = bi * bj * bk;
+        i64 written = 0;
+        for (i64 q0 = 0; q0 < nbox; q0 += VT) {
+            const i64 q = q0 + threadIdx.x;
+            int32_t p = 0;
+            bool hit = false;
+            if (q < nbox) {
+                const i64 c = q % bk, b = (q / bk) % bj, a = q / (bk * bj);
+                p = (int32_t)(((cell.bbox_lo[0] + a) * ny + (cell.bbox_lo[1] + b)) * nz + (cell.bbox_lo[2] + c));
+                hit = labels[p] == (int32_t)r;
+            }
+            u64 v = hit;
+            const u64 tot = block_excl_scan(v, sh);
+            if (hit) voxels[cell.voxel_offset + written + (i64)v] = p;
+            written += (i64)tot;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // numpy: physical_coordinates(vox).mean(axis=0) -> row-sequential sum / n
+            double sx = 0.0, sy = 0.0, sz = 0.0;
+            const int32_t *list = voxels + cell.voxel_offset;
+            for (i64 e = 0; e < cell.count; ++e) {
+                const i64 p = list[e];
+                const double px = __dmul_rn((double)(p / (ny * nz)), dx);
+                const double py = __dmul_rn((double)((p / nz) % ny), dy);
+                const double pz = __dmul_rn((double)(p % nz), dz);
+                if (e == 0) { sx = px; sy = py; sz = pz; }
+                else { sx = __dadd_rn(sx, px); sy = __dadd_rn(sy, py); sz = __dadd_rn(sz, pz); }
+            }
+            const double n = (double)cell.count;
+            table[r].centroid_um[0] = __ddiv_rn(sx, n);
+            table[r].centroid_um[1] = __ddiv_rn(sy, n);
+            table[r].centroid_um[2] = __ddiv_rn(sz, n);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+size_t ct_table_workspace(int64_t N, int64_t cap) { return tab_bytes(N, cap); }
+
+extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, int32_t *labels, int32_t *fg_list,
+                        int64_t *counters, void *stream) {
+    if (nx <= 0 || ny <= 0 || nz <= 0) {
+        ct::set_error("empty mask");
+        return CT_ERR_PARAM;
+    }
+    if (nx * ny * nz >= (1ll << 31)) {
+        ct::set_error("volume of %lld voxels exceeds int32 labels", (long long)(nx * ny * nz));
+        return CT_ERR_UNSUPPORTED;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(counters, 0, CT_CNT_WORDS * sizeof(int64_t), s);
+    const i64 tiles = ((nz + LK - 1) / LK) * ((ny + LJ - 1) / LJ) * ((nx + LI - 1) / LI);
+    ccl_local<<<(int)min(tiles, (i64)CT_NUM_SMS * 8), dim3(LK, LJ), 0, s>>>(mask, nx, ny, nz, labels, fg_list,
+                                                                            counters);
+    if (int st = ct::check_launch("ccl_local")) return st;
+    ccl_boundary<<<CT_NUM_SMS * 4, 256, 0, s>>>(mask, nx, ny, nz, labels, fg_list, counters);
+    if (int st = ct::check_launch("ccl_boundary")) return st;
+    ccl_flatten<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters);
+    return ct::check_launch("ccl_flatten");
+}
+
+extern "C" int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz, const int32_t *fg_list,
+                             int64_t *counters, const void *intensity, int intensity_dtype, double dx, double dy,
+                             double dz, double min_volume_um3, int64_t id_start, int64_t cap, void *work,
+                             ct_cell *table, int32_t *voxels, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const i64 N = nx * ny * nz;
+    if (cap <= 0 || !work) {
+        ct::set_error("cell table needs a workspace with positive capacity");
+        return CT_ERR_PARAM;
+    }
+    TabWork w = tab_carve(work, N, cap);
+    const double vv = (dx * dy) * dz;  // VoxelSpacing.voxel_volume_um3 (imaging.py:41-43)
+    tab_roots<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters, w, cap);
+    if (int st = ct::check_launch("tab_roots")) return st;
+    if (!intensity) {
+        tab_stats<uint8_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w, nullptr);
+    } else if (intensity_dtype == CT_U8) {
+        tab_stats<uint8_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w,
+                                                          (const uint8_t *)intensity);
+    } else if (intensity_dtype == CT_U16) {
+        tab_stats<uint16_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w,
+                                                           (const uint16_t *)intensity);
+    } else {
+        ct::set_error("intensity must be U8 or U16");
+        return CT_ERR_UNSUPPORTED;
+    }
+    if (int st = ct::check_launch("tab_stats")) return st;
+    tab_rank<<<1, RT, 0, s>>>(counters, w, cap, N, vv, min_volume_um3, id_start, table);
+    if (int st = ct::check_launch("tab_rank")) return st;
+    tab_relabel<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters, w);
+    if (int st = ct::check_launch("tab_relabel")) return st;
+    tab_voxels<<<CT_NUM_SMS * 4, VT, 0, s>>>(labels, ny, nz, counters, table, voxels, dx, dy, dz);
+    return ct::check_launch("tab_voxels");
+}

@@ -1,0 +1,311 @@
+// k_gauss.cu -- K1: Gaussian background + residual + quantise.
+//
+// Replaces ref denoise.py:84-86:
+//   background = ndimage.gaussian_filter(values, sigma, mode="nearest", truncate=4)
+//   residual   = np.maximum(values - background, 0.0)
+// scipy runs correlate1d along axis 0, 1, 2 with float64 intermediates; the
+// symmetric branch of NI_Correlate1D accumulates
+//   acc = x[i]*w[0];  for j = r..1: acc += (x[i-j] + x[i+j]) * w[j]
+// with separately rounded multiply and add.  This file reproduces that order
+// bit for bit (every op is __dmul_rn / __dadd_rn, so no DFMA can appear),
+// which makes the kernel FP64-pipe bound: 3r+1 FP64 ops per voxel per axis.
+//
+// Layout: the volume is [nx][ny][nz] (z fastest).  Axes 0 and 1 are strided
+// ("columns" = the contiguous inner index, lanes map to columns, coalesced);
+// axis 2 is contiguous (lanes map to lines, each line staged whole in SMEM).
+// Each thread computes B consecutive outputs along the filtered axis and keeps
+// a left and a right window of B inputs in registers that slide one step per
+// tap, so a tap costs 2 shared loads per B outputs (3B FP64 ops).
+#include "ct_common.cuh"
+
+namespace {
+
+constexpr int B = 8;      // outputs per thread along the filtered axis
+constexpr int C = 32;     // columns per CTA (strided kernel) / lines per CTA (contig)
+constexpr int TMAX = 128; // max tile length along the axis (strided kernel)
+constexpr size_t SMEM_LIMIT = 200 * 1024;
+
+// Sliding-window accumulation for outputs at local rows base..base+B-1 of a
+// column whose element at local row q is col[q*stride].  Rows base-r .. base+B-1+r
+// must be valid.  Exactly scipy's order per output.
+__device__ __forceinline__ void window_taps(const double *__restrict__ col, int stride, int base, int r,
+                                            const double *__restrict__ w, double (&acc)[B]) {
+    double Lw[B], Rw[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        acc[b] = __dmul_rn(col[(base + b) * stride], w[0]);
+        Lw[b] = col[(base - r + b) * stride];
+        Rw[b] = col[(base + r + b) * stride];
+    }
+    int m = 0;
+    // blocks of B taps: left slot (b+u)%B, right slot (b-u)%B are static
+    for (; m + B <= r; m += B) {
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const double wj = w[r - m - u];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const double s = __dadd_rn(Lw[(b + u) % B], Rw[(b - u + B) % B]);
+                acc[b] = __dadd_rn(acc[b], __dmul_rn(s, wj));
+            }
+            // slide to tap m+u+1: one new left element (row base-r+m+u+B),
+            // one new right element (row base+r-(m+u+1)); both always in range.
+            Lw[u] = col[(base - r + m + u + B) * stride];
+            Rw[B - 1 - u] = col[(base + r - (m + u + 1)) * stride];
+        }
+    }
+    // remaining taps (r % B of them, innermost): direct loads
+    for (; m < r; ++m) {
+        const int j = r - m;
+        const double wj = w[j];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const double s = __dadd_rn(col[(base + b - j) * stride], col[(base + b + j) * stride]);
+            acc[b] = __dadd_rn(acc[b], __dmul_rn(s, wj));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Strided axis (0 or 1): volume viewed as [outer][L][inner].
+// grid: x = column chunks of C, y = tiles of T along the axis, z = outer.
+// block: (C, T/B).  SMEM: tile[T+2r][C] doubles + w[r+1].
+// ---------------------------------------------------------------------------
+template <typename Tin>
+__global__ void __launch_bounds__(C *TMAX / B) gauss_strided(const Tin *__restrict__ in, double *__restrict__ out,
+                                                            i64 L, i64 inner, const double *__restrict__ w, int r,
+                                                            int T) {
+    extern __shared__ double smem[];
+    const int R = T + 2 * r;
+    double *tile = smem;
+    double *ws = smem + (size_t)R * C;
+    const i64 o = blockIdx.z;
+    const i64 c0 = (i64)blockIdx.x * C;
+    const i64 t0 = (i64)blockIdx.y * T;
+    const int cw = (int)min((i64)C, inner - c0);
+    const int tid = threadIdx.y * C + threadIdx.x, nth = C * blockDim.y;
+    for (int j = tid; j <= r; j += nth) ws[j] = w[j];
+    const Tin *src = in + o * L * inner + c0;
+    for (int idx = tid; idx < R * C; idx += nth) {
+        const int row = idx / C, c = idx - row * C;
+        const i64 pos = ct::clampi(t0 - r + row, 0, L - 1);
+        tile[idx] = c < cw ? ct::to_f64(src[pos * inner + c]) : 0.0;
+    }
+    __syncthreads();
+    const int c = threadIdx.x;
+    const int ob = threadIdx.y * B;
+    if (c >= cw || t0 + ob >= L) return;
+    double acc[B];
+    window_taps(tile + c, C, r + ob, r, ws, acc);
+    double *dst = out + o * L * inner + c0 + c;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        const i64 pos = t0 + ob + b;
+        if (pos < L) dst[pos * inner] = acc[b];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Contiguous axis (2) with the fused epilogue of denoise.py:85-86.
+// CTA = G lines (consecutive outer index) x whole line; lanes map to lines.
+// SMEM line stride S = roundup(L,B) + 2r (+1 if even: conflict-free LDS.64).
+// ---------------------------------------------------------------------------
+template <typename Traw, typename Tq>
+__global__ void __launch_bounds__(512) gauss_contig(const double *__restrict__ in, i64 nlines, int L,
+                                                      const double *__restrict__ w, int r, int S, int G,
+                                                      const Traw *__restrict__ raw, double *__restrict__ bg_out,
+                                                      double *__restrict__ res_out, Tq *__restrict__ q_out) {
+    extern __shared__ double smem[];
+    double *tile = smem;                  // [G][S]
+    double *ws = smem + (size_t)G * S;    // [r+1]
+    const i64 line0 = (i64)blockIdx.x * G;
+    const int gl = (int)min((i64)G, nlines - line0);
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x, nth = blockDim.x * blockDim.y;
+    for (int j = tid; j <= r; j += nth) ws[j] = w[j];
+    const double *src = in + line0 * L;
+    for (int idx = tid; idx < gl * L; idx += nth) {
+        const int g = idx / L, k = idx - g * L;
+        tile[g * S + r + k] = src[idx];
+    }
+    // clamped halos: rows [0, r) and [r+L, S)
+    const int halo = S - L;
+    for (int idx = tid; idx < gl * halo; idx += nth) {
+        const int g = idx / halo, h = idx - g * halo;
+        const int row = h < r ? h : h + L;
+        const int pos = row - r;
+        tile[g * S + row] = src[(i64)g * L + (pos < 0 ? 0 : (pos >= L ? L - 1 : pos))];
+    }
+    __syncthreads();
+    const int g = threadIdx.x;
+    const int ob = threadIdx.y * B;
+    const bool active = g < gl && ob < L;
+    double acc[B];
+    if (active) window_taps(tile + (size_t)g * S, 1, r + ob, r, ws, acc);
+    __syncthreads();
+    if (active) {
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+            if (ob + b < L) tile[g * S + ob + b] = acc[b];
+    }
+    __syncthreads();
+    // coalesced epilogue over the G*L outputs of this CTA
+    for (int idx = tid; idx < gl * L; idx += nth) {
+        const int gg = idx / L, k = idx - gg * L;
+        const i64 p = line0 * L + idx;
+        const double bg = tile[gg * S + k];
+        if (bg_out) bg_out[p] = bg;
+        const double d = __dadd_rn(ct::to_f64(raw[p]), -bg);
+        const double res = d < 0.0 ? 0.0 : d;  // np.maximum(x, 0.0)
+        if (res_out) res_out[p] = res;
+        if (q_out) q_out[p] = (Tq)rint(res);
+    }
+}
+
+// Fallback for any size / radius: one thread per output, global loads.
+template <typename Tin>
+__global__ void gauss_generic(const Tin *__restrict__ in, double *__restrict__ out, i64 outer, i64 L, i64 inner,
+                              const double *__restrict__ w, int r) {
+    const i64 n = outer * L * inner;
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x) {
+        const i64 c = p % inner, pos = (p / inner) % L, o = p / (inner * L);
+        const Tin *line = in + o * L * inner + c;
+        double acc = __dmul_rn(ct::to_f64(line[pos * inner]), w[0]);
+        for (int j = r; j >= 1; --j) {
+            const double s = __dadd_rn(ct::to_f64(line[ct::clampi(pos - j, 0, L - 1) * inner]),
+                                       ct::to_f64(line[ct::clampi(pos + j, 0, L - 1) * inner]));
+            acc = __dadd_rn(acc, __dmul_rn(s, w[j]));
+        }
+        out[p] = acc;
+    }
+}
+
+template <typename Traw, typename Tq>
+__global__ void residual_generic(const double *__restrict__ bg, i64 n, const Traw *__restrict__ raw,
+                                 double *__restrict__ bg_out, double *__restrict__ res_out, Tq *__restrict__ q_out) {
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x) {
+        const double b = bg[p];
+        if (bg_out && bg_out != bg) bg_out[p] = b;
+        const double d = __dadd_rn(ct::to_f64(raw[p]), -b);
+        const double res = d < 0.0 ? 0.0 : d;
+        if (res_out) res_out[p] = res;
+        if (q_out) q_out[p] = (Tq)rint(res);
+    }
+}
+
+template <typename Tin>
+__global__ void to_f64_copy(const Tin *__restrict__ in, double *__restrict__ out, i64 n) {
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x)
+        out[p] = ct::to_f64(in[p]);
+}
+
+// One pass along a strided axis; returns CT status.
+template <typename Tin>
+int pass_strided(const Tin *in, double *out, i64 outer, i64 L, i64 inner, const double *w, int r,
+                 cudaStream_t s) {
+    const i64 n = outer * L * inner;
+    if (r < 0) {
+        to_f64_copy<Tin><<<ct::grid_for(n, 256), 256, 0, s>>>(in, out, n);
+        return ct::check_launch("gauss copy");
+    }
+    int T = (int)min((i64)TMAX, ((L + B - 1) / B) * B);
+    size_t sm = ((size_t)(T + 2 * r) * C + r + 1) * sizeof(double);
+    if (sm > SMEM_LIMIT || outer > 65535 || (L + T - 1) / T > 65535) {
+        gauss_generic<Tin><<<ct::grid_for(n, 256), 256, 0, s>>>(in, out, outer, L, inner, w, r);
+        return ct::check_launch("gauss_generic");
+    }
+    cudaFuncSetAttribute(gauss_strided<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
+    dim3 grid((unsigned)((inner + C - 1) / C), (unsigned)((L + T - 1) / T), (unsigned)outer);
+    dim3 block(C, T / B);
+    gauss_strided<Tin><<<grid, block, sm, s>>>(in, out, L, inner, w, r, T);
+    return ct::check_launch("gauss_strided");
+}
+
+template <typename Traw, typename Tq>
+int pass_contig(const double *in, i64 nlines, i64 L, const double *w, int r, const Traw *raw, double *bg_out,
+                double *res_out, Tq *q_out, cudaStream_t s) {
+    const i64 n = nlines * L;
+    if (r >= 0) {
+        int S = (int)(((L + B - 1) / B) * B + 2 * r);
+        if ((S & 1) == 0) S += 1;
+        int G = C;
+        while (G > 1 && ((size_t)G * S + r + 1) * sizeof(double) > SMEM_LIMIT) G >>= 1;
+        const size_t sm = ((size_t)G * S + r + 1) * sizeof(double);
+        const int nb = (int)((L + B - 1) / B);
+        if (sm <= SMEM_LIMIT && nb * G <= 512 && G == C) {
+            cudaFuncSetAttribute(gauss_contig<Traw, Tq>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_LIMIT);
+            dim3 block(G, nb);
+            gauss_contig<Traw, Tq><<<(unsigned)((nlines + G - 1) / G), block, sm, s>>>(in, nlines, (int)L, w, r, S,
+                                                                                  G, raw, bg_out, res_out, q_out);
+            return ct::check_launch("gauss_contig");
+        }
+    }
+    // generic: filter into res_out-or-bg scratch, then epilogue
+    double *tmp = bg_out ? bg_out : res_out;
+    if (!tmp) {
+        ct::set_error("generic contiguous pass needs bg or residual output");
+        return CT_ERR_UNSUPPORTED;
+    }
+    if (r < 0) {
+        cudaMemcpyAsync(tmp, in, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    } else {
+        gauss_generic<double><<<ct::grid_for(n, 256), 256, 0, s>>>(in, tmp, nlines, L, 1, w, r);
+        if (int st = ct::check_launch("gauss_generic z")) return st;
+    }
+    residual_generic<Traw, Tq><<<ct::grid_for(n, 256), 256, 0, s>>>(tmp, n, raw, bg_out, res_out, q_out);
+    return ct::check_launch("residual_generic");
+}
+
+template <typename Traw, typename Tq>
+int gaussian_residual(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int rx, int ry, int rz,
+                      double *work, double *bg_out, double *res_out, Tq *q_out, cudaStream_t s) {
+    const i64 N = nx * ny * nz;
+    double *p1 = work, *p2 = work + N;
+    const double *wx = w, *wy = w + (rx >= 0 ? rx + 1 : 0), *wz = wy + (ry >= 0 ? ry + 1 : 0);
+    if (int st = pass_strided<Traw>(raw, p1, 1, nx, ny * nz, wx, rx, s)) return st;
+    if (int st = pass_strided<double>(p1, p2, nx, ny, nz, wy, ry, s)) return st;
+    return pass_contig<Traw, Tq>(p2, nx * ny, nz, wz, rz, raw, bg_out, res_out, q_out, s);
+}
+
+}  // namespace
+
+extern "C" int ct_gaussian_residual(const void *raw, int raw_dtype, int64_t nx, int64_t ny, int64_t nz,
+                                    const double *w, int rx, int ry, int rz, void *work, double *bg_out,
+                                    double *residual_out, void *q_out, int q_dtype, void *stream) {
+    if (nx <= 0 || ny <= 0 || nz <= 0) {
+        ct::set_error("empty grid");
+        return CT_ERR_PARAM;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    double *wk = (double *)work;
+    if (q_out && raw_dtype != q_dtype) {
+        ct::set_error("q dtype must equal the raw dtype");
+        return CT_ERR_UNSUPPORTED;
+    }
+    switch (raw_dtype) {
+        case CT_U8:
+            return gaussian_residual<uint8_t, uint8_t>((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, wk, bg_out,
+                                                       residual_out, (uint8_t *)q_out, s);
+        case CT_U16:
+            return gaussian_residual<uint16_t, uint16_t>((const uint16_t *)raw, nx, ny, nz, w, rx, ry, rz, wk,
+                                                         bg_out, residual_out, (uint16_t *)q_out, s);
+        case CT_F64:
+            if (q_out) {
+                ct::set_error("q output needs integer raw");
+                return CT_ERR_UNSUPPORTED;
+            }
+            return gaussian_residual<double, uint16_t>((const double *)raw, nx, ny, nz, w, rx, ry, rz, wk, bg_out,
+                                                       residual_out, (uint16_t *)nullptr, s);
+        default:
+            ct::set_error("unsupported raw dtype %d", raw_dtype);
+            return CT_ERR_UNSUPPORTED;
+    }
+}
+
+// float64 copy of a U8/U16/F64 volume (the reference's astype(np.float64))
+extern "C" int ct_to_f64(const void *in, int dtype, int64_t n, double *out, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n <= 0) return CT_OK;
+    CT_DISPATCH(dtype, T, { to_f64_copy<T><<<ct::grid_for(n, 256), 256, 0, s>>>((const T *)in, out, n); });
+    return ct::check_launch("to_f64");
+}

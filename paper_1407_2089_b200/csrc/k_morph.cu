@@ -1,0 +1,168 @@
+// k_morph.cu -- K4: threshold + morphological closing.
+//
+// Replaces ref segment.py:204 (mask = rint(v) > t) and segment.py:166-189
+// (ball closing: pad r+1 zeros, binary_dilation, binary_erosion, crop), i.e.
+// closing on the infinite zero domain:
+//   D(q) = OR_{o in ball} M(q+o)   for q within r of the volume (M = 0 outside)
+//   out(p) = AND_{o in ball} D(p+o)
+// r == 1 (the default 6-cross): one fused tile kernel, halo 2 staged in SMEM,
+// D computed for the tile + 1 shell, then the erosion.  r > 1: two passes
+// through an extended (n+2r)^3 byte buffer.
+#include "ct_common.cuh"
+
+namespace {
+
+constexpr int TK = 32, TJ = 8, TI = 4;
+
+__device__ __forceinline__ i64 threshold_of(const int64_t *res, i64 t_host, bool &empty) {
+    empty = false;
+    if (!res) return t_host;
+    if (res[CT_OTSU_STATUS] != 0) empty = true;
+    return res[CT_OTSU_T];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TK *TJ) close1_kernel(const T *__restrict__ in, i64 nx, i64 ny, i64 nz,
+                                                        const int64_t *__restrict__ otsu, i64 t_host,
+                                                        uint8_t *__restrict__ out) {
+    __shared__ uint8_t m[TI + 4][TJ + 4][TK + 4];
+    __shared__ uint8_t d[TI + 2][TJ + 2][TK + 2];
+    bool empty;
+    const i64 t = threshold_of(otsu, t_host, empty);
+    const int tid = threadIdx.y * TK + threadIdx.x, nth = TK * TJ;
+    const i64 tk = (nz + TK - 1) / TK, tj = (ny + TJ - 1) / TJ, ti = (nx + TI - 1) / TI;
+    const i64 ntiles = tk * tj * ti;
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const i64 k0 = (tile % tk) * TK, j0 = ((tile / tk) % tj) * TJ, i0 = (tile / (tk * tj)) * TI;
+        if (empty) {
+            for (int idx = tid; idx < TI * TJ * TK; idx += nth) {
+                const int kk = idx % TK, jj = (idx / TK) % TJ, ii = idx / (TK * TJ);
+                const i64 i = i0 + ii, j = j0 + jj, k = k0 + kk;
+                if (i < nx && j < ny && k < nz) out[(i * ny + j) * nz + k] = 0;
+            }
+            continue;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < (TI + 4) * (TJ + 4) * (TK + 4); idx += nth) {
+            const int kk = idx % (TK + 4), jj = (idx / (TK + 4)) % (TJ + 4), ii = idx / ((TK + 4) * (TJ + 4));
+            const i64 i = i0 + ii - 2, j = j0 + jj - 2, k = k0 + kk - 2;
+            uint8_t v = 0;
+            if (i >= 0 && i < nx && j >= 0 && j < ny && k >= 0 && k < nz) v = ct::above(in[(i * ny + j) * nz + k], t);
+            m[ii][jj][kk] = v;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < (TI + 2) * (TJ + 2) * (TK + 2); idx += nth) {
+            const int c = idx % (TK + 2), b = (idx / (TK + 2)) % (TJ + 2), a = idx / ((TK + 2) * (TJ + 2));
+            const int A = a + 1, Bj = b + 1, Cc = c + 1;
+            d[a][b][c] = m[A][Bj][Cc] | m[A - 1][Bj][Cc] | m[A + 1][Bj][Cc] | m[A][Bj - 1][Cc] | m[A][Bj + 1][Cc] |
+                         m[A][Bj][Cc - 1] | m[A][Bj][Cc + 1];
+        }
+        __syncthreads();
+        const int c = threadIdx.x, b = threadIdx.y;
+        const i64 j = j0 + b, k = k0 + c;
+        if (j < ny && k < nz) {
+#pragma unroll
+            for (int a = 0; a < TI; ++a) {
+                const i64 i = i0 + a;
+                if (i >= nx) break;
+                const int A = a + 1, Bj = b + 1, Cc = c + 1;
+                out[(i * ny + j) * nz + k] = d[A][Bj][Cc] & d[A - 1][Bj][Cc] & d[A + 1][Bj][Cc] & d[A][Bj - 1][Cc] &
+                                             d[A][Bj + 1][Cc] & d[A][Bj][Cc - 1] & d[A][Bj][Cc + 1];
+            }
+        }
+    }
+}
+
+template <typename T>
+__global__ void threshold_kernel(const T *__restrict__ in, i64 n, const int64_t *__restrict__ otsu, i64 t_host,
+                                 uint8_t *__restrict__ out) {
+    bool empty;
+    const i64 t = threshold_of(otsu, t_host, empty);
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x)
+        out[p] = empty ? 0 : ct::above(in[p], t);
+}
+
+// r > 1: dilation into the extended domain, then erosion.
+template <typename T>
+__global__ void dilate_ext(const T *__restrict__ in, i64 nx, i64 ny, i64 nz, int r, const int64_t *__restrict__ otsu,
+                           i64 t_host, uint8_t *__restrict__ ext) {
+    bool empty;
+    const i64 t = threshold_of(otsu, t_host, empty);
+    const i64 ex = nx + 2 * r, ey = ny + 2 * r, ez = nz + 2 * r, n = ex * ey * ez;
+    for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < n; q += (i64)gridDim.x * blockDim.x) {
+        const i64 c = q % ez - r, b = (q / ez) % ey - r, a = q / (ey * ez) - r;
+        uint8_t v = 0;
+        if (!empty) {
+            for (int da = -r; da <= r && !v; ++da)
+                for (int db = -r; db <= r && !v; ++db)
+                    for (int dc = -r; dc <= r && !v; ++dc) {
+                        if (da * da + db * db + dc * dc > r * r) continue;
+                        const i64 i = a + da, j = b + db, k = c + dc;
+                        if (i >= 0 && i < nx && j >= 0 && j < ny && k >= 0 && k < nz)
+                            v = ct::above(in[(i * ny + j) * nz + k], t);
+                    }
+        }
+        ext[q] = v;
+    }
+}
+
+__global__ void erode_ext(const uint8_t *__restrict__ ext, i64 nx, i64 ny, i64 nz, int r, uint8_t *__restrict__ out) {
+    const i64 ey = ny + 2 * r, ez = nz + 2 * r, n = nx * ny * nz;
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x) {
+        const i64 k = p % nz, j = (p / nz) % ny, i = p / (ny * nz);
+        uint8_t v = 1;
+        for (int da = -r; da <= r && v; ++da)
+            for (int db = -r; db <= r && v; ++db)
+                for (int dc = -r; dc <= r && v; ++dc) {
+                    if (da * da + db * db + dc * dc > r * r) continue;
+                    v = ext[((i + r + da) * ey + (j + r + db)) * ez + (k + r + dc)];
+                }
+        out[p] = v;
+    }
+}
+
+template <typename T>
+int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i64 t_host, int r, uint8_t *out,
+                    uint8_t *work, cudaStream_t s) {
+    const i64 n = nx * ny * nz;
+    if (r == 0) {
+        threshold_kernel<T><<<ct::grid_for(n, 256), 256, 0, s>>>(in, n, otsu, t_host, out);
+        return ct::check_launch("threshold");
+    }
+    if (r == 1) {
+        const i64 tiles = ((nz + TK - 1) / TK) * ((ny + TJ - 1) / TJ) * ((nx + TI - 1) / TI);
+        const int grid = (int)min(tiles, (i64)CT_NUM_SMS * 8);
+        close1_kernel<T><<<grid, dim3(TK, TJ), 0, s>>>(in, nx, ny, nz, otsu, t_host, out);
+        return ct::check_launch("close1");
+    }
+    if (!work) {
+        ct::set_error("closing radius %d needs a workspace", r);
+        return CT_ERR_PARAM;
+    }
+    const i64 ne = (nx + 2 * r) * (ny + 2 * r) * (nz + 2 * r);
+    dilate_ext<T><<<ct::grid_for(ne, 256), 256, 0, s>>>(in, nx, ny, nz, r, otsu, t_host, work);
+    if (int st = ct::check_launch("dilate_ext")) return st;
+    erode_ext<<<ct::grid_for(n, 256), 256, 0, s>>>(work, nx, ny, nz, r, out);
+    return ct::check_launch("erode_ext");
+}
+
+}  // namespace
+
+extern "C" int ct_threshold_close(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz,
+                                  const int64_t *otsu_result, int64_t t_host, int radius, uint8_t *mask_out,
+                                  void *work, void *stream) {
+    if (nx <= 0 || ny <= 0 || nz <= 0 || radius < 0) {
+        ct::set_error("bad closing arguments");
+        return CT_ERR_PARAM;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    CT_DISPATCH(dtype, T, {
+        return threshold_close<T>((const T *)in, nx, ny, nz, otsu_result, t_host, radius, mask_out, (uint8_t *)work, s);
+    });
+    return CT_OK;
+}
+
+extern "C" int ct_closing(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, int radius, uint8_t *out, void *work,
+                          void *stream) {
+    return ct_threshold_close(mask, CT_U8, nx, ny, nz, nullptr, 0, radius, out, work, stream);
+}

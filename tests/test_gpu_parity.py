@@ -1,0 +1,267 @@
+"""CUDA path vs the reference (golden fixtures) and the CPU oracle.
+
+Bit-exact: q / histograms / thresholds / masks / canonical labels / voxel
+lists / ids / centroids / volumes and the denoised float64 grid.  EDT within
+1e-9 um (the reference's own contract, ref test_acceptance.py:318-332)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import PIPELINE_CASES, golden
+from paper_1407_2089_b200 import denoise as D
+from paper_1407_2089_b200 import segment as S
+from paper_1407_2089_b200 import synth
+from paper_1407_2089_b200.imaging import VoxelGrid, VoxelSpacing
+from paper_1407_2089_b200.pipeline import FramePipeline
+
+pytestmark = pytest.mark.gpu
+
+ANISO = VoxelSpacing(0.8, 0.8, 1.0)
+UNIT = VoxelSpacing(1.0, 1.0, 1.0)
+
+
+def assert_dets(dets, g, prefix):
+    assert [d.id for d in dets] == list(g[prefix + "ids"])
+    assert [d.voxel_count for d in dets] == list(g[prefix + "counts"])
+    vox = np.concatenate([d.voxels for d in dets]) if dets else np.empty((0, 3))
+    np.testing.assert_array_equal(vox, g[prefix + "voxels"])
+    np.testing.assert_array_equal(np.array([d.centroid_um for d in dets]).reshape(-1, 3), g[prefix + "centroids"])
+    np.testing.assert_array_equal(np.array([d.volume_um3 for d in dets]), g[prefix + "volumes"])
+
+
+def assert_rows(rows, voxels_lin, dims, g, prefix):
+    """Fused-pipeline table vs golden detections."""
+    _, ny, nz = dims
+    assert list(rows["id"]) == list(g[prefix + "ids"])
+    assert list(rows["count"]) == list(g[prefix + "counts"])
+    np.testing.assert_array_equal(rows["centroid_um"].reshape(-1, 3), g[prefix + "centroids"])
+    np.testing.assert_array_equal(rows["volume_um3"], g[prefix + "volumes"])
+    lin = voxels_lin[: int(rows["count"].sum())]
+    vox = np.stack([lin // (ny * nz), (lin // nz) % ny, lin % nz], axis=1)
+    np.testing.assert_array_equal(vox, g[prefix + "voxels"])
+
+
+def spec_of(case, g):
+    kw = {"r_min": 2.0, "r_max": 3.0} if case == "tiny_u8" else {}
+    return synth.SceneSpec(*[int(x) for x in g["dims"]], dtype=str(g["dtype"]), n_cells=int(g["n_cells"]),
+                           seed=int(g["seed"]), **kw)
+
+
+@pytest.mark.parametrize("case", PIPELINE_CASES)
+def test_api_matches_reference_golden(cuda, case):
+    g = golden(f"pipeline_{case}.npz")
+    sigma = float(g["sigma_um"])
+    for t in range(2):
+        raw_c, raw_v = g[f"t{t}_raw_cell"], g[f"t{t}_raw_vessel"]
+        den = D.denoise_cell_channel(VoxelGrid(values=raw_c, spacing=ANISO), D.CellDenoiseParams(sigma))
+        np.testing.assert_array_equal(den.values, g[f"t{t}_denoised"])
+        dets = S.segment_cell_channel(den, S.SegmentationConfig(), frame=t, id_start=100 * t)
+        assert_dets(dets, g, f"t{t}_")
+        st = D.mrf_denoise_state(VoxelGrid(values=raw_v, spacing=ANISO))
+        meta = g[f"t{t}_mrf"]
+        assert (st.sigma_hat, st.delta, st.iteration, float(st.converged)) == tuple(meta)
+        mask, dm = S.segment_vessel_channel(st.current)
+        np.testing.assert_array_equal(mask, g[f"t{t}_vmask"])
+        np.testing.assert_allclose(dm.values, g[f"t{t}_vdist"], rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("case", PIPELINE_CASES)
+def test_fused_pipeline_matches_reference_golden(cuda, case):
+    g = golden(f"pipeline_{case}.npz")
+    spec = spec_of(case, g)
+    pipe = FramePipeline(spec.dims, spec.dtype, ANISO, D.CellDenoiseParams(float(g["sigma_um"])))
+    for t in range(2):
+        raw_c = synth.generate(spec, t, synth.CELL)
+        raw_v = synth.generate(spec, t, synth.VESSEL)
+        # device generator == the frames the reference saw
+        np.testing.assert_array_equal(raw_c.cpu().numpy() if spec.dtype == "u8" else
+                                      raw_c.cpu().view(torch.int16).numpy().view(np.uint16), g[f"t{t}_raw_cell"])
+        res = pipe.cell(raw_c, frame=t, id_start=100 * t)
+        cnt, rows = pipe.finish_cell(res)
+        assert_rows(rows, pipe.voxels.cpu().numpy(), spec.dims, g, f"t{t}_")
+        vres = pipe.vessel(raw_v)
+        mask, dm = pipe.finish_vessel(vres, raw_v)
+        np.testing.assert_array_equal(mask.cpu().numpy(), g[f"t{t}_vmask"])
+        np.testing.assert_allclose(dm.values.cpu().numpy(), g[f"t{t}_vdist"], rtol=0, atol=1e-9)
+
+
+def test_fused_pipeline_vs_oracle_c1(cuda, oracle):
+    """Full BASELINE config-1 frames (256x256x32 u8, 50 cells), both channels."""
+    spec = synth.C1
+    pipe = FramePipeline(spec.dims, spec.dtype, ANISO)
+    for t in (0, 3):
+        raw_c = synth.generate(spec, t, synth.CELL)
+        raw_v = synth.generate(spec, t, synth.VESSEL)
+        host_c = oracle.synth_frame(spec.dims, "u8", spec.frame_seed(t, 0), spec.vmax, balls=spec.balls(t),
+                                    amp_ball=spec.amp_cell)
+        host_v = oracle.synth_frame(spec.dims, "u8", spec.frame_seed(t, 1), spec.vmax, tubes=spec.tubes(),
+                                    amp_tube=spec.amp_tube)
+        np.testing.assert_array_equal(raw_c.cpu().numpy(), host_c)
+        np.testing.assert_array_equal(raw_v.cpu().numpy(), host_v)
+        o = oracle.denoise_cell(host_c, ANISO.as_array(), 10.0)
+        # K1 quantised residual and K2 median, bit-exact
+        res = pipe.cell(raw_c, frame=t, id_start=t * 1000)
+        np.testing.assert_array_equal(pipe.q.cpu().numpy(), np.rint(o["residual"]).astype(np.uint8))
+        np.testing.assert_array_equal(pipe.med.cpu().numpy(), np.rint(o["denoised"]).astype(np.uint8))
+        hist = oracle.histogram(o["denoised"])
+        np.testing.assert_array_equal(pipe.hist.cpu().numpy()[: hist.size], hist)
+        assert int(pipe.otsu[0]) == oracle.otsu(hist)
+        odets = oracle.segment_cell(o["denoised"], ANISO.as_array(), frame=t, id_start=t * 1000, intensity=host_c)
+        cnt, rows = pipe.finish_cell(res)
+        assert len(rows) == len(odets) > 10
+        for r, d in zip(rows, odets):
+            assert r["id"] == d.id and r["count"] == d.voxel_count and r["root"] == d.root
+            np.testing.assert_array_equal(r["centroid_um"], d.centroid_um)
+            np.testing.assert_array_equal(np.concatenate([r["bbox_lo"], r["bbox_hi"]]), d.bbox)
+            assert r["intensity_sum"] == d.intensity_sum
+        # canonical label volume
+        lab = pipe.labels.cpu().numpy()
+        for r, d in zip(rows, odets):
+            assert np.all(lab[tuple(d.voxels.T)] == r["id"] - t * 1000)
+        assert (lab >= 0).sum() == rows["count"].sum()
+        vres = pipe.vessel(raw_v)
+        mask, dm = pipe.finish_vessel(vres, raw_v)
+        st = oracle.mrf(host_v)
+        assert st["iteration"] == 0
+        om, odist, _ = oracle.segment_vessel(st["current"], ANISO.as_array())
+        np.testing.assert_array_equal(mask.cpu().numpy(), om)
+        np.testing.assert_array_equal(dm.values.cpu().numpy(), odist)  # same envelope arithmetic: bit-exact
+
+
+def test_u16_frame_vs_oracle(cuda, oracle):
+    spec = synth.SceneSpec(96, 80, 32, "u16", n_cells=20, seed=11)
+    pipe = FramePipeline(spec.dims, spec.dtype, ANISO)
+    raw = synth.generate(spec, 1, synth.CELL)
+    host = oracle.synth_frame(spec.dims, "u16", spec.frame_seed(1, 0), spec.vmax, balls=spec.balls(1),
+                              amp_ball=spec.amp_cell)
+    np.testing.assert_array_equal(raw.cpu().view(torch.int16).numpy().view(np.uint16), host)
+    o = oracle.denoise_cell(host, ANISO.as_array(), 10.0)
+    res = pipe.cell(raw)
+    cnt, rows = pipe.finish_cell(res)
+    odets = oracle.segment_cell(o["denoised"], ANISO.as_array())
+    assert [int(r["count"]) for r in rows] == [d.voxel_count for d in odets]
+    for r, d in zip(rows, odets):
+        np.testing.assert_array_equal(r["centroid_um"], d.centroid_um)
+
+
+def test_otsu_golden(cuda):
+    g = golden("otsu.npz")
+    for h, (nb, t) in zip(g["hists"], g["meta"]):
+        assert S.otsu_threshold(h[:nb]) == t
+    for h, t in zip(list(g["big"]) + [g["wrap"]], g["big_t"]):
+        assert S.otsu_threshold(h) == t
+
+
+def test_masks_golden(cuda):
+    g = golden("masks.npz")
+    for i in range(6):
+        m = g[f"m{i}"]
+        np.testing.assert_array_equal(S.morphological_closing(m, 1), g[f"close1_{i}"])
+        np.testing.assert_array_equal(S.morphological_closing(m, 2), g[f"close2_{i}"])
+        assert_dets(S.detections_from_mask(m, ANISO, frame=1, min_volume_um3=1.5, id_start=7), g, f"d{i}_")
+        if m.any():
+            np.testing.assert_allclose(S.distance_map(m, ANISO).values, g[f"edt{i}"], rtol=0, atol=1e-9)
+
+
+def test_mrf_golden(cuda):
+    g = golden("mrf.npz")
+    for seed in range(4):
+        st = D.mrf_denoise_state(VoxelGrid(values=g[f"v{seed}"], spacing=UNIT))
+        assert (st.sigma_hat, st.delta, st.iteration, float(st.converged)) == tuple(g[f"meta{seed}"])
+        np.testing.assert_array_equal(st.current.values, g[f"cur{seed}"])
+    v = g["noise_v"]
+    assert D.estimate_noise_variance(VoxelGrid(values=v, spacing=UNIT)) == g["noise_sigma"][0]
+    assert D.intensity_step(v) == g["noise_step"][0]
+    np.testing.assert_array_equal(D._neighbor_sign_sum(v), g["noise_sign"])
+
+
+def test_random_masks_vs_oracle(cuda, oracle):
+    rng = np.random.default_rng(2024)
+    for _ in range(6):
+        shape = tuple(int(x) for x in rng.integers(5, 40, 3))
+        m = rng.random(shape) > rng.uniform(0.5, 0.95)
+        np.testing.assert_array_equal(S.morphological_closing(m, 1), oracle.closing(m, 1))
+        np.testing.assert_array_equal(S.morphological_closing(m, 3), oracle.closing(m, 3))
+        d_gpu = S.detections_from_mask(m, ANISO, frame=0, min_volume_um3=0.0)
+        d_ora = oracle.detections(m, ANISO.as_array(), min_volume_um3=0.0)
+        assert len(d_gpu) == len(d_ora)
+        for a, b in zip(d_gpu, d_ora):
+            assert a.id == b.id
+            np.testing.assert_array_equal(a.voxels, b.voxels)
+            np.testing.assert_array_equal(a.centroid_um, b.centroid_um)
+        if m.any():
+            np.testing.assert_array_equal(S.distance_map(m, ANISO).values, oracle.edt(m, ANISO.as_array()))
+
+
+def test_median_radii_and_dtypes_vs_oracle(cuda, oracle):
+    rng = np.random.default_rng(8)
+    for rad in (1, 2, 3):
+        for dt in (np.uint8, np.uint16, np.float64):
+            shape = (13, 11, 37)
+            v = (rng.integers(0, 300, size=shape)).astype(dt) if dt != np.uint8 else rng.integers(0, 256, shape).astype(dt)
+            t = torch.from_numpy(v if dt != np.uint16 else v.view(np.int16)).cuda()
+            if dt == np.uint16:
+                t = t.view(torch.uint16)
+            out = torch.empty_like(t)
+            hist = torch.zeros(65536, dtype=torch.int64, device=t.device)
+            from paper_1407_2089_b200._lib import call
+            from paper_1407_2089_b200 import _dev
+            call("ct_median", t.data_ptr(), _dev.ct_code(t), *shape, rad, out.data_ptr(), hist.data_ptr(),
+                 _dev.stream_handle())
+            ref = oracle.median(v.astype(np.float64), rad)
+            got = out.cpu()
+            got = got.view(torch.int16).numpy().view(np.uint16) if dt == np.uint16 else got.numpy()
+            np.testing.assert_array_equal(got.astype(np.float64), ref)
+            if dt != np.float64:
+                np.testing.assert_array_equal(hist.cpu().numpy()[:65536], np.bincount(ref.astype(np.int64).ravel(),
+                                                                                      minlength=65536))
+
+
+def test_gaussian_sigma_sweep_vs_oracle(cuda, oracle):
+    """C5-style sigma sweep incl. radius > extent and skipped clamping paths."""
+    rng = np.random.default_rng(3)
+    for sig, shape in [(1.0, (40, 30, 20)), (2.0, (33, 17, 9)), (3.0, (20, 64, 40)), (4.0, (70, 20, 12))]:
+        v = rng.integers(0, 256, size=shape).astype(np.uint8)
+        g = D.denoise_cell_channel(VoxelGrid(values=v, spacing=UNIT), D.CellDenoiseParams(sig))
+        o = oracle.denoise_cell(v, (1.0, 1.0, 1.0), sig)
+        np.testing.assert_array_equal(g.values, o["denoised"])
+
+
+def test_large_frame_properties(cuda):
+    """BASELINE config-2 size (1024x1024x64 u8): size-independent invariants."""
+    spec = synth.C2
+    pipe = FramePipeline(spec.dims, spec.dtype, ANISO)
+    raw = synth.generate(spec, 5, synth.CELL)
+    res = pipe.cell(raw, frame=5, id_start=123)
+    cnt, rows = pipe.finish_cell(res)
+    labels1 = pipe.labels.clone()
+    nk = len(rows)
+    assert nk > 1000
+    assert list(rows["id"]) == list(range(123, 123 + nk))
+    key = list(zip(-rows["count"], rows["root"]))
+    assert key == sorted(key)
+    assert np.all(rows["volume_um3"] >= 19.0)
+    lab = pipe.labels
+    counts = torch.bincount(lab[lab >= 0].to(torch.int64), minlength=nk).cpu().numpy()
+    np.testing.assert_array_equal(counts, rows["count"])
+    vox = pipe.voxels[: int(rows["count"].sum())].cpu().numpy().astype(np.int64)
+    # voxel lists: ascending within each cell, first voxel == root, label == rank
+    for r in rows[:: max(1, nk // 50)]:
+        seg = vox[r["voxel_offset"] : r["voxel_offset"] + r["count"]]
+        assert seg[0] == r["root"] and np.all(np.diff(seg) > 0)
+        assert torch.all(lab.view(-1)[torch.from_numpy(seg).cuda()] == r["id"] - 123)
+        ny, nz = spec.ny, spec.nz
+        pts = np.stack([seg // (ny * nz), (seg // nz) % ny, seg % nz], axis=1).astype(np.float64) * ANISO.as_array()
+        np.testing.assert_array_equal(pts.mean(axis=0), r["centroid_um"])  # numpy's own mean
+    # determinism: rerun gives identical labels and table
+    res2 = pipe.cell(raw, frame=5, id_start=123)
+    cnt2, rows2 = pipe.finish_cell(res2)
+    assert torch.equal(labels1, pipe.labels)
+    assert rows2.tobytes() == rows.tobytes()
+    # vessel channel at full size
+    rawv = synth.generate(spec, 5, synth.VESSEL)
+    vres = pipe_v = FramePipeline(spec.dims, spec.dtype, ANISO, cell=False).vessel(rawv)
+    assert int(vres.state[5]) == 0
+    assert torch.all(vres.distance[vres.mask.bool()] == 0)
+    assert torch.all(vres.distance[~vres.mask.bool()] > 0)
