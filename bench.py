@@ -246,6 +246,16 @@ def run_ours(args):
     total_vox = world * args.steps * 2 * nvox
     value = total_vox / (ms_max / 1e3)
 
+    # --- serialized pass (one stream) for clean per-kernel times ----------
+    pipe.marks = []
+    for i in range(min(3, args.steps)):
+        t, rc, rv = inputs[i % ring]
+        pipe.cell(rc, frame=t)
+        pipe.vessel(rv)
+    torch.cuda.synchronize()
+    serial_ms = pipe.stage_times_ms()
+    pipe.marks = None
+
     # --- e2e through the public pipeline API with pinned host buffers -------
     e2e = None
     if not args.no_e2e:
@@ -274,14 +284,18 @@ def run_ours(args):
             "fp64_ops_per_voxel": fp64_ops,
             "share_of_cell_stream": k1_ms / sum(v for k, v in stage_ms.items() if k.startswith(("K1", "K2", "K3 o", "K4", "K5", "K6"))),
         }
-    kernels = {}
+    kernels, kernels_serial = {}, {}
     bpv = {"K2 median+hist": 2, "K4 threshold+close": 2, "K5 ccl": 5, "K6 table": 0, "K7 mrf": 3,
            "K3+K4 vessel otsu+close": 2, "K8 edt": 9, "K1 gaussian": 2}
-    for k, v in stage_ms.items():
-        b = bpv.get(k)
-        kernels[k] = {"ms": v, "hbm_gbs": (b * nvox / (v / 1e3) / 1e9) if b else None,
+    for src, dst in ((stage_ms, kernels), (serial_ms, kernels_serial)):
+        for k, v in src.items():
+            b = bpv.get(k)
+            dst[k] = {"ms": v, "hbm_gbs": (b * nvox / (v / 1e3) / 1e9) if b else None,
                       "hbm_frac": (b * nvox / (v / 1e3) / 1e9 / pk["hbm_gbs"]) if b else None,
                       "algorithmic_bytes_per_voxel": b}
+    if roof is not None and serial_ms.get("K1 gaussian"):
+        roof["serial_ms"] = serial_ms["K1 gaussian"]
+        roof["serial_frac"] = fp64_ops * nvox / (serial_ms["K1 gaussian"] / 1e3) / 1e12 / fp64_peak
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -301,7 +315,7 @@ def run_ours(args):
                        "frames_per_s": world * args.steps / (ms_max / 1e3),
                        "l2": f"inputs larger than L2: {2 * nvox / 1e6:.0f} MB/step from a ring of {ring} "
                              "distinct time points, plus GB-scale intermediates"},
-            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof, "kernels": kernels,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof, "kernels": kernels, "kernels_serial": kernels_serial,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -64,3 +64,59 @@ __device__ __forceinline__ bool above(double v, i64 t) { return rint(v) > (doubl
             ct::set_error("unsupported dtype code %d", (int)(dtype)); \
             return CT_ERR_UNSUPPORTED;                               \
     }
+
+namespace ct {
+
+__device__ __forceinline__ unsigned laneid() {
+    unsigned l;
+    asm("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+}
+
+// Conflict-free 256-bin histogram for 256-thread CTAs: every thread owns a
+// private 8-bit counter per bin (no atomics).  Counter (bin, thread) lives in
+// byte (warp % 4) of word [(warp / 4) * 256 + bin] * 32 + lane, so a warp's
+// 32 increments always hit 32 distinct banks whatever the values.  Each
+// thread may add at most 255 values between flush() calls; flush() folds the
+// bytes into per-CTA 32-bit totals with one DP4A per word.
+// SMEM: 64 KB of counters + 1 KB totals.
+struct ByteHist256 {
+    uint32_t *words;  // [2][256][32]
+    uint32_t *tot;    // [256]
+    static constexpr size_t kBytes = 2 * 256 * 32 * 4 + 256 * 4;
+
+    __device__ void init(void *smem) {
+        words = (uint32_t *)smem;
+        tot = words + 2 * 256 * 32;
+        for (int i = threadIdx.x; i < 2 * 256 * 32; i += blockDim.x) words[i] = 0;
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) tot[i] = 0;
+    }
+    __device__ __forceinline__ void add(int v) {
+        const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        uint8_t *p = (uint8_t *)(words + ((w >> 2) * 256 + v) * 32 + lane) + (w & 3);
+        *p = (uint8_t)(*p + 1);
+    }
+    // all threads; blockDim.x == 256
+    __device__ void flush() {
+        __syncthreads();
+        const int b = threadIdx.x;
+        unsigned s = tot[b];
+        for (int g = 0; g < 2; ++g) {
+            uint32_t *row = words + (g * 256 + b) * 32;
+#pragma unroll 8
+            for (int l = 0; l < 32; ++l) {
+                const int c = (l + b) & 31;  // rotate: lanes hit distinct banks
+                s = __dp4a(row[c], 0x01010101u, s);
+                row[c] = 0;
+            }
+        }
+        tot[b] = s;
+        __syncthreads();
+    }
+    __device__ void to_global(unsigned long long *g) {
+        const int b = threadIdx.x;
+        if (tot[b]) atomicAdd(g + b, (unsigned long long)tot[b]);
+    }
+};
+
+}  // namespace ct

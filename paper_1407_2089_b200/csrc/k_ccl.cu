@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64
         r.centroid_um[0] = r.centroid_um[1] = r.centroid_um[2] = 0.0;
         r.volume_um3 = __dmul_rn((double)r.count, vv);
         r.voxel_offset = (int64_t)voff;
-        r.reserved = c;
+        r.reserved = 0;
         table[e] = r;
         voff += w.count[c];
     }

@@ -1,20 +1,26 @@
 // k_mrf.cu -- K7: vessel-channel MRF denoise (ref denoise.py:92-195).
 //
-//   delta     = intensity_step: min gap of the distinct values (denoise.py:135-144)
-//               integer input: from the histogram's non-empty bins;
-//               float input: radix-sorted copy (CUB), min positive neighbour gap
+//   delta     = intensity_step (denoise.py:135-144): min gap of the distinct
+//               values.  Integer input: from the histogram's non-empty bins;
+//               float input: radix-sorted copy (CUB), min positive gap.
 //   sigma_hat = estimate_noise_variance (denoise.py:92-114) = np.std(lap)/sqrt(42)
 //               over the interior 6-neighbour Laplacian.  np.std reduces with
 //               numpy's pairwise summation (8-way unrolled leaves of <= 128,
-//               halving splits rounded to multiples of 8); that tree is
-//               reproduced exactly: CTA b sums the depth-D node b of the tree
-//               (all depth-D nodes exist because D is chosen from the smallest
-//               path), with the leaves below it enumerated and recombined in
-//               recursion order, and one CTA folds the 2^D partials pairwise.
-//   first step: proposal = I0 + delta*sign(S), S = edge-replicated sign sum
-//               (denoise.py:117-132); stop when ||proposal - I0|| > sigma_hat
-//               (denoise.py:173) or no voxel moves (denoise.py:175).  On
-//               realistic volumes this stops at iteration 0; further iterations
+//               halving splits rounded to multiples of 8).
+//               * integer input: every Laplacian and every partial sum is an
+//                 integer below 2^53, so the mean's sum is order-independent and
+//                 is taken as an exact int64 reduction in the fused statistics
+//                 pass; only sum((lap - mean)^2) needs numpy's tree.
+//               * the tree: CTA b owns depth-D node b (D from the smallest path,
+//                 so every depth-D node exists), stages its elements in SMEM
+//                 with coalesced loads, sums its <= 128-element leaves (one
+//                 thread each) and recombines them in recursion order; one CTA
+//                 folds the 2^D partials pairwise.
+//   first step (denoise.py:172-176): proposal = I0 + delta*sign(S), S the
+//               edge-replicated sign sum (denoise.py:117-132).  For integer
+//               input ||proposal - I0||^2 = delta^2 * #{S != 0} exactly, so the
+//               statistics pass only counts non-zero sign sums.  On realistic
+//               volumes the step is rejected (decision 0); further iterations
 //               run through ct_mrf_step driven by the host.
 #include <cub/device/device_radix_sort.cuh>
 
@@ -42,6 +48,31 @@ inline int pw_depth(i64 n) {
     return d;
 }
 
+// largest node size at depth D (sizes per level form a tiny set)
+inline i64 pw_max_node(i64 n, int D) {
+    i64 sizes[64];
+    int ns = 1;
+    sizes[0] = n;
+    for (int d = 0; d < D; ++d) {
+        i64 nxt[64];
+        int nn = 0;
+        for (int i = 0; i < ns; ++i) {
+            const i64 l = pw_left(sizes[i]), r = sizes[i] - l;
+            const i64 c[2] = {l, r};
+            for (int q = 0; q < 2; ++q) {
+                bool seen = false;
+                for (int u = 0; u < nn; ++u) seen |= nxt[u] == c[q];
+                if (!seen && nn < 64) nxt[nn++] = c[q];
+            }
+        }
+        ns = nn;
+        for (int i = 0; i < ns; ++i) sizes[i] = nxt[i];
+    }
+    i64 m = 0;
+    for (int i = 0; i < ns; ++i) m = sizes[i] > m ? sizes[i] : m;
+    return m;
+}
+
 // node at depth D with path bits `idx` (MSB first = first split)
 __device__ void pw_node(i64 n, int D, i64 idx, i64 &off, i64 &len) {
     off = 0;
@@ -53,31 +84,42 @@ __device__ void pw_node(i64 n, int D, i64 idx, i64 &off, i64 &len) {
     }
 }
 
-// element functors over the flattened C-order interior (nx-2, ny-2, nz-2)
+__device__ __forceinline__ int sgn(double x) { return (x > 0.0) - (x < 0.0); }
+
+// Laplacian element e of the flattened C-order interior (nx-2, ny-2, nz-2);
+// interior sizes fit 32 bits (volumes are < 2^31 voxels).
 template <typename T>
-struct LapElem {
+__device__ __forceinline__ double lap_at(const T *v, uint32_t e, uint32_t my, uint32_t mz, i64 ny, i64 nz) {
+    const uint32_t row = e / mz, c = e - row * mz;
+    const uint32_t a = row / my, b = row - a * my;
+    const i64 s0 = ny * nz;
+    const i64 p = (i64)(a + 1) * s0 + (i64)(b + 1) * nz + (c + 1);
+    double l = __dadd_rn(ct::to_f64(v[p - s0]), ct::to_f64(v[p + s0]));
+    l = __dadd_rn(l, ct::to_f64(v[p - nz]));
+    l = __dadd_rn(l, ct::to_f64(v[p + nz]));
+    l = __dadd_rn(l, ct::to_f64(v[p - 1]));
+    l = __dadd_rn(l, ct::to_f64(v[p + 1]));
+    return __dadd_rn(l, -__dmul_rn(6.0, ct::to_f64(v[p])));
+}
+
+// element functors
+template <typename T>
+struct LapElem {  // lap (squared == 0) or (lap - mean)^2
     const T *v;
-    i64 ny, nz, my, mz;
-    const double *mean;  // device pointer (squared == 1)
-    int squared;         // 0: lap, 1: (lap-mean)^2
+    i64 ny, nz;
+    uint32_t my, mz;
+    const double *mean;            // device, when squared == 1 and !int_sum
+    const long long *int_sum;      // device exact sum of lap (integer input), mean = sum / n
+    i64 n_interior;
+    int squared;
     __device__ double operator()(i64 e) const {
-        const i64 c = e % mz, b = (e / mz) % my, a = e / (mz * my);
-        const i64 i = a + 1, j = b + 1, k = c + 1;
-        const i64 s0 = ny * nz;
-        const i64 p = i * s0 + j * nz + k;
-        double l = __dadd_rn(ct::to_f64(v[p - s0]), ct::to_f64(v[p + s0]));
-        l = __dadd_rn(l, ct::to_f64(v[p - nz]));
-        l = __dadd_rn(l, ct::to_f64(v[p + nz]));
-        l = __dadd_rn(l, ct::to_f64(v[p - 1]));
-        l = __dadd_rn(l, ct::to_f64(v[p + 1]));
-        l = __dadd_rn(l, -__dmul_rn(6.0, ct::to_f64(v[p])));
+        const double l = lap_at(v, (uint32_t)e, my, mz, ny, nz);
         if (!squared) return l;
-        const double x = __dadd_rn(l, -*mean);
+        const double m = int_sum ? __ddiv_rn((double)*int_sum, (double)n_interior) : *mean;
+        const double x = __dadd_rn(l, -m);
         return __dmul_rn(x, x);
     }
 };
-
-__device__ __forceinline__ int sgn(double x) { return (x > 0.0) - (x < 0.0); }
 
 template <typename T>
 __device__ __forceinline__ int sign_sum_at(const T *v, const double *cur, i64 nx, i64 ny, i64 nz, i64 p) {
@@ -92,13 +134,12 @@ __device__ __forceinline__ int sign_sum_at(const T *v, const double *cur, i64 nx
     return s;
 }
 
-// (proposal - original)^2 for the step from `cur` (nullptr = original)
 template <typename T>
-struct StepElem {
+struct StepElem {  // (proposal - original)^2 for the step from `cur` (nullptr = original)
     const T *v;
     const double *cur;
     i64 nx, ny, nz;
-    const double *delta;  // device pointer
+    const double *delta;
     __device__ double operator()(i64 p) const {
         const double c = cur ? cur[p] : ct::to_f64(v[p]);
         const int s = sgn((double)sign_sum_at(v, cur, nx, ny, nz, p));
@@ -108,45 +149,46 @@ struct StepElem {
     }
 };
 
-// numpy pairwise_sum leaf (n <= 128)
-template <class F>
-__device__ double pw_leaf(const F &f, i64 off, i64 n) {
+// numpy pairwise_sum leaf (n <= 128) over an SMEM array
+__device__ double pw_leaf(const double *a, int n) {
     if (n < 8) {
         double res = 0.0;
-        for (i64 i = 0; i < n; ++i) res = __dadd_rn(res, f(off + i));
+        for (int i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
         return res;
     }
     double r[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = f(off + j);
-    i64 i;
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i;
     for (i = 8; i < n - (n % 8); i += 8)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(off + i + j));
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
     double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, f(off + i));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
     return res;
 }
 
-// CTA b: exact numpy-order sum of depth-D node b.
+// CTA b: exact numpy-order sum of depth-D node b; elements staged in SMEM.
 template <class F>
 __global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__restrict__ partial) {
-    __shared__ i64 loff[MAX_LEAVES], llen[MAX_LEAVES];
+    extern __shared__ double vals[];
+    __shared__ int loff[MAX_LEAVES], llen[MAX_LEAVES];
     __shared__ double lsum[MAX_LEAVES];
     __shared__ int nleaves;
     i64 off, len;
     pw_node(n, D, blockIdx.x, off, len);
+    for (int i = threadIdx.x; i < len; i += PT) vals[i] = f(off + i);
     if (threadIdx.x == 0) {
         // enumerate leaves in order (explicit DFS stack, right child pushed first)
         i64 so[64], sl[64];
         int sp = 0, nl = 0;
-        so[sp] = off; sl[sp] = len; ++sp;
+        so[sp] = 0; sl[sp] = len; ++sp;
         while (sp) {
             --sp;
             const i64 o = so[sp], l = sl[sp];
             if (l <= 128) {
-                loff[nl] = o; llen[nl] = l; ++nl;
+                loff[nl] = (int)o; llen[nl] = (int)l; ++nl;
             } else {
                 const i64 h = pw_left(l);
                 so[sp] = o + h; sl[sp] = l - h; ++sp;
@@ -156,29 +198,27 @@ __global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__re
         nleaves = nl;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < nleaves; e += PT) lsum[e] = pw_leaf(f, loff[e], llen[e]);
+    for (int e = threadIdx.x; e < nleaves; e += PT) lsum[e] = pw_leaf(vals + loff[e], llen[e]);
     __syncthreads();
     if (threadIdx.x == 0) {
         // recombine in recursion order: post-order evaluation with a value stack
-        i64 so[64], sl[64];
+        i64 sl[64];
         int st[64];
         double vs[64];
         int sp = 0, vp = 0, leaf = 0;
-        so[sp] = off; sl[sp] = len; st[sp] = 0; ++sp;
+        sl[sp] = len; st[sp] = 0; ++sp;
         while (sp) {
             const int top = sp - 1;
-            const i64 o = so[top], l = sl[top];
+            const i64 l = sl[top];
             if (l <= 128) {
                 vs[vp++] = lsum[leaf++];
                 --sp;
             } else if (st[top] == 0) {
                 st[top] = 1;
-                const i64 h = pw_left(l);
-                so[sp] = o; sl[sp] = h; st[sp] = 0; ++sp;
+                sl[sp] = pw_left(l); st[sp] = 0; ++sp;
             } else if (st[top] == 1) {
                 st[top] = 2;
-                const i64 h = pw_left(l);
-                so[sp] = o + h; sl[sp] = l - h; st[sp] = 0; ++sp;
+                sl[sp] = l - pw_left(l); st[sp] = 0; ++sp;
             } else {
                 const double b = vs[--vp], a = vs[--vp];
                 vs[vp++] = __dadd_rn(a, b);
@@ -209,7 +249,13 @@ int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s
         return ct::check_launch("pairwise empty");
     }
     const int D = pw_depth(n);
-    pw_subtree<F><<<(unsigned)(1ll << D), PT, 0, s>>>(f, n, D, partial);
+    const size_t sm = (size_t)pw_max_node(n, D) * sizeof(double);
+    if (sm > 200 * 1024) {
+        ct::set_error("pairwise subtree too large");
+        return CT_ERR_UNSUPPORTED;
+    }
+    cudaFuncSetAttribute(pw_subtree<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    pw_subtree<F><<<(unsigned)(1ll << D), PT, sm, s>>>(f, n, D, partial);
     if (int st = ct::check_launch("pw_subtree")) return st;
     pw_fold<<<1, 1024, 0, s>>>(partial, D, out);
     return ct::check_launch("pw_fold");
@@ -217,38 +263,104 @@ int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s
 
 // state words
 enum { S_DELTA = 0, S_SIGMA, S_SIGMA_STATUS, S_NNZ, S_NORM, S_DECISION, S_SUM1, S_SUM2, S_SUM3, S_WORDS };
+// scalar words (u64) in the workspace
+enum { W_NNZ = 0, W_BEST_BITS, W_MOVED, W_LAPSUM, W_WORDS = 8 };
+
+// ---------------------------------------------------------------------------
+// Fused statistics pass over an integer volume (one read of the input):
+// histogram, #{sign sum != 0}, exact int64 sum of the interior Laplacian.
+// Tiles of (TI x TJ x TK) voxels with a clamped halo staged in SMEM.
+// ---------------------------------------------------------------------------
+constexpr int STI = 4, STJ = 8, STK = 32;
 
 template <typename T>
-__global__ void mrf_stats(const T *__restrict__ v, i64 nx, i64 ny, i64 nz, uint64_t *__restrict__ hist,
-                          unsigned long long *__restrict__ nnz) {
-    __shared__ uint32_t sh[4096];
-    __shared__ unsigned long long snz;
-    for (int b = threadIdx.x; b < 4096; b += blockDim.x) sh[b] = 0;
-    if (threadIdx.x == 0) snz = 0;
-    __syncthreads();
-    const i64 n = nx * ny * nz;
-    unsigned long long local = 0;
-    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x) {
-        local += sign_sum_at<T>(v, nullptr, nx, ny, nz, p) != 0;
-        if (hist) {
-            const int b = ct::hist_bin(v[p]);
-            if (b < 4096) atomicAdd(&sh[b], 1u);
-            else atomicAdd((unsigned long long *)&hist[b], 1ull);
+__global__ void __launch_bounds__(256) mrf_stats_int(const T *__restrict__ v, i64 nx, i64 ny, i64 nz,
+                                                     unsigned long long *__restrict__ ghist,
+                                                     unsigned long long *__restrict__ scal) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    int *tile = (int *)dsm;  // [STI+2][STJ+2][STK+2]
+    constexpr bool BYTE = sizeof(T) == 1;
+    ct::ByteHist256 bh;
+    uint32_t *sh16 = nullptr;  // u16: [4096] SMEM bins
+    unsigned char *hbase = dsm + (STI + 2) * (STJ + 2) * (STK + 2) * sizeof(int);
+    if (BYTE) bh.init(hbase);
+    else {
+        sh16 = (uint32_t *)hbase;
+        for (int b = threadIdx.x; b < 4096; b += 256) sh16[b] = 0;
+    }
+    const int tk = threadIdx.x & 31, tj = threadIdx.x >> 5;
+    const i64 ntk = (nz + STK - 1) / STK, ntj = (ny + STJ - 1) / STJ, nti = (nx + STI - 1) / STI;
+    const i64 ntiles = ntk * ntj * nti;
+    unsigned long long nnz = 0;
+    long long lsum = 0;
+    int since_flush = 0;
+    for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const i64 k0 = (t % ntk) * STK, j0 = ((t / ntk) % ntj) * STJ, i0 = (t / (ntk * ntj)) * STI;
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < (STI + 2) * (STJ + 2) * (STK + 2); idx += 256) {
+            const int kk = idx % (STK + 2), jj = (idx / (STK + 2)) % (STJ + 2), ii = idx / ((STK + 2) * (STJ + 2));
+            const i64 i = ct::clampi(i0 + ii - 1, 0, nx - 1), j = ct::clampi(j0 + jj - 1, 0, ny - 1),
+                      k = ct::clampi(k0 + kk - 1, 0, nz - 1);
+            tile[idx] = (int)v[(i * ny + j) * nz + k];
+        }
+        __syncthreads();
+        const i64 j = j0 + tj, k = k0 + tk;
+#pragma unroll
+        for (int a = 0; a < STI; ++a) {
+            const i64 i = i0 + a;
+            if (i >= nx || j >= ny || k >= nz) continue;
+#define TL(da, db, dc) tile[((a + 1 + (da)) * (STJ + 2) + (tj + 1 + (db))) * (STK + 2) + (tk + 1 + (dc))]
+            const int c = TL(0, 0, 0);
+            const int xm = TL(-1, 0, 0), xp = TL(1, 0, 0), ym = TL(0, -1, 0), yp = TL(0, 1, 0), zm = TL(0, 0, -1),
+                      zp = TL(0, 0, 1);
+#undef TL
+            const int s = ((xm > c) - (xm < c)) + ((c > xp) - (c < xp)) + ((ym > c) - (ym < c)) +
+                          ((c > yp) - (c < yp)) + ((zm > c) - (zm < c)) + ((c > zp) - (c < zp));
+            nnz += s != 0;
+            if (i > 0 && i < nx - 1 && j > 0 && j < ny - 1 && k > 0 && k < nz - 1)
+                lsum += (long long)(xm + xp + ym + yp + zm + zp) - 6ll * c;
+            if (BYTE) bh.add(c);
+            else if (c < 4096) atomicAdd(&sh16[c], 1u);
+            else atomicAdd(&ghist[c], 1ull);
+        }
+        if (BYTE && ++since_flush == 60) {  // <= 240 adds per thread between flushes
+            bh.flush();
+            since_flush = 0;
         }
     }
+    for (int o = 16; o; o >>= 1) {
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&scal[W_NNZ], nnz);
+        atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
+    }
+    if (BYTE) {
+        bh.flush();
+        bh.to_global(ghist);
+    } else {
+        __syncthreads();
+        for (int b = threadIdx.x; b < 4096; b += 256)
+            if (sh16[b]) atomicAdd(&ghist[b], (unsigned long long)sh16[b]);
+    }
+}
+
+// float input: #{sign sum != 0} only (delta via sort; sums via the tree)
+template <typename T>
+__global__ void mrf_nnz_generic(const T *__restrict__ v, i64 nx, i64 ny, i64 nz, unsigned long long *__restrict__ nnz) {
+    const i64 n = nx * ny * nz;
+    unsigned long long local = 0;
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x)
+        local += sign_sum_at<T>(v, nullptr, nx, ny, nz, p) != 0;
     for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(&snz, local);
-    __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(nnz, snz);
-    if (hist)
-        for (int b = threadIdx.x; b < 4096; b += blockDim.x)
-            if (sh[b]) atomicAdd((unsigned long long *)&hist[b], (unsigned long long)sh[b]);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(nnz, local);
 }
 
 // delta from the histogram of integer values (min gap of non-empty bins)
 __global__ void delta_from_hist(const uint64_t *__restrict__ hist, double *state) {
     __shared__ int prev_of[1024];
-    // each thread: first and last non-empty bin in its 64-bin chunk and its internal min gap
+    __shared__ int wg[32];
     const int t = threadIdx.x;
     int first = -1, last = -1, gap = INT32_MAX;
     for (int b = t * 64; b < t * 64 + 64; ++b) {
@@ -259,13 +371,11 @@ __global__ void delta_from_hist(const uint64_t *__restrict__ hist, double *state
     }
     prev_of[t] = last;
     __syncthreads();
-    // gap to the previous non-empty chunk's last bin
     if (first >= 0) {
         for (int u = t - 1; u >= 0; --u)
             if (prev_of[u] >= 0) { gap = min(gap, first - prev_of[u]); break; }
     }
     for (int o = 16; o; o >>= 1) gap = min(gap, __shfl_xor_sync(0xffffffffu, gap, o));
-    __shared__ int wg[32];
     if ((t & 31) == 0) wg[t >> 5] = gap;
     __syncthreads();
     if (t == 0) {
@@ -292,26 +402,31 @@ __global__ void delta_store(const unsigned long long *best_bits, double *state) 
     state[S_DELTA] = *best_bits == ~0ull ? 0.0 : __longlong_as_double((long long)*best_bits);
 }
 
-__global__ void mrf_decide(double *state, i64 n_interior, const unsigned long long *nnz) {
-    const double n = (double)n_interior;
+__global__ void mean_from_sum(double *state, i64 n) { state[S_SUM1] = __ddiv_rn(state[S_SUM1], (double)n); }
+
+// int_path: norm^2 = delta^2 * nnz (exact); else state[S_SUM3] holds the tree sum
+__global__ void mrf_decide(double *state, i64 n_interior, const unsigned long long *scal, int int_path) {
     if (n_interior < 2) {
         state[S_SIGMA] = 0.0;
         state[S_SIGMA_STATUS] = 1.0;
     } else {
-        const double var = __ddiv_rn(state[S_SUM2], n);
+        const double var = __ddiv_rn(state[S_SUM2], (double)n_interior);
         state[S_SIGMA] = __ddiv_rn(__dsqrt_rn(var), __dsqrt_rn(42.0));
         state[S_SIGMA_STATUS] = 0.0;
     }
-    state[S_NNZ] = (double)*nnz;
+    const unsigned long long nnz = scal[W_NNZ];
+    state[S_NNZ] = (double)nnz;
+    if (int_path) {
+        state[S_SUM1] = n_interior > 0 ? __ddiv_rn((double)(long long)scal[W_LAPSUM], (double)n_interior) : 0.0;
+        state[S_SUM3] = __dmul_rn(__dmul_rn(state[S_DELTA], state[S_DELTA]), (double)nnz);
+    }
     const double norm = __dsqrt_rn(state[S_SUM3]);
     state[S_NORM] = norm;
-    if (state[S_DELTA] == 0.0) state[S_DECISION] = 2.0;             // constant: input returned as is
-    else if (norm > state[S_SIGMA]) state[S_DECISION] = 0.0;        // stop before the first step
-    else if (*nnz == 0) state[S_DECISION] = 0.0;                    // fixed point
-    else state[S_DECISION] = 1.0;                                   // iterate (host loop)
+    if (state[S_DELTA] == 0.0) state[S_DECISION] = 2.0;       // constant: input returned as is
+    else if (norm > state[S_SIGMA]) state[S_DECISION] = 0.0;  // stop before the first step
+    else if (nnz == 0) state[S_DECISION] = 0.0;               // fixed point
+    else state[S_DECISION] = 1.0;                             // iterate (host loop)
 }
-
-__global__ void mean_from_sum(double *state, i64 n) { state[S_SUM1] = __ddiv_rn(state[S_SUM1], (double)n); }
 
 template <typename T>
 __global__ void mrf_apply(const T *__restrict__ v, const double *__restrict__ cur, i64 nx, i64 ny, i64 nz,
@@ -331,10 +446,22 @@ __global__ void mrf_apply(const T *__restrict__ v, const double *__restrict__ cu
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(moved, local);
 }
 
+template <typename T>
+__global__ void sign_sum_kernel(const T *__restrict__ v, i64 nx, i64 ny, i64 nz, int64_t *__restrict__ out) {
+    const i64 n = nx * ny * nz;
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x)
+        out[p] = sign_sum_at<T>(v, nullptr, nx, ny, nz, p);
+}
+
+__global__ void step_finish(double *out2, const unsigned long long *moved) {
+    out2[0] = __dsqrt_rn(out2[0]);
+    out2[1] = (double)*moved;
+}
+
 struct MrfWork {
-    double *partial;              // 2^D
-    unsigned long long *scal;     // [4]: nnz, best_bits, moved, pad
-    double *sorted;               // float path: n
+    double *partial;           // 2 * 2^D
+    unsigned long long *scal;  // W_WORDS
+    double *sorted;            // float path: n
     void *cub_tmp;
     size_t cub_bytes;
 };
@@ -352,7 +479,7 @@ MrfWork mrf_carve(void *work, i64 n, int dtype) {
     char *p = (char *)work;
     const i64 parts = 1ll << pw_depth(n > 0 ? n : 1);
     w.partial = (double *)p; p += al(parts * 8 * 2 + 64);
-    w.scal = (unsigned long long *)p; p += al(64);
+    w.scal = (unsigned long long *)p; p += al(W_WORDS * 8);
     w.sorted = nullptr; w.cub_tmp = nullptr; w.cub_bytes = 0;
     if (dtype == CT_F64) {
         w.sorted = (double *)p; p += al(n * 8);
@@ -362,19 +489,59 @@ MrfWork mrf_carve(void *work, i64 n, int dtype) {
     return w;
 }
 
+template <typename T>
+int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint64_t *hist, cudaStream_t s) {
+    const i64 mx = nx - 2 > 0 ? nx - 2 : 0, my = ny - 2 > 0 ? ny - 2 : 0, mz = nz - 2 > 0 ? nz - 2 : 0;
+    const i64 ni = mx * my * mz;
+    const size_t sm = (STI + 2) * (STJ + 2) * (STK + 2) * sizeof(int) +
+                      (sizeof(T) == 1 ? ct::ByteHist256::kBytes : 4096 * sizeof(uint32_t));
+    cudaFuncSetAttribute(mrf_stats_int<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const i64 tiles = ((nz + STK - 1) / STK) * ((ny + STJ - 1) / STJ) * ((nx + STI - 1) / STI);
+    mrf_stats_int<T><<<(int)min(tiles, (i64)CT_NUM_SMS * 2), 256, sm, s>>>(v, nx, ny, nz,
+                                                                         (unsigned long long *)hist, w.scal);
+    if (int st = ct::check_launch("mrf_stats_int")) return st;
+    delta_from_hist<<<1, 1024, 0, s>>>(hist, state);
+    if (int st = ct::check_launch("delta_from_hist")) return st;
+    if (ni >= 2) {
+        LapElem<T> f{v, ny, nz, (uint32_t)my, (uint32_t)mz, nullptr, (const long long *)&w.scal[W_LAPSUM], ni, 1};
+        if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s)) return st;
+    }
+    mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 1);
+    return ct::check_launch("mrf_decide");
+}
+
+int mrf_f64(const double *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, cudaStream_t s) {
+    const i64 n = nx * ny * nz;
+    const i64 mx = nx - 2 > 0 ? nx - 2 : 0, my = ny - 2 > 0 ? ny - 2 : 0, mz = nz - 2 > 0 ? nz - 2 : 0;
+    const i64 ni = mx * my * mz;
+    mrf_nnz_generic<double><<<ct::grid_for(n, 256, CT_NUM_SMS * 4), 256, 0, s>>>(v, nx, ny, nz, &w.scal[W_NNZ]);
+    if (int st = ct::check_launch("mrf_nnz")) return st;
+    size_t tb = w.cub_bytes;
+    cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, v, w.sorted, (int)n, 0, 64, s);
+    delta_from_sorted<<<ct::grid_for(n, 256, CT_NUM_SMS * 4), 256, 0, s>>>(w.sorted, n, &w.scal[W_BEST_BITS]);
+    delta_store<<<1, 1, 0, s>>>(&w.scal[W_BEST_BITS], state);
+    if (int st = ct::check_launch("mrf delta")) return st;
+    if (ni >= 2) {
+        LapElem<double> f1{v, ny, nz, (uint32_t)my, (uint32_t)mz, nullptr, nullptr, ni, 0};
+        if (int st = pairwise_sum(f1, ni, w.partial, &state[S_SUM1], s)) return st;
+        mean_from_sum<<<1, 1, 0, s>>>(state, ni);
+        LapElem<double> f2{v, ny, nz, (uint32_t)my, (uint32_t)mz, &state[S_SUM1], nullptr, ni, 1};
+        if (int st = pairwise_sum(f2, ni, w.partial, &state[S_SUM2], s)) return st;
+    }
+    StepElem<double> f3{v, nullptr, nx, ny, nz, &state[S_DELTA]};
+    if (int st = pairwise_sum(f3, n, w.partial, &state[S_SUM3], s)) return st;
+    mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 0);
+    return ct::check_launch("mrf_decide");
+}
+
 }  // namespace
 
 size_t ct_mrf_workspace(int64_t nx, int64_t ny, int64_t nz, int dtype) {
     const i64 n = nx * ny * nz;
     const i64 parts = 1ll << pw_depth(n > 0 ? n : 1);
-    size_t b = al(parts * 8 * 2 + 64) + al(64);
+    size_t b = al(parts * 8 * 2 + 64) + al(W_WORDS * 8);
     if (dtype == CT_F64) b += al(n * 8) + al(cub_sort_bytes(n));
     return b + 1024;
-}
-
-__global__ void step_finish(double *out2, const unsigned long long *moved) {
-    out2[0] = __dsqrt_rn(out2[0]);
-    out2[1] = (double)*moved;
 }
 
 extern "C" int ct_mrf(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz, void *work, double *state,
@@ -385,8 +552,8 @@ extern "C" int ct_mrf(const void *in, int dtype, int64_t nx, int64_t ny, int64_t
     }
     cudaStream_t s = (cudaStream_t)stream;
     const i64 n = nx * ny * nz;
-    if (n >= (1ll << 31) && dtype == CT_F64) {
-        ct::set_error("float MRF limited to 2^31 voxels");
+    if (n >= (1ll << 31)) {
+        ct::set_error("MRF limited to 2^31 voxels");
         return CT_ERR_UNSUPPORTED;
     }
     if (dtype != CT_F64 && !hist) {
@@ -395,36 +562,16 @@ extern "C" int ct_mrf(const void *in, int dtype, int64_t nx, int64_t ny, int64_t
     }
     MrfWork w = mrf_carve(work, n, dtype);
     cudaMemsetAsync(state, 0, S_WORDS * sizeof(double), s);
-    cudaMemsetAsync(w.scal, 0, 64, s);
-    cudaMemsetAsync(&w.scal[1], 0xff, 8, s);
-    const i64 mx = nx - 2 > 0 ? nx - 2 : 0, my = ny - 2 > 0 ? ny - 2 : 0, mz = nz - 2 > 0 ? nz - 2 : 0;
-    const i64 ni = mx * my * mz;
-    CT_DISPATCH(dtype, T, {
-        const T *v = (const T *)in;
-        mrf_stats<T><<<ct::grid_for(n, 256, CT_NUM_SMS * 4), 256, 0, s>>>(v, nx, ny, nz,
-                                                                          dtype == CT_F64 ? nullptr : hist, &w.scal[0]);
-        if (int st = ct::check_launch("mrf_stats")) return st;
-        if (dtype == CT_F64) {
-            size_t tb = w.cub_bytes;
-            cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, (const double *)in, w.sorted, (int)n, 0, 64, s);
-            delta_from_sorted<<<ct::grid_for(n, 256, CT_NUM_SMS * 4), 256, 0, s>>>(w.sorted, n, &w.scal[1]);
-            delta_store<<<1, 1, 0, s>>>(&w.scal[1], state);
-        } else {
-            delta_from_hist<<<1, 1024, 0, s>>>(hist, state);
-        }
-        if (int st = ct::check_launch("mrf delta")) return st;
-        if (ni >= 2) {
-            LapElem<T> f1{v, ny, nz, my, mz, nullptr, 0};
-            if (int st = pairwise_sum(f1, ni, w.partial, &state[S_SUM1], s)) return st;
-            mean_from_sum<<<1, 1, 0, s>>>(state, ni);
-            LapElem<T> f2{v, ny, nz, my, mz, &state[S_SUM1], 1};
-            if (int st = pairwise_sum(f2, ni, w.partial, &state[S_SUM2], s)) return st;
-        }
-        StepElem<T> f3{v, nullptr, nx, ny, nz, &state[S_DELTA]};
-        if (int st = pairwise_sum(f3, n, w.partial, &state[S_SUM3], s)) return st;
-        mrf_decide<<<1, 1, 0, s>>>(state, ni, &w.scal[0]);
-    });
-    return ct::check_launch("mrf_decide");
+    cudaMemsetAsync(w.scal, 0, W_WORDS * 8, s);
+    cudaMemsetAsync(&w.scal[W_BEST_BITS], 0xff, 8, s);
+    switch (dtype) {
+        case CT_U8: return mrf_int<uint8_t>((const uint8_t *)in, nx, ny, nz, w, state, hist, s);
+        case CT_U16: return mrf_int<uint16_t>((const uint16_t *)in, nx, ny, nz, w, state, hist, s);
+        case CT_F64: return mrf_f64((const double *)in, nx, ny, nz, w, state, s);
+        default:
+            ct::set_error("unsupported dtype %d", dtype);
+            return CT_ERR_UNSUPPORTED;
+    }
 }
 
 extern "C" int ct_mrf_step(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *cur,
@@ -432,26 +579,18 @@ extern "C" int ct_mrf_step(const void *in, int dtype, int64_t nx, int64_t ny, in
     cudaStream_t s = (cudaStream_t)stream;
     const i64 n = nx * ny * nz;
     MrfWork w = mrf_carve(work, n, dtype);
-    cudaMemsetAsync(&w.scal[2], 0, 8, s);
+    cudaMemsetAsync(&w.scal[W_MOVED], 0, 8, s);
     CT_DISPATCH(dtype, T, {
         const T *v = (const T *)in;
         StepElem<T> f{v, cur, nx, ny, nz, &state[S_DELTA]};
         if (int st = pairwise_sum(f, n, w.partial, &out2[0], s)) return st;
-        mrf_apply<T><<<ct::grid_for(n, 256), 256, 0, s>>>(v, cur, nx, ny, nz, state + S_DELTA, next, &w.scal[2]);
+        mrf_apply<T><<<ct::grid_for(n, 256), 256, 0, s>>>(v, cur, nx, ny, nz, state + S_DELTA, next,
+                                                          &w.scal[W_MOVED]);
         if (int st = ct::check_launch("mrf_apply")) return st;
     });
-    step_finish<<<1, 1, 0, s>>>(out2, &w.scal[2]);
+    step_finish<<<1, 1, 0, s>>>(out2, &w.scal[W_MOVED]);
     return ct::check_launch("mrf_step_finish");
 }
-
-namespace {
-template <typename T>
-__global__ void sign_sum_kernel(const T *__restrict__ v, i64 nx, i64 ny, i64 nz, int64_t *__restrict__ out) {
-    const i64 n = nx * ny * nz;
-    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x)
-        out[p] = sign_sum_at<T>(v, nullptr, nx, ny, nz, p);
-}
-}  // namespace
 
 // ref denoise.py:117-132 _neighbor_sign_sum: int64 sign sum, edges replicated.
 extern "C" int ct_sign_sum(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz, int64_t *out,

@@ -1,0 +1,50 @@
+"""Frame sharding across GPUs.
+
+Time points are independent units (ref SPEC.md:103,176,353): each rank owns a
+contiguous block of frames and runs the whole per-frame path locally; volumes
+never cross GPUs.  The only cross-frame dependency in the reference is the
+running detection-id counter (ref session.py:295-300: frame t's ids start at
+the number of detections in frames < t).  Ranks therefore segment with
+id_start = 0, all_gather the per-frame detection counts (NCCL over NVLink on
+the GPU box, gloo in the CPU tests), and shift their ids by the exclusive
+prefix sum -- exactly the reference's ids.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def frame_shard(t_count: int, world: int, rank: int) -> range:
+    """Contiguous block of frames owned by `rank` (all channels of a frame together)."""
+    per = (t_count + world - 1) // world
+    return range(min(rank * per, t_count), min((rank + 1) * per, t_count))
+
+
+def global_id_starts(local_counts: dict[int, int], t_count: int, device=None, group=None) -> list[int]:
+    """id_start for every frame from the per-rank detection counts.
+
+    local_counts maps the frames this rank processed to their detection
+    counts.  One all_gather of a t_count-long int64 vector (owned frames
+    filled, others 0); the sum over ranks is the global per-frame count and its
+    exclusive prefix sum the reference's id_start per frame."""
+    dev = device or torch.device("cpu")
+    mine = torch.zeros(t_count, dtype=torch.int64, device=dev)
+    for t, c in local_counts.items():
+        mine[t] = int(c)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        parts = [torch.zeros_like(mine) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(parts, mine, group=group)
+        total = torch.stack(parts).sum(dim=0)
+    else:
+        total = mine
+    starts = torch.cumsum(total, 0) - total
+    return [int(x) for x in starts.cpu()]
+
+
+def relabel_rows(rows, id_start: int):
+    """Shift a frame's ct_cell rows (segmented with id_start 0) to global ids."""
+    out = rows.copy()
+    out["id"] += id_start
+    return out
