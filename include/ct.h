@@ -116,8 +116,10 @@ int ct_otsu(const uint64_t *hist, int64_t nbins, int64_t *result, void *stream);
 
 /* K4 -- ref segment.py:204 + :175-189: mask = rint(v) > t (t from a ct_otsu
  * result; status 1 -> empty mask), then ball closing of radius r on the
- * infinite zero domain.  r == 0 skips the closing.  work: radius > 1 needs
- * ct_workspace_bytes(1,...). otsu_result == NULL thresholds at t_host. */
+ * infinite zero domain.  r == 0 skips the closing.  work: radius >= 1 takes
+ * ct_workspace_bytes(1,...) (r == 1 runs bit-packed when nz <= 64 and
+ * nz % 4 == 0; without work it uses a byte-tile kernel; r > 1 requires it).
+ * otsu_result == NULL thresholds at t_host. */
 int ct_threshold_close(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz,
                        const int64_t *otsu_result, int64_t t_host, int radius, uint8_t *mask_out,
                        void *work, void *stream);

@@ -38,7 +38,11 @@ extern "C" size_t ct_workspace_bytes(int which, int64_t nx, int64_t ny, int64_t 
     const int64_t N = nx * ny * nz;
     switch (which) {
         case 0: return (size_t)(2 * N) * sizeof(double);                                // gaussian
-        case 1: return (size_t)((nx + 2 * cap) * (ny + 2 * cap) * (nz + 2 * cap));      // closing, cap = radius
+        case 1: {                                                                      // closing, cap = radius
+            const size_t ext = (size_t)((nx + 2 * cap) * (ny + 2 * cap) * (nz + 2 * cap));
+            const size_t rows = (size_t)(nx * ny) * 8 + 256;
+            return ext > rows ? ext : rows;
+        }
         case 2: return ct_table_workspace(N, cap);                                      // table
         case 3: return ct_edt_workspace(nx, ny, nz);                                    // edt
         case 4: return ct_mrf_workspace(nx, ny, nz, (int)cap);                          // mrf, cap = dtype

@@ -2,120 +2,212 @@
 //
 // Replaces ref segment.py:292-304: ndimage.distance_transform_edt(~mask,
 // sampling=(dx,dy,dz)) -- the distance (um) from every voxel to the nearest
-// foreground voxel, computed by scipy from an integer feature transform as
-//   sqrt(((fi-i)dx)^2 + ((fj-j)dy)^2 + ((fk-k)dz)^2), summed axis 0 -> 2.
-// Here the feature coordinates are carried through three separable passes
-// (x: nearest foreground on the line; y, z: lower envelope of parabolas,
-// Felzenszwalb-Huttenlocher) and the distance is formed from them in
-// scipy's order, so distances agree bit for bit whenever the chosen feature
-// is scipy's (equidistant features may differ in the last ulp; the
-// reference's own contract is 1e-9 um, ref test_acceptance.py:318-332).
-// Arithmetic is identical to oracle/ct_oracle.c (no FMA: __d*_rn).
+// foreground voxel.  scipy forms it from an integer feature transform as
+//   sqrt(((fi-i)dx)^2 + ((fj-j)dy)^2 + ((fk-k)dz)^2), summed axis 0 -> 2;
+// here the nearest feature's integer offsets are carried through three
+// separable passes and the distance is formed from them in exactly that order.
+//
+//   pass z : per (i,j) line (contiguous, nz <= 128): the line's mask is four
+//            warp ballots; each voxel's nearest set bit is one CLZ/FFS pair.
+//            Output: dk (int8), or NONE.                       1 B in, 1 B out
+//   pass y : per (i,k) line along j: lower envelope of the parabolas
+//            (dk*dz)^2 + ((j-q)*dy)^2 over the sites q (Felzenszwalb-
+//            Huttenlocher).  Output (dj, dk) packed in int32.   1 B in, 4 B out
+//   pass x : per (j,k) line along i, site cost (dj*dy)^2 + (dk*dz)^2, output
+//            the float64 distance.                              4 B in, 8 B out
+// Lines map to consecutive k across a warp, so every load/store is coalesced.
+// Each thread keeps its envelope stack (site position + payload) in SMEM
+// (spilling to a global scratch beyond 16 entries); intersections are
+// recomputed from the stack, so neither the build nor the output loop issues a
+// dependent global load.  Arithmetic matches oracle/ct_oracle.c ora_edt bit for
+// bit (separately rounded __d*_rn ops); equidistant features may differ from
+// scipy's choice in the last ulp, within the reference's 1e-9 um contract
+// (ref test_acceptance.py:318-332).
+#include <type_traits>
+
 #include "ct_common.cuh"
 
 namespace {
 
-constexpr int FB = 21;
-constexpr i64 FM = (1ll << FB) - 1;
-
-__device__ __forceinline__ i64 fpack(i64 a, i64 b, i64 c) { return (a << (2 * FB)) | (b << FB) | c; }
+constexpr int8_t NONE8 = -128;
+constexpr int32_t NONE32 = INT32_MIN;
+constexpr int SC = 16;       // SMEM stack entries per thread
+constexpr int LT = 256;      // threads per envelope CTA
 
 __device__ __forceinline__ double sq(double x) { return __dmul_rn(x, x); }
 
-__device__ __forceinline__ double cost(i64 f, i64 i, i64 j, i64 k, int upto, double dx, double dy, double dz) {
-    const i64 fi = (f >> (2 * FB)) & FM, fj = (f >> FB) & FM, fk = f & FM;
-    const double t0 = sq(__dmul_rn((double)(fi - i), dx));
-    if (upto == 0) return t0;
-    const double t1 = sq(__dmul_rn((double)(fj - j), dy));
-    if (upto == 1) return __dadd_rn(t0, t1);
-    const double t2 = sq(__dmul_rn((double)(fk - k), dz));
-    return __dadd_rn(__dadd_rn(t0, t1), t2);
-}
-
-// pass 0: per (j,k) line along x, nearest foreground (ties -> lower i)
-__global__ void edt_pass_x(const uint8_t *__restrict__ mask, i64 nx, i64 ny, i64 nz, i64 *__restrict__ f) {
-    const i64 nl = ny * nz, S = ny * nz;
-    for (i64 l = blockIdx.x * (i64)blockDim.x + threadIdx.x; l < nl; l += (i64)gridDim.x * blockDim.x) {
-        const i64 j = l / nz, k = l % nz;
-        i64 last = -1;
-        for (i64 i = 0; i < nx; ++i) {
-            const i64 p = i * S + l;
-            if (mask[p]) last = i;
-            f[p] = last;
-        }
-        i64 next = -1;
-        for (i64 i = nx - 1; i >= 0; --i) {
-            const i64 p = i * S + l;
-            if (mask[p]) next = i;
-            i64 best = f[p];
-            if (next >= 0 && (best < 0 || next - i < i - best)) best = next;
-            f[p] = best < 0 ? -1 : fpack(best, j, k);
+// ---------------------------------------------------------------------------
+// pass z: nearest foreground along k, ties -> lower k
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) edt_pass_z(const uint8_t *__restrict__ mask, i64 nlines, int nz,
+                                                  int8_t *__restrict__ dk) {
+    const unsigned lane = threadIdx.x & 31;
+    const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+    const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+    const int W = (nz + 31) >> 5;  // <= 4
+    for (i64 l = warp; l < nlines; l += nwarps) {
+        const uint8_t *m = mask + l * nz;
+        uint32_t words[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+            if (w < W) {
+                const int k = 32 * w + lane;
+                words[w] = __ballot_sync(0xffffffffu, k < nz && m[k] != 0);
+            }
+        const u64 lo = ((u64)words[1] << 32) | words[0], hi = ((u64)words[3] << 32) | words[2];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int k = 32 * w + lane;
+            if (w >= W || k >= nz) continue;
+            // previous set bit <= k
+            int prev = -1, next = -1;
+            if (k < 64) {
+                const u64 x = lo & (k == 63 ? ~0ull : ((2ull << k) - 1));
+                if (x) prev = 63 - __clzll((long long)x);
+                const u64 y = lo & ~((1ull << k) - 1);
+                if (y) next = __ffsll((long long)y) - 1;
+                else if (hi) next = 64 + __ffsll((long long)hi) - 1;
+            } else {
+                const int kk = k - 64;
+                const u64 x = hi & (kk == 63 ? ~0ull : ((2ull << kk) - 1));
+                if (x) prev = 64 + 63 - __clzll((long long)x);
+                else if (lo) prev = 63 - __clzll((long long)lo);
+                const u64 y = hi & ~((1ull << kk) - 1);
+                if (y) next = 64 + __ffsll((long long)y) - 1;
+            }
+            int best = prev;
+            if (next >= 0 && (best < 0 || next - k < k - best)) best = next;
+            dk[l * nz + k] = best < 0 ? NONE8 : (int8_t)(best - k);
         }
     }
 }
 
-// passes 1 (axis y) and 2 (axis z): lower envelope per line; scratch laid
-// out [position][line] so neighbouring threads (lines) coalesce.
-template <int AXIS>
-__global__ void edt_pass_env(const i64 *__restrict__ fin, i64 *__restrict__ fout, i64 nx, i64 ny, i64 nz, double dx,
-                             double dy, double dz, int32_t *__restrict__ vs, double *__restrict__ zs,
-                             double *__restrict__ gs) {
-    const i64 nl = AXIS == 1 ? nx * nz : nx * ny;
-    const i64 L = AXIS == 1 ? ny : nz;
-    const double d = AXIS == 1 ? dy : dz, d2 = __dmul_rn(d, d);
-    for (i64 l = blockIdx.x * (i64)blockDim.x + threadIdx.x; l < nl; l += (i64)gridDim.x * blockDim.x) {
-        i64 ci, cj = 0, ck = 0, base, stride;
-        if (AXIS == 1) {
-            ci = l / nz; ck = l % nz; base = ci * ny * nz + ck; stride = nz;
-        } else {
-            ci = l / ny; cj = l % ny; base = l * nz; stride = 1;
+// generic pass z for nz > 128 (one thread per line, two sweeps); offsets must fit int8
+__global__ void edt_pass_z_generic(const uint8_t *__restrict__ mask, i64 nlines, int nz, int8_t *__restrict__ dk) {
+    for (i64 l = blockIdx.x * (i64)blockDim.x + threadIdx.x; l < nlines; l += (i64)gridDim.x * blockDim.x) {
+        const uint8_t *m = mask + l * nz;
+        int8_t *o = dk + l * nz;
+        int last = -1;
+        for (int k = 0; k < nz; ++k) {
+            if (m[k]) last = k;
+            o[k] = last < 0 ? NONE8 : (int8_t)max(-127, last - k);
         }
-#define V(x) vs[(x) * nl + l]
-#define Z(x) zs[(x) * nl + l]
-#define G(x) gs[(x) * nl + l]
-        i64 kk = -1;
-        for (i64 q = 0; q < L; ++q) {
-            const i64 f = fin[base + q * stride];
-            if (f < 0) continue;
-            const double gq = AXIS == 1 ? cost(f, ci, q, ck, 0, dx, dy, dz) : cost(f, ci, cj, q, 1, dx, dy, dz);
-            G(q) = gq;
-            if (kk < 0) {
-                kk = 0; V(0) = (int32_t)q; Z(0) = -INFINITY; Z(1) = INFINITY;
+        int next = -1;
+        for (int k = nz - 1; k >= 0; --k) {
+            if (m[k]) next = k;
+            const int prev = o[k] == NONE8 ? -1 : k + o[k];
+            int best = prev;
+            if (next >= 0 && (best < 0 || next - k < k - best)) best = next;
+            o[k] = best < 0 ? NONE8 : (int8_t)(best - k);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// envelope passes (AXIS 1: y, input int8 dk; AXIS 0: x, input packed (dj,dk))
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int32_t pack(int dj, int dk) { return (int32_t)((dj << 8) | (uint8_t)(int8_t)dk); }
+__device__ __forceinline__ int unpack_dj(int32_t p) { return p >> 8; }
+__device__ __forceinline__ int unpack_dk(int32_t p) { return (int)(int8_t)(p & 0xff); }
+
+template <int AXIS>
+struct Env {
+    // payload of a site (the feature's offsets along the already-done axes)
+    typedef typename std::conditional<AXIS == 1, int8_t, int32_t>::type In;
+    __device__ static bool site(In v) { return AXIS == 1 ? v != NONE8 : v != NONE32; }
+    __device__ static int32_t payload(In v) { return (int32_t)v; }
+    // cost of the site's feature on its own line position (previous axes only)
+    __device__ static double g(int32_t pl, double dy, double dz) {
+        if (AXIS == 1) return sq(__dmul_rn((double)pl, dz));
+        return __dadd_rn(sq(__dmul_rn((double)unpack_dj(pl), dy)), sq(__dmul_rn((double)unpack_dk(pl), dz)));
+    }
+};
+
+__device__ __forceinline__ double isect(int q, double gq, int p, double gp, double d2) {
+    return __dmul_rn(__dadd_rn(__ddiv_rn(__dadd_rn(gq, -gp), __dmul_rn(d2, (double)(q - p))), (double)(q + p)), 0.5);
+}
+
+template <int AXIS>
+__global__ void __launch_bounds__(LT) edt_pass_env(const typename Env<AXIS>::In *__restrict__ in, i64 nlines, int L,
+                                                   i64 stride, double dx, double dy, double dz,
+                                                   int32_t *__restrict__ out32, double *__restrict__ out64,
+                                                   u64 *__restrict__ spill) {
+    __shared__ u64 stk[SC][LT];  // entry = (position << 32) | payload
+    typedef Env<AXIS> E;
+    const double d = AXIS == 1 ? dy : dx, d2 = __dmul_rn(d, d);
+    const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
+    if (l < nlines) {
+        // line l: element x at base + x*stride
+        i64 base;
+        if (AXIS == 1) {  // lines (i, k), position j, stride nz
+            const i64 nz = stride, ny = L;
+            base = (l / nz) * ny * nz + (l % nz);
+        } else {          // lines (j, k) = flattened plane index, position i
+            base = l;
+        }
+#define ENT(e) (*((e) < SC ? &stk[(e)][threadIdx.x] : &spill[((e) - SC) * nlines + l]))
+        int K = 0;  // stack size
+        for (int x = 0; x < L; ++x) {
+            const typename E::In v = in[base + (i64)x * stride];
+            if (!E::site(v)) continue;
+            const int32_t pl = E::payload(v);
+            const double gx = E::g(pl, dy, dz);
+            while (K > 0) {
+                const u64 top = ENT(K - 1);
+                const int p = (int)(top >> 32);
+                const double gp = E::g((int32_t)(top & 0xffffffffu), dy, dz);
+                const double s = isect(x, gx, p, gp, d2);
+                double zt = -INFINITY;  // boundary where the top entry starts
+                if (K > 1) {
+                    const u64 below = ENT(K - 2);
+                    const int pb = (int)(below >> 32);
+                    zt = isect(p, gp, pb, E::g((int32_t)(below & 0xffffffffu), dy, dz), d2);
+                }
+                if (s <= zt) --K;
+                else break;
+            }
+            ENT(K) = ((u64)(uint32_t)x << 32) | (uint32_t)pl;
+            ++K;
+        }
+        // output: segment e covers x with z[e] < x <= z[e+1]
+        int e = 0;
+        u64 cur = K ? ENT(0) : 0;
+        double znext = INFINITY;
+        if (K > 1) {
+            const u64 nx_ = ENT(1);
+            znext = isect((int)(nx_ >> 32), E::g((int32_t)(nx_ & 0xffffffffu), dy, dz), (int)(cur >> 32),
+                          E::g((int32_t)(cur & 0xffffffffu), dy, dz), d2);
+        }
+        for (int x = 0; x < L; ++x) {
+            const i64 o = base + (i64)x * stride;
+            if (K == 0) {
+                if (AXIS == 1) out32[o] = NONE32;
+                else out64[o] = INFINITY;
                 continue;
             }
-            double s;
-            for (;;) {
-                const i64 p = V(kk);
-                s = __dmul_rn(__dadd_rn(__ddiv_rn(__dadd_rn(gq, -G(p)), __dmul_rn(d2, (double)(q - p))),
-                                        (double)(q + p)),
-                              0.5);
-                if (s <= Z(kk)) { --kk; continue; }
-                break;
+            while (znext < (double)x) {
+                ++e;
+                cur = ENT(e);
+                if (e + 1 < K) {
+                    const u64 nx_ = ENT(e + 1);
+                    znext = isect((int)(nx_ >> 32), E::g((int32_t)(nx_ & 0xffffffffu), dy, dz), (int)(cur >> 32),
+                                  E::g((int32_t)(cur & 0xffffffffu), dy, dz), d2);
+                } else {
+                    znext = INFINITY;
+                }
             }
-            ++kk; V(kk) = (int32_t)q; Z(kk) = s; Z(kk + 1) = INFINITY;
+            const int q = (int)(cur >> 32);
+            const int32_t pl = (int32_t)(cur & 0xffffffffu);
+            if (AXIS == 1) {
+                out32[o] = pack(q - x, pl);
+            } else {
+                const double t0 = sq(__dmul_rn((double)(q - x), dx));
+                const double t1 = sq(__dmul_rn((double)unpack_dj(pl), dy));
+                const double t2 = sq(__dmul_rn((double)unpack_dk(pl), dz));
+                out64[o] = __dsqrt_rn(__dadd_rn(__dadd_rn(t0, t1), t2));
+            }
         }
-        if (kk < 0) {
-            for (i64 x = 0; x < L; ++x) fout[base + x * stride] = -1;
-            continue;
-        }
-        i64 e = 0;
-        for (i64 x = 0; x < L; ++x) {
-            while (Z(e + 1) < (double)x) ++e;
-            fout[base + x * stride] = fin[base + (i64)V(e) * stride];
-        }
-#undef V
-#undef Z
-#undef G
-    }
-}
-
-__global__ void edt_final(const i64 *__restrict__ f, i64 nx, i64 ny, i64 nz, double dx, double dy, double dz,
-                          double *__restrict__ out) {
-    const i64 n = nx * ny * nz;
-    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x) {
-        const i64 k = p % nz, j = (p / nz) % ny, i = p / (ny * nz);
-        const i64 fv = f[p];
-        out[p] = fv < 0 ? INFINITY : __dsqrt_rn(cost(fv, i, j, k, 2, dx, dy, dz));
+#undef ENT
     }
 }
 
@@ -123,9 +215,10 @@ __global__ void edt_final(const i64 *__restrict__ f, i64 nx, i64 ny, i64 nz, dou
 
 size_t ct_edt_workspace(int64_t nx, int64_t ny, int64_t nz) {
     const i64 N = nx * ny * nz;
-    const i64 ly = nx * nz * (ny + 2), lz = nx * ny * (nz + 2);
-    const i64 L = ly > lz ? ly : lz;
-    return (size_t)(2 * N * 8) + (size_t)L * (4 + 8 + 8) + 1024;
+    // dk (1 B) + packed (4 B) + spill: (L - SC) entries per line, 8 B
+    const i64 ly = nx * nz * (ny > SC ? ny - SC : 0), lx = ny * nz * (nx > SC ? nx - SC : 0);
+    const i64 sp = ly > lx ? ly : lx;
+    return (size_t)N * 5 + (size_t)sp * 8 + 4096;
 }
 
 extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, double dx, double dy, double dz,
@@ -134,25 +227,25 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         ct::set_error("mask has no voxels");
         return CT_ERR_PARAM;
     }
-    if (nx > FM || ny > FM || nz > FM) {
-        ct::set_error("EDT supports extents below 2^21");
-        return CT_ERR_UNSUPPORTED;
+    if (nz > 127 || ny > 32767 || nx > (1 << 30)) {
+        // dk offsets are int8 and dj int24 in the packed payload
+        if (nz > 127) {
+            ct::set_error("EDT: nz > 127 unsupported by the packed feature format");
+            return CT_ERR_UNSUPPORTED;
+        }
     }
     cudaStream_t s = (cudaStream_t)stream;
     const i64 N = nx * ny * nz;
-    i64 *fa = (i64 *)work, *fb = fa + N;
-    const i64 ly = nx * nz * (ny + 2), lz = nx * ny * (nz + 2);
-    const i64 L = ly > lz ? ly : lz;
-    char *sp = (char *)(fb + N);
-    double *zs = (double *)sp;
-    double *gs = zs + L;
-    int32_t *vs = (int32_t *)(gs + L);
-    edt_pass_x<<<ct::grid_for(ny * nz, 128), 128, 0, s>>>(mask, nx, ny, nz, fa);
-    if (int st = ct::check_launch("edt_pass_x")) return st;
-    edt_pass_env<1><<<ct::grid_for(nx * nz, 128), 128, 0, s>>>(fa, fb, nx, ny, nz, dx, dy, dz, vs, zs, gs);
-    if (int st = ct::check_launch("edt_pass_y")) return st;
-    edt_pass_env<2><<<ct::grid_for(nx * ny, 128), 128, 0, s>>>(fb, fa, nx, ny, nz, dx, dy, dz, vs, zs, gs);
+    int8_t *dk = (int8_t *)work;
+    int32_t *pk = (int32_t *)((char *)work + ((N + 255) & ~(i64)255));
+    u64 *spill = (u64 *)((char *)pk + ((N * 4 + 255) & ~(i64)255));
+    edt_pass_z<<<ct::grid_for(nx * ny * 32, 256, CT_NUM_SMS * 16), 256, 0, s>>>(mask, nx * ny, (int)nz, dk);
     if (int st = ct::check_launch("edt_pass_z")) return st;
-    edt_final<<<ct::grid_for(N, 256), 256, 0, s>>>(fa, nx, ny, nz, dx, dy, dz, out);
-    return ct::check_launch("edt_final");
+    const i64 ly = nx * nz, lx = ny * nz;
+    edt_pass_env<1><<<(unsigned)((ly + LT - 1) / LT), LT, 0, s>>>(dk, ly, (int)ny, nz, dx, dy, dz, pk, nullptr,
+                                                                    spill);
+    if (int st = ct::check_launch("edt_pass_y")) return st;
+    edt_pass_env<0><<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(pk, lx, (int)nx, ny * nz, dx, dy, dz, nullptr, out,
+                                                                    spill);
+    return ct::check_launch("edt_pass_x");
 }

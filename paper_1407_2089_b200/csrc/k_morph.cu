@@ -121,6 +121,98 @@ __global__ void erode_ext(const uint8_t *__restrict__ ext, i64 nx, i64 ny, i64 n
     }
 }
 
+// ---------------------------------------------------------------------------
+// r == 1, nz <= 64: z-rows as 64-bit words.
+//   pack_rows   : M(i,j) = threshold bits of row (i,j) (two ballots per row).
+//   close1_bits : D(q) = OR of the 6-cross of M around q, E(p) = AND of the
+//                 6-cross of D around p, with the out-of-volume D values of the
+//                 infinite zero domain: D(i=-1,j) = M(0,j), D(i,j,k=-1) =
+//                 M(i,j,0), ... (the only in-volume cross neighbour).  One
+//                 thread per row, 13 word loads (L2-resident: N/8 bytes),
+//                 bytes written through an SMEM transpose for coalescing.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) pack_rows(const T *__restrict__ in, i64 nrows, int nz,
+                                                 const int64_t *__restrict__ otsu, i64 t_host,
+                                                 u64 *__restrict__ rows) {
+    bool empty;
+    const i64 t = threshold_of(otsu, t_host, empty);
+    const unsigned lane = threadIdx.x & 31;
+    const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+    const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
+        u64 mine = 0;
+        const int nr = (int)min((i64)32, nrows - r0);
+        for (int r = 0; r < nr; ++r) {
+            const T *row = in + (r0 + r) * nz;
+            const bool a = !empty && (int)lane < nz && ct::above(row[lane], t);
+            const bool b = !empty && (int)lane + 32 < nz && ct::above(row[lane + 32], t);
+            const unsigned wa = __ballot_sync(0xffffffffu, a), wb = __ballot_sync(0xffffffffu, b);
+            if ((int)lane == r) mine = ((u64)wb << 32) | wa;
+        }
+        if ((int)lane < nr) rows[r0 + lane] = mine;
+    }
+}
+
+__device__ __forceinline__ u64 rowM(const u64 *rows, i64 i, i64 j, i64 nx, i64 ny) {
+    return (i >= 0 && i < nx && j >= 0 && j < ny) ? rows[i * ny + j] : 0ull;
+}
+
+// dilation row D(i,j) over the whole (possibly out-of-volume) row
+__device__ __forceinline__ u64 rowD(const u64 *rows, i64 i, i64 j, i64 nx, i64 ny, u64 kmask) {
+    const u64 c = rowM(rows, i, j, nx, ny);
+    return (c | (c << 1) | (c >> 1) | rowM(rows, i - 1, j, nx, ny) | rowM(rows, i + 1, j, nx, ny) |
+            rowM(rows, i, j - 1, nx, ny) | rowM(rows, i, j + 1, nx, ny)) & kmask;
+}
+
+__global__ void __launch_bounds__(256) close1_bits(const u64 *__restrict__ rows, i64 nx, i64 ny, int nz,
+                                                   uint8_t *__restrict__ out, u64 *__restrict__ out_rows) {
+    __shared__ __align__(16) uint8_t stage[8][32 * 64];
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u64 kmask = nz == 64 ? ~0ull : ((1ull << nz) - 1);
+    const u64 top = 1ull << (nz - 1);
+    const i64 nrows = nx * ny;
+    const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+    const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
+        const i64 r = r0 + lane;
+        u64 e = 0;
+        if (r < nrows) {
+            const i64 i = r / ny, j = r - i * ny;
+            const u64 m = rows[r];
+            const u64 d = rowD(rows, i, j, nx, ny, kmask);
+            // cross neighbours of D; outside the volume D equals the single in-volume M
+            const u64 dxm = i > 0 ? rowD(rows, i - 1, j, nx, ny, kmask) : m;
+            const u64 dxp = i < nx - 1 ? rowD(rows, i + 1, j, nx, ny, kmask) : m;
+            const u64 dym = j > 0 ? rowD(rows, i, j - 1, nx, ny, kmask) : m;
+            const u64 dyp = j < ny - 1 ? rowD(rows, i, j + 1, nx, ny, kmask) : m;
+            const u64 dkm = ((d << 1) | (m & 1ull)) & kmask;    // D at k-1; k=-1 -> M(k=0)
+            const u64 dkp = (d >> 1) | (m & top);               // D at k+1; k=nz -> M(k=nz-1)
+            e = d & dxm & dxp & dym & dyp & dkm & dkp;
+            if (out_rows) out_rows[r] = e;
+        }
+        if (out) {
+            // bits -> bytes via SMEM, then a coalesced copy of the warp's 32 rows
+            uint8_t *st = stage[wid];
+            for (int k = 0; k < nz; k += 4) {
+                const unsigned nib = (unsigned)((e >> k) & 0xF);
+                const uint32_t bytes = ((nib * 0x00204081u) & 0x01010101u);
+                *reinterpret_cast<uint32_t *>(st + lane * nz + k) = bytes;  // nz % 4 == 0 guaranteed by caller
+            }
+            __syncwarp();
+            const int nr = (int)min((i64)32, nrows - r0);
+            const int nbytes = nr * nz;
+            uint8_t *dst = out + r0 * nz;
+            for (int b = lane * 16; b < nbytes; b += 32 * 16) {
+                if (b + 16 <= nbytes) *reinterpret_cast<uint4 *>(dst + b) = *reinterpret_cast<const uint4 *>(st + b);
+                else
+                    for (int q = b; q < nbytes; ++q) dst[q] = st[q];
+            }
+            __syncwarp();
+        }
+    }
+}
+
 template <typename T>
 int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i64 t_host, int r, uint8_t *out,
                     uint8_t *work, cudaStream_t s) {
@@ -128,6 +220,14 @@ int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i6
     if (r == 0) {
         threshold_kernel<T><<<ct::grid_for(n, 256), 256, 0, s>>>(in, n, otsu, t_host, out);
         return ct::check_launch("threshold");
+    }
+    if (r == 1 && nz <= 64 && nz % 4 == 0 && work && ((uintptr_t)out & 15) == 0) {
+        u64 *rows = (u64 *)work;
+        const i64 nrows = nx * ny;
+        pack_rows<T><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(in, nrows, (int)nz, otsu, t_host, rows);
+        if (int st = ct::check_launch("pack_rows")) return st;
+        close1_bits<<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(rows, nx, ny, (int)nz, out, nullptr);
+        return ct::check_launch("close1_bits");
     }
     if (r == 1) {
         const i64 tiles = ((nz + TK - 1) / TK) * ((ny + TJ - 1) / TJ) * ((nx + TI - 1) / TI);

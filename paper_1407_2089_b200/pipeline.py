@@ -103,7 +103,7 @@ class FramePipeline:
             self.twork = E(workspace_bytes(2, nx, ny, nz, self.cap), torch.uint8)
             self.table = E(self.cap * CELL_DTYPE.itemsize, torch.uint8)
             self.voxels = E(n, torch.int32)
-            self.cwork = E(workspace_bytes(1, nx, ny, nz, cr), torch.uint8) if cr > 1 else None
+            self.cwork = E(workspace_bytes(1, nx, ny, nz, cr), torch.uint8) if cr >= 1 else None
         if vessel:
             self.mwork = E(workspace_bytes(4, nx, ny, nz, self.code), torch.uint8)
             self.state = Z(9, torch.float64)
@@ -112,7 +112,7 @@ class FramePipeline:
             self.vmask = E(self.dims, torch.uint8)
             self.ework = E(workspace_bytes(3, nx, ny, nz), torch.uint8)
             self.dist = E(self.dims, torch.float64)
-            self.vcwork = E(workspace_bytes(1, nx, ny, nz, cr), torch.uint8) if cr > 1 else None
+            self.vcwork = E(workspace_bytes(1, nx, ny, nz, cr), torch.uint8) if cr >= 1 else None
 
     # -- optional per-stage CUDA events (on the launching stream) -----------
     def _t0(self):

@@ -164,7 +164,7 @@ def _close_dev(values: torch.Tensor, otsu_res, t_host: int, radius: int) -> torc
     nx, ny, nz = (int(d) for d in values.shape)
     out = _dev.empty((nx, ny, nz), torch.uint8)
     work = None
-    if radius > 1:
+    if radius >= 1:
         work = _dev.empty(workspace_bytes(1, nx, ny, nz, radius), torch.uint8)
     call(
         "ct_threshold_close", values.data_ptr(), _dev.ct_code(values), nx, ny, nz,
