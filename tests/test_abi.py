@@ -38,7 +38,7 @@ def test_workspace_sizes_are_sane():
     n = 1024 * 1024 * 64
     assert _lib.workspace_bytes(0, 1024, 1024, 64) == 2 * n * 8
     assert _lib.workspace_bytes(2, 1024, 1024, 64, 1 << 20) > n * 4
-    assert _lib.workspace_bytes(3, 1024, 1024, 64) > 2 * n * 8
+    assert _lib.workspace_bytes(3, 1024, 1024, 64) >= 5 * n
 
 
 def test_library_is_sm100a():
