@@ -123,8 +123,21 @@ struct Env {
     }
 };
 
-__device__ __forceinline__ double isect(int q, double gq, int p, double gp, double d2) {
-    return __dmul_rn(__dadd_rn(__ddiv_rn(__dadd_rn(gq, -gp), __dmul_rn(d2, (double)(q - p))), (double)(q + p)), 0.5);
+// Division-free envelope predicates (identical op order in oracle/ct_oracle.c).
+// Sites b < p < q with costs gb, gp, gq; a = q - p, c = p - b.  The parabola
+// of q overtakes p before p overtakes b (pop p) iff
+//   c*(gq - gp) - a*(gp - gb) <= -(d2*a*c*(a + c))
+// and position x has passed the p|q boundary iff
+//   gq - gp < d2*a*(2x - q - p).
+__device__ __forceinline__ bool env_pop(int q, double gq, int p, double gp, int b, double gb, double d2) {
+    const double a = (double)(q - p), c = (double)(p - b);
+    const double lhs = __dadd_rn(__dmul_rn(c, __dadd_rn(gq, -gp)), -__dmul_rn(a, __dadd_rn(gp, -gb)));
+    const double rhs = -__dmul_rn(__dmul_rn(__dmul_rn(d2, a), c), a + c);
+    return lhs <= rhs;
+}
+
+__device__ __forceinline__ bool env_past(int x, int q, double gq, int p, double gp, double d2) {
+    return __dadd_rn(gq, -gp) < __dmul_rn(__dmul_rn(d2, (double)(q - p)), (double)(2 * x - q - p));
 }
 
 template <int AXIS>
@@ -134,81 +147,84 @@ __global__ void __launch_bounds__(LT) edt_pass_env(const typename Env<AXIS>::In 
                                                    u64 *__restrict__ spill) {
     __shared__ u64 stk[SC][LT];  // entry = (position << 32) | payload
     typedef Env<AXIS> E;
+    typedef typename E::In In;
     const double d = AXIS == 1 ? dy : dx, d2 = __dmul_rn(d, d);
     const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
-    if (l < nlines) {
-        // line l: element x at base + x*stride
-        i64 base;
-        if (AXIS == 1) {  // lines (i, k), position j, stride nz
-            const i64 nz = stride, ny = L;
-            base = (l / nz) * ny * nz + (l % nz);
-        } else {          // lines (j, k) = flattened plane index, position i
-            base = l;
-        }
-#define ENT(e) (*((e) < SC ? &stk[(e)][threadIdx.x] : &spill[((e) - SC) * nlines + l]))
-        int K = 0;  // stack size
-        for (int x = 0; x < L; ++x) {
-            const typename E::In v = in[base + (i64)x * stride];
-            if (!E::site(v)) continue;
-            const int32_t pl = E::payload(v);
-            const double gx = E::g(pl, dy, dz);
-            while (K > 0) {
-                const u64 top = ENT(K - 1);
-                const int p = (int)(top >> 32);
-                const double gp = E::g((int32_t)(top & 0xffffffffu), dy, dz);
-                const double s = isect(x, gx, p, gp, d2);
-                double zt = -INFINITY;  // boundary where the top entry starts
-                if (K > 1) {
-                    const u64 below = ENT(K - 2);
-                    const int pb = (int)(below >> 32);
-                    zt = isect(p, gp, pb, E::g((int32_t)(below & 0xffffffffu), dy, dz), d2);
-                }
-                if (s <= zt) --K;
-                else break;
-            }
-            ENT(K) = ((u64)(uint32_t)x << 32) | (uint32_t)pl;
-            ++K;
-        }
-        // output: segment e covers x with z[e] < x <= z[e+1]
-        int e = 0;
-        u64 cur = K ? ENT(0) : 0;
-        double znext = INFINITY;
-        if (K > 1) {
-            const u64 nx_ = ENT(1);
-            znext = isect((int)(nx_ >> 32), E::g((int32_t)(nx_ & 0xffffffffu), dy, dz), (int)(cur >> 32),
-                          E::g((int32_t)(cur & 0xffffffffu), dy, dz), d2);
-        }
-        for (int x = 0; x < L; ++x) {
-            const i64 o = base + (i64)x * stride;
-            if (K == 0) {
-                if (AXIS == 1) out32[o] = NONE32;
-                else out64[o] = INFINITY;
-                continue;
-            }
-            while (znext < (double)x) {
-                ++e;
-                cur = ENT(e);
-                if (e + 1 < K) {
-                    const u64 nx_ = ENT(e + 1);
-                    znext = isect((int)(nx_ >> 32), E::g((int32_t)(nx_ & 0xffffffffu), dy, dz), (int)(cur >> 32),
-                                  E::g((int32_t)(cur & 0xffffffffu), dy, dz), d2);
-                } else {
-                    znext = INFINITY;
-                }
-            }
-            const int q = (int)(cur >> 32);
-            const int32_t pl = (int32_t)(cur & 0xffffffffu);
-            if (AXIS == 1) {
-                out32[o] = pack(q - x, pl);
-            } else {
-                const double t0 = sq(__dmul_rn((double)(q - x), dx));
-                const double t1 = sq(__dmul_rn((double)unpack_dj(pl), dy));
-                const double t2 = sq(__dmul_rn((double)unpack_dk(pl), dz));
-                out64[o] = __dsqrt_rn(__dadd_rn(__dadd_rn(t0, t1), t2));
-            }
-        }
-#undef ENT
+    if (l >= nlines) return;
+    i64 base;
+    if (AXIS == 1) {  // lines (i, k), position j, stride nz
+        const i64 nz = stride, ny = L;
+        base = (l / nz) * ny * nz + (l % nz);
+    } else {          // lines (j, k) = flattened plane index, position i
+        base = l;
     }
+#define ENT(e) (*((e) < SC ? &stk[(e)][threadIdx.x] : &spill[((e) - SC) * nlines + l]))
+    // build: stack entries 0..K-1 in memory; the top two also in registers
+    int K = 0;
+    int tp = 0, bp = 0;            // top / below positions
+    double tg = 0.0, bg = 0.0;     // top / below costs
+    In v = in[base];
+    for (int x = 0; x < L; ++x) {
+        const In cur = v;
+        if (x + 1 < L) v = in[base + (i64)(x + 1) * stride];  // prefetch
+        if (!E::site(cur)) continue;
+        const int32_t pl = E::payload(cur);
+        const double gx = E::g(pl, dy, dz);
+        while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+            --K;
+            tp = bp;
+            tg = bg;
+            if (K >= 2) {
+                const u64 e = ENT(K - 2);
+                bp = (int)(e >> 32);
+                bg = E::g((int32_t)(e & 0xffffffffu), dy, dz);
+            }
+        }
+        ENT(K) = ((u64)(uint32_t)x << 32) | (uint32_t)pl;
+        bp = tp;
+        bg = tg;
+        tp = x;
+        tg = gx;
+        ++K;
+    }
+    // output: advance while x has passed the boundary to the next entry
+    int e = 0;
+    int cp = 0, np = 0;
+    int32_t cpl = 0, npl = 0;
+    double cg = 0.0, ng = 0.0;
+    if (K) {
+        const u64 c0 = ENT(0);
+        cp = (int)(c0 >> 32); cpl = (int32_t)(c0 & 0xffffffffu); cg = E::g(cpl, dy, dz);
+        if (K > 1) {
+            const u64 c1 = ENT(1);
+            np = (int)(c1 >> 32); npl = (int32_t)(c1 & 0xffffffffu); ng = E::g(npl, dy, dz);
+        }
+    }
+    for (int x = 0; x < L; ++x) {
+        const i64 o = base + (i64)x * stride;
+        if (K == 0) {
+            if (AXIS == 1) out32[o] = NONE32;
+            else out64[o] = INFINITY;
+            continue;
+        }
+        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+            ++e;
+            cp = np; cpl = npl; cg = ng;
+            if (e + 1 < K) {
+                const u64 c1 = ENT(e + 1);
+                np = (int)(c1 >> 32); npl = (int32_t)(c1 & 0xffffffffu); ng = E::g(npl, dy, dz);
+            }
+        }
+        if (AXIS == 1) {
+            out32[o] = pack(cp - x, cpl);
+        } else {
+            const double t0 = sq(__dmul_rn((double)(cp - x), dx));
+            const double t1 = sq(__dmul_rn((double)unpack_dj(cpl), dy));
+            const double t2 = sq(__dmul_rn((double)unpack_dk(cpl), dz));
+            out64[o] = __dsqrt_rn(__dadd_rn(__dadd_rn(t0, t1), t2));
+        }
+    }
+#undef ENT
 }
 
 }  // namespace
