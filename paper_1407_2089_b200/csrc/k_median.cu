@@ -234,20 +234,34 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 i0 = (tile / tj) * BTI, j0 = (tile % tj) * BTJ;
         __syncthreads();
-        // planes of the (BTI+2) x (BTJ+2) input rows (clamped), one warp per (row, word)
-        for (int u = wid; u < RI * RJ * W; u += 8) {
-            const int w = u % W, row = u / W;
-            const int rj = row % RJ, ri = row / RJ;
-            const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
-            const int k = 32 * w + lane;
-            const unsigned v = k < nz ? (unsigned)in[(i * ny + j) * nz + k] : 0u;
-            uint32_t mine = 0;
+        // planes of the (BTI+2) x (BTJ+2) input rows (clamped), one warp per
+        // (row, word); loads are batched 8 deep so their latencies overlap
+        for (int u0 = wid; u0 < RI * RJ * W; u0 += 8 * 8) {
+            unsigned vals[8];
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                const uint32_t word = __ballot_sync(0xffffffffu, (v >> b) & 1u);
-                if ((int)lane == b) mine = word;
+            for (int q = 0; q < 8; ++q) {
+                const int u = u0 + 8 * q;
+                vals[q] = 0u;
+                if (u < RI * RJ * W) {
+                    const int w = u % W, row = u / W;
+                    const int rj = row % RJ, ri = row / RJ;
+                    const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
+                    const int k = 32 * w + lane;
+                    if (k < nz) vals[q] = (unsigned)in[(i * ny + j) * nz + k];
+                }
             }
-            if ((int)lane < NB) planes[(row * W + w) * NB + lane] = mine;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int u = u0 + 8 * q;
+                if (u >= RI * RJ * W) break;
+                uint32_t mine = 0;
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    const uint32_t word = __ballot_sync(0xffffffffu, (vals[q] >> b) & 1u);
+                    if ((int)lane == b) mine = word;
+                }
+                if ((int)lane < NB) planes[u * NB + lane] = mine;
+            }
         }
         __syncthreads();
         for (int u = threadIdx.x; u < units; u += 256) {
