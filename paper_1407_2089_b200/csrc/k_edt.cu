@@ -169,7 +169,13 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
 }
 
 // ---------------------------------------------------------------------------
-// pass z: CTA = ZL consecutive (i,j) lines of nz <= 128 elements, all in SMEM
+// pass z: CTA = ZL consecutive (i,j) lines of nz <= 128 elements.
+//   phase 1 (all threads, coalesced): g = (di*dx)^2 + (dj*dy)^2 of every
+//            element into SMEM (+inf for no site);
+//   phase 2 (thread per line): envelope build with the top two costs in
+//            registers, stack of uint8 positions in SMEM;
+//   phase 3: distance sqrt(g_site + ((q-x)*dz)^2) -- g_site = t0 + t1, so this
+//            is ((t0 + t1) + t2), scipy's order -- written straight out.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double gyz(int32_t pl, double dx, double dy) {
     return __dadd_rn(sq(__dmul_rn((double)unpack_di(pl), dx)), sq(__dmul_rn((double)unpack_dj(pl), dy)));
@@ -179,60 +185,61 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
                                                  double dy, double dz, double *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char zsm[];
     const int S = nz + 1;                               // padded line stride (conflict-free)
-    int32_t *lin = (int32_t *)zsm;                      // [ZL][S]
-    uint8_t *stk = (uint8_t *)(lin + ZL * S);           // [ZL][nz] positions
-    double *res = (double *)(zsm + (((size_t)ZL * S * 4 + (size_t)ZL * nz + 15) & ~(size_t)15));  // [ZL][S]
+    double *gs = (double *)zsm;                         // [ZL][S]
+    uint8_t *stk = (uint8_t *)(gs + ZL * S);            // [ZL][nz] positions
     const i64 l0 = blockIdx.x * (i64)ZL;
     const int nl = (int)min((i64)ZL, nlines - l0);
     const int tot = nl * nz;
     const int32_t *src = in + l0 * nz;
     for (int idx = threadIdx.x; idx < tot; idx += ZL) {
         const int g = idx / nz, k = idx - g * nz;
-        lin[g * S + k] = src[idx];
+        const int32_t pl = src[idx];
+        gs[g * S + k] = pl == NONE32 ? INFINITY : gyz(pl, dx, dy);
     }
     __syncthreads();
     const int t = threadIdx.x;
-    if (t < nl) {
-        const int32_t *L = lin + t * S;
-        uint8_t *st = stk + t * nz;
-        double *R = res + t * S;
-        const double d2 = __dmul_rn(dz, dz);
-        int K = 0;
-        for (int x = 0; x < nz; ++x) {
-            if (L[x] == NONE32) continue;
-            const double gx = gyz(L[x], dx, dy);
-            while (K >= 2 && env_pop(x, gx, st[K - 1], gyz(L[st[K - 1]], dx, dy), st[K - 2],
-                                     gyz(L[st[K - 2]], dx, dy), d2))
-                --K;
-            st[K++] = (uint8_t)x;
-        }
-        int e = 0;
-        for (int x = 0; x < nz; ++x) {
-            if (K == 0) {
-                R[x] = INFINITY;
-                continue;
+    if (t >= nl) return;
+    const double *G = gs + t * S;
+    uint8_t *st = stk + t * nz;
+    const double d2 = __dmul_rn(dz, dz);
+    int K = 0, tp = 0, bp = 0;
+    double tg = 0.0, bg = 0.0;
+    for (int x = 0; x < nz; ++x) {
+        const double gx = G[x];
+        if (gx == INFINITY) continue;
+        while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+            --K;
+            tp = bp;
+            tg = bg;
+            if (K >= 2) {
+                bp = st[K - 2];
+                bg = G[bp];
             }
-            while (e + 1 < K && env_past(x, st[e + 1], gyz(L[st[e + 1]], dx, dy), st[e], gyz(L[st[e]], dx, dy), d2))
-                ++e;
-            const int q = st[e];
-            const int32_t pl = L[q];
-            const double t0 = sq(__dmul_rn((double)unpack_di(pl), dx));
-            const double t1 = sq(__dmul_rn((double)unpack_dj(pl), dy));
-            const double t2 = sq(__dmul_rn((double)(q - x), dz));
-            R[x] = __dsqrt_rn(__dadd_rn(__dadd_rn(t0, t1), t2));
         }
+        st[K++] = (uint8_t)x;
+        bp = tp; bg = tg; tp = x; tg = gx;
     }
-    __syncthreads();
-    double *dst = out + l0 * nz;
-    for (int idx = threadIdx.x; idx < tot; idx += ZL) {
-        const int g = idx / nz, k = idx - g * nz;
-        dst[idx] = res[g * S + k];
+    double *dst = out + (l0 + t) * nz;
+    if (K == 0) {
+        for (int x = 0; x < nz; ++x) dst[x] = INFINITY;
+        return;
+    }
+    int e = 0;
+    int cp = st[0], np = K > 1 ? st[1] : 0;
+    double cg = G[cp], ng = K > 1 ? G[np] : 0.0;
+    for (int x = 0; x < nz; ++x) {
+        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+            ++e;
+            cp = np; cg = ng;
+            if (e + 1 < K) { np = st[e + 1]; ng = G[np]; }
+        }
+        dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
     }
 }
 
 inline size_t zsmem(int nz) {
     const int S = nz + 1;
-    return (((size_t)ZL * S * 4 + (size_t)ZL * nz + 15) & ~(size_t)15) + (size_t)ZL * S * 8;
+    return (size_t)ZL * S * 8 + (size_t)ZL * nz + 16;
 }
 
 }  // namespace
