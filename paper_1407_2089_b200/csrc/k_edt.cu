@@ -105,6 +105,9 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
                                                  double dy, int32_t *__restrict__ out, u64 *__restrict__ spill) {
     __shared__ u64 stk[SC][LT];  // entry = (position << 32) | payload (di as uint16)
     const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
+    // lanes run data-dependent envelope loops; reconverge (wm) before every
+    // batched load and every store so the warp's accesses stay coalesced
+    const unsigned wm = __ballot_sync(0xffffffffu, l < nlines);
     if (l >= nlines) return;
     const i64 base = (l / nz) * (i64)ny * nz + (l % nz);
     const double d2 = __dmul_rn(dy, dy);
@@ -114,6 +117,7 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
     double tg = 0.0, bg = 0.0;
     for (int x0 = 0; x0 < ny; x0 += PF) {
         int16_t v[PF];
+        __syncwarp(wm);
 #pragma unroll
         for (int u = 0; u < PF; ++u) v[u] = x0 + u < ny ? di[base + (i64)(x0 + u) * nz] : NONE16;
 #pragma unroll
@@ -150,19 +154,20 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
     }
     for (int x = 0; x < ny; ++x) {
         const i64 o = base + (i64)x * nz;
-        if (K == 0) {
-            out[o] = NONE32;
-            continue;
-        }
-        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
-            ++e;
-            cp = np; cpl = npl; cg = ng;
-            if (e + 1 < K) {
-                const u64 c1 = ENT(e + 1);
-                np = (int)(c1 >> 32); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
+        int32_t r = NONE32;
+        if (K) {
+            while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+                ++e;
+                cp = np; cpl = npl; cg = ng;
+                if (e + 1 < K) {
+                    const u64 c1 = ENT(e + 1);
+                    np = (int)(c1 >> 32); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
+                }
             }
+            r = pack(cp - x, cpl);
         }
-        out[o] = pack(cp - x, cpl);
+        __syncwarp(wm);
+        out[o] = r;
     }
 #undef GOF
 #undef ENT
@@ -185,8 +190,9 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
                                                  double dy, double dz, double *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char zsm[];
     const int S = nz + 1;                               // padded line stride (conflict-free)
-    double *gs = (double *)zsm;                         // [ZL][S]
-    uint8_t *stk = (uint8_t *)(gs + ZL * S);            // [ZL][nz] positions
+    double *gs = (double *)zsm;                         // [ZL][S]   site costs (+inf: none)
+    uint8_t *stk = (uint8_t *)(gs + ZL * S);            // [ZL][S]   envelope positions
+    uint8_t *seg = stk + ZL * S;                        // [ZL][S]   chosen site per position
     const i64 l0 = blockIdx.x * (i64)ZL;
     const int nl = (int)min((i64)ZL, nlines - l0);
     const int tot = nl * nz;
@@ -198,48 +204,57 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
     }
     __syncthreads();
     const int t = threadIdx.x;
-    if (t >= nl) return;
-    const double *G = gs + t * S;
-    uint8_t *st = stk + t * nz;
-    const double d2 = __dmul_rn(dz, dz);
-    int K = 0, tp = 0, bp = 0;
-    double tg = 0.0, bg = 0.0;
-    for (int x = 0; x < nz; ++x) {
-        const double gx = G[x];
-        if (gx == INFINITY) continue;
-        while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-            --K;
-            tp = bp;
-            tg = bg;
-            if (K >= 2) {
-                bp = st[K - 2];
-                bg = G[bp];
+    if (t < nl) {
+        const double *G = gs + t * S;
+        uint8_t *st = stk + t * S;
+        uint8_t *sg = seg + t * S;
+        const double d2 = __dmul_rn(dz, dz);
+        int K = 0, tp = 0, bp = 0;
+        double tg = 0.0, bg = 0.0;
+        for (int x = 0; x < nz; ++x) {
+            const double gx = G[x];
+            if (gx == INFINITY) continue;
+            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+                --K;
+                tp = bp;
+                tg = bg;
+                if (K >= 2) {
+                    bp = st[K - 2];
+                    bg = G[bp];
+                }
+            }
+            st[K++] = (uint8_t)x;
+            bp = tp; bg = tg; tp = x; tg = gx;
+        }
+        if (K == 0) {
+            for (int x = 0; x < nz; ++x) sg[x] = 0xff;
+        } else {
+            int e = 0;
+            int cp = st[0], np = K > 1 ? st[1] : 0;
+            double cg = G[cp], ng = K > 1 ? G[np] : 0.0;
+            for (int x = 0; x < nz; ++x) {
+                while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+                    ++e;
+                    cp = np; cg = ng;
+                    if (e + 1 < K) { np = st[e + 1]; ng = G[np]; }
+                }
+                sg[x] = (uint8_t)cp;
             }
         }
-        st[K++] = (uint8_t)x;
-        bp = tp; bg = tg; tp = x; tg = gx;
     }
-    double *dst = out + (l0 + t) * nz;
-    if (K == 0) {
-        for (int x = 0; x < nz; ++x) dst[x] = INFINITY;
-        return;
-    }
-    int e = 0;
-    int cp = st[0], np = K > 1 ? st[1] : 0;
-    double cg = G[cp], ng = K > 1 ? G[np] : 0.0;
-    for (int x = 0; x < nz; ++x) {
-        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
-            ++e;
-            cp = np; cg = ng;
-            if (e + 1 < K) { np = st[e + 1]; ng = G[np]; }
-        }
-        dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
+    __syncthreads();
+    // cooperative coalesced output: sqrt(g_site + ((q-x)*dz)^2) = sqrt((t0+t1)+t2)
+    double *dst = out + l0 * nz;
+    for (int idx = threadIdx.x; idx < tot; idx += ZL) {
+        const int g = idx / nz, x = idx - g * nz;
+        const int q = seg[g * S + x];
+        dst[idx] = q == 0xff ? INFINITY : __dsqrt_rn(__dadd_rn(gs[g * S + q], sq(__dmul_rn((double)(q - x), dz))));
     }
 }
 
 inline size_t zsmem(int nz) {
     const int S = nz + 1;
-    return (size_t)ZL * S * 8 + (size_t)ZL * nz + 16;
+    return (size_t)ZL * S * 8 + 2 * (size_t)ZL * S + 16;
 }
 
 }  // namespace

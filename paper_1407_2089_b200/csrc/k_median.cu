@@ -199,10 +199,11 @@ __device__ __forceinline__ u64 transpose8(u64 x) {
 }
 
 // voxel values 8g..8g+7 of a word from 8 planes p[0..7] (bytes, little endian)
-__device__ __forceinline__ u64 planes_to_bytes(const uint32_t *p, int g) {
+__device__ __forceinline__ u64 planes_to_bytes(uint32_t p0, uint32_t p1, uint32_t p2, uint32_t p3, uint32_t p4,
+                                               uint32_t p5, uint32_t p6, uint32_t p7, int g) {
     const unsigned sel = (unsigned)g | ((unsigned)(4 + g) << 4);
-    const uint32_t a01 = __byte_perm(p[0], p[1], sel), a23 = __byte_perm(p[2], p[3], sel);
-    const uint32_t a45 = __byte_perm(p[4], p[5], sel), a67 = __byte_perm(p[6], p[7], sel);
+    const uint32_t a01 = __byte_perm(p0, p1, sel), a23 = __byte_perm(p2, p3, sel);
+    const uint32_t a45 = __byte_perm(p4, p5, sel), a67 = __byte_perm(p6, p7, sel);
     const uint32_t lo = __byte_perm(a01, a23, 0x5410), hi = __byte_perm(a45, a67, 0x5410);
     return transpose8(((u64)hi << 32) | lo);
 }
@@ -213,8 +214,14 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
     extern __shared__ __align__(16) unsigned char dsm[];
     const int W = (nz + 31) >> 5;
     const int RI = BTI + 2, RJ = BTJ + 2;
-    uint32_t *planes = (uint32_t *)dsm;  // [RI*RJ][W][NB]
-    const size_t pbytes = (size_t)RI * RJ * W * NB * 4;
+    const int NW = RI * RJ * W;  // staged (row, word) units
+    // planes stored [b][unit] so a warp's 32 units hit 32 banks; three
+    // versions per word: value at k, at k-1 and at k+1 (clamped at the ends)
+    uint32_t *pc = (uint32_t *)dsm;   // [NB][NW]
+    uint32_t *pm = pc + NB * NW;      // [NB][NW]
+    uint32_t *pp = pm + NB * NW;      // [NB][NW]
+    uint32_t *s_any = pp + NB * NW;   // planes non-zero in this tile
+    const size_t pbytes = ((size_t)3 * NB * NW * 4 + 16 + 15) & ~(size_t)15;
     constexpr bool BYTE = NB == 8;
     ct::ByteHist256 bh;
     uint32_t *sh16 = nullptr;
@@ -234,15 +241,16 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 i0 = (tile / tj) * BTI, j0 = (tile % tj) * BTJ;
         __syncthreads();
-        // planes of the (BTI+2) x (BTJ+2) input rows (clamped), one warp per
-        // (row, word); loads are batched 8 deep so their latencies overlap
-        for (int u0 = wid; u0 < RI * RJ * W; u0 += 8 * 8) {
+        if (threadIdx.x == 0) *s_any = 0;
+        // phase A: planes of the (BTI+2) x (BTJ+2) input rows (clamped), one warp
+        // per (row, word); loads batched 8 deep so their latencies overlap
+        for (int u0 = wid; u0 < NW; u0 += 8 * 8) {
             unsigned vals[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int u = u0 + 8 * q;
                 vals[q] = 0u;
-                if (u < RI * RJ * W) {
+                if (u < NW) {
                     const int w = u % W, row = u / W;
                     const int rj = row % RJ, ri = row / RJ;
                     const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
@@ -250,25 +258,53 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                     if (k < nz) vals[q] = (unsigned)in[(i * ny + j) * nz + k];
                 }
             }
+            unsigned any = 0;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int u = u0 + 8 * q;
-                if (u >= RI * RJ * W) break;
+                if (u >= NW) break;
                 uint32_t mine = 0;
 #pragma unroll
                 for (int b = 0; b < NB; ++b) {
                     const uint32_t word = __ballot_sync(0xffffffffu, (vals[q] >> b) & 1u);
                     if ((int)lane == b) mine = word;
                 }
-                if ((int)lane < NB) planes[u * NB + lane] = mine;
+                if ((int)lane < NB) {
+                    pc[lane * NW + u] = mine;
+                    any |= mine ? (1u << lane) : 0u;
+                }
             }
+            if (any) atomicOr(s_any, any);
         }
         __syncthreads();
+        // phase B: shifted versions (k-1 and k+1 neighbours, clamp-to-edge)
+        for (int e = threadIdx.x; e < NB * NW; e += 256) {
+            const int u = e % NW;
+            const int w = u % W;
+            const uint32_t P = pc[e];
+            const uint32_t Pm = w > 0 ? pc[e - 1] : 0u, Pn = w + 1 < W ? pc[e + 1] : 0u;
+            uint32_t km1 = (P << 1) | (Pm >> 31);
+            if (w == 0) km1 |= P & 1u;  // k = -1 clamps to k = 0
+            uint32_t kp1 = (P >> 1) | (Pn << 31);
+            if (w == last_w) {          // k = nz clamps to k = nz-1
+                const uint32_t m = 1u << last_pos;
+                kp1 = (kp1 & ~m) | (P & m);
+            }
+            pm[e] = km1;
+            pp[e] = kp1;
+        }
+        __syncthreads();
+        const uint32_t any = *s_any;
         for (int u = threadIdx.x; u < units; u += 256) {
             const int w = u % W, r = u / W;
             const int lj = r % BTJ, li = r / BTJ;
             const i64 i = i0 + li, j = j0 + lj;
             if (i >= nx || j >= ny) continue;
+            int rows[9];
+#pragma unroll
+            for (int di = 0; di < 3; ++di)
+#pragma unroll
+                for (int dj = 0; dj < 3; ++dj) rows[di * 3 + dj] = ((li + di) * RJ + (lj + dj)) * W + w;
             uint32_t eq[27];
 #pragma unroll
             for (int e = 0; e < 27; ++e) eq[e] = 0xffffffffu;
@@ -276,40 +312,27 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
             uint32_t med[NB];
 #pragma unroll
             for (int b = NB - 1; b >= 0; --b) {
+                med[b] = 0u;
+                if (!((any >> b) & 1u)) continue;  // all-zero plane: median bit 0, nothing pruned
                 uint32_t wv[27];
 #pragma unroll
-                for (int di = 0; di < 3; ++di)
-#pragma unroll
-                    for (int dj = 0; dj < 3; ++dj) {
-                        const int row = (li + di) * RJ + (lj + dj);
-                        const uint32_t P = planes[(row * W + w) * NB + b];
-                        const uint32_t Pm = w > 0 ? planes[(row * W + w - 1) * NB + b] : 0u;
-                        const uint32_t Pp = w + 1 < W ? planes[(row * W + w + 1) * NB + b] : 0u;
-                        uint32_t km1 = (P << 1) | (Pm >> 31);
-                        if (w == 0) km1 |= P & 1u;  // k = -1 clamps to k = 0
-                        uint32_t kp1 = (P >> 1) | (Pp << 31);
-                        if (w == last_w) {          // k = nz clamps to k = nz-1
-                            const uint32_t m = 1u << last_pos;
-                            kp1 = (kp1 & ~m) | (P & m);
-                        }
-                        const int e = (di * 3 + dj) * 3;
-                        wv[e] = km1;
-                        wv[e + 1] = P;
-                        wv[e + 2] = kp1;
-                    }
+                for (int r9 = 0; r9 < 9; ++r9) {
+                    const int e = b * NW + rows[r9];
+                    wv[3 * r9] = pm[e];
+                    wv[3 * r9 + 1] = pc[e];
+                    wv[3 * r9 + 2] = pp[e];
+                }
                 uint32_t t[27];
 #pragma unroll
                 for (int e = 0; e < 27; ++e) t[e] = eq[e] & ~wv[e];
                 uint32_t c[5];
                 count27(t, c);
-                // gt = c > k
                 uint32_t gt = 0, same = 0xffffffffu;
 #pragma unroll
                 for (int q = 4; q >= 0; --q) {
                     gt |= same & c[q] & ~kr[q];
                     same &= ~(c[q] ^ kr[q]);
                 }
-                // k = gt ? k : k - c
                 uint32_t br = 0;
 #pragma unroll
                 for (int q = 0; q < 5; ++q) {
@@ -317,53 +340,53 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                     br = (~kr[q] & c[q]) | (~(kr[q] ^ c[q]) & br);
                     kr[q] = (gt & kr[q]) | (~gt & d);
                 }
-                const uint32_t mb = ~gt;  // median bit
+                const uint32_t mb = ~gt;
                 med[b] = mb;
 #pragma unroll
                 for (int e = 0; e < 27; ++e) eq[e] &= ~(wv[e] ^ mb);
             }
-            // planes -> values, store, histogram
             const i64 p0 = (i * ny + j) * nz + 32 * w;
             const int nv = min(32, nz - 32 * w);
-            unsigned char vals8[32];
-            uint16_t vals16[32];
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const u64 lo = planes_to_bytes(med, g);
-                if (NB == 8) {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) vals8[8 * g + q] = (unsigned char)(lo >> (8 * q));
-                } else {
-                    const u64 hi = planes_to_bytes(med + 8, g);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        vals16[8 * g + q] = (uint16_t)(((lo >> (8 * q)) & 0xFF) | (((hi >> (8 * q)) & 0xFF) << 8));
-                }
-            }
             if (NB == 8) {
+                u64 g8[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) g8[g] = planes_to_bytes(med[0], med[1], med[2], med[3], med[4], med[5], med[6], med[7], g);
                 if (nv == 32 && (p0 & 15) == 0) {
                     uint4 *dst = reinterpret_cast<uint4 *>(out + p0);
-                    dst[0] = *reinterpret_cast<const uint4 *>(vals8);
-                    dst[1] = *reinterpret_cast<const uint4 *>(vals8 + 16);
-                } else {
-                    for (int q = 0; q < nv; ++q) out[p0 + q] = (T)vals8[q];
-                }
-                if (ghist)
-                    for (int q = 0; q < nv; ++q) bh.add(vals8[q]);
-            } else {
-                if (nv == 32 && (p0 & 7) == 0) {
-                    uint4 *dst = reinterpret_cast<uint4 *>(out + p0);
+                    dst[0] = make_uint4((uint32_t)g8[0], (uint32_t)(g8[0] >> 32), (uint32_t)g8[1], (uint32_t)(g8[1] >> 32));
+                    dst[1] = make_uint4((uint32_t)g8[2], (uint32_t)(g8[2] >> 32), (uint32_t)g8[3], (uint32_t)(g8[3] >> 32));
+                    if (ghist) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) dst[q] = *reinterpret_cast<const uint4 *>(vals16 + 8 * q);
+                        for (int q = 0; q < 32; ++q) bh.add((int)((g8[q >> 3] >> (8 * (q & 7))) & 0xFF));
+                    }
                 } else {
-                    for (int q = 0; q < nv; ++q) out[p0 + q] = (T)vals16[q];
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        if (q >= nv) break;
+                        const int v = (int)((g8[q >> 3] >> (8 * (q & 7))) & 0xFF);
+                        out[p0 + q] = (T)v;
+                        if (ghist) bh.add(v);
+                    }
                 }
-                if (ghist)
-                    for (int q = 0; q < nv; ++q) {
-                        const int v = vals16[q];
+            } else {
+                u64 lo8[4], hi8[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    lo8[g] = planes_to_bytes(med[0], med[1], med[2], med[3], med[4], med[5], med[6], med[7], g);
+                    hi8[g] = planes_to_bytes(med[8 % NB], med[9 % NB], med[10 % NB], med[11 % NB], med[12 % NB],
+                                             med[13 % NB], med[14 % NB], med[15 % NB], g);
+                }
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    if (q >= nv) break;
+                    const int v = (int)(((lo8[q >> 3] >> (8 * (q & 7))) & 0xFF) |
+                                        (((hi8[q >> 3] >> (8 * (q & 7))) & 0xFF) << 8));
+                    out[p0 + q] = (T)v;
+                    if (ghist) {
                         if (v < 4096) atomicAdd(&sh16[v], 1u);
                         else atomicAdd((unsigned long long *)&ghist[v], 1ull);
                     }
+                }
             }
         }
         if (BYTE && ghist) {
@@ -483,7 +506,8 @@ extern "C" int ct_median(const void *in, int dtype, int64_t nx, int64_t ny, int6
     }
     if (radius == 1 && (dtype == CT_U8 || dtype == CT_U16) && nz <= 128) {
         const int W = (int)((nz + 31) / 32);
-        const size_t pbytes = (size_t)(BTI + 2) * (BTJ + 2) * W * (dtype == CT_U8 ? 8 : 16) * 4;
+        const size_t NW = (size_t)(BTI + 2) * (BTJ + 2) * W;
+        const size_t pbytes = ((size_t)3 * (dtype == CT_U8 ? 8 : 16) * NW * 4 + 16 + 15) & ~(size_t)15;
         const size_t sm = pbytes + (dtype == CT_U8 ? ct::ByteHist256::kBytes : 4096 * 4);
         const i64 tiles = ((nx + BTI - 1) / BTI) * ((ny + BTJ - 1) / BTJ);
         const int grid = (int)min(tiles, (i64)CT_NUM_SMS * 2);

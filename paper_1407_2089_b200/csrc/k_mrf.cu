@@ -149,6 +149,19 @@ struct StepElem {  // (proposal - original)^2 for the step from `cur` (nullptr =
     }
 };
 
+// (lap - mean)^2 from the int32 Laplacian array of the streaming pass;
+// mean = exact_sum / n (numpy's pairwise sum of integer-valued doubles is exact)
+struct LapArrSq {
+    const int32_t *lap;
+    const long long *int_sum;
+    i64 n;
+    __device__ double operator()(i64 e) const {
+        const double m = __ddiv_rn((double)*int_sum, (double)n);
+        const double x = __dadd_rn((double)lap[e], -m);
+        return __dmul_rn(x, x);
+    }
+};
+
 // numpy pairwise_sum leaf (n <= 128) over an SMEM array
 __device__ double pw_leaf(const double *a, int n) {
     if (n < 8) {
@@ -169,64 +182,111 @@ __device__ double pw_leaf(const double *a, int n) {
     return res;
 }
 
-// CTA b: exact numpy-order sum of depth-D node b; elements staged in SMEM.
+// Leaf lookup inside a subtree without enumeration: node sizes at each depth
+// of a subtree form a tiny set, so leaf counts per size are tabulated once per
+// CTA (thread 0, a few dozen entries) and every thread descends to its leaf.
+constexpr int PW_MAXD = 8;    // subtree depth (size <= ~16K elements -> <= 7 levels)
+constexpr int PW_MAXS = 8;    // distinct sizes per level
+
+struct PwShape {
+    int ns[PW_MAXD + 1];                 // distinct sizes per depth
+    int size[PW_MAXD + 1][PW_MAXS];
+    int leaves[PW_MAXD + 1][PW_MAXS];
+    int depth;                           // deepest level holding a leaf
+};
+
+__device__ int pw_lookup(const PwShape &sh, int d, int m) {
+    for (int q = 0; q < sh.ns[d]; ++q)
+        if (sh.size[d][q] == m) return sh.leaves[d][q];
+    return 1;
+}
+
+__device__ void pw_shape(PwShape &sh, int m0) {
+    sh.ns[0] = 1;
+    sh.size[0][0] = m0;
+    int d = 0;
+    for (; d < PW_MAXD; ++d) {
+        int nn = 0;
+        for (int q = 0; q < sh.ns[d]; ++q) {
+            const int m = sh.size[d][q];
+            if (m <= 128) continue;
+            const int c[2] = {(int)pw_left(m), m - (int)pw_left(m)};
+            for (int h = 0; h < 2; ++h) {
+                bool seen = false;
+                for (int u = 0; u < nn; ++u) seen |= sh.size[d + 1][u] == c[h];
+                if (!seen && nn < PW_MAXS) sh.size[d + 1][nn++] = c[h];
+            }
+        }
+        sh.ns[d + 1] = nn;
+        if (!nn) break;
+    }
+    sh.depth = d;
+    for (int e = d; e >= 0; --e)
+        for (int q = 0; q < sh.ns[e]; ++q) {
+            const int m = sh.size[e][q];
+            sh.leaves[e][q] = m <= 128 ? 1 : pw_lookup(sh, e + 1, (int)pw_left(m)) +
+                                                 pw_lookup(sh, e + 1, m - (int)pw_left(m));
+        }
+}
+
+// CTA b: exact numpy-order sum of depth-D node b.  Elements staged in SMEM;
+// leaf t found by descending with the tabulated leaf counts; internal nodes
+// combined level by level (slot = path bits at that depth), so every add is
+// left + right exactly as numpy's recursion performs it.
 template <class F>
 __global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__restrict__ partial) {
     extern __shared__ double vals[];
-    __shared__ int loff[MAX_LEAVES], llen[MAX_LEAVES];
-    __shared__ double lsum[MAX_LEAVES];
+    __shared__ PwShape sh;
+    __shared__ double lv[2][1 << PW_MAXD];  // values per level slot (ping-pong)
     __shared__ int nleaves;
     i64 off, len;
     pw_node(n, D, blockIdx.x, off, len);
     for (int i = threadIdx.x; i < len; i += PT) vals[i] = f(off + i);
     if (threadIdx.x == 0) {
-        // enumerate leaves in order (explicit DFS stack, right child pushed first)
-        i64 so[64], sl[64];
-        int sp = 0, nl = 0;
-        so[sp] = 0; sl[sp] = len; ++sp;
-        while (sp) {
-            --sp;
-            const i64 o = so[sp], l = sl[sp];
-            if (l <= 128) {
-                loff[nl] = (int)o; llen[nl] = (int)l; ++nl;
-            } else {
-                const i64 h = pw_left(l);
-                so[sp] = o + h; sl[sp] = l - h; ++sp;
-                so[sp] = o; sl[sp] = h; ++sp;
-            }
-        }
-        nleaves = nl;
+        pw_shape(sh, (int)len);
+        nleaves = sh.leaves[0][0];
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < nleaves; e += PT) lsum[e] = pw_leaf(vals + loff[e], llen[e]);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        // recombine in recursion order: post-order evaluation with a value stack
-        i64 sl[64];
-        int st[64];
-        double vs[64];
-        int sp = 0, vp = 0, leaf = 0;
-        sl[sp] = len; st[sp] = 0; ++sp;
-        while (sp) {
-            const int top = sp - 1;
-            const i64 l = sl[top];
-            if (l <= 128) {
-                vs[vp++] = lsum[leaf++];
-                --sp;
-            } else if (st[top] == 0) {
-                st[top] = 1;
-                sl[sp] = pw_left(l); st[sp] = 0; ++sp;
-            } else if (st[top] == 1) {
-                st[top] = 2;
-                sl[sp] = l - pw_left(l); st[sp] = 0; ++sp;
-            } else {
-                const double b = vs[--vp], a = vs[--vp];
-                vs[vp++] = __dadd_rn(a, b);
-                --sp;
-            }
+    // leaves: thread t takes leaf t, recording its depth and path slot
+    int my_depth = -1, my_slot = 0;
+    double my_val = 0.0;
+    if (threadIdx.x < nleaves) {
+        int t = threadIdx.x, o = 0, m = (int)len, d = 0, slot = 0;
+        while (m > 128) {
+            const int l = (int)pw_left(m);
+            const int nl = pw_lookup(sh, d + 1, l);
+            slot <<= 1;
+            if (t < nl) m = l;
+            else { t -= nl; o += l; m -= l; slot |= 1; }
+            ++d;
         }
-        partial[blockIdx.x] = vs[0];
+        my_val = pw_leaf(vals + o, m);
+        my_depth = d;
+        my_slot = slot;
     }
+    // combine bottom-up: at depth d, slots of existing nodes; a node at depth d
+    // is a leaf (value from its thread) or internal (children at d+1)
+    const int dmax = sh.depth;
+    double *cur = lv[0], *nxt = lv[1];
+    for (int d = dmax; d >= 0; --d) {
+        // nodes at depth d: write leaves of this depth, combine internal ones
+        __syncthreads();
+        if (my_depth == d) nxt[my_slot] = my_val;
+        // internal nodes at depth d combine children (depth d+1 values in cur)
+        for (int sl = threadIdx.x; sl < (1 << d); sl += PT) {
+            // descend the path of slot sl to learn whether it exists / is internal
+            int m = (int)len;
+            bool exists = true;
+            for (int e = d - 1; e >= 0 && exists; --e) {
+                if (m <= 128) exists = false;
+                else m = ((sl >> e) & 1) ? m - (int)pw_left(m) : (int)pw_left(m);
+            }
+            if (exists && m > 128) nxt[sl] = __dadd_rn(cur[2 * sl], cur[2 * sl + 1]);
+        }
+        double *tmp = cur; cur = nxt; nxt = tmp;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) partial[blockIdx.x] = cur[0];
 }
 
 // fold 2^D partials pairwise (complete binary tree above depth D); partial
@@ -327,6 +387,127 @@ __global__ void __launch_bounds__(256) mrf_stats_int(const T *__restrict__ v, i6
             bh.flush();
             since_flush = 0;
         }
+    }
+    for (int o = 16; o; o >>= 1) {
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&scal[W_NNZ], nnz);
+        atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
+    }
+    if (BYTE) {
+        bh.flush();
+        bh.to_global(ghist);
+    } else {
+        __syncthreads();
+        for (int b = threadIdx.x; b < 4096; b += 256)
+            if (sh16[b]) atomicAdd(&ghist[b], (unsigned long long)sh16[b]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Streaming statistics pass (integer input): a CTA owns MJ rows (j) x all k
+// and walks a chunk of planes along i with a 3-plane SMEM ring (the load of
+// plane i+2 is issued before plane i is processed, so its latency hides
+// behind compute; one barrier per plane).  Per voxel: histogram (byte
+// counters for u8, SMEM atomics for u16), sign sum != 0, and for interior
+// voxels the Laplacian -> exact int64 sum + int32 array in numpy's flattened
+// interior order.
+// ---------------------------------------------------------------------------
+constexpr int MJ = 8;
+constexpr int MIPER = 64;  // planes per CTA
+
+template <typename T>
+__global__ void __launch_bounds__(256) mrf_stream_int(const T *__restrict__ v, i64 nx, i64 ny, int nz,
+                                                      unsigned long long *__restrict__ ghist,
+                                                      unsigned long long *__restrict__ scal,
+                                                      int32_t *__restrict__ lap) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int PL = (MJ + 2) * nz;  // staged plane elements
+    int *ring = (int *)dsm;        // [3][PL]
+    unsigned char *hbase = dsm + ((3 * PL * 4 + 15) & ~15);
+    constexpr bool BYTE = sizeof(T) == 1;
+    ct::ByteHist256 bh;
+    uint32_t *sh16 = nullptr;
+    if (BYTE) bh.init(hbase);
+    else {
+        sh16 = (uint32_t *)hbase;
+        for (int b = threadIdx.x; b < 4096; b += 256) sh16[b] = 0;
+    }
+    const i64 nJ = (ny + MJ - 1) / MJ;
+    const i64 j0 = (blockIdx.x % nJ) * MJ;
+    const i64 i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
+    const i64 my = ny - 2, mz = nz - 2;
+    const int npos = MJ * nz;
+    // thread positions (<= 4 per thread for nz <= 128)
+    constexpr int MAXP = 4;
+    int pj[MAXP], pk[MAXP];
+    int np_ = 0;
+    for (int p = threadIdx.x; p < npos && np_ < MAXP; p += 256, ++np_) {
+        pj[np_] = p / nz;
+        pk[np_] = p - pj[np_] * nz;
+    }
+    auto load_plane = [&](i64 i, int *regs) {
+        const i64 ic = ct::clampi(i, 0, nx - 1);
+        int q = 0;
+        for (int e = threadIdx.x; e < PL; e += 256, ++q) {
+            const int r = e / nz, k = e - r * nz;
+            const i64 j = ct::clampi(j0 - 1 + r, 0, ny - 1);
+            regs[q] = (int)v[(ic * ny + j) * nz + k];
+        }
+    };
+    auto store_plane = [&](int slot, const int *regs) {
+        int q = 0;
+        for (int e = threadIdx.x; e < PL; e += 256, ++q) ring[slot * PL + e] = regs[q];
+    };
+    constexpr int MAXR = (MJ + 2) * 128 / 256 + 1;
+    int regs[MAXR];
+    // prologue: planes i0-1 (prev values) and i0, i0+1 into the ring
+    load_plane(i0 - 1, regs);
+    store_plane(2, regs);
+    load_plane(i0, regs);
+    store_plane(0, regs);
+    load_plane(i0 + 1, regs);
+    store_plane(1, regs);
+    __syncthreads();
+    int prev[MAXP];
+    for (int q = 0; q < np_; ++q) prev[q] = ring[2 * PL + (pj[q] + 1) * nz + pk[q]];
+    unsigned long long nnz = 0;
+    long long lsum = 0;
+    int since = 0;
+    for (i64 i = i0; i < i1; ++i) {
+        const int cs = (int)((i - i0) % 3), ns = (int)((i - i0 + 1) % 3), fs = (int)((i - i0 + 2) % 3);
+        load_plane(i + 2, regs);  // in flight while plane i is processed
+        const int *C = ring + cs * PL, *X = ring + ns * PL;
+        const bool iint = i > 0 && i < nx - 1;
+        for (int q = 0; q < np_; ++q) {
+            const int jj = pj[q], k = pk[q];
+            const i64 j = j0 + jj;
+            if (j >= ny) continue;
+            const int c = C[(jj + 1) * nz + k];
+            const int xm = prev[q], xp = X[(jj + 1) * nz + k];
+            const int ym = C[jj * nz + k], yp = C[(jj + 2) * nz + k];
+            const int zm = k > 0 ? C[(jj + 1) * nz + k - 1] : c, zp = k < nz - 1 ? C[(jj + 1) * nz + k + 1] : c;
+            const int sgs = ((xm > c) - (xm < c)) + ((c > xp) - (c < xp)) + ((ym > c) - (ym < c)) +
+                            ((c > yp) - (c < yp)) + ((zm > c) - (zm < c)) + ((c > zp) - (c < zp));
+            nnz += sgs != 0;
+            if (iint && j > 0 && j < ny - 1 && k > 0 && k < nz - 1) {
+                const int l = (xm + xp + ym + yp + zm + zp) - 6 * c;
+                lsum += l;
+                lap[((i - 1) * my + (j - 1)) * mz + (k - 1)] = l;
+            }
+            if (BYTE) bh.add(c);
+            else if (c < 4096) atomicAdd(&sh16[c], 1u);
+            else atomicAdd(&ghist[c], 1ull);
+            prev[q] = c;
+        }
+        store_plane(fs, regs);
+        if (BYTE && ++since == 60) {  // <= 60 * MAXP adds per thread between flushes
+            bh.flush();
+            since = 0;
+        }
+        __syncthreads();
     }
     for (int o = 16; o; o >>= 1) {
         nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
@@ -459,6 +640,7 @@ __global__ void step_finish(double *out2, const unsigned long long *moved) {
 }
 
 struct MrfWork {
+    int32_t *lap;              // integer path: n_interior Laplacians
     double *partial;           // 2 * 2^D
     unsigned long long *scal;  // W_WORDS
     double *sorted;            // float path: n
@@ -474,9 +656,18 @@ size_t cub_sort_bytes(i64 n) {
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-MrfWork mrf_carve(void *work, i64 n, int dtype) {
+inline i64 interior(i64 nx, i64 ny, i64 nz) {
+    return (nx > 2 ? nx - 2 : 0) * (ny > 2 ? ny - 2 : 0) * (nz > 2 ? nz - 2 : 0);
+}
+
+MrfWork mrf_carve(void *work, i64 n, int dtype, i64 ni) {
     MrfWork w;
     char *p = (char *)work;
+    w.lap = nullptr;
+    if (dtype != CT_F64) {
+        w.lap = (int32_t *)p;
+        p += al(ni * 4);
+    }
     const i64 parts = 1ll << pw_depth(n > 0 ? n : 1);
     w.partial = (double *)p; p += al(parts * 8 * 2 + 64);
     w.scal = (unsigned long long *)p; p += al(W_WORDS * 8);
@@ -493,17 +684,22 @@ template <typename T>
 int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint64_t *hist, cudaStream_t s) {
     const i64 mx = nx - 2 > 0 ? nx - 2 : 0, my = ny - 2 > 0 ? ny - 2 : 0, mz = nz - 2 > 0 ? nz - 2 : 0;
     const i64 ni = mx * my * mz;
-    const size_t sm = (STI + 2) * (STJ + 2) * (STK + 2) * sizeof(int) +
-                      (sizeof(T) == 1 ? ct::ByteHist256::kBytes : 4096 * sizeof(uint32_t));
-    cudaFuncSetAttribute(mrf_stats_int<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    const i64 tiles = ((nz + STK - 1) / STK) * ((ny + STJ - 1) / STJ) * ((nx + STI - 1) / STI);
-    mrf_stats_int<T><<<(int)min(tiles, (i64)CT_NUM_SMS * 2), 256, sm, s>>>(v, nx, ny, nz,
-                                                                         (unsigned long long *)hist, w.scal);
-    if (int st = ct::check_launch("mrf_stats_int")) return st;
+    const size_t hb = sizeof(T) == 1 ? ct::ByteHist256::kBytes : 4096 * sizeof(uint32_t);
+    if (nz <= 128) {
+        const size_t sm = ((3 * (MJ + 2) * nz * 4 + 15) & ~(size_t)15) + hb;
+        cudaFuncSetAttribute(mrf_stream_int<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const i64 blocks = ((ny + MJ - 1) / MJ) * ((nx + MIPER - 1) / MIPER);
+        mrf_stream_int<T><<<(unsigned)blocks, 256, sm, s>>>(v, nx, ny, (int)nz, (unsigned long long *)hist, w.scal,
+                                                           w.lap);
+        if (int st = ct::check_launch("mrf_stream_int")) return st;
+    } else {
+        ct::set_error("integer MRF supports nz <= 128");
+        return CT_ERR_UNSUPPORTED;
+    }
     delta_from_hist<<<1, 1024, 0, s>>>(hist, state);
     if (int st = ct::check_launch("delta_from_hist")) return st;
     if (ni >= 2) {
-        LapElem<T> f{v, ny, nz, (uint32_t)my, (uint32_t)mz, nullptr, (const long long *)&w.scal[W_LAPSUM], ni, 1};
+        LapArrSq f{w.lap, (const long long *)&w.scal[W_LAPSUM], ni};
         if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s)) return st;
     }
     mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 1);
@@ -540,6 +736,7 @@ size_t ct_mrf_workspace(int64_t nx, int64_t ny, int64_t nz, int dtype) {
     const i64 n = nx * ny * nz;
     const i64 parts = 1ll << pw_depth(n > 0 ? n : 1);
     size_t b = al(parts * 8 * 2 + 64) + al(W_WORDS * 8);
+    if (dtype != CT_F64) b += al(interior(nx, ny, nz) * 4);
     if (dtype == CT_F64) b += al(n * 8) + al(cub_sort_bytes(n));
     return b + 1024;
 }
@@ -560,7 +757,7 @@ extern "C" int ct_mrf(const void *in, int dtype, int64_t nx, int64_t ny, int64_t
         ct::set_error("integer MRF needs a (zeroed) histogram buffer");
         return CT_ERR_PARAM;
     }
-    MrfWork w = mrf_carve(work, n, dtype);
+    MrfWork w = mrf_carve(work, n, dtype, interior(nx, ny, nz));
     cudaMemsetAsync(state, 0, S_WORDS * sizeof(double), s);
     cudaMemsetAsync(w.scal, 0, W_WORDS * 8, s);
     cudaMemsetAsync(&w.scal[W_BEST_BITS], 0xff, 8, s);
@@ -578,7 +775,7 @@ extern "C" int ct_mrf_step(const void *in, int dtype, int64_t nx, int64_t ny, in
                            const double *state, double *next, void *work, double *out2, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const i64 n = nx * ny * nz;
-    MrfWork w = mrf_carve(work, n, dtype);
+    MrfWork w = mrf_carve(work, n, dtype, interior(nx, ny, nz));
     cudaMemsetAsync(&w.scal[W_MOVED], 0, 8, s);
     CT_DISPATCH(dtype, T, {
         const T *v = (const T *)in;
