@@ -29,7 +29,7 @@ namespace {
 
 constexpr int16_t NONE16 = INT16_MIN;
 constexpr int32_t NONE32 = INT32_MIN;
-constexpr int SC = 16;   // SMEM stack entries per thread (pass y)
+constexpr int SC = 48;   // SMEM stack entries per thread (pass y)
 constexpr int LT = 256;  // threads per pass-x / pass-y CTA
 constexpr int PF = 16;   // prefetch depth (positions)
 constexpr int ZL = 128;  // lines per pass-z CTA
@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(LT) edt_pass_x(const uint8_t *__restrict__ mas
 // pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di, i64 nlines, int ny, int nz, double dx,
-                                                 double dy, int32_t *__restrict__ out, u64 *__restrict__ spill) {
-    __shared__ u64 stk[SC][LT];  // entry = (position << 32) | payload (di as uint16)
+                                                 double dy, int32_t *__restrict__ out, uint32_t *__restrict__ spill) {
+    __shared__ uint32_t stk[SC][LT];  // entry = (position << 16) | payload (di as uint16)
     const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
     // lanes run data-dependent envelope loops; reconverge (wm) before every
     // batched load and every store so the warp's accesses stay coalesced
@@ -111,7 +111,12 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
     if (l >= nlines) return;
     const i64 base = (l / nz) * (i64)ny * nz + (l % nz);
     const double d2 = __dmul_rn(dy, dy);
-#define ENT(e) (*((e) < SC ? &stk[(e)][threadIdx.x] : &spill[((e) - SC) * nlines + l]))
+    // explicit shared / global accesses (no generic pointers)
+    auto ent_ld = [&](int e) -> uint32_t { return e < SC ? stk[e][threadIdx.x] : spill[(i64)(e - SC) * nlines + l]; };
+    auto ent_st = [&](int e, uint32_t v) {
+        if (e < SC) stk[e][threadIdx.x] = v;
+        else spill[(i64)(e - SC) * nlines + l] = v;
+    };
 #define GOF(pl) sq(__dmul_rn((double)(int16_t)(pl), dx))
     int K = 0, tp = 0, bp = 0;
     double tg = 0.0, bg = 0.0;
@@ -131,12 +136,12 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
                 tp = bp;
                 tg = bg;
                 if (K >= 2) {
-                    const u64 e = ENT(K - 2);
-                    bp = (int)(e >> 32);
+                    const uint32_t e = ent_ld(K - 2);
+                    bp = (int)(e >> 16);
                     bg = GOF(e & 0xffff);
                 }
             }
-            ENT(K) = ((u64)(uint32_t)x << 32) | (uint16_t)v[u];
+            ent_st(K, ((uint32_t)x << 16) | (uint16_t)v[u]);
             bp = tp; bg = tg; tp = x; tg = gx;
             ++K;
         }
@@ -145,11 +150,11 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
     int16_t cpl = 0, npl = 0;
     double cg = 0.0, ng = 0.0;
     if (K) {
-        const u64 c0 = ENT(0);
-        cp = (int)(c0 >> 32); cpl = (int16_t)(c0 & 0xffff); cg = GOF(cpl);
+        const uint32_t c0 = ent_ld(0);
+        cp = (int)(c0 >> 16); cpl = (int16_t)(c0 & 0xffff); cg = GOF(cpl);
         if (K > 1) {
-            const u64 c1 = ENT(1);
-            np = (int)(c1 >> 32); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
+            const uint32_t c1 = ent_ld(1);
+            np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
         }
     }
     for (int x = 0; x < ny; ++x) {
@@ -160,8 +165,8 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
                 ++e;
                 cp = np; cpl = npl; cg = ng;
                 if (e + 1 < K) {
-                    const u64 c1 = ENT(e + 1);
-                    np = (int)(c1 >> 32); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
+                    const uint32_t c1 = ent_ld(e + 1);
+                    np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
                 }
             }
             r = pack(cp - x, cpl);
@@ -170,7 +175,6 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
         out[o] = r;
     }
 #undef GOF
-#undef ENT
 }
 
 // ---------------------------------------------------------------------------
@@ -262,7 +266,7 @@ inline size_t zsmem(int nz) {
 size_t ct_edt_workspace(int64_t nx, int64_t ny, int64_t nz) {
     const i64 N = nx * ny * nz;
     const i64 sp = nx * nz * (ny > SC ? ny - SC : 0);  // pass-y spill entries
-    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 8 + 4096;
+    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 4 + 4096;
 }
 
 extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, double dx, double dy, double dz,
@@ -279,7 +283,7 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     const i64 N = nx * ny * nz;
     int16_t *di = (int16_t *)work;
     int32_t *pk = (int32_t *)((char *)work + (((size_t)N * 2 + 255) & ~(size_t)255));
-    u64 *spill = (u64 *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
+    uint32_t *spill = (uint32_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
     const i64 lx = ny * nz, ly = nx * nz, lz = nx * ny;
     edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
     if (int st = ct::check_launch("edt_pass_x")) return st;
