@@ -146,27 +146,45 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
             ++K;
         }
     }
+    // output: segment boundaries as integer cut points.  env_past(x, q, p) is
+    // monotone in x (its right side only grows with x), so the first x where
+    // it holds is found by binary search and the per-position loop becomes an
+    // integer compare.
     int e = 0, cp = 0, np = 0;
     int16_t cpl = 0, npl = 0;
     double cg = 0.0, ng = 0.0;
+    auto first_past = [&](int lo) -> int {  // min x in [lo, ny) with env_past, else ny
+        int hi = ny;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (env_past(mid, np, ng, cp, cg, d2)) hi = mid;
+            else lo = mid + 1;
+        }
+        return lo;
+    };
+    int cut = ny;
     if (K) {
         const uint32_t c0 = ent_ld(0);
         cp = (int)(c0 >> 16); cpl = (int16_t)(c0 & 0xffff); cg = GOF(cpl);
         if (K > 1) {
             const uint32_t c1 = ent_ld(1);
             np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
+            cut = first_past(0);
         }
     }
     for (int x = 0; x < ny; ++x) {
         const i64 o = base + (i64)x * nz;
         int32_t r = NONE32;
         if (K) {
-            while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+            while (x >= cut) {
                 ++e;
                 cp = np; cpl = npl; cg = ng;
                 if (e + 1 < K) {
                     const uint32_t c1 = ent_ld(e + 1);
                     np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
+                    cut = first_past(x);
+                } else {
+                    cut = ny;
                 }
             }
             r = pack(cp - x, cpl);
@@ -178,13 +196,11 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
 }
 
 // ---------------------------------------------------------------------------
-// pass z: CTA = ZL consecutive (i,j) lines of nz <= 128 elements.
-//   phase 1 (all threads, coalesced): g = (di*dx)^2 + (dj*dy)^2 of every
-//            element into SMEM (+inf for no site);
-//   phase 2 (thread per line): envelope build with the top two costs in
-//            registers, stack of uint8 positions in SMEM;
-//   phase 3: distance sqrt(g_site + ((q-x)*dz)^2) -- g_site = t0 + t1, so this
-//            is ((t0 + t1) + t2), scipy's order -- written straight out.
+// pass z: thread per (i,j) line along the contiguous k (nz <= 128), lines of a
+// warp adjacent in memory (each thread streams its own 4*nz bytes through L1);
+// site costs g = (di*dx)^2 + (dj*dy)^2 are recomputed from the packed offsets
+// (top two in registers), the stack holds byte positions in SMEM.  Output
+// sqrt(g_site + ((q-x)*dz)^2) = sqrt((t0 + t1) + t2), scipy's order.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double gyz(int32_t pl, double dx, double dy) {
     return __dadd_rn(sq(__dmul_rn((double)unpack_di(pl), dx)), sq(__dmul_rn((double)unpack_dj(pl), dy)));
@@ -192,74 +208,53 @@ __device__ __forceinline__ double gyz(int32_t pl, double dx, double dy) {
 
 __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in, i64 nlines, int nz, double dx,
                                                  double dy, double dz, double *__restrict__ out) {
-    extern __shared__ __align__(16) unsigned char zsm[];
-    const int S = nz + 1;                               // padded line stride (conflict-free)
-    double *gs = (double *)zsm;                         // [ZL][S]   site costs (+inf: none)
-    uint8_t *stk = (uint8_t *)(gs + ZL * S);            // [ZL][S]   envelope positions
-    uint8_t *seg = stk + ZL * S;                        // [ZL][S]   chosen site per position
-    const i64 l0 = blockIdx.x * (i64)ZL;
-    const int nl = (int)min((i64)ZL, nlines - l0);
-    const int tot = nl * nz;
-    const int32_t *src = in + l0 * nz;
-    for (int idx = threadIdx.x; idx < tot; idx += ZL) {
-        const int g = idx / nz, k = idx - g * nz;
-        const int32_t pl = src[idx];
-        gs[g * S + k] = pl == NONE32 ? INFINITY : gyz(pl, dx, dy);
-    }
-    __syncthreads();
-    const int t = threadIdx.x;
-    if (t < nl) {
-        const double *G = gs + t * S;
-        uint8_t *st = stk + t * S;
-        uint8_t *sg = seg + t * S;
-        const double d2 = __dmul_rn(dz, dz);
-        int K = 0, tp = 0, bp = 0;
-        double tg = 0.0, bg = 0.0;
-        for (int x = 0; x < nz; ++x) {
-            const double gx = G[x];
-            if (gx == INFINITY) continue;
-            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-                --K;
-                tp = bp;
-                tg = bg;
-                if (K >= 2) {
-                    bp = st[K - 2];
-                    bg = G[bp];
-                }
-            }
-            st[K++] = (uint8_t)x;
-            bp = tp; bg = tg; tp = x; tg = gx;
-        }
-        if (K == 0) {
-            for (int x = 0; x < nz; ++x) sg[x] = 0xff;
-        } else {
-            int e = 0;
-            int cp = st[0], np = K > 1 ? st[1] : 0;
-            double cg = G[cp], ng = K > 1 ? G[np] : 0.0;
-            for (int x = 0; x < nz; ++x) {
-                while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
-                    ++e;
-                    cp = np; cg = ng;
-                    if (e + 1 < K) { np = st[e + 1]; ng = G[np]; }
-                }
-                sg[x] = (uint8_t)cp;
+    extern __shared__ uint8_t zstk[];  // [nz][ZL]: entry e of thread t at e*ZL + t (conflict-free)
+    const i64 l = blockIdx.x * (i64)ZL + threadIdx.x;
+    if (l >= nlines) return;
+    const int32_t *L = in + l * nz;
+    double *dst = out + l * nz;
+    uint8_t *st = zstk + threadIdx.x;
+    const double d2 = __dmul_rn(dz, dz);
+    int K = 0, tp = 0, bp = 0;
+    double tg = 0.0, bg = 0.0;
+    for (int x = 0; x < nz; ++x) {
+        const int32_t pl = L[x];
+        if (pl == NONE32) continue;
+        const double gx = gyz(pl, dx, dy);
+        while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+            --K;
+            tp = bp;
+            tg = bg;
+            if (K >= 2) {
+                bp = st[(K - 2) * ZL];
+                bg = gyz(L[bp], dx, dy);
             }
         }
+        st[K * ZL] = (uint8_t)x;
+        ++K;
+        bp = tp; bg = tg; tp = x; tg = gx;
     }
-    __syncthreads();
-    // cooperative coalesced output: sqrt(g_site + ((q-x)*dz)^2) = sqrt((t0+t1)+t2)
-    double *dst = out + l0 * nz;
-    for (int idx = threadIdx.x; idx < tot; idx += ZL) {
-        const int g = idx / nz, x = idx - g * nz;
-        const int q = seg[g * S + x];
-        dst[idx] = q == 0xff ? INFINITY : __dsqrt_rn(__dadd_rn(gs[g * S + q], sq(__dmul_rn((double)(q - x), dz))));
+    if (K == 0) {
+        for (int x = 0; x < nz; ++x) dst[x] = INFINITY;
+        return;
+    }
+    int e = 0;
+    int cp = st[0], np = K > 1 ? st[ZL] : 0;
+    double cg = gyz(L[cp], dx, dy), ng = K > 1 ? gyz(L[np], dx, dy) : 0.0;
+    for (int x = 0; x < nz; ++x) {
+        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+            ++e;
+            cp = np; cg = ng;
+            if (e + 1 < K) {
+                np = st[(e + 1) * ZL];
+                ng = gyz(L[np], dx, dy);
+            }
+        }
+        dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
     }
 }
 
-inline size_t zsmem(int nz) {
-    const int S = nz + 1;
-    return (size_t)ZL * S * 8 + 2 * (size_t)ZL * S + 16;
-}
+inline size_t zsmem(int nz) { return (size_t)ZL * nz + 16; }
 
 }  // namespace
 
