@@ -7,19 +7,19 @@
 // here the nearest feature's integer offsets are carried through three
 // separable passes and the distance is formed from them in exactly that order.
 //
+// Pass order x -> z -> y keeps every envelope sparse on vessel masks:
 //   pass x : per (j,k) line along i: nearest foreground (two sweeps over a
-//            register-prefetched stream).                 1 B in, 2 B (di) out
-//   pass y : per (i,k) line along j: lower envelope (Felzenszwalb-Huttenlocher)
-//            of the parabolas (di*dx)^2 + ((j-q)*dy)^2 over the sites q; the
-//            sites are sparse after pass x (only columns that hold foreground),
-//            so each thread's stack lives in SMEM (global spill past 16).
-//                                                           2 B in, 4 B (dj,di) out
-//   pass z : per (i,j) line along the contiguous k (nz <= 128): a CTA stages
-//            128 whole lines in SMEM (coalesced), runs the envelope of
-//            (di*dx)^2 + (dj*dy)^2 + ((k-q)*dz)^2 per thread entirely in SMEM
-//            and writes the float64 distances back coalesced.  4 B in, 8 B out
-// Lines of passes x and y map to consecutive k across a warp (coalesced).  The
-// envelope uses division-free predicates; arithmetic is identical to
+//            register-prefetched stream).  Only columns holding foreground get
+//            an offset.                                     1 B in, 2 B (di) out
+//   pass z : per (i,j) line along the contiguous k: lower envelope (Felzenszwalb-
+//            Huttenlocher) of (di*dx)^2 + ((k-q)*dz)^2; sites only where a
+//            foreground column crosses the line.            2 B in, 4 B (dk,di) out
+//   pass y : per (i,k) line along j, sites (di,dk): cost (di*dx)^2 + (dk*dz)^2,
+//            output sqrt(((di*dx)^2 + (dj*dy)^2) + (dk*dz)^2).   4 B in, 8 B out
+// Lines of passes x and y map to consecutive k across a warp (coalesced); pass
+// z streams each thread's contiguous line through L1.  Envelope stacks live in
+// SMEM (global spill beyond the SMEM slots), top-of-stack in registers, and
+// the predicates are division-free.  Arithmetic is identical to
 // oracle/ct_oracle.c ora_edt, so results match it bit for bit; equidistant
 // features may differ from scipy's choice in the last ulp, within the
 // reference's 1e-9 um contract (ref test_acceptance.py:318-332).
@@ -29,15 +29,16 @@ namespace {
 
 constexpr int16_t NONE16 = INT16_MIN;
 constexpr int32_t NONE32 = INT32_MIN;
-constexpr int SC = 48;   // SMEM stack entries per thread (pass y)
+constexpr int SCE = 24;  // SMEM stack entries (8 B) per thread (pass y)
 constexpr int LT = 256;  // threads per pass-x / pass-y CTA
 constexpr int PF = 16;   // prefetch depth (positions)
-constexpr int ZL = 128;  // lines per pass-z CTA
+constexpr int ZL = 128;  // threads per pass-z CTA
 
 __device__ __forceinline__ double sq(double x) { return __dmul_rn(x, x); }
 
-__device__ __forceinline__ int32_t pack(int dj, int di) { return (int32_t)(((uint32_t)dj << 16) | (uint16_t)di); }
-__device__ __forceinline__ int unpack_dj(int32_t p) { return p >> 16; }
+// packed (dk, di): dk in the high half, di in the low half
+__device__ __forceinline__ int32_t pack(int dk, int di) { return (int32_t)(((uint32_t)dk << 16) | (uint16_t)di); }
+__device__ __forceinline__ int unpack_dk(int32_t p) { return p >> 16; }
 __device__ __forceinline__ int unpack_di(int32_t p) { return (int)(int16_t)(p & 0xffff); }
 
 // Division-free envelope predicates (same op order as oracle/ct_oracle.c).
@@ -99,135 +100,34 @@ __global__ void __launch_bounds__(LT) edt_pass_x(const uint8_t *__restrict__ mas
 }
 
 // ---------------------------------------------------------------------------
-// pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di)
+// pass z: thread per (i,j) line along the contiguous k (nz <= 128); sites di
+// != NONE, cost (di*dx)^2; output packed (dk, di).  Stack of byte positions in
+// SMEM ([entry][thread], conflict-free); each thread streams its own line.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di, i64 nlines, int ny, int nz, double dx,
-                                                 double dy, int32_t *__restrict__ out, uint32_t *__restrict__ spill) {
-    __shared__ uint32_t stk[SC][LT];  // entry = (position << 16) | payload (di as uint16)
-    const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
-    // lanes run data-dependent envelope loops; reconverge (wm) before every
-    // batched load and every store so the warp's accesses stay coalesced
-    const unsigned wm = __ballot_sync(0xffffffffu, l < nlines);
-    if (l >= nlines) return;
-    const i64 base = (l / nz) * (i64)ny * nz + (l % nz);
-    const double d2 = __dmul_rn(dy, dy);
-    // explicit shared / global accesses (no generic pointers)
-    auto ent_ld = [&](int e) -> uint32_t { return e < SC ? stk[e][threadIdx.x] : spill[(i64)(e - SC) * nlines + l]; };
-    auto ent_st = [&](int e, uint32_t v) {
-        if (e < SC) stk[e][threadIdx.x] = v;
-        else spill[(i64)(e - SC) * nlines + l] = v;
-    };
-#define GOF(pl) sq(__dmul_rn((double)(int16_t)(pl), dx))
-    int K = 0, tp = 0, bp = 0;
-    double tg = 0.0, bg = 0.0;
-    for (int x0 = 0; x0 < ny; x0 += PF) {
-        int16_t v[PF];
-        __syncwarp(wm);
-#pragma unroll
-        for (int u = 0; u < PF; ++u) v[u] = x0 + u < ny ? di[base + (i64)(x0 + u) * nz] : NONE16;
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int x = x0 + u;
-            if (x >= ny) break;
-            if (v[u] == NONE16) continue;
-            const double gx = GOF(v[u]);
-            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-                --K;
-                tp = bp;
-                tg = bg;
-                if (K >= 2) {
-                    const uint32_t e = ent_ld(K - 2);
-                    bp = (int)(e >> 16);
-                    bg = GOF(e & 0xffff);
-                }
-            }
-            ent_st(K, ((uint32_t)x << 16) | (uint16_t)v[u]);
-            bp = tp; bg = tg; tp = x; tg = gx;
-            ++K;
-        }
-    }
-    // output: segment boundaries as integer cut points.  env_past(x, q, p) is
-    // monotone in x (its right side only grows with x), so the first x where
-    // it holds is found by binary search and the per-position loop becomes an
-    // integer compare.
-    int e = 0, cp = 0, np = 0;
-    int16_t cpl = 0, npl = 0;
-    double cg = 0.0, ng = 0.0;
-    auto first_past = [&](int lo) -> int {  // min x in [lo, ny) with env_past, else ny
-        int hi = ny;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (env_past(mid, np, ng, cp, cg, d2)) hi = mid;
-            else lo = mid + 1;
-        }
-        return lo;
-    };
-    int cut = ny;
-    if (K) {
-        const uint32_t c0 = ent_ld(0);
-        cp = (int)(c0 >> 16); cpl = (int16_t)(c0 & 0xffff); cg = GOF(cpl);
-        if (K > 1) {
-            const uint32_t c1 = ent_ld(1);
-            np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
-            cut = first_past(0);
-        }
-    }
-    for (int x = 0; x < ny; ++x) {
-        const i64 o = base + (i64)x * nz;
-        int32_t r = NONE32;
-        if (K) {
-            while (x >= cut) {
-                ++e;
-                cp = np; cpl = npl; cg = ng;
-                if (e + 1 < K) {
-                    const uint32_t c1 = ent_ld(e + 1);
-                    np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
-                    cut = first_past(x);
-                } else {
-                    cut = ny;
-                }
-            }
-            r = pack(cp - x, cpl);
-        }
-        __syncwarp(wm);
-        out[o] = r;
-    }
-#undef GOF
-}
+__device__ __forceinline__ double gx_of(int16_t d, double dx) { return sq(__dmul_rn((double)d, dx)); }
 
-// ---------------------------------------------------------------------------
-// pass z: thread per (i,j) line along the contiguous k (nz <= 128), lines of a
-// warp adjacent in memory (each thread streams its own 4*nz bytes through L1);
-// site costs g = (di*dx)^2 + (dj*dy)^2 are recomputed from the packed offsets
-// (top two in registers), the stack holds byte positions in SMEM.  Output
-// sqrt(g_site + ((q-x)*dz)^2) = sqrt((t0 + t1) + t2), scipy's order.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double gyz(int32_t pl, double dx, double dy) {
-    return __dadd_rn(sq(__dmul_rn((double)unpack_di(pl), dx)), sq(__dmul_rn((double)unpack_dj(pl), dy)));
-}
-
-__global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in, i64 nlines, int nz, double dx,
-                                                 double dy, double dz, double *__restrict__ out) {
-    extern __shared__ uint8_t zstk[];  // [nz][ZL]: entry e of thread t at e*ZL + t (conflict-free)
+__global__ void __launch_bounds__(ZL) edt_pass_z(const int16_t *__restrict__ di, i64 nlines, int nz, double dx,
+                                                 double dz, int32_t *__restrict__ out) {
+    extern __shared__ uint8_t zstk[];  // [nz][ZL]
     const i64 l = blockIdx.x * (i64)ZL + threadIdx.x;
     if (l >= nlines) return;
-    const int32_t *L = in + l * nz;
-    double *dst = out + l * nz;
+    const int16_t *L = di + l * nz;
+    int32_t *dst = out + l * nz;
     uint8_t *st = zstk + threadIdx.x;
     const double d2 = __dmul_rn(dz, dz);
     int K = 0, tp = 0, bp = 0;
     double tg = 0.0, bg = 0.0;
     for (int x = 0; x < nz; ++x) {
-        const int32_t pl = L[x];
-        if (pl == NONE32) continue;
-        const double gx = gyz(pl, dx, dy);
+        const int16_t v = L[x];
+        if (v == NONE16) continue;
+        const double gx = gx_of(v, dx);
         while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
             --K;
             tp = bp;
             tg = bg;
             if (K >= 2) {
                 bp = st[(K - 2) * ZL];
-                bg = gyz(L[bp], dx, dy);
+                bg = gx_of(L[bp], dx);
             }
         }
         st[K * ZL] = (uint8_t)x;
@@ -235,33 +135,115 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
         bp = tp; bg = tg; tp = x; tg = gx;
     }
     if (K == 0) {
-        for (int x = 0; x < nz; ++x) dst[x] = INFINITY;
+        for (int x = 0; x < nz; ++x) dst[x] = NONE32;
         return;
     }
     int e = 0;
     int cp = st[0], np = K > 1 ? st[ZL] : 0;
-    double cg = gyz(L[cp], dx, dy), ng = K > 1 ? gyz(L[np], dx, dy) : 0.0;
+    double cg = gx_of(L[cp], dx), ng = K > 1 ? gx_of(L[np], dx) : 0.0;
     for (int x = 0; x < nz; ++x) {
         while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
             ++e;
             cp = np; cg = ng;
             if (e + 1 < K) {
                 np = st[(e + 1) * ZL];
-                ng = gyz(L[np], dx, dy);
+                ng = gx_of(L[np], dx);
             }
         }
-        dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
+        dst[x] = pack(cp - x, L[cp]);
     }
 }
 
-inline size_t zsmem(int nz) { return (size_t)ZL * nz + 16; }
+// ---------------------------------------------------------------------------
+// pass y: envelope along j; sites (dk,di) != NONE, cost (di*dx)^2 + (dk*dz)^2;
+// output the float64 distance in scipy's term order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double gxz(int32_t p, double dx, double dz) {
+    return __dadd_rn(sq(__dmul_rn((double)unpack_di(p), dx)), sq(__dmul_rn((double)unpack_dk(p), dz)));
+}
+
+__global__ void __launch_bounds__(LT) edt_pass_y(const int32_t *__restrict__ in, i64 nlines, int ny, int nz, double dx,
+                                                 double dy, double dz, double *__restrict__ out,
+                                                 u64 *__restrict__ spill) {
+    __shared__ u64 stk[SCE][LT];  // entry = (position << 32) | payload
+    const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
+    // lanes run data-dependent loops; reconverge (wm) before every batched
+    // load and every store so the warp's accesses stay coalesced
+    const unsigned wm = __ballot_sync(0xffffffffu, l < nlines);
+    if (l >= nlines) return;
+    const i64 base = (l / nz) * (i64)ny * nz + (l % nz);
+    const double d2 = __dmul_rn(dy, dy);
+    auto ent_ld = [&](int e) -> u64 { return e < SCE ? stk[e][threadIdx.x] : spill[(i64)(e - SCE) * nlines + l]; };
+    auto ent_st = [&](int e, u64 v) {
+        if (e < SCE) stk[e][threadIdx.x] = v;
+        else spill[(i64)(e - SCE) * nlines + l] = v;
+    };
+    int K = 0, tp = 0, bp = 0;
+    double tg = 0.0, bg = 0.0;
+    for (int x0 = 0; x0 < ny; x0 += PF) {
+        int32_t v[PF];
+        __syncwarp(wm);
+#pragma unroll
+        for (int u = 0; u < PF; ++u) v[u] = x0 + u < ny ? in[base + (i64)(x0 + u) * nz] : NONE32;
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int x = x0 + u;
+            if (x >= ny) break;
+            if (v[u] == NONE32) continue;
+            const double gx = gxz(v[u], dx, dz);
+            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+                --K;
+                tp = bp;
+                tg = bg;
+                if (K >= 2) {
+                    const u64 e = ent_ld(K - 2);
+                    bp = (int)(e >> 32);
+                    bg = gxz((int32_t)(e & 0xffffffffu), dx, dz);
+                }
+            }
+            ent_st(K, ((u64)(uint32_t)x << 32) | (uint32_t)v[u]);
+            bp = tp; bg = tg; tp = x; tg = gx;
+            ++K;
+        }
+    }
+    int e = 0, cp = 0, np = 0;
+    int32_t cpl = 0, npl = 0;
+    double cg = 0.0, ng = 0.0;
+    if (K) {
+        const u64 c0 = ent_ld(0);
+        cp = (int)(c0 >> 32); cpl = (int32_t)(c0 & 0xffffffffu); cg = gxz(cpl, dx, dz);
+        if (K > 1) {
+            const u64 c1 = ent_ld(1);
+            np = (int)(c1 >> 32); npl = (int32_t)(c1 & 0xffffffffu); ng = gxz(npl, dx, dz);
+        }
+    }
+    for (int x = 0; x < ny; ++x) {
+        double r = INFINITY;
+        if (K) {
+            while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+                ++e;
+                cp = np; cpl = npl; cg = ng;
+                if (e + 1 < K) {
+                    const u64 c1 = ent_ld(e + 1);
+                    np = (int)(c1 >> 32); npl = (int32_t)(c1 & 0xffffffffu); ng = gxz(npl, dx, dz);
+                }
+            }
+            const double t0 = sq(__dmul_rn((double)unpack_di(cpl), dx));
+            const double t1 = sq(__dmul_rn((double)(cp - x), dy));
+            const double t2 = sq(__dmul_rn((double)unpack_dk(cpl), dz));
+            r = __dsqrt_rn(__dadd_rn(__dadd_rn(t0, t1), t2));
+        }
+        __syncwarp(wm);
+        out[base + (i64)x * nz] = r;
+    }
+}
 
 }  // namespace
 
 size_t ct_edt_workspace(int64_t nx, int64_t ny, int64_t nz) {
     const i64 N = nx * ny * nz;
-    const i64 sp = nx * nz * (ny > SC ? ny - SC : 0);  // pass-y spill entries
-    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 4 + 4096;
+    const i64 sp = nx * nz * (ny > SCE ? ny - SCE : 0);  // pass-y spill entries
+    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 8 + 4096;
 }
 
 extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, double dx, double dy, double dz,
@@ -271,21 +253,20 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         return CT_ERR_PARAM;
     }
     if (nx > 32767 || ny > 32767 || nz > 128) {
-        ct::set_error("EDT supports nx, ny < 32768 and nz <= 128 (packed int16 offsets, SMEM z lines)");
+        ct::set_error("EDT supports nx, ny < 32768 and nz <= 128 (packed int16 offsets, byte stacks)");
         return CT_ERR_UNSUPPORTED;
     }
     cudaStream_t s = (cudaStream_t)stream;
     const i64 N = nx * ny * nz;
     int16_t *di = (int16_t *)work;
     int32_t *pk = (int32_t *)((char *)work + (((size_t)N * 2 + 255) & ~(size_t)255));
-    uint32_t *spill = (uint32_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
-    const i64 lx = ny * nz, ly = nx * nz, lz = nx * ny;
+    u64 *spill = (u64 *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
+    const i64 lx = ny * nz, lz = nx * ny, ly = nx * nz;
     edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
     if (int st = ct::check_launch("edt_pass_x")) return st;
-    edt_pass_y<<<(unsigned)((ly + LT - 1) / LT), LT, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, pk, spill);
-    if (int st = ct::check_launch("edt_pass_y")) return st;
-    const size_t sm = zsmem((int)nz);
-    cudaFuncSetAttribute(edt_pass_z, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    edt_pass_z<<<(unsigned)((lz + ZL - 1) / ZL), ZL, sm, s>>>(pk, lz, (int)nz, dx, dy, dz, out);
-    return ct::check_launch("edt_pass_z");
+    const size_t zsm = (size_t)ZL * nz + 16;
+    edt_pass_z<<<(unsigned)((lz + ZL - 1) / ZL), ZL, zsm, s>>>(di, lz, (int)nz, dx, dz, pk);
+    if (int st = ct::check_launch("edt_pass_z")) return st;
+    edt_pass_y<<<(unsigned)((ly + LT - 1) / LT), LT, 0, s>>>(pk, ly, (int)ny, (int)nz, dx, dy, dz, out, spill);
+    return ct::check_launch("edt_pass_y");
 }
