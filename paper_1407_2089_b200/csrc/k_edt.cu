@@ -17,7 +17,7 @@
 //   pass y : per (i,k) line along j, sites (di,dk): cost (di*dx)^2 + (dk*dz)^2,
 //            output sqrt(((di*dx)^2 + (dj*dy)^2) + (dk*dz)^2).   4 B in, 8 B out
 // Lines of passes x and y map to consecutive k across a warp (coalesced); pass
-// z streams each thread's contiguous line through L1.  Envelope stacks live in
+// z stages whole contiguous lines through SMEM.  Envelope stacks live in
 // SMEM (global spill beyond the SMEM slots), top-of-stack in registers, and
 // the predicates are division-free.  Arithmetic is identical to
 // oracle/ct_oracle.c ora_edt, so results match it bit for bit; equidistant
@@ -29,7 +29,7 @@ namespace {
 
 constexpr int16_t NONE16 = INT16_MIN;
 constexpr int32_t NONE32 = INT32_MIN;
-constexpr int SCE = 24;  // SMEM stack entries (8 B) per thread (pass y)
+constexpr int SCE = 96;  // SMEM stack entries (2 B positions) per thread (pass y)
 constexpr int LT = 256;  // threads per pass-x / pass-y CTA
 constexpr int PF = 16;   // prefetch depth (positions)
 constexpr int ZL = 128;  // threads per pass-z CTA
@@ -100,57 +100,84 @@ __global__ void __launch_bounds__(LT) edt_pass_x(const uint8_t *__restrict__ mas
 }
 
 // ---------------------------------------------------------------------------
-// pass z: thread per (i,j) line along the contiguous k (nz <= 128); sites di
-// != NONE, cost (di*dx)^2; output packed (dk, di).  Stack of byte positions in
-// SMEM ([entry][thread], conflict-free); each thread streams its own line.
+// pass z: per (i,j) line along the contiguous k (nz <= 128); sites di != NONE,
+// cost (di*dx)^2; output packed (dk, di).  A CTA stages ZL consecutive lines
+// in SMEM (coalesced in and out); per-thread stacks hold (position, di).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double gx_of(int16_t d, double dx) { return sq(__dmul_rn((double)d, dx)); }
 
 __global__ void __launch_bounds__(ZL) edt_pass_z(const int16_t *__restrict__ di, i64 nlines, int nz, double dx,
                                                  double dz, int32_t *__restrict__ out) {
-    extern __shared__ uint8_t zstk[];  // [nz][ZL]
-    const i64 l = blockIdx.x * (i64)ZL + threadIdx.x;
-    if (l >= nlines) return;
-    const int16_t *L = di + l * nz;
-    int32_t *dst = out + l * nz;
-    uint8_t *st = zstk + threadIdx.x;
-    const double d2 = __dmul_rn(dz, dz);
-    int K = 0, tp = 0, bp = 0;
-    double tg = 0.0, bg = 0.0;
-    for (int x = 0; x < nz; ++x) {
-        const int16_t v = L[x];
-        if (v == NONE16) continue;
-        const double gx = gx_of(v, dx);
-        while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-            --K;
-            tp = bp;
-            tg = bg;
-            if (K >= 2) {
-                bp = st[(K - 2) * ZL];
-                bg = gx_of(L[bp], dx);
+    // CTA = ZL consecutive lines (contiguous in memory): staged in and out of
+    // SMEM with coalesced copies; the envelope runs per thread on its line.
+    extern __shared__ __align__(16) unsigned char zsm[];
+    const int S = nz + 1;                          // padded stride
+    int32_t *io = (int32_t *)zsm;                  // [ZL][S] in: di (as int32), out: packed
+    int16_t *sdi = (int16_t *)(io + ZL * S);       // [nz][ZL] di of each stack entry
+    uint8_t *stk = (uint8_t *)(sdi + ZL * nz);     // [nz][ZL] byte positions
+    const i64 l0 = blockIdx.x * (i64)ZL;
+    const int nl = (int)min((i64)ZL, nlines - l0);
+    const int tot = nl * nz;
+    const int16_t *src = di + l0 * nz;
+    for (int idx = threadIdx.x; idx < tot; idx += ZL) {
+        const int g = idx / nz, k = idx - g * nz;
+        io[g * S + k] = src[idx];
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < nl) {
+        int32_t *L = io + t * S;
+        uint8_t *st = stk + t;
+        int16_t *sd = sdi + t;
+        const double d2 = __dmul_rn(dz, dz);
+        int K = 0, tp = 0, bp = 0;
+        double tg = 0.0, bg = 0.0;
+        for (int x = 0; x < nz; ++x) {
+            const int32_t v = L[x];
+            if (v == NONE16) continue;
+            const double gx = gx_of((int16_t)v, dx);
+            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+                --K;
+                tp = bp;
+                tg = bg;
+                if (K >= 2) {
+                    bp = st[(K - 2) * ZL];
+                    bg = gx_of(sd[(K - 2) * ZL], dx);
+                }
+            }
+            st[K * ZL] = (uint8_t)x;
+            sd[K * ZL] = (int16_t)v;
+            ++K;
+            bp = tp; bg = tg; tp = x; tg = gx;
+        }
+        // results overwrite the staged line in place; stack entries keep
+        // their own di, so no overwritten element is read again
+        if (K == 0) {
+            for (int x = 0; x < nz; ++x) L[x] = NONE32;
+        } else {
+            int e = 0;
+            int cp = st[0], np = K > 1 ? st[ZL] : 0;
+            int cdi = sd[0], ndi = K > 1 ? sd[ZL] : 0;
+            double cg = gx_of((int16_t)cdi, dx), ng = K > 1 ? gx_of((int16_t)ndi, dx) : 0.0;
+            for (int x = 0; x < nz; ++x) {
+                while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+                    ++e;
+                    cp = np; cdi = ndi; cg = ng;
+                    if (e + 1 < K) {
+                        np = st[(e + 1) * ZL];
+                        ndi = sd[(e + 1) * ZL];
+                        ng = gx_of((int16_t)ndi, dx);
+                    }
+                }
+                L[x] = pack(cp - x, cdi);
             }
         }
-        st[K * ZL] = (uint8_t)x;
-        ++K;
-        bp = tp; bg = tg; tp = x; tg = gx;
     }
-    if (K == 0) {
-        for (int x = 0; x < nz; ++x) dst[x] = NONE32;
-        return;
-    }
-    int e = 0;
-    int cp = st[0], np = K > 1 ? st[ZL] : 0;
-    double cg = gx_of(L[cp], dx), ng = K > 1 ? gx_of(L[np], dx) : 0.0;
-    for (int x = 0; x < nz; ++x) {
-        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
-            ++e;
-            cp = np; cg = ng;
-            if (e + 1 < K) {
-                np = st[(e + 1) * ZL];
-                ng = gx_of(L[np], dx);
-            }
-        }
-        dst[x] = pack(cp - x, L[cp]);
+    __syncthreads();
+    int32_t *dst = out + l0 * nz;
+    for (int idx = threadIdx.x; idx < tot; idx += ZL) {
+        const int g = idx / nz, k = idx - g * nz;
+        dst[idx] = io[g * S + k];
     }
 }
 
@@ -164,8 +191,9 @@ __device__ __forceinline__ double gxz(int32_t p, double dx, double dz) {
 
 __global__ void __launch_bounds__(LT) edt_pass_y(const int32_t *__restrict__ in, i64 nlines, int ny, int nz, double dx,
                                                  double dy, double dz, double *__restrict__ out,
-                                                 u64 *__restrict__ spill) {
-    __shared__ u64 stk[SCE][LT];  // entry = (position << 32) | payload
+                                                 uint16_t *__restrict__ spill) {
+    // stack of site positions (payloads are re-read from the input: L1-resident)
+    __shared__ uint16_t stk[SCE][LT];
     const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
     // lanes run data-dependent loops; reconverge (wm) before every batched
     // load and every store so the warp's accesses stay coalesced
@@ -173,11 +201,14 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int32_t *__restrict__ in,
     if (l >= nlines) return;
     const i64 base = (l / nz) * (i64)ny * nz + (l % nz);
     const double d2 = __dmul_rn(dy, dy);
-    auto ent_ld = [&](int e) -> u64 { return e < SCE ? stk[e][threadIdx.x] : spill[(i64)(e - SCE) * nlines + l]; };
-    auto ent_st = [&](int e, u64 v) {
-        if (e < SCE) stk[e][threadIdx.x] = v;
-        else spill[(i64)(e - SCE) * nlines + l] = v;
+    auto ent_ld = [&](int e) -> int {
+        return e < SCE ? stk[e][threadIdx.x] : spill[(i64)(e - SCE) * nlines + l];
     };
+    auto ent_st = [&](int e, int pos) {
+        if (e < SCE) stk[e][threadIdx.x] = (uint16_t)pos;
+        else spill[(i64)(e - SCE) * nlines + l] = (uint16_t)pos;
+    };
+    auto pay = [&](int pos) -> int32_t { return in[base + (i64)pos * nz]; };
     int K = 0, tp = 0, bp = 0;
     double tg = 0.0, bg = 0.0;
     for (int x0 = 0; x0 < ny; x0 += PF) {
@@ -196,12 +227,11 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int32_t *__restrict__ in,
                 tp = bp;
                 tg = bg;
                 if (K >= 2) {
-                    const u64 e = ent_ld(K - 2);
-                    bp = (int)(e >> 32);
-                    bg = gxz((int32_t)(e & 0xffffffffu), dx, dz);
+                    bp = ent_ld(K - 2);
+                    bg = gxz(pay(bp), dx, dz);
                 }
             }
-            ent_st(K, ((u64)(uint32_t)x << 32) | (uint32_t)v[u]);
+            ent_st(K, x);
             bp = tp; bg = tg; tp = x; tg = gx;
             ++K;
         }
@@ -210,12 +240,8 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int32_t *__restrict__ in,
     int32_t cpl = 0, npl = 0;
     double cg = 0.0, ng = 0.0;
     if (K) {
-        const u64 c0 = ent_ld(0);
-        cp = (int)(c0 >> 32); cpl = (int32_t)(c0 & 0xffffffffu); cg = gxz(cpl, dx, dz);
-        if (K > 1) {
-            const u64 c1 = ent_ld(1);
-            np = (int)(c1 >> 32); npl = (int32_t)(c1 & 0xffffffffu); ng = gxz(npl, dx, dz);
-        }
+        cp = ent_ld(0); cpl = pay(cp); cg = gxz(cpl, dx, dz);
+        if (K > 1) { np = ent_ld(1); npl = pay(np); ng = gxz(npl, dx, dz); }
     }
     for (int x = 0; x < ny; ++x) {
         double r = INFINITY;
@@ -223,10 +249,7 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int32_t *__restrict__ in,
             while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
                 ++e;
                 cp = np; cpl = npl; cg = ng;
-                if (e + 1 < K) {
-                    const u64 c1 = ent_ld(e + 1);
-                    np = (int)(c1 >> 32); npl = (int32_t)(c1 & 0xffffffffu); ng = gxz(npl, dx, dz);
-                }
+                if (e + 1 < K) { np = ent_ld(e + 1); npl = pay(np); ng = gxz(npl, dx, dz); }
             }
             const double t0 = sq(__dmul_rn((double)unpack_di(cpl), dx));
             const double t1 = sq(__dmul_rn((double)(cp - x), dy));
@@ -243,7 +266,7 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int32_t *__restrict__ in,
 size_t ct_edt_workspace(int64_t nx, int64_t ny, int64_t nz) {
     const i64 N = nx * ny * nz;
     const i64 sp = nx * nz * (ny > SCE ? ny - SCE : 0);  // pass-y spill entries
-    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 8 + 4096;
+    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 2 + 4096;
 }
 
 extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, double dx, double dy, double dz,
@@ -260,11 +283,11 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     const i64 N = nx * ny * nz;
     int16_t *di = (int16_t *)work;
     int32_t *pk = (int32_t *)((char *)work + (((size_t)N * 2 + 255) & ~(size_t)255));
-    u64 *spill = (u64 *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
+    uint16_t *spill = (uint16_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
     const i64 lx = ny * nz, lz = nx * ny, ly = nx * nz;
     edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
     if (int st = ct::check_launch("edt_pass_x")) return st;
-    const size_t zsm = (size_t)ZL * nz + 16;
+    const size_t zsm = (size_t)ZL * (nz + 1) * 4 + (size_t)ZL * nz * 3 + 16;
     edt_pass_z<<<(unsigned)((lz + ZL - 1) / ZL), ZL, zsm, s>>>(di, lz, (int)nz, dx, dz, pk);
     if (int st = ct::check_launch("edt_pass_z")) return st;
     edt_pass_y<<<(unsigned)((ly + LT - 1) / LT), LT, 0, s>>>(pk, ly, (int)ny, (int)nz, dx, dy, dz, out, spill);
