@@ -29,7 +29,6 @@ namespace {
 
 constexpr int16_t NONE16 = INT16_MIN;
 constexpr int32_t NONE32 = INT32_MIN;
-constexpr int SCE = 96;  // SMEM stack entries (2 B positions) per thread (pass y)
 constexpr int LT = 256;  // threads per pass-x / pass-y CTA
 constexpr int PF = 16;   // prefetch depth (positions)
 constexpr int ZL = 128;  // threads per pass-z CTA
@@ -107,7 +106,7 @@ __global__ void __launch_bounds__(LT) edt_pass_x(const uint8_t *__restrict__ mas
 __device__ __forceinline__ double gx_of(int16_t d, double dx) { return sq(__dmul_rn((double)d, dx)); }
 
 __global__ void __launch_bounds__(ZL) edt_pass_z(const int16_t *__restrict__ di, i64 nlines, int nz, double dx,
-                                                 double dz, int32_t *__restrict__ out) {
+                                                 double dz, int32_t *__restrict__ out, uint8_t *__restrict__ rowflag) {
     // CTA = ZL consecutive lines (contiguous in memory): staged in and out of
     // SMEM with coalesced copies; the envelope runs per thread on its line.
     extern __shared__ __align__(16) unsigned char zsm[];
@@ -150,6 +149,7 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int16_t *__restrict__ di,
             ++K;
             bp = tp; bg = tg; tp = x; tg = gx;
         }
+        rowflag[l0 + t] = K > 0;
         // results overwrite the staged line in place; stack entries keep
         // their own di, so no overwritten element is read again
         if (K == 0) {
@@ -189,84 +189,123 @@ __device__ __forceinline__ double gxz(int32_t p, double dx, double dz) {
     return __dadd_rn(sq(__dmul_rn((double)unpack_di(p), dx)), sq(__dmul_rn((double)unpack_dk(p), dz)));
 }
 
-__global__ void __launch_bounds__(LT) edt_pass_y(const int32_t *__restrict__ in, i64 nlines, int ny, int nz, double dx,
-                                                 double dy, double dz, double *__restrict__ out,
-                                                 uint16_t *__restrict__ spill) {
-    // stack of site positions (payloads are re-read from the input: L1-resident)
-    __shared__ uint16_t stk[SCE][LT];
-    const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
-    // lanes run data-dependent loops; reconverge (wm) before every batched
-    // load and every store so the warp's accesses stay coalesced
-    const unsigned wm = __ballot_sync(0xffffffffu, l < nlines);
-    if (l >= nlines) return;
-    const i64 base = (l / nz) * (i64)ny * nz + (l % nz);
+// The sites of line (i,k) are the rows j whose z-line (i,j) had a site
+// (pass z flags them); that row set does not depend on k.  A CTA owns plane i
+// and KC consecutive k: it compacts the site rows once (ordered ballot scan),
+// stages their payloads in SMEM, builds the KC envelopes (one thread each,
+// stacks of row indices in SMEM), then all 256 threads write the KC x ny
+// outputs -- thread (k, chunk) finds its chunk's first segment and streams.
+constexpr int KC = 16;
+constexpr int YT = 256;
+
+__global__ void __launch_bounds__(YT) edt_pass_y(const int32_t *__restrict__ in, const uint8_t *__restrict__ rowflag,
+                                                 int nx, int ny, int nz, double dx, double dy, double dz,
+                                                 double *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char ysm[];
+    uint16_t *J = (uint16_t *)ysm;                          // [ny] site rows
+    int32_t *P = (int32_t *)(ysm + (((size_t)ny * 2 + 15) & ~(size_t)15));   // [nJ][KC] payloads
+    uint16_t *st = (uint16_t *)(P + (size_t)ny * KC);       // [KC][ny] stack (indices into J)
+    __shared__ int s_n, s_wsum[YT / 32], s_K[KC];
+    const int kchunks = (nz + KC - 1) / KC;
+    const int i = blockIdx.x / kchunks, k0 = (blockIdx.x % kchunks) * KC;
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const i64 plane = (i64)i * ny;
+    // 1. ordered compaction of the flagged rows
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int j0 = 0; j0 < ny; j0 += YT) {
+        const int j = j0 + threadIdx.x;
+        const bool f = j < ny && rowflag[plane + j];
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s_wsum[wid] = __popc(m);
+        __syncthreads();
+        int before = s_n;
+        for (unsigned w = 0; w < wid; ++w) before += s_wsum[w];
+        if (f) J[before + __popc(m & ((1u << lane) - 1))] = (uint16_t)j;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < YT / 32; ++w) t += s_wsum[w];
+            s_n += t;
+        }
+        __syncthreads();
+    }
+    const int nJ = s_n;
+    // 2. payloads of the site rows (rows of KC contiguous int32)
+    for (int e = threadIdx.x; e < nJ * KC; e += YT) {
+        const int r = e / KC, kk = e - r * KC;
+        P[e] = k0 + kk < nz ? in[(plane + J[r]) * nz + k0 + kk] : NONE32;
+    }
+    __syncthreads();
     const double d2 = __dmul_rn(dy, dy);
-    auto ent_ld = [&](int e) -> int {
-        return e < SCE ? stk[e][threadIdx.x] : spill[(i64)(e - SCE) * nlines + l];
-    };
-    auto ent_st = [&](int e, int pos) {
-        if (e < SCE) stk[e][threadIdx.x] = (uint16_t)pos;
-        else spill[(i64)(e - SCE) * nlines + l] = (uint16_t)pos;
-    };
-    auto pay = [&](int pos) -> int32_t { return in[base + (i64)pos * nz]; };
-    int K = 0, tp = 0, bp = 0;
-    double tg = 0.0, bg = 0.0;
-    for (int x0 = 0; x0 < ny; x0 += PF) {
-        int32_t v[PF];
-        __syncwarp(wm);
-#pragma unroll
-        for (int u = 0; u < PF; ++u) v[u] = x0 + u < ny ? in[base + (i64)(x0 + u) * nz] : NONE32;
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int x = x0 + u;
-            if (x >= ny) break;
-            if (v[u] == NONE32) continue;
-            const double gx = gxz(v[u], dx, dz);
+    // 3. envelopes, one thread per k
+    if (threadIdx.x < KC && k0 + (int)threadIdx.x < nz) {
+        const int kk = threadIdx.x;
+        uint16_t *S = st + kk * ny;
+        int K = 0, tp = 0, bp = 0, tr = 0, br = 0;
+        double tg = 0.0, bg = 0.0;
+        for (int r = 0; r < nJ; ++r) {
+            const int32_t v = P[r * KC + kk];
+            if (v == NONE32) continue;
+            const int x = J[r];
+            const double gx = gxz(v, dx, dz);
             while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
                 --K;
-                tp = bp;
-                tg = bg;
+                tp = bp; tg = bg; tr = br;
                 if (K >= 2) {
-                    bp = ent_ld(K - 2);
-                    bg = gxz(pay(bp), dx, dz);
+                    br = S[K - 2];
+                    bp = J[br];
+                    bg = gxz(P[br * KC + kk], dx, dz);
                 }
             }
-            ent_st(K, x);
-            bp = tp; bg = tg; tp = x; tg = gx;
+            S[K] = (uint16_t)r;
             ++K;
+            bp = tp; bg = tg; br = tr;
+            tp = x; tg = gx; tr = r;
         }
+        s_K[kk] = K;
     }
-    int e = 0, cp = 0, np = 0;
-    int32_t cpl = 0, npl = 0;
-    double cg = 0.0, ng = 0.0;
-    if (K) {
-        cp = ent_ld(0); cpl = pay(cp); cg = gxz(cpl, dx, dz);
-        if (K > 1) { np = ent_ld(1); npl = pay(np); ng = gxz(npl, dx, dz); }
+    __syncthreads();
+    // 4. outputs: thread = (k, chunk of rows)
+    const int kk = threadIdx.x % KC, c = threadIdx.x / KC;
+    const int nchunk = YT / KC, CH = (ny + nchunk - 1) / nchunk;
+    const int ja = c * CH, jb = min(ny, ja + CH);
+    if (k0 + kk >= nz || ja >= jb) return;
+    const int K = s_K[kk];
+    const uint16_t *S = st + kk * ny;
+    double *o = out + (plane + ja) * nz + k0 + kk;
+    if (K == 0) {
+        for (int j = ja; j < jb; ++j, o += nz) *o = INFINITY;
+        return;
     }
-    for (int x = 0; x < ny; ++x) {
-        double r = INFINITY;
-        if (K) {
-            while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
-                ++e;
-                cp = np; cpl = npl; cg = ng;
-                if (e + 1 < K) { np = ent_ld(e + 1); npl = pay(np); ng = gxz(npl, dx, dz); }
-            }
-            const double t0 = sq(__dmul_rn((double)unpack_di(cpl), dx));
-            const double t1 = sq(__dmul_rn((double)(cp - x), dy));
-            const double t2 = sq(__dmul_rn((double)unpack_dk(cpl), dz));
-            r = __dsqrt_rn(__dadd_rn(__dadd_rn(t0, t1), t2));
+    int e = 0;
+    int cr = S[0], cp = J[cr];
+    int32_t cpl = P[cr * KC + kk];
+    double cg = gxz(cpl, dx, dz);
+    int nr = 0, np = 0;
+    double ng = 0.0;
+    if (K > 1) { nr = S[1]; np = J[nr]; ng = gxz(P[nr * KC + kk], dx, dz); }
+    for (int j = ja; j < jb; ++j, o += nz) {
+        while (e + 1 < K && env_past(j, np, ng, cp, cg, d2)) {
+            ++e;
+            cr = nr; cp = np; cg = ng;
+            cpl = P[cr * KC + kk];
+            if (e + 1 < K) { nr = S[e + 1]; np = J[nr]; ng = gxz(P[nr * KC + kk], dx, dz); }
         }
-        __syncwarp(wm);
-        out[base + (i64)x * nz] = r;
+        const double t0 = sq(__dmul_rn((double)unpack_di(cpl), dx));
+        const double t1 = sq(__dmul_rn((double)(cp - j), dy));
+        const double t2 = sq(__dmul_rn((double)unpack_dk(cpl), dz));
+        *o = __dsqrt_rn(__dadd_rn(__dadd_rn(t0, t1), t2));
     }
 }
+
+inline size_t ysmem(int ny) { return (((size_t)ny * 2 + 15) & ~(size_t)15) + (size_t)ny * KC * 4 + (size_t)KC * ny * 2; }
 
 }  // namespace
 
 size_t ct_edt_workspace(int64_t nx, int64_t ny, int64_t nz) {
     const i64 N = nx * ny * nz;
-    const i64 sp = nx * nz * (ny > SCE ? ny - SCE : 0);  // pass-y spill entries
-    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 2 + 4096;
+    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)nx * ny + 4096;
 }
 
 extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, double dx, double dy, double dz,
@@ -283,14 +322,21 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     const i64 N = nx * ny * nz;
     int16_t *di = (int16_t *)work;
     int32_t *pk = (int32_t *)((char *)work + (((size_t)N * 2 + 255) & ~(size_t)255));
-    uint16_t *spill = (uint16_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
-    const i64 lx = ny * nz, lz = nx * ny, ly = nx * nz;
+    uint8_t *rowflag = (uint8_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
+    const i64 lx = ny * nz, lz = nx * ny;
     edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
     if (int st = ct::check_launch("edt_pass_x")) return st;
     const size_t zsm = (size_t)ZL * (nz + 1) * 4 + (size_t)ZL * nz * 3 + 16;
     cudaFuncSetAttribute(edt_pass_z, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
-    edt_pass_z<<<(unsigned)((lz + ZL - 1) / ZL), ZL, zsm, s>>>(di, lz, (int)nz, dx, dz, pk);
+    edt_pass_z<<<(unsigned)((lz + ZL - 1) / ZL), ZL, zsm, s>>>(di, lz, (int)nz, dx, dz, pk, rowflag);
     if (int st = ct::check_launch("edt_pass_z")) return st;
-    edt_pass_y<<<(unsigned)((ly + LT - 1) / LT), LT, 0, s>>>(pk, ly, (int)ny, (int)nz, dx, dy, dz, out, spill);
+    const size_t ysm = ysmem((int)ny);
+    if (ysm > 220 * 1024) {
+        ct::set_error("EDT: ny too large for the SMEM pass-y layout");
+        return CT_ERR_UNSUPPORTED;
+    }
+    cudaFuncSetAttribute(edt_pass_y, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm);
+    const i64 ychunks = nx * ((nz + KC - 1) / KC);
+    edt_pass_y<<<(unsigned)ychunks, YT, ysm, s>>>(pk, rowflag, (int)nx, (int)ny, (int)nz, dx, dy, dz, out);
     return ct::check_launch("edt_pass_y");
 }
