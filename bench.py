@@ -300,10 +300,10 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, dt = cpu_sample_voxels_per_s(spec, 0, args.cpu_crop, threads)
+        v, dt = cpu_sample_voxels_per_s(spec, 0, args.cpu_baseline_crop, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"oracle/ct_oracle.c port, both channels of C2 t=0 cropped to {args.cpu_crop}x1024x64 "
-                         f"({dt:.1f} s)"}
+               "sample": f"oracle/ct_oracle.c port (OpenMP), both channels of C2 t=0 "
+                         f"({args.cpu_baseline_crop}x1024x64 per channel, {dt:.1f} s)"}
 
     if rank == 0:
         line = {
@@ -444,11 +444,12 @@ def run_e2e(args, pipe, spec, sp, dev, world, s_cell, s_vess):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ring", type=int, default=6)
-    ap.add_argument("--cpu-crop", type=int, default=128)
+    ap.add_argument("--cpu-crop", type=int, default=128, help="x-slices per --impl reference step")
+    ap.add_argument("--cpu-baseline-crop", type=int, default=1024, help="x-slices of the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
