@@ -108,12 +108,21 @@ __global__ void __launch_bounds__(LK *LJ) ccl_local(const uint8_t *__restrict__ 
         __syncthreads();
         const int c = threadIdx.x, b = threadIdx.y;
         const i64 j = j0 + b, k = k0 + c;
+        uint8_t mv[LI];
+        bool any = false;
 #pragma unroll
         for (int a = 0; a < LI; ++a) {
             const i64 i = i0 + a;
-            const int v = (a * LJ + b) * LK + c;
             const bool in = i < nx && j < ny && k < nz;
-            L[v] = (in && mask[(i * ny + j) * nz + k]) ? v : -1;
+            mv[a] = in ? mask[(i * ny + j) * nz + k] : 0;
+            any |= mv[a] != 0;
+        }
+        // labels were pre-filled with -1: an all-background tile needs no work
+        if (!__syncthreads_or(any)) continue;
+#pragma unroll
+        for (int a = 0; a < LI; ++a) {
+            const int v = (a * LJ + b) * LK + c;
+            L[v] = mv[a] ? v : -1;
         }
         __syncthreads();
 #pragma unroll
@@ -138,18 +147,13 @@ __global__ void __launch_bounds__(LK *LJ) ccl_local(const uint8_t *__restrict__ 
         for (int a = 0; a < LI; ++a) {
             const i64 i = i0 + a;
             const int v = (a * LJ + b) * LK + c;
-            const bool in = i < nx && j < ny && k < nz;
             const int r = L[v];
             const i64 p = (i * ny + j) * nz + k;
-            if (in) {
-                int32_t lab = -1;
-                if (r >= 0) {
-                    const int ra = r / (LJ * LK), rb = (r / LK) % LJ, rc = r % LK;
-                    lab = (int32_t)(((i0 + ra) * ny + (j0 + rb)) * nz + (k0 + rc));
-                }
-                labels[p] = lab;
+            if (r >= 0) {
+                const int ra = r / (LJ * LK), rb = (r / LK) % LJ, rc = r % LK;
+                labels[p] = (int32_t)(((i0 + ra) * ny + (j0 + rb)) * nz + (k0 + rc));
             }
-            append(fg, (unsigned long long *)&counters[CT_CNT_FG], (int32_t)p, in && r >= 0);
+            append(fg, (unsigned long long *)&counters[CT_CNT_FG], (int32_t)p, r >= 0);
         }
     }
 }
@@ -337,12 +341,28 @@ __global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64
     int rbits = 1;
     while ((((u64)N - 1) >> rbits) && rbits < 40) ++rbits;
     const int passes = (cbits + rbits + 3) / 4;
-    // 2. stable LSD radix sort of sa[0..nk) by key
+    // 2. order sa[0..nk) by key (keys are unique: roots differ).  Few cells:
+    //    rank by counting against all keys staged in SMEM (O(nk^2), no passes);
+    //    many: stable LSD radix sort, 4-bit digits.
     int32_t *src = w.sa, *dst = w.sb;
     const i64 kchunk = ((i64)nk + RT - 1) / RT;
     const i64 e0 = min((i64)tid * kchunk, (i64)nk), e1 = min(e0 + kchunk, (i64)nk);
     __threadfence_block();
     __syncthreads();
+    u64 *skey = reinterpret_cast<u64 *>(&hcnt[0][0]);  // RD*RT*4 bytes = 4096 keys
+    if (nk <= (u64)(RD * RT / 2)) {
+        for (i64 e = tid; e < (i64)nk; e += RT) skey[e] = sort_key(w, src[e], mc, rbits);
+        __syncthreads();
+        for (i64 e = tid; e < (i64)nk; e += RT) {
+            const u64 k = skey[e];
+            i64 r = 0;
+            for (i64 f = 0; f < (i64)nk; ++f) r += skey[f] < k;
+            dst[r] = src[e];
+        }
+        __threadfence_block();
+        __syncthreads();
+        int32_t *t = src; src = dst; dst = t;
+    } else {
     for (int pass = 0; pass < passes; ++pass) {
         const int shift = 4 * pass;
         uint32_t cnt[RD];
@@ -380,6 +400,7 @@ __global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64
         __threadfence_block();
         __syncthreads();
         int32_t *t = src; src = dst; dst = t;
+    }
     }
     // 3. ranks, ids, offsets
     u64 vox = 0;
@@ -451,11 +472,14 @@ __global__ void __launch_bounds__(VT) tab_voxels(const int32_t *__restrict__ lab
             // numpy: physical_coordinates(vox).mean(axis=0) -> row-sequential sum / n
             double sx = 0.0, sy = 0.0, sz = 0.0;
             const int32_t *list = voxels + cell.voxel_offset;
+            const uint32_t uny = (uint32_t)ny, unz = (uint32_t)nz;
             for (i64 e = 0; e < cell.count; ++e) {
-                const i64 p = list[e];
-                const double px = __dmul_rn((double)(p / (ny * nz)), dx);
-                const double py = __dmul_rn((double)((p / nz) % ny), dy);
-                const double pz = __dmul_rn((double)(p % nz), dz);
+                const uint32_t p = (uint32_t)list[e];
+                const uint32_t row = p / unz, kk = p - row * unz;
+                const uint32_t ii = row / uny, jj = row - ii * uny;
+                const double px = __dmul_rn((double)ii, dx);
+                const double py = __dmul_rn((double)jj, dy);
+                const double pz = __dmul_rn((double)kk, dz);
                 if (e == 0) { sx = px; sy = py; sz = pz; }
                 else { sx = __dadd_rn(sx, px); sy = __dadd_rn(sy, py); sz = __dadd_rn(sz, pz); }
             }
@@ -484,6 +508,7 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
     }
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(counters, 0, CT_CNT_WORDS * sizeof(int64_t), s);
+    cudaMemsetAsync(labels, 0xff, (size_t)(nx * ny * nz) * sizeof(int32_t), s);  // background = -1
     const i64 tiles = ((nz + LK - 1) / LK) * ((ny + LJ - 1) / LJ) * ((nx + LI - 1) / LI);
     ccl_local<<<(int)min(tiles, (i64)CT_NUM_SMS * 8), dim3(LK, LJ), 0, s>>>(mask, nx, ny, nz, labels, fg_list,
                                                                             counters);
