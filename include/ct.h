@@ -92,6 +92,19 @@ int ct_gaussian_residual(const void *raw, int raw_dtype, int64_t nx, int64_t ny,
                          const double *w, int rx, int ry, int rz, void *work,
                          double *bg_out, double *residual_out, void *q_out, int q_dtype, void *stream);
 
+/* K1 fast path of the fused pipeline: q = rint(max(raw - bg, 0)) for U8/U16
+ * raw, with bg accumulated by FMA and CERTIFIED exact: voxels whose residual
+ * lies within the rigorous FMA-vs-scipy error bound of a half-integer are
+ * listed in fix (device: [0] count, [1] overflow, [2..2+fix_cap) linear
+ * indices) and recomputed in scipy's exact order by a fix-up kernel, so q is
+ * bit-identical to ct_gaussian_residual's.  fix[1] != 0 (list overflow) means
+ * q is not certified: rerun ct_gaussian_residual.  eps_override > 0 replaces
+ * the bound (tests force the fix-up path with it).  Falls back to the exact
+ * path when a tiled kernel does not apply. */
+int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry,
+                  int rz, void *work, void *q_out, unsigned long long *fix, int64_t fix_cap, double eps_override,
+                  void *stream);
+
 /* float64 copy of a U8/U16/F64 volume (ref denoise.py:84, :158 astype). */
 int ct_to_f64(const void *in, int dtype, int64_t n, double *out, void *stream);
 

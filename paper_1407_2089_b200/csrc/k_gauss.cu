@@ -28,6 +28,7 @@ constexpr size_t SMEM_LIMIT = 200 * 1024;
 // Sliding-window accumulation for outputs at local rows base..base+B-1 of a
 // column whose element at local row q is col[q*stride].  Rows base-r .. base+B-1+r
 // must be valid.  Exactly scipy's order per output.
+template <bool FMA = false>
 __device__ __forceinline__ void window_taps(const double *__restrict__ col, int stride, int base, int r,
                                             const double *__restrict__ w, double (&acc)[B]) {
     double Lw[B], Rw[B];
@@ -46,7 +47,7 @@ __device__ __forceinline__ void window_taps(const double *__restrict__ col, int 
 #pragma unroll
             for (int b = 0; b < B; ++b) {
                 const double s = __dadd_rn(Lw[(b + u) % B], Rw[(b - u + B) % B]);
-                acc[b] = __dadd_rn(acc[b], __dmul_rn(s, wj));
+                acc[b] = FMA ? __fma_rn(s, wj, acc[b]) : __dadd_rn(acc[b], __dmul_rn(s, wj));
             }
             // slide to tap m+u+1: one new left element (row base-r+m+u+B),
             // one new right element (row base+r-(m+u+1)); both always in range.
@@ -61,7 +62,7 @@ __device__ __forceinline__ void window_taps(const double *__restrict__ col, int 
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             const double s = __dadd_rn(col[(base + b - j) * stride], col[(base + b + j) * stride]);
-            acc[b] = __dadd_rn(acc[b], __dmul_rn(s, wj));
+            acc[b] = FMA ? __fma_rn(s, wj, acc[b]) : __dadd_rn(acc[b], __dmul_rn(s, wj));
         }
     }
 }
@@ -71,7 +72,7 @@ __device__ __forceinline__ void window_taps(const double *__restrict__ col, int 
 // grid: x = column chunks of C, y = tiles of T along the axis, z = outer.
 // block: (C, T/B).  SMEM: tile[T+2r][C] doubles + w[r+1].
 // ---------------------------------------------------------------------------
-template <typename Tin>
+template <typename Tin, bool FMA = false>
 __global__ void __launch_bounds__(C *TMAX / B) gauss_strided(const Tin *__restrict__ in, double *__restrict__ out,
                                                             i64 L, i64 inner, const double *__restrict__ w, int r,
                                                             int T) {
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(C *TMAX / B) gauss_strided(const Tin *__restri
     const int ob = threadIdx.y * B;
     if (c >= cw || t0 + ob >= L) return;
     double acc[B];
-    window_taps(tile + c, C, r + ob, r, ws, acc);
+    window_taps<FMA>(tile + c, C, r + ob, r, ws, acc);
     double *dst = out + o * L * inner + c0 + c;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -110,11 +111,21 @@ __global__ void __launch_bounds__(C *TMAX / B) gauss_strided(const Tin *__restri
 // CTA = G lines (consecutive outer index) x whole line; lanes map to lines.
 // SMEM line stride S = roundup(L,B) + 2r (+1 if even: conflict-free LDS.64).
 // ---------------------------------------------------------------------------
-template <typename Traw, typename Tq>
+// Certification of the FMA fast path (fused pipeline only): results within
+// `cert` of a rounding boundary k+0.5 are appended to `fix` for the exact
+// recompute (ct_gaussian_q); fix[0] = count, fix[1] = overflow, fix[2..] = p.
+struct Cert {
+    double eps;
+    unsigned long long *fix;
+    long long cap;
+};
+
+template <typename Traw, typename Tq, bool FMA = false>
 __global__ void __launch_bounds__(512) gauss_contig(const double *__restrict__ in, i64 nlines, int L,
                                                       const double *__restrict__ w, int r, int S, int G,
                                                       const Traw *__restrict__ raw, double *__restrict__ bg_out,
-                                                      double *__restrict__ res_out, Tq *__restrict__ q_out) {
+                                                      double *__restrict__ res_out, Tq *__restrict__ q_out,
+                                                      Cert cert = Cert{0.0, nullptr, 0}) {
     extern __shared__ double smem[];
     double *tile = smem;                  // [G][S]
     double *ws = smem + (size_t)G * S;    // [r+1]
@@ -140,7 +151,7 @@ __global__ void __launch_bounds__(512) gauss_contig(const double *__restrict__ i
     const int ob = threadIdx.y * B;
     const bool active = g < gl && ob < L;
     double acc[B];
-    if (active) window_taps(tile + (size_t)g * S, 1, r + ob, r, ws, acc);
+    if (active) window_taps<FMA>(tile + (size_t)g * S, 1, r + ob, r, ws, acc);
     __syncthreads();
     if (active) {
 #pragma unroll
@@ -158,6 +169,14 @@ __global__ void __launch_bounds__(512) gauss_contig(const double *__restrict__ i
         const double res = d < 0.0 ? 0.0 : d;  // np.maximum(x, 0.0)
         if (res_out) res_out[p] = res;
         if (q_out) q_out[p] = (Tq)rint(res);
+        if (FMA && cert.fix) {
+            const double fr = __dadd_rn(res, -floor(res));
+            if (fabs(__dadd_rn(fr, -0.5)) <= cert.eps) {
+                const unsigned long long at = atomicAdd(&cert.fix[0], 1ull);
+                if ((long long)at < cert.cap) cert.fix[2 + at] = (unsigned long long)p;
+                else cert.fix[1] = 1;
+            }
+        }
     }
 }
 
@@ -199,7 +218,7 @@ __global__ void to_f64_copy(const Tin *__restrict__ in, double *__restrict__ out
 }
 
 // One pass along a strided axis; returns CT status.
-template <typename Tin>
+template <typename Tin, bool FMA = false>
 int pass_strided(const Tin *in, double *out, i64 outer, i64 L, i64 inner, const double *w, int r,
                  cudaStream_t s) {
     const i64 n = outer * L * inner;
@@ -213,10 +232,10 @@ int pass_strided(const Tin *in, double *out, i64 outer, i64 L, i64 inner, const 
         gauss_generic<Tin><<<ct::grid_for(n, 256), 256, 0, s>>>(in, out, outer, L, inner, w, r);
         return ct::check_launch("gauss_generic");
     }
-    cudaFuncSetAttribute(gauss_strided<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
+    cudaFuncSetAttribute(gauss_strided<Tin, FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
     dim3 grid((unsigned)((inner + C - 1) / C), (unsigned)((L + T - 1) / T), (unsigned)outer);
     dim3 block(C, T / B);
-    gauss_strided<Tin><<<grid, block, sm, s>>>(in, out, L, inner, w, r, T);
+    gauss_strided<Tin, FMA><<<grid, block, sm, s>>>(in, out, L, inner, w, r, T);
     return ct::check_launch("gauss_strided");
 }
 
@@ -308,4 +327,118 @@ extern "C" int ct_to_f64(const void *in, int dtype, int64_t n, double *out, void
     if (n <= 0) return CT_OK;
     CT_DISPATCH(dtype, T, { to_f64_copy<T><<<ct::grid_for(n, 256), 256, 0, s>>>((const T *)in, out, n); });
     return ct::check_launch("to_f64");
+}
+
+// ---------------------------------------------------------------------------
+// Fused-pipeline fast path: q = rint(max(raw - bg, 0)) with the three passes
+// accumulated by FMA (2 FP64 ops per tap instead of 3), certified exact.  Both
+// the FMA result and scipy's separately rounded result lie within
+// (2(rx+ry+rz)+9) u M of the real convolution (u = 2^-53, M = max input,
+// weights positive and summing to 1), so q can differ only where the residual
+// is that close to a half-integer; those voxels (fix list) are recomputed
+// exactly from their full dependency cone: pass-x values for the (2ry+1) x nz
+// rows around the voxel, pass y on its z-line, pass z at the voxel -- the same
+// operations in the same order as ct_gaussian_residual.
+// ---------------------------------------------------------------------------
+namespace {
+
+template <typename Traw, typename Tq>
+__global__ void __launch_bounds__(256) gauss_fixup(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz,
+                                                   const double *__restrict__ w, int rx, int ry, int rz,
+                                                   const unsigned long long *__restrict__ fix, long long cap,
+                                                   Tq *__restrict__ q_out) {
+    extern __shared__ double fsm[];
+    const int RJ = 2 * ry + 1;
+    double *P1 = fsm;                      // [RJ][nz]
+    double *P2 = fsm + (size_t)RJ * nz;    // [nz]
+    const double *wx = w, *wy = w + rx + 1, *wz = wy + ry + 1;
+    const long long cnt = min((long long)fix[0], cap);
+    for (long long f = blockIdx.x; f < cnt; f += gridDim.x) {
+        const i64 p = (i64)fix[2 + f];
+        const i64 k = p % nz, j = (p / nz) % ny, i = p / (ny * nz);
+        __syncthreads();
+        for (i64 e = threadIdx.x; e < (i64)RJ * nz; e += blockDim.x) {
+            const i64 t = e / nz - ry, kk = e % nz;
+            const i64 jj = ct::clampi(j + t, 0, ny - 1);
+            const Traw *col = raw + jj * nz + kk;
+            const i64 S = ny * nz;
+            double acc = __dmul_rn(ct::to_f64(col[i * S]), wx[0]);
+            for (int d = rx; d >= 1; --d) {
+                const double sm = __dadd_rn(ct::to_f64(col[ct::clampi(i - d, 0, nx - 1) * S]),
+                                            ct::to_f64(col[ct::clampi(i + d, 0, nx - 1) * S]));
+                acc = __dadd_rn(acc, __dmul_rn(sm, wx[d]));
+            }
+            P1[e] = acc;
+        }
+        __syncthreads();
+        for (i64 kk = threadIdx.x; kk < nz; kk += blockDim.x) {
+            // row offset t lives at index (t + ry); clamping was applied when staging
+            double acc = __dmul_rn(P1[(i64)ry * nz + kk], wy[0]);
+            for (int d = ry; d >= 1; --d) {
+                const double sm = __dadd_rn(P1[(i64)(ry - d) * nz + kk], P1[(i64)(ry + d) * nz + kk]);
+                acc = __dadd_rn(acc, __dmul_rn(sm, wy[d]));
+            }
+            P2[kk] = acc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double acc = __dmul_rn(P2[k], wz[0]);
+            for (int d = rz; d >= 1; --d) {
+                const double sm = __dadd_rn(P2[ct::clampi(k - d, 0, nz - 1)], P2[ct::clampi(k + d, 0, nz - 1)]);
+                acc = __dadd_rn(acc, __dmul_rn(sm, wz[d]));
+            }
+            const double dd = __dadd_rn(ct::to_f64(raw[p]), -acc);
+            q_out[p] = (Tq)rint(dd < 0.0 ? 0.0 : dd);
+        }
+    }
+}
+
+template <typename Traw>
+int gaussian_q_fast(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int rx, int ry, int rz, double *work,
+                    Traw *q, unsigned long long *fix, long long cap, double maxv, double eps_override,
+                    cudaStream_t s) {
+    const i64 N = nx * ny * nz;
+    double *p1 = work, *p2 = work + N;
+    const double *wx = w, *wy = w + rx + 1, *wz = wy + ry + 1;
+    cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
+    if (int st = pass_strided<Traw, true>(raw, p1, 1, nx, ny * nz, wx, rx, s)) return st;
+    if (int st = pass_strided<double, true>(p1, p2, nx, ny, nz, wy, ry, s)) return st;
+    int S = (int)(((nz + B - 1) / B) * B + 2 * rz);
+    if ((S & 1) == 0) S += 1;
+    const size_t sm = ((size_t)C * S + rz + 1) * sizeof(double);
+    const int nb = (int)((nz + B - 1) / B);
+    const double u = 1.1102230246251565e-16;  // 2^-53
+    Cert cert{eps_override > 0.0 ? eps_override : 4.0 * (2.0 * (rx + ry + rz) + 11.0) * u * maxv, fix, cap};
+    cudaFuncSetAttribute(gauss_contig<Traw, Traw, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
+    gauss_contig<Traw, Traw, true><<<(unsigned)((nx * ny + C - 1) / C), dim3(C, nb), sm, s>>>(
+        p2, nx * ny, (int)nz, wz, rz, S, C, raw, nullptr, nullptr, q, cert);
+    if (int st = ct::check_launch("gauss_contig fma")) return st;
+    const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
+    cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    gauss_fixup<Traw, Traw><<<CT_NUM_SMS, 256, fsm, s>>>(raw, nx, ny, nz, w, rx, ry, rz, fix, cap, q);
+    return ct::check_launch("gauss_fixup");
+}
+
+}  // namespace
+
+extern "C" int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx,
+                             int ry, int rz, void *work, void *q_out, unsigned long long *fix, int64_t fix_cap,
+                             double eps_override, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    // the fast kernels need the tiled paths (see pass_strided / pass_contig) and every axis filtered
+    const bool fast = rx >= 0 && ry >= 0 && rz >= 0 && nz <= 128 &&
+                      ((size_t)(TMAX + 2 * (rx > ry ? rx : ry)) * C + 64) * sizeof(double) <= SMEM_LIMIT &&
+                      nx * ny <= (1ll << 31) && (((nz + B - 1) / B) * B + 2 * rz + 1) * C * 8 < (i64)SMEM_LIMIT &&
+                      ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double) <= SMEM_LIMIT && nx <= 65535 * 128 &&
+                      ny <= 65535 * 128;
+    if (!fast || (dtype != CT_U8 && dtype != CT_U16)) {
+        if (fix) cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
+        return ct_gaussian_residual(raw, dtype, nx, ny, nz, w, rx, ry, rz, work, nullptr, nullptr, q_out, dtype,
+                                    stream);
+    }
+    if (dtype == CT_U8)
+        return gaussian_q_fast<uint8_t>((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, (double *)work,
+                                        (uint8_t *)q_out, fix, fix_cap, 255.0, eps_override, s);
+    return gaussian_q_fast<uint16_t>((const uint16_t *)raw, nx, ny, nz, w, rx, ry, rz, (double *)work,
+                                     (uint16_t *)q_out, fix, fix_cap, 65535.0, eps_override, s);
 }

@@ -78,6 +78,7 @@ class FramePipeline:
         dev = device or _dev.require_cuda()
         self.device = dev
         self.marks = None  # list of (stage, start_event, end_event) when timing
+        self.exact_k1 = False  # True: scipy-order K1 (no FMA fast path)
         E = lambda shape, dt: torch.empty(shape, dtype=dt, device=dev)  # noqa: E731
         Z = lambda shape, dt: torch.zeros(shape, dtype=dt, device=dev)  # noqa: E731
         cr = self.seg.closing_radius
@@ -91,6 +92,8 @@ class FramePipeline:
                     )
             self.w, self.r = device_taps(sig, dev)
             self.gwork = E(2 * n, torch.float64)
+            self.fix_cap = 1 << 20
+            self.fix = Z(2 + self.fix_cap, torch.int64)  # certified-K1 fix-up list
             self.q = E(self.dims, self.tdtype)
             self.med = E(self.dims, self.tdtype)
             self.hist = Z(65536, torch.int64)
@@ -144,8 +147,13 @@ class FramePipeline:
         rx, ry, rz = self.r
         self.hist.zero_()
         e = self._t0()
-        call("ct_gaussian_residual", raw.data_ptr(), self.code, nx, ny, nz, self.w.data_ptr(), rx, ry, rz,
-             self.gwork.data_ptr(), None, None, self.q.data_ptr(), self.code, s)
+        if self.exact_k1:
+            call("ct_gaussian_residual", raw.data_ptr(), self.code, nx, ny, nz, self.w.data_ptr(), rx, ry, rz,
+                 self.gwork.data_ptr(), None, None, self.q.data_ptr(), self.code, s)
+            self.fix[:2].zero_()
+        else:
+            call("ct_gaussian_q", raw.data_ptr(), self.code, nx, ny, nz, self.w.data_ptr(), rx, ry, rz,
+                 self.gwork.data_ptr(), self.q.data_ptr(), self.fix.data_ptr(), self.fix_cap, 0.0, s)
         self._t1("K1 gaussian", e)
         e = self._t0()
         call("ct_median", self.q.data_ptr(), self.code, nx, ny, nz, self.denoise.median_radius,
@@ -198,6 +206,8 @@ class FramePipeline:
         """Raise reference errors; return (counters, rows) or Detections."""
         if int(res.otsu[OTSU_STATUS].item()) == 2:
             raise DegenerateHistogramError("frame is constant; no threshold separates it")
+        if int(self.fix[1].item()):
+            raise RuntimeError("certified K1 fix-up list overflowed; rerun with exact_k1=True")
         cnt = res.cells.counters.cpu().numpy()
         if cnt[CNT_OVERFLOW]:
             raise RuntimeError("component capacity exceeded; raise FramePipeline(capacity=...)")

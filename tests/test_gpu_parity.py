@@ -265,3 +265,43 @@ def test_large_frame_properties(cuda):
     assert int(vres.state[5]) == 0
     assert torch.all(vres.distance[vres.mask.bool()] == 0)
     assert torch.all(vres.distance[~vres.mask.bool()] > 0)
+
+
+def _q_exact_and_fast(raw, spacing, sigma_um, eps=0.0, cap=1 << 20):
+    from paper_1407_2089_b200 import _dev
+    from paper_1407_2089_b200._lib import call
+
+    nx, ny, nz = (int(d) for d in raw.shape)
+    sig = tuple(sigma_um / s for s in (spacing.dx, spacing.dy, spacing.dz))
+    w, (rx, ry, rz) = D.device_taps(sig, raw.device)
+    work = torch.empty(2 * nx * ny * nz, dtype=torch.float64, device=raw.device)
+    q1 = torch.empty_like(raw)
+    q2 = torch.empty_like(raw)
+    fix = torch.zeros(2 + cap, dtype=torch.int64, device=raw.device)
+    code = _dev.ct_code(raw)
+    s = _dev.stream_handle()
+    call("ct_gaussian_residual", raw.data_ptr(), code, nx, ny, nz, w.data_ptr(), rx, ry, rz, work.data_ptr(), None,
+         None, q1.data_ptr(), code, s)
+    call("ct_gaussian_q", raw.data_ptr(), code, nx, ny, nz, w.data_ptr(), rx, ry, rz, work.data_ptr(),
+         q2.data_ptr(), fix.data_ptr(), cap, eps, s)
+    return q1, q2, fix[:2].cpu().numpy()
+
+
+def test_certified_fma_k1_matches_exact(cuda):
+    for spec in (synth.C1, synth.SceneSpec(128, 96, 48, "u16", n_cells=20, seed=4)):
+        raw = synth.generate(spec, 2, synth.CELL)
+        q1, q2, fx = _q_exact_and_fast(raw, ANISO, 10.0)
+        assert fx[1] == 0
+        assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
+
+
+def test_certified_fixup_recomputes_exactly(cuda):
+    # eps 0.6 flags every voxel: the fix-up kernel alone must reproduce K1
+    rng = np.random.default_rng(12)
+    v = torch.from_numpy(rng.integers(0, 256, size=(40, 36, 20), dtype=np.uint8)).cuda()
+    q1, q2, fx = _q_exact_and_fast(v, ANISO, 3.0, eps=0.6)
+    assert fx[0] == v.numel() and fx[1] == 0
+    assert torch.equal(q1, q2)
+    # overflow is reported when the list is too small
+    _, _, fx = _q_exact_and_fast(v, ANISO, 3.0, eps=0.6, cap=10)
+    assert fx[1] == 1
