@@ -16,6 +16,8 @@
 // Each thread computes B consecutive outputs along the filtered axis and keeps
 // a left and a right window of B inputs in registers that slide one step per
 // tap, so a tap costs 2 shared loads per B outputs (3B FP64 ops).
+#include <type_traits>
+
 #include "ct_common.cuh"
 
 namespace {
@@ -72,6 +74,25 @@ __device__ __forceinline__ void window_taps(const double *__restrict__ col, int 
 // grid: x = column chunks of C, y = tiles of T along the axis, z = outer.
 // block: (C, T/B).  SMEM: tile[T+2r][C] doubles + w[r+1].
 // ---------------------------------------------------------------------------
+// CH consecutive elements (one vector load: 4 x u8, 4 x u16, 2 x f64) -> doubles
+template <typename Tin>
+struct Chunk {
+    static constexpr int CH = sizeof(Tin) == 8 ? 2 : 4;
+    using V = typename std::conditional<sizeof(Tin) == 1, uint32_t,
+                                        typename std::conditional<sizeof(Tin) == 2, uint2, double2>::type>::type;
+    __device__ static __forceinline__ void to_f64(const V &v, double (&o)[CH]) {
+        if constexpr (sizeof(Tin) == 1) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[e] = (double)((v >> (8 * e)) & 0xffu);
+        } else if constexpr (sizeof(Tin) == 2) {
+            o[0] = (double)(v.x & 0xffffu); o[1] = (double)(v.x >> 16);
+            o[2] = (double)(v.y & 0xffffu); o[3] = (double)(v.y >> 16);
+        } else {
+            o[0] = v.x; o[1] = v.y;
+        }
+    }
+};
+
 template <typename Tin, bool FMA = false>
 __global__ void __launch_bounds__(C *TMAX / B) gauss_strided(const Tin *__restrict__ in, double *__restrict__ out,
                                                             i64 L, i64 inner, const double *__restrict__ w, int r,
@@ -87,10 +108,39 @@ __global__ void __launch_bounds__(C *TMAX / B) gauss_strided(const Tin *__restri
     const int tid = threadIdx.y * C + threadIdx.x, nth = C * blockDim.y;
     for (int j = tid; j <= r; j += nth) ws[j] = w[j];
     const Tin *src = in + o * L * inner + c0;
-    for (int idx = tid; idx < R * C; idx += nth) {
-        const int row = idx / C, c = idx - row * C;
-        const i64 pos = ct::clampi(t0 - r + row, 0, L - 1);
-        tile[idx] = c < cw ? ct::to_f64(src[pos * inner + c]) : 0.0;
+    using CK = Chunk<Tin>;
+    constexpr int CH = CK::CH, CPR = C / CH;
+    if (cw == C && (inner % CH) == 0 && ((uintptr_t)in % sizeof(typename CK::V)) == 0) {
+        // vector loads, up to 8 in flight per thread, then convert + store
+        const int total = R * CPR;
+        for (int q0 = tid; q0 < total; q0 += 8 * nth) {
+            typename CK::V buf[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * nth;
+                if (q < total) {
+                    const int row = q / CPR, h = q - row * CPR;
+                    const i64 pos = ct::clampi(t0 - r + row, 0, L - 1);
+                    buf[u] = __ldg((const typename CK::V *)(src + pos * inner) + h);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * nth;
+                if (q < total) {
+                    double v[CH];
+                    CK::to_f64(buf[u], v);
+#pragma unroll
+                    for (int e = 0; e < CH; ++e) tile[q * CH + e] = v[e];
+                }
+            }
+        }
+    } else {
+        for (int idx = tid; idx < R * C; idx += nth) {
+            const int row = idx / C, c = idx - row * C;
+            const i64 pos = ct::clampi(t0 - r + row, 0, L - 1);
+            tile[idx] = c < cw ? ct::to_f64(src[pos * inner + c]) : 0.0;
+        }
     }
     __syncthreads();
     const int c = threadIdx.x;
@@ -134,6 +184,7 @@ __global__ void __launch_bounds__(512) gauss_contig(const double *__restrict__ i
     const int tid = threadIdx.y * blockDim.x + threadIdx.x, nth = blockDim.x * blockDim.y;
     for (int j = tid; j <= r; j += nth) ws[j] = w[j];
     const double *src = in + line0 * L;
+#pragma unroll 4
     for (int idx = tid; idx < gl * L; idx += nth) {
         const int g = idx / L, k = idx - g * L;
         tile[g * S + r + k] = src[idx];

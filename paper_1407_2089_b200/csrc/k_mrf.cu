@@ -24,6 +24,8 @@
 //               run through ct_mrf_step driven by the host.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <type_traits>
+
 #include "ct_common.cuh"
 
 namespace {
@@ -149,38 +151,18 @@ struct StepElem {  // (proposal - original)^2 for the step from `cur` (nullptr =
     }
 };
 
-// (lap - mean)^2 from the int32 Laplacian array of the streaming pass;
-// mean = exact_sum / n (numpy's pairwise sum of integer-valued doubles is exact)
+// (lap - mean)^2 from the Laplacian array of the streaming pass (int16 for
+// u8 input: |lap| <= 6*255; int32 for u16); mean = exact_sum / n (numpy's
+// pairwise sum of integer-valued doubles is exact)
+template <typename LT>
 struct LapArrSq {
-    const int32_t *lap;
-    const long long *int_sum;
-    i64 n;
+    const LT *lap;
+    const double *mean;  // device: exact_sum / n, computed once (lap_mean)
     __device__ double operator()(i64 e) const {
-        const double m = __ddiv_rn((double)*int_sum, (double)n);
-        const double x = __dadd_rn((double)lap[e], -m);
+        const double x = __dadd_rn((double)lap[e], -*mean);
         return __dmul_rn(x, x);
     }
 };
-
-// numpy pairwise_sum leaf (n <= 128) over an SMEM array
-__device__ double pw_leaf(const double *a, int n) {
-    if (n < 8) {
-        double res = 0.0;
-        for (int i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
-        return res;
-    }
-    double r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int i;
-    for (i = 8; i < n - (n % 8); i += 8)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
-}
 
 // Leaf lookup inside a subtree without enumeration: node sizes at each depth
 // of a subtree form a tiny set, so leaf counts per size are tabulated once per
@@ -229,40 +211,64 @@ __device__ void pw_shape(PwShape &sh, int m0) {
         }
 }
 
-// CTA b: exact numpy-order sum of depth-D node b.  Elements staged in SMEM;
-// leaf t found by descending with the tabulated leaf counts; internal nodes
+// CTA b: exact numpy-order sum of depth-D node b.  Elements are evaluated in
+// place by the leaf lanes (f(e) reads global memory); leaf t found by descending with the tabulated leaf counts; internal nodes
 // combined level by level (slot = path bits at that depth), so every add is
 // left + right exactly as numpy's recursion performs it.
 template <class F>
 __global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__restrict__ partial) {
-    extern __shared__ double vals[];
     __shared__ PwShape sh;
     __shared__ double lv[2][1 << PW_MAXD];  // values per level slot (ping-pong)
     __shared__ int nleaves;
+    __shared__ double lval[MAX_LEAVES];
+    __shared__ int lpos[MAX_LEAVES];  // depth << 16 | slot
     i64 off, len;
     pw_node(n, D, blockIdx.x, off, len);
-    for (int i = threadIdx.x; i < len; i += PT) vals[i] = f(off + i);
     if (threadIdx.x == 0) {
         pw_shape(sh, (int)len);
         nleaves = sh.leaves[0][0];
     }
     __syncthreads();
-    // leaves: thread t takes leaf t, recording its depth and path slot
-    int my_depth = -1, my_slot = 0;
-    double my_val = 0.0;
-    if (threadIdx.x < nleaves) {
-        int t = threadIdx.x, o = 0, m = (int)len, d = 0, slot = 0;
-        while (m > 128) {
-            const int l = (int)pw_left(m);
-            const int nl = pw_lookup(sh, d + 1, l);
-            slot <<= 1;
-            if (t < nl) m = l;
-            else { t -= nl; o += l; m -= l; slot |= 1; }
-            ++d;
+    // leaves: 8 lanes per leaf; lane j accumulates numpy's r[j] (a[j], a[j+8],
+    // ...), then the group combines ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by
+    // shuffles and lane 0 adds the n % 8 tail -- numpy's leaf order exactly.
+    const int grp = threadIdx.x >> 3, sub = threadIdx.x & 7;
+    for (int base = 0; base < nleaves; base += PT / 8) {
+        const int L = base + grp;
+        int o = 0, m = 0, d = 0, slot = 0;
+        if (L < nleaves) {
+            int t = L;
+            m = (int)len;
+            while (m > 128) {
+                const int l = (int)pw_left(m);
+                const int nl = pw_lookup(sh, d + 1, l);
+                slot <<= 1;
+                if (t < nl) m = l;
+                else { t -= nl; o += l; m -= l; slot |= 1; }
+                ++d;
+            }
         }
-        my_val = pw_leaf(vals + o, m);
-        my_depth = d;
-        my_slot = slot;
+        const i64 a0 = off + o;  // leaf elements f(a0 .. a0+m-1), evaluated in place
+        const int lim = m - (m & 7);
+        double r = m >= 8 ? f(a0 + sub) : 0.0;
+        for (int i = 8 + sub; i < lim; i += 8) r = __dadd_rn(r, f(a0 + i));
+        double t = __shfl_down_sync(0xffffffffu, r, 1, 8);
+        if ((sub & 1) == 0) r = __dadd_rn(r, t);
+        t = __shfl_down_sync(0xffffffffu, r, 2, 8);
+        if ((sub & 3) == 0) r = __dadd_rn(r, t);
+        t = __shfl_down_sync(0xffffffffu, r, 4, 8);
+        if (sub == 0 && L < nleaves) {
+            double res;
+            if (m < 8) {
+                res = 0.0;
+                for (int i = 0; i < m; ++i) res = __dadd_rn(res, f(a0 + i));
+            } else {
+                res = __dadd_rn(r, t);
+                for (int i = lim; i < m; ++i) res = __dadd_rn(res, f(a0 + i));
+            }
+            lval[L] = res;
+            lpos[L] = (d << 16) | slot;
+        }
     }
     // combine bottom-up: at depth d, slots of existing nodes; a node at depth d
     // is a leaf (value from its thread) or internal (children at d+1)
@@ -271,7 +277,8 @@ __global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__re
     for (int d = dmax; d >= 0; --d) {
         // nodes at depth d: write leaves of this depth, combine internal ones
         __syncthreads();
-        if (my_depth == d) nxt[my_slot] = my_val;
+        for (int L = threadIdx.x; L < nleaves; L += PT)
+            if ((lpos[L] >> 16) == d) nxt[lpos[L] & 0xffff] = lval[L];
         // internal nodes at depth d combine children (depth d+1 values in cur)
         for (int sl = threadIdx.x; sl < (1 << d); sl += PT) {
             // descend the path of slot sl to learn whether it exists / is internal
@@ -309,13 +316,11 @@ int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s
         return ct::check_launch("pairwise empty");
     }
     const int D = pw_depth(n);
-    const size_t sm = (size_t)pw_max_node(n, D) * sizeof(double);
-    if (sm > 200 * 1024) {
+    if (pw_max_node(n, D) > 64 * MAX_LEAVES) {
         ct::set_error("pairwise subtree too large");
         return CT_ERR_UNSUPPORTED;
     }
-    cudaFuncSetAttribute(pw_subtree<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    pw_subtree<F><<<(unsigned)(1ll << D), PT, sm, s>>>(f, n, D, partial);
+    pw_subtree<F><<<(unsigned)(1ll << D), PT, 0, s>>>(f, n, D, partial);
     if (int st = ct::check_launch("pw_subtree")) return st;
     pw_fold<<<1, 1024, 0, s>>>(partial, D, out);
     return ct::check_launch("pw_fold");
@@ -325,86 +330,6 @@ int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s
 enum { S_DELTA = 0, S_SIGMA, S_SIGMA_STATUS, S_NNZ, S_NORM, S_DECISION, S_SUM1, S_SUM2, S_SUM3, S_WORDS };
 // scalar words (u64) in the workspace
 enum { W_NNZ = 0, W_BEST_BITS, W_MOVED, W_LAPSUM, W_WORDS = 8 };
-
-// ---------------------------------------------------------------------------
-// Fused statistics pass over an integer volume (one read of the input):
-// histogram, #{sign sum != 0}, exact int64 sum of the interior Laplacian.
-// Tiles of (TI x TJ x TK) voxels with a clamped halo staged in SMEM.
-// ---------------------------------------------------------------------------
-constexpr int STI = 4, STJ = 8, STK = 32;
-
-template <typename T>
-__global__ void __launch_bounds__(256) mrf_stats_int(const T *__restrict__ v, i64 nx, i64 ny, i64 nz,
-                                                     unsigned long long *__restrict__ ghist,
-                                                     unsigned long long *__restrict__ scal) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    int *tile = (int *)dsm;  // [STI+2][STJ+2][STK+2]
-    constexpr bool BYTE = sizeof(T) == 1;
-    ct::ByteHist256 bh;
-    uint32_t *sh16 = nullptr;  // u16: [4096] SMEM bins
-    unsigned char *hbase = dsm + (STI + 2) * (STJ + 2) * (STK + 2) * sizeof(int);
-    if (BYTE) bh.init(hbase);
-    else {
-        sh16 = (uint32_t *)hbase;
-        for (int b = threadIdx.x; b < 4096; b += 256) sh16[b] = 0;
-    }
-    const int tk = threadIdx.x & 31, tj = threadIdx.x >> 5;
-    const i64 ntk = (nz + STK - 1) / STK, ntj = (ny + STJ - 1) / STJ, nti = (nx + STI - 1) / STI;
-    const i64 ntiles = ntk * ntj * nti;
-    unsigned long long nnz = 0;
-    long long lsum = 0;
-    int since_flush = 0;
-    for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const i64 k0 = (t % ntk) * STK, j0 = ((t / ntk) % ntj) * STJ, i0 = (t / (ntk * ntj)) * STI;
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < (STI + 2) * (STJ + 2) * (STK + 2); idx += 256) {
-            const int kk = idx % (STK + 2), jj = (idx / (STK + 2)) % (STJ + 2), ii = idx / ((STK + 2) * (STJ + 2));
-            const i64 i = ct::clampi(i0 + ii - 1, 0, nx - 1), j = ct::clampi(j0 + jj - 1, 0, ny - 1),
-                      k = ct::clampi(k0 + kk - 1, 0, nz - 1);
-            tile[idx] = (int)v[(i * ny + j) * nz + k];
-        }
-        __syncthreads();
-        const i64 j = j0 + tj, k = k0 + tk;
-#pragma unroll
-        for (int a = 0; a < STI; ++a) {
-            const i64 i = i0 + a;
-            if (i >= nx || j >= ny || k >= nz) continue;
-#define TL(da, db, dc) tile[((a + 1 + (da)) * (STJ + 2) + (tj + 1 + (db))) * (STK + 2) + (tk + 1 + (dc))]
-            const int c = TL(0, 0, 0);
-            const int xm = TL(-1, 0, 0), xp = TL(1, 0, 0), ym = TL(0, -1, 0), yp = TL(0, 1, 0), zm = TL(0, 0, -1),
-                      zp = TL(0, 0, 1);
-#undef TL
-            const int s = ((xm > c) - (xm < c)) + ((c > xp) - (c < xp)) + ((ym > c) - (ym < c)) +
-                          ((c > yp) - (c < yp)) + ((zm > c) - (zm < c)) + ((c > zp) - (c < zp));
-            nnz += s != 0;
-            if (i > 0 && i < nx - 1 && j > 0 && j < ny - 1 && k > 0 && k < nz - 1)
-                lsum += (long long)(xm + xp + ym + yp + zm + zp) - 6ll * c;
-            if (BYTE) bh.add(c);
-            else if (c < 4096) atomicAdd(&sh16[c], 1u);
-            else atomicAdd(&ghist[c], 1ull);
-        }
-        if (BYTE && ++since_flush == 60) {  // <= 240 adds per thread between flushes
-            bh.flush();
-            since_flush = 0;
-        }
-    }
-    for (int o = 16; o; o >>= 1) {
-        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
-        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&scal[W_NNZ], nnz);
-        atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
-    }
-    if (BYTE) {
-        bh.flush();
-        bh.to_global(ghist);
-    } else {
-        __syncthreads();
-        for (int b = threadIdx.x; b < 4096; b += 256)
-            if (sh16[b]) atomicAdd(&ghist[b], (unsigned long long)sh16[b]);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Streaming statistics pass (integer input): a CTA owns MJ rows (j) x all k
@@ -418,23 +343,20 @@ __global__ void __launch_bounds__(256) mrf_stats_int(const T *__restrict__ v, i6
 constexpr int MJ = 8;
 constexpr int MIPER = 64;  // planes per CTA
 
-template <typename T>
+template <typename T, typename LT>
 __global__ void __launch_bounds__(256) mrf_stream_int(const T *__restrict__ v, i64 nx, i64 ny, int nz,
                                                       unsigned long long *__restrict__ ghist,
                                                       unsigned long long *__restrict__ scal,
-                                                      int32_t *__restrict__ lap) {
+                                                      LT *__restrict__ lap) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const int PL = (MJ + 2) * nz;  // staged plane elements
     int *ring = (int *)dsm;        // [3][PL]
     unsigned char *hbase = dsm + ((3 * PL * 4 + 15) & ~15);
     constexpr bool BYTE = sizeof(T) == 1;
-    ct::ByteHist256 bh;
-    uint32_t *sh16 = nullptr;
-    if (BYTE) bh.init(hbase);
-    else {
-        sh16 = (uint32_t *)hbase;
-        for (int b = threadIdx.x; b < 4096; b += 256) sh16[b] = 0;
-    }
+    // u8: one 256-bin u32 histogram per warp (8 KB); u16: 4096 shared bins
+    uint32_t *sh16 = (uint32_t *)hbase;
+    uint32_t *wh = sh16 + (threadIdx.x >> 5) * 256;
+    for (int b = threadIdx.x; b < (BYTE ? 8 * 256 : 4096); b += 256) sh16[b] = 0;
     const i64 nJ = (ny + MJ - 1) / MJ;
     const i64 j0 = (blockIdx.x % nJ) * MJ;
     const i64 i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
@@ -475,7 +397,6 @@ __global__ void __launch_bounds__(256) mrf_stream_int(const T *__restrict__ v, i
     for (int q = 0; q < np_; ++q) prev[q] = ring[2 * PL + (pj[q] + 1) * nz + pk[q]];
     unsigned long long nnz = 0;
     long long lsum = 0;
-    int since = 0;
     for (i64 i = i0; i < i1; ++i) {
         const int cs = (int)((i - i0) % 3), ns = (int)((i - i0 + 1) % 3), fs = (int)((i - i0 + 2) % 3);
         load_plane(i + 2, regs);  // in flight while plane i is processed
@@ -495,18 +416,14 @@ __global__ void __launch_bounds__(256) mrf_stream_int(const T *__restrict__ v, i
             if (iint && j > 0 && j < ny - 1 && k > 0 && k < nz - 1) {
                 const int l = (xm + xp + ym + yp + zm + zp) - 6 * c;
                 lsum += l;
-                lap[((i - 1) * my + (j - 1)) * mz + (k - 1)] = l;
+                lap[((i - 1) * my + (j - 1)) * mz + (k - 1)] = (LT)l;
             }
-            if (BYTE) bh.add(c);
+            if (BYTE) atomicAdd(&wh[c], 1u);
             else if (c < 4096) atomicAdd(&sh16[c], 1u);
             else atomicAdd(&ghist[c], 1ull);
             prev[q] = c;
         }
         store_plane(fs, regs);
-        if (BYTE && ++since == 60) {  // <= 60 * MAXP adds per thread between flushes
-            bh.flush();
-            since = 0;
-        }
         __syncthreads();
     }
     for (int o = 16; o; o >>= 1) {
@@ -517,13 +434,129 @@ __global__ void __launch_bounds__(256) mrf_stream_int(const T *__restrict__ v, i
         atomicAdd(&scal[W_NNZ], nnz);
         atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
     }
+    __syncthreads();
     if (BYTE) {
-        bh.flush();
-        bh.to_global(ghist);
+        unsigned t = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += sh16[q * 256 + threadIdx.x];
+        if (t) atomicAdd(&ghist[threadIdx.x], (unsigned long long)t);
     } else {
-        __syncthreads();
         for (int b = threadIdx.x; b < 4096; b += 256)
             if (sh16[b]) atomicAdd(&ghist[b], (unsigned long long)sh16[b]);
+    }
+}
+
+// Same pass specialised for nz == NZ (32, 64, 128): thread t owns column
+// k = t % NZ of rows t / NZ + p * (256 / NZ); planes staged as raw T in SMEM
+// via 32-bit vector loads; 32-bit indexing (volumes < 2^31 voxels).
+template <typename T, typename LT, int NZ>
+__global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, int nx, int ny,
+                                                     unsigned long long *__restrict__ ghist,
+                                                     unsigned long long *__restrict__ scal,
+                                                     LT *__restrict__ lap) {
+    constexpr int RP = 256 / NZ;           // rows per thread sweep
+    constexpr int P = MJ / RP;             // positions per thread
+    constexpr int PL = (MJ + 2) * NZ;      // staged plane elements
+    constexpr int PW = PL * (int)sizeof(T) / 4;  // 32-bit words per plane
+    constexpr int LW = (PW + 255) / 256;   // words per thread
+    constexpr int RW = NZ * (int)sizeof(T) / 4;  // words per row
+    constexpr bool BYTE = sizeof(T) == 1;
+    __shared__ __align__(16) T ring[3][PL];
+    __shared__ uint32_t hsm[BYTE ? 8 * 256 : 4096];
+    uint32_t *wh = hsm + (BYTE ? (threadIdx.x >> 5) * 256 : 0);
+    for (int b = threadIdx.x; b < (BYTE ? 8 * 256 : 4096); b += 256) hsm[b] = 0;
+    const int nJ = (ny + MJ - 1) / MJ;
+    const int j0 = (blockIdx.x % nJ) * MJ;
+    const int i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
+    const int my = ny - 2, mz = NZ - 2;
+    const int k = threadIdx.x % NZ, jt = threadIdx.x / NZ;
+    // word w of a plane: row w / RW (clamped j), word w % RW
+    int goff[LW];
+#pragma unroll
+    for (int q = 0; q < LW; ++q) {
+        const int w = threadIdx.x + q * 256;
+        const int row = w / RW, cw = w - row * RW;
+        const int j = min(max(j0 - 1 + row, 0), ny - 1);
+        goff[q] = w < PW ? j * RW + cw : 0;
+    }
+    const uint32_t *vw = (const uint32_t *)v;
+    const size_t plane_w = (size_t)ny * RW;
+    auto load_plane = [&](int i, uint32_t (&regs)[LW]) {
+        const int ic = min(max(i, 0), nx - 1);
+        const uint32_t *base = vw + (size_t)ic * plane_w;
+#pragma unroll
+        for (int q = 0; q < LW; ++q)
+            if (threadIdx.x + q * 256 < PW) regs[q] = __ldg(base + goff[q]);
+    };
+    auto store_plane = [&](int slot, const uint32_t (&regs)[LW]) {
+        uint32_t *dst = (uint32_t *)ring[slot];
+#pragma unroll
+        for (int q = 0; q < LW; ++q)
+            if (threadIdx.x + q * 256 < PW) dst[threadIdx.x + q * 256] = regs[q];
+    };
+    uint32_t regs[LW];
+    load_plane(i0 - 1, regs);
+    store_plane(2, regs);
+    load_plane(i0, regs);
+    store_plane(0, regs);
+    load_plane(i0 + 1, regs);
+    store_plane(1, regs);
+    __syncthreads();
+    int prev[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) prev[p] = ring[2][(jt + p * RP + 1) * NZ + k];
+    unsigned nnz = 0;
+    long long lsum = 0;
+    int cs = 0, ns = 1, fs = 2;
+    for (int i = i0; i < i1; ++i) {
+        load_plane(i + 2, regs);  // in flight while plane i is processed
+        const T *C = ring[cs], *X = ring[ns];
+        const bool iint = i > 0 && i < nx - 1;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int jj = jt + p * RP, j = j0 + jj;
+            if (j < ny) {
+                const int o = (jj + 1) * NZ + k;
+                const int c = C[o];
+                const int xm = prev[p], xp = X[o];
+                const int ym = C[o - NZ], yp = C[o + NZ];
+                const int zm = k > 0 ? C[o - 1] : c, zp = k < NZ - 1 ? C[o + 1] : c;
+                const int sgs = ((xm > c) - (xm < c)) + ((c > xp) - (c < xp)) + ((ym > c) - (ym < c)) +
+                                ((c > yp) - (c < yp)) + ((zm > c) - (zm < c)) + ((c > zp) - (c < zp));
+                nnz += sgs != 0;
+                if (iint && j > 0 && j < ny - 1 && k > 0 && k < NZ - 1) {
+                    const int l = (xm + xp + ym + yp + zm + zp) - 6 * c;
+                    lsum += l;
+                    lap[((unsigned)(i - 1) * (unsigned)my + (unsigned)(j - 1)) * (unsigned)mz + (unsigned)(k - 1)] =
+                        (LT)l;
+                }
+                if (BYTE || c < 4096) atomicAdd(&wh[c], 1u);
+                else atomicAdd(&ghist[c], 1ull);
+                prev[p] = c;
+            }
+        }
+        store_plane(fs, regs);
+        __syncthreads();
+        const int t = cs; cs = ns; ns = fs; fs = t;
+    }
+    unsigned long long nnz64 = nnz;
+    for (int o = 16; o; o >>= 1) {
+        nnz64 += __shfl_xor_sync(0xffffffffu, nnz64, o);
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&scal[W_NNZ], nnz64);
+        atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
+    }
+    __syncthreads();
+    if (BYTE) {
+        unsigned t = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += hsm[q * 256 + threadIdx.x];
+        if (t) atomicAdd(&ghist[threadIdx.x], (unsigned long long)t);
+    } else {
+        for (int b = threadIdx.x; b < 4096; b += 256)
+            if (hsm[b]) atomicAdd(&ghist[b], (unsigned long long)hsm[b]);
     }
 }
 
@@ -539,12 +572,14 @@ __global__ void mrf_nnz_generic(const T *__restrict__ v, i64 nx, i64 ny, i64 nz,
 }
 
 // delta from the histogram of integer values (min gap of non-empty bins)
-__global__ void delta_from_hist(const uint64_t *__restrict__ hist, double *state) {
+// (nbins: 256 for u8 input -- no other bin can be non-empty -- else 65536)
+__global__ void delta_from_hist(const uint64_t *__restrict__ hist, int nbins, double *state) {
     __shared__ int prev_of[1024];
     __shared__ int wg[32];
     const int t = threadIdx.x;
+    const int per = (nbins + 1023) / 1024;
     int first = -1, last = -1, gap = INT32_MAX;
-    for (int b = t * 64; b < t * 64 + 64; ++b) {
+    for (int b = t * per; b < min(t * per + per, nbins); ++b) {
         if (!hist[b]) continue;
         if (last >= 0) gap = min(gap, b - last);
         if (first < 0) first = b;
@@ -584,6 +619,9 @@ __global__ void delta_store(const unsigned long long *best_bits, double *state) 
 }
 
 __global__ void mean_from_sum(double *state, i64 n) { state[S_SUM1] = __ddiv_rn(state[S_SUM1], (double)n); }
+__global__ void lap_mean(double *state, const long long *sum, i64 n) {
+    state[S_SUM1] = __ddiv_rn((double)*sum, (double)n);
+}
 
 // int_path: norm^2 = delta^2 * nnz (exact); else state[S_SUM3] holds the tree sum
 __global__ void mrf_decide(double *state, i64 n_interior, const unsigned long long *scal, int int_path) {
@@ -640,7 +678,7 @@ __global__ void step_finish(double *out2, const unsigned long long *moved) {
 }
 
 struct MrfWork {
-    int32_t *lap;              // integer path: n_interior Laplacians
+    void *lap;                 // integer path: n_interior Laplacians (int16 for u8, int32 for u16)
     double *partial;           // 2 * 2^D
     unsigned long long *scal;  // W_WORDS
     double *sorted;            // float path: n
@@ -665,8 +703,8 @@ MrfWork mrf_carve(void *work, i64 n, int dtype, i64 ni) {
     char *p = (char *)work;
     w.lap = nullptr;
     if (dtype != CT_F64) {
-        w.lap = (int32_t *)p;
-        p += al(ni * 4);
+        w.lap = p;
+        p += al(ni * (dtype == CT_U8 ? 2 : 4));
     }
     const i64 parts = 1ll << pw_depth(n > 0 ? n : 1);
     w.partial = (double *)p; p += al(parts * 8 * 2 + 64);
@@ -684,22 +722,29 @@ template <typename T>
 int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint64_t *hist, cudaStream_t s) {
     const i64 mx = nx - 2 > 0 ? nx - 2 : 0, my = ny - 2 > 0 ? ny - 2 : 0, mz = nz - 2 > 0 ? nz - 2 : 0;
     const i64 ni = mx * my * mz;
-    const size_t hb = sizeof(T) == 1 ? ct::ByteHist256::kBytes : 4096 * sizeof(uint32_t);
-    if (nz <= 128) {
+    using LT = typename std::conditional<sizeof(T) == 1, int16_t, int32_t>::type;
+    LT *lap = (LT *)w.lap;
+    const i64 blocks = ((ny + MJ - 1) / MJ) * ((nx + MIPER - 1) / MIPER);
+    if ((nz == 32 || nz == 64 || nz == 128) && ((uintptr_t)v & 3) == 0 && nx * ny * nz < (1ll << 31)) {
+        auto kern = nz == 32 ? mrf_stream_nz<T, LT, 32> : nz == 64 ? mrf_stream_nz<T, LT, 64> : mrf_stream_nz<T, LT, 128>;
+        kern<<<(unsigned)blocks, 256, 0, s>>>(v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal, lap);
+        if (int st = ct::check_launch("mrf_stream_nz")) return st;
+    } else if (nz <= 128) {
+        const size_t hb = sizeof(T) == 1 ? 8 * 256 * sizeof(uint32_t) : 4096 * sizeof(uint32_t);
         const size_t sm = ((3 * (MJ + 2) * nz * 4 + 15) & ~(size_t)15) + hb;
-        cudaFuncSetAttribute(mrf_stream_int<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        const i64 blocks = ((ny + MJ - 1) / MJ) * ((nx + MIPER - 1) / MIPER);
-        mrf_stream_int<T><<<(unsigned)blocks, 256, sm, s>>>(v, nx, ny, (int)nz, (unsigned long long *)hist, w.scal,
-                                                           w.lap);
+        cudaFuncSetAttribute(mrf_stream_int<T, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        mrf_stream_int<T, LT><<<(unsigned)blocks, 256, sm, s>>>(v, nx, ny, (int)nz, (unsigned long long *)hist,
+                                                               w.scal, lap);
         if (int st = ct::check_launch("mrf_stream_int")) return st;
     } else {
         ct::set_error("integer MRF supports nz <= 128");
         return CT_ERR_UNSUPPORTED;
     }
-    delta_from_hist<<<1, 1024, 0, s>>>(hist, state);
+    delta_from_hist<<<1, 1024, 0, s>>>(hist, sizeof(T) == 1 ? 256 : 65536, state);
     if (int st = ct::check_launch("delta_from_hist")) return st;
     if (ni >= 2) {
-        LapArrSq f{w.lap, (const long long *)&w.scal[W_LAPSUM], ni};
+        lap_mean<<<1, 1, 0, s>>>(state, (const long long *)&w.scal[W_LAPSUM], ni);
+        LapArrSq<LT> f{lap, &state[S_SUM1]};
         if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s)) return st;
     }
     mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 1);
@@ -736,7 +781,7 @@ size_t ct_mrf_workspace(int64_t nx, int64_t ny, int64_t nz, int dtype) {
     const i64 n = nx * ny * nz;
     const i64 parts = 1ll << pw_depth(n > 0 ? n : 1);
     size_t b = al(parts * 8 * 2 + 64) + al(W_WORDS * 8);
-    if (dtype != CT_F64) b += al(interior(nx, ny, nz) * 4);
+    if (dtype != CT_F64) b += al(interior(nx, ny, nz) * (dtype == CT_U8 ? 2 : 4));
     if (dtype == CT_F64) b += al(n * 8) + al(cub_sort_bytes(n));
     return b + 1024;
 }

@@ -72,6 +72,9 @@ class FramePipeline:
         self.dtype = dtype
         self.tdtype = torch.uint8 if dtype == "u8" else torch.uint16
         self.code = 1 if dtype == "u8" else 2
+        # u8 volumes (and the u8-stored median) never exceed 255, so the
+        # reference's intensity_histogram has exactly 256 bins (segment.py:161)
+        self.nbins = 256 if dtype == "u8" else 0
         self.spacing = spacing
         self.denoise = denoise or CellDenoiseParams()
         self.seg = seg or SegmentationConfig()
@@ -160,7 +163,7 @@ class FramePipeline:
              self.med.data_ptr(), self.hist.data_ptr(), s)
         self._t1("K2 median+hist", e)
         e = self._t0()
-        call("ct_otsu", self.hist.data_ptr(), 0, self.otsu.data_ptr(), s)
+        call("ct_otsu", self.hist.data_ptr(), self.nbins, self.otsu.data_ptr(), s)
         self._t1("K3 otsu", e)
         e = self._t0()
         call("ct_threshold_close", self.med.data_ptr(), self.code, nx, ny, nz, self.otsu.data_ptr(), 0,
@@ -189,7 +192,7 @@ class FramePipeline:
              self.vhist.data_ptr(), s)
         self._t1("K7 mrf", e)
         e = self._t0()
-        call("ct_otsu", self.vhist.data_ptr(), 0, self.votsu.data_ptr(), s)
+        call("ct_otsu", self.vhist.data_ptr(), self.nbins, self.votsu.data_ptr(), s)
         call("ct_threshold_close", raw.data_ptr(), self.code, nx, ny, nz, self.votsu.data_ptr(), 0,
              self.seg.closing_radius, self.vmask.data_ptr(),
              self.vcwork.data_ptr() if self.vcwork is not None else None, s)

@@ -10,6 +10,15 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 out = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{kre}", "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
+# several matching kernels: keep the block of the first (or the one whose
+# name contains argv[4])
+pick = sys.argv[4] if len(sys.argv) > 4 else None
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+blk = 0
+if pick:
+    blk = next(b for b in range(len(starts) - 1) if pick in rows[starts[b]][1])
+print(rows[starts[blk]][1][:100])
+rows = rows[starts[blk]:starts[blk + 1]]
 h = rows[1]
 ai, si, wi, ii = h.index("Address"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), \
     h.index("Instructions Executed")
