@@ -98,6 +98,81 @@ __global__ void __launch_bounds__(LT) edt_pass_x(const uint8_t *__restrict__ mas
     }
 }
 
+// Parallel pass x (nx <= 1024 * W): CTA = 32 consecutive lines x 32 segments
+// of 32*W rows.  Each thread packs its segment's mask into W 32-bit words
+// (bit u = row u); the last / first foreground of every segment goes through
+// SMEM so each thread knows the nearest foreground left and right of its
+// segment; then per row the nearest left / right foreground comes from the
+// words by clz / ffs.  Same tie rule as the sweeps (equal distance -> lower i).
+template <int W>
+__global__ void __launch_bounds__(1024) edt_pass_x_seg(const uint8_t *__restrict__ mask, i64 nlines, int nx,
+                                                        int16_t *__restrict__ di) {
+    __shared__ int segL[32][33], segF[32][33];
+    const int c = threadIdx.x, y = threadIdx.y;
+    const i64 l = blockIdx.x * 32ll + c;
+    const bool valid = l < nlines;
+    const i64 S = nlines;
+    const int row0 = y * 32 * W;
+    uint32_t bits[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        uint8_t m[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const int x = row0 + w * 32 + u;
+            m[u] = (valid && x < nx) ? mask[(i64)x * S + l] : 0;
+        }
+        uint32_t b = 0;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) b |= (m[u] ? 1u : 0u) << u;
+        bits[w] = b;
+    }
+    int last = -1, first = -1;
+#pragma unroll
+    for (int w = W - 1; w >= 0; --w)
+        if (last < 0 && bits[w]) last = row0 + w * 32 + 31 - __clz(bits[w]);
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+        if (first < 0 && bits[w]) first = row0 + w * 32 + __ffs(bits[w]) - 1;
+    segL[y][c] = last;
+    segF[y][c] = first;
+    __syncthreads();
+    int left = -1, right = -1;
+    for (int yy = y - 1; yy >= 0; --yy)
+        if (segL[yy][c] >= 0) { left = segL[yy][c]; break; }
+    for (int yy = y + 1; yy < 32; ++yy)
+        if (segF[yy][c] >= 0) { right = segF[yy][c]; break; }
+    if (!valid) return;
+    int rctx[W];
+    {
+        int r = right;
+#pragma unroll
+        for (int w = W - 1; w >= 0; --w) {
+            rctx[w] = r;
+            if (bits[w]) r = row0 + w * 32 + __ffs(bits[w]) - 1;
+        }
+    }
+    int lc = left;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const int wb = row0 + w * 32;
+        const uint32_t b = bits[w];
+#pragma unroll 8
+        for (int u = 0; u < 32; ++u) {
+            const int x = wb + u;
+            if (x >= nx) break;
+            const uint32_t lo = b & ((2u << u) - 1u);  // rows <= x (u = 31: all)
+            const uint32_t hi = b & ~((1u << u) - 1u);  // rows >= x
+            const int lf = lo ? wb + 31 - __clz(lo) : lc;
+            const int rf = hi ? wb + __ffs(hi) - 1 : rctx[w];
+            int best = lf;
+            if (rf >= 0 && (best < 0 || rf - x < x - best)) best = rf;
+            di[(i64)x * S + l] = best < 0 ? NONE16 : (int16_t)(best - x);
+        }
+        if (b) lc = wb + 31 - __clz(b);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di)
 // ---------------------------------------------------------------------------
@@ -190,8 +265,10 @@ __device__ __forceinline__ double gyz(int32_t pl, double dx, double dy) {
     return __dadd_rn(sq(__dmul_rn((double)unpack_di(pl), dx)), sq(__dmul_rn((double)unpack_dj(pl), dy)));
 }
 
-__global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in, i64 nlines, int nz, double dx,
+template <int NZ>  // NZ > 0: compile-time line length (== nz); 0: runtime
+__global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in, i64 nlines, int nz_, double dx,
                                                  double dy, double dz, double *__restrict__ out) {
+    const int nz = NZ > 0 ? NZ : nz_;
     extern __shared__ __align__(16) unsigned char zsm[];
     const int S = nz + 1;                               // padded line stride (conflict-free)
     double *gs = (double *)zsm;                         // [ZL][S]
@@ -200,10 +277,33 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
     const int nl = (int)min((i64)ZL, nlines - l0);
     const int tot = nl * nz;
     const int32_t *src = in + l0 * nz;
-    for (int idx = threadIdx.x; idx < tot; idx += ZL) {
-        const int g = idx / nz, k = idx - g * nz;
-        const int32_t pl = src[idx];
-        gs[g * S + k] = pl == NONE32 ? INFINITY : gyz(pl, dx, dy);
+    if (NZ > 0 && nl == ZL && ((uintptr_t)src & 15) == 0) {
+        // 16-byte loads, 8 in flight per thread (two rounds for NZ = 64)
+        constexpr int T4 = ZL * (NZ > 0 ? NZ : 4) / 4;
+        for (int i0 = threadIdx.x; i0 < T4; i0 += 8 * ZL) {
+            int4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + u * ZL < T4) v[u] = __ldg((const int4 *)src + i0 + u * ZL);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = i0 + u * ZL;
+                if (q < T4) {
+                    const int idx = q * 4, g = idx / nz, k = idx - g * nz;
+                    double *d = gs + g * S + k;
+                    d[0] = v[u].x == NONE32 ? INFINITY : gyz(v[u].x, dx, dy);
+                    d[1] = v[u].y == NONE32 ? INFINITY : gyz(v[u].y, dx, dy);
+                    d[2] = v[u].z == NONE32 ? INFINITY : gyz(v[u].z, dx, dy);
+                    d[3] = v[u].w == NONE32 ? INFINITY : gyz(v[u].w, dx, dy);
+                }
+            }
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < tot; idx += ZL) {
+            const int g = idx / nz, k = idx - g * nz;
+            const int32_t pl = src[idx];
+            gs[g * S + k] = pl == NONE32 ? INFINITY : gyz(pl, dx, dy);
+        }
     }
     __syncthreads();
     const int t = threadIdx.x;
@@ -275,12 +375,19 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     int32_t *pk = (int32_t *)((char *)work + (((size_t)N * 2 + 255) & ~(size_t)255));
     uint32_t *spill = (uint32_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
     const i64 lx = ny * nz, ly = nx * nz, lz = nx * ny;
-    edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
+    if (nx <= 1024) {
+        edt_pass_x_seg<1><<<(unsigned)((lx + 31) / 32), dim3(32, 32), 0, s>>>(mask, lx, (int)nx, di);
+    } else if (nx <= 4096) {
+        edt_pass_x_seg<4><<<(unsigned)((lx + 31) / 32), dim3(32, 32), 0, s>>>(mask, lx, (int)nx, di);
+    } else {
+        edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
+    }
     if (int st = ct::check_launch("edt_pass_x")) return st;
     edt_pass_y<<<(unsigned)((ly + LT - 1) / LT), LT, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, pk, spill);
     if (int st = ct::check_launch("edt_pass_y")) return st;
     const size_t sm = zsmem((int)nz);
-    cudaFuncSetAttribute(edt_pass_z, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    edt_pass_z<<<(unsigned)((lz + ZL - 1) / ZL), ZL, sm, s>>>(pk, lz, (int)nz, dx, dy, dz, out);
+    auto kz = nz == 64 ? edt_pass_z<64> : nz == 32 ? edt_pass_z<32> : nz == 128 ? edt_pass_z<128> : edt_pass_z<0>;
+    cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kz<<<(unsigned)((lz + ZL - 1) / ZL), ZL, sm, s>>>(pk, lz, (int)nz, dx, dy, dz, out);
     return ct::check_launch("edt_pass_z");
 }

@@ -208,11 +208,36 @@ __device__ __forceinline__ u64 planes_to_bytes(uint32_t p0, uint32_t p1, uint32_
     return transpose8(((u64)hi << 32) | lo);
 }
 
-template <typename T, int NB>
+// bit 8i+b of x (byte i, bit b) -> bit 4b+i: nibble b = plane b of 4 voxels
+__device__ __forceinline__ uint32_t t4x8(uint32_t x) {
+    uint32_t t;
+    t = ((x >> 7) ^ x) & 0x00aa00aau; x ^= t ^ (t << 7);
+    t = ((x >> 14) ^ x) & 0x0000ccccu; x ^= t ^ (t << 14);
+    t = ((x >> 4) ^ x) & 0x00f000f0u; x ^= t ^ (t << 4);
+    t = ((x >> 8) ^ x) & 0x0000ff00u; x ^= t ^ (t << 8);
+    return x;
+}
+
+// 8x8 nibble transpose across the 8 lanes of a group (lane s holds row s):
+// afterwards lane s holds nibble s of every lane's row (row t at nibble t).
+__device__ __forceinline__ uint32_t nib_transpose8(uint32_t y, unsigned sub) {
+#pragma unroll
+    for (int s = 4; s >= 1; s >>= 1) {
+        const uint32_t m = s == 4 ? 0x0000ffffu : (s == 2 ? 0x00ff00ffu : 0x0f0f0f0fu);
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, y, s);
+        y = (sub & s) ? ((y & ~m) | ((o & ~m) >> (4 * s))) : ((y & m) | ((o & m) << (4 * s)));
+    }
+    return y;
+}
+
+// WC > 0: nz == 32 * WC at compile time (u8: planes built by in-register
+// transposes from 32-bit loads instead of per-bit ballots)
+template <typename T, int NB, int WC = 0>
 __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T *__restrict__ out, i64 nx, i64 ny,
-                                                    int nz, uint64_t *__restrict__ ghist) {
+                                                    int nz_, uint64_t *__restrict__ ghist) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    const int W = (nz + 31) >> 5;
+    const int nz = WC > 0 ? 32 * WC : nz_;
+    const int W = WC > 0 ? WC : (nz + 31) >> 5;
     const int RI = BTI + 2, RJ = BTJ + 2;
     const int NW = RI * RJ * W;  // staged (row, word) units
     // planes stored [b][unit] so a warp's 32 units hit 32 banks; three
@@ -242,39 +267,74 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
         const i64 i0 = (tile / tj) * BTI, j0 = (tile % tj) * BTJ;
         __syncthreads();
         if (threadIdx.x == 0) *s_any = 0;
-        // phase A: planes of the (BTI+2) x (BTJ+2) input rows (clamped), one warp
-        // per (row, word); loads batched 8 deep so their latencies overlap
-        for (int u0 = wid; u0 < NW; u0 += 8 * 8) {
-            unsigned vals[8];
+        if constexpr (NB == 8 && WC > 0) {
+            // phase A (u8, nz = 32 WC): each lane loads 4 voxels (32 bits); a row
+            // is 8 WC lanes; t4x8 + a nibble transpose over the 8 lanes of a
+            // word leave lane s with plane s of that word
+            constexpr int LPR = 8 * WC, RPW = 32 / LPR;
+            const int NR = RI * RJ;
+            const int lrow = lane / LPR, lw = (lane % LPR) >> 3;
+            const unsigned sub = lane & 7;
+            unsigned anyw = 0;
+            for (int r0 = wid * RPW; r0 < NR; r0 += 8 * RPW * 4) {
+                uint32_t x[4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int u = u0 + 8 * q;
-                vals[q] = 0u;
-                if (u < NW) {
-                    const int w = u % W, row = u / W;
-                    const int rj = row % RJ, ri = row / RJ;
-                    const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
-                    const int k = 32 * w + lane;
-                    if (k < nz) vals[q] = (unsigned)in[(i * ny + j) * nz + k];
+                for (int q = 0; q < 4; ++q) {
+                    const int r = r0 + q * 8 * RPW + lrow;
+                    x[q] = 0u;
+                    if (r < NR) {
+                        const int ri = r / RJ, rj = r - ri * RJ;
+                        const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
+                        x[q] = __ldg((const uint32_t *)(in + (i * ny + j) * nz) + (lane % LPR));
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r = r0 + q * 8 * RPW + lrow;
+                    const uint32_t y = nib_transpose8(t4x8(x[q]), sub);
+                    if (r < NR) {
+                        pc[sub * NW + r * W + lw] = y;
+                        anyw |= y ? (1u << sub) : 0u;
+                    }
                 }
             }
-            unsigned any = 0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int u = u0 + 8 * q;
-                if (u >= NW) break;
-                uint32_t mine = 0;
-#pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    const uint32_t word = __ballot_sync(0xffffffffu, (vals[q] >> b) & 1u);
-                    if ((int)lane == b) mine = word;
+            anyw = __reduce_or_sync(0xffffffffu, anyw);
+            if (lane == 0 && anyw) atomicOr(s_any, anyw);
+        } else {
+            // phase A: planes of the (BTI+2) x (BTJ+2) input rows (clamped), one warp
+            // per (row, word); loads batched 8 deep so their latencies overlap
+            for (int u0 = wid; u0 < NW; u0 += 8 * 8) {
+                unsigned vals[8];
+    #pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int u = u0 + 8 * q;
+                    vals[q] = 0u;
+                    if (u < NW) {
+                        const int w = u % W, row = u / W;
+                        const int rj = row % RJ, ri = row / RJ;
+                        const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
+                        const int k = 32 * w + lane;
+                        if (k < nz) vals[q] = (unsigned)in[(i * ny + j) * nz + k];
+                    }
                 }
-                if ((int)lane < NB) {
-                    pc[lane * NW + u] = mine;
-                    any |= mine ? (1u << lane) : 0u;
+                unsigned any = 0;
+    #pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int u = u0 + 8 * q;
+                    if (u >= NW) break;
+                    uint32_t mine = 0;
+    #pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        const uint32_t word = __ballot_sync(0xffffffffu, (vals[q] >> b) & 1u);
+                        if ((int)lane == b) mine = word;
+                    }
+                    if ((int)lane < NB) {
+                        pc[lane * NW + u] = mine;
+                        any |= mine ? (1u << lane) : 0u;
+                    }
                 }
+                if (any) atomicOr(s_any, any);
             }
-            if (any) atomicOr(s_any, any);
         }
         __syncthreads();
         // phase B: shifted versions (k-1 and k+1 neighbours, clamp-to-edge)
@@ -512,8 +572,12 @@ extern "C" int ct_median(const void *in, int dtype, int64_t nx, int64_t ny, int6
         const i64 tiles = ((nx + BTI - 1) / BTI) * ((ny + BTJ - 1) / BTJ);
         const int grid = (int)min(tiles, (i64)CT_NUM_SMS * 2);
         if (dtype == CT_U8) {
-            cudaFuncSetAttribute(median3_bits<uint8_t, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            median3_bits<uint8_t, 8><<<grid, 256, sm, s>>>((const uint8_t *)in, (uint8_t *)out, nx, ny, (int)nz, hist);
+            const bool al4 = ((uintptr_t)in & 3) == 0;
+            auto k = (al4 && nz == 64) ? median3_bits<uint8_t, 8, 2>
+                     : (al4 && nz == 32) ? median3_bits<uint8_t, 8, 1>
+                     : (al4 && nz == 128) ? median3_bits<uint8_t, 8, 4> : median3_bits<uint8_t, 8, 0>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k<<<grid, 256, sm, s>>>((const uint8_t *)in, (uint8_t *)out, nx, ny, (int)nz, hist);
         } else {
             cudaFuncSetAttribute(median3_bits<uint16_t, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             median3_bits<uint16_t, 16><<<grid, 256, sm, s>>>((const uint16_t *)in, (uint16_t *)out, nx, ny, (int)nz,
