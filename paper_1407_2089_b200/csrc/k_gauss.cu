@@ -48,8 +48,13 @@ __device__ __forceinline__ void window_taps(const double *__restrict__ col, int 
             const double wj = w[r - m - u];
 #pragma unroll
             for (int b = 0; b < B; ++b) {
-                const double s = __dadd_rn(Lw[(b + u) % B], Rw[(b - u + B) % B]);
-                acc[b] = FMA ? __fma_rn(s, wj, acc[b]) : __dadd_rn(acc[b], __dmul_rn(s, wj));
+                if (FMA) {  // two independent FMAs: no add -> multiply dependency
+                    acc[b] = __fma_rn(Lw[(b + u) % B], wj, acc[b]);
+                    acc[b] = __fma_rn(Rw[(b - u + B) % B], wj, acc[b]);
+                } else {
+                    const double s = __dadd_rn(Lw[(b + u) % B], Rw[(b - u + B) % B]);
+                    acc[b] = __dadd_rn(acc[b], __dmul_rn(s, wj));
+                }
             }
             // slide to tap m+u+1: one new left element (row base-r+m+u+B),
             // one new right element (row base+r-(m+u+1)); both always in range.
@@ -63,8 +68,13 @@ __device__ __forceinline__ void window_taps(const double *__restrict__ col, int 
         const double wj = w[j];
 #pragma unroll
         for (int b = 0; b < B; ++b) {
-            const double s = __dadd_rn(col[(base + b - j) * stride], col[(base + b + j) * stride]);
-            acc[b] = FMA ? __fma_rn(s, wj, acc[b]) : __dadd_rn(acc[b], __dmul_rn(s, wj));
+            if (FMA) {
+                acc[b] = __fma_rn(col[(base + b - j) * stride], wj, acc[b]);
+                acc[b] = __fma_rn(col[(base + b + j) * stride], wj, acc[b]);
+            } else {
+                const double s = __dadd_rn(col[(base + b - j) * stride], col[(base + b + j) * stride]);
+                acc[b] = __dadd_rn(acc[b], __dmul_rn(s, wj));
+            }
         }
     }
 }
@@ -170,12 +180,13 @@ struct Cert {
     long long cap;
 };
 
-template <typename Traw, typename Tq, bool FMA = false>
-__global__ void __launch_bounds__(512) gauss_contig(const double *__restrict__ in, i64 nlines, int L,
+template <typename Traw, typename Tq, bool FMA = false, int LC = 0>  // LC > 0: L == LC at compile time
+__global__ void __launch_bounds__(512) gauss_contig(const double *__restrict__ in, i64 nlines, int L_,
                                                       const double *__restrict__ w, int r, int S, int G,
                                                       const Traw *__restrict__ raw, double *__restrict__ bg_out,
                                                       double *__restrict__ res_out, Tq *__restrict__ q_out,
                                                       Cert cert = Cert{0.0, nullptr, 0}) {
+    const int L = LC > 0 ? LC : L_;
     extern __shared__ double smem[];
     double *tile = smem;                  // [G][S]
     double *ws = smem + (size_t)G * S;    // [r+1]
@@ -189,13 +200,14 @@ __global__ void __launch_bounds__(512) gauss_contig(const double *__restrict__ i
         const int g = idx / L, k = idx - g * L;
         tile[g * S + r + k] = src[idx];
     }
-    // clamped halos: rows [0, r) and [r+L, S)
+    // clamped halos: rows [0, r) and [r+L, S); x = line, y strides the halo
     const int halo = S - L;
-    for (int idx = tid; idx < gl * halo; idx += nth) {
-        const int g = idx / halo, h = idx - g * halo;
-        const int row = h < r ? h : h + L;
-        const int pos = row - r;
-        tile[g * S + row] = src[(i64)g * L + (pos < 0 ? 0 : (pos >= L ? L - 1 : pos))];
+    if (threadIdx.x < gl) {
+        const double lo = src[(i64)threadIdx.x * L], hi = src[(i64)threadIdx.x * L + L - 1];
+        for (int h = threadIdx.y; h < halo; h += blockDim.y) {
+            const int row = h < r ? h : h + L;
+            tile[threadIdx.x * S + row] = h < r ? lo : hi;
+        }
     }
     __syncthreads();
     const int g = threadIdx.x;
@@ -382,10 +394,13 @@ extern "C" int ct_to_f64(const void *in, int dtype, int64_t n, double *out, void
 
 // ---------------------------------------------------------------------------
 // Fused-pipeline fast path: q = rint(max(raw - bg, 0)) with the three passes
-// accumulated by FMA (2 FP64 ops per tap instead of 3), certified exact.  Both
-// the FMA result and scipy's separately rounded result lie within
-// (2(rx+ry+rz)+9) u M of the real convolution (u = 2^-53, M = max input,
-// weights positive and summing to 1), so q can differ only where the residual
+// accumulated by FMA chains (acc = fma(x[i-j], w_j, acc); acc = fma(x[i+j],
+// w_j, acc): 2 FP64 ops per tap instead of 3, no add->multiply dependency),
+// certified exact.  A pass of 2r+1 chained FMAs is within gamma_{2r+1} M of
+// the real convolution and scipy's order within gamma_{r+3} M (u = 2^-53, M =
+// max input, weights positive and summing to 1), so over three passes the two
+// differ by at most (3(rx+ry+rz)+12) u M (+ the residual's rounding), which
+// eps = 4(2(rx+ry+rz)+11) u M covers; q can differ only where the residual
 // is that close to a half-integer; those voxels (fix list) are recomputed
 // exactly from their full dependency cone: pass-x values for the (2ry+1) x nz
 // rows around the voxel, pass y on its z-line, pass z at the voxel -- the same
@@ -460,9 +475,12 @@ int gaussian_q_fast(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, in
     const int nb = (int)((nz + B - 1) / B);
     const double u = 1.1102230246251565e-16;  // 2^-53
     Cert cert{eps_override > 0.0 ? eps_override : 4.0 * (2.0 * (rx + ry + rz) + 11.0) * u * maxv, fix, cap};
-    cudaFuncSetAttribute(gauss_contig<Traw, Traw, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
-    gauss_contig<Traw, Traw, true><<<(unsigned)((nx * ny + C - 1) / C), dim3(C, nb), sm, s>>>(
-        p2, nx * ny, (int)nz, wz, rz, S, C, raw, nullptr, nullptr, q, cert);
+    auto kc = nz == 64 ? gauss_contig<Traw, Traw, true, 64>
+              : nz == 32 ? gauss_contig<Traw, Traw, true, 32>
+              : nz == 128 ? gauss_contig<Traw, Traw, true, 128> : gauss_contig<Traw, Traw, true, 0>;
+    cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
+    kc<<<(unsigned)((nx * ny + C - 1) / C), dim3(C, nb), sm, s>>>(p2, nx * ny, (int)nz, wz, rz, S, C, raw, nullptr,
+                                                                 nullptr, q, cert);
     if (int st = ct::check_launch("gauss_contig fma")) return st;
     const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
     cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
