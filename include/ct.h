@@ -93,17 +93,25 @@ int ct_gaussian_residual(const void *raw, int raw_dtype, int64_t nx, int64_t ny,
                          double *bg_out, double *residual_out, void *q_out, int q_dtype, void *stream);
 
 /* K1 fast path of the fused pipeline: q = rint(max(raw - bg, 0)) for U8/U16
- * raw, with bg accumulated by FMA and CERTIFIED exact: voxels whose residual
- * lies within the rigorous FMA-vs-scipy error bound of a half-integer are
- * listed in fix (device: [0] count, [1] overflow, [2..2+fix_cap) linear
- * indices) and recomputed in scipy's exact order by a fix-up kernel, so q is
- * bit-identical to ct_gaussian_residual's.  fix[1] != 0 (list overflow) means
- * q is not certified: rerun ct_gaussian_residual.  eps_override > 0 replaces
- * the bound (tests force the fix-up path with it).  Falls back to the exact
- * path when a tiled kernel does not apply. */
+ * raw, CERTIFIED exact.  U8 volumes with nz in {32, 64}, rx, ry <= 64 and
+ * rz <= 48 run on the tensor cores (tcgen05 int8 MMA: taps as 35-bit
+ * integers in 8-bit limbs, intermediates as 32-bit fixed point, exact int32
+ * accumulation; k_gauss_tc.cu); other inputs accumulate bg by FP64 FMA.
+ * Voxels whose residual lies within the path's rigorous error bound (vs
+ * scipy's float64 result) of a half-integer are listed in fix (device: [0]
+ * count, [1] overflow, [2..2+fix_cap) linear indices) and recomputed in
+ * scipy's exact order by a fix-up kernel, so q is bit-identical to
+ * ct_gaussian_residual's.  fix[1] != 0 (list overflow) means q is not
+ * certified: rerun ct_gaussian_residual.  eps_override > 0 replaces the
+ * bound (tests force the fix-up path with it).  Falls back to the exact path
+ * when no tiled kernel applies.  work: ct_workspace_bytes(0,...). */
 int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry,
                   int rz, void *work, void *q_out, unsigned long long *fix, int64_t fix_cap, double eps_override,
                   void *stream);
+
+/* Selects ct_gaussian_q's fast path (process-wide): 0 auto, 1 FP64 FMA
+ * only, 2 tensor cores only (CT_ERR_UNSUPPORTED when the shape does not fit). */
+int ct_set_k1_path(int mode);
 
 /* float64 copy of a U8/U16/F64 volume (ref denoise.py:84, :158 astype). */
 int ct_to_f64(const void *in, int dtype, int64_t n, double *out, void *stream);

@@ -16,6 +16,7 @@
 // Each thread computes B consecutive outputs along the filtered axis and keeps
 // a left and a right window of B inputs in registers that slide one step per
 // tap, so a tap costs 2 shared loads per B outputs (3B FP64 ops).
+#include <cstdlib>
 #include <type_traits>
 
 #include "ct_common.cuh"
@@ -103,8 +104,8 @@ struct Chunk {
     }
 };
 
-template <typename Tin, bool FMA = false>
-__global__ void __launch_bounds__(C *TMAX / B) gauss_strided(const Tin *__restrict__ in, double *__restrict__ out,
+template <typename Tin, bool FMA = false, int TT = TMAX, int MINB = 1>
+__global__ void __launch_bounds__(C *TT / B, MINB) gauss_strided(const Tin *__restrict__ in, double *__restrict__ out,
                                                             i64 L, i64 inner, const double *__restrict__ w, int r,
                                                             int T) {
     extern __shared__ double smem[];
@@ -289,16 +290,21 @@ int pass_strided(const Tin *in, double *out, i64 outer, i64 L, i64 inner, const 
         to_f64_copy<Tin><<<ct::grid_for(n, 256), 256, 0, s>>>(in, out, n);
         return ct::check_launch("gauss copy");
     }
-    int T = (int)min((i64)TMAX, ((L + B - 1) / B) * B);
+    static const int cfg = [] { const char *e = getenv("CT_GAUSS_CFG"); return e ? atoi(e) : 0; }();
+    const int TT = (cfg == 2 || cfg == 3) ? 64 : TMAX;
+    int T = (int)min((i64)TT, ((L + B - 1) / B) * B);
     size_t sm = ((size_t)(T + 2 * r) * C + r + 1) * sizeof(double);
     if (sm > SMEM_LIMIT || outer > 65535 || (L + T - 1) / T > 65535) {
         gauss_generic<Tin><<<ct::grid_for(n, 256), 256, 0, s>>>(in, out, outer, L, inner, w, r);
         return ct::check_launch("gauss_generic");
     }
-    cudaFuncSetAttribute(gauss_strided<Tin, FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
+    auto k = cfg == 1 ? gauss_strided<Tin, FMA, TMAX, 1>
+             : cfg == 2 ? gauss_strided<Tin, FMA, 64, 3>
+             : cfg == 3 ? gauss_strided<Tin, FMA, 64, 2> : gauss_strided<Tin, FMA, TMAX, 2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
     dim3 grid((unsigned)((inner + C - 1) / C), (unsigned)((L + T - 1) / T), (unsigned)outer);
     dim3 block(C, T / B);
-    gauss_strided<Tin, FMA><<<grid, block, sm, s>>>(in, out, L, inner, w, r, T);
+    k<<<grid, block, sm, s>>>(in, out, L, inner, w, r, T);
     return ct::check_launch("gauss_strided");
 }
 
@@ -490,6 +496,22 @@ int gaussian_q_fast(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, in
 
 }  // namespace
 
+int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry, int rz,
+                     void *work, uint8_t *q, unsigned long long *fix, int64_t cap, double eps_override,
+                     cudaStream_t s);
+
+// K1 fast-path selection (ct_set_k1_path): 0 auto (tensor cores when the
+// shape fits, else FP64 FMA), 1 FP64 FMA, 2 tensor cores only.
+static int g_k1_path = 0;
+extern "C" int ct_set_k1_path(int mode) {
+    if (mode < 0 || mode > 2) {
+        ct::set_error("k1 path mode must be 0, 1 or 2");
+        return CT_ERR_PARAM;
+    }
+    g_k1_path = mode;
+    return CT_OK;
+}
+
 extern "C" int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx,
                              int ry, int rz, void *work, void *q_out, unsigned long long *fix, int64_t fix_cap,
                              double eps_override, void *stream) {
@@ -505,9 +527,28 @@ extern "C" int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny,
         return ct_gaussian_residual(raw, dtype, nx, ny, nz, w, rx, ry, rz, work, nullptr, nullptr, q_out, dtype,
                                     stream);
     }
-    if (dtype == CT_U8)
+    if (dtype == CT_U8) {
+        // tensor-core path (k_gauss_tc.cu) unless disabled or the shape does not fit
+        if (g_k1_path != 1) {
+            const int st = ct_gaussian_q_tc((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, work, (uint8_t *)q_out,
+                                            fix, fix_cap, eps_override, s);
+            if (st == CT_OK) {
+                const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
+                cudaFuncSetAttribute(gauss_fixup<uint8_t, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)fsm);
+                gauss_fixup<uint8_t, uint8_t><<<CT_NUM_SMS, 256, fsm, s>>>((const uint8_t *)raw, nx, ny, nz, w, rx,
+                                                                            ry, rz, fix, fix_cap,
+                                                                            (uint8_t *)q_out);
+                return ct::check_launch("gauss_fixup");
+            }
+            if (st != CT_ERR_UNSUPPORTED || g_k1_path == 2) {
+                if (st == CT_ERR_UNSUPPORTED) ct::set_error("tensor-core K1 does not support this shape");
+                return st;
+            }
+        }
         return gaussian_q_fast<uint8_t>((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, (double *)work,
                                         (uint8_t *)q_out, fix, fix_cap, 255.0, eps_override, s);
+    }
     return gaussian_q_fast<uint16_t>((const uint16_t *)raw, nx, ny, nz, w, rx, ry, rz, (double *)work,
                                      (uint16_t *)q_out, fix, fix_cap, 65535.0, eps_override, s);
 }

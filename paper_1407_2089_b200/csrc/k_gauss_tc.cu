@@ -1,0 +1,462 @@
+// k_gauss_tc.cu -- K1 on the 5th-generation tensor cores (tcgen05, kind::i8).
+//
+// Certified fast path of ct_gaussian_q (ref denoise.py:84-86, see k_gauss.cu):
+// q = rint(max(raw - gaussian_filter(raw), 0)) for u8 volumes.  Each 1-D pass
+// is a banded integer GEMM: the double taps w_j are scaled to 35-bit integers
+// Q_j = rint(w_j 2^35) (2^34, ... when a tap >= 1/8) split into four 8-bit limbs, intermediates are 32-bit
+// fixed point (24 fractional bits) split into four byte planes, and every
+// limb product is accumulated exactly in int32 by UTCIMMA.  The result S is
+// the convolution in fixed point (scale 2^43 for the default 35-bit taps) with a rigorously bounded error
+// (weight rounding, truncation of intermediates, dropped limb pairs of weight
+// < 2^-43, and scipy's own float64 rounding); voxels whose residual lies
+// within that bound of a rounding boundary go to the fix list and are
+// recomputed in scipy's exact operation order (gauss_fixup in k_gauss.cu).
+//
+//   pass x, y (strided axes): D[out row][col] = A[out row][in row] * B[in row][col]
+//       A = the tap band (128 x 256, Toeplitz, constant) held in TMEM;
+//       B = 256 input rows (clamped at the edges = mode "nearest") x 32
+//       columns of a byte plane, MN-major in shared memory.
+//   pass z (contiguous axis, nz <= 64): D[line][out k] = A[line][in k] * B[in k][out k]
+//       A = 128 lines x (nz + 96) bytes with 48 replicated halo bytes per
+//       side, K-major; B = the tap band (constant), K-major; both in SMEM.
+//   Limb pairs (a, b) with a + b >= 2 (data limb a, weight limb b) are kept;
+//   pairs of equal a + b share an accumulator (5 accumulators).
+#include <algorithm>
+
+#include "ct_common.cuh"
+#include "tc_common.cuh"
+
+namespace {
+
+constexpr int FW = 35;         // weight scale bits (lowered per axis so that every Q_j < 2^32)
+constexpr int FD = 24;         // fractional bits of the intermediates
+constexpr int TM = 128;        // output rows per tile (passes x, y) / lines per tile (pass z)
+constexpr int TN = 32;         // columns per tile (passes x, y)
+constexpr int KXY = 256;       // input rows per tile (passes x, y): TM + 2r <= 256
+constexpr int HZ = 48;         // halo bytes per side (pass z): rz <= 48
+constexpr int NT = 128;        // threads per CTA
+constexpr int PMAX = 65;       // max taps per side + 1
+
+struct TcParams {
+    long long Q[3][PMAX];  // integer taps per axis (Q[axis][|j|] = rint(w_j 2^fw[axis]))
+    int fw[3];             // weight scale bits per axis (<= FW, four 8-bit limbs)
+    long long eps;         // certification threshold in units of 2^-(fw[2] + 8)
+};
+
+// ---------------------------------------------------------------------------
+// Setup: integer taps and the certified error bound (single thread).
+// ---------------------------------------------------------------------------
+__global__ void tc_prep(const double *__restrict__ w, int rx, int ry, int rz, double vmax, double eps_override,
+                        TcParams *prm) {
+    if (threadIdx.x || blockIdx.x) return;
+    const int rr[3] = {rx, ry, rz};
+    const double *ws[3] = {w, w + rx + 1, w + rx + 1 + ry + 1};
+    double bound = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        int fw = FW;
+        double wmax = 0.0;
+        for (int j = 0; j <= rr[a]; ++j) wmax = fmax(wmax, ws[a][j]);
+        while (fw > 24 && wmax * ldexp(1.0, fw) >= 4294967295.0) --fw;
+        prm->fw[a] = fw;
+        const double scale = ldexp(1.0, fw);
+        double dq = 0.0, qsum0 = 0.0, qsum1 = 0.0;
+        for (int j = 0; j < PMAX; ++j) prm->Q[a][j] = 0;
+        for (int j = 0; j <= rr[a]; ++j) {
+            const double x = ws[a][j] * scale;     // exact (power-of-two scaling)
+            const long long q = __double2ll_rn(x);
+            prm->Q[a][j] = q;
+            const double d = fabs((double)q - x);  // exact
+            const double mult = j ? 2.0 : 1.0;     // taps -j and +j
+            dq += mult * d;
+            qsum0 += mult * (double)(q & 0xff);
+            qsum1 += mult * (double)((q >> 8) & 0xff);
+        }
+        // weight rounding: sum_j |Q_j 2^-35 - w_j| * max input (inputs of passes
+        // y, z are bounded by vmax up to rounding of the taps' sum)
+        bound += dq / scale * vmax * 1.001;
+        if (a > 0) {
+            // dropped limb pairs (a+b <= 1): (0,0), (1,0), (0,1); data limbs <= 255
+            bound += 255.0 * (qsum0 * ldexp(1.0, -fw - FD) + (qsum0 + qsum1) * ldexp(1.0, 8 - fw - FD));
+        }
+    }
+    bound += 2.0 * ldexp(1.0, -FD);                                     // truncation of P1, P2
+    bound += 4.0 * (rx + ry + rz + 12) * ldexp(1.0, -53) * vmax;         // scipy float64 order + residual
+    const int zs = prm->fw[2] + 8;  // scale bits of the final sum
+    prm->eps = (long long)ceil(bound * 1.25 * ldexp(1.0, zs)) + 16;
+    if (eps_override > 0.0) prm->eps = (long long)ceil(eps_override * ldexp(1.0, zs));
+}
+
+__device__ __forceinline__ uint32_t limb(long long q, int b) { return (uint32_t)((q >> (8 * b)) & 0xff); }
+
+// byte a of four u32 values -> one u32 (plane words), all four planes
+__device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3, uint32_t (&p)[4]) {
+    const uint32_t l01 = __byte_perm(o0, o1, 0x5140), h01 = __byte_perm(o0, o1, 0x7362);
+    const uint32_t l23 = __byte_perm(o2, o3, 0x5140), h23 = __byte_perm(o2, o3, 0x7362);
+    p[0] = __byte_perm(l01, l23, 0x5410);
+    p[1] = __byte_perm(l01, l23, 0x7632);
+    p[2] = __byte_perm(h01, h23, 0x5410);
+    p[3] = __byte_perm(h01, h23, 0x7632);
+}
+
+// ---------------------------------------------------------------------------
+// Passes x and y.  NPIN = 1 (raw u8 input; pairs (0,b), accumulator b, shift
+// 8b; output S >> 11) or 4 (byte planes of P1; pairs a+b >= 2, accumulator
+// a+b-2, shift 8(a+b-2); output S >> 19).  Volume viewed as [outer][L][inner].
+// ---------------------------------------------------------------------------
+template <int NPIN>
+__global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ in, long long plane_in, int L,
+                                                     int inner, int outer, const TcParams *__restrict__ prm, int axis,
+                                                     int r, uint8_t *__restrict__ out, long long plane_out) {
+    constexpr int NACC = NPIN == 1 ? 4 : 5;
+    constexpr uint32_t LBO = (TN / 16) * 128, SBO = 128;                // MN-major B
+    constexpr int BUF = KXY * TN;                                       // bytes per plane per buffer
+    extern __shared__ __align__(1024) uint8_t sm[];                     // [2][NPIN][BUF]
+    __shared__ uint32_t tbase;
+    __shared__ uint64_t mbar;
+    __shared__ long long Qs[PMAX];
+    const int t = threadIdx.x, wp = t >> 5;
+    if (wp == 0) tc::tmem_alloc(&tbase, 512);
+    for (int j = t; j < PMAX; j += NT) Qs[j] = prm->Q[axis][j];
+    if (t == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
+    const int shift_out = NPIN == 1 ? prm->fw[axis] - FD : prm->fw[axis] - 16;
+    const uint32_t base = tbase;
+    const uint32_t lane_addr = base + ((uint32_t)(wp * 32) << 16);
+    // A (taps) into TMEM columns [0, 256): limb b at 64 b; row m = t
+    for (int b = 0; b < 4; ++b) {
+        for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int kk = 4 * (c0 + i) + e, j = kk - r - t;
+                    const uint32_t byte = (j >= -r && j <= r) ? limb(Qs[j < 0 ? -j : j], b) : 0u;
+                    word |= byte << (8 * e);
+                }
+                v[i] = word;
+            }
+            tc::tmem_st8(lane_addr + b * 64 + c0, v);
+        }
+    }
+    tc::tmem_st_wait();
+
+    const int nti = (L + TM - 1) / TM, ncb = inner / TN;
+    const long long ntiles = (long long)outer * nti * ncb;
+    const uint32_t idesc = tc::idesc_i8(TM, TN, false, false, false, true);
+    auto tile_coords = [&](long long tile, int &o, int &ti, int &cb) {
+        cb = (int)(tile % ncb);
+        const long long r2 = tile / ncb;
+        ti = (int)(r2 % nti);
+        o = (int)(r2 / nti);
+    };
+    // stage the B operand of a tile: NPIN planes x 256 rows x 32 bytes
+    auto stage = [&](long long tile, int buf) {
+        int o, ti, cb;
+        tile_coords(tile, o, ti, cb);
+        const int i0 = ti * TM;
+        uint4 v[NPIN * 4];
+#pragma unroll
+        for (int p = 0; p < NPIN; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = t + NT * q, kk = e >> 1, g = e & 1;
+                const int ii = min(max(i0 - r + kk, 0), L - 1);
+                v[p * 4 + q] = __ldg((const uint4 *)(in + p * plane_in + ((long long)o * L + ii) * inner +
+                                                     (long long)cb * TN + 16 * g));
+            }
+#pragma unroll
+        for (int p = 0; p < NPIN; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = t + NT * q, kk = e >> 1, g = e & 1;
+                *(uint4 *)(sm + (buf * NPIN + p) * BUF + tc::mnmajor_off(kk, 16 * g, LBO, SBO)) = v[p * 4 + q];
+            }
+    };
+
+    long long tile = blockIdx.x;
+    int buf = 0;
+    uint32_t phase = 0;
+    if (tile < ntiles) stage(tile, 0);
+    for (; tile < ntiles; tile += gridDim.x) {
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (t == 0) {
+            const uint32_t sb = tc::smem_u32(sm + buf * NPIN * BUF);
+            bool first[NACC];
+#pragma unroll
+            for (int s = 0; s < NACC; ++s) first[s] = true;
+#pragma unroll
+            for (int a = 0; a < NPIN; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int acc = NPIN == 1 ? b : a + b - 2;
+                    if (acc < 0) continue;
+                    const uint32_t d = base + 256 + TN * acc;
+#pragma unroll
+                    for (int ks = 0; ks < KXY / 32; ++ks) {
+                        const uint64_t bd = tc::smem_desc(sb + a * BUF + ks * 4 * LBO, LBO, SBO);
+                        tc::mma_i8_ts(d, base + b * 64 + ks * 8, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
+                    }
+                    first[acc] = false;
+                }
+            tc::mma_commit(&mbar);
+        }
+        const long long nxt = tile + gridDim.x;
+        if (nxt < ntiles) stage(nxt, buf ^ 1);  // overlaps the MMAs
+        tc::mbar_wait(&mbar, phase);
+        phase ^= 1;
+        tc::fence_after();
+        // epilogue: row m = t of the tile, 32 columns
+        int o, ti, cb;
+        tile_coords(tile, o, ti, cb);
+        const int i = ti * TM + t;
+#pragma unroll
+        for (int h = 0; h < TN; h += 16) {
+            long long S[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) S[c] = 0;
+#pragma unroll
+            for (int acc = 0; acc < NACC; ++acc) {
+                uint32_t v[16];
+                tc::tmem_ld16(lane_addr + 256 + TN * acc + h, v);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 16; ++c) S[c] += (long long)v[c] << (8 * acc);
+            }
+            if (i < L) {
+                uint32_t ov[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) ov[c] = (uint32_t)(S[c] >> shift_out);
+                uint32_t pw[4][4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t p4[4];
+                    planes4(ov[4 * q], ov[4 * q + 1], ov[4 * q + 2], ov[4 * q + 3], p4);
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) pw[a][q] = p4[a];
+                }
+                const long long off = ((long long)o * L + i) * inner + (long long)cb * TN + h;
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+                    *(uint4 *)(out + a * plane_out + off) = make_uint4(pw[a][0], pw[a][1], pw[a][2], pw[a][3]);
+            }
+        }
+        tc::fence_before();
+        buf ^= 1;
+    }
+    __syncthreads();
+    tc::fence_after();
+    if (wp == 0) tc::tmem_dealloc(base, 512);
+}
+
+// ---------------------------------------------------------------------------
+// Pass z + residual + quantisation + certification.  NZ in {32, 64}.
+// ---------------------------------------------------------------------------
+template <int NZ>
+__global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ in, long long plane, long long nlines,
+                                                    const TcParams *__restrict__ prm, int r,
+                                                    const uint8_t *__restrict__ raw, uint8_t *__restrict__ q,
+                                                    unsigned long long *__restrict__ fix, long long cap) {
+    constexpr int KZ = NZ + 2 * HZ;             // 128 or 160
+    constexpr int NCH = KZ / 16;                // 16-byte chunks per line
+    constexpr uint32_t LBO = 128, SBO = NCH * 128;
+    constexpr int ABUF = TM * KZ;               // bytes per plane per buffer
+    constexpr int BW = NZ * KZ;                 // bytes per weight limb
+    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] weights, then [2][4][ABUF] data
+    uint8_t *sw = sm;
+    uint8_t *sa = sm + 4 * BW;
+    __shared__ uint32_t tbase;
+    __shared__ uint64_t mbar;
+    __shared__ long long Qs[PMAX];
+    const int t = threadIdx.x, wp = t >> 5;
+    if (wp == 0) tc::tmem_alloc(&tbase, 512);
+    for (int j = t; j < PMAX; j += NT) Qs[j] = prm->Q[2][j];
+    if (t == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    // weights B_b[n][kk] = limb_b(Q[|kk - HZ - n|]), K-major
+    for (int e = t; e < 4 * NZ * KZ; e += NT) {
+        const int b = e / (NZ * KZ), rem = e - b * NZ * KZ, n = rem / KZ, kk = rem - n * KZ;
+        const int j = kk - HZ - n;
+        sw[b * BW + tc::kmajor_off(n, kk, LBO, SBO)] =
+            (uint8_t)((j >= -r && j <= r) ? limb(Qs[j < 0 ? -j : j], b) : 0u);
+    }
+    const long long eps = prm->eps;
+    const int zs = prm->fw[2] + 8;  // S has scale 2^zs
+    const long long half = 1ll << (zs - 1), fmask = (1ll << zs) - 1;
+    const uint32_t base = tbase;
+    const uint32_t lane_addr = base + ((uint32_t)(wp * 32) << 16);
+    const long long ntiles = (nlines + TM - 1) / TM;
+    const uint32_t idesc = tc::idesc_i8(TM, NZ, false, false, false, false);
+
+    auto stage = [&](long long tile, int buf) {
+        const long long l = tile * TM + t;
+        const bool ok = l < nlines;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            uint4 v[NZ / 16];
+#pragma unroll
+            for (int c = 0; c < NZ / 16; ++c)
+                v[c] = ok ? __ldg((const uint4 *)(in + a * plane + l * NZ) + c) : make_uint4(0, 0, 0, 0);
+            const uint32_t lo = (v[0].x & 0xffu) * 0x01010101u, hi = (v[NZ / 16 - 1].w >> 24) * 0x01010101u;
+            uint8_t *dst = sa + (buf * 4 + a) * ABUF;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                uint4 u;
+                if (c < HZ / 16) u = make_uint4(lo, lo, lo, lo);
+                else if (c >= HZ / 16 + NZ / 16) u = make_uint4(hi, hi, hi, hi);
+                else u = v[c - HZ / 16];
+                *(uint4 *)(dst + tc::kmajor_off(t, 16 * c, LBO, SBO)) = u;
+            }
+        }
+    };
+
+    long long tile = blockIdx.x;
+    int buf = 0;
+    uint32_t phase = 0;
+    if (tile < ntiles) stage(tile, 0);
+    for (; tile < ntiles; tile += gridDim.x) {
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (t == 0) {
+            const uint32_t sA = tc::smem_u32(sa + buf * 4 * ABUF), sB = tc::smem_u32(sw);
+            bool first[5] = {true, true, true, true, true};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int acc = a + b - 2;
+                    if (acc < 0) continue;
+#pragma unroll
+                    for (int ks = 0; ks < KZ / 32; ++ks) {
+                        const uint64_t ad = tc::smem_desc(sA + a * ABUF + ks * 2 * LBO, LBO, SBO);
+                        const uint64_t bd = tc::smem_desc(sB + b * BW + ks * 2 * LBO, LBO, SBO);
+                        tc::mma_i8_ss(base + NZ * acc, ad, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
+                    }
+                    first[acc] = false;
+                }
+            tc::mma_commit(&mbar);
+        }
+        const long long nxt = tile + gridDim.x;
+        if (nxt < ntiles) stage(nxt, buf ^ 1);
+        tc::mbar_wait(&mbar, phase);
+        phase ^= 1;
+        tc::fence_after();
+        const long long l = tile * TM + t;
+#pragma unroll
+        for (int h = 0; h < NZ; h += 16) {
+            long long S[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) S[c] = 0;
+#pragma unroll
+            for (int acc = 0; acc < 5; ++acc) {
+                uint32_t v[16];
+                tc::tmem_ld16(lane_addr + NZ * acc + h, v);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 16; ++c) S[c] += (long long)v[c] << (8 * acc);
+            }
+            if (l < nlines) {
+                const uint4 rv = __ldg((const uint4 *)(raw + l * NZ + h));
+                const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+                uint32_t qw[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const long long R = ((long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) - S[c];
+                    // q = rint(max(R, 0) / 2^43); certified unless R is within eps
+                    // of a rounding boundary (k + 1/2) 2^43
+                    uint32_t qv = 0;
+                    long long dist;
+                    if (R > 0) {
+                        qv = (uint32_t)((R + half) >> zs);
+                        dist = (R & fmask) - half;
+                        dist = dist < 0 ? -dist : dist;
+                    } else {
+                        dist = half - R;
+                    }
+                    if (dist <= eps) {
+                        const unsigned long long at = atomicAdd(&fix[0], 1ull);
+                        if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h + c);
+                        else fix[1] = 1;
+                    }
+                    qw[c >> 2] |= (qv & 0xffu) << (8 * (c & 3));
+                }
+                *(uint4 *)(q + l * NZ + h) = make_uint4(qw[0], qw[1], qw[2], qw[3]);
+            }
+        }
+        tc::fence_before();
+        buf ^= 1;
+    }
+    __syncthreads();
+    tc::fence_after();
+    if (wp == 0) tc::tmem_dealloc(base, 512);
+}
+
+}  // namespace
+
+// TC path of ct_gaussian_q (u8).  Returns CT_ERR_UNSUPPORTED when the shape
+// does not fit (the caller then uses the SIMT FMA path).  work: >= 8 N bytes
+// (byte planes of P1 and P2) + sizeof(TcParams).
+int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry, int rz,
+                     void *work, uint8_t *q, unsigned long long *fix, int64_t cap, double eps_override,
+                     cudaStream_t s) {
+    if (!(nz == 32 || nz == 64) || rx < 0 || ry < 0 || rz < 0 || rx > (KXY - TM) / 2 || ry > (KXY - TM) / 2 ||
+        rz > HZ || rx >= PMAX || ry >= PMAX || (ny * nz) % TN || nx * ny * nz >= (1ll << 31) ||
+        ((uintptr_t)raw & 15))
+        return CT_ERR_UNSUPPORTED;
+    const long long N = nx * ny * nz;
+    uint8_t *p1 = (uint8_t *)work, *p2 = p1 + 4 * N;
+    TcParams *prm = (TcParams *)(p2 + 4 * N);
+    cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
+    tc_prep<<<1, 1, 0, s>>>(w, rx, ry, rz, 255.0, eps_override, prm);
+    if (int st = ct::check_launch("tc_prep")) return st;
+    // pass x: [1][nx][ny*nz]
+    {
+        const size_t sm = 2 * 1 * KXY * TN + 1024;
+        cudaFuncSetAttribute(tc_pass_xy<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TN);
+        tc_pass_xy<1><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
+            raw, 0, (int)nx, (int)(ny * nz), 1, prm, 0, rx, p1, N);
+        if (int st = ct::check_launch("tc_pass_x")) return st;
+    }
+    // pass y: [nx][ny][nz]
+    {
+        const size_t sm = 2 * 4 * KXY * TN + 1024;
+        cudaFuncSetAttribute(tc_pass_xy<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TN);
+        tc_pass_xy<4><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
+            p1, N, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2, N);
+        if (int st = ct::check_launch("tc_pass_y")) return st;
+    }
+    // pass z + epilogue
+    {
+        const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
+        const int KZ = (int)nz + 2 * HZ;
+        const size_t sm = 4 * nz * KZ + 2 * 4 * TM * KZ + 1024;
+        auto kz = nz == 64 ? tc_pass_z<64> : tc_pass_z<32>;
+        cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kz<<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
+        if (int st = ct::check_launch("tc_pass_z")) return st;
+    }
+    return CT_OK;
+}
+
+size_t ct_gaussian_q_tc_work(int64_t nx, int64_t ny, int64_t nz) {
+    return (size_t)8 * nx * ny * nz + sizeof(TcParams) + 256;
+}

@@ -287,12 +287,42 @@ def _q_exact_and_fast(raw, spacing, sigma_um, eps=0.0, cap=1 << 20):
     return q1, q2, fix[:2].cpu().numpy()
 
 
-def test_certified_fma_k1_matches_exact(cuda):
-    for spec in (synth.C1, synth.SceneSpec(128, 96, 48, "u16", n_cells=20, seed=4)):
-        raw = synth.generate(spec, 2, synth.CELL)
-        q1, q2, fx = _q_exact_and_fast(raw, ANISO, 10.0)
-        assert fx[1] == 0
-        assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
+def _k1_path(mode):
+    from paper_1407_2089_b200._lib import call
+    call("ct_set_k1_path", mode)
+
+
+@pytest.mark.parametrize("mode", [1, 0])  # FP64 FMA, auto (tensor cores where the shape fits)
+def test_certified_fast_k1_matches_exact(cuda, mode):
+    _k1_path(mode)
+    try:
+        for spec in (synth.C1, synth.SceneSpec(128, 96, 48, "u16", n_cells=20, seed=4),
+                     synth.SceneSpec(160, 96, 64, "u8", n_cells=30, seed=9)):
+            raw = synth.generate(spec, 2, synth.CELL)
+            q1, q2, fx = _q_exact_and_fast(raw, ANISO, 10.0)
+            assert fx[1] == 0
+            assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
+    finally:
+        _k1_path(0)
+
+
+@pytest.mark.parametrize("sigma,shape,seed", [(10.0, (256, 192, 64), 1), (6.0, (200, 64, 32), 2),
+                                              (12.0, (130, 130, 64), 3), (3.0, (64, 32, 32), 4)])
+def test_tensor_core_k1_matches_exact(cuda, sigma, shape, seed):
+    # tensor-core K1 alone (mode 2) on noise and on a synthetic scene, incl.
+    # row counts that are not multiples of the 128-row tile
+    _k1_path(2)
+    try:
+        rng = np.random.default_rng(seed)
+        noise = torch.from_numpy(rng.integers(0, 256, size=shape, dtype=np.uint8)).cuda()
+        scene = synth.generate(synth.SceneSpec(*shape, "u8", n_cells=40, seed=seed), 1, synth.CELL)
+        for raw in (noise, scene):
+            q1, q2, fx = _q_exact_and_fast(raw, ANISO, sigma)
+            assert fx[1] == 0
+            assert fx[0] < 0.001 * raw.numel(), fx
+            assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
+    finally:
+        _k1_path(0)
 
 
 def test_certified_fixup_recomputes_exactly(cuda):
@@ -302,6 +332,15 @@ def test_certified_fixup_recomputes_exactly(cuda):
     q1, q2, fx = _q_exact_and_fast(v, ANISO, 3.0, eps=0.6)
     assert fx[0] == v.numel() and fx[1] == 0
     assert torch.equal(q1, q2)
+    # tensor-core path: everything with residual > -0.1 is flagged and fixed
+    _k1_path(2)
+    try:
+        v2 = torch.from_numpy(rng.integers(0, 256, size=(40, 36, 32), dtype=np.uint8)).cuda()
+        q1, q2, fx = _q_exact_and_fast(v2, ANISO, 3.0, eps=0.6)
+        assert fx[0] > v2.numel() // 3 and fx[1] == 0
+        assert torch.equal(q1, q2)
+    finally:
+        _k1_path(0)
     # overflow is reported when the list is too small
     _, _, fx = _q_exact_and_fast(v, ANISO, 3.0, eps=0.6, cap=10)
     assert fx[1] == 1
