@@ -94,7 +94,7 @@ int ct_gaussian_residual(const void *raw, int raw_dtype, int64_t nx, int64_t ny,
 
 /* K1 fast path of the fused pipeline: q = rint(max(raw - bg, 0)) for U8/U16
  * raw, CERTIFIED exact.  U8 volumes with nz in {32, 64}, rx, ry <= 64 and
- * rz <= 48 run on the tensor cores (tcgen05 int8 MMA: taps as 35-bit
+ * rz <= 64 run on the tensor cores (tcgen05 int8 MMA: taps as 35-bit
  * integers in 8-bit limbs, intermediates as 32-bit fixed point, exact int32
  * accumulation; k_gauss_tc.cu); other inputs accumulate bg by FP64 FMA.
  * Voxels whose residual lies within the path's rigorous error bound (vs

@@ -414,18 +414,20 @@ extern "C" int ct_to_f64(const void *in, int dtype, int64_t n, double *out, void
 // ---------------------------------------------------------------------------
 namespace {
 
+// Entries f >= start of the fix list, one CTA per entry (fallback for lists
+// larger than the scratch of the grid-wide kernels below).
 template <typename Traw, typename Tq>
 __global__ void __launch_bounds__(256) gauss_fixup(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz,
                                                    const double *__restrict__ w, int rx, int ry, int rz,
                                                    const unsigned long long *__restrict__ fix, long long cap,
-                                                   Tq *__restrict__ q_out) {
+                                                   Tq *__restrict__ q_out, long long start) {
     extern __shared__ double fsm[];
     const int RJ = 2 * ry + 1;
     double *P1 = fsm;                      // [RJ][nz]
     double *P2 = fsm + (size_t)RJ * nz;    // [nz]
     const double *wx = w, *wy = w + rx + 1, *wz = wy + ry + 1;
     const long long cnt = min((long long)fix[0], cap);
-    for (long long f = blockIdx.x; f < cnt; f += gridDim.x) {
+    for (long long f = start + blockIdx.x; f < cnt; f += gridDim.x) {
         const i64 p = (i64)fix[2 + f];
         const i64 k = p % nz, j = (p / nz) % ny, i = p / (ny * nz);
         __syncthreads();
@@ -465,6 +467,82 @@ __global__ void __launch_bounds__(256) gauss_fixup(const Traw *__restrict__ raw,
     }
 }
 
+// Grid-wide exact recompute of the first F = min(count, capF) fix entries in
+// three phases (scratch P1[F][2ry+1][nz], P2[F][nz] doubles): pass x at the
+// (2ry+1) x nz positions of each entry's cone, pass y on its z-line, pass z +
+// residual at the voxel -- the operations and order of ct_gaussian_residual.
+template <typename Traw>
+__global__ void fix_p1(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz, const double *__restrict__ w, int rx,
+                       int ry, const unsigned long long *__restrict__ fix, long long cap, long long capF,
+                       double *__restrict__ P1) {
+    const long long F = min(min((long long)fix[0], cap), capF);
+    const i64 RJ = 2 * ry + 1, per = RJ * nz, S = ny * nz;
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < F * per; e += (i64)gridDim.x * blockDim.x) {
+        const i64 f = e / per, rem = e - f * per, tt = rem / nz, kk = rem - tt * nz;
+        const i64 p = (i64)fix[2 + f];
+        const i64 j = (p / nz) % ny, i = p / S;
+        const i64 jj = ct::clampi(j + tt - ry, 0, ny - 1);
+        const Traw *col = raw + jj * nz + kk;
+        double acc = __dmul_rn(ct::to_f64(col[i * S]), w[0]);
+        for (int d = rx; d >= 1; --d) {
+            const double sm = __dadd_rn(ct::to_f64(col[ct::clampi(i - d, 0, nx - 1) * S]),
+                                        ct::to_f64(col[ct::clampi(i + d, 0, nx - 1) * S]));
+            acc = __dadd_rn(acc, __dmul_rn(sm, w[d]));
+        }
+        P1[e] = acc;
+    }
+}
+
+__global__ void fix_p2(i64 nz, const double *__restrict__ wy, int ry, const unsigned long long *__restrict__ fix,
+                       long long cap, long long capF, const double *__restrict__ P1, double *__restrict__ P2) {
+    const long long F = min(min((long long)fix[0], cap), capF);
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < F * nz; e += (i64)gridDim.x * blockDim.x) {
+        const i64 f = e / nz, kk = e - f * nz;
+        const double *c = P1 + f * (2 * ry + 1) * nz + kk;
+        double acc = __dmul_rn(c[(i64)ry * nz], wy[0]);
+        for (int d = ry; d >= 1; --d)
+            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(c[(i64)(ry - d) * nz], c[(i64)(ry + d) * nz]), wy[d]));
+        P2[e] = acc;
+    }
+}
+
+template <typename Traw, typename Tq>
+__global__ void fix_q(const Traw *__restrict__ raw, i64 nz, const double *__restrict__ wz, int rz,
+                      const unsigned long long *__restrict__ fix, long long cap, long long capF,
+                      const double *__restrict__ P2, Tq *__restrict__ q_out) {
+    const long long F = min(min((long long)fix[0], cap), capF);
+    for (i64 f = blockIdx.x * (i64)blockDim.x + threadIdx.x; f < F; f += (i64)gridDim.x * blockDim.x) {
+        const i64 p = (i64)fix[2 + f], k = p % nz;
+        const double *l = P2 + f * nz;
+        double acc = __dmul_rn(l[k], wz[0]);
+        for (int d = rz; d >= 1; --d)
+            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(l[ct::clampi(k - d, 0, nz - 1)], l[ct::clampi(k + d, 0, nz - 1)]),
+                                           wz[d]));
+        const double dd = __dadd_rn(ct::to_f64(raw[p]), -acc);
+        q_out[p] = (Tq)rint(dd < 0.0 ? 0.0 : dd);
+    }
+}
+
+// fix-up of a certified fast path: grid-wide phases for the first capF
+// entries (scratch = the dead K1 workspace), per-CTA fallback for the rest
+template <typename Traw>
+int launch_fixup(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int rx, int ry, int rz, void *work,
+                 size_t work_bytes, const unsigned long long *fix, long long cap, Traw *q, cudaStream_t s) {
+    const double *wx = w, *wy = w + rx + 1, *wz = wy + ry + 1;
+    const i64 per = (2 * (i64)ry + 1) * nz;
+    const long long capF = (long long)(work_bytes / ((size_t)(per + nz) * sizeof(double)));
+    double *P1 = (double *)work, *P2 = P1 + (size_t)capF * per;
+    const int grid = CT_NUM_SMS * 8;
+    fix_p1<Traw><<<grid, 256, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
+    fix_p2<<<grid, 256, 0, s>>>(nz, wy, ry, fix, cap, capF, P1, P2);
+    fix_q<Traw, Traw><<<grid, 256, 0, s>>>(raw, nz, wz, rz, fix, cap, capF, P2, q);
+    if (int st = ct::check_launch("fixup phases")) return st;
+    const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
+    cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    gauss_fixup<Traw, Traw><<<CT_NUM_SMS, 256, fsm, s>>>(raw, nx, ny, nz, w, rx, ry, rz, fix, cap, q, capF);
+    return ct::check_launch("gauss_fixup");
+}
+
 template <typename Traw>
 int gaussian_q_fast(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int rx, int ry, int rz, double *work,
                     Traw *q, unsigned long long *fix, long long cap, double maxv, double eps_override,
@@ -488,10 +566,7 @@ int gaussian_q_fast(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, in
     kc<<<(unsigned)((nx * ny + C - 1) / C), dim3(C, nb), sm, s>>>(p2, nx * ny, (int)nz, wz, rz, S, C, raw, nullptr,
                                                                  nullptr, q, cert);
     if (int st = ct::check_launch("gauss_contig fma")) return st;
-    const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
-    cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-    gauss_fixup<Traw, Traw><<<CT_NUM_SMS, 256, fsm, s>>>(raw, nx, ny, nz, w, rx, ry, rz, fix, cap, q);
-    return ct::check_launch("gauss_fixup");
+    return launch_fixup<Traw>(raw, nx, ny, nz, w, rx, ry, rz, work, (size_t)2 * N * sizeof(double), fix, cap, q, s);
 }
 
 }  // namespace
@@ -532,15 +607,10 @@ extern "C" int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny,
         if (g_k1_path != 1) {
             const int st = ct_gaussian_q_tc((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, work, (uint8_t *)q_out,
                                             fix, fix_cap, eps_override, s);
-            if (st == CT_OK) {
-                const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
-                cudaFuncSetAttribute(gauss_fixup<uint8_t, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)fsm);
-                gauss_fixup<uint8_t, uint8_t><<<CT_NUM_SMS, 256, fsm, s>>>((const uint8_t *)raw, nx, ny, nz, w, rx,
-                                                                            ry, rz, fix, fix_cap,
-                                                                            (uint8_t *)q_out);
-                return ct::check_launch("gauss_fixup");
-            }
+            if (st == CT_OK)
+                return launch_fixup<uint8_t>((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, work,
+                                             (size_t)2 * nx * ny * nz * sizeof(double), fix, fix_cap,
+                                             (uint8_t *)q_out, s);
             if (st != CT_ERR_UNSUPPORTED || g_k1_path == 2) {
                 if (st == CT_ERR_UNSUPPORTED) ct::set_error("tensor-core K1 does not support this shape");
                 return st;

@@ -16,9 +16,11 @@
 //       A = the tap band (128 x 256, Toeplitz, constant) held in TMEM;
 //       B = 256 input rows (clamped at the edges = mode "nearest") x 32
 //       columns of a byte plane, MN-major in shared memory.
-//   pass z (contiguous axis, nz <= 64): D[line][out k] = A[line][in k] * B[in k][out k]
-//       A = 128 lines x (nz + 96) bytes with 48 replicated halo bytes per
-//       side, K-major; B = the tap band (constant), K-major; both in SMEM.
+//   pass z (contiguous axis, nz in {32, 64}): D[line][out k] = A[line][in k] * B[in k][out k]
+//       A = 128 lines x nz bytes, K-major; B = the taps with the clamped
+//       boundary folded in (nz x nz, constant), K-major; both in SMEM.
+// Operand tiles are staged with cp.async (double-buffered) so the next
+// tile's loads overlap the MMAs and the epilogue of the current one.
 //   Limb pairs (a, b) with a + b >= 2 (data limb a, weight limb b) are kept;
 //   pairs of equal a + b share an accumulator (5 accumulators).
 #include <algorithm>
@@ -33,7 +35,6 @@ constexpr int FD = 24;         // fractional bits of the intermediates
 constexpr int TM = 128;        // output rows per tile (passes x, y) / lines per tile (pass z)
 constexpr int TN = 32;         // columns per tile (passes x, y)
 constexpr int KXY = 256;       // input rows per tile (passes x, y): TM + 2r <= 256
-constexpr int HZ = 48;         // halo bytes per side (pass z): rz <= 48
 constexpr int NT = 128;        // threads per CTA
 constexpr int PMAX = 65;       // max taps per side + 1
 
@@ -54,8 +55,10 @@ __global__ void tc_prep(const double *__restrict__ w, int rx, int ry, int rz, do
     double bound = 0.0;
     for (int a = 0; a < 3; ++a) {
         int fw = FW;
+        // largest integer tap: w_0 (x, y) or the folded edge sum_{j>=0} w_j (z)
         double wmax = 0.0;
-        for (int j = 0; j <= rr[a]; ++j) wmax = fmax(wmax, ws[a][j]);
+        for (int j = 0; j <= rr[a]; ++j) wmax = a == 2 ? wmax + ws[a][j] : fmax(wmax, ws[a][j]);
+        wmax *= 1.0000001;
         while (fw > 24 && wmax * ldexp(1.0, fw) >= 4294967295.0) --fw;
         prm->fw[a] = fw;
         const double scale = ldexp(1.0, fw);
@@ -74,6 +77,7 @@ __global__ void tc_prep(const double *__restrict__ w, int rx, int ry, int rz, do
         // weight rounding: sum_j |Q_j 2^-35 - w_j| * max input (inputs of passes
         // y, z are bounded by vmax up to rounding of the taps' sum)
         bound += dq / scale * vmax * 1.001;
+        if (a == 2) qsum0 = qsum1 = 64.0 * 255.0;  // folded taps: bound the limb sums per row
         if (a > 0) {
             // dropped limb pairs (a+b <= 1): (0,0), (1,0), (0,1); data limbs <= 255
             bound += 255.0 * (qsum0 * ldexp(1.0, -fw - FD) + (qsum0 + qsum1) * ldexp(1.0, 8 - fw - FD));
@@ -157,28 +161,21 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         ti = (int)(r2 % nti);
         o = (int)(r2 / nti);
     };
-    // stage the B operand of a tile: NPIN planes x 256 rows x 32 bytes
+    // stage the B operand of a tile (cp.async): NPIN planes x 256 rows x 32 bytes
     auto stage = [&](long long tile, int buf) {
         int o, ti, cb;
         tile_coords(tile, o, ti, cb);
         const int i0 = ti * TM;
-        uint4 v[NPIN * 4];
 #pragma unroll
         for (int p = 0; p < NPIN; ++p)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int e = t + NT * q, kk = e >> 1, g = e & 1;
                 const int ii = min(max(i0 - r + kk, 0), L - 1);
-                v[p * 4 + q] = __ldg((const uint4 *)(in + p * plane_in + ((long long)o * L + ii) * inner +
-                                                     (long long)cb * TN + 16 * g));
+                tc::cp_async16(sm + (buf * NPIN + p) * BUF + tc::mnmajor_off(kk, 16 * g, LBO, SBO),
+                               in + p * plane_in + ((long long)o * L + ii) * inner + (long long)cb * TN + 16 * g);
             }
-#pragma unroll
-        for (int p = 0; p < NPIN; ++p)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = t + NT * q, kk = e >> 1, g = e & 1;
-                *(uint4 *)(sm + (buf * NPIN + p) * BUF + tc::mnmajor_off(kk, 16 * g, LBO, SBO)) = v[p * 4 + q];
-            }
+        tc::cp_commit();
     };
 
     long long tile = blockIdx.x;
@@ -186,6 +183,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     uint32_t phase = 0;
     if (tile < ntiles) stage(tile, 0);
     for (; tile < ntiles; tile += gridDim.x) {
+        tc::cp_wait_all();
         tc::fence_async_smem();
         tc::fence_before();
         __syncthreads();
@@ -222,16 +220,16 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         const int i = ti * TM + t;
 #pragma unroll
         for (int h = 0; h < TN; h += 16) {
+            uint32_t v[NACC][16];
+#pragma unroll
+            for (int acc = 0; acc < NACC; ++acc) tc::tmem_ld16(lane_addr + 256 + TN * acc + h, v[acc]);
+            tc::tmem_ld_wait();
             long long S[16];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) S[c] = 0;
+            for (int c = 0; c < 16; ++c) {
+                S[c] = 0;
 #pragma unroll
-            for (int acc = 0; acc < NACC; ++acc) {
-                uint32_t v[16];
-                tc::tmem_ld16(lane_addr + 256 + TN * acc + h, v);
-                tc::tmem_ld_wait();
-#pragma unroll
-                for (int c = 0; c < 16; ++c) S[c] += (long long)v[c] << (8 * acc);
+                for (int acc = 0; acc < NACC; ++acc) S[c] += (long long)v[acc][c] << (8 * acc);
             }
             if (i < L) {
                 uint32_t ov[16];
@@ -260,21 +258,23 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// Pass z + residual + quantisation + certification.  NZ in {32, 64}.
+// Pass z + residual + quantisation + certification.  NZ in {32, 64}.  The
+// whole line is one tile, so the clamped boundary is folded into the taps:
+// B[n][k] = sum of Q_|j| over the taps j with clamp(n + j) = k.
 // ---------------------------------------------------------------------------
 template <int NZ>
 __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ in, long long plane, long long nlines,
                                                     const TcParams *__restrict__ prm, int r,
                                                     const uint8_t *__restrict__ raw, uint8_t *__restrict__ q,
                                                     unsigned long long *__restrict__ fix, long long cap) {
-    constexpr int KZ = NZ + 2 * HZ;             // 128 or 160
-    constexpr int NCH = KZ / 16;                // 16-byte chunks per line
+    constexpr int NCH = NZ / 16;                // 16-byte chunks per line
     constexpr uint32_t LBO = 128, SBO = NCH * 128;
-    constexpr int ABUF = TM * KZ;               // bytes per plane per buffer
-    constexpr int BW = NZ * KZ;                 // bytes per weight limb
-    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] weights, then [2][4][ABUF] data
+    constexpr int ABUF = TM * NZ;               // bytes per plane per buffer
+    constexpr int BW = NZ * NZ;                 // bytes per weight limb
+    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [2][4][ABUF] data, [2][ABUF] raw
     uint8_t *sw = sm;
     uint8_t *sa = sm + 4 * BW;
+    uint8_t *sr = sa + 2 * 4 * ABUF;
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
     __shared__ long long Qs[PMAX];
@@ -288,12 +288,16 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    // weights B_b[n][kk] = limb_b(Q[|kk - HZ - n|]), K-major
-    for (int e = t; e < 4 * NZ * KZ; e += NT) {
-        const int b = e / (NZ * KZ), rem = e - b * NZ * KZ, n = rem / KZ, kk = rem - n * KZ;
-        const int j = kk - HZ - n;
-        sw[b * BW + tc::kmajor_off(n, kk, LBO, SBO)] =
-            (uint8_t)((j >= -r && j <= r) ? limb(Qs[j < 0 ? -j : j], b) : 0u);
+    // folded taps, K-major
+    for (int e = t; e < NZ * NZ; e += NT) {
+        const int n = e / NZ, k = e - n * NZ;
+        long long qf = 0;
+        for (int j = -r; j <= r; ++j) {
+            const int kk = min(max(n + j, 0), NZ - 1);
+            if (kk == k) qf += Qs[j < 0 ? -j : j];
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) sw[b * BW + tc::kmajor_off(n, k, LBO, SBO)] = (uint8_t)limb(qf, b);
     }
     const long long eps = prm->eps;
     const int zs = prm->fw[2] + 8;  // S has scale 2^zs
@@ -303,26 +307,22 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     const long long ntiles = (nlines + TM - 1) / TM;
     const uint32_t idesc = tc::idesc_i8(TM, NZ, false, false, false, false);
 
+    // data planes (K-major canonical) and raw (plain) of a tile via cp.async
     auto stage = [&](long long tile, int buf) {
-        const long long l = tile * TM + t;
-        const bool ok = l < nlines;
+        const long long l0 = tile * TM;
+        const int nl = (int)min((long long)TM, nlines - l0);
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            uint4 v[NZ / 16];
+        for (int q2 = 0; q2 < TM * NCH / NT; ++q2) {
+            const int e = t + NT * q2, l = e / NCH, c = e - l * NCH;
+            if (l < nl) {
 #pragma unroll
-            for (int c = 0; c < NZ / 16; ++c)
-                v[c] = ok ? __ldg((const uint4 *)(in + a * plane + l * NZ) + c) : make_uint4(0, 0, 0, 0);
-            const uint32_t lo = (v[0].x & 0xffu) * 0x01010101u, hi = (v[NZ / 16 - 1].w >> 24) * 0x01010101u;
-            uint8_t *dst = sa + (buf * 4 + a) * ABUF;
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                uint4 u;
-                if (c < HZ / 16) u = make_uint4(lo, lo, lo, lo);
-                else if (c >= HZ / 16 + NZ / 16) u = make_uint4(hi, hi, hi, hi);
-                else u = v[c - HZ / 16];
-                *(uint4 *)(dst + tc::kmajor_off(t, 16 * c, LBO, SBO)) = u;
+                for (int a = 0; a < 4; ++a)
+                    tc::cp_async16(sa + (buf * 4 + a) * ABUF + tc::kmajor_off(l, 16 * c, LBO, SBO),
+                                   in + a * plane + (l0 + l) * NZ + 16 * c);
+                tc::cp_async16(sr + buf * ABUF + l * NZ + 16 * c, raw + (l0 + l) * NZ + 16 * c);
             }
         }
+        tc::cp_commit();
     };
 
     long long tile = blockIdx.x;
@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     uint32_t phase = 0;
     if (tile < ntiles) stage(tile, 0);
     for (; tile < ntiles; tile += gridDim.x) {
+        tc::cp_wait_all();
         tc::fence_async_smem();
         tc::fence_before();
         __syncthreads();
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
                     const int acc = a + b - 2;
                     if (acc < 0) continue;
 #pragma unroll
-                    for (int ks = 0; ks < KZ / 32; ++ks) {
+                    for (int ks = 0; ks < NZ / 32; ++ks) {
                         const uint64_t ad = tc::smem_desc(sA + a * ABUF + ks * 2 * LBO, LBO, SBO);
                         const uint64_t bd = tc::smem_desc(sB + b * BW + ks * 2 * LBO, LBO, SBO);
                         tc::mma_i8_ss(base + NZ * acc, ad, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
@@ -359,28 +360,25 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         phase ^= 1;
         tc::fence_after();
         const long long l = tile * TM + t;
+        const uint8_t *rl = sr + buf * ABUF + t * NZ;
 #pragma unroll
         for (int h = 0; h < NZ; h += 16) {
-            long long S[16];
+            uint32_t v[5][16];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) S[c] = 0;
-#pragma unroll
-            for (int acc = 0; acc < 5; ++acc) {
-                uint32_t v[16];
-                tc::tmem_ld16(lane_addr + NZ * acc + h, v);
-                tc::tmem_ld_wait();
-#pragma unroll
-                for (int c = 0; c < 16; ++c) S[c] += (long long)v[c] << (8 * acc);
-            }
+            for (int acc = 0; acc < 5; ++acc) tc::tmem_ld16(lane_addr + NZ * acc + h, v[acc]);
+            tc::tmem_ld_wait();
             if (l < nlines) {
-                const uint4 rv = __ldg((const uint4 *)(raw + l * NZ + h));
+                const uint4 rv = *(const uint4 *)(rl + h);
                 const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
                 uint32_t qw[4] = {0, 0, 0, 0};
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
-                    const long long R = ((long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) - S[c];
-                    // q = rint(max(R, 0) / 2^43); certified unless R is within eps
-                    // of a rounding boundary (k + 1/2) 2^43
+                    long long S = 0;
+#pragma unroll
+                    for (int acc = 0; acc < 5; ++acc) S += (long long)v[acc][c] << (8 * acc);
+                    const long long R = ((long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) - S;
+                    // q = rint(max(R, 0) / 2^zs); certified unless R is within eps
+                    // of a rounding boundary (k + 1/2) 2^zs
                     uint32_t qv = 0;
                     long long dist;
                     if (R > 0) {
@@ -417,7 +415,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
                      void *work, uint8_t *q, unsigned long long *fix, int64_t cap, double eps_override,
                      cudaStream_t s) {
     if (!(nz == 32 || nz == 64) || rx < 0 || ry < 0 || rz < 0 || rx > (KXY - TM) / 2 || ry > (KXY - TM) / 2 ||
-        rz > HZ || rx >= PMAX || ry >= PMAX || (ny * nz) % TN || nx * ny * nz >= (1ll << 31) ||
+        rz >= PMAX || (ny * nz) % TN || nx * ny * nz >= (1ll << 31) ||
         ((uintptr_t)raw & 15))
         return CT_ERR_UNSUPPORTED;
     const long long N = nx * ny * nz;
@@ -447,8 +445,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     // pass z + epilogue
     {
         const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
-        const int KZ = (int)nz + 2 * HZ;
-        const size_t sm = 4 * nz * KZ + 2 * 4 * TM * KZ + 1024;
+        const size_t sm = 4 * nz * nz + 2 * 4 * TM * nz + 2 * TM * nz + 1024;
         auto kz = nz == 64 ? tc_pass_z<64> : tc_pass_z<32>;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         kz<<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
