@@ -19,8 +19,8 @@
 //   pass z (contiguous axis, nz in {32, 64}): D[line][out k] = A[line][in k] * B[in k][out k]
 //       A = 128 lines x nz bytes, K-major; B = the taps with the clamped
 //       boundary folded in (nz x nz, constant), K-major; both in SMEM.
-// Operand tiles are staged with cp.async (double-buffered) so the next
-// tile's loads overlap the MMAs and the epilogue of the current one.
+// Operand tiles are staged with cp.async several tiles ahead, and each
+// tile's epilogue (from registers) overlaps the next tile's MMAs.
 //   Limb pairs (a, b) with a + b >= 2 (data limb a, weight limb b) are kept;
 //   pairs of equal a + b share an accumulator (5 accumulators).
 #include <algorithm>
@@ -35,7 +35,7 @@ constexpr int FD = 24;         // fractional bits of the intermediates
 constexpr int TM = 128;        // output rows per tile (passes x, y) / lines per tile (pass z)
 constexpr int TN = 32;         // columns per tile (passes x, y)
 constexpr int KXY = 256;       // input rows per tile (passes x, y): TM + 2r <= 256
-constexpr int NT = 128;        // threads per CTA
+constexpr int NT = 512;        // threads per CTA: 16 warps = 4 TMEM sub-partitions x 4 column groups
 constexpr int PMAX = 65;       // max taps per side + 1
 
 struct TcParams {
@@ -107,18 +107,20 @@ __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, u
 // 8b; output S >> 11) or 4 (byte planes of P1; pairs a+b >= 2, accumulator
 // a+b-2, shift 8(a+b-2); output S >> 19).  Volume viewed as [outer][L][inner].
 // ---------------------------------------------------------------------------
-template <int NPIN>
+template <int NPIN, int STAGES>
 __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ in, long long plane_in, int L,
                                                      int inner, int outer, const TcParams *__restrict__ prm, int axis,
                                                      int r, uint8_t *__restrict__ out, long long plane_out) {
     constexpr int NACC = NPIN == 1 ? 4 : 5;
     constexpr uint32_t LBO = (TN / 16) * 128, SBO = 128;                // MN-major B
     constexpr int BUF = KXY * TN;                                       // bytes per plane per buffer
-    extern __shared__ __align__(1024) uint8_t sm[];                     // [2][NPIN][BUF]
+    extern __shared__ __align__(1024) uint8_t sm[];                     // [STAGES][NPIN][BUF]
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
     __shared__ long long Qs[PMAX];
-    const int t = threadIdx.x, wp = t >> 5;
+    // thread t: TMEM row (lane) m = t % 128 of sub-partition (t / 32) % 4,
+    // column group cg = t / 128
+    const int t = threadIdx.x, wp = t >> 5, m = t & (TM - 1), cg = t >> 7;
     if (wp == 0) tc::tmem_alloc(&tbase, 512);
     for (int j = t; j < PMAX; j += NT) Qs[j] = prm->Q[axis][j];
     if (t == 0) {
@@ -131,9 +133,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
     const int shift_out = NPIN == 1 ? prm->fw[axis] - FD : prm->fw[axis] - 16;
     const uint32_t base = tbase;
-    const uint32_t lane_addr = base + ((uint32_t)(wp * 32) << 16);
-    // A (taps) into TMEM columns [0, 256): limb b at 64 b; row m = t
-    for (int b = 0; b < 4; ++b) {
+    const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
+    // A (taps) into TMEM columns [0, 256): limb b = cg at 64 b; row m
+    {
+        const int b = cg;
         for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
             uint32_t v[8];
 #pragma unroll
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
                 uint32_t word = 0;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int kk = 4 * (c0 + i) + e, j = kk - r - t;
+                    const int kk = 4 * (c0 + i) + e, j = kk - r - m;
                     const uint32_t byte = (j >= -r && j <= r) ? limb(Qs[j < 0 ? -j : j], b) : 0u;
                     word |= byte << (8 * e);
                 }
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
 #pragma unroll
         for (int p = 0; p < NPIN; ++p)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < 2 * KXY / NT; ++q) {
                 const int e = t + NT * q, kk = e >> 1, g = e & 1;
                 const int ii = min(max(i0 - r + kk, 0), L - 1);
                 tc::cp_async16(sm + (buf * NPIN + p) * BUF + tc::mnmajor_off(kk, 16 * g, LBO, SBO),
@@ -178,80 +181,88 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         tc::cp_commit();
     };
 
-    long long tile = blockIdx.x;
-    int buf = 0;
-    uint32_t phase = 0;
-    if (tile < ntiles) stage(tile, 0);
-    for (; tile < ntiles; tile += gridDim.x) {
-        tc::cp_wait_all();
+    // Software pipeline over this CTA's tiles k = 0, 1, ... (tile t0 + k gs):
+    // STAGES tiles are staged ahead by cp.async (slot k % STAGES); after
+    // MMA(k) completes its accumulators are read into registers, a barrier
+    // frees TMEM, MMA(k+1) is issued, and the epilogue of tile k (combine +
+    // stores) runs from registers while MMA(k+1) executes.
+    const long long t0 = blockIdx.x, gs = gridDim.x;
+    const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
+    auto issue = [&](long long k) {
+        if (t != 0) return;
+        const uint32_t sb = tc::smem_u32(sm + (int)(k % STAGES) * NPIN * BUF);
+        bool first[NACC];
+#pragma unroll
+        for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
+#pragma unroll
+        for (int a = 0; a < NPIN; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int acc = NPIN == 1 ? b : a + b - 2;
+                if (acc < 0) continue;
+                const uint32_t d = base + 256 + TN * acc;
+#pragma unroll
+                for (int ks = 0; ks < KXY / 32; ++ks) {
+                    const uint64_t bd = tc::smem_desc(sb + a * BUF + ks * 4 * LBO, LBO, SBO);
+                    tc::mma_i8_ts(d, base + b * 64 + ks * 8, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
+                }
+                first[acc] = false;
+            }
+        tc::mma_commit(&mbar);
+    };
+#pragma unroll
+    for (int k = 0; k < STAGES; ++k) {
+        if (k < nmine) stage(t0 + k * gs, k);
+        else tc::cp_commit();
+    }
+    if (nmine > 0) {
+        tc::cp_wait_group<STAGES - 1>();
         tc::fence_async_smem();
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
-        if (t == 0) {
-            const uint32_t sb = tc::smem_u32(sm + buf * NPIN * BUF);
-            bool first[NACC];
-#pragma unroll
-            for (int s = 0; s < NACC; ++s) first[s] = true;
-#pragma unroll
-            for (int a = 0; a < NPIN; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int acc = NPIN == 1 ? b : a + b - 2;
-                    if (acc < 0) continue;
-                    const uint32_t d = base + 256 + TN * acc;
-#pragma unroll
-                    for (int ks = 0; ks < KXY / 32; ++ks) {
-                        const uint64_t bd = tc::smem_desc(sb + a * BUF + ks * 4 * LBO, LBO, SBO);
-                        tc::mma_i8_ts(d, base + b * 64 + ks * 8, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
-                    }
-                    first[acc] = false;
-                }
-            tc::mma_commit(&mbar);
-        }
-        const long long nxt = tile + gridDim.x;
-        if (nxt < ntiles) stage(nxt, buf ^ 1);  // overlaps the MMAs
+        issue(0);
+    }
+    uint32_t phase = 0;
+    const int h = 8 * cg;
+    for (long long k = 0; k < nmine; ++k) {
         tc::mbar_wait(&mbar, phase);
         phase ^= 1;
         tc::fence_after();
-        // epilogue: row m = t of the tile, 32 columns
-        int o, ti, cb;
-        tile_coords(tile, o, ti, cb);
-        const int i = ti * TM + t;
+        uint32_t v[NACC][8];
 #pragma unroll
-        for (int h = 0; h < TN; h += 16) {
-            uint32_t v[NACC][16];
-#pragma unroll
-            for (int acc = 0; acc < NACC; ++acc) tc::tmem_ld16(lane_addr + 256 + TN * acc + h, v[acc]);
-            tc::tmem_ld_wait();
-            long long S[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                S[c] = 0;
-#pragma unroll
-                for (int acc = 0; acc < NACC; ++acc) S[c] += (long long)v[acc][c] << (8 * acc);
-            }
-            if (i < L) {
-                uint32_t ov[16];
-#pragma unroll
-                for (int c = 0; c < 16; ++c) ov[c] = (uint32_t)(S[c] >> shift_out);
-                uint32_t pw[4][4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint32_t p4[4];
-                    planes4(ov[4 * q], ov[4 * q + 1], ov[4 * q + 2], ov[4 * q + 3], p4);
-#pragma unroll
-                    for (int a = 0; a < 4; ++a) pw[a][q] = p4[a];
-                }
-                const long long off = ((long long)o * L + i) * inner + (long long)cb * TN + h;
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-                    *(uint4 *)(out + a * plane_out + off) = make_uint4(pw[a][0], pw[a][1], pw[a][2], pw[a][3]);
-            }
-        }
+        for (int acc = 0; acc < NACC; ++acc) tc::tmem_ld8(lane_addr + 256 + TN * acc + h, v[acc]);
+        tc::tmem_ld_wait();
+        tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
+        tc::fence_async_smem();
         tc::fence_before();
-        buf ^= 1;
+        __syncthreads();
+        tc::fence_after();
+        if (k + 1 < nmine) issue(k + 1);
+        if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
+        else tc::cp_commit();
+        // epilogue of tile k: row m, columns [8 cg, 8 cg + 8)
+        int o, ti, cb;
+        tile_coords(t0 + k * gs, o, ti, cb);
+        const int i = ti * TM + m;
+        if (i < L) {
+            uint32_t ov[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                long long S = 0;
+#pragma unroll
+                for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][c] << (8 * acc);
+                ov[c] = (uint32_t)(S >> shift_out);
+            }
+            uint32_t lo[4], hi[4];
+            planes4(ov[0], ov[1], ov[2], ov[3], lo);
+            planes4(ov[4], ov[5], ov[6], ov[7], hi);
+            const long long off = ((long long)o * L + i) * inner + (long long)cb * TN + h;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) *(uint2 *)(out + a * plane_out + off) = make_uint2(lo[a], hi[a]);
+        }
     }
+    tc::cp_wait_all();
     __syncthreads();
     tc::fence_after();
     if (wp == 0) tc::tmem_dealloc(base, 512);
@@ -262,7 +273,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
 // whole line is one tile, so the clamped boundary is folded into the taps:
 // B[n][k] = sum of Q_|j| over the taps j with clamp(n + j) = k.
 // ---------------------------------------------------------------------------
-template <int NZ>
+template <int NZ, int STAGES>
 __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ in, long long plane, long long nlines,
                                                     const TcParams *__restrict__ prm, int r,
                                                     const uint8_t *__restrict__ raw, uint8_t *__restrict__ q,
@@ -271,16 +282,16 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     constexpr uint32_t LBO = 128, SBO = NCH * 128;
     constexpr int ABUF = TM * NZ;               // bytes per plane per buffer
     constexpr int BW = NZ * NZ;                 // bytes per weight limb
-    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [2][4][ABUF] data, [2][ABUF] raw
+    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [STAGES][4][ABUF] data, [STAGES][ABUF] raw
     uint8_t *sw = sm;
     uint8_t *sa = sm + 4 * BW;
-    uint8_t *sr = sa + 2 * 4 * ABUF;
+    uint8_t *sr = sa + STAGES * 4 * ABUF;
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
-    __shared__ long long Qs[PMAX];
-    const int t = threadIdx.x, wp = t >> 5;
+    __shared__ long long Qs[PMAX], Ts[PMAX + 1];
+    const int t = threadIdx.x, wp = t >> 5, m = t & (TM - 1), cg = t >> 7;
     if (wp == 0) tc::tmem_alloc(&tbase, 512);
-    for (int j = t; j < PMAX; j += NT) Qs[j] = prm->Q[2][j];
+    for (int j = t; j < PMAX; j += NT) Qs[j] = j <= r ? prm->Q[2][j] : 0;
     if (t == 0) {
         tc::mbar_init(&mbar, 1);
         tc::mbar_fence_init();
@@ -288,13 +299,21 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    // folded taps, K-major
+    if (t == 0) {  // tail sums T[m] = sum_{j >= m} Q_j
+        Ts[PMAX] = 0;
+        for (int j = PMAX - 1; j >= 0; --j) Ts[j] = Ts[j + 1] + Qs[j];
+    }
+    __syncthreads();
+    // folded taps, K-major: interior k gets Q_|k-n|; k = 0 collects the taps
+    // j <= -n, k = nz-1 the taps j >= nz-1-n
     for (int e = t; e < NZ * NZ; e += NT) {
         const int n = e / NZ, k = e - n * NZ;
         long long qf = 0;
-        for (int j = -r; j <= r; ++j) {
-            const int kk = min(max(n + j, 0), NZ - 1);
-            if (kk == k) qf += Qs[j < 0 ? -j : j];
+        if (k == 0) qf = n < PMAX ? Ts[n] : 0;
+        else if (k == NZ - 1) qf = NZ - 1 - n < PMAX ? Ts[NZ - 1 - n] : 0;
+        else {
+            const int d = k > n ? k - n : n - k;
+            qf = d < PMAX ? Qs[d] : 0;
         }
 #pragma unroll
         for (int b = 0; b < 4; ++b) sw[b * BW + tc::kmajor_off(n, k, LBO, SBO)] = (uint8_t)limb(qf, b);
@@ -303,7 +322,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     const int zs = prm->fw[2] + 8;  // S has scale 2^zs
     const long long half = 1ll << (zs - 1), fmask = (1ll << zs) - 1;
     const uint32_t base = tbase;
-    const uint32_t lane_addr = base + ((uint32_t)(wp * 32) << 16);
+    const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
     const long long ntiles = (nlines + TM - 1) / TM;
     const uint32_t idesc = tc::idesc_i8(TM, NZ, false, false, false, false);
 
@@ -312,9 +331,9 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         const long long l0 = tile * TM;
         const int nl = (int)min((long long)TM, nlines - l0);
 #pragma unroll
-        for (int q2 = 0; q2 < TM * NCH / NT; ++q2) {
+        for (int q2 = 0; q2 < (TM * NCH + NT - 1) / NT; ++q2) {
             const int e = t + NT * q2, l = e / NCH, c = e - l * NCH;
-            if (l < nl) {
+            if (e < TM * NCH && l < nl) {
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
                     tc::cp_async16(sa + (buf * 4 + a) * ABUF + tc::kmajor_off(l, 16 * c, LBO, SBO),
@@ -325,82 +344,104 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         tc::cp_commit();
     };
 
-    long long tile = blockIdx.x;
-    int buf = 0;
-    uint32_t phase = 0;
-    if (tile < ntiles) stage(tile, 0);
-    for (; tile < ntiles; tile += gridDim.x) {
-        tc::cp_wait_all();
+    // same software pipeline as tc_pass_xy
+    const long long t0 = blockIdx.x, gs = gridDim.x;
+    const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
+    auto issue = [&](long long k) {
+        if (t != 0) return;
+        const uint32_t sA = tc::smem_u32(sa + (int)(k % STAGES) * 4 * ABUF), sB = tc::smem_u32(sw);
+        bool first[5] = {true, true, true, true, true};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int acc = a + b - 2;
+                if (acc < 0) continue;
+#pragma unroll
+                for (int ks = 0; ks < NZ / 32; ++ks) {
+                    const uint64_t ad = tc::smem_desc(sA + a * ABUF + ks * 2 * LBO, LBO, SBO);
+                    const uint64_t bd = tc::smem_desc(sB + b * BW + ks * 2 * LBO, LBO, SBO);
+                    tc::mma_i8_ss(base + NZ * acc, ad, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
+                }
+                first[acc] = false;
+            }
+        tc::mma_commit(&mbar);
+    };
+#pragma unroll
+    for (int k = 0; k < STAGES; ++k) {
+        if (k < nmine) stage(t0 + k * gs, k);
+        else tc::cp_commit();
+    }
+    if (nmine > 0) {
+        tc::cp_wait_group<STAGES - 1>();
         tc::fence_async_smem();
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
-        if (t == 0) {
-            const uint32_t sA = tc::smem_u32(sa + buf * 4 * ABUF), sB = tc::smem_u32(sw);
-            bool first[5] = {true, true, true, true, true};
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int acc = a + b - 2;
-                    if (acc < 0) continue;
-#pragma unroll
-                    for (int ks = 0; ks < NZ / 32; ++ks) {
-                        const uint64_t ad = tc::smem_desc(sA + a * ABUF + ks * 2 * LBO, LBO, SBO);
-                        const uint64_t bd = tc::smem_desc(sB + b * BW + ks * 2 * LBO, LBO, SBO);
-                        tc::mma_i8_ss(base + NZ * acc, ad, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
-                    }
-                    first[acc] = false;
-                }
-            tc::mma_commit(&mbar);
-        }
-        const long long nxt = tile + gridDim.x;
-        if (nxt < ntiles) stage(nxt, buf ^ 1);
+        issue(0);
+    }
+    uint32_t phase = 0;
+    constexpr int CW = NZ / 4;  // columns per thread
+    const int h0 = cg * CW;
+    for (long long k = 0; k < nmine; ++k) {
         tc::mbar_wait(&mbar, phase);
         phase ^= 1;
         tc::fence_after();
-        const long long l = tile * TM + t;
-        const uint8_t *rl = sr + buf * ABUF + t * NZ;
+        uint32_t v[5][CW];
 #pragma unroll
-        for (int h = 0; h < NZ; h += 16) {
-            uint32_t v[5][16];
+        for (int acc = 0; acc < 5; ++acc)
 #pragma unroll
-            for (int acc = 0; acc < 5; ++acc) tc::tmem_ld16(lane_addr + NZ * acc + h, v[acc]);
-            tc::tmem_ld_wait();
-            if (l < nlines) {
-                const uint4 rv = *(const uint4 *)(rl + h);
-                const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
-                uint32_t qw[4] = {0, 0, 0, 0};
+            for (int g8 = 0; g8 < CW; g8 += 8)
+                tc::tmem_ld8(lane_addr + NZ * acc + h0 + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
+        tc::tmem_ld_wait();
+        // raw of tile k (slot k % STAGES) before the slot is restaged
+        const long long l = (t0 + k * gs) * TM + m;
+        const uint8_t *rl = sr + (int)(k % STAGES) * ABUF + m * NZ + h0;
+        uint32_t rw[CW / 4];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    long long S = 0;
-#pragma unroll
-                    for (int acc = 0; acc < 5; ++acc) S += (long long)v[acc][c] << (8 * acc);
-                    const long long R = ((long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) - S;
-                    // q = rint(max(R, 0) / 2^zs); certified unless R is within eps
-                    // of a rounding boundary (k + 1/2) 2^zs
-                    uint32_t qv = 0;
-                    long long dist;
-                    if (R > 0) {
-                        qv = (uint32_t)((R + half) >> zs);
-                        dist = (R & fmask) - half;
-                        dist = dist < 0 ? -dist : dist;
-                    } else {
-                        dist = half - R;
-                    }
-                    if (dist <= eps) {
-                        const unsigned long long at = atomicAdd(&fix[0], 1ull);
-                        if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h + c);
-                        else fix[1] = 1;
-                    }
-                    qw[c >> 2] |= (qv & 0xffu) << (8 * (c & 3));
-                }
-                *(uint4 *)(q + l * NZ + h) = make_uint4(qw[0], qw[1], qw[2], qw[3]);
-            }
-        }
+        for (int c4 = 0; c4 < CW / 4; ++c4) rw[c4] = *(const uint32_t *)(rl + 4 * c4);
+        tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
+        tc::fence_async_smem();
         tc::fence_before();
-        buf ^= 1;
+        __syncthreads();
+        tc::fence_after();
+        if (k + 1 < nmine) issue(k + 1);
+        if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
+        else tc::cp_commit();
+        if (l < nlines) {
+            uint32_t qw[CW / 4];
+#pragma unroll
+            for (int c4 = 0; c4 < CW / 4; ++c4) qw[c4] = 0;
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+                long long S = 0;
+#pragma unroll
+                for (int acc = 0; acc < 5; ++acc) S += (long long)v[acc][c] << (8 * acc);
+                const long long R = ((long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) - S;
+                // q = rint(max(R, 0) / 2^zs); certified unless R is within eps
+                // of a rounding boundary (k + 1/2) 2^zs
+                uint32_t qv = 0;
+                long long dist;
+                if (R > 0) {
+                    qv = (uint32_t)((R + half) >> zs);
+                    dist = (R & fmask) - half;
+                    dist = dist < 0 ? -dist : dist;
+                } else {
+                    dist = half - R;
+                }
+                if (dist <= eps) {
+                    const unsigned long long at = atomicAdd(&fix[0], 1ull);
+                    if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
+                    else fix[1] = 1;
+                }
+                qw[c >> 2] |= (qv & 0xffu) << (8 * (c & 3));
+            }
+#pragma unroll
+            for (int c4 = 0; c4 < CW / 4; c4 += 2)
+                *(uint2 *)(q + l * NZ + h0 + 4 * c4) = make_uint2(qw[c4], qw[c4 + 1]);
+        }
     }
+    tc::cp_wait_all();
     __syncthreads();
     tc::fence_after();
     if (wp == 0) tc::tmem_dealloc(base, 512);
@@ -426,27 +467,27 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     if (int st = ct::check_launch("tc_prep")) return st;
     // pass x: [1][nx][ny*nz]
     {
-        const size_t sm = 2 * 1 * KXY * TN + 1024;
-        cudaFuncSetAttribute(tc_pass_xy<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const size_t sm = 8 * 1 * KXY * TN + 1024;
+        cudaFuncSetAttribute(tc_pass_xy<1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TN);
-        tc_pass_xy<1><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
+        tc_pass_xy<1, 8><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
             raw, 0, (int)nx, (int)(ny * nz), 1, prm, 0, rx, p1, N);
         if (int st = ct::check_launch("tc_pass_x")) return st;
     }
     // pass y: [nx][ny][nz]
     {
-        const size_t sm = 2 * 4 * KXY * TN + 1024;
-        cudaFuncSetAttribute(tc_pass_xy<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const size_t sm = 5 * 4 * KXY * TN + 1024;
+        cudaFuncSetAttribute(tc_pass_xy<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TN);
-        tc_pass_xy<4><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
+        tc_pass_xy<4, 5><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
             p1, N, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2, N);
         if (int st = ct::check_launch("tc_pass_y")) return st;
     }
     // pass z + epilogue
     {
         const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
-        const size_t sm = 4 * nz * nz + 2 * 4 * TM * nz + 2 * TM * nz + 1024;
-        auto kz = nz == 64 ? tc_pass_z<64> : tc_pass_z<32>;
+        const size_t sm = 4 * nz * nz + 4 * 4 * TM * nz + 4 * TM * nz + 1024;
+        auto kz = nz == 64 ? tc_pass_z<64, 4> : tc_pass_z<32, 4>;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         kz<<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
         if (int st = ct::check_launch("tc_pass_z")) return st;
