@@ -114,7 +114,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     constexpr int NACC = NPIN == 1 ? 4 : 5;
     constexpr uint32_t LBO = (TN / 16) * 128, SBO = 128;                // MN-major B
     constexpr int BUF = KXY * TN;                                       // bytes per plane per buffer
-    extern __shared__ __align__(1024) uint8_t sm[];                     // [STAGES][NPIN][BUF]
+    constexpr int OROW = 48;                                            // padded output row (bytes)
+    constexpr int OBUF = 4 * TM * OROW;                                 // output tile: [4 planes][128 rows]
+    extern __shared__ __align__(1024) uint8_t sm[];                     // [STAGES][NPIN][BUF], [2][OBUF]
+    uint8_t *sout = sm + STAGES * NPIN * BUF;
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
     __shared__ long long Qs[PMAX];
@@ -159,10 +162,23 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     const long long ntiles = (long long)outer * nti * ncb;
     const uint32_t idesc = tc::idesc_i8(TM, TN, false, false, false, true);
     auto tile_coords = [&](long long tile, int &o, int &ti, int &cb) {
-        cb = (int)(tile % ncb);
-        const long long r2 = tile / ncb;
-        ti = (int)(r2 % nti);
-        o = (int)(r2 / nti);
+        const unsigned tl = (unsigned)tile, r2 = tl / (unsigned)ncb;
+        cb = (int)(tl - r2 * (unsigned)ncb);
+        o = (int)(r2 / (unsigned)nti);
+        ti = (int)(r2 - (unsigned)o * (unsigned)nti);
+    };
+    // coalesced store of a staged output tile: 4 planes x 128 rows x 32 bytes
+    auto flush = [&](long long tile, const uint8_t *ob) {
+        int o, ti, cb;
+        tile_coords(tile, o, ti, cb);
+#pragma unroll
+        for (int q2 = 0; q2 < 4 * TM * 2 / NT; ++q2) {
+            const int e = t + NT * q2, a = e / (2 * TM), mm = (e >> 1) & (TM - 1), hh = e & 1;
+            const int i = ti * TM + mm;
+            if (i < L)
+                *(uint4 *)(out + a * plane_out + ((long long)o * L + i) * inner + (long long)cb * TN + 16 * hh) =
+                    *(const uint4 *)(ob + (a * TM + mm) * OROW + 16 * hh);
+        }
     };
     // stage the B operand of a tile (cp.async): NPIN planes x 256 rows x 32 bytes
     auto stage = [&](long long tile, int buf) {
@@ -241,27 +257,25 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         if (k + 1 < nmine) issue(k + 1);
         if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
         else tc::cp_commit();
-        // epilogue of tile k: row m, columns [8 cg, 8 cg + 8)
-        int o, ti, cb;
-        tile_coords(t0 + k * gs, o, ti, cb);
-        const int i = ti * TM + m;
-        if (i < L) {
-            uint32_t ov[8];
+        if (k > 0) flush(t0 + (k - 1) * gs, sout + (int)((k - 1) & 1) * OBUF);
+        // epilogue of tile k: row m, columns [8 cg, 8 cg + 8) -> staged output
+        uint32_t ov[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                long long S = 0;
+        for (int c = 0; c < 8; ++c) {
+            long long S = 0;
 #pragma unroll
-                for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][c] << (8 * acc);
-                ov[c] = (uint32_t)(S >> shift_out);
-            }
-            uint32_t lo[4], hi[4];
-            planes4(ov[0], ov[1], ov[2], ov[3], lo);
-            planes4(ov[4], ov[5], ov[6], ov[7], hi);
-            const long long off = ((long long)o * L + i) * inner + (long long)cb * TN + h;
-#pragma unroll
-            for (int a = 0; a < 4; ++a) *(uint2 *)(out + a * plane_out + off) = make_uint2(lo[a], hi[a]);
+            for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][c] << (8 * acc);
+            ov[c] = (uint32_t)(S >> shift_out);
         }
+        uint32_t lo[4], hi[4];
+        planes4(ov[0], ov[1], ov[2], ov[3], lo);
+        planes4(ov[4], ov[5], ov[6], ov[7], hi);
+        uint8_t *ob = sout + (int)(k & 1) * OBUF;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) *(uint2 *)(ob + (a * TM + m) * OROW + h) = make_uint2(lo[a], hi[a]);
     }
+    __syncthreads();
+    if (nmine > 0) flush(t0 + (nmine - 1) * gs, sout + (int)((nmine - 1) & 1) * OBUF);
     tc::cp_wait_all();
     __syncthreads();
     tc::fence_after();
@@ -282,10 +296,12 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     constexpr uint32_t LBO = 128, SBO = NCH * 128;
     constexpr int ABUF = TM * NZ;               // bytes per plane per buffer
     constexpr int BW = NZ * NZ;                 // bytes per weight limb
-    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [STAGES][4][ABUF] data, [STAGES][ABUF] raw
+    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [STAGES][4][ABUF] data, [STAGES][ABUF] raw,
+                                                     // [2][ABUF] q tile
     uint8_t *sw = sm;
     uint8_t *sa = sm + 4 * BW;
     uint8_t *sr = sa + STAGES * 4 * ABUF;
+    uint8_t *sq = sr + STAGES * ABUF;
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
     __shared__ long long Qs[PMAX], Ts[PMAX + 1];
@@ -344,6 +360,12 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         tc::cp_commit();
     };
 
+    // coalesced store of a staged q tile (lines are contiguous in global)
+    auto flush = [&](long long tile, const uint8_t *qb) {
+        const long long l0 = tile * TM;
+        const int nbytes = (int)min((long long)TM, nlines - l0) * NZ;
+        for (int e = 16 * t; e < nbytes; e += 16 * NT) *(uint4 *)(q + l0 * NZ + e) = *(const uint4 *)(qb + e);
+    };
     // same software pipeline as tc_pass_xy
     const long long t0 = blockIdx.x, gs = gridDim.x;
     const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
@@ -408,10 +430,11 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         if (k + 1 < nmine) issue(k + 1);
         if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
         else tc::cp_commit();
-        if (l < nlines) {
-            uint32_t qw[CW / 4];
+        if (k > 0) flush(t0 + (k - 1) * gs, sq + (int)((k - 1) & 1) * ABUF);
+        uint32_t qw[CW / 4];
 #pragma unroll
-            for (int c4 = 0; c4 < CW / 4; ++c4) qw[c4] = 0;
+        for (int c4 = 0; c4 < CW / 4; ++c4) qw[c4] = 0;
+        if (l < nlines) {
 #pragma unroll
             for (int c = 0; c < CW; ++c) {
                 long long S = 0;
@@ -436,11 +459,13 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
                 }
                 qw[c >> 2] |= (qv & 0xffu) << (8 * (c & 3));
             }
-#pragma unroll
-            for (int c4 = 0; c4 < CW / 4; c4 += 2)
-                *(uint2 *)(q + l * NZ + h0 + 4 * c4) = make_uint2(qw[c4], qw[c4 + 1]);
         }
+        uint8_t *qb = sq + (int)(k & 1) * ABUF + m * NZ + h0;
+#pragma unroll
+        for (int c4 = 0; c4 < CW / 4; c4 += 2) *(uint2 *)(qb + 4 * c4) = make_uint2(qw[c4], qw[c4 + 1]);
     }
+    __syncthreads();
+    if (nmine > 0) flush(t0 + (nmine - 1) * gs, sq + (int)((nmine - 1) & 1) * ABUF);
     tc::cp_wait_all();
     __syncthreads();
     tc::fence_after();
@@ -467,7 +492,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     if (int st = ct::check_launch("tc_prep")) return st;
     // pass x: [1][nx][ny*nz]
     {
-        const size_t sm = 8 * 1 * KXY * TN + 1024;
+        const size_t sm = 8 * 1 * KXY * TN + 2 * 4 * TM * 48 + 1024;
         cudaFuncSetAttribute(tc_pass_xy<1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TN);
         tc_pass_xy<1, 8><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
@@ -476,7 +501,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     }
     // pass y: [nx][ny][nz]
     {
-        const size_t sm = 5 * 4 * KXY * TN + 1024;
+        const size_t sm = 5 * 4 * KXY * TN + 2 * 4 * TM * 48 + 1024;
         cudaFuncSetAttribute(tc_pass_xy<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TN);
         tc_pass_xy<4, 5><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
@@ -486,7 +511,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     // pass z + epilogue
     {
         const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
-        const size_t sm = 4 * nz * nz + 4 * 4 * TM * nz + 4 * TM * nz + 1024;
+        const size_t sm = 4 * nz * nz + 4 * 4 * TM * nz + 4 * TM * nz + 2 * TM * nz + 1024;
         auto kz = nz == 64 ? tc_pass_z<64, 4> : tc_pass_z<32, 4>;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         kz<<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
