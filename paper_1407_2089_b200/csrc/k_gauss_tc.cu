@@ -204,27 +204,30 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     // stores) runs from registers while MMA(k+1) executes.
     const long long t0 = blockIdx.x, gs = gridDim.x;
     const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
+    // MMA issue: warp 0, one elected lane; descriptors = one base + constants
     auto issue = [&](long long k) {
-        if (t != 0) return;
-        const uint32_t sb = tc::smem_u32(sm + (int)(k % STAGES) * NPIN * BUF);
-        bool first[NACC];
+        if (wp != 0) return;
+        const uint64_t d0 = tc::smem_desc(tc::smem_u32(sm + (int)(k % STAGES) * NPIN * BUF), LBO, SBO);
+        if (tc::elect_one()) {
+            bool first[NACC];
 #pragma unroll
-        for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
+            for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
 #pragma unroll
-        for (int a = 0; a < NPIN; ++a)
+            for (int a = 0; a < NPIN; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int acc = NPIN == 1 ? b : a + b - 2;
-                if (acc < 0) continue;
-                const uint32_t d = base + 256 + TN * acc;
+                for (int b = 0; b < 4; ++b) {
+                    const int acc = NPIN == 1 ? b : a + b - 2;
+                    if (acc < 0) continue;
 #pragma unroll
-                for (int ks = 0; ks < KXY / 32; ++ks) {
-                    const uint64_t bd = tc::smem_desc(sb + a * BUF + ks * 4 * LBO, LBO, SBO);
-                    tc::mma_i8_ts(d, base + b * 64 + ks * 8, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
+                    for (int ks = 0; ks < KXY / 32; ++ks)
+                        tc::mma_i8_ts(base + 256 + TN * acc, base + b * 64 + ks * 8,
+                                      d0 + (uint64_t)((a * BUF + ks * 4 * LBO) >> 4), idesc,
+                                      first[acc] && ks == 0 ? 0u : 1u);
+                    first[acc] = false;
                 }
-                first[acc] = false;
-            }
-        tc::mma_commit(&mbar);
+            tc::mma_commit(&mbar);
+        }
+        __syncwarp();
     };
 #pragma unroll
     for (int k = 0; k < STAGES; ++k) {
@@ -370,24 +373,27 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     const long long t0 = blockIdx.x, gs = gridDim.x;
     const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
     auto issue = [&](long long k) {
-        if (t != 0) return;
-        const uint32_t sA = tc::smem_u32(sa + (int)(k % STAGES) * 4 * ABUF), sB = tc::smem_u32(sw);
-        bool first[5] = {true, true, true, true, true};
+        if (wp != 0) return;
+        const uint64_t a0 = tc::smem_desc(tc::smem_u32(sa + (int)(k % STAGES) * 4 * ABUF), LBO, SBO);
+        const uint64_t b0 = tc::smem_desc(tc::smem_u32(sw), LBO, SBO);
+        if (tc::elect_one()) {
+            bool first[5] = {true, true, true, true, true};
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int acc = a + b - 2;
-                if (acc < 0) continue;
+                for (int b = 0; b < 4; ++b) {
+                    const int acc = a + b - 2;
+                    if (acc < 0) continue;
 #pragma unroll
-                for (int ks = 0; ks < NZ / 32; ++ks) {
-                    const uint64_t ad = tc::smem_desc(sA + a * ABUF + ks * 2 * LBO, LBO, SBO);
-                    const uint64_t bd = tc::smem_desc(sB + b * BW + ks * 2 * LBO, LBO, SBO);
-                    tc::mma_i8_ss(base + NZ * acc, ad, bd, idesc, first[acc] && ks == 0 ? 0u : 1u);
+                    for (int ks = 0; ks < NZ / 32; ++ks)
+                        tc::mma_i8_ss(base + NZ * acc, a0 + (uint64_t)((a * ABUF + ks * 2 * LBO) >> 4),
+                                      b0 + (uint64_t)((b * BW + ks * 2 * LBO) >> 4), idesc,
+                                      first[acc] && ks == 0 ? 0u : 1u);
+                    first[acc] = false;
                 }
-                first[acc] = false;
-            }
-        tc::mma_commit(&mbar);
+            tc::mma_commit(&mbar);
+        }
+        __syncwarp();
     };
 #pragma unroll
     for (int k = 0; k < STAGES; ++k) {
