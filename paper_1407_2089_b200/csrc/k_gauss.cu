@@ -467,9 +467,9 @@ __global__ void __launch_bounds__(256) gauss_fixup(const Traw *__restrict__ raw,
     }
 }
 
-// Grid-wide exact recompute of the first F = min(count, capF) fix entries in
-// three phases (scratch P1[F][2ry+1][nz], P2[F][nz] doubles): pass x at the
-// (2ry+1) x nz positions of each entry's cone, pass y on its z-line, pass z +
+// Exact recompute of the first F = min(count, capF) fix entries (scratch
+// P1[F][2ry+1][nz] doubles): pass x at the (2ry+1) x nz positions of each
+// entry's cone (grid-wide), then per entry pass y on its z-line and pass z +
 // residual at the voxel -- the operations and order of ct_gaussian_residual.
 template <typename Traw>
 __global__ void fix_p1(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz, const double *__restrict__ w, int rx,
@@ -484,7 +484,18 @@ __global__ void fix_p1(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz, con
         const i64 jj = ct::clampi(j + tt - ry, 0, ny - 1);
         const Traw *col = raw + jj * nz + kk;
         double acc = __dmul_rn(ct::to_f64(col[i * S]), w[0]);
-        for (int d = rx; d >= 1; --d) {
+        int d = rx;
+        for (; d >= 8; d -= 8) {  // loads of 8 taps in flight, adds in scipy's order
+            double lo[8], hi[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                lo[u] = ct::to_f64(__ldg(col + ct::clampi(i - (d - u), 0, nx - 1) * S));
+                hi[u] = ct::to_f64(__ldg(col + ct::clampi(i + (d - u), 0, nx - 1) * S));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(lo[u], hi[u]), w[d - u]));
+        }
+        for (; d >= 1; --d) {
             const double sm = __dadd_rn(ct::to_f64(col[ct::clampi(i - d, 0, nx - 1) * S]),
                                         ct::to_f64(col[ct::clampi(i + d, 0, nx - 1) * S]));
             acc = __dadd_rn(acc, __dmul_rn(sm, w[d]));
@@ -493,33 +504,45 @@ __global__ void fix_p1(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz, con
     }
 }
 
-__global__ void fix_p2(i64 nz, const double *__restrict__ wy, int ry, const unsigned long long *__restrict__ fix,
-                       long long cap, long long capF, const double *__restrict__ P1, double *__restrict__ P2) {
-    const long long F = min(min((long long)fix[0], cap), capF);
-    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < F * nz; e += (i64)gridDim.x * blockDim.x) {
-        const i64 f = e / nz, kk = e - f * nz;
-        const double *c = P1 + f * (2 * ry + 1) * nz + kk;
-        double acc = __dmul_rn(c[(i64)ry * nz], wy[0]);
-        for (int d = ry; d >= 1; --d)
-            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(c[(i64)(ry - d) * nz], c[(i64)(ry + d) * nz]), wy[d]));
-        P2[e] = acc;
-    }
-}
-
+// phases 2+3: one CTA (nz threads) per entry: P2 line in SMEM, then pass z +
+// residual at the voxel
 template <typename Traw, typename Tq>
-__global__ void fix_q(const Traw *__restrict__ raw, i64 nz, const double *__restrict__ wz, int rz,
-                      const unsigned long long *__restrict__ fix, long long cap, long long capF,
-                      const double *__restrict__ P2, Tq *__restrict__ q_out) {
+__global__ void fix_p2q(const Traw *__restrict__ raw, i64 nz, const double *__restrict__ wy, int ry,
+                        const double *__restrict__ wz, int rz, const unsigned long long *__restrict__ fix,
+                        long long cap, long long capF, const double *__restrict__ P1, Tq *__restrict__ q_out) {
+    __shared__ double line[128];
     const long long F = min(min((long long)fix[0], cap), capF);
-    for (i64 f = blockIdx.x * (i64)blockDim.x + threadIdx.x; f < F; f += (i64)gridDim.x * blockDim.x) {
-        const i64 p = (i64)fix[2 + f], k = p % nz;
-        const double *l = P2 + f * nz;
-        double acc = __dmul_rn(l[k], wz[0]);
-        for (int d = rz; d >= 1; --d)
-            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(l[ct::clampi(k - d, 0, nz - 1)], l[ct::clampi(k + d, 0, nz - 1)]),
-                                           wz[d]));
-        const double dd = __dadd_rn(ct::to_f64(raw[p]), -acc);
-        q_out[p] = (Tq)rint(dd < 0.0 ? 0.0 : dd);
+    const int kk = threadIdx.x;
+    for (long long f = blockIdx.x; f < F; f += gridDim.x) {
+        __syncthreads();
+        if (kk < nz) {
+            const double *c = P1 + f * (2 * ry + 1) * nz + kk;
+            double acc = __dmul_rn(c[(i64)ry * nz], wy[0]);
+            int d = ry;
+            for (; d >= 8; d -= 8) {  // 16 loads in flight, adds in scipy's order
+                double lo[8], hi[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    lo[u] = c[(i64)(ry - (d - u)) * nz];
+                    hi[u] = c[(i64)(ry + (d - u)) * nz];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(lo[u], hi[u]), wy[d - u]));
+            }
+            for (; d >= 1; --d)
+                acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(c[(i64)(ry - d) * nz], c[(i64)(ry + d) * nz]), wy[d]));
+            line[kk] = acc;
+        }
+        __syncthreads();
+        if (kk == 0) {
+            const i64 p = (i64)fix[2 + f], k = p % nz;
+            double acc = __dmul_rn(line[k], wz[0]);
+            for (int d = rz; d >= 1; --d)
+                acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(line[ct::clampi(k - d, 0, nz - 1)],
+                                                         line[ct::clampi(k + d, 0, nz - 1)]), wz[d]));
+            const double dd = __dadd_rn(ct::to_f64(raw[p]), -acc);
+            q_out[p] = (Tq)rint(dd < 0.0 ? 0.0 : dd);
+        }
     }
 }
 
@@ -530,12 +553,10 @@ int launch_fixup(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int r
                  size_t work_bytes, const unsigned long long *fix, long long cap, Traw *q, cudaStream_t s) {
     const double *wx = w, *wy = w + rx + 1, *wz = wy + ry + 1;
     const i64 per = (2 * (i64)ry + 1) * nz;
-    const long long capF = (long long)(work_bytes / ((size_t)(per + nz) * sizeof(double)));
-    double *P1 = (double *)work, *P2 = P1 + (size_t)capF * per;
-    const int grid = CT_NUM_SMS * 8;
-    fix_p1<Traw><<<grid, 256, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
-    fix_p2<<<grid, 256, 0, s>>>(nz, wy, ry, fix, cap, capF, P1, P2);
-    fix_q<Traw, Traw><<<grid, 256, 0, s>>>(raw, nz, wz, rz, fix, cap, capF, P2, q);
+    const long long capF = nz <= 128 ? (long long)(work_bytes / ((size_t)per * sizeof(double))) : 0;
+    double *P1 = (double *)work;
+    fix_p1<Traw><<<CT_NUM_SMS * 8, 256, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
+    fix_p2q<Traw, Traw><<<CT_NUM_SMS * 2, 128, 0, s>>>(raw, nz, wy, ry, wz, rz, fix, cap, capF, P1, q);
     if (int st = ct::check_launch("fixup phases")) return st;
     const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
     cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);

@@ -30,7 +30,7 @@
 
 namespace {
 
-constexpr int FW = 35;         // weight scale bits (lowered per axis so that every Q_j < 2^32)
+constexpr int FW = 40;         // max weight scale bits (lowered per axis so that every Q_j < 2^32)
 constexpr int FD = 24;         // fractional bits of the intermediates
 constexpr int TM = 128;        // output rows per tile (passes x, y) / lines per tile (pass z)
 constexpr int TN = 32;         // columns per tile (passes x, y)
@@ -45,49 +45,62 @@ struct TcParams {
 };
 
 // ---------------------------------------------------------------------------
-// Setup: integer taps and the certified error bound (single thread).
+// Setup: integer taps and the certified error bound (one warp per axis).
 // ---------------------------------------------------------------------------
-__global__ void tc_prep(const double *__restrict__ w, int rx, int ry, int rz, double vmax, double eps_override,
-                        TcParams *prm) {
-    if (threadIdx.x || blockIdx.x) return;
+__global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int rx, int ry, int rz, double vmax,
+                                               double eps_override, TcParams *prm) {
+    // warp a handles axis a: lane-parallel taps, warp reductions
+    const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rr[3] = {rx, ry, rz};
-    const double *ws[3] = {w, w + rx + 1, w + rx + 1 + ry + 1};
-    double bound = 0.0;
-    for (int a = 0; a < 3; ++a) {
-        int fw = FW;
-        // largest integer tap: w_0 (x, y) or the folded edge sum_{j>=0} w_j (z)
-        double wmax = 0.0;
-        for (int j = 0; j <= rr[a]; ++j) wmax = a == 2 ? wmax + ws[a][j] : fmax(wmax, ws[a][j]);
-        wmax *= 1.0000001;
-        while (fw > 24 && wmax * ldexp(1.0, fw) >= 4294967295.0) --fw;
-        prm->fw[a] = fw;
-        const double scale = ldexp(1.0, fw);
-        double dq = 0.0, qsum0 = 0.0, qsum1 = 0.0;
-        for (int j = 0; j < PMAX; ++j) prm->Q[a][j] = 0;
-        for (int j = 0; j <= rr[a]; ++j) {
-            const double x = ws[a][j] * scale;     // exact (power-of-two scaling)
-            const long long q = __double2ll_rn(x);
-            prm->Q[a][j] = q;
-            const double d = fabs((double)q - x);  // exact
-            const double mult = j ? 2.0 : 1.0;     // taps -j and +j
-            dq += mult * d;
+    const double *ws = a == 0 ? w : (a == 1 ? w + rx + 1 : w + rx + 1 + ry + 1);
+    const int r = rr[a];
+    double wmax = 0.0;  // largest tap (w_0)
+    for (int j = lane; j <= r; j += 32) wmax = fmax(wmax, ws[j]);
+    for (int o = 16; o; o >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    wmax *= 1.0000001;
+    int fw = FW;
+    while (fw > 24 && wmax * ldexp(1.0, fw) >= 4294967295.0) --fw;
+    const double scale = ldexp(1.0, fw);
+    double dq = 0.0, qsum0 = 0.0, qsum1 = 0.0;
+    for (int j = lane; j < PMAX; j += 32) {
+        long long q = 0;
+        if (j <= r) {
+            const double x = ws[j] * scale;     // exact (power-of-two scaling)
+            q = __double2ll_rn(x);
+            const double mult = j ? 2.0 : 1.0;  // taps -j and +j
+            dq += mult * fabs((double)q - x);   // exact difference
             qsum0 += mult * (double)(q & 0xff);
             qsum1 += mult * (double)((q >> 8) & 0xff);
         }
-        // weight rounding: sum_j |Q_j 2^-35 - w_j| * max input (inputs of passes
-        // y, z are bounded by vmax up to rounding of the taps' sum)
-        bound += dq / scale * vmax * 1.001;
-        if (a == 2) qsum0 = qsum1 = 64.0 * 255.0;  // folded taps: bound the limb sums per row
-        if (a > 0) {
-            // dropped limb pairs (a+b <= 1): (0,0), (1,0), (0,1); data limbs <= 255
-            bound += 255.0 * (qsum0 * ldexp(1.0, -fw - FD) + (qsum0 + qsum1) * ldexp(1.0, 8 - fw - FD));
-        }
+        prm->Q[a][j] = q;
     }
-    bound += 2.0 * ldexp(1.0, -FD);                                     // truncation of P1, P2
-    bound += 4.0 * (rx + ry + rz + 12) * ldexp(1.0, -53) * vmax;         // scipy float64 order + residual
-    const int zs = prm->fw[2] + 8;  // scale bits of the final sum
-    prm->eps = (long long)ceil(bound * 1.25 * ldexp(1.0, zs)) + 16;
-    if (eps_override > 0.0) prm->eps = (long long)ceil(eps_override * ldexp(1.0, zs));
+    for (int o = 16; o; o >>= 1) {
+        dq += __shfl_xor_sync(0xffffffffu, dq, o);
+        qsum0 += __shfl_xor_sync(0xffffffffu, qsum0, o);
+        qsum1 += __shfl_xor_sync(0xffffffffu, qsum1, o);
+    }
+    // per-axis bound: weight rounding sum_j |Q_j 2^-fw - w_j| * max input (the
+    // inputs of passes y, z are bounded by vmax up to the taps' sum rounding)
+    // plus, for y and z, the dropped limb pairs (a+b <= 1: (0,0), (1,0), (0,1))
+    double b = dq / scale * vmax * 1.001;
+    if (a > 0) b += 255.0 * (qsum0 * ldexp(1.0, -fw - FD) + (qsum0 + qsum1) * ldexp(1.0, 8 - fw - FD));
+    __shared__ double bs[3];
+    __shared__ int fws[3];
+    if (lane == 0) {
+        bs[a] = b;
+        fws[a] = fw;
+        prm->fw[a] = fw;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bound = bs[0] + bs[1] + bs[2];
+        bound += 2.0 * ldexp(1.0, -FD);                              // truncation of P1, P2
+        bound += 4.0 * ldexp(1.0, -(fws[2] + 8));                    // floor of pass z edge terms
+        bound += 4.0 * (rx + ry + rz + 12) * ldexp(1.0, -53) * vmax;  // scipy float64 order + residual
+        const int zs = fws[2] + 8;  // scale bits of the final sum
+        prm->eps = (long long)ceil(bound * 1.25 * ldexp(1.0, zs)) + 16;
+        if (eps_override > 0.0) prm->eps = (long long)ceil(eps_override * ldexp(1.0, zs));
+    }
 }
 
 __device__ __forceinline__ uint32_t limb(long long q, int b) { return (uint32_t)((q >> (8 * b)) & 0xff); }
@@ -287,8 +300,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
 
 // ---------------------------------------------------------------------------
 // Pass z + residual + quantisation + certification.  NZ in {32, 64}.  The
-// whole line is one tile, so the clamped boundary is folded into the taps:
-// B[n][k] = sum of Q_|j| over the taps j with clamp(n + j) = k.
+// whole line is one tile: the MMA applies the taps that land inside the line
+// (B[n][k] = Q_|k-n|); the taps beyond either end all read the edge value
+// (mode "nearest"), so the epilogue adds x[0] E0[n] + x[nz-1] EL[n] with the
+// integer tail sums E0[n] = sum_{j < -n} Q_|j|, EL[n] = sum_{j > nz-1-n} Q_j.
 // ---------------------------------------------------------------------------
 template <int NZ, int STAGES>
 __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ in, long long plane, long long nlines,
@@ -308,6 +323,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
     __shared__ long long Qs[PMAX], Ts[PMAX + 1];
+    __shared__ uint4 Et[NZ];  // edge tail sums split at 2^16: {E0 >> 16, E0 & 0xffff, EL >> 16, EL & 0xffff}
     const int t = threadIdx.x, wp = t >> 5, m = t & (TM - 1), cg = t >> 7;
     if (wp == 0) tc::tmem_alloc(&tbase, 512);
     for (int j = t; j < PMAX; j += NT) Qs[j] = j <= r ? prm->Q[2][j] : 0;
@@ -323,19 +339,17 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         for (int j = PMAX - 1; j >= 0; --j) Ts[j] = Ts[j + 1] + Qs[j];
     }
     __syncthreads();
-    // folded taps, K-major: interior k gets Q_|k-n|; k = 0 collects the taps
-    // j <= -n, k = nz-1 the taps j >= nz-1-n
+    // taps inside the line, K-major; edge tail sums
     for (int e = t; e < NZ * NZ; e += NT) {
         const int n = e / NZ, k = e - n * NZ;
-        long long qf = 0;
-        if (k == 0) qf = n < PMAX ? Ts[n] : 0;
-        else if (k == NZ - 1) qf = NZ - 1 - n < PMAX ? Ts[NZ - 1 - n] : 0;
-        else {
-            const int d = k > n ? k - n : n - k;
-            qf = d < PMAX ? Qs[d] : 0;
-        }
+        const int d = k > n ? k - n : n - k;
+        const long long qv = d < PMAX ? Qs[d] : 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) sw[b * BW + tc::kmajor_off(n, k, LBO, SBO)] = (uint8_t)limb(qf, b);
+        for (int b = 0; b < 4; ++b) sw[b * BW + tc::kmajor_off(n, k, LBO, SBO)] = (uint8_t)limb(qv, b);
+    }
+    for (int n = t; n < NZ; n += NT) {
+        const long long e0 = n + 1 <= PMAX ? Ts[n + 1] : 0, el = NZ - n <= PMAX ? Ts[NZ - n] : 0;
+        Et[n] = make_uint4((uint32_t)(e0 >> 16), (uint32_t)(e0 & 0xffff), (uint32_t)(el >> 16), (uint32_t)(el & 0xffff));
     }
     const long long eps = prm->eps;
     const int zs = prm->fw[2] + 8;  // S has scale 2^zs
@@ -422,12 +436,22 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
             for (int g8 = 0; g8 < CW; g8 += 8)
                 tc::tmem_ld8(lane_addr + NZ * acc + h0 + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
         tc::tmem_ld_wait();
-        // raw of tile k (slot k % STAGES) before the slot is restaged
+        // raw and the line's edge values of tile k (slot k % STAGES) before the slot is restaged
         const long long l = (t0 + k * gs) * TM + m;
         const uint8_t *rl = sr + (int)(k % STAGES) * ABUF + m * NZ + h0;
         uint32_t rw[CW / 4];
 #pragma unroll
         for (int c4 = 0; c4 < CW / 4; ++c4) rw[c4] = *(const uint32_t *)(rl + 4 * c4);
+        uint32_t x0 = 0, xl = 0;
+        {
+            const uint8_t *ab = sa + (int)(k % STAGES) * 4 * ABUF;
+            const uint32_t o0 = tc::kmajor_off(m, 0, LBO, SBO), ol = tc::kmajor_off(m, NZ - 1, LBO, SBO);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                x0 |= (uint32_t)ab[a * ABUF + o0] << (8 * a);
+                xl |= (uint32_t)ab[a * ABUF + ol] << (8 * a);
+            }
+        }
         tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
         tc::fence_async_smem();
         tc::fence_before();
@@ -446,6 +470,12 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
                 long long S = 0;
 #pragma unroll
                 for (int acc = 0; acc < 5; ++acc) S += (long long)v[acc][c] << (8 * acc);
+                {   // edge taps: floor((x0 E0 + xl EL) / 2^16), split to stay in 64 bits
+                    const uint4 e = Et[h0 + c];
+                    const unsigned long long hi = (unsigned long long)x0 * e.x + (unsigned long long)xl * e.z;
+                    const unsigned long long lo = (unsigned long long)x0 * e.y + (unsigned long long)xl * e.w;
+                    S += (long long)(hi + (lo >> 16));
+                }
                 const long long R = ((long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) - S;
                 // q = rint(max(R, 0) / 2^zs); certified unless R is within eps
                 // of a rounding boundary (k + 1/2) 2^zs
@@ -494,7 +524,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     uint8_t *p1 = (uint8_t *)work, *p2 = p1 + 4 * N;
     TcParams *prm = (TcParams *)(p2 + 4 * N);
     cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
-    tc_prep<<<1, 1, 0, s>>>(w, rx, ry, rz, 255.0, eps_override, prm);
+    tc_prep<<<1, 96, 0, s>>>(w, rx, ry, rz, 255.0, eps_override, prm);
     if (int st = ct::check_launch("tc_prep")) return st;
     // pass x: [1][nx][ny*nz]
     {
