@@ -261,41 +261,42 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, pipe, spec, sp, dev, world, s_cell, s_vess)
 
-    # --- roofline of the dominant kernel (K1, FP64-pipe bound) --------------
+    # --- roofline of the dominant stage -------------------------------------
+    # algorithmic HBM bytes per voxel of each stage (inputs read + outputs
+    # written once) and, for K1, the int8 tensor-core work per voxel
     pk = peaks()
     rx, ry, rz = pipe.r
-    fp64_ops = 3 * (rx + ry + rz) + 3
-    k1_ms = stage_ms.get("K1 gaussian")
-    fp64_peak = measured_fp64_peak(dev)
-    roof = None
-    if k1_ms:
-        k1_bytes = 2 * nvox  # read raw u8 + write q u8 (algorithmic)
-        achieved_tf = fp64_ops * nvox / (k1_ms / 1e3) / 1e12
-        traffic = ncu_traffic("gauss")
-        roof = {
-            "kernel": "K1 gaussian (3 separable FP64 passes, scipy order, no FMA)",
-            "bound": "fp64",
-            "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak,
-            "peak_source": "ct_fp64_peak (DADD+DMUL dependent-free loop, measured in this run)",
-            "traffic": traffic,
-            "hbm": {"achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / pk["hbm_gbs"], "peak_source": pk["source"],
-                    "algorithmic_bytes_per_voxel": 2},
-            "fp64_ops_per_voxel": fp64_ops,
-            "share_of_cell_stream": k1_ms / sum(v for k, v in stage_ms.items() if k.startswith(("K1", "K2", "K3 o", "K4", "K5", "K6"))),
-        }
+    nzv = spec.nz
+    k1_tc = pipe.k1_path_tc
+    k1_macs = (4 * 256 + 13 * 256 + 13 * nzv) if k1_tc else None  # limb-pair MMAs (see k_gauss_tc.cu)
+    bpv = {"K1 gaussian": 2, "K2 median+hist": 2, "K4 threshold+close": 2, "K5 ccl": 5, "K6 table": 0,
+           "K7 mrf": 3, "K3+K4 vessel otsu+close": 2, "K8 edt": 9}
     kernels, kernels_serial = {}, {}
-    bpv = {"K2 median+hist": 2, "K4 threshold+close": 2, "K5 ccl": 5, "K6 table": 0, "K7 mrf": 3,
-           "K3+K4 vessel otsu+close": 2, "K8 edt": 9, "K1 gaussian": 2}
     for src, dst in ((stage_ms, kernels), (serial_ms, kernels_serial)):
         for k, v in src.items():
             b = bpv.get(k)
             dst[k] = {"ms": v, "hbm_gbs": (b * nvox / (v / 1e3) / 1e9) if b else None,
                       "hbm_frac": (b * nvox / (v / 1e3) / 1e9 / pk["hbm_gbs"]) if b else None,
                       "algorithmic_bytes_per_voxel": b}
-    if roof is not None and serial_ms.get("K1 gaussian"):
-        roof["serial_ms"] = serial_ms["K1 gaussian"]
-        roof["serial_frac"] = fp64_ops * nvox / (serial_ms["K1 gaussian"] / 1e3) / 1e12 / fp64_peak
+    dom = max(serial_ms, key=serial_ms.get)
+    ms_dom = serial_ms[dom]
+    if dom == "K1 gaussian" and k1_tc:
+        int8_peak = 2.0 * pk["bf16_tflops"]
+        achieved = 2 * k1_macs * nvox / (ms_dom / 1e3) / 1e12
+        roof = {"kernel": "K1 gaussian on tcgen05 int8 (limb-split taps, 3 banded GEMM passes)", "bound": "tensor",
+                "achieved": achieved, "peak": int8_peak, "unit": "TOPS", "frac": achieved / int8_peak,
+                "peak_source": "2 x measured dense bf16 (" + pk["source"] + "): B200 int8 dense = 2x bf16",
+                "work_per_voxel": {"int8_macs": k1_macs, "useful_taps": (2 * rx + 1) + (2 * ry + 1) + (2 * rz + 1)}}
+    else:
+        b = bpv.get(dom) or 1
+        achieved = b * nvox / (ms_dom / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"], "algorithmic_bytes_per_voxel": b}
+    roof.update({"stage": dom, "ms_serial": ms_dom, "ms_overlapped": stage_ms.get(dom),
+                 "timing": "CUDA events around the stage on its stream, serialized pass (3 time points)",
+                 "traffic": ncu_traffic(dom),
+                 "traffic_note": "DRAM bytes of the stage's kernels per time point, ncu launch list (profiles/)",
+                 "share_of_step_serial": ms_dom / sum(serial_ms.values())})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -315,7 +316,8 @@ def run_ours(args):
                        "frames_per_s": world * args.steps / (ms_max / 1e3),
                        "l2": f"inputs larger than L2: {2 * nvox / 1e6:.0f} MB/step from a ring of {ring} "
                              "distinct time points, plus GB-scale intermediates"},
-            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof, "kernels": kernels, "kernels_serial": kernels_serial,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof, "kernels": kernels,
+            "kernels_serial": kernels_serial,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -113,6 +113,10 @@ int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz
  * only, 2 tensor cores only (CT_ERR_UNSUPPORTED when the shape does not fit). */
 int ct_set_k1_path(int mode);
 
+/* Which arithmetic ct_gaussian_q uses for this shape under the current mode:
+ * 2 tensor cores, 1 FP64 FMA (both certified; informational). */
+int ct_k1_path(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz);
+
 /* float64 copy of a U8/U16/F64 volume (ref denoise.py:84, :158 astype). */
 int ct_to_f64(const void *in, int dtype, int64_t n, double *out, void *stream);
 

@@ -60,6 +60,7 @@ SIGNATURES = {
     "ct_gaussian_residual": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _P, _INT, _P]),
     "ct_gaussian_q": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _I64, _D, _P]),
     "ct_set_k1_path": (_INT, [_INT]),
+    "ct_k1_path": (_INT, [_INT, _I64, _I64, _I64, _INT, _INT, _INT]),
     "ct_to_f64": (_INT, [_P, _INT, _I64, _P, _P]),
     "ct_median": (_INT, [_P, _INT, _I64, _I64, _I64, _INT, _P, _P, _P]),
     "ct_histogram": (_INT, [_P, _INT, _I64, _P, _P]),

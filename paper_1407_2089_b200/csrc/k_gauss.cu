@@ -596,9 +596,16 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
                      void *work, uint8_t *q, unsigned long long *fix, int64_t cap, double eps_override,
                      cudaStream_t s);
 
+bool ct_gaussian_q_tc_fits(int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz);
+
 // K1 fast-path selection (ct_set_k1_path): 0 auto (tensor cores when the
 // shape fits, else FP64 FMA), 1 FP64 FMA, 2 tensor cores only.
 static int g_k1_path = 0;
+extern "C" int ct_k1_path(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz) {
+    if (dtype == CT_U8 && g_k1_path != 1 && ct_gaussian_q_tc_fits(nx, ny, nz, rx, ry, rz)) return 2;
+    return 1;
+}
+
 extern "C" int ct_set_k1_path(int mode) {
     if (mode < 0 || mode > 2) {
         ct::set_error("k1 path mode must be 0, 1 or 2");

@@ -513,13 +513,15 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
 // TC path of ct_gaussian_q (u8).  Returns CT_ERR_UNSUPPORTED when the shape
 // does not fit (the caller then uses the SIMT FMA path).  work: >= 8 N bytes
 // (byte planes of P1 and P2) + sizeof(TcParams).
+bool ct_gaussian_q_tc_fits(int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz) {
+    return (nz == 32 || nz == 64) && rx >= 0 && ry >= 0 && rz >= 0 && rx <= (KXY - TM) / 2 && ry <= (KXY - TM) / 2 &&
+           rz < PMAX && (ny * nz) % TN == 0 && nx * ny * nz < (1ll << 31);
+}
+
 int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry, int rz,
                      void *work, uint8_t *q, unsigned long long *fix, int64_t cap, double eps_override,
                      cudaStream_t s) {
-    if (!(nz == 32 || nz == 64) || rx < 0 || ry < 0 || rz < 0 || rx > (KXY - TM) / 2 || ry > (KXY - TM) / 2 ||
-        rz >= PMAX || (ny * nz) % TN || nx * ny * nz >= (1ll << 31) ||
-        ((uintptr_t)raw & 15))
-        return CT_ERR_UNSUPPORTED;
+    if (!ct_gaussian_q_tc_fits(nx, ny, nz, rx, ry, rz) || ((uintptr_t)raw & 15)) return CT_ERR_UNSUPPORTED;
     const long long N = nx * ny * nz;
     uint8_t *p1 = (uint8_t *)work, *p2 = p1 + 4 * N;
     TcParams *prm = (TcParams *)(p2 + 4 * N);

@@ -144,6 +144,15 @@ class FramePipeline:
         return {k: float(np.mean(v)) for k, v in out.items()}
 
     # -- launches (current torch stream; no host sync) ---------------------
+    @property
+    def k1_path_tc(self) -> bool:
+        """True when K1 runs on the tensor cores (ct_k1_path == 2)."""
+        if self.exact_k1 or not hasattr(self, "w"):
+            return False
+        from ._lib import lib
+        nx, ny, nz = self.dims
+        return lib().ct_k1_path(self.code, nx, ny, nz, *self.r) == 2
+
     def cell(self, raw: torch.Tensor, frame: int = 0, id_start: int = 0) -> CellResult:
         nx, ny, nz = self.dims
         s = _dev.stream_handle()
