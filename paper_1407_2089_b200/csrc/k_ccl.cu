@@ -24,6 +24,7 @@
 //                 the ordered voxel list (segment.py:207-217) with a block
 //                 scan; thread 0 then forms the centroid by the row-sequential
 //                 float64 sum numpy's mean(axis=0) performs (segment.py:260).
+#include <algorithm>
 #include <cstdlib>
 
 #include "ct_common.cuh"
@@ -408,6 +409,7 @@ __global__ void tab_stats(const int32_t *__restrict__ labels, i64 ny, i64 nz, co
 }
 
 constexpr int RT = 512;    // tab_rank threads
+constexpr int RK = 4096;   // kept cells ordered by the multi-CTA path (tab_keep / tab_rank_keys / tab_emit)
 constexpr int RD = 16;     // radix digits (4 bits)
 
 __device__ __forceinline__ u64 sort_key(const TabWork &w, int c, u64 maxc, int rbits) {
@@ -444,6 +446,7 @@ __global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64
     __shared__ u64 sh[RT / 32 + 1];
     __shared__ u64 s_maxc;
     const int tid = threadIdx.x;
+    if (counters[CT_CNT_KEPT] <= RK) return;  // ordered by tab_rank_keys / tab_emit
     i64 nc = counters[CT_CNT_COMPONENTS];
     if (nc > cap) nc = cap;
     if (counters[CT_CNT_OVERFLOW]) nc = 0;
@@ -562,6 +565,83 @@ __global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64
         counters[CT_CNT_KEPT] = (int64_t)nk;
         counters[CT_CNT_KEPT_VOXELS] = (int64_t)total_vox;
     }
+}
+
+// Multi-CTA ordering for up to RK kept cells (the usual case); tab_rank
+// (single CTA, radix sort) takes over above that.
+
+__device__ __forceinline__ u64 order_key(const TabWork &w, int c) {  // (-count, root) ascending
+    return ((u64)(0x7fffffffu - w.count[c]) << 32) | (u64)(uint32_t)w.root[c];
+}
+
+// kept components (volume filter in float64, segment.py:253-255), any order
+__global__ void tab_keep(int64_t *counters, TabWork w, i64 cap, double vv, double min_volume) {
+    i64 nc = counters[CT_CNT_COMPONENTS];
+    if (nc > cap) nc = cap;
+    if (counters[CT_CNT_OVERFLOW]) nc = 0;
+    for (i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x; c < nc; c += (i64)gridDim.x * blockDim.x) {
+        w.rank[c] = -1;
+        const double vol = __dmul_rn((double)w.count[c], vv);
+        const bool keep = !(vol < min_volume);
+        const unsigned m = __ballot_sync(__activemask(), keep);
+        if (!keep) continue;
+        const unsigned lane = lane_id();
+        const int leader = __ffs(m) - 1;
+        unsigned long long base = 0;
+        if ((int)lane == leader) base = atomicAdd((unsigned long long *)&counters[CT_CNT_KEPT], (u64)__popc(m));
+        base = __shfl_sync(m, base, leader);
+        w.sa[base + __popc(m & ((1u << lane) - 1))] = (int32_t)c;
+    }
+}
+
+// rank of each kept cell = number of smaller keys (keys are unique); all keys in SMEM
+__global__ void __launch_bounds__(256) tab_rank_keys(const int64_t *__restrict__ counters, TabWork w) {
+    __shared__ u64 key[RK];
+    const i64 nk = counters[CT_CNT_KEPT];
+    if (nk > RK || (i64)blockIdx.x * 256 >= nk) return;
+    for (i64 e = threadIdx.x; e < nk; e += 256) key[e] = order_key(w, w.sa[e]);
+    __syncthreads();
+    const i64 e = (i64)blockIdx.x * 256 + threadIdx.x;
+    if (e >= nk) return;
+    const u64 k = key[e];
+    int r = 0;
+    for (int f = 0; f < (int)nk; ++f) r += key[f] < k;
+    w.sb[r] = w.sa[e];
+}
+
+// table rows in rank order, voxel offsets by an exclusive scan (one CTA)
+__global__ void __launch_bounds__(1024) tab_emit(int64_t *counters, TabWork w, double vv, i64 id_start,
+                                                 ct_cell *table) {
+    __shared__ u64 sh[1024 / 32 + 1];
+    const i64 nk = counters[CT_CNT_KEPT];
+    if (nk > RK) return;
+    const int tid = threadIdx.x;
+    const i64 chunk = (nk + 1023) / 1024;
+    const i64 e0 = min((i64)tid * chunk, nk), e1 = min(e0 + chunk, nk);
+    u64 vox = 0;
+    for (i64 e = e0; e < e1; ++e) vox += w.count[w.sb[e]];
+    u64 voff = vox;
+    const u64 total_vox = block_excl_scan(voff, sh);
+    for (i64 e = e0; e < e1; ++e) {
+        const int c = w.sb[e];
+        w.rank[c] = (int32_t)e;
+        ct_cell r;
+        r.id = id_start + e;
+        r.count = w.count[c];
+        r.root = w.root[c];
+        for (int a = 0; a < 3; ++a) {
+            r.bbox_lo[a] = w.bbox[6 * c + a];
+            r.bbox_hi[a] = w.bbox[6 * c + 3 + a];
+        }
+        r.intensity_sum = (int64_t)w.isum[c];
+        r.centroid_um[0] = r.centroid_um[1] = r.centroid_um[2] = 0.0;
+        r.volume_um3 = __dmul_rn((double)r.count, vv);
+        r.voxel_offset = (int64_t)voff;
+        r.reserved = 0;
+        table[e] = r;
+        voff += w.count[c];
+    }
+    if (tid == 0) counters[CT_CNT_KEPT_VOXELS] = (int64_t)total_vox;
 }
 
 __global__ void tab_relabel(int32_t *labels, const int32_t *__restrict__ fg, const int64_t *__restrict__ counters,
@@ -687,6 +767,10 @@ extern "C" int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz
         return CT_ERR_UNSUPPORTED;
     }
     if (int st = ct::check_launch("tab_stats")) return st;
+    cudaMemsetAsync(&counters[CT_CNT_KEPT], 0, sizeof(int64_t), s);
+    tab_keep<<<CT_NUM_SMS * 2, 256, 0, s>>>(counters, w, cap, vv, min_volume_um3);
+    tab_rank_keys<<<(unsigned)((std::min<i64>(cap, RK) + 255) / 256), 256, 0, s>>>(counters, w);
+    tab_emit<<<1, 1024, 0, s>>>(counters, w, vv, id_start, table);
     tab_rank<<<1, RT, 0, s>>>(counters, w, cap, N, vv, min_volume_um3, id_start, table);
     if (int st = ct::check_launch("tab_rank")) return st;
     tab_relabel<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters, w);
