@@ -75,6 +75,31 @@ __device__ __forceinline__ int find_g(volatile int32_t *L, int x) {
     return x;
 }
 
+// find with path halving (x's parent becomes its grandparent): parents only
+// ever move to ancestors, so concurrent unions (atomicMin on roots) stay valid
+__device__ __forceinline__ int find_gh(volatile int32_t *L, int x) {
+    int y = L[x];
+    while (y != x) {
+        const int z = L[y];
+        if (z != y) L[x] = z;
+        x = y;
+        y = z;
+    }
+    return x;
+}
+
+__device__ void union_gh(int32_t *L, int a, int b) {
+    for (;;) {
+        a = find_gh(L, a);
+        b = find_gh(L, b);
+        if (a == b) return;
+        if (a > b) { const int t = a; a = b; b = t; }
+        const int old = atomicMin(&L[b], a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
 __device__ void union_g(int32_t *L, int a, int b) {
     for (;;) {
         a = find_g(L, a);
@@ -270,7 +295,7 @@ __global__ void ccl_run_union(const uint8_t *__restrict__ mask, i64 nx, i64 ny, 
                     const unsigned long long below = ustart & (b == 63 ? ~0ull : ((2ull << b) - 1));
                     const int su = 63 - __clzll((long long)below);
                     o &= ~run_mask(u, su);
-                    union_g(labels, (int)(r * nz + s), (int)(nb[q] * nz + su));
+                    union_gh(labels, (int)(r * nz + s), (int)(nb[q] * nz + su));
                 }
             }
         }
