@@ -57,6 +57,18 @@ __device__ __forceinline__ bool env_past(int x, int q, double gq, int p, double 
     return __dadd_rn(gq, -gp) < __dmul_rn(__dmul_rn(d2, (double)(q - p)), (double)(2 * x - q - p));
 }
 
+// smallest x in [xlo, xhi) with env_past(x, q, gq, p, gp) (xhi if none).  The
+// predicate is monotone in x (its right side is a rounded increasing function
+// of x), so a float estimate corrected by exact tests gives the same answer
+// as testing every x in turn.
+__device__ __forceinline__ int first_past(int xlo, int xhi, int q, double gq, int p, double gp, double d2) {
+    const double xs = 0.5 * ((gq - gp) / (d2 * (double)(q - p)) + (double)(q + p));
+    int x = xs < (double)xlo ? xlo : (xs >= (double)xhi ? xhi : (int)xs + 1);
+    while (x > xlo && env_past(x - 1, q, gq, p, gp, d2)) --x;
+    while (x < xhi && !env_past(x, q, gq, p, gp, d2)) ++x;
+    return x;
+}
+
 // ---------------------------------------------------------------------------
 // pass x: nearest foreground along i (ties -> lower i), di = fi - i
 // ---------------------------------------------------------------------------
@@ -234,22 +246,27 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
             np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
         }
     }
-    for (int x = 0; x < ny; ++x) {
-        const i64 o = base + (i64)x * nz;
+    // sw = first x at which the envelope has moved past site cp
+    int sw = (K > 1) ? first_past(0, ny, np, ng, cp, cg, d2) : ny;
+    int32_t *o = out + base;
+    for (int x = 0; x < ny; ++x, o += nz) {
         int32_t r = NONE32;
         if (K) {
-            while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+            while (x >= sw) {
                 ++e;
                 cp = np; cpl = npl; cg = ng;
                 if (e + 1 < K) {
                     const uint32_t c1 = ent_ld(e + 1);
                     np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
+                    sw = first_past(x, ny, np, ng, cp, cg, d2);
+                } else {
+                    sw = ny;
                 }
             }
             r = pack(cp - x, cpl);
         }
         __syncwarp(wm);
-        out[o] = r;
+        *o = r;
     }
 #undef GOF
 }
@@ -411,11 +428,18 @@ __global__ void __launch_bounds__(ZL) edt_pass_zp(const int32_t *__restrict__ in
     int e = 0;
     int cp = st[0], np = K > 1 ? st[1] : 0;
     double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
+    int sw = K > 1 ? first_past(0, NZ, np, ng, cp, cg, d2) : NZ;  // envelope moves past cp at x = sw
     for (int x = 0; x < NZ; ++x) {
-        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+        while (x >= sw) {
             ++e;
             cp = np; cg = ng;
-            if (e + 1 < K) { np = st[e + 1]; ng = G(np); }
+            if (e + 1 < K) {
+                np = st[e + 1];
+                ng = G(np);
+                sw = first_past(x, NZ, np, ng, cp, cg, d2);
+            } else {
+                sw = NZ;
+            }
         }
         dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
     }
