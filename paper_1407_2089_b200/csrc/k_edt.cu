@@ -187,6 +187,66 @@ __global__ void __launch_bounds__(1024) edt_pass_x_seg(const uint8_t *__restrict
     }
 }
 
+// pass x for nx <= 1024 with 4 adjacent lines per thread (32-bit mask loads,
+// 64-bit stores): CTA = 4 XG lines x 32 segments of 32 rows.
+constexpr int XG = 8;
+__global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4(const uint8_t *__restrict__ mask, i64 nlines, int nx,
+                                                           int16_t *__restrict__ di) {
+    __shared__ int segL[32][4 * XG + 1], segF[32][4 * XG + 1];
+    const int c = threadIdx.x, y = threadIdx.y;  // c: 4-line group, y: segment
+    const i64 l0 = blockIdx.x * (4ll * XG) + 4 * c;
+    const bool valid = l0 < nlines;             // nlines % 4 == 0
+    const i64 S = nlines;
+    const int row0 = y * 32;
+    uint32_t bits[4] = {0, 0, 0, 0};
+    uint32_t v[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+        const int x = row0 + u;
+        v[u] = (valid && x < nx) ? __ldg((const uint32_t *)(mask + (i64)x * S + l0)) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bits[q] |= (((v[u] >> (8 * q)) & 0xffu) ? 1u : 0u) << u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        segL[y][4 * c + q] = bits[q] ? row0 + 31 - __clz(bits[q]) : -1;
+        segF[y][4 * c + q] = bits[q] ? row0 + __ffs(bits[q]) - 1 : -1;
+    }
+    __syncthreads();
+    if (!valid) return;
+    int lc[4], rc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        lc[q] = -1;
+        rc[q] = -1;
+        for (int yy = y - 1; yy >= 0; --yy)
+            if (segL[yy][4 * c + q] >= 0) { lc[q] = segL[yy][4 * c + q]; break; }
+        for (int yy = y + 1; yy < 32; ++yy)
+            if (segF[yy][4 * c + q] >= 0) { rc[q] = segF[yy][4 * c + q]; break; }
+    }
+#pragma unroll 4
+    for (int u = 0; u < 32; ++u) {
+        const int x = row0 + u;
+        if (x >= nx) break;
+        uint32_t packed[2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t b = bits[q];
+            const uint32_t lo = b & ((2u << u) - 1u), hi = b & ~((1u << u) - 1u);
+            const int lf = lo ? row0 + 31 - __clz(lo) : lc[q];
+            const int rf = hi ? row0 + __ffs(hi) - 1 : rc[q];
+            int best = lf;
+            if (rf >= 0 && (best < 0 || rf - x < x - best)) best = rf;
+            const uint32_t d = (uint16_t)(best < 0 ? NONE16 : (int16_t)(best - x));
+            if (q & 1) packed[q >> 1] |= d << 16;
+            else packed[q >> 1] = d;
+        }
+        *(uint2 *)(di + (i64)x * S + l0) = make_uint2(packed[0], packed[1]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di)
 // ---------------------------------------------------------------------------
@@ -523,7 +583,9 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     int32_t *pk = (int32_t *)((char *)work + (((size_t)N * 2 + 255) & ~(size_t)255));
     uint32_t *spill = (uint32_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
     const i64 lx = ny * nz, ly = nx * nz, lz = nx * ny;
-    if (nx <= 1024) {
+    if (nx <= 1024 && lx % 4 == 0 && ((uintptr_t)mask & 3) == 0 && ((uintptr_t)di & 7) == 0) {
+        edt_pass_x_seg4<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
+    } else if (nx <= 1024) {
         edt_pass_x_seg<1><<<(unsigned)((lx + 31) / 32), dim3(32, 32), 0, s>>>(mask, lx, (int)nx, di);
     } else if (nx <= 4096) {
         edt_pass_x_seg<4><<<(unsigned)((lx + 31) / 32), dim3(32, 32), 0, s>>>(mask, lx, (int)nx, di);
