@@ -677,6 +677,81 @@ __global__ void tab_relabel(int32_t *labels, const int32_t *__restrict__ fg, con
         labels[fg[e]] = over ? -1 : w.rank[w.comp[e]];
 }
 
+// One warp per kept cell: bbox scan in C order with ballots (no block
+// barriers); the centroid is the row-sequential float64 sum of numpy's
+// mean(axis=0), accumulated by lane 0 in list order via shuffles.
+constexpr int TVB = 8;  // chunks of 32 candidates in flight per warp
+__global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ labels, i64 ny, i64 nz,
+                                                    const int64_t *__restrict__ counters, ct_cell *table,
+                                                    int32_t *__restrict__ voxels, double dx, double dy, double dz) {
+    __shared__ double csm[8][32 * 3];
+    const unsigned lane = threadIdx.x & 31;
+    double *cs = csm[threadIdx.x >> 5];
+    const i64 nk = counters[CT_CNT_KEPT];
+    const i64 w0 = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 r = w0; r < nk; r += nw) {
+        const int lo0 = table[r].bbox_lo[0], lo1 = table[r].bbox_lo[1], lo2 = table[r].bbox_lo[2];
+        const int bi = table[r].bbox_hi[0] - lo0 + 1, bj = table[r].bbox_hi[1] - lo1 + 1,
+                  bk = table[r].bbox_hi[2] - lo2 + 1;
+        const i64 off = table[r].voxel_offset;
+        const i64 nbox = (i64)bi * bj * bk;
+        i64 written = 0;
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+        for (i64 q00 = 0; q00 < nbox; q00 += 32 * TVB) {
+            // labels of TVB chunks in flight, then ballots / list / sums in order
+            int32_t pv[TVB], lv[TVB];
+            int av[TVB], bv[TVB], cv[TVB];
+#pragma unroll
+            for (int u = 0; u < TVB; ++u) {
+                const i64 q = q00 + 32 * u + lane;
+                pv[u] = 0; lv[u] = -2; av[u] = bv[u] = cv[u] = 0;
+                if (q < nbox) {
+                    cv[u] = (int)(q % bk);
+                    const i64 t2 = q / bk;
+                    bv[u] = (int)(t2 % bj);
+                    av[u] = (int)(t2 / bj);
+                    pv[u] = (int32_t)(((i64)(lo0 + av[u]) * ny + (lo1 + bv[u])) * nz + (lo2 + cv[u]));
+                    lv[u] = __ldg(labels + pv[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < TVB; ++u) {
+                const bool hit = lv[u] == (int32_t)r;
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (hit) voxels[off + written + __popc(m & ((1u << lane) - 1))] = pv[u];
+                // hits' coordinates compacted in list order into the warp's SMEM
+                // slots, then lane 0 continues the row-sequential sum
+                const int nh = __popc(m);
+                if (hit) {
+                    double *slot = cs + 3 * __popc(m & ((1u << lane) - 1));
+                    slot[0] = __dmul_rn((double)(lo0 + av[u]), dx);
+                    slot[1] = __dmul_rn((double)(lo1 + bv[u]), dy);
+                    slot[2] = __dmul_rn((double)(lo2 + cv[u]), dz);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    int h0 = 0;
+                    if (written == 0 && nh) { sx = cs[0]; sy = cs[1]; sz = cs[2]; h0 = 1; }
+#pragma unroll 4
+                    for (int h = h0; h < nh; ++h) {
+                        sx = __dadd_rn(sx, cs[3 * h]);
+                        sy = __dadd_rn(sy, cs[3 * h + 1]);
+                        sz = __dadd_rn(sz, cs[3 * h + 2]);
+                    }
+                }
+                __syncwarp();
+                written += nh;
+            }
+        }
+        if (lane == 0) {
+            const double n = (double)table[r].count;
+            table[r].centroid_um[0] = __ddiv_rn(sx, n);
+            table[r].centroid_um[1] = __ddiv_rn(sy, n);
+            table[r].centroid_um[2] = __ddiv_rn(sz, n);
+        }
+    }
+}
+
 constexpr int VT = 256;
 
 __global__ void __launch_bounds__(VT) tab_voxels(const int32_t *__restrict__ labels, i64 ny, i64 nz,
@@ -800,6 +875,6 @@ extern "C" int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz
     if (int st = ct::check_launch("tab_rank")) return st;
     tab_relabel<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters, w);
     if (int st = ct::check_launch("tab_relabel")) return st;
-    tab_voxels<<<CT_NUM_SMS * 4, VT, 0, s>>>(labels, ny, nz, counters, table, voxels, dx, dy, dz);
+    tab_voxels_w<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, counters, table, voxels, dx, dy, dz);
     return ct::check_launch("tab_voxels");
 }
