@@ -24,6 +24,7 @@
 //               run through ct_mrf_step driven by the host.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "ct_common.cuh"
@@ -560,6 +561,126 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
     }
 }
 
+// u8 input, nz == NZ: 4 voxels per thread as one 32-bit word (SIMD byte
+// compares for the sign sum, packed 16-bit lanes for the Laplacian).  A CTA
+// owns MJ4 = 256 / (NZ/4) rows and walks MIPER planes along i with the same
+// 3-plane SMEM ring.  Edge neighbours are clamped exactly like the scalar
+// kernels (j, i by the clamped row/plane loads; k by byte replication).
+template <int NZ>
+__global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__ v, int nx, int ny,
+                                                     unsigned long long *__restrict__ ghist,
+                                                     unsigned long long *__restrict__ scal,
+                                                     int16_t *__restrict__ lap) {
+    constexpr int W = NZ / 4;               // words per row
+    constexpr int MJ4 = 256 / W;            // rows per CTA
+    constexpr int PW = (MJ4 + 2) * W;       // staged words per plane
+    constexpr int LW = (PW + 255) / 256;
+    __shared__ uint32_t ring[3][PW];
+    __shared__ uint32_t hsm[8 * 256];
+    uint32_t *wh = hsm + (threadIdx.x >> 5) * 256;
+    for (int b = threadIdx.x; b < 8 * 256; b += 256) hsm[b] = 0;
+    const int nJ = (ny + MJ4 - 1) / MJ4;
+    const int j0 = (blockIdx.x % nJ) * MJ4;
+    const int i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
+    const int my = ny - 2, mz = NZ - 2;
+    const int jj = threadIdx.x / W, kw = threadIdx.x % W, j = j0 + jj;
+    int goff[LW];
+#pragma unroll
+    for (int q = 0; q < LW; ++q) {
+        const int w = threadIdx.x + q * 256;
+        const int row = w / W, cw = w - row * W;
+        goff[q] = w < PW ? min(max(j0 - 1 + row, 0), ny - 1) * W + cw : 0;
+    }
+    const uint32_t *vw = (const uint32_t *)v;
+    const size_t plane_w = (size_t)ny * W;
+    auto load_plane = [&](int i, uint32_t (&regs)[LW]) {
+        const uint32_t *base = vw + (size_t)min(max(i, 0), nx - 1) * plane_w;
+#pragma unroll
+        for (int q = 0; q < LW; ++q)
+            if (threadIdx.x + q * 256 < PW) regs[q] = __ldg(base + goff[q]);
+    };
+    auto store_plane = [&](int slot, const uint32_t (&regs)[LW]) {
+#pragma unroll
+        for (int q = 0; q < LW; ++q)
+            if (threadIdx.x + q * 256 < PW) ring[slot][threadIdx.x + q * 256] = regs[q];
+    };
+    uint32_t regs[LW], regs2[LW];
+    load_plane(i0 - 1, regs);
+    store_plane(2, regs);
+    load_plane(i0, regs);
+    store_plane(0, regs);
+    load_plane(i0 + 1, regs);
+    store_plane(1, regs);
+    load_plane(i0 + 2, regs2);  // two planes ahead from here on
+    __syncthreads();
+    const int o = (jj + 1) * W + kw;
+    uint32_t xm = ring[2][o];
+    unsigned nnz = 0;
+    long long lsum = 0;
+    const bool jin = j < ny, jint = j > 0 && j < ny - 1;
+    int cs = 0, ns = 1, fs = 2;
+    for (int i = i0; i < i1; ++i) {
+        load_plane(i + 3, regs);  // planes i+2 (regs2) and i+3 (regs) in flight while plane i is processed
+        const uint32_t c = ring[cs][o], xp = ring[ns][o];
+        const uint32_t ym = ring[cs][o - W], yp = ring[cs][o + W];
+        const uint32_t wl = kw > 0 ? ring[cs][o - 1] : c << 24, wr = kw < W - 1 ? ring[cs][o + 1] : c >> 24;
+        const uint32_t zm = __funnelshift_l(wl, c, 8), zp = __funnelshift_r(c, wr, 8);
+        // sign sum != 0 per byte: #(+1 terms) != #(-1 terms)
+        const uint32_t one = 0x01010101u;
+        const uint32_t pos = (__vcmpgtu4(xm, c) & one) + (__vcmpgtu4(c, xp) & one) + (__vcmpgtu4(ym, c) & one) +
+                             (__vcmpgtu4(c, yp) & one) + (__vcmpgtu4(zm, c) & one) + (__vcmpgtu4(c, zp) & one);
+        const uint32_t neg = (__vcmpgtu4(c, xm) & one) + (__vcmpgtu4(xp, c) & one) + (__vcmpgtu4(c, ym) & one) +
+                             (__vcmpgtu4(yp, c) & one) + (__vcmpgtu4(c, zm) & one) + (__vcmpgtu4(zp, c) & one);
+        // Laplacian in 16-bit lanes: bytes 0, 2 (lo) and 1, 3 (hi)
+        const uint32_t m16 = 0x00ff00ffu;
+        const uint32_t sl = (xm & m16) + (xp & m16) + (ym & m16) + (yp & m16) + (zm & m16) + (zp & m16);
+        const uint32_t sh = ((xm >> 8) & m16) + ((xp >> 8) & m16) + ((ym >> 8) & m16) + ((yp >> 8) & m16) +
+                            ((zm >> 8) & m16) + ((zp >> 8) & m16);
+        const uint32_t ll = __vsub2(sl, (c & m16) * 6u), lh = __vsub2(sh, ((c >> 8) & m16) * 6u);
+        // voxel b's Laplacian: b0 = ll.lo, b1 = lh.lo, b2 = ll.hi, b3 = lh.hi
+        const uint32_t w01 = __byte_perm(ll, lh, 0x5410), w23 = __byte_perm(ll, lh, 0x7632);
+        const uint32_t nb0 = __shfl_down_sync(0xffffffffu, w01 & 0xffffu, 1);  // next word's b0
+        if (jin) {
+            nnz += __popc(__vcmpne4(pos, neg)) >> 3;
+            atomicAdd(&wh[c & 0xff], 1u);
+            atomicAdd(&wh[(c >> 8) & 0xff], 1u);
+            atomicAdd(&wh[(c >> 16) & 0xff], 1u);
+            atomicAdd(&wh[c >> 24], 1u);
+            if (jint && i > 0 && i < nx - 1) {
+                // elements k-1 for k = 4kw+1 .. 4kw+4 (two aligned 32-bit words)
+                const uint32_t e0 = __byte_perm(w01, w23, 0x5432), e1 = __byte_perm(w23, nb0, 0x5432);
+                uint32_t *dst = (uint32_t *)(lap + ((size_t)(i - 1) * my + (j - 1)) * mz + 4 * kw);
+                dst[0] = e0;
+                lsum += (int)(int16_t)(e0 & 0xffff) + (int)(int16_t)(e0 >> 16);
+                if (kw < W - 1) {
+                    dst[1] = e1;
+                    lsum += (int)(int16_t)(e1 & 0xffff) + (int)(int16_t)(e1 >> 16);
+                }
+            }
+        }
+        xm = c;
+        store_plane(fs, regs2);
+#pragma unroll
+        for (int q = 0; q < LW; ++q) regs2[q] = regs[q];
+        __syncthreads();
+        const int t = cs; cs = ns; ns = fs; fs = t;
+    }
+    unsigned long long nnz64 = nnz;
+    for (int q = 16; q; q >>= 1) {
+        nnz64 += __shfl_xor_sync(0xffffffffu, nnz64, q);
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, q);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&scal[W_NNZ], nnz64);
+        atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
+    }
+    __syncthreads();
+    unsigned tt = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tt += hsm[q * 256 + threadIdx.x];
+    if (tt) atomicAdd(&ghist[threadIdx.x], (unsigned long long)tt);
+}
+
 // float input: #{sign sum != 0} only (delta via sort; sums via the tree)
 template <typename T>
 __global__ void mrf_nnz_generic(const T *__restrict__ v, i64 nx, i64 ny, i64 nz, unsigned long long *__restrict__ nnz) {
@@ -725,7 +846,14 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
     using LT = typename std::conditional<sizeof(T) == 1, int16_t, int32_t>::type;
     LT *lap = (LT *)w.lap;
     const i64 blocks = ((ny + MJ - 1) / MJ) * ((nx + MIPER - 1) / MIPER);
-    if ((nz == 32 || nz == 64 || nz == 128) && ((uintptr_t)v & 3) == 0 && nx * ny * nz < (1ll << 31)) {
+    if (sizeof(T) == 1 && (nz == 32 || nz == 64 || nz == 128) && ((uintptr_t)v & 3) == 0 && ((uintptr_t)lap & 3) == 0 &&
+        nx * ny * nz < (1ll << 31) && getenv("CT_MRF_SCALAR") == nullptr) {
+        auto kern = nz == 32 ? mrf_stream_v4<32> : nz == 64 ? mrf_stream_v4<64> : mrf_stream_v4<128>;
+        const i64 b4 = ((ny + 256 / (nz / 4) - 1) / (256 / (nz / 4))) * ((nx + MIPER - 1) / MIPER);
+        kern<<<(unsigned)b4, 256, 0, s>>>((const uint8_t *)v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal,
+                                          (int16_t *)lap);
+        if (int st = ct::check_launch("mrf_stream_v4")) return st;
+    } else if ((nz == 32 || nz == 64 || nz == 128) && ((uintptr_t)v & 3) == 0 && nx * ny * nz < (1ll << 31)) {
         auto kern = nz == 32 ? mrf_stream_nz<T, LT, 32> : nz == 64 ? mrf_stream_nz<T, LT, 64> : mrf_stream_nz<T, LT, 128>;
         kern<<<(unsigned)blocks, 256, 0, s>>>(v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal, lap);
         if (int st = ct::check_launch("mrf_stream_nz")) return st;
