@@ -178,13 +178,13 @@ struct PwShape {
     int depth;                           // deepest level holding a leaf
 };
 
-__device__ int pw_lookup(const PwShape &sh, int d, int m) {
+__host__ __device__ inline int pw_lookup(const PwShape &sh, int d, int m) {
     for (int q = 0; q < sh.ns[d]; ++q)
         if (sh.size[d][q] == m) return sh.leaves[d][q];
     return 1;
 }
 
-__device__ void pw_shape(PwShape &sh, int m0) {
+__host__ __device__ inline void pw_shape(PwShape &sh, int m0) {
     sh.ns[0] = 1;
     sh.size[0][0] = m0;
     int d = 0;
@@ -212,24 +212,37 @@ __device__ void pw_shape(PwShape &sh, int m0) {
         }
 }
 
+// the distinct node sizes at depth D (a handful) with their shapes, tabulated
+// on the host and passed by value (param space)
+constexpr int PW_NSH = 4;
+struct PwShapes {
+    int count;
+    int len[PW_NSH];
+    PwShape sh[PW_NSH];
+};
+
 // CTA b: exact numpy-order sum of depth-D node b.  Elements are evaluated in
 // place by the leaf lanes (f(e) reads global memory); leaf t found by descending with the tabulated leaf counts; internal nodes
 // combined level by level (slot = path bits at that depth), so every add is
 // left + right exactly as numpy's recursion performs it.
 template <class F>
-__global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__restrict__ partial) {
-    __shared__ PwShape sh;
+__global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__restrict__ partial,
+                                                 const __grid_constant__ PwShapes shapes) {
+    __shared__ PwShape shs;
     __shared__ double lv[2][1 << PW_MAXD];  // values per level slot (ping-pong)
-    __shared__ int nleaves;
     __shared__ double lval[MAX_LEAVES];
     __shared__ int lpos[MAX_LEAVES];  // depth << 16 | slot
     i64 off, len;
     pw_node(n, D, blockIdx.x, off, len);
-    if (threadIdx.x == 0) {
-        pw_shape(sh, (int)len);
-        nleaves = sh.leaves[0][0];
+    int si = -1;
+    for (int q = 0; q < shapes.count; ++q)
+        if (shapes.len[q] == (int)len) si = q;
+    if (si < 0) {  // not tabulated: build it here
+        if (threadIdx.x == 0) pw_shape(shs, (int)len);
+        __syncthreads();
     }
-    __syncthreads();
+    const PwShape &sh = si >= 0 ? shapes.sh[si] : shs;
+    const int nleaves = sh.leaves[0][0];
     // leaves: 8 lanes per leaf; lane j accumulates numpy's r[j] (a[j], a[j+8],
     // ...), then the group combines ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by
     // shuffles and lane 0 adds the n % 8 tail -- numpy's leaf order exactly.
@@ -321,7 +334,34 @@ int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s
         ct::set_error("pairwise subtree too large");
         return CT_ERR_UNSUPPORTED;
     }
-    pw_subtree<F><<<(unsigned)(1ll << D), PT, 0, s>>>(f, n, D, partial);
+    // tabulate the shapes of the distinct node sizes at depth D
+    PwShapes shapes;
+    shapes.count = 0;
+    {
+        i64 sizes[64];
+        int ns = 1;
+        sizes[0] = n;
+        for (int d = 0; d < D; ++d) {
+            i64 nxt[64];
+            int nn = 0;
+            for (int i = 0; i < ns; ++i) {
+                const i64 l = pw_left(sizes[i]), c2[2] = {l, sizes[i] - l};
+                for (int q = 0; q < 2; ++q) {
+                    bool seen = false;
+                    for (int u = 0; u < nn; ++u) seen |= nxt[u] == c2[q];
+                    if (!seen && nn < 64) nxt[nn++] = c2[q];
+                }
+            }
+            ns = nn;
+            for (int i = 0; i < ns; ++i) sizes[i] = nxt[i];
+        }
+        for (int i = 0; i < ns && shapes.count < PW_NSH; ++i) {
+            shapes.len[shapes.count] = (int)sizes[i];
+            pw_shape(shapes.sh[shapes.count], (int)sizes[i]);
+            ++shapes.count;
+        }
+    }
+    pw_subtree<F><<<(unsigned)(1ll << D), PT, 0, s>>>(f, n, D, partial, shapes);
     if (int st = ct::check_launch("pw_subtree")) return st;
     pw_fold<<<1, 1024, 0, s>>>(partial, D, out);
     return ct::check_launch("pw_fold");
