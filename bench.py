@@ -385,24 +385,26 @@ def run_e2e(args, pipe, spec, sp, dev, world, s_cell, s_vess):
             for _ in range(2)]
     rows = 4096
     out_host = torch.empty(rows * 128 + 64 + 72 + 32, dtype=torch.uint8, pin_memory=True)
-    s_copy = torch.cuda.Stream(dev)
-    copied = [torch.cuda.Event() for _ in range(2)]
+    # one copy stream per channel (two DMA engines share the PCIe link)
+    s_copy = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    copied = [[torch.cuda.Event(), torch.cuda.Event()] for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]
     for d in done:
         d.record()
 
     def h2d(i):
         slot = i % 2
-        with torch.cuda.stream(s_copy):
-            s_copy.wait_event(done[slot])
-            dbuf[slot][0].copy_(host[i % nring][0], non_blocking=True)
-            dbuf[slot][1].copy_(host[i % nring][1], non_blocking=True)
-            copied[slot].record()
+        for ch in range(2):
+            with torch.cuda.stream(s_copy[ch]):
+                s_copy[ch].wait_event(done[slot])
+                dbuf[slot][ch].copy_(host[i % nring][ch], non_blocking=True)
+                copied[slot][ch].record()
 
     def compute(i):
         slot = i % 2
         main = torch.cuda.current_stream()
-        main.wait_event(copied[slot])
+        main.wait_event(copied[slot][0])
+        main.wait_event(copied[slot][1])
         s_cell.wait_stream(main)
         s_vess.wait_stream(main)
         with torch.cuda.stream(s_cell):
