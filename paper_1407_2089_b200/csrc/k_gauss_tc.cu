@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     }
     const long long eps = prm->eps;
     const int zs = prm->fw[2] + 8;  // S has scale 2^zs
-    const long long half = 1ll << (zs - 1), fmask = (1ll << zs) - 1;
+    const long long half = 1ll << (zs - 1), one = 1ll << zs, fmask = one - 1;
     const uint32_t base = tbase;
     const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
     const long long ntiles = (nlines + TM - 1) / TM;
@@ -467,28 +467,20 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         if (l < nlines) {
 #pragma unroll
             for (int c = 0; c < CW; ++c) {
-                long long S = 0;
-#pragma unroll
-                for (int acc = 0; acc < 5; ++acc) S += (long long)v[acc][c] << (8 * acc);
-                {   // edge taps: floor((x0 E0 + xl EL) / 2^16), split to stay in 64 bits
-                    const uint4 e = Et[h0 + c];
-                    const unsigned long long hi = (unsigned long long)x0 * e.x + (unsigned long long)xl * e.z;
-                    const unsigned long long lo = (unsigned long long)x0 * e.y + (unsigned long long)xl * e.w;
-                    S += (long long)(hi + (lo >> 16));
-                }
-                const long long R = ((long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) - S;
-                // q = rint(max(R, 0) / 2^zs); certified unless R is within eps
-                // of a rounding boundary (k + 1/2) 2^zs
-                uint32_t qv = 0;
-                long long dist;
-                if (R > 0) {
-                    qv = (uint32_t)((R + half) >> zs);
-                    dist = (R & fmask) - half;
-                    dist = dist < 0 ? -dist : dist;
-                } else {
-                    dist = half - R;
-                }
-                if (dist <= eps) {
+                // S = sum_acc v[acc] 2^(8 acc) (IMAD.WIDE chain) + edge taps
+                const uint4 e = Et[h0 + c];
+                const unsigned long long lo = (unsigned long long)x0 * e.y + (unsigned long long)xl * e.w;
+                unsigned long long S = (unsigned long long)v[0][c] + (unsigned long long)v[1][c] * 0x100ull +
+                                       (unsigned long long)v[2][c] * 0x10000ull +
+                                       (unsigned long long)v[3][c] * 0x1000000ull + ((unsigned long long)v[4][c] << 32);
+                S += (unsigned long long)x0 * e.x + (unsigned long long)xl * e.z + (lo >> 16);
+                // T = R + 2^(zs-1), R = raw 2^zs - S: q = max(T, 0) >> zs; the
+                // rounding boundaries R = (k + 1/2) 2^zs (k >= 0) are T = (k+1) 2^zs,
+                // flagged when T is within eps of one of them
+                const long long T = (long long)(((unsigned long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) -
+                                                S) + half;
+                const uint32_t qv = T > 0 ? (uint32_t)(T >> zs) : 0u;
+                if (T >= one - eps && ((T + eps) & fmask) <= 2 * eps) {
                     const unsigned long long at = atomicAdd(&fix[0], 1ull);
                     if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
                     else fix[1] = 1;
