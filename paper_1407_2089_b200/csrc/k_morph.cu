@@ -154,6 +154,35 @@ __global__ void __launch_bounds__(256) pack_rows(const T *__restrict__ in, i64 n
     }
 }
 
+// u8, nz == 64: one thread per row, 4 x 16-byte loads, SIMD byte compares
+__global__ void __launch_bounds__(256) pack_rows_u8x64(const uint8_t *__restrict__ in, i64 nrows,
+                                                       const int64_t *__restrict__ otsu, i64 t_host,
+                                                       u64 *__restrict__ rows) {
+    bool empty;
+    const i64 t = threshold_of(otsu, t_host, empty);
+    // above(v, t) = v > t for integers: all bytes if t < 0, none if t >= 255 or empty
+    const bool all = !empty && t < 0, none = empty || t >= 255;
+    const uint32_t tb = (uint32_t)(all || none ? 0 : t) * 0x01010101u;
+    for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
+        u64 w = 0;
+        if (all) w = ~0ull;
+        else if (!none) {
+            const uint4 *src = (const uint4 *)(in + r * 64);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 v = __ldg(src + c);
+                const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t g = __vcmpgtu4(x[q], tb) & 0x80808080u;  // high bit per byte
+                    w |= (u64)(((g >> 7) * 0x10204080u) >> 28) << (16 * c + 4 * q);
+                }
+            }
+        }
+        rows[r] = w;
+    }
+}
+
 __device__ __forceinline__ u64 rowM(const u64 *rows, i64 i, i64 j, i64 nx, i64 ny) {
     return (i >= 0 && i < nx && j >= 0 && j < ny) ? rows[i * ny + j] : 0ull;
 }
@@ -194,10 +223,19 @@ __global__ void __launch_bounds__(256) close1_bits(const u64 *__restrict__ rows,
         if (out) {
             // bits -> bytes via SMEM, then a coalesced copy of the warp's 32 rows
             uint8_t *st = stage[wid];
-            for (int k = 0; k < nz; k += 4) {
-                const unsigned nib = (unsigned)((e >> k) & 0xF);
-                const uint32_t bytes = ((nib * 0x00204081u) & 0x01010101u);
-                *reinterpret_cast<uint32_t *>(st + lane * nz + k) = bytes;  // nz % 4 == 0 guaranteed by caller
+            if (nz % 16 == 0) {  // 16-byte SMEM stores (a plain 4-byte loop is 16-way bank conflicted)
+                for (int k = 0; k < nz; k += 16) {
+                    uint32_t b4[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) b4[q] = ((unsigned)((e >> (k + 4 * q)) & 0xF) * 0x00204081u) & 0x01010101u;
+                    *reinterpret_cast<uint4 *>(st + lane * nz + k) = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+                }
+            } else {
+                for (int k = 0; k < nz; k += 4) {
+                    const unsigned nib = (unsigned)((e >> k) & 0xF);
+                    const uint32_t bytes = ((nib * 0x00204081u) & 0x01010101u);
+                    *reinterpret_cast<uint32_t *>(st + lane * nz + k) = bytes;  // nz % 4 == 0 guaranteed by caller
+                }
             }
             __syncwarp();
             const int nr = (int)min((i64)32, nrows - r0);
@@ -224,7 +262,12 @@ int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i6
     if (r == 1 && nz <= 64 && nz % 4 == 0 && work && ((uintptr_t)out & 15) == 0) {
         u64 *rows = (u64 *)work;
         const i64 nrows = nx * ny;
-        pack_rows<T><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(in, nrows, (int)nz, otsu, t_host, rows);
+        if (sizeof(T) == 1 && nz == 64 && ((uintptr_t)in & 15) == 0)
+            pack_rows_u8x64<<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>((const uint8_t *)in, nrows, otsu,
+                                                                                      t_host, rows);
+        else
+            pack_rows<T><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(in, nrows, (int)nz, otsu, t_host,
+                                                                                   rows);
         if (int st = ct::check_launch("pack_rows")) return st;
         close1_bits<<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(rows, nx, ny, (int)nz, out, nullptr);
         return ct::check_launch("close1_bits");
