@@ -16,7 +16,6 @@
 
 namespace {
 
-constexpr int NT = 1024;
 
 struct U384 {
     u64 w[6];
@@ -82,13 +81,15 @@ __device__ void merge(Cand &x, const Cand &y) {
     else if (!better(x, y) && y.t < x.t) x = y;
 }
 
+template <int NT>  // threads (256 when the caller fixes 256 bins, else 1024)
 __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ hist, i64 nbins_given,
                                                   i64 *__restrict__ result) {
+    constexpr int NW = NT / 32;
     __shared__ u64 s_w[NT], s_s[NT];
-    __shared__ double s_best[32];
-    __shared__ i64 s_cnt[32];
+    __shared__ double s_best[NW];
+    __shared__ i64 s_cnt[NW];
     __shared__ int s_hi;
-    __shared__ Cand s_c[32];
+    __shared__ Cand s_c[NW];
     const int tid = threadIdx.x;
     if (tid == 0) s_hi = 0;
     __syncthreads();
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     const u64 W = s_w[NT - 1], S = s_s[NT - 1];
     const u64 pre_w = tid ? s_w[tid - 1] : 0, pre_s = tid ? s_s[tid - 1] : 0;
     i64 nonzero = 0;
-    for (int i = 0; i < 32; ++i) nonzero += s_cnt[i];
+    for (int i = 0; i < NW; ++i) nonzero += s_cnt[i];
     if (nonzero < 2 || nb < 2) {
         if (tid == 0) {
             result[CT_OTSU_T] = 0;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     if ((tid & 31) == 0) s_best[tid >> 5] = best;
     __syncthreads();
     best = s_best[0];
-    for (int i = 1; i < 32; ++i) best = fmax(best, s_best[i]);
+    for (int i = 1; i < NW; ++i) best = fmax(best, s_best[i]);
     const double cut = __dmul_rn(best, 1.0 - 1e-9);
     // pass B: candidates, exact comparison
     Cand mine;
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     __syncthreads();
     if (tid == 0) {
         Cand r = s_c[0];
-        for (int i = 1; i < 32; ++i) merge(r, s_c[i]);
+        for (int i = 1; i < NW; ++i) merge(r, s_c[i]);
         result[CT_OTSU_T] = r.t < 0 ? 0 : r.t;
         result[CT_OTSU_STATUS] = 0;
         result[CT_OTSU_NBINS] = nb;
@@ -227,6 +228,7 @@ extern "C" int ct_otsu(const uint64_t *hist, int64_t nbins, int64_t *result, voi
         ct::set_error("otsu supports at most 65536 bins (got %lld)", (long long)nbins);
         return CT_ERR_UNSUPPORTED;
     }
-    otsu_kernel<<<1, NT, 0, (cudaStream_t)stream>>>(hist, nbins, result);
+    if (nbins > 0 && nbins <= 256) otsu_kernel<256><<<1, 256, 0, (cudaStream_t)stream>>>(hist, nbins, result);
+    else otsu_kernel<1024><<<1, 1024, 0, (cudaStream_t)stream>>>(hist, nbins, result);
     return ct::check_launch("otsu");
 }
