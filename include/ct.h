@@ -173,6 +173,15 @@ int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz, const int
                   double dz, double min_volume_um3, int64_t id_start, int64_t cap, void *work,
                   ct_cell *table, int32_t *voxels, void *stream);
 
+/* Results on-disk format -- ref segment.py:321-337
+ * encode_voxel_runs per detection (session.py:668): z-runs [i, j, k0, length]
+ * of every kept cell's C-order voxel list from ct_cell_table.  runs: int32
+ * [4 * cap_runs]; run_offset: int64[CT kept cells + 1] (cell r's runs are
+ * [run_offset[r], run_offset[r+1])); nruns: int64[2] = total runs, overflow
+ * (runs not written when the total exceeds cap_runs). */
+int ct_voxel_runs(const int32_t *voxels, const ct_cell *table, const int64_t *counters, int64_t ny, int64_t nz,
+                  int64_t cap_runs, int32_t *runs, int64_t *run_offset, int64_t *nruns, void *stream);
+
 /* K7 -- ref denoise.py:92-195 (MRF vessel denoise).  Computes on device,
  * without synchronising: delta = intensity_step (denoise.py:135-144),
  * sigma_hat = estimate_noise_variance (denoise.py:92-114, numpy pairwise

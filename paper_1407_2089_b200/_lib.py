@@ -60,6 +60,7 @@ SIGNATURES = {
     "ct_gaussian_residual": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _P, _INT, _P]),
     "ct_gaussian_q": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _I64, _D, _P]),
     "ct_set_k1_path": (_INT, [_INT]),
+    "ct_voxel_runs": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P]),
     "ct_k1_path": (_INT, [_INT, _I64, _I64, _I64, _INT, _INT, _INT]),
     "ct_to_f64": (_INT, [_P, _INT, _I64, _P, _P]),
     "ct_median": (_INT, [_P, _INT, _I64, _I64, _I64, _INT, _P, _P, _P]),
@@ -113,7 +114,7 @@ def exported_symbols() -> list[str]:
 # bench's gpu_launches count
 LAUNCHES = {
     "ct_gaussian_residual": 3, "ct_gaussian_q": 7, "ct_to_f64": 1, "ct_median": 1, "ct_histogram": 1, "ct_otsu": 1,
-    "ct_threshold_close": 2, "ct_closing": 2, "ct_ccl26": 4, "ct_cell_table": 8, "ct_mrf": 5,
+    "ct_threshold_close": 2, "ct_closing": 2, "ct_ccl26": 4, "ct_cell_table": 8, "ct_voxel_runs": 3, "ct_mrf": 5,
     "ct_mrf_step": 4, "ct_sign_sum": 1, "ct_edt": 3, "ct_synth_frame": 3,
 }
 launch_counter = {"enabled": False, "count": 0}

@@ -385,6 +385,28 @@ def encode_voxel_runs(voxels: np.ndarray) -> list[list[int]]:
     return [[int(a), int(b), int(c), int(n)] for (a, b, c), n in zip(v[starts], lengths)]
 
 
+def cell_runs(ct: CellTable, dims, cap_runs: int | None = None):
+    """encode_voxel_runs of every kept cell of a device CellTable, computed on
+    the GPU (ct_voxel_runs): returns (runs int32 (R, 4) = [i, j, k0, length],
+    offsets int64 (ncells + 1)); cell r's runs are runs[offsets[r]:offsets[r+1]],
+    identical to encode_voxel_runs(detections[r].voxels)."""
+    _, ny, nz = (int(d) for d in dims)
+    cnt = ct.counters.cpu().numpy()
+    nk = int(cnt[CNT_KEPT])
+    nv = int(cnt[CNT_KEPT_VOXELS])
+    cap = int(cap_runs if cap_runs is not None else max(nv, 1))
+    dev = ct.voxels.device
+    runs = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+    offs = torch.empty(nk + 1, dtype=torch.int64, device=dev)
+    nr = torch.zeros(2, dtype=torch.int64, device=dev)
+    call("ct_voxel_runs", ct.voxels.data_ptr(), ct.table.data_ptr(), ct.counters.data_ptr(), ny, nz, cap,
+         runs.data_ptr(), offs.data_ptr(), nr.data_ptr(), _dev.stream_handle())
+    n_runs, over = (int(x) for x in nr.cpu())
+    if over:
+        raise RuntimeError(f"{n_runs} runs exceed cap_runs={cap}")
+    return runs[:n_runs].cpu().numpy(), offs.cpu().numpy()
+
+
 def decode_voxel_runs(runs: list[list[int]]) -> np.ndarray:
     """Inverse of encode_voxel_runs."""
     if not runs:

@@ -344,3 +344,52 @@ def test_certified_fixup_recomputes_exactly(cuda):
     # overflow is reported when the list is too small
     _, _, fx = _q_exact_and_fast(v, ANISO, 3.0, eps=0.6, cap=10)
     assert fx[1] == 1
+
+
+def _ref_encode_runs(voxels):
+    """The reference's per-voxel loop (ref segment.py:321-337), restated."""
+    if voxels.shape[0] == 0:
+        return []
+    v = voxels[np.lexsort((voxels[:, 2], voxels[:, 1], voxels[:, 0]))]
+    runs, start, n = [], v[0], 1
+    for prev, cur in zip(v[:-1], v[1:]):
+        if cur[0] == prev[0] and cur[1] == prev[1] and cur[2] == prev[2] + 1:
+            n += 1
+        else:
+            runs.append([int(start[0]), int(start[1]), int(start[2]), n])
+            start, n = cur, 1
+    runs.append([int(start[0]), int(start[1]), int(start[2]), n])
+    return runs
+
+
+@pytest.mark.parametrize("case", PIPELINE_CASES)
+def test_gpu_voxel_runs_match_encode_voxel_runs(cuda, case):
+    """ct_voxel_runs == encode_voxel_runs(det.voxels) per detection."""
+    g = golden(f"pipeline_{case}.npz")
+    spec = spec_of(case, g)
+    pipe = FramePipeline(spec.dims, spec.dtype, ANISO, D.CellDenoiseParams(float(g["sigma_um"])))
+    for t in range(2):
+        res = pipe.cell(synth.generate(spec, t, synth.CELL), frame=t)
+        dets = pipe.finish_cell(res, materialize=True)
+        runs, offs = S.cell_runs(res.cells, spec.dims)
+        assert offs.shape[0] == len(dets) + 1 and offs[-1] == runs.shape[0]
+        for r, d in enumerate(dets):
+            assert runs[offs[r]:offs[r + 1]].tolist() == _ref_encode_runs(d.voxels)
+            assert S.encode_voxel_runs(d.voxels) == runs[offs[r]:offs[r + 1]].tolist()
+
+
+def test_gpu_voxel_runs_c2_properties(cuda):
+    """Full C2 frame: runs decode to exactly the C-order voxel lists."""
+    spec = synth.C2
+    pipe = FramePipeline(spec.dims, spec.dtype, ANISO)
+    res = pipe.cell(synth.generate(spec, 0, synth.CELL))
+    cnt, rows = pipe.finish_cell(res)
+    runs, offs = S.cell_runs(res.cells, spec.dims)
+    vox = pipe.voxels[: int(rows["count"].sum())].cpu().numpy().astype(np.int64)
+    nx, ny, nz = spec.dims
+    for r in range(0, len(rows), 97):
+        o, c = int(rows[r]["voxel_offset"]), int(rows[r]["count"])
+        lin = vox[o:o + c]
+        dec = S.decode_voxel_runs(runs[offs[r]:offs[r + 1]].tolist())
+        np.testing.assert_array_equal(dec, np.stack([lin // (ny * nz), (lin // nz) % ny, lin % nz], axis=1))
+    assert runs[:, 3].sum() == vox.shape[0]
