@@ -33,7 +33,8 @@ namespace {
 constexpr int FW = 40;         // max weight scale bits (lowered per axis so that every Q_j < 2^32)
 constexpr int FD = 24;         // fractional bits of the intermediates
 constexpr int TM = 128;        // output rows per tile (passes x, y) / lines per tile (pass z)
-constexpr int TN = 32;         // columns per tile (passes x, y)
+constexpr int TNX = 64;        // columns per tile, pass x (4 accumulators: 256 + 4*64 TMEM columns)
+constexpr int TNY = 32;        // columns per tile, pass y (5 accumulators: 256 + 5*32)
 constexpr int KXY = 256;       // input rows per tile (passes x, y): TM + 2r <= 256
 constexpr int NT = 512;        // threads per CTA: 16 warps = 4 TMEM sub-partitions x 4 column groups
 constexpr int PMAX = 65;       // max taps per side + 1
@@ -120,14 +121,16 @@ __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, u
 // 8b; output S >> 11) or 4 (byte planes of P1; pairs a+b >= 2, accumulator
 // a+b-2, shift 8(a+b-2); output S >> 19).  Volume viewed as [outer][L][inner].
 // ---------------------------------------------------------------------------
-template <int NPIN, int STAGES>
+template <int NPIN, int STAGES, int TN>  // TN: columns per tile (32 or 64)
 __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ in, long long plane_in, int L,
                                                      int inner, int outer, const TcParams *__restrict__ prm, int axis,
                                                      int r, uint8_t *__restrict__ out, long long plane_out) {
     constexpr int NACC = NPIN == 1 ? 4 : 5;
     constexpr uint32_t LBO = (TN / 16) * 128, SBO = 128;                // MN-major B
     constexpr int BUF = KXY * TN;                                       // bytes per plane per buffer
-    constexpr int OROW = 48;                                            // padded output row (bytes)
+    constexpr int OROW = TN + 16;                                       // padded output row (bytes)
+    constexpr int CPR = TN / 16;                                        // 16-byte chunks per row
+    constexpr int CW = TN / 4;                                          // columns per thread (epilogue)
     constexpr int OBUF = 4 * TM * OROW;                                 // output tile: [4 planes][128 rows]
     extern __shared__ __align__(1024) uint8_t sm[];                     // [STAGES][NPIN][BUF], [2][OBUF]
     uint8_t *sout = sm + STAGES * NPIN * BUF;
@@ -185,8 +188,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         int o, ti, cb;
         tile_coords(tile, o, ti, cb);
 #pragma unroll
-        for (int q2 = 0; q2 < 4 * TM * 2 / NT; ++q2) {
-            const int e = t + NT * q2, a = e / (2 * TM), mm = (e >> 1) & (TM - 1), hh = e & 1;
+        for (int q2 = 0; q2 < 4 * TM * CPR / NT; ++q2) {
+            const int e = t + NT * q2, a = e / (CPR * TM), mm = (e / CPR) & (TM - 1), hh = e % CPR;
             const int i = ti * TM + mm;
             if (i < L)
                 *(uint4 *)(out + a * plane_out + ((long long)o * L + i) * inner + (long long)cb * TN + 16 * hh) =
@@ -201,8 +204,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
 #pragma unroll
         for (int p = 0; p < NPIN; ++p)
 #pragma unroll
-            for (int q = 0; q < 2 * KXY / NT; ++q) {
-                const int e = t + NT * q, kk = e >> 1, g = e & 1;
+            for (int q = 0; q < CPR * KXY / NT; ++q) {
+                const int e = t + NT * q, kk = e / CPR, g = e % CPR;
                 const int ii = min(max(i0 - r + kk, 0), L - 1);
                 tc::cp_async16(sm + (buf * NPIN + p) * BUF + tc::mnmajor_off(kk, 16 * g, LBO, SBO),
                                in + p * plane_in + ((long long)o * L + ii) * inner + (long long)cb * TN + 16 * g);
@@ -256,14 +259,17 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         issue(0);
     }
     uint32_t phase = 0;
-    const int h = 8 * cg;
+    const int h = CW * cg;
     for (long long k = 0; k < nmine; ++k) {
         tc::mbar_wait(&mbar, phase);
         phase ^= 1;
         tc::fence_after();
-        uint32_t v[NACC][8];
+        uint32_t v[NACC][CW];
 #pragma unroll
-        for (int acc = 0; acc < NACC; ++acc) tc::tmem_ld8(lane_addr + 256 + TN * acc + h, v[acc]);
+        for (int acc = 0; acc < NACC; ++acc)
+#pragma unroll
+            for (int g8 = 0; g8 < CW; g8 += 8)
+                tc::tmem_ld8(lane_addr + 256 + TN * acc + h + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
         tc::tmem_ld_wait();
         tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
         tc::fence_async_smem();
@@ -274,21 +280,24 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
         else tc::cp_commit();
         if (k > 0) flush(t0 + (k - 1) * gs, sout + (int)((k - 1) & 1) * OBUF);
-        // epilogue of tile k: row m, columns [8 cg, 8 cg + 8) -> staged output
-        uint32_t ov[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            long long S = 0;
-#pragma unroll
-            for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][c] << (8 * acc);
-            ov[c] = (uint32_t)(S >> shift_out);
-        }
-        uint32_t lo[4], hi[4];
-        planes4(ov[0], ov[1], ov[2], ov[3], lo);
-        planes4(ov[4], ov[5], ov[6], ov[7], hi);
+        // epilogue of tile k: row m, columns [h, h + CW) -> staged output
         uint8_t *ob = sout + (int)(k & 1) * OBUF;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) *(uint2 *)(ob + (a * TM + m) * OROW + h) = make_uint2(lo[a], hi[a]);
+        for (int g8 = 0; g8 < CW; g8 += 8) {
+            uint32_t ov[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                long long S = 0;
+#pragma unroll
+                for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][g8 + c] << (8 * acc);
+                ov[c] = (uint32_t)(S >> shift_out);
+            }
+            uint32_t lo[4], hi[4];
+            planes4(ov[0], ov[1], ov[2], ov[3], lo);
+            planes4(ov[4], ov[5], ov[6], ov[7], hi);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) *(uint2 *)(ob + (a * TM + m) * OROW + h + g8) = make_uint2(lo[a], hi[a]);
+        }
     }
     __syncthreads();
     if (nmine > 0) flush(t0 + (nmine - 1) * gs, sout + (int)((nmine - 1) & 1) * OBUF);
@@ -507,7 +516,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
 // (byte planes of P1 and P2) + sizeof(TcParams).
 bool ct_gaussian_q_tc_fits(int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz) {
     return (nz == 32 || nz == 64) && rx >= 0 && ry >= 0 && rz >= 0 && rx <= (KXY - TM) / 2 && ry <= (KXY - TM) / 2 &&
-           rz < PMAX && (ny * nz) % TN == 0 && nx * ny * nz < (1ll << 31);
+           rz < PMAX && (ny * nz) % TNX == 0 && nz % TNY == 0 && nx * ny * nz < (1ll << 31);
 }
 
 int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry, int rz,
@@ -522,19 +531,19 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     if (int st = ct::check_launch("tc_prep")) return st;
     // pass x: [1][nx][ny*nz]
     {
-        const size_t sm = 8 * 1 * KXY * TN + 2 * 4 * TM * 48 + 1024;
-        cudaFuncSetAttribute(tc_pass_xy<1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TN);
-        tc_pass_xy<1, 8><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
+        const size_t sm = 6 * 1 * KXY * TNX + 2 * 4 * TM * (TNX + 16) + 1024;
+        cudaFuncSetAttribute(tc_pass_xy<1, 6, TNX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TNX);
+        tc_pass_xy<1, 6, TNX><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
             raw, 0, (int)nx, (int)(ny * nz), 1, prm, 0, rx, p1, N);
         if (int st = ct::check_launch("tc_pass_x")) return st;
     }
     // pass y: [nx][ny][nz]
     {
-        const size_t sm = 5 * 4 * KXY * TN + 2 * 4 * TM * 48 + 1024;
-        cudaFuncSetAttribute(tc_pass_xy<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TN);
-        tc_pass_xy<4, 5><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
+        const size_t sm = 5 * 4 * KXY * TNY + 2 * 4 * TM * (TNY + 16) + 1024;
+        cudaFuncSetAttribute(tc_pass_xy<4, 5, TNY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TNY);
+        tc_pass_xy<4, 5, TNY><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
             p1, N, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2, N);
         if (int st = ct::check_launch("tc_pass_y")) return st;
     }
