@@ -35,6 +35,7 @@ constexpr int SC = 48;   // SMEM stack entries per thread (pass y)
 constexpr int LT = 256;  // threads per pass-x / pass-y CTA
 constexpr int PF = 16;   // prefetch depth (positions)
 constexpr int ZL = 128;  // lines per pass-z CTA
+constexpr int YSEG = 1;  // pass-y output segments per line (2 measured slower: the build dominates)
 
 __device__ __forceinline__ double sq(double x) { return __dmul_rn(x, x); }
 
@@ -250,10 +251,16 @@ __global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4(const uint8_t *__rest
 // ---------------------------------------------------------------------------
 // pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di)
 // ---------------------------------------------------------------------------
+// blockIdx.y = output segment: every segment's threads build the line's whole
+// envelope (cheap: sites are sparse after pass x) and emit only their part of
+// the line, which multiplies the parallelism of the long output walk.
 __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di, i64 nlines, int ny, int nz, double dx,
                                                  double dy, int32_t *__restrict__ out, uint32_t *__restrict__ spill) {
     __shared__ uint32_t stk[SC][LT];  // entry = (position << 16) | payload (di as uint16)
     const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
+    const int nseg = gridDim.y, seg = blockIdx.y;
+    const int xs0 = (int)((i64)ny * seg / nseg), xs1 = (int)((i64)ny * (seg + 1) / nseg);
+    spill += (size_t)seg * nlines * (ny > SC ? ny - SC : 0);  // private spill stacks per segment
     // lanes run data-dependent envelope loops; reconverge (wm) before every
     // batched load and every store so the warp's accesses stay coalesced
     const unsigned wm = __ballot_sync(0xffffffffu, l < nlines);
@@ -308,8 +315,8 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
     }
     // sw = first x at which the envelope has moved past site cp
     int sw = (K > 1) ? first_past(0, ny, np, ng, cp, cg, d2) : ny;
-    int32_t *o = out + base;
-    for (int x = 0; x < ny; ++x, o += nz) {
+    int32_t *o = out + base + (i64)xs0 * nz;
+    for (int x = xs0; x < xs1; ++x, o += nz) {
         int32_t r = NONE32;
         if (K) {
             while (x >= sw) {
@@ -563,7 +570,7 @@ inline size_t zsmem(int nz) {
 
 size_t ct_edt_workspace(int64_t nx, int64_t ny, int64_t nz) {
     const i64 N = nx * ny * nz;
-    const i64 sp = nx * nz * (ny > SC ? ny - SC : 0);  // pass-y spill entries
+    const i64 sp = YSEG * nx * nz * (ny > SC ? ny - SC : 0);  // pass-y spill entries (per segment)
     return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 4 + 4096;
 }
 
@@ -593,7 +600,7 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
     }
     if (int st = ct::check_launch("edt_pass_x")) return st;
-    edt_pass_y<<<(unsigned)((ly + LT - 1) / LT), LT, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, pk, spill);
+    edt_pass_y<<<dim3((unsigned)((ly + LT - 1) / LT), YSEG), LT, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, pk, spill);
     if (int st = ct::check_launch("edt_pass_y")) return st;
     const size_t sm = zsmem((int)nz);
     static const int zmode = [] { const char *e = getenv("CT_EDT_Z"); return e ? atoi(e) : 1; }();
