@@ -24,6 +24,7 @@
 //   Limb pairs (a, b) with a + b >= 2 (data limb a, weight limb b) are kept;
 //   pairs of equal a + b share an accumulator (5 accumulators).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ct_common.cuh"
 #include "tc_common.cuh"
@@ -524,6 +525,9 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
                      cudaStream_t s) {
     if (!ct_gaussian_q_tc_fits(nx, ny, nz, rx, ry, rz) || ((uintptr_t)raw & 15)) return CT_ERR_UNSUPPORTED;
     const long long N = nx * ny * nz;
+    // persistent grids: one CTA per SM (CT_TC_SMS caps it, e.g. to leave SMs to a concurrent stream)
+    static const int nsm = [] { const char *e = getenv("CT_TC_SMS"); const int v = e ? atoi(e) : 0;
+                                return v > 0 && v < CT_NUM_SMS ? v : CT_NUM_SMS; }();
     uint8_t *p1 = (uint8_t *)work, *p2 = p1 + 4 * N;
     TcParams *prm = (TcParams *)(p2 + 4 * N);
     cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
@@ -534,7 +538,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
         const size_t sm = 6 * 1 * KXY * TNX + 2 * 4 * TM * (TNX + 16) + 1024;
         cudaFuncSetAttribute(tc_pass_xy<1, 6, TNX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TNX);
-        tc_pass_xy<1, 6, TNX><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
+        tc_pass_xy<1, 6, TNX><<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(
             raw, 0, (int)nx, (int)(ny * nz), 1, prm, 0, rx, p1, N);
         if (int st = ct::check_launch("tc_pass_x")) return st;
     }
@@ -543,7 +547,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
         const size_t sm = 5 * 4 * KXY * TNY + 2 * 4 * TM * (TNY + 16) + 1024;
         cudaFuncSetAttribute(tc_pass_xy<4, 5, TNY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TNY);
-        tc_pass_xy<4, 5, TNY><<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(
+        tc_pass_xy<4, 5, TNY><<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(
             p1, N, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2, N);
         if (int st = ct::check_launch("tc_pass_y")) return st;
     }
@@ -553,7 +557,7 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
         const size_t sm = 4 * nz * nz + 4 * 4 * TM * nz + 4 * TM * nz + 2 * TM * nz + 1024;
         auto kz = nz == 64 ? tc_pass_z<64, 4> : tc_pass_z<32, 4>;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        kz<<<(unsigned)std::min<long long>(tiles, CT_NUM_SMS), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
+        kz<<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
         if (int st = ct::check_launch("tc_pass_z")) return st;
     }
     return CT_OK;
