@@ -393,3 +393,29 @@ def test_gpu_voxel_runs_c2_properties(cuda):
         dec = S.decode_voxel_runs(runs[offs[r]:offs[r + 1]].tolist())
         np.testing.assert_array_equal(dec, np.stack([lin // (ny * nz), (lin // nz) % ny, lin % nz], axis=1))
     assert runs[:, 3].sum() == vox.shape[0]
+
+
+@pytest.mark.parametrize("shape", [(24, 40, 64), (16, 24, 32), (12, 20, 128), (10, 12, 70)])
+def test_specialised_kernel_paths_vs_oracle(cuda, oracle, shape):
+    """nz-specialised kernels (SIMD MRF stream for nz in {32, 64, 128}, run-based
+    CCL with the vectorised row pack for nz == 64, packed EDT pass z for
+    nz in {32, 64}) and their generic fallbacks (nz = 70) against the oracle."""
+    rng = np.random.default_rng(sum(shape))
+    # MRF statistics on u8 volumes: smooth ramp + noise (0 iterations) and pure noise
+    ramp = (np.add.outer(np.add.outer(np.arange(shape[0]), np.arange(shape[1])), np.arange(shape[2])) % 50)
+    for v in ((ramp + rng.integers(0, 9, shape)).astype(np.uint8), rng.integers(0, 256, shape).astype(np.uint8)):
+        st = D.mrf_denoise_state(VoxelGrid(values=v, spacing=UNIT))
+        o = oracle.mrf(v)
+        assert (st.sigma_hat, st.delta, st.iteration, st.converged) == \
+            (o["sigma_hat"], o["delta"], o["iteration"], o["converged"])
+        np.testing.assert_array_equal(np.asarray(st.current.values, dtype=np.float64), o["current"])
+    # labels / detections and the EDT on random masks of two densities
+    for thr in (0.55, 0.9):
+        m = rng.random(shape) > thr
+        d_gpu = S.detections_from_mask(m, ANISO, frame=0, min_volume_um3=0.0)
+        d_ora = oracle.detections(m, ANISO.as_array(), min_volume_um3=0.0)
+        assert [d.id for d in d_gpu] == [d.id for d in d_ora]
+        for a, b in zip(d_gpu, d_ora):
+            np.testing.assert_array_equal(a.voxels, b.voxels)
+            np.testing.assert_array_equal(a.centroid_um, b.centroid_um)
+        np.testing.assert_array_equal(S.distance_map(m, ANISO).values, oracle.edt(m, ANISO.as_array()))
