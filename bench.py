@@ -165,11 +165,15 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+GATHER_ROWS = 2048  # per-cell records exchanged per frame and rank (C2: ~1,550 cells)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_1407_2089_b200 import _lib, synth
+    from paper_1407_2089_b200.distributed import gather_tables
     from paper_1407_2089_b200.imaging import VoxelSpacing
     from paper_1407_2089_b200.pipeline import FramePipeline
 
@@ -211,7 +215,9 @@ def run_ours(args):
         main.wait_stream(s_cell)
         main.wait_stream(s_vess)
         if world > 1:
+            # the frame's detection count (global ids) and its per-cell records, over NCCL
             dist.all_gather_into_tensor(gathered, counts_dev)
+            gather_tables(pipe.table, pipe.counters[2], max_rows=GATHER_ROWS)
 
     for i in range(args.warmup):
         step(i)

@@ -48,3 +48,25 @@ def relabel_rows(rows, id_start: int):
     out = rows.copy()
     out["id"] += id_start
     return out
+
+
+def gather_tables(rows: torch.Tensor, nrows: torch.Tensor, max_rows: int, group=None):
+    """All-gather of fixed-width per-cell records.
+
+    rows: uint8 tensor holding this rank's ct_cell rows (>= max_rows * 128
+    bytes; 128 B per row), nrows: int64 scalar tensor (valid rows, on the same
+    device).  Exchanges max_rows rows per rank in one all_gather_into_tensor
+    (fixed size: no size round trip; NCCL over NVLink on the GPU box) plus the
+    counts.  Returns (gathered uint8 [world, max_rows * 128], counts int64
+    [world]); rank r's valid rows are gathered[r, :counts[r] * 128]."""
+    row = 128
+    buf = rows[: max_rows * row].contiguous()
+    cnt = nrows.reshape(1).to(torch.int64)
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if world == 1:
+        return buf.reshape(1, -1), cnt.clamp(max=max_rows)
+    out = torch.empty(world * buf.numel(), dtype=buf.dtype, device=buf.device)
+    cnts = torch.empty(world, dtype=torch.int64, device=buf.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    dist.all_gather_into_tensor(cnts, cnt, group=group)
+    return out.reshape(world, -1), cnts.clamp(max=max_rows)

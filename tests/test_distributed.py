@@ -7,7 +7,7 @@ import socket
 import numpy as np
 import torch.multiprocessing as mp
 
-from paper_1407_2089_b200.distributed import frame_shard, global_id_starts
+from paper_1407_2089_b200.distributed import frame_shard, gather_tables, global_id_starts
 
 
 def _free_port():
@@ -61,3 +61,38 @@ def test_id_starts_world2_gloo():
         assert starts == expected
         owned |= set(frames)
     assert owned == set(range(len(counts)))
+
+
+def _gather_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 3 + 2 * rank
+    rows = torch.zeros(8 * 128, dtype=torch.uint8)
+    for i in range(n):
+        rows[i * 128:(i + 1) * 128] = 10 * rank + i
+    got, cnts = gather_tables(rows, torch.tensor(n), max_rows=8)
+    q.put((rank, got.numpy(), cnts.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_tables_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for _, got, cnts in res:
+        assert cnts.tolist() == [3, 5]
+        for r in range(2):
+            for i in range(int(cnts[r])):
+                assert (got[r, i * 128:(i + 1) * 128] == 10 * r + i).all()
