@@ -119,4 +119,23 @@ struct ByteHist256 {
     }
 };
 
+// z-row words: u64 for nz <= 64, unsigned __int128 for nz <= 128 (bit k = voxel k)
+using u128 = unsigned __int128;
+__device__ __forceinline__ int rffs(unsigned long long x) { return __ffsll((long long)x); }
+__device__ __forceinline__ int rffs(u128 x) {
+    const unsigned long long lo = (unsigned long long)x, hi = (unsigned long long)(x >> 64);
+    return lo ? __ffsll((long long)lo) : (hi ? 64 + __ffsll((long long)hi) : 0);
+}
+__device__ __forceinline__ int rclz(unsigned long long x) { return __clzll((long long)x); }  // 64 bits
+__device__ __forceinline__ int rclz(u128 x) {  // 128 bits
+    const unsigned long long lo = (unsigned long long)x, hi = (unsigned long long)(x >> 64);
+    return hi ? __clzll((long long)hi) : 64 + __clzll((long long)lo);
+}
+__device__ __forceinline__ int rpopc(unsigned long long x) { return __popcll(x); }
+__device__ __forceinline__ int rpopc(u128 x) {
+    return __popcll((unsigned long long)x) + __popcll((unsigned long long)(x >> 64));
+}
+template <typename R> __host__ __device__ constexpr int rbits() { return (int)(8 * sizeof(R)); }
+template <typename R> __device__ __forceinline__ R rmask(int n) { return n >= rbits<R>() ? ~(R)0 : (((R)1 << n) - 1); }
+
 }  // namespace ct

@@ -222,7 +222,7 @@ __global__ void ccl_flatten(int32_t *labels, const int32_t *__restrict__ fg, con
 }
 
 // ---------------------------------------------------------------------------
-// Run-based labelling for nz <= 64: every z-row is one 64-bit word (packed on
+// Run-based labelling for nz <= 128: every z-row is one 64- or 128-bit word (packed on
 // the fly from the mask bytes); union-find nodes are the runs of consecutive
 // foreground voxels, identified by their first voxel's linear index (so the
 // component root -- the minimum node -- is again its minimum voxel).
@@ -231,49 +231,52 @@ __global__ void ccl_flatten(int32_t *labels, const int32_t *__restrict__ fg, con
 //                   (i, j-1), (i-1, j-1..j+1) that touch it in z +- 1
 //   ccl_run_emit  : labels of every run voxel = find(run start); fg list
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long pack_row(const uint8_t *__restrict__ row, int nz) {
-    unsigned long long w = 0;
-    if (nz == 64 && ((uintptr_t)row & 15) == 0) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
+template <typename R>
+__device__ __forceinline__ R pack_row(const uint8_t *__restrict__ row, int nz) {
+    R w = 0;
+    if (nz % 16 == 0 && ((uintptr_t)row & 15) == 0) {
+        for (int c = 0; c < nz / 16; ++c) {
             const uint4 v = __ldg((const uint4 *)row + c);
             const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t t = (x[q] | ((x[q] & 0x7f7f7f7fu) + 0x7f7f7f7fu)) & 0x80808080u;
-                w |= (unsigned long long)(((t >> 7) * 0x10204080u) >> 28) << (16 * c + 4 * q);
+                w |= (R)(((t >> 7) * 0x10204080u) >> 28) << (16 * c + 4 * q);
             }
         }
     } else {
         for (int k = 0; k < nz; ++k)
-            if (row[k]) w |= 1ull << k;
+            if (row[k]) w |= (R)1 << k;
     }
     return w;
 }
 
 // run of w starting at bit s: mask of its bits
-__device__ __forceinline__ unsigned long long run_mask(unsigned long long w, int s) {
-    const unsigned long long above = ~(w >> s);  // first zero at or above s
-    const int len = above ? __ffsll((long long)above) - 1 : 64 - s;
-    return (len >= 64 ? ~0ull : ((1ull << len) - 1)) << s;
+template <typename R>
+__device__ __forceinline__ R run_mask(R w, int s) {
+    const R above = ~(w >> s);  // first zero at or above s
+    const int len = above ? ct::rffs(above) - 1 : ct::rbits<R>() - s;
+    return ct::rmask<R>(len) << s;
 }
 
+template <typename R>
 __global__ void ccl_run_init(const uint8_t *__restrict__ mask, i64 nrows, int nz, int32_t *__restrict__ labels) {
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        unsigned long long st = pack_row(mask + r * nz, nz);
+        R st = pack_row<R>(mask + r * nz, nz);
         st &= ~(st << 1);  // run starts
         while (st) {
-            const int s = __ffsll((long long)st) - 1;
+            const int s = ct::rffs(st) - 1;
             st &= st - 1;
             labels[r * nz + s] = (int32_t)(r * nz + s);
         }
     }
 }
 
+template <typename R>
 __global__ void ccl_run_union(const uint8_t *__restrict__ mask, i64 nx, i64 ny, int nz, int32_t *labels) {
     const i64 nrows = nx * ny;
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        const unsigned long long w = pack_row(mask + r * nz, nz);
+        const R w = pack_row<R>(mask + r * nz, nz);
         if (!w) continue;
         const i64 i = r / ny, j = r - i * ny;
         const i64 nb[4] = {j > 0 ? r - 1 : -1, (i > 0 && j > 0) ? r - ny - 1 : -1, i > 0 ? r - ny : -1,
@@ -281,19 +284,19 @@ __global__ void ccl_run_union(const uint8_t *__restrict__ mask, i64 nx, i64 ny, 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (nb[q] < 0) continue;
-            const unsigned long long u = pack_row(mask + nb[q] * nz, nz);
+            const R u = pack_row<R>(mask + nb[q] * nz, nz);
             if (!u) continue;
-            const unsigned long long ustart = u & ~(u << 1);
-            unsigned long long rem = w;
+            const R ustart = u & ~(u << 1);
+            R rem = w;
             while (rem) {
-                const int s = __ffsll((long long)rem) - 1;
-                const unsigned long long mr = run_mask(w, s);
+                const int s = ct::rffs(rem) - 1;
+                const R mr = run_mask(w, s);
                 rem &= ~mr;
-                unsigned long long o = (mr | (mr << 1) | (mr >> 1)) & u;  // 26-neighbours in row nb
+                R o = (mr | (mr << 1) | (mr >> 1)) & u;  // 26-neighbours in row nb
                 while (o) {
-                    const int b = __ffsll((long long)o) - 1;
-                    const unsigned long long below = ustart & (b == 63 ? ~0ull : ((2ull << b) - 1));
-                    const int su = 63 - __clzll((long long)below);
+                    const int b = ct::rffs(o) - 1;
+                    const R below = ustart & ct::rmask<R>(b + 1);
+                    const int su = ct::rbits<R>() - 1 - ct::rclz(below);
                     o &= ~run_mask(u, su);
                     union_gh(labels, (int)(r * nz + s), (int)(nb[q] * nz + su));
                 }
@@ -302,38 +305,37 @@ __global__ void ccl_run_union(const uint8_t *__restrict__ mask, i64 nx, i64 ny, 
     }
 }
 
+template <typename R>
 __global__ void ccl_run_emit(const uint8_t *__restrict__ mask, i64 nrows, int nz, int32_t *labels,
                              int32_t *__restrict__ fg, int64_t *__restrict__ counters) {
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        const unsigned long long w = pack_row(mask + r * nz, nz);
+        const R w = pack_row<R>(mask + r * nz, nz);
         if (!w) continue;
-        const int n = __popcll(w);
+        const int n = ct::rpopc(w);
         const unsigned long long base = atomicAdd((unsigned long long *)&counters[CT_CNT_FG], (unsigned long long)n);
-        unsigned long long rem = w;
+        R rem = w;
         int e = 0;
         while (rem) {
-            const int s = __ffsll((long long)rem) - 1;
-            const unsigned long long mr = run_mask(w, s);
+            const int s = ct::rffs(rem) - 1;
+            const R mr = run_mask(w, s);
             rem &= ~mr;
             const int32_t root = (int32_t)find_g(labels, (int)(r * nz + s));
-            for (unsigned long long m = mr; m; m &= m - 1) {
-                const int k = __ffsll((long long)m) - 1;
-                fg[base + e++] = (int32_t)(r * nz + k);
-            }
+            for (R m = mr; m; m &= m - 1) fg[base + e++] = (int32_t)(r * nz + ct::rffs(m) - 1);
             // run starts hold the union-find links until every thread's find is done:
             // write the run's other voxels now, the start in a second sweep
-            for (unsigned long long m = mr & (mr - 1); m; m &= m - 1) labels[r * nz + __ffsll((long long)m) - 1] = root;
+            for (R m = mr & (mr - 1); m; m &= m - 1) labels[r * nz + ct::rffs(m) - 1] = root;
         }
     }
 }
 
 // final sweep: run starts take their root (after all finds of ccl_run_emit)
+template <typename R>
 __global__ void ccl_run_roots(const uint8_t *__restrict__ mask, i64 nrows, int nz, int32_t *labels) {
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        unsigned long long st = pack_row(mask + r * nz, nz);
+        R st = pack_row<R>(mask + r * nz, nz);
         st &= ~(st << 1);
         while (st) {
-            const int s = __ffsll((long long)st) - 1;
+            const int s = ct::rffs(st) - 1;
             st &= st - 1;
             labels[r * nz + s] = find_g(labels, (int)(r * nz + s));  // path compression to the root
         }
@@ -821,14 +823,18 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(counters, 0, CT_CNT_WORDS * sizeof(int64_t), s);
     cudaMemsetAsync(labels, 0xff, (size_t)(nx * ny * nz) * sizeof(int32_t), s);  // background = -1
-    if (nz <= 64 && getenv("CT_CCL_TILES") == nullptr) {
+    if (nz <= 128 && getenv("CT_CCL_TILES") == nullptr) {
         const i64 nrows = nx * ny;
         const int g = (int)min((nrows + 255) / 256, (i64)CT_NUM_SMS * 16);
-        ccl_run_init<<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels);
-        ccl_run_union<<<g, 256, 0, s>>>(mask, nx, ny, (int)nz, labels);
-        ccl_run_emit<<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels, fg_list, counters);
-        ccl_run_roots<<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels);
-        return ct::check_launch("ccl_run");
+        auto run = [&](auto tag) -> int {
+            using R = decltype(tag);
+            ccl_run_init<R><<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels);
+            ccl_run_union<R><<<g, 256, 0, s>>>(mask, nx, ny, (int)nz, labels);
+            ccl_run_emit<R><<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels, fg_list, counters);
+            ccl_run_roots<R><<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels);
+            return ct::check_launch("ccl_run");
+        };
+        return nz <= 64 ? run((unsigned long long)0) : run((ct::u128)0);
     }
     const i64 tiles = ((nz + LK - 1) / LK) * ((ny + LJ - 1) / LJ) * ((nx + LI - 1) / LI);
     ccl_local<<<(int)min(tiles, (i64)CT_NUM_SMS * 8), dim3(LK, LJ), 0, s>>>(mask, nx, ny, nz, labels, fg_list,

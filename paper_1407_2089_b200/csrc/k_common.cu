@@ -40,7 +40,7 @@ extern "C" size_t ct_workspace_bytes(int which, int64_t nx, int64_t ny, int64_t 
         case 0: return (size_t)(2 * N) * sizeof(double);                                // gaussian
         case 1: {                                                                      // closing, cap = radius
             const size_t ext = (size_t)((nx + 2 * cap) * (ny + 2 * cap) * (nz + 2 * cap));
-            const size_t rows = (size_t)(nx * ny) * 8 + 256;
+            const size_t rows = (size_t)(nx * ny) * 16 + 256;  // z-row words (u64 / u128)
             return ext > rows ? ext : rows;
         }
         case 2: return ct_table_workspace(N, cap);                                      // table

@@ -131,51 +131,54 @@ __global__ void erode_ext(const uint8_t *__restrict__ ext, i64 nx, i64 ny, i64 n
 //                 thread per row, 13 word loads (L2-resident: N/8 bytes),
 //                 bytes written through an SMEM transpose for coalescing.
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, typename R>
 __global__ void __launch_bounds__(256) pack_rows(const T *__restrict__ in, i64 nrows, int nz,
                                                  const int64_t *__restrict__ otsu, i64 t_host,
-                                                 u64 *__restrict__ rows) {
+                                                 R *__restrict__ rows) {
     bool empty;
     const i64 t = threshold_of(otsu, t_host, empty);
     const unsigned lane = threadIdx.x & 31;
     const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
     const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
     for (i64 r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
-        u64 mine = 0;
+        R mine = 0;
         const int nr = (int)min((i64)32, nrows - r0);
         for (int r = 0; r < nr; ++r) {
             const T *row = in + (r0 + r) * nz;
-            const bool a = !empty && (int)lane < nz && ct::above(row[lane], t);
-            const bool b = !empty && (int)lane + 32 < nz && ct::above(row[lane + 32], t);
-            const unsigned wa = __ballot_sync(0xffffffffu, a), wb = __ballot_sync(0xffffffffu, b);
-            if ((int)lane == r) mine = ((u64)wb << 32) | wa;
+            R word = 0;
+#pragma unroll
+            for (int q = 0; q < ct::rbits<R>() / 32; ++q) {
+                const int k = (int)lane + 32 * q;
+                const bool a = !empty && k < nz && ct::above(row[k], t);
+                word |= (R)__ballot_sync(0xffffffffu, a) << (32 * q);
+            }
+            if ((int)lane == r) mine = word;
         }
         if ((int)lane < nr) rows[r0 + lane] = mine;
     }
 }
 
-// u8, nz == 64: one thread per row, 4 x 16-byte loads, SIMD byte compares
-__global__ void __launch_bounds__(256) pack_rows_u8x64(const uint8_t *__restrict__ in, i64 nrows,
-                                                       const int64_t *__restrict__ otsu, i64 t_host,
-                                                       u64 *__restrict__ rows) {
+// u8, nz % 16 == 0 (<= 128): one thread per row, 16-byte loads, SIMD byte compares
+template <typename R>
+__global__ void __launch_bounds__(256) pack_rows_u8v(const uint8_t *__restrict__ in, i64 nrows, int nz,
+                                                     const int64_t *__restrict__ otsu, i64 t_host,
+                                                     R *__restrict__ rows) {
     bool empty;
     const i64 t = threshold_of(otsu, t_host, empty);
-    // above(v, t) = v > t for integers: all bytes if t < 0, none if t >= 255 or empty
     const bool all = !empty && t < 0, none = empty || t >= 255;
     const uint32_t tb = (uint32_t)(all || none ? 0 : t) * 0x01010101u;
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        u64 w = 0;
-        if (all) w = ~0ull;
+        R w = 0;
+        if (all) w = ct::rmask<R>(nz);
         else if (!none) {
-            const uint4 *src = (const uint4 *)(in + r * 64);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            const uint4 *src = (const uint4 *)(in + r * nz);
+            for (int c = 0; c < nz / 16; ++c) {
                 const uint4 v = __ldg(src + c);
                 const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const uint32_t g = __vcmpgtu4(x[q], tb) & 0x80808080u;  // high bit per byte
-                    w |= (u64)(((g >> 7) * 0x10204080u) >> 28) << (16 * c + 4 * q);
+                    w |= (R)(((g >> 7) * 0x10204080u) >> 28) << (16 * c + 4 * q);
                 }
             }
         }
@@ -183,40 +186,43 @@ __global__ void __launch_bounds__(256) pack_rows_u8x64(const uint8_t *__restrict
     }
 }
 
-__device__ __forceinline__ u64 rowM(const u64 *rows, i64 i, i64 j, i64 nx, i64 ny) {
-    return (i >= 0 && i < nx && j >= 0 && j < ny) ? rows[i * ny + j] : 0ull;
+template <typename R>
+__device__ __forceinline__ R rowM(const R *rows, i64 i, i64 j, i64 nx, i64 ny) {
+    return (i >= 0 && i < nx && j >= 0 && j < ny) ? rows[i * ny + j] : (R)0;
 }
 
 // dilation row D(i,j) over the whole (possibly out-of-volume) row
-__device__ __forceinline__ u64 rowD(const u64 *rows, i64 i, i64 j, i64 nx, i64 ny, u64 kmask) {
-    const u64 c = rowM(rows, i, j, nx, ny);
+template <typename R>
+__device__ __forceinline__ R rowD(const R *rows, i64 i, i64 j, i64 nx, i64 ny, R kmask) {
+    const R c = rowM(rows, i, j, nx, ny);
     return (c | (c << 1) | (c >> 1) | rowM(rows, i - 1, j, nx, ny) | rowM(rows, i + 1, j, nx, ny) |
             rowM(rows, i, j - 1, nx, ny) | rowM(rows, i, j + 1, nx, ny)) & kmask;
 }
 
-__global__ void __launch_bounds__(256) close1_bits(const u64 *__restrict__ rows, i64 nx, i64 ny, int nz,
-                                                   uint8_t *__restrict__ out, u64 *__restrict__ out_rows) {
-    __shared__ __align__(16) uint8_t stage[8][32 * 64];
+template <typename R>
+__global__ void __launch_bounds__(256) close1_bits(const R *__restrict__ rows, i64 nx, i64 ny, int nz,
+                                                   uint8_t *__restrict__ out, R *__restrict__ out_rows) {
+    __shared__ __align__(16) uint8_t stage[8][32 * ct::rbits<R>()];
     const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u64 kmask = nz == 64 ? ~0ull : ((1ull << nz) - 1);
-    const u64 top = 1ull << (nz - 1);
+    const R kmask = ct::rmask<R>(nz);
+    const R top = (R)1 << (nz - 1);
     const i64 nrows = nx * ny;
     const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
     const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
     for (i64 r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
         const i64 r = r0 + lane;
-        u64 e = 0;
+        R e = 0;
         if (r < nrows) {
             const i64 i = r / ny, j = r - i * ny;
-            const u64 m = rows[r];
-            const u64 d = rowD(rows, i, j, nx, ny, kmask);
+            const R m = rows[r];
+            const R d = rowD(rows, i, j, nx, ny, kmask);
             // cross neighbours of D; outside the volume D equals the single in-volume M
-            const u64 dxm = i > 0 ? rowD(rows, i - 1, j, nx, ny, kmask) : m;
-            const u64 dxp = i < nx - 1 ? rowD(rows, i + 1, j, nx, ny, kmask) : m;
-            const u64 dym = j > 0 ? rowD(rows, i, j - 1, nx, ny, kmask) : m;
-            const u64 dyp = j < ny - 1 ? rowD(rows, i, j + 1, nx, ny, kmask) : m;
-            const u64 dkm = ((d << 1) | (m & 1ull)) & kmask;    // D at k-1; k=-1 -> M(k=0)
-            const u64 dkp = (d >> 1) | (m & top);               // D at k+1; k=nz -> M(k=nz-1)
+            const R dxm = i > 0 ? rowD(rows, i - 1, j, nx, ny, kmask) : m;
+            const R dxp = i < nx - 1 ? rowD(rows, i + 1, j, nx, ny, kmask) : m;
+            const R dym = j > 0 ? rowD(rows, i, j - 1, nx, ny, kmask) : m;
+            const R dyp = j < ny - 1 ? rowD(rows, i, j + 1, nx, ny, kmask) : m;
+            const R dkm = ((d << 1) | (m & (R)1)) & kmask;    // D at k-1; k=-1 -> M(k=0)
+            const R dkp = (d >> 1) | (m & top);               // D at k+1; k=nz -> M(k=nz-1)
             e = d & dxm & dxp & dym & dyp & dkm & dkp;
             if (out_rows) out_rows[r] = e;
         }
@@ -259,18 +265,23 @@ int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i6
         threshold_kernel<T><<<ct::grid_for(n, 256), 256, 0, s>>>(in, n, otsu, t_host, out);
         return ct::check_launch("threshold");
     }
-    if (r == 1 && nz <= 64 && nz % 4 == 0 && work && ((uintptr_t)out & 15) == 0) {
-        u64 *rows = (u64 *)work;
+    if (r == 1 && nz <= 128 && nz % 4 == 0 && work && ((uintptr_t)out & 15) == 0) {
         const i64 nrows = nx * ny;
-        if (sizeof(T) == 1 && nz == 64 && ((uintptr_t)in & 15) == 0)
-            pack_rows_u8x64<<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>((const uint8_t *)in, nrows, otsu,
-                                                                                      t_host, rows);
-        else
-            pack_rows<T><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(in, nrows, (int)nz, otsu, t_host,
-                                                                                   rows);
-        if (int st = ct::check_launch("pack_rows")) return st;
-        close1_bits<<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(rows, nx, ny, (int)nz, out, nullptr);
-        return ct::check_launch("close1_bits");
+        auto run = [&](auto tag) -> int {
+            using R = decltype(tag);
+            R *rows = (R *)work;
+            if (sizeof(T) == 1 && nz % 16 == 0 && ((uintptr_t)in & 15) == 0)
+                pack_rows_u8v<R><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(
+                    (const uint8_t *)in, nrows, (int)nz, otsu, t_host, rows);
+            else
+                pack_rows<T, R><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(in, nrows, (int)nz, otsu,
+                                                                                          t_host, rows);
+            if (int st = ct::check_launch("pack_rows")) return st;
+            close1_bits<R><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(rows, nx, ny, (int)nz, out,
+                                                                                      nullptr);
+            return ct::check_launch("close1_bits");
+        };
+        return nz <= 64 ? run((u64)0) : run((ct::u128)0);
     }
     if (r == 1) {
         const i64 tiles = ((nz + TK - 1) / TK) * ((ny + TJ - 1) / TJ) * ((nx + TI - 1) / TI);
