@@ -435,6 +435,41 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     uint32_t phase = 0;
     constexpr int CW = NZ / 4;  // columns per thread
     const int h0 = cg * CW;
+    // q of one voxel (column h0 + c of line l) from its 5 accumulator words,
+    // the raw byte and the line's edge values; flags it for the fix-up
+    auto qbyte = [&](const uint32_t v0, const uint32_t v1, const uint32_t v2, const uint32_t v3, const uint32_t v4,
+                     int c, uint32_t raw8, uint32_t x0, uint32_t xl, long long l) -> uint32_t {
+        // S = sum_acc v[acc] 2^(8 acc) (IMAD.WIDE chain) + edge taps
+        const uint4 e = Et[h0 + c];
+        const unsigned long long lo = (unsigned long long)x0 * e.y + (unsigned long long)xl * e.w;
+        unsigned long long S = (unsigned long long)v0 + (unsigned long long)v1 * 0x100ull +
+                               (unsigned long long)v2 * 0x10000ull + (unsigned long long)v3 * 0x1000000ull +
+                               ((unsigned long long)v4 << 32);
+        S += (unsigned long long)x0 * e.x + (unsigned long long)xl * e.z + (lo >> 16);
+        // T = R + 2^(zs-1), R = raw 2^zs - S: q = max(T, 0) >> zs; the
+        // rounding boundaries R = (k + 1/2) 2^zs (k >= 0) are T = (k+1) 2^zs,
+        // flagged when T is within eps of one of them
+        const long long T = (long long)(((unsigned long long)raw8 << zs) - S) + half;
+        const uint32_t qv = T > 0 ? (uint32_t)(T >> zs) : 0u;
+        if (T >= one - eps && ((T + eps) & fmask) <= 2 * eps) {
+            const unsigned long long at = atomicAdd(&fix[0], 1ull);
+            if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
+            else fix[1] = 1;
+        }
+        return qv & 0xffu;
+    };
+    auto edges = [&](long long k, uint32_t &x0, uint32_t &xl) {
+        const uint8_t *ab = sa + (int)(k % STAGES) * 4 * ABUF;
+        const uint32_t o0 = tc::kmajor_off(m, 0, LBO, SBO), ol = tc::kmajor_off(m, NZ - 1, LBO, SBO);
+        x0 = xl = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            x0 |= (uint32_t)ab[a * ABUF + o0] << (8 * a);
+            xl |= (uint32_t)ab[a * ABUF + ol] << (8 * a);
+        }
+    };
+    if constexpr (NZ <= 64) {
+    // accumulators -> registers, barrier, MMA(k+1), then the epilogue of k
     for (long long k = 0; k < nmine; ++k) {
         tc::mbar_wait(&mbar, phase);
         phase ^= 1;
@@ -452,16 +487,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         uint32_t rw[CW / 4];
 #pragma unroll
         for (int c4 = 0; c4 < CW / 4; ++c4) rw[c4] = *(const uint32_t *)(rl + 4 * c4);
-        uint32_t x0 = 0, xl = 0;
-        {
-            const uint8_t *ab = sa + (int)(k % STAGES) * 4 * ABUF;
-            const uint32_t o0 = tc::kmajor_off(m, 0, LBO, SBO), ol = tc::kmajor_off(m, NZ - 1, LBO, SBO);
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                x0 |= (uint32_t)ab[a * ABUF + o0] << (8 * a);
-                xl |= (uint32_t)ab[a * ABUF + ol] << (8 * a);
-            }
-        }
+        uint32_t x0, xl;
+        edges(k, x0, xl);
         tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
         tc::fence_async_smem();
         tc::fence_before();
@@ -476,31 +503,52 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         for (int c4 = 0; c4 < CW / 4; ++c4) qw[c4] = 0;
         if (l < nlines) {
 #pragma unroll
-            for (int c = 0; c < CW; ++c) {
-                // S = sum_acc v[acc] 2^(8 acc) (IMAD.WIDE chain) + edge taps
-                const uint4 e = Et[h0 + c];
-                const unsigned long long lo = (unsigned long long)x0 * e.y + (unsigned long long)xl * e.w;
-                unsigned long long S = (unsigned long long)v[0][c] + (unsigned long long)v[1][c] * 0x100ull +
-                                       (unsigned long long)v[2][c] * 0x10000ull +
-                                       (unsigned long long)v[3][c] * 0x1000000ull + ((unsigned long long)v[4][c] << 32);
-                S += (unsigned long long)x0 * e.x + (unsigned long long)xl * e.z + (lo >> 16);
-                // T = R + 2^(zs-1), R = raw 2^zs - S: q = max(T, 0) >> zs; the
-                // rounding boundaries R = (k + 1/2) 2^zs (k >= 0) are T = (k+1) 2^zs,
-                // flagged when T is within eps of one of them
-                const long long T = (long long)(((unsigned long long)((rw[c >> 2] >> (8 * (c & 3))) & 0xff) << zs) -
-                                                S) + half;
-                const uint32_t qv = T > 0 ? (uint32_t)(T >> zs) : 0u;
-                if (T >= one - eps && ((T + eps) & fmask) <= 2 * eps) {
-                    const unsigned long long at = atomicAdd(&fix[0], 1ull);
-                    if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
-                    else fix[1] = 1;
-                }
-                qw[c >> 2] |= (qv & 0xffu) << (8 * (c & 3));
-            }
+            for (int c = 0; c < CW; ++c)
+                qw[c >> 2] |= qbyte(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], c,
+                                    (rw[c >> 2] >> (8 * (c & 3))) & 0xff, x0, xl, l) << (8 * (c & 3));
         }
         uint8_t *qb = sq + (int)(k & 1) * ABUF + m * NZ + h0;
 #pragma unroll
         for (int c4 = 0; c4 < CW / 4; c4 += 2) *(uint2 *)(qb + 4 * c4) = make_uint2(qw[c4], qw[c4 + 1]);
+    }
+    } else {
+    // long lines (NZ = 96): the accumulators do not fit in registers at once,
+    // so the epilogue drains them in 8-column chunks before MMA(k+1) is issued
+    for (long long k = 0; k < nmine; ++k) {
+        tc::mbar_wait(&mbar, phase);
+        phase ^= 1;
+        tc::fence_after();
+        const long long l = (t0 + k * gs) * TM + m;
+        const uint8_t *rl = sr + (int)(k % STAGES) * ABUF + m * NZ + h0;
+        uint32_t x0, xl;
+        edges(k, x0, xl);
+        uint8_t *qb = sq + (int)(k & 1) * ABUF + m * NZ + h0;
+#pragma unroll
+        for (int g8 = 0; g8 < CW; g8 += 8) {
+            uint32_t v[5][8];
+#pragma unroll
+            for (int acc = 0; acc < 5; ++acc) tc::tmem_ld8(lane_addr + NZ * acc + h0 + g8, v[acc]);
+            tc::tmem_ld_wait();
+            const uint32_t r0w = *(const uint32_t *)(rl + g8), r1w = *(const uint32_t *)(rl + g8 + 4);
+            uint32_t qw[2] = {0, 0};
+            if (l < nlines) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    qw[c >> 2] |= qbyte(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], g8 + c,
+                                        ((c < 4 ? r0w : r1w) >> (8 * (c & 3))) & 0xff, x0, xl, l) << (8 * (c & 3));
+            }
+            *(uint2 *)(qb + g8) = make_uint2(qw[0], qw[1]);
+        }
+        tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (k + 1 < nmine) issue(k + 1);
+        if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
+        else tc::cp_commit();
+        if (k > 0) flush(t0 + (k - 1) * gs, sq + (int)((k - 1) & 1) * ABUF);
+    }
     }
     __syncthreads();
     if (nmine > 0) flush(t0 + (nmine - 1) * gs, sq + (int)((nmine - 1) & 1) * ABUF);
@@ -516,7 +564,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
 // does not fit (the caller then uses the SIMT FMA path).  work: >= 8 N bytes
 // (byte planes of P1 and P2) + sizeof(TcParams).
 bool ct_gaussian_q_tc_fits(int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz) {
-    return (nz == 32 || nz == 64) && rx >= 0 && ry >= 0 && rz >= 0 && rx <= (KXY - TM) / 2 && ry <= (KXY - TM) / 2 &&
+    return (nz == 32 || nz == 64 || nz == 96) && rx >= 0 && ry >= 0 && rz >= 0 && rx <= (KXY - TM) / 2 && ry <= (KXY - TM) / 2 &&
            rz < PMAX && (ny * nz) % TNX == 0 && nz % TNY == 0 && nx * ny * nz < (1ll << 31);
 }
 
@@ -554,8 +602,9 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     // pass z + epilogue
     {
         const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
-        const size_t sm = 4 * nz * nz + 4 * 4 * TM * nz + 4 * TM * nz + 2 * TM * nz + 1024;
-        auto kz = nz == 64 ? tc_pass_z<64, 4> : tc_pass_z<32, 4>;
+        const int stg = nz == 96 ? 2 : 4;
+        const size_t sm = 4 * nz * nz + (size_t)stg * (4 * TM * nz + TM * nz) + 2 * TM * nz + 1024;
+        auto kz = nz == 64 ? tc_pass_z<64, 4> : nz == 96 ? tc_pass_z<96, 2> : tc_pass_z<32, 4>;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         kz<<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
         if (int st = ct::check_launch("tc_pass_z")) return st;

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                 for (int q = 0; q < 4; ++q) {
                     const int r = r0 + q * 8 * RPW + lrow;
                     x[q] = 0u;
-                    if (r < NR) {
+                    if (r < NR && lrow < RPW) {  // (WC = 3: lanes 24-31 idle)
                         const int ri = r / RJ, rj = r - ri * RJ;
                         const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
                         x[q] = __ldg((const uint32_t *)(in + (i * ny + j) * nz) + (lane % LPR));
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                 for (int q = 0; q < 4; ++q) {
                     const int r = r0 + q * 8 * RPW + lrow;
                     const uint32_t y = nib_transpose8(t4x8(x[q]), sub);
-                    if (r < NR) {
+                    if (r < NR && lrow < RPW) {
                         pc[sub * NW + r * W + lw] = y;
                         anyw |= y ? (1u << sub) : 0u;
                     }
@@ -575,6 +575,7 @@ extern "C" int ct_median(const void *in, int dtype, int64_t nx, int64_t ny, int6
             const bool al4 = ((uintptr_t)in & 3) == 0;
             auto k = (al4 && nz == 64) ? median3_bits<uint8_t, 8, 2>
                      : (al4 && nz == 32) ? median3_bits<uint8_t, 8, 1>
+                     : (al4 && nz == 96) ? median3_bits<uint8_t, 8, 3>
                      : (al4 && nz == 128) ? median3_bits<uint8_t, 8, 4> : median3_bits<uint8_t, 8, 0>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             k<<<grid, 256, sm, s>>>((const uint8_t *)in, (uint8_t *)out, nx, ny, (int)nz, hist);

@@ -624,6 +624,7 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
     const int i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
     const int my = ny - 2, mz = NZ - 2;
     const int jj = threadIdx.x / W, kw = threadIdx.x % W, j = j0 + jj;
+    const bool own = jj < MJ4;  // (NZ = 96: 256 = 10 rows x 24 words + 16 idle threads)
     int goff[LW];
 #pragma unroll
     for (int q = 0; q < LW; ++q) {
@@ -653,11 +654,11 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
     store_plane(1, regs);
     load_plane(i0 + 2, regs2);  // two planes ahead from here on
     __syncthreads();
-    const int o = (jj + 1) * W + kw;
+    const int o = own ? (jj + 1) * W + kw : W;
     uint32_t xm = ring[2][o];
     unsigned nnz = 0;
     long long lsum = 0;
-    const bool jin = j < ny, jint = j > 0 && j < ny - 1;
+    const bool jin = own && j < ny, jint = j > 0 && j < ny - 1;
     int cs = 0, ns = 1, fs = 2;
     for (int i = i0; i < i1; ++i) {
         load_plane(i + 3, regs);  // planes i+2 (regs2) and i+3 (regs) in flight while plane i is processed
@@ -886,9 +887,11 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
     using LT = typename std::conditional<sizeof(T) == 1, int16_t, int32_t>::type;
     LT *lap = (LT *)w.lap;
     const i64 blocks = ((ny + MJ - 1) / MJ) * ((nx + MIPER - 1) / MIPER);
-    if (sizeof(T) == 1 && (nz == 32 || nz == 64 || nz == 128) && ((uintptr_t)v & 3) == 0 && ((uintptr_t)lap & 3) == 0 &&
+    if (sizeof(T) == 1 && (nz == 32 || nz == 64 || nz == 96 || nz == 128) && ((uintptr_t)v & 3) == 0 &&
+        ((uintptr_t)lap & 3) == 0 &&
         nx * ny * nz < (1ll << 31) && getenv("CT_MRF_SCALAR") == nullptr) {
-        auto kern = nz == 32 ? mrf_stream_v4<32> : nz == 64 ? mrf_stream_v4<64> : mrf_stream_v4<128>;
+        auto kern = nz == 32 ? mrf_stream_v4<32> : nz == 64 ? mrf_stream_v4<64> : nz == 96 ? mrf_stream_v4<96>
+                                                                                      : mrf_stream_v4<128>;
         const i64 b4 = ((ny + 256 / (nz / 4) - 1) / (256 / (nz / 4))) * ((nx + MIPER - 1) / MIPER);
         kern<<<(unsigned)b4, 256, 0, s>>>((const uint8_t *)v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal,
                                           (int16_t *)lap);
