@@ -435,27 +435,27 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
 // Same pass with the packed (dj, di) offsets kept in SMEM instead of the
 // float64 costs (costs recomputed on use by gyz, same operations): 4 + 1
 // bytes per element instead of 8 + 1, so ~1.8x more lines per SM.
-template <int NZ>
-__global__ void __launch_bounds__(ZL) edt_pass_zp(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
+template <int NZ, int ZLN = ZL>  // ZLN lines per CTA
+__global__ void __launch_bounds__(ZLN) edt_pass_zp(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
                                                   double dz, double *__restrict__ out) {
     constexpr int S = NZ + 1;  // padded line stride (conflict-free)
-    __shared__ int32_t ps[ZL * S];
-    __shared__ uint8_t stk[ZL * NZ];
+    __shared__ int32_t ps[ZLN * S];
+    __shared__ uint8_t stk[ZLN * NZ];
 
-    const i64 l0 = blockIdx.x * (i64)ZL;
-    const int nl = (int)min((i64)ZL, nlines - l0);
+    const i64 l0 = blockIdx.x * (i64)ZLN;
+    const int nl = (int)min((i64)ZLN, nlines - l0);
     const int32_t *src = in + l0 * NZ;
-    constexpr int T4 = ZL * NZ / 4;
-    for (int i0 = threadIdx.x; i0 < T4; i0 += 8 * ZL) {
+    constexpr int T4 = ZLN * NZ / 4;
+    for (int i0 = threadIdx.x; i0 < T4; i0 += 8 * ZLN) {
         int4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int q = i0 + u * ZL;
+            const int q = i0 + u * ZLN;
             if (q < T4 && q * 4 < nl * NZ) v[u] = __ldg((const int4 *)src + q);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int q = i0 + u * ZL;
+            const int q = i0 + u * ZLN;
             if (q < T4 && q * 4 < nl * NZ) {
                 const int idx = q * 4, g = idx / NZ, k = idx - g * NZ;
                 int32_t *d = ps + g * S + k;
@@ -512,55 +512,6 @@ __global__ void __launch_bounds__(ZL) edt_pass_zp(const int32_t *__restrict__ in
     }
 }
 
-// Same pass reading the packed offsets straight from global memory (L1
-// cached, each lane walks its own 256-byte line); only the stacks live in
-// SMEM, so occupancy is set by registers rather than shared memory.
-template <int NZ>
-__global__ void __launch_bounds__(ZL) edt_pass_zg(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
-                                                  double dz, double *__restrict__ out) {
-    __shared__ uint8_t stk[ZL * NZ];
-    const i64 l = blockIdx.x * (i64)ZL + threadIdx.x;
-    if (l >= nlines) return;
-    const int32_t *P = in + l * NZ;
-    auto G = [&](int x) -> double { const int32_t pl = __ldg(P + x); return pl == NONE32 ? INFINITY : gyz(pl, dx, dy); };
-    uint8_t *st = stk + threadIdx.x * NZ;
-    const double d2 = __dmul_rn(dz, dz);
-    int K = 0, tp = 0, bp = 0;
-    double tg = 0.0, bg = 0.0;
-    for (int x = 0; x < NZ; ++x) {
-        const int32_t px = __ldg(P + x);
-        if (px == NONE32) continue;
-        const double gx = gyz(px, dx, dy);
-        while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-            --K;
-            tp = bp;
-            tg = bg;
-            if (K >= 2) {
-                bp = st[K - 2];
-                bg = G(bp);
-            }
-        }
-        st[K++] = (uint8_t)x;
-        bp = tp; bg = tg; tp = x; tg = gx;
-    }
-    double *dst = out + l * NZ;
-    if (K == 0) {
-        for (int x = 0; x < NZ; ++x) dst[x] = INFINITY;
-        return;
-    }
-    int e = 0;
-    int cp = st[0], np = K > 1 ? st[1] : 0;
-    double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
-    for (int x = 0; x < NZ; ++x) {
-        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
-            ++e;
-            cp = np; cg = ng;
-            if (e + 1 < K) { np = st[e + 1]; ng = G(np); }
-        }
-        dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
-    }
-}
-
 inline size_t zsmem(int nz) {
     const int S = nz + 1;
     return (size_t)ZL * S * 8 + (size_t)ZL * nz + 16;
@@ -603,15 +554,10 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     edt_pass_y<<<dim3((unsigned)((ly + LT - 1) / LT), YSEG), LT, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, pk, spill);
     if (int st = ct::check_launch("edt_pass_y")) return st;
     const size_t sm = zsmem((int)nz);
-    static const int zmode = [] { const char *e = getenv("CT_EDT_Z"); return e ? atoi(e) : 1; }();
-    if (zmode == 2 && (nz == 64 || nz == 32)) {
-        if (nz == 64) edt_pass_zg<64><<<(unsigned)((lz + ZL - 1) / ZL), ZL, 0, s>>>(pk, lz, dx, dy, dz, out);
-        else edt_pass_zg<32><<<(unsigned)((lz + ZL - 1) / ZL), ZL, 0, s>>>(pk, lz, dx, dy, dz, out);
-        return ct::check_launch("edt_pass_zg");
-    }
-    if (zmode == 1 && (nz == 64 || nz == 32) && ((uintptr_t)pk & 15) == 0) {
+    if ((nz == 64 || nz == 32 || nz == 96) && ((uintptr_t)pk & 15) == 0) {
         if (nz == 64) edt_pass_zp<64><<<(unsigned)((lz + ZL - 1) / ZL), ZL, 0, s>>>(pk, lz, dx, dy, dz, out);
-        else edt_pass_zp<32><<<(unsigned)((lz + ZL - 1) / ZL), ZL, 0, s>>>(pk, lz, dx, dy, dz, out);
+        else if (nz == 32) edt_pass_zp<32><<<(unsigned)((lz + ZL - 1) / ZL), ZL, 0, s>>>(pk, lz, dx, dy, dz, out);
+        else edt_pass_zp<96, 64><<<(unsigned)((lz + 63) / 64), 64, 0, s>>>(pk, lz, dx, dy, dz, out);
         return ct::check_launch("edt_pass_zp");
     }
     auto kz = nz == 64 ? edt_pass_z<64> : nz == 32 ? edt_pass_z<32> : nz == 128 ? edt_pass_z<128> : edt_pass_z<0>;

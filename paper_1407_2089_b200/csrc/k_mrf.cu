@@ -680,7 +680,18 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
         const uint32_t ll = __vsub2(sl, (c & m16) * 6u), lh = __vsub2(sh, ((c >> 8) & m16) * 6u);
         // voxel b's Laplacian: b0 = ll.lo, b1 = lh.lo, b2 = ll.hi, b3 = lh.hi
         const uint32_t w01 = __byte_perm(ll, lh, 0x5410), w23 = __byte_perm(ll, lh, 0x7632);
-        const uint32_t nb0 = __shfl_down_sync(0xffffffffu, w01 & 0xffffu, 1);  // next word's b0
+        // next word's b0 (voxel k = 4 kw + 4): from the neighbour lane when rows
+        // are whole within warps, else recomputed from the ring (slot fs holds plane i-1)
+        uint32_t nb0;
+        if constexpr (32 % W == 0) {
+            nb0 = __shfl_down_sync(0xffffffffu, w01 & 0xffffu, 1);
+        } else {
+            const int o1 = kw < W - 1 ? o + 1 : o;
+            const int c1 = (int)(ring[cs][o1] & 0xffu);
+            const int s6 = (int)(ring[fs][o1] & 0xffu) + (int)(ring[ns][o1] & 0xffu) + (int)(ring[cs][o1 - W] & 0xffu) +
+                           (int)(ring[cs][o1 + W] & 0xffu) + (int)(c >> 24) + (int)((ring[cs][o1] >> 8) & 0xffu);
+            nb0 = (uint32_t)(s6 - 6 * c1) & 0xffffu;
+        }
         if (jin) {
             nnz += __popc(__vcmpne4(pos, neg)) >> 3;
             atomicAdd(&wh[c & 0xff], 1u);

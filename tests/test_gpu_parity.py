@@ -396,7 +396,7 @@ def test_gpu_voxel_runs_c2_properties(cuda):
     assert runs[:, 3].sum() == vox.shape[0]
 
 
-@pytest.mark.parametrize("shape", [(24, 40, 64), (16, 24, 32), (12, 20, 128), (10, 12, 70)])
+@pytest.mark.parametrize("shape", [(24, 40, 64), (16, 24, 32), (12, 20, 128), (10, 12, 70), (14, 18, 96)])
 def test_specialised_kernel_paths_vs_oracle(cuda, oracle, shape):
     """nz-specialised kernels (SIMD MRF stream for nz in {32, 64, 128}, run-based
     CCL with the vectorised row pack for nz == 64, packed EDT pass z for
