@@ -472,9 +472,13 @@ __global__ void __launch_bounds__(ZLN) edt_pass_zp(const int32_t *__restrict__ i
     const double d2 = __dmul_rn(dz, dz);
     int K = 0, tp = 0, bp = 0;
     double tg = 0.0, bg = 0.0;
+    int32_t pcur = P[0];
     for (int x = 0; x < NZ; ++x) {
-        if (P[x] == NONE32) continue;
-        const double gx = G(x);
+        const int32_t pnx = x + 1 < NZ ? P[x + 1] : NONE32;  // next element in flight
+        const int32_t px = pcur;
+        pcur = pnx;
+        if (px == NONE32) continue;
+        const double gx = gyz(px, dx, dy);
         while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
             --K;
             tp = bp;
