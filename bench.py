@@ -63,7 +63,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -71,7 +71,16 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def wait_first(self, keep_busy, timeout=10.0):
+        """Keep the GPU busy (untimed) until nvidia-smi has produced a sample."""
+        t_end = time.monotonic() + timeout
+        while self.proc and not self.lines and time.monotonic() < t_end:
+            keep_busy()
+
+    def mark(self, which):
+        setattr(self, which, time.monotonic())
 
     def stop(self):
         if not self.proc:
@@ -83,7 +92,10 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        # samples inside the timed window (plus one sampling period either side)
+        inside = [ln for t, ln in self.lines if t0 is None or t0 - 0.025 <= t <= t1 + 0.025]
+        for ln in inside:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -202,7 +214,7 @@ def run_ours(args):
     gathered = torch.zeros(world, dtype=torch.int64, device=dev)
     torch.cuda.synchronize()
 
-    def step(i, timing=False):
+    def step(i, timing=False, coll=True):
         t, rc, rv = inputs[i % ring]
         main = torch.cuda.current_stream()
         s_cell.wait_stream(main)
@@ -214,7 +226,7 @@ def run_ours(args):
             pipe.vessel(rv)
         main.wait_stream(s_cell)
         main.wait_stream(s_vess)
-        if world > 1:
+        if world > 1 and coll:
             # the frame's detection count (global ids) and its per-cell records, over NCCL
             dist.all_gather_into_tensor(gathered, counts_dev)
             gather_tables(pipe.table, pipe.counters[2], max_rows=GATHER_ROWS)
@@ -230,15 +242,21 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.wait_first(lambda: (step(0, coll=False), torch.cuda.synchronize()))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     _lib.launch_counter.update(enabled=True, count=0)
     pipe.marks = []
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark("t0")
     e0.record()
     for i in range(args.steps):
         step(args.warmup + i)
     e1.record()
     torch.cuda.synchronize()
+    clocks.mark("t1")
     _lib.launch_counter["enabled"] = False
     launches = _lib.launch_counter["count"]
     clk = clocks.stop()
@@ -517,7 +535,7 @@ def run_materialized(args, pipe, spec, dev, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=None, help="default 200 (ours), 20 (--impl reference)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ring", type=int, default=6)
@@ -528,6 +546,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.steps is None:
+        args.steps = 20 if args.impl == "reference" else 200
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
