@@ -434,13 +434,25 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
 
 // Same pass with the packed (dj, di) offsets kept in SMEM instead of the
 // float64 costs (costs recomputed on use by gyz, same operations): 4 + 1
-// bytes per element instead of 8 + 1, so ~1.8x more lines per SM.
+// bytes per element instead of 8 + 1, so ~1.8x more lines per SM.  Split in
+// two phases: (1) one thread per line builds the envelope and sweeps it,
+// writing only the chosen feature position per voxel (u8, SMEM); (2) all
+// threads form the float64 distances voxel-parallel -- the correctly rounded
+// sqrt off the sequential chain, stores coalesced along k.
+template <int NZ, int ZLN>
+constexpr size_t zp_smem() {
+    return (size_t)ZLN * (NZ + 1) * 4 + 2 * (size_t)ZLN * (NZ + 4);
+}
+
 template <int NZ, int ZLN = ZL>  // ZLN lines per CTA
 __global__ void __launch_bounds__(ZLN) edt_pass_zp(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
                                                   double dz, double *__restrict__ out) {
-    constexpr int S = NZ + 1;  // padded line stride (conflict-free)
-    __shared__ int32_t ps[ZLN * S];
-    __shared__ uint8_t stk[ZLN * NZ];
+    constexpr int S = NZ + 1;   // padded line stride (conflict-free)
+    constexpr int SB = NZ + 4;  // byte rows: 4-byte pad keeps per-thread rows in distinct banks
+    extern __shared__ __align__(16) unsigned char zsm[];
+    int32_t *ps = (int32_t *)zsm;
+    uint8_t *stk = zsm + (size_t)ZLN * S * 4;
+    uint8_t *fid = stk + ZLN * SB;
 
     const i64 l0 = blockIdx.x * (i64)ZLN;
     const int nl = (int)min((i64)ZLN, nlines - l0);
@@ -464,55 +476,70 @@ __global__ void __launch_bounds__(ZLN) edt_pass_zp(const int32_t *__restrict__ i
         }
     }
     __syncthreads();
-    const int t = threadIdx.x;
-    if (t >= nl) return;
-    const int32_t *P = ps + t * S;
-    auto G = [&](int x) -> double { const int32_t pl = P[x]; return pl == NONE32 ? INFINITY : gyz(pl, dx, dy); };
-    uint8_t *st = stk + t * NZ;
     const double d2 = __dmul_rn(dz, dz);
-    int K = 0, tp = 0, bp = 0;
-    double tg = 0.0, bg = 0.0;
-    int32_t pcur = P[0];
-    for (int x = 0; x < NZ; ++x) {
-        const int32_t pnx = x + 1 < NZ ? P[x + 1] : NONE32;  // next element in flight
-        const int32_t px = pcur;
-        pcur = pnx;
-        if (px == NONE32) continue;
-        const double gx = gyz(px, dx, dy);
-        while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-            --K;
-            tp = bp;
-            tg = bg;
-            if (K >= 2) {
-                bp = st[K - 2];
-                bg = G(bp);
+    const int t = threadIdx.x;
+    if (t < nl) {
+        const int32_t *P = ps + t * S;
+        auto G = [&](int x) -> double { return gyz(P[x], dx, dy); };
+        uint8_t *st = stk + t * SB;
+        uint8_t *fo = fid + t * SB;
+        int K = 0, tp = 0, bp = 0;
+        double tg = 0.0, bg = 0.0;
+        int32_t pcur = P[0];
+        for (int x = 0; x < NZ; ++x) {
+            const int32_t pnx = x + 1 < NZ ? P[x + 1] : NONE32;  // next element in flight
+            const int32_t px = pcur;
+            pcur = pnx;
+            if (px == NONE32) continue;
+            const double gx = gyz(px, dx, dy);
+            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+                --K;
+                tp = bp;
+                tg = bg;
+                if (K >= 2) {
+                    bp = st[K - 2];
+                    bg = G(bp);
+                }
+            }
+            st[K++] = (uint8_t)x;
+            bp = tp; bg = tg; tp = x; tg = gx;
+        }
+        if (K == 0) {
+            for (int x = 0; x < NZ; ++x) fo[x] = 255;
+        } else {
+            int e = 0;
+            int cp = st[0], np = K > 1 ? st[1] : 0;
+            double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
+            {  // jump to each switch point
+                int sw = K > 1 ? first_past(0, NZ, np, ng, cp, cg, d2) : NZ;
+                int x = 0;
+                for (;;) {
+                    for (; x < sw; ++x) fo[x] = (uint8_t)cp;
+                    if (x >= NZ) break;
+                    ++e;
+                    cp = np; cg = ng;
+                    if (e + 1 < K) {
+                        np = st[e + 1];
+                        ng = G(np);
+                        sw = first_past(x, NZ, np, ng, cp, cg, d2);
+                    } else {
+                        sw = NZ;
+                    }
+                }
             }
         }
-        st[K++] = (uint8_t)x;
-        bp = tp; bg = tg; tp = x; tg = gx;
     }
-    double *dst = out + (l0 + t) * NZ;
-    if (K == 0) {
-        for (int x = 0; x < NZ; ++x) dst[x] = INFINITY;
-        return;
-    }
-    int e = 0;
-    int cp = st[0], np = K > 1 ? st[1] : 0;
-    double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
-    int sw = K > 1 ? first_past(0, NZ, np, ng, cp, cg, d2) : NZ;  // envelope moves past cp at x = sw
-    for (int x = 0; x < NZ; ++x) {
-        while (x >= sw) {
-            ++e;
-            cp = np; cg = ng;
-            if (e + 1 < K) {
-                np = st[e + 1];
-                ng = G(np);
-                sw = first_past(x, NZ, np, ng, cp, cg, d2);
-            } else {
-                sw = NZ;
-            }
-        }
-        dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
+    __syncthreads();
+    // phase 2: voxel-parallel distances, warp-contiguous along k
+    double *dst = out + l0 * NZ;
+    const int tot = nl * NZ;
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < tot; idx += ZLN) {
+        const int g = idx / NZ, x = idx - g * NZ;
+        const int f = fid[g * SB + x];
+        double r = INFINITY;
+        if (f != 255) r = __dsqrt_rn(__dadd_rn(gyz(ps[g * S + f], dx, dy), sq(__dmul_rn((double)(f - x), dz))));
+        dst[idx] = r;
     }
 }
 
@@ -559,9 +586,13 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     if (int st = ct::check_launch("edt_pass_y")) return st;
     const size_t sm = zsmem((int)nz);
     if ((nz == 64 || nz == 32 || nz == 96) && ((uintptr_t)pk & 15) == 0) {
-        if (nz == 64) edt_pass_zp<64><<<(unsigned)((lz + ZL - 1) / ZL), ZL, 0, s>>>(pk, lz, dx, dy, dz, out);
-        else if (nz == 32) edt_pass_zp<32><<<(unsigned)((lz + ZL - 1) / ZL), ZL, 0, s>>>(pk, lz, dx, dy, dz, out);
-        else edt_pass_zp<96, 64><<<(unsigned)((lz + 63) / 64), 64, 0, s>>>(pk, lz, dx, dy, dz, out);
+        auto launch = [&](auto kern, int zln, size_t smem) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kern<<<(unsigned)((lz + zln - 1) / zln), zln, smem, s>>>(pk, lz, dx, dy, dz, out);
+        };
+        if (nz == 64) launch(edt_pass_zp<64, ZL>, ZL, zp_smem<64, ZL>());
+        else if (nz == 32) launch(edt_pass_zp<32, ZL>, ZL, zp_smem<32, ZL>());
+        else launch(edt_pass_zp<96, 64>, 64, zp_smem<96, 64>());
         return ct::check_launch("edt_pass_zp");
     }
     auto kz = nz == 64 ? edt_pass_z<64> : nz == 32 ? edt_pass_z<32> : nz == 128 ? edt_pass_z<128> : edt_pass_z<0>;
