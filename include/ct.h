@@ -43,6 +43,8 @@ extern "C" {
 #define CT_ERR_PARAM 1       /* ParameterError (ref errors.py:16)              */
 #define CT_ERR_CUDA 3        /* CUDA launch/runtime failure                    */
 #define CT_ERR_UNSUPPORTED 4 /* dtype / size outside what a kernel supports    */
+#define CT_ERR_IO 5          /* unreadable / unsupported image file: ManifestError
+                              * "failed to read image" (ref imaging.py:213-216) */
 
 /* ct_otsu result words (int64, device): */
 #define CT_OTSU_T 0        /* threshold t (segment.py:150)                      */
@@ -225,6 +227,41 @@ int ct_fp64_peak(double *out, int iters, void *stream);
 int ct_synth_frame(void *out, int dtype, int64_t nx, int64_t ny, int64_t nz, uint64_t seed, int64_t vmax,
                    const int64_t *balls, int64_t n_balls, int64_t amp_ball, const int64_t *tubes,
                    int64_t n_tubes, int64_t amp_tube, void *stream);
+
+/* ---- Ingest ------------------------------------------
+ * ref imaging.py:211-220 load_tiff_volume = tifffile.imread (pages z, rows y,
+ * samples x) + a host transpose to (x, y, z); ref imaging.py:232-240
+ * save_grid = tifffile.imwrite of the (z, y, x) transpose.  Here the host
+ * moves page bytes only (ct_tiff_read, multi-threaded pread into caller
+ * memory, normally pinned) and the transpose runs on the device after the
+ * H2D copy (ct_transpose_xz).  Reader: classic/BigTIFF, II/MM, uncompressed
+ * strips, 1 sample of 8/16/32/64 bits, equal pages. */
+typedef struct ct_tiff_info {
+    int64_t nx, ny, nz;       /* page width, page height, pages              */
+    int32_t bytes_per_sample; /* 1, 2, 4, 8                                   */
+    int32_t sample_format;    /* 1 uint, 2 int, 3 float (TIFF SampleFormat)   */
+    int32_t big_endian;       /* 1: samples are big-endian in the file (MM)   */
+    int32_t reserved;
+    int64_t segments;         /* contiguous file ranges the pages occupy      */
+} ct_tiff_info;
+
+/* Parse the IFD chain; *handle stays valid until ct_tiff_close.
+ * CT_ERR_IO (message names the file) for anything unreadable. */
+int ct_tiff_open(const char *path, ct_tiff_info *info, void **handle);
+/* All pages, (z, y, x) order, file byte order, into dst (>= nx*ny*nz*bps
+ * bytes) with nthreads concurrent preads. */
+int ct_tiff_read(void *handle, void *dst, int64_t dst_bytes, int32_t nthreads);
+void ct_tiff_close(void *handle);
+/* Write a (z, y, x) stack as a little-endian multi-page TIFF (one strip per
+ * page, ImageDescription {"shape": [nz, ny, nx]}, BigTIFF past 4 GiB). */
+int ct_tiff_write(const char *path, const void *src_zyx, int64_t nx, int64_t ny, int64_t nz,
+                  int32_t bytes_per_sample, int32_t sample_format);
+/* Device: dst[c][b][a] = src[a][b][c] for an (na, nb, nc) C-order array of
+ * elem_bytes-wide elements (1, 2, 4, 8), optionally byte-swapping each
+ * element (big-endian files).  (nz, ny, nx) pages -> (nx, ny, nz) grid with
+ * (na, nb, nc) = (nz, ny, nx), and back with (nx, ny, nz). */
+int ct_transpose_xz(const void *src, void *dst, int64_t na, int64_t nb, int64_t nc, int32_t elem_bytes,
+                    int32_t byteswap, void *stream);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ from .errors import (
     ManifestError,
     ParameterError,
 )
-from .imaging import VoxelGrid, VoxelSpacing, physical_coordinates
+from .imaging import VoxelGrid, VoxelSpacing, load_tiff_volume, physical_coordinates, save_grid
 from .segment import (
     Detection,
     DistanceMap,
@@ -43,7 +43,9 @@ __all__ = [
     "denoise_cell_channel",
     "mrf_denoise",
     "mrf_denoise_state",
+    "load_tiff_volume",
     "physical_coordinates",
+    "save_grid",
     "segment_cell_channel",
     "segment_vessel_channel",
 ]

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libct.so")
 
 CT_U8, CT_U16, CT_I32, CT_F64 = 1, 2, 4, 8
-CT_OK, CT_ERR_PARAM, CT_ERR_CUDA, CT_ERR_UNSUPPORTED = 0, 1, 3, 4
+CT_OK, CT_ERR_PARAM, CT_ERR_CUDA, CT_ERR_UNSUPPORTED, CT_ERR_IO = 0, 1, 3, 4, 5
 
 # result / counter word indices (ct.h)
 OTSU_T, OTSU_STATUS, OTSU_NBINS, OTSU_NONZERO = 0, 1, 2, 3
@@ -81,6 +81,31 @@ SIGNATURES = {
     "ct_synth_frame": (_INT, [_P, _INT, _I64, _I64, _I64, _U64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P]),
 }
 
+
+
+class TiffInfo(ctypes.Structure):
+    """ct_tiff_info (include/ct.h)."""
+
+    _fields_ = [
+        ("nx", ctypes.c_int64),
+        ("ny", ctypes.c_int64),
+        ("nz", ctypes.c_int64),
+        ("bytes_per_sample", ctypes.c_int32),
+        ("sample_format", ctypes.c_int32),
+        ("big_endian", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("segments", ctypes.c_int64),
+    ]
+
+
+SIGNATURES.update({
+    "ct_tiff_open": (_INT, [ctypes.c_char_p, ctypes.POINTER(TiffInfo), ctypes.POINTER(ctypes.c_void_p)]),
+    "ct_tiff_read": (_INT, [_P, _P, _I64, ctypes.c_int32]),
+    "ct_tiff_close": (None, [_P]),
+    "ct_tiff_write": (_INT, [ctypes.c_char_p, _P, _I64, _I64, _I64, ctypes.c_int32, ctypes.c_int32]),
+    "ct_transpose_xz": (_INT, [_P, _P, _I64, _I64, _I64, ctypes.c_int32, ctypes.c_int32, _P]),
+})
+
 _lib = None
 
 
@@ -131,6 +156,10 @@ def call(name: str, *args) -> None:
     msg = lib().ct_last_error().decode(errors="replace")
     if st == CT_ERR_PARAM:
         raise ParameterError(msg)
+    if st == CT_ERR_IO:
+        from .errors import ManifestError
+
+        raise ManifestError(msg)
     raise LibctError(f"{name} failed ({st}): {msg}")
 
 

@@ -70,3 +70,18 @@ class VoxelGrid:
 def physical_coordinates(voxels: np.ndarray, spacing: VoxelSpacing) -> np.ndarray:
     """Voxel-centre positions in micrometres for an (n, 3) index array."""
     return np.asarray(voxels, dtype=np.float64) * spacing.as_array()
+
+
+def load_tiff_volume(path, device=None, threads: int = 8):
+    """ref imaging.py:211-220 -- see ingest.load_tiff_volume (pread of the page
+    bytes on the host, (z, y, x) -> (x, y, z) transpose on the device)."""
+    from .ingest import load_tiff_volume as _load
+
+    return _load(path, device=device, threads=threads)
+
+
+def save_grid(grid: VoxelGrid, path) -> None:
+    """ref imaging.py:232-240 -- see ingest.save_grid."""
+    from .ingest import save_grid as _save
+
+    _save(grid, path)
