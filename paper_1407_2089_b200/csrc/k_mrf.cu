@@ -27,6 +27,10 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
 #include "ct_common.cuh"
 
 namespace {
@@ -365,6 +369,196 @@ int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s
     if (int st = ct::check_launch("pw_subtree")) return st;
     pw_fold<<<1, 1024, 0, s>>>(partial, D, out);
     return ct::check_launch("pw_fold");
+}
+
+// ---------------------------------------------------------------------------
+// Vectorised numpy-order sum of (lap - mean)^2 over the Laplacian array.
+// Same tree as pw_subtree, but each leaf (<= 128 elements, 8-aligned) is one
+// thread: numpy's 8 accumulators are 8 independent FP64 chains fed by 16-byte
+// loads, and the in-subtree combine follows a host-built schedule (internal
+// nodes grouped by height, so every group is independent) instead of
+// per-thread tree descents.
+// ---------------------------------------------------------------------------
+constexpr int PWV_SUB = 8192;   // nodes at depth D hold >= 8192 elements
+constexpr int PWV_LEAVES = 256; // leaves per subtree (sizes < 2*PWV_SUB + 16)
+constexpr int PWV_NSH = 4;
+constexpr int PWV_MAXH = 16;
+constexpr int PWV_T = 128;
+
+struct PwvTabs {
+    int count;
+    int len[PWV_NSH], nleaves[PWV_NSH], nh[PWV_NSH];
+    int hstart[PWV_NSH][PWV_MAXH + 1];       // internal nodes of height h: [hstart[h-1], hstart[h])
+    uint32_t leaf[PWV_NSH][PWV_LEAVES];      // offset << 8 | length
+    uint32_t node[PWV_NSH][PWV_LEAVES];      // left | right << 16 (indices into leaves ++ nodes)
+};
+
+inline int pwv_depth(i64 n) {
+    int d = 0;
+    i64 m = n;
+    while (m > 128 && pw_left(m) >= PWV_SUB && d < 24) {
+        m = pw_left(m);
+        ++d;
+    }
+    return d;
+}
+
+// builds node m at offset off; returns (value index, height)
+inline bool pwv_build(PwvTabs &t, int q, int m, int off, std::vector<std::pair<int, int>> &nodes,
+                      std::vector<int> &heights, int &idx, int &h) {
+    if (m <= 128) {
+        if (t.nleaves[q] >= PWV_LEAVES) return false;
+        t.leaf[q][t.nleaves[q]] = ((uint32_t)off << 8) | (uint32_t)m;
+        idx = t.nleaves[q]++;
+        h = 0;
+        return true;
+    }
+    const int l = (int)pw_left(m);
+    int ia, ha, ib, hb;
+    if (!pwv_build(t, q, l, off, nodes, heights, ia, ha) || !pwv_build(t, q, m - l, off + l, nodes, heights, ib, hb))
+        return false;
+    nodes.push_back({ia, ib});
+    h = (ha > hb ? ha : hb) + 1;
+    heights.push_back(h);
+    idx = -(int)nodes.size();  // internal: resolved after sorting
+    return true;
+}
+
+inline bool pwv_table(PwvTabs &t, int q, int len) {
+    t.len[q] = len;
+    t.nleaves[q] = 0;
+    std::vector<std::pair<int, int>> nodes;
+    std::vector<int> heights;
+    int idx, h;
+    if (!pwv_build(t, q, len, 0, nodes, heights, idx, h) || h > PWV_MAXH) return false;
+    const int nl = t.nleaves[q], ni = (int)nodes.size();
+    // order internal nodes by height; value index of internal node = nl + position
+    std::vector<int> order(ni), pos(ni);
+    for (int i = 0; i < ni; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return heights[a] < heights[b]; });
+    for (int i = 0; i < ni; ++i) pos[order[i]] = i;
+    auto vidx = [&](int v) { return v >= 0 ? v : nl + pos[-v - 1]; };
+    t.nh[q] = h;
+    for (int hh = 0; hh <= PWV_MAXH; ++hh) t.hstart[q][hh] = 0;
+    for (int i = 0; i < ni; ++i) {
+        const int n = order[i];
+        t.node[q][i] = (uint32_t)vidx(nodes[n].first) | ((uint32_t)vidx(nodes[n].second) << 16);
+        t.hstart[q][heights[n]] = i + 1;
+    }
+    for (int hh = 1; hh <= h; ++hh)
+        if (t.hstart[q][hh] < t.hstart[q][hh - 1]) t.hstart[q][hh] = t.hstart[q][hh - 1];
+    return true;
+}
+
+template <typename LT>
+__device__ __forceinline__ void load8(const LT *p, double (&x)[8]);
+template <>
+__device__ __forceinline__ void load8<int16_t>(const int16_t *p, double (&x)[8]) {
+    const int4 v = __ldg((const int4 *)p);
+    const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        x[2 * i] = (double)(int16_t)(w[i] & 0xffff);
+        x[2 * i + 1] = (double)(int16_t)(w[i] >> 16);
+    }
+}
+template <>
+__device__ __forceinline__ void load8<int32_t>(const int32_t *p, double (&x)[8]) {
+    const int4 a = __ldg((const int4 *)p), b = __ldg((const int4 *)p + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+}
+
+template <typename LT>
+__global__ void __launch_bounds__(PWV_T) pw_subtree_lap(const LT *__restrict__ lap, const double *__restrict__ meanp,
+                                                        i64 n, int D, double *__restrict__ partial,
+                                                        const __grid_constant__ PwvTabs tabs) {
+    __shared__ double val[2 * PWV_LEAVES];
+    i64 off, len;
+    pw_node(n, D, blockIdx.x, off, len);
+    int q = 0;
+    for (int i = 1; i < tabs.count; ++i)
+        if (tabs.len[i] == (int)len) q = i;
+    const double mean = *meanp;
+    const int nl = tabs.nleaves[q];
+    auto sq = [&](double x) { const double d = __dadd_rn(x, -mean); return __dmul_rn(d, d); };
+    for (int L = threadIdx.x; L < nl; L += PWV_T) {
+        const uint32_t e = tabs.leaf[q][L];
+        const int m = (int)(e & 0xff);
+        const LT *a = lap + off + (e >> 8);
+        double res;
+        if (m < 8) {
+            res = 0.0;
+            for (int i = 0; i < m; ++i) res = __dadd_rn(res, sq((double)a[i]));
+        } else {
+            double r[8], x[8];
+            load8<LT>(a, x);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = sq(x[j]);
+            const int lim = m - (m & 7);
+            for (int i = 8; i < lim; i += 8) {
+                load8<LT>(a + i, x);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sq(x[j]));
+            }
+            res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            for (int i = lim; i < m; ++i) res = __dadd_rn(res, sq((double)a[i]));
+        }
+        val[L] = res;
+    }
+    for (int h = 1; h <= tabs.nh[q]; ++h) {
+        __syncthreads();
+        for (int i = tabs.hstart[q][h - 1] + threadIdx.x; i < tabs.hstart[q][h]; i += PWV_T) {
+            const uint32_t nd = tabs.node[q][i];
+            val[nl + i] = __dadd_rn(val[nd & 0xffff], val[nd >> 16]);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) partial[blockIdx.x] = nl > 1 ? val[nl + tabs.hstart[q][tabs.nh[q]] - 1] : val[0];
+}
+
+// returns 1 when the shapes do not fit the tables (caller falls back)
+template <typename LT>
+int pairwise_sum_lap(const LT *lap, const double *mean, i64 n, double *partial, double *out, cudaStream_t s) {
+    if (n < 8 || ((uintptr_t)lap & 15) != 0 || n >= (1ll << 31)) return 1;
+    const int D = pwv_depth(n);
+    static thread_local i64 cached_n = -1;
+    static thread_local PwvTabs tabs;
+    static thread_local bool ok = false;
+    if (cached_n != n) {
+        cached_n = n;
+        ok = true;
+        i64 sizes[64];
+        int ns = 1;
+        sizes[0] = n;
+        for (int d = 0; d < D && ok; ++d) {
+            i64 nxt[64];
+            int nn = 0;
+            for (int i = 0; i < ns; ++i) {
+                const i64 l = pw_left(sizes[i]), c2[2] = {l, sizes[i] - l};
+                for (int k = 0; k < 2; ++k) {
+                    bool seen = false;
+                    for (int u = 0; u < nn; ++u) seen |= nxt[u] == c2[k];
+                    if (!seen) {
+                        if (nn == 64) { ok = false; break; }
+                        nxt[nn++] = c2[k];
+                    }
+                }
+            }
+            ns = nn;
+            for (int i = 0; i < ns; ++i) sizes[i] = nxt[i];
+        }
+        if (ns > PWV_NSH || sizes[0] >= (1 << 23)) ok = false;
+        tabs.count = ns;
+        for (int i = 0; i < ns && ok; ++i) ok = pwv_table(tabs, i, (int)sizes[i]);
+    }
+    if (!ok) return 1;
+    pw_subtree_lap<LT><<<(unsigned)(1ll << D), PWV_T, 0, s>>>(lap, mean, n, D, partial, tabs);
+    if (int st = ct::check_launch("pw_subtree_lap")) return -st;
+    pw_fold<<<1, 1024, 0, s>>>(partial, D, out);
+    if (int st = ct::check_launch("pw_fold")) return -st;
+    return 0;
 }
 
 // state words
@@ -926,8 +1120,13 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
     if (int st = ct::check_launch("delta_from_hist")) return st;
     if (ni >= 2) {
         lap_mean<<<1, 1, 0, s>>>(state, (const long long *)&w.scal[W_LAPSUM], ni);
-        LapArrSq<LT> f{lap, &state[S_SUM1]};
-        if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s)) return st;
+        static const bool scalar_pw = getenv("CT_PW_SCALAR") != nullptr;
+        const int vs = scalar_pw ? 1 : pairwise_sum_lap<LT>(lap, &state[S_SUM1], ni, w.partial, &state[S_SUM2], s);
+        if (vs < 0) return -vs;
+        if (vs == 1) {
+            LapArrSq<LT> f{lap, &state[S_SUM1]};
+            if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s)) return st;
+        }
     }
     mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 1);
     return ct::check_launch("mrf_decide");

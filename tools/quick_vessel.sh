@@ -1,7 +1,7 @@
 #!/bin/bash
 # GPU quick loop for the vessel channel: parity subset, then an ncu launch list
 # per value of the variant knob named in $1 (values in $2, e.g. "0 1").
-python -m pytest tests -m gpu -x -q -k "edt or vessel or specialised or distance" > gpurun_out/qv_tests.log 2>&1 || { tail -30 gpurun_out/qv_tests.log; exit 1; }
+python -m pytest tests -m gpu -x -q -k "${QV_K:-edt or vessel or specialised or distance or mrf or noise}" > gpurun_out/qv_tests.log 2>&1 || { tail -30 gpurun_out/qv_tests.log; exit 1; }
 tail -1 gpurun_out/qv_tests.log
 knob=${1:-CT_NONE}
 for v in ${2:-0}; do
