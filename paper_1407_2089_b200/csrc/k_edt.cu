@@ -339,6 +339,149 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
 }
 
 // ---------------------------------------------------------------------------
+// pass y in two kernels (parallelism: only nx*nz lines exist, too few threads
+// for one-thread-per-line sweeps of ny outputs):
+//   build  : thread per line (64-thread CTAs spread the lines evenly over the
+//            SMs), loads PFB deep with compile-time strides; the envelope
+//            stack (first SC entries in SMEM, the rest in the spill buffer) is
+//            published to global, the switch points sw_e = first_past(sw_{e-1},
+//            ...) -- exactly where the one-kernel sweep switches -- go to swh
+//            (e-major) / over the line's consumed di entries, and est[s] = the
+//            entry in force where output segment s starts.
+//   output : YS threads per line, each starts at est[s] and sweeps its x
+//            range with coalesced row stores.
+// (Tried: YB scanners per line compacting the sparse sites into SMEM before a
+// single-thread envelope, with the switch points in parallel -- slower: the
+// envelope thread then runs in 2 of 16 warps.)
+// ---------------------------------------------------------------------------
+constexpr int PFB = 16;  // build prefetch depth
+constexpr int LTB = 64;  // build CTA size: small CTAs spread the nx*nz lines evenly over the SMs
+constexpr int YS = 8;    // output segments per line
+
+template <int NZ>
+__global__ void __launch_bounds__(LTB) edt_y_build(int16_t *__restrict__ di, i64 nlines, int ny, int nz_, double dx,
+                                                  double dy, uint32_t *__restrict__ head,
+                                                  uint32_t *__restrict__ spill, int32_t *__restrict__ kc,
+                                                  int16_t *__restrict__ swh, int16_t *__restrict__ est) {
+    __shared__ uint32_t stk[SC][LTB];
+    const int nz = NZ > 0 ? NZ : nz_;
+    const i64 l = blockIdx.x * (i64)LTB + threadIdx.x;
+    const unsigned wm = __ballot_sync(0xffffffffu, l < nlines);
+    if (l >= nlines) return;
+    int16_t *line = di + (l / nz) * (i64)ny * nz + (l % nz);
+    const double d2 = __dmul_rn(dy, dy);
+    auto ent_ld = [&](int e) -> uint32_t { return e < SC ? stk[e][threadIdx.x] : spill[(i64)(e - SC) * nlines + l]; };
+    auto ent_st = [&](int e, uint32_t v) {
+        if (e < SC) stk[e][threadIdx.x] = v;
+        else spill[(i64)(e - SC) * nlines + l] = v;
+    };
+#define GOF(pl) sq(__dmul_rn((double)(int16_t)(pl), dx))
+    int K = 0, tp = 0, bp = 0;
+    double tg = 0.0, bg = 0.0;
+    for (int x0 = 0; x0 < ny; x0 += PFB) {
+        int16_t v[PFB];
+        __syncwarp(wm);
+        const int16_t *p = line + (i64)x0 * nz;
+        if (x0 + PFB <= ny) {
+#pragma unroll
+            for (int u = 0; u < PFB; ++u) v[u] = __ldg(p + u * nz);
+        } else {
+#pragma unroll
+            for (int u = 0; u < PFB; ++u) v[u] = x0 + u < ny ? __ldg(p + u * nz) : NONE16;
+        }
+#pragma unroll
+        for (int u = 0; u < PFB; ++u) {
+            if (v[u] == NONE16) continue;
+            const int x = x0 + u;
+            const double gx = GOF(v[u]);
+            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+                --K;
+                tp = bp;
+                tg = bg;
+                if (K >= 2) {
+                    const uint32_t e = ent_ld(K - 2);
+                    bp = (int)(e >> 16);
+                    bg = GOF(e & 0xffff);
+                }
+            }
+            ent_st(K, ((uint32_t)x << 16) | (uint16_t)v[u]);
+            bp = tp; bg = tg; tp = x; tg = gx;
+            ++K;
+        }
+    }
+    kc[l] = K;
+    for (int e = 0; e < K && e < SC; ++e) head[(i64)e * nlines + l] = stk[e][threadIdx.x];
+    // switch points: the envelope moves past entry e at x = sw_e (nondecreasing).
+    // Entries < SC go to swh (e-major, coalesced across lines), the rest over
+    // the line's own (already consumed) di entries.  est[s] = envelope entry
+    // in force at the first x of output segment s.
+    int s_next = 1, xs_next = (int)((i64)ny / YS);
+    est[l] = 0;
+    if (K > 1) {
+        uint32_t c = ent_ld(0);
+        int cp = (int)(c >> 16);
+        double cg = GOF(c & 0xffff);
+        int sw = 0;
+        for (int e = 0; e + 1 < K; ++e) {
+            const uint32_t nxt = ent_ld(e + 1);
+            const int np = (int)(nxt >> 16);
+            const double ng = GOF(nxt & 0xffff);
+            sw = first_past(sw, ny, np, ng, cp, cg, d2);
+            if (e < SC) swh[(i64)e * nlines + l] = (int16_t)sw;
+            else line[(i64)e * nz] = (int16_t)sw;
+            while (s_next < YS && xs_next < sw) {  // segments starting before sw keep entry e
+                est[(i64)s_next * nlines + l] = (int16_t)e;
+                ++s_next;
+                xs_next = (int)((i64)ny * s_next / YS);
+            }
+            cp = np;
+            cg = ng;
+        }
+    }
+    for (; s_next < YS; ++s_next) est[(i64)s_next * nlines + l] = (int16_t)(K > 0 ? K - 1 : 0);
+#undef GOF
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(LT) edt_y_out(const int16_t *__restrict__ swa, i64 nlines, int ny, int nz_,
+                                                const uint32_t *__restrict__ head, const uint32_t *__restrict__ spill,
+                                                const int32_t *__restrict__ kc, const int16_t *__restrict__ swh,
+                                                const int16_t *__restrict__ est, int32_t *__restrict__ out) {
+    const int nz = NZ > 0 ? NZ : nz_;
+    const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
+    const unsigned wm = __ballot_sync(0xffffffffu, l < nlines);
+    if (l >= nlines) return;
+    const int seg = blockIdx.y;
+    const int x0 = (int)((i64)ny * seg / YS), x1 = (int)((i64)ny * (seg + 1) / YS);
+    const i64 base = (l / nz) * (i64)ny * nz + (l % nz);
+    const int16_t *sw = swa + base;
+    int32_t *o = out + base + (i64)x0 * nz;
+    const int K = kc[l];
+    auto ent = [&](int e) -> uint32_t { return e < SC ? head[(i64)e * nlines + l] : spill[(i64)(e - SC) * nlines + l]; };
+    auto swv = [&](int e) -> int { return e < SC ? (int)swh[(i64)e * nlines + l] : (int)sw[(i64)e * nz]; };
+    // lines without sites write NONE through the same (converged) loop
+    int e = K ? est[(i64)seg * nlines + l] : 0;
+    uint32_t c = K ? ent(e) : 0u;
+    int nsw = e + 1 < K ? swv(e) : ny;
+    const uint32_t step = K ? 1u << 16 : 0u;
+    // packed (dj, di) drops by 1 << 16 per step in x while the feature is fixed
+    uint32_t r = K ? (uint32_t)pack((int)(c >> 16) - x0, (int16_t)(c & 0xffff)) : (uint32_t)NONE32;
+    for (int x = x0; x < x1; ++x, o += nz) {
+        if (x >= nsw) {
+            do {
+                ++e;
+                nsw = e + 1 < K ? swv(e) : ny;
+            } while (x >= nsw);
+            c = ent(e);
+            r = (uint32_t)pack((int)(c >> 16) - x, (int16_t)(c & 0xffff));
+        }
+        __syncwarp(wm);  // lanes = consecutive k: keep the row store coalesced
+        *o = (int32_t)r;
+        r -= step;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // pass z: CTA = ZL consecutive (i,j) lines of nz <= 128 elements.
 //   phase 1 (all threads, coalesced): g = (di*dx)^2 + (dj*dy)^2 of every
 //            element into SMEM (+inf for no site);
@@ -553,7 +696,9 @@ inline size_t zsmem(int nz) {
 size_t ct_edt_workspace(int64_t nx, int64_t ny, int64_t nz) {
     const i64 N = nx * ny * nz;
     const i64 sp = YSEG * nx * nz * (ny > SC ? ny - SC : 0);  // pass-y spill entries (per segment)
-    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 4 + 4096;
+    const i64 ly = nx * nz;  // pass-y lines: published stack heads (SC each) + entry counts
+    return (((size_t)N * 2 + 255) & ~(size_t)255) + (((size_t)N * 4 + 255) & ~(size_t)255) + (size_t)sp * 4 +
+           (size_t)ly * (SC + 1) * 4 + (size_t)ly * (SC + YS) * 2 + 4096;
 }
 
 extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, double dx, double dy, double dz,
@@ -582,8 +727,23 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
     }
     if (int st = ct::check_launch("edt_pass_x")) return st;
-    edt_pass_y<<<dim3((unsigned)((ly + LT - 1) / LT), YSEG), LT, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, pk, spill);
-    if (int st = ct::check_launch("edt_pass_y")) return st;
+    static const bool y1 = getenv("CT_EDT_Y1") != nullptr;  // one-kernel pass y (A/B knob)
+    if (y1) {
+        edt_pass_y<<<dim3((unsigned)((ly + LT - 1) / LT), YSEG), LT, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, pk, spill);
+        if (int st = ct::check_launch("edt_pass_y")) return st;
+    } else {
+        uint32_t *head = spill + (size_t)YSEG * ly * (ny > SC ? ny - SC : 0);
+        int32_t *kc = (int32_t *)(head + (size_t)SC * ly);
+        int16_t *swh = (int16_t *)(kc + ly);
+        int16_t *est = swh + (size_t)SC * ly;
+        const unsigned gb = (unsigned)((ly + LT - 1) / LT);
+        auto yb = nz == 64 ? edt_y_build<64> : nz == 32 ? edt_y_build<32> : nz == 96 ? edt_y_build<96> : edt_y_build<0>;
+        auto yo = nz == 64 ? edt_y_out<64> : nz == 32 ? edt_y_out<32> : nz == 96 ? edt_y_out<96> : edt_y_out<0>;
+        yb<<<(unsigned)((ly + LTB - 1) / LTB), LTB, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, head, spill, kc, swh, est);
+        if (int st = ct::check_launch("edt_y_build")) return st;
+        yo<<<dim3(gb, YS), LT, 0, s>>>(di, ly, (int)ny, (int)nz, head, spill, kc, swh, est, pk);
+        if (int st = ct::check_launch("edt_y_out")) return st;
+    }
     const size_t sm = zsmem((int)nz);
     if ((nz == 64 || nz == 32 || nz == 96) && ((uintptr_t)pk & 15) == 0) {
         auto launch = [&](auto kern, int zln, size_t smem) {
