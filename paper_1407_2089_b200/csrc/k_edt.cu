@@ -23,6 +23,7 @@
 // oracle/ct_oracle.c ora_edt, so results match it bit for bit; equidistant
 // features may differ from scipy's choice in the last ulp, within the
 // reference's 1e-9 um contract (ref test_acceptance.py:318-332).
+#include <climits>
 #include <cstdlib>
 
 #include "ct_common.cuh"
@@ -62,9 +63,11 @@ __device__ __forceinline__ bool env_past(int x, int q, double gq, int p, double 
 // predicate is monotone in x (its right side is a rounded increasing function
 // of x), so a float estimate corrected by exact tests gives the same answer
 // as testing every x in turn.
+// The estimate is single precision (approximate reciprocal): a float64
+// division was the largest instruction block of the pass-z sweep.
 __device__ __forceinline__ int first_past(int xlo, int xhi, int q, double gq, int p, double gp, double d2) {
-    const double xs = 0.5 * ((gq - gp) / (d2 * (double)(q - p)) + (double)(q + p));
-    int x = xs < (double)xlo ? xlo : (xs >= (double)xhi ? xhi : (int)xs + 1);
+    const float xs = 0.5f * (__fdividef((float)(gq - gp), (float)d2 * (float)(q - p)) + (float)(q + p));
+    int x = !(xs >= (float)xlo) ? xlo : (xs >= (float)xhi ? xhi : (int)xs + 1);
     while (x > xlo && env_past(x - 1, q, gq, p, gp, d2)) --x;
     while (x < xhi && !env_past(x, q, gq, p, gp, d2)) ++x;
     return x;
@@ -248,6 +251,80 @@ __global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4(const uint8_t *__rest
     }
 }
 
+// Same pass, leaner per-row work (edt_pass_x_seg4 was ALU bound: two masks,
+// clz and ffs per voxel and line): the nearest foreground at or below the row
+// is carried forward (one bit test and select per voxel) and the nearest at or
+// above is recomputed by ffs only after the walk passes it, i.e. once per
+// foreground voxel.  Rows fully unrolled.
+__global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4b(const uint8_t *__restrict__ mask, i64 nlines, int nx,
+                                                            int16_t *__restrict__ di) {
+    __shared__ int segL[32][4 * XG + 1], segF[32][4 * XG + 1];
+    const int c = threadIdx.x, y = threadIdx.y;
+    const i64 l0 = blockIdx.x * (4ll * XG) + 4 * c;
+    const bool valid = l0 < nlines;
+    const i64 S = nlines;
+    const int row0 = y * 32;
+    uint32_t bits[4] = {0, 0, 0, 0};
+    {
+        uint32_t v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const int x = row0 + u;
+            v[u] = (valid && x < nx) ? __ldg((const uint32_t *)(mask + (i64)x * S + l0)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            // nonzero bytes -> bit 7 of each byte, then gather the 4 flags
+            const uint32_t nzb = ((v[u] & 0x7f7f7f7fu) + 0x7f7f7f7fu) | v[u];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) bits[q] |= ((nzb >> (8 * q + 7)) & 1u) << u;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        segL[y][4 * c + q] = bits[q] ? row0 + 31 - __clz(bits[q]) : -1;
+        segF[y][4 * c + q] = bits[q] ? row0 + __ffs(bits[q]) - 1 : -1;
+    }
+    __syncthreads();
+    if (!valid) return;
+    int last[4], nxt[4], rcv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        int lc = -1, rc = -1;
+        for (int yy = y - 1; yy >= 0; --yy)
+            if (segL[yy][4 * c + q] >= 0) { lc = segL[yy][4 * c + q]; break; }
+        for (int yy = y + 1; yy < 32; ++yy)
+            if (segF[yy][4 * c + q] >= 0) { rc = segF[yy][4 * c + q]; break; }
+        last[q] = lc;
+        rcv[q] = rc < 0 ? INT_MAX / 2 : rc;
+        nxt[q] = bits[q] ? row0 + __ffs(bits[q]) - 1 : rc;
+        if (nxt[q] < 0) nxt[q] = INT_MAX / 2;  // no foreground above: never closer
+    }
+    const int nrows = min(32, nx - row0);
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+        if (u >= nrows) break;
+        const int x = row0 + u;
+        uint32_t d[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t b = bits[q];
+            if ((b >> u) & 1u) {
+                last[q] = x;
+                nxt[q] = x;
+            } else if (x > nxt[q]) {  // walked past the nearest foreground above: next one
+                // (none left in this segment: the first of the next non-empty one)
+                const uint32_t rem = u < 31 ? b >> (u + 1) : 0u;
+                nxt[q] = rem ? x + __ffs(rem) : rcv[q];
+            }
+            int best = last[q];
+            if (nxt[q] < INT_MAX / 2 && (best < 0 || nxt[q] - x < x - best)) best = nxt[q];
+            d[q] = (uint16_t)(best < 0 ? NONE16 : (int16_t)(best - x));
+        }
+        *(uint2 *)(di + (i64)x * S + l0) = make_uint2(d[0] | (d[1] << 16), d[2] | (d[3] << 16));
+    }
+}
+
 // ---------------------------------------------------------------------------
 // pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di)
 // ---------------------------------------------------------------------------
@@ -354,11 +431,10 @@ __global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di,
 // single-thread envelope, with the switch points in parallel -- slower: the
 // envelope thread then runs in 2 of 16 warps.)
 // ---------------------------------------------------------------------------
-constexpr int PFB = 16;  // build prefetch depth
 constexpr int LTB = 64;  // build CTA size: small CTAs spread the nx*nz lines evenly over the SMs
 constexpr int YS = 8;    // output segments per line
 
-template <int NZ>
+template <int NZ, int PFB>
 __global__ void __launch_bounds__(LTB) edt_y_build(int16_t *__restrict__ di, i64 nlines, int ny, int nz_, double dx,
                                                   double dy, uint32_t *__restrict__ head,
                                                   uint32_t *__restrict__ spill, int32_t *__restrict__ kc,
@@ -686,6 +762,262 @@ __global__ void __launch_bounds__(ZLN) edt_pass_zp(const int32_t *__restrict__ i
     }
 }
 
+// Pass z, third form.  Same envelope and arithmetic as edt_pass_zp; the
+// distance phase is reworked (it was ~40% of the kernel's instructions):
+//   * each thread forms 4 consecutive voxels of a line (one 32-bit SMEM load
+//     of their feature positions, two 16-byte stores); the site cost
+//     gyz(site) is formed once per distinct feature among the 4;
+//   * the z term sq((f - x) * dz) comes from a CTA table over f - x in
+//     (-NZ, NZ) (same operations, so the same bits).
+// GD = true: the load phase forms every element's cost (t0 + t1) as float64
+// into SMEM (voxel-parallel), so neither the envelope nor the distance phase
+// converts or multiplies offsets; it costs 8 instead of 4 SMEM bytes per
+// element (fewer lines per SM).
+template <int NZ, int ZLN, bool GD>
+constexpr size_t zq_smem() {
+    return (size_t)ZLN * (NZ + 1) * (GD ? 8 : 4) + 2 * (size_t)ZLN * (NZ + 4) + (size_t)(2 * NZ) * 8;
+}
+
+template <int NZ, int ZLN, bool GD>
+__global__ void __launch_bounds__(ZLN) edt_pass_zq(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
+                                                  double dz, double *__restrict__ out) {
+    constexpr int S = NZ + 1;   // padded line stride (conflict-free)
+    constexpr int SB = NZ + 4;  // byte rows (multiple of 4: 32-bit loads of 4 positions)
+    extern __shared__ __align__(16) unsigned char zsm[];
+    double *czt = (double *)zsm;                       // [2 NZ]: czt[d + NZ] = sq(d * dz)
+    double *gd = czt + 2 * NZ;                         // GD: [ZLN][S] costs
+    int32_t *ps = (int32_t *)(czt + 2 * NZ);           // !GD: [ZLN][S] packed offsets
+    uint8_t *stk = (uint8_t *)(czt + 2 * NZ) + (size_t)ZLN * S * (GD ? 8 : 4);
+    uint8_t *fid = stk + ZLN * SB;
+
+    for (int d = threadIdx.x; d < 2 * NZ; d += ZLN) czt[d] = sq(__dmul_rn((double)(d - NZ), dz));
+    const i64 l0 = blockIdx.x * (i64)ZLN;
+    const int nl = (int)min((i64)ZLN, nlines - l0);
+    const int32_t *src = in + l0 * NZ;
+    constexpr int T4 = ZLN * NZ / 4;
+    for (int i0 = threadIdx.x; i0 < T4; i0 += 8 * ZLN) {
+        int4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = i0 + u * ZLN;
+            if (q < T4 && q * 4 < nl * NZ) v[u] = __ldg((const int4 *)src + q);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = i0 + u * ZLN;
+            if (q < T4 && q * 4 < nl * NZ) {
+                const int idx = q * 4, g = idx / NZ, k = idx - g * NZ;
+                if constexpr (GD) {
+                    double *d = gd + g * S + k;
+                    d[0] = v[u].x == NONE32 ? INFINITY : gyz(v[u].x, dx, dy);
+                    d[1] = v[u].y == NONE32 ? INFINITY : gyz(v[u].y, dx, dy);
+                    d[2] = v[u].z == NONE32 ? INFINITY : gyz(v[u].z, dx, dy);
+                    d[3] = v[u].w == NONE32 ? INFINITY : gyz(v[u].w, dx, dy);
+                } else {
+                    int32_t *d = ps + g * S + k;
+                    d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const double d2 = __dmul_rn(dz, dz);
+    const int t = threadIdx.x;
+    if (t < nl) {
+        uint8_t *st = stk + t * SB;
+        uint8_t *fo = fid + t * SB;
+        int K = 0, tp = 0, bp = 0;
+        double tg = 0.0, bg = 0.0;
+        if constexpr (GD) {
+            const double *G = gd + t * S;
+            double gnx = G[0];
+            for (int x = 0; x < NZ; ++x) {
+                const double gx = gnx;
+                gnx = x + 1 < NZ ? G[x + 1] : INFINITY;  // next element in flight
+                if (gx == INFINITY) continue;
+                while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+                    --K;
+                    tp = bp;
+                    tg = bg;
+                    if (K >= 2) {
+                        bp = st[K - 2];
+                        bg = G[bp];
+                    }
+                }
+                st[K++] = (uint8_t)x;
+                bp = tp; bg = tg; tp = x; tg = gx;
+            }
+        } else {
+            const int32_t *P = ps + t * S;
+            int32_t pcur = P[0];
+            for (int x = 0; x < NZ; ++x) {
+                const int32_t px = pcur;
+                pcur = x + 1 < NZ ? P[x + 1] : NONE32;
+                if (px == NONE32) continue;
+                const double gx = gyz(px, dx, dy);
+                while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+                    --K;
+                    tp = bp;
+                    tg = bg;
+                    if (K >= 2) {
+                        bp = st[K - 2];
+                        bg = gyz(P[bp], dx, dy);
+                    }
+                }
+                st[K++] = (uint8_t)x;
+                bp = tp; bg = tg; tp = x; tg = gx;
+            }
+        }
+        if (K == 0) {
+            for (int x = 0; x < NZ; x += 4) *(uint32_t *)(fo + x) = 0xffffffffu;
+        } else {
+            auto G = [&](int x) -> double {
+                if constexpr (GD) return gd[t * S + x];
+                else return gyz(ps[t * S + x], dx, dy);
+            };
+            int e = 0;
+            int cp = st[0], np = K > 1 ? st[1] : 0;
+            double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
+            int sw = K > 1 ? first_past(0, NZ, np, ng, cp, cg, d2) : NZ;
+            int x = 0;
+            for (;;) {
+                for (; x < sw; ++x) fo[x] = (uint8_t)cp;
+                if (x >= NZ) break;
+                ++e;
+                cp = np; cg = ng;
+                if (e + 1 < K) {
+                    np = st[e + 1];
+                    ng = G(np);
+                    sw = first_past(x, NZ, np, ng, cp, cg, d2);
+                } else {
+                    sw = NZ;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // distances: thread = 4 consecutive voxels of one line
+    double *dst = out + l0 * NZ;
+    constexpr int NQ = NZ / 4;
+    const int totq = nl * NQ;
+#pragma unroll 2
+    for (int iq = threadIdx.x; iq < totq; iq += ZLN) {
+        const int g = iq / NQ, x0 = (iq - g * NQ) * 4;
+        const uint32_t f4 = *(const uint32_t *)(fid + g * SB + x0);
+        double r[4];
+        int fprev = -1;
+        double gprev = 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = (f4 >> (8 * u)) & 0xff;
+            if (f == 255) {
+                r[u] = INFINITY;
+                continue;
+            }
+            if (f != fprev) {
+                if constexpr (GD) gprev = gd[g * S + f];
+                else gprev = gyz(ps[g * S + f], dx, dy);
+                fprev = f;
+            }
+            r[u] = __dsqrt_rn(__dadd_rn(gprev, czt[f - (x0 + u) + NZ]));
+        }
+        double2 *o = (double2 *)(dst + (i64)g * NZ + x0);
+        o[0] = make_double2(r[0], r[1]);
+        o[1] = make_double2(r[2], r[3]);
+    }
+}
+
+// Pass z, register-streamed form.  ncu on edt_pass_zp: the thread-per-line
+// envelope is latency bound (wait stalls, 16 warps/SM) and the SMEM staging of
+// whole lines (396 B per line) is what caps the warps.  Here a thread streams
+// its own line from global memory (two 16-byte loads per 8 elements, the next
+// chunk in flight), keeps only the envelope stack in SMEM (positions for all
+// entries, packed offsets for the first SCZ; deeper entries re-read their
+// offsets from the line, which stays in L1/L2), and forms the distances in the
+// sweep itself, four voxels per 32-byte store (one full sector per lane).
+// 128 B of SMEM per line: 32 warps per SM.  Same predicates and arithmetic
+// as edt_pass_zp (bit-identical output).
+__device__ __forceinline__ void st_v4(double *p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+constexpr int ZRT = 256;  // threads (lines) per CTA
+template <int NZ, int SCZ>
+__global__ void __launch_bounds__(ZRT, 4) edt_pass_zr(const int32_t *__restrict__ in, i64 nlines, double dx,
+                                                      double dy, double dz, double *__restrict__ out) {
+    __shared__ double czt[2 * NZ];          // czt[d + NZ] = sq(d * dz)
+    __shared__ uint8_t posS[NZ][ZRT];       // stack positions
+    __shared__ int32_t pkS[SCZ][ZRT];       // packed offsets of the first SCZ entries
+    for (int d = threadIdx.x; d < 2 * NZ; d += ZRT) czt[d] = sq(__dmul_rn((double)(d - NZ), dz));
+    __syncthreads();
+    const i64 l = blockIdx.x * (i64)ZRT + threadIdx.x;
+    if (l >= nlines) return;
+    const int t = threadIdx.x;
+    const int32_t *line = in + l * NZ;
+    const double d2 = __dmul_rn(dz, dz);
+    auto pk_ld = [&](int e, int pos) -> int32_t { return e < SCZ ? pkS[e][t] : __ldg(line + pos); };
+    int K = 0, tp = 0, bp = 0;
+    double tg = 0.0, bg = 0.0;
+    int4 na = __ldg((const int4 *)line), nb = __ldg((const int4 *)line + 1);
+    for (int c = 0; c < NZ; c += 8) {
+        const int32_t v[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
+        if (c + 8 < NZ) {
+            na = __ldg((const int4 *)(line + c + 8));
+            nb = __ldg((const int4 *)(line + c + 12));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int32_t px = v[u];
+            if (px == NONE32) continue;
+            const int x = c + u;
+            const double gx = gyz(px, dx, dy);
+            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+                --K;
+                tp = bp;
+                tg = bg;
+                if (K >= 2) {
+                    bp = posS[K - 2][t];
+                    bg = gyz(pk_ld(K - 2, bp), dx, dy);
+                }
+            }
+            posS[K][t] = (uint8_t)x;
+            if (K < SCZ) pkS[K][t] = px;
+            ++K;
+            bp = tp; bg = tg; tp = x; tg = gx;
+        }
+    }
+    double *dst = out + l * NZ;
+    if (K == 0) {
+#pragma unroll 4
+        for (int x = 0; x < NZ; x += 4) st_v4(dst + x, INFINITY, INFINITY, INFINITY, INFINITY);
+        return;
+    }
+    int e = 0;
+    int cp = posS[0][t], np = K > 1 ? posS[1][t] : 0;
+    double cg = gyz(pk_ld(0, cp), dx, dy), ng = K > 1 ? gyz(pk_ld(1, np), dx, dy) : 0.0;
+    int sw = K > 1 ? first_past(0, NZ, np, ng, cp, cg, d2) : NZ;
+    for (int x0 = 0; x0 < NZ; x0 += 4) {
+        double r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int x = x0 + u;
+            while (x >= sw) {
+                ++e;
+                cp = np; cg = ng;
+                if (e + 1 < K) {
+                    np = posS[e + 1][t];
+                    ng = gyz(pk_ld(e + 1, np), dx, dy);
+                    sw = first_past(x, NZ, np, ng, cp, cg, d2);
+                } else {
+                    sw = NZ;
+                }
+            }
+            r[u] = __dsqrt_rn(__dadd_rn(cg, czt[cp - x + NZ]));
+        }
+        st_v4(dst + x0, r[0], r[1], r[2], r[3]);
+    }
+}
+
 inline size_t zsmem(int nz) {
     const int S = nz + 1;
     return (size_t)ZL * S * 8 + (size_t)ZL * nz + 16;
@@ -718,7 +1050,10 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     uint32_t *spill = (uint32_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
     const i64 lx = ny * nz, ly = nx * nz, lz = nx * ny;
     if (nx <= 1024 && lx % 4 == 0 && ((uintptr_t)mask & 3) == 0 && ((uintptr_t)di & 7) == 0) {
-        edt_pass_x_seg4<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
+        // A/B knob: CT_EDT_XV=1 selects edt_pass_x_seg4b (measured slower: 137 vs 99 us on C2)
+        static const bool xv1 = getenv("CT_EDT_XV") && atoi(getenv("CT_EDT_XV")) == 1;
+        if (!xv1) edt_pass_x_seg4<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
+        else edt_pass_x_seg4b<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
     } else if (nx <= 1024) {
         edt_pass_x_seg<1><<<(unsigned)((lx + 31) / 32), dim3(32, 32), 0, s>>>(mask, lx, (int)nx, di);
     } else if (nx <= 4096) {
@@ -737,7 +1072,10 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         int16_t *swh = (int16_t *)(kc + ly);
         int16_t *est = swh + (size_t)SC * ly;
         const unsigned gb = (unsigned)((ly + LT - 1) / LT);
-        auto yb = nz == 64 ? edt_y_build<64> : nz == 32 ? edt_y_build<32> : nz == 96 ? edt_y_build<96> : edt_y_build<0>;
+        static const int ypf = getenv("CT_EDT_YPF") ? atoi(getenv("CT_EDT_YPF")) : 16;  // build prefetch depth (A/B knob; 16: 95 us, 32: 107, 64: 126 on C2)
+        auto yb = ypf == 16 ? (nz == 64 ? edt_y_build<64, 16> : nz == 32 ? edt_y_build<32, 16> : nz == 96 ? edt_y_build<96, 16> : edt_y_build<0, 16>)
+                : ypf == 8 ? (nz == 64 ? edt_y_build<64, 8> : nz == 32 ? edt_y_build<32, 8> : nz == 96 ? edt_y_build<96, 8> : edt_y_build<0, 8>)
+                            : (nz == 64 ? edt_y_build<64, 32> : nz == 32 ? edt_y_build<32, 32> : nz == 96 ? edt_y_build<96, 32> : edt_y_build<0, 32>);
         auto yo = nz == 64 ? edt_y_out<64> : nz == 32 ? edt_y_out<32> : nz == 96 ? edt_y_out<96> : edt_y_out<0>;
         yb<<<(unsigned)((ly + LTB - 1) / LTB), LTB, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, head, spill, kc, swh, est);
         if (int st = ct::check_launch("edt_y_build")) return st;
@@ -750,10 +1088,26 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             kern<<<(unsigned)((lz + zln - 1) / zln), zln, smem, s>>>(pk, lz, dx, dy, dz, out);
         };
-        if (nz == 64) launch(edt_pass_zp<64, ZL>, ZL, zp_smem<64, ZL>());
-        else if (nz == 32) launch(edt_pass_zp<32, ZL>, ZL, zp_smem<32, ZL>());
-        else launch(edt_pass_zp<96, 64>, 64, zp_smem<96, 64>());
-        return ct::check_launch("edt_pass_zp");
+        static const int zv = getenv("CT_EDT_ZV") ? atoi(getenv("CT_EDT_ZV")) : 3;  // pass-z form (A/B knob)
+        if (zv == 0) {
+            if (nz == 64) launch(edt_pass_zp<64, ZL>, ZL, zp_smem<64, ZL>());
+            else if (nz == 32) launch(edt_pass_zp<32, ZL>, ZL, zp_smem<32, ZL>());
+            else launch(edt_pass_zp<96, 64>, 64, zp_smem<96, 64>());
+        } else if (zv == 1) {
+            if (nz == 64) launch(edt_pass_zq<64, 128, false>, 128, zq_smem<64, 128, false>());
+            else if (nz == 32) launch(edt_pass_zq<32, 128, false>, 128, zq_smem<32, 128, false>());
+            else launch(edt_pass_zq<96, 64, false>, 64, zq_smem<96, 64, false>());
+        } else if (zv == 3) {
+            const unsigned g = (unsigned)((lz + ZRT - 1) / ZRT);
+            if (nz == 64) edt_pass_zr<64, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
+            else if (nz == 32) edt_pass_zr<32, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
+            else edt_pass_zr<96, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
+        } else {
+            if (nz == 64) launch(edt_pass_zq<64, 64, true>, 64, zq_smem<64, 64, true>());
+            else if (nz == 32) launch(edt_pass_zq<32, 128, true>, 128, zq_smem<32, 128, true>());
+            else launch(edt_pass_zq<96, 32, true>, 32, zq_smem<96, 32, true>());
+        }
+        return ct::check_launch("edt_pass_z");
     }
     auto kz = nz == 64 ? edt_pass_z<64> : nz == 32 ? edt_pass_z<32> : nz == 128 ? edt_pass_z<128> : edt_pass_z<0>;
     cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
