@@ -151,6 +151,17 @@ int ct_threshold_close(const void *in, int dtype, int64_t nx, int64_t ny, int64_
                        const int64_t *otsu_result, int64_t t_host, int radius, uint8_t *mask_out,
                        void *work, void *stream);
 
+/* K4 for the fused cell path: ct_threshold_close with radius 1 that also
+ * writes the closed mask as packed z-rows -- rows_out[(i*ny + j)*W ...] with
+ * W = 1 uint64 (nz <= 64) or 2 (nz <= 128, one 128-bit word, low half first),
+ * bit k = voxel (i,j,k) -- for ct_ccl26_rows.  mask_out may be NULL (no byte
+ * mask).  Requires nz <= 128, nz % 4 == 0, 16-byte aligned outputs and the
+ * ct_workspace_bytes(1,...) work area (else CT_ERR_UNSUPPORTED / PARAM).
+ * Same reference semantics as ct_threshold_close (segment.py:175-204). */
+int ct_threshold_close_rows(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz,
+                            const int64_t *otsu_result, int64_t t_host, uint8_t *mask_out, void *rows_out,
+                            void *work, void *stream);
+
 /* ref segment.py:175-189 on a given mask (0/1 bytes). */
 int ct_closing(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, int radius, uint8_t *out,
                void *work, void *stream);
@@ -161,6 +172,11 @@ int ct_closing(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, int radi
  * counters: int64[CT_CNT_WORDS] (zeroed by the call). */
 int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, int32_t *labels, int32_t *fg_list,
              int64_t *counters, void *stream);
+
+/* K5 on packed z-rows (ct_threshold_close_rows output, nz <= 128): same
+ * outputs as ct_ccl26 (ref segment.py:254) without re-reading a byte mask. */
+int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t nz, int32_t *labels, int32_t *fg_list,
+                  int64_t *counters, void *stream);
 
 /* K6 -- ref segment.py:242-276 detections_from_mask minus the hull: volume
  * filter count*((dx*dy)*dz) >= min_volume (float64), rank by (-count, root),

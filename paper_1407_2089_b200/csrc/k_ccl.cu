@@ -251,6 +251,14 @@ __device__ __forceinline__ R pack_row(const uint8_t *__restrict__ row, int nz) {
     return w;
 }
 
+// z-row word r: from pre-packed rows (ct_threshold_close_rows) or packed
+// on the fly from the mask bytes
+template <typename R, bool BITS>
+__device__ __forceinline__ R load_row(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 r, int nz) {
+    if constexpr (BITS) return rows[r];
+    else return pack_row<R>(mask + r * nz, nz);
+}
+
 // run of w starting at bit s: mask of its bits
 template <typename R>
 __device__ __forceinline__ R run_mask(R w, int s) {
@@ -259,10 +267,11 @@ __device__ __forceinline__ R run_mask(R w, int s) {
     return ct::rmask<R>(len) << s;
 }
 
-template <typename R>
-__global__ void ccl_run_init(const uint8_t *__restrict__ mask, i64 nrows, int nz, int32_t *__restrict__ labels) {
+template <typename R, bool BITS>
+__global__ void ccl_run_init(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 nrows, int nz,
+                             int32_t *__restrict__ labels) {
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        R st = pack_row<R>(mask + r * nz, nz);
+        R st = load_row<R, BITS>(mask, rows, r, nz);
         st &= ~(st << 1);  // run starts
         while (st) {
             const int s = ct::rffs(st) - 1;
@@ -272,11 +281,12 @@ __global__ void ccl_run_init(const uint8_t *__restrict__ mask, i64 nrows, int nz
     }
 }
 
-template <typename R>
-__global__ void ccl_run_union(const uint8_t *__restrict__ mask, i64 nx, i64 ny, int nz, int32_t *labels) {
+template <typename R, bool BITS>
+__global__ void ccl_run_union(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 nx, i64 ny, int nz,
+                              int32_t *labels) {
     const i64 nrows = nx * ny;
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        const R w = pack_row<R>(mask + r * nz, nz);
+        const R w = load_row<R, BITS>(mask, rows, r, nz);
         if (!w) continue;
         const i64 i = r / ny, j = r - i * ny;
         const i64 nb[4] = {j > 0 ? r - 1 : -1, (i > 0 && j > 0) ? r - ny - 1 : -1, i > 0 ? r - ny : -1,
@@ -284,7 +294,7 @@ __global__ void ccl_run_union(const uint8_t *__restrict__ mask, i64 nx, i64 ny, 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (nb[q] < 0) continue;
-            const R u = pack_row<R>(mask + nb[q] * nz, nz);
+            const R u = load_row<R, BITS>(mask, rows, nb[q], nz);
             if (!u) continue;
             const R ustart = u & ~(u << 1);
             R rem = w;
@@ -305,14 +315,30 @@ __global__ void ccl_run_union(const uint8_t *__restrict__ mask, i64 nx, i64 ny, 
     }
 }
 
-template <typename R>
-__global__ void ccl_run_emit(const uint8_t *__restrict__ mask, i64 nrows, int nz, int32_t *labels,
-                             int32_t *__restrict__ fg, int64_t *__restrict__ counters) {
-    for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        const R w = pack_row<R>(mask + r * nz, nz);
-        if (!w) continue;
+template <typename R, bool BITS>
+__global__ void ccl_run_emit(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 nrows, int nz,
+                             int32_t *labels, int32_t *__restrict__ fg, int64_t *__restrict__ counters) {
+    // the loop runs whole warps (trip count uniform per warp) so the fg-list
+    // slots are claimed with one atomic per warp: a per-row atomic on the one
+    // counter serialised ~10^5 non-empty rows
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    const unsigned lane = threadIdx.x & 31;
+    for (i64 r0 = blockIdx.x * (i64)blockDim.x + (threadIdx.x & ~31u); r0 < nrows; r0 += stride) {
+        const i64 r = r0 + lane;
+        const R w = r < nrows ? load_row<R, BITS>(mask, rows, r, nz) : (R)0;
         const int n = ct::rpopc(w);
-        const unsigned long long base = atomicAdd((unsigned long long *)&counters[CT_CNT_FG], (unsigned long long)n);
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += v;
+        }
+        unsigned long long wbase = 0;
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 31 && tot) wbase = atomicAdd((unsigned long long *)&counters[CT_CNT_FG], (unsigned long long)tot);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
+        if (!w) continue;
+        const unsigned long long base = wbase + (unsigned long long)(incl - n);
         R rem = w;
         int e = 0;
         while (rem) {
@@ -329,10 +355,11 @@ __global__ void ccl_run_emit(const uint8_t *__restrict__ mask, i64 nrows, int nz
 }
 
 // final sweep: run starts take their root (after all finds of ccl_run_emit)
-template <typename R>
-__global__ void ccl_run_roots(const uint8_t *__restrict__ mask, i64 nrows, int nz, int32_t *labels) {
+template <typename R, bool BITS>
+__global__ void ccl_run_roots(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 nrows, int nz,
+                              int32_t *labels) {
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
-        R st = pack_row<R>(mask + r * nz, nz);
+        R st = load_row<R, BITS>(mask, rows, r, nz);
         st &= ~(st << 1);
         while (st) {
             const int s = ct::rffs(st) - 1;
@@ -828,10 +855,10 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
         const int g = (int)min((nrows + 255) / 256, (i64)CT_NUM_SMS * 16);
         auto run = [&](auto tag) -> int {
             using R = decltype(tag);
-            ccl_run_init<R><<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels);
-            ccl_run_union<R><<<g, 256, 0, s>>>(mask, nx, ny, (int)nz, labels);
-            ccl_run_emit<R><<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels, fg_list, counters);
-            ccl_run_roots<R><<<g, 256, 0, s>>>(mask, nrows, (int)nz, labels);
+            ccl_run_init<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels);
+            ccl_run_union<R, false><<<g, 256, 0, s>>>(mask, nullptr, nx, ny, (int)nz, labels);
+            ccl_run_emit<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels, fg_list, counters);
+            ccl_run_roots<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels);
             return ct::check_launch("ccl_run");
         };
         return nz <= 64 ? run((unsigned long long)0) : run((ct::u128)0);
@@ -844,6 +871,33 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
     if (int st = ct::check_launch("ccl_boundary")) return st;
     ccl_flatten<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters);
     return ct::check_launch("ccl_flatten");
+}
+
+extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t nz, int32_t *labels,
+                             int32_t *fg_list, int64_t *counters, void *stream) {
+    if (nx <= 0 || ny <= 0 || nz <= 0) {
+        ct::set_error("empty mask");
+        return CT_ERR_PARAM;
+    }
+    if (nx * ny * nz >= (1ll << 31) || nz > 128) {
+        ct::set_error("ct_ccl26_rows: needs nz <= 128 and < 2^31 voxels");
+        return CT_ERR_UNSUPPORTED;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(counters, 0, CT_CNT_WORDS * sizeof(int64_t), s);
+    cudaMemsetAsync(labels, 0xff, (size_t)(nx * ny * nz) * sizeof(int32_t), s);  // background = -1
+    const i64 nrows = nx * ny;
+    const int g = (int)min((nrows + 255) / 256, (i64)CT_NUM_SMS * 16);
+    auto run = [&](auto tag) -> int {
+        using R = decltype(tag);
+        const R *rw = (const R *)rows;
+        ccl_run_init<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels);
+        ccl_run_union<R, true><<<g, 256, 0, s>>>(nullptr, rw, nx, ny, (int)nz, labels);
+        ccl_run_emit<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels, fg_list, counters);
+        ccl_run_roots<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels);
+        return ct::check_launch("ccl_run_rows");
+    };
+    return nz <= 64 ? run((unsigned long long)0) : run((ct::u128)0);
 }
 
 extern "C" int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz, const int32_t *fg_list,

@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(256) close1_bits(const R *__restrict__ rows, i
 
 template <typename T>
 int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i64 t_host, int r, uint8_t *out,
-                    uint8_t *work, cudaStream_t s) {
+                    uint8_t *work, cudaStream_t s, void *rows_out = nullptr) {
     const i64 n = nx * ny * nz;
     if (r == 0) {
         threshold_kernel<T><<<ct::grid_for(n, 256), 256, 0, s>>>(in, n, otsu, t_host, out);
@@ -278,7 +278,7 @@ int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i6
                                                                                           t_host, rows);
             if (int st = ct::check_launch("pack_rows")) return st;
             close1_bits<R><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(rows, nx, ny, (int)nz, out,
-                                                                                      nullptr);
+                                                                                      (R *)rows_out);
             return ct::check_launch("close1_bits");
         };
         return nz <= 64 ? run((u64)0) : run((ct::u128)0);
@@ -312,6 +312,25 @@ extern "C" int ct_threshold_close(const void *in, int dtype, int64_t nx, int64_t
     cudaStream_t s = (cudaStream_t)stream;
     CT_DISPATCH(dtype, T, {
         return threshold_close<T>((const T *)in, nx, ny, nz, otsu_result, t_host, radius, mask_out, (uint8_t *)work, s);
+    });
+    return CT_OK;
+}
+
+extern "C" int ct_threshold_close_rows(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz,
+                                       const int64_t *otsu_result, int64_t t_host, uint8_t *mask_out, void *rows_out,
+                                       void *work, void *stream) {
+    if (nx <= 0 || ny <= 0 || nz <= 0 || !rows_out || !work) {
+        ct::set_error("bad closing arguments");
+        return CT_ERR_PARAM;
+    }
+    if (nz > 128 || nz % 4 != 0 || ((uintptr_t)mask_out & 15) || ((uintptr_t)rows_out & 15)) {
+        ct::set_error("ct_threshold_close_rows: needs nz <= 128, nz %% 4 == 0, 16-byte aligned outputs");
+        return CT_ERR_UNSUPPORTED;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    CT_DISPATCH(dtype, T, {
+        return threshold_close<T>((const T *)in, nx, ny, nz, otsu_result, t_host, 1, mask_out, (uint8_t *)work, s,
+                                  rows_out);
     });
     return CT_OK;
 }

@@ -101,7 +101,6 @@ class FramePipeline:
             self.med = E(self.dims, self.tdtype)
             self.hist = Z(65536, torch.int64)
             self.otsu = Z(4, torch.int64)
-            self.mask = E(self.dims, torch.uint8)
             self.labels = E(self.dims, torch.int32)
             self.fg = E(n, torch.int32)
             self.counters = Z(8, torch.int64)
@@ -110,6 +109,11 @@ class FramePipeline:
             self.table = E(self.cap * CELL_DTYPE.itemsize, torch.uint8)
             self.voxels = E(n, torch.int32)
             self.cwork = E(workspace_bytes(1, nx, ny, nz, cr), torch.uint8) if cr >= 1 else None
+            # K4 -> K5 through packed z-rows (r == 1, nz <= 128): the closed mask
+            # is never materialised as bytes on the fused path
+            self.rows_path = cr == 1 and nz <= 128 and nz % 4 == 0
+            self.crows = E(nx * ny * (1 if nz <= 64 else 2), torch.int64) if self.rows_path else None
+            self.mask = None if self.rows_path else E(self.dims, torch.uint8)
         if vessel:
             self.mwork = E(workspace_bytes(4, nx, ny, nz, self.code), torch.uint8)
             self.state = Z(9, torch.float64)
@@ -175,13 +179,21 @@ class FramePipeline:
         call("ct_otsu", self.hist.data_ptr(), self.nbins, self.otsu.data_ptr(), s)
         self._t1("K3 otsu", e)
         e = self._t0()
-        call("ct_threshold_close", self.med.data_ptr(), self.code, nx, ny, nz, self.otsu.data_ptr(), 0,
-             self.seg.closing_radius, self.mask.data_ptr(),
-             self.cwork.data_ptr() if self.cwork is not None else None, s)
+        if self.rows_path:
+            call("ct_threshold_close_rows", self.med.data_ptr(), self.code, nx, ny, nz, self.otsu.data_ptr(), 0,
+                 None, self.crows.data_ptr(), self.cwork.data_ptr(), s)
+        else:
+            call("ct_threshold_close", self.med.data_ptr(), self.code, nx, ny, nz, self.otsu.data_ptr(), 0,
+                 self.seg.closing_radius, self.mask.data_ptr(),
+                 self.cwork.data_ptr() if self.cwork is not None else None, s)
         self._t1("K4 threshold+close", e)
         e = self._t0()
-        call("ct_ccl26", self.mask.data_ptr(), nx, ny, nz, self.labels.data_ptr(), self.fg.data_ptr(),
-             self.counters.data_ptr(), s)
+        if self.rows_path:
+            call("ct_ccl26_rows", self.crows.data_ptr(), nx, ny, nz, self.labels.data_ptr(), self.fg.data_ptr(),
+                 self.counters.data_ptr(), s)
+        else:
+            call("ct_ccl26", self.mask.data_ptr(), nx, ny, nz, self.labels.data_ptr(), self.fg.data_ptr(),
+                 self.counters.data_ptr(), s)
         self._t1("K5 ccl", e)
         e = self._t0()
         sp = self.spacing

@@ -420,3 +420,53 @@ def test_specialised_kernel_paths_vs_oracle(cuda, oracle, shape):
             np.testing.assert_array_equal(a.voxels, b.voxels)
             np.testing.assert_array_equal(a.centroid_um, b.centroid_um)
         np.testing.assert_array_equal(S.distance_map(m, ANISO).values, oracle.edt(m, ANISO.as_array()))
+
+
+@pytest.mark.parametrize("shape", [(24, 40, 64), (16, 24, 32), (12, 20, 128), (14, 18, 96), (9, 11, 20)])
+def test_packed_rows_closing_and_ccl(cuda, oracle, shape):
+    """ct_threshold_close_rows (packed z-row output of K4) and ct_ccl26_rows
+    (K5 on those rows, the fused pipeline's cell path) against the byte-mask
+    entry points and the oracle's closing: same words, labels, counters."""
+    from paper_1407_2089_b200._lib import call, workspace_bytes
+    from paper_1407_2089_b200 import _dev
+
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx * ny * nz)
+    for dens in (0.5, 0.85, 0.97):
+        v = (rng.random(shape) * 255).astype(np.uint8)
+        t = int(255 * dens)
+        dv = torch.from_numpy(v).cuda()
+        otsu = torch.tensor([t, 0, 0, 0], dtype=torch.int64, device="cuda")
+        work = torch.empty(workspace_bytes(1, nx, ny, nz, 1), dtype=torch.uint8, device="cuda")
+        W = 1 if nz <= 64 else 2
+        rows = torch.zeros(nx * ny * W, dtype=torch.int64, device="cuda")
+        mask_b = torch.empty(shape, dtype=torch.uint8, device="cuda")
+        mask_r = torch.empty(shape, dtype=torch.uint8, device="cuda")
+        s = _dev.stream_handle()
+        call("ct_threshold_close", dv.data_ptr(), 1, nx, ny, nz, otsu.data_ptr(), 0, 1, mask_b.data_ptr(),
+             work.data_ptr(), s)
+        call("ct_threshold_close_rows", dv.data_ptr(), 1, nx, ny, nz, otsu.data_ptr(), 0, mask_r.data_ptr(),
+             rows.data_ptr(), work.data_ptr(), s)
+        torch.cuda.synchronize()
+        mb = mask_b.cpu().numpy()
+        np.testing.assert_array_equal(mb, mask_r.cpu().numpy())
+        np.testing.assert_array_equal(mb.astype(bool), oracle.closing(v > t, 1))
+        # unpack the words: bit k of row (i, j)
+        words = rows.cpu().numpy().view(np.uint64).reshape(nx * ny, W)
+        bits = np.zeros((nx * ny, nz), dtype=np.uint8)
+        for k in range(nz):
+            bits[:, k] = (words[:, k // 64] >> np.uint64(k % 64)) & np.uint64(1)
+        np.testing.assert_array_equal(bits.reshape(shape), mb)
+        outs = []
+        for name, src in (("ct_ccl26", mask_b), ("ct_ccl26_rows", rows)):
+            labels = torch.empty(shape, dtype=torch.int32, device="cuda")
+            fg = torch.empty(nx * ny * nz, dtype=torch.int32, device="cuda")
+            cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
+            call(name, src.data_ptr(), nx, ny, nz, labels.data_ptr(), fg.data_ptr(), cnt.data_ptr(), s)
+            torch.cuda.synchronize()
+            c = cnt.cpu().numpy()
+            outs.append((labels.cpu().numpy(), c, np.sort(fg[: int(c[0])].cpu().numpy()) if c[0] else None))
+        np.testing.assert_array_equal(outs[0][0], outs[1][0])
+        np.testing.assert_array_equal(outs[0][1], outs[1][1])
+        if outs[0][2] is not None:
+            np.testing.assert_array_equal(outs[0][2], outs[1][2])
