@@ -40,6 +40,7 @@ constexpr int YSEG = 1;  // pass-y output segments per line (2 measured slower: 
 
 __device__ __forceinline__ double sq(double x) { return __dmul_rn(x, x); }
 
+
 __device__ __forceinline__ int32_t pack(int dj, int di) { return (int32_t)(((uint32_t)dj << 16) | (uint16_t)di); }
 __device__ __forceinline__ int unpack_dj(int32_t p) { return p >> 16; }
 __device__ __forceinline__ int unpack_di(int32_t p) { return (int)(int16_t)(p & 0xffff); }

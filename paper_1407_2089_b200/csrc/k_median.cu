@@ -268,6 +268,15 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
         __syncthreads();
         if (threadIdx.x == 0) *s_any = 0;
         if constexpr (NB == 8 && WC > 0) {
+            // clamped row offsets of the tile's input rows, once per tile
+            // (the per-load clamp / divide was a third of phase A)
+            __shared__ long long roff[(BTI + 2) * (BTJ + 2)];
+            for (int r = threadIdx.x; r < RI * RJ; r += 256) {
+                const int ri = r / RJ, rj = r - ri * RJ;
+                const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
+                roff[r] = (i * ny + j) * nz;
+            }
+            __syncthreads();
             // phase A (u8, nz = 32 WC): each lane loads 4 voxels (32 bits); a row
             // is 8 WC lanes; t4x8 + a nibble transpose over the 8 lanes of a
             // word leave lane s with plane s of that word
@@ -282,11 +291,8 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                 for (int q = 0; q < 4; ++q) {
                     const int r = r0 + q * 8 * RPW + lrow;
                     x[q] = 0u;
-                    if (r < NR && lrow < RPW) {  // (WC = 3: lanes 24-31 idle)
-                        const int ri = r / RJ, rj = r - ri * RJ;
-                        const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
-                        x[q] = __ldg((const uint32_t *)(in + (i * ny + j) * nz) + (lane % LPR));
-                    }
+                    if (r < NR && lrow < RPW)  // (WC = 3: lanes 24-31 idle)
+                        x[q] = __ldg((const uint32_t *)(in + roff[r]) + (lane % LPR));
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
