@@ -326,6 +326,86 @@ __global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4b(const uint8_t *__res
     }
 }
 
+// Same pass without clz / ffs (edt_pass_x_seg4 is XU bound: two bit scans per
+// voxel and line): a backward sweep over the segment's rows carries the
+// nearest foreground at or above each row and parks the distances in the
+// output rows (the thread's own 8-byte words; re-read from L2), then a forward
+// sweep carries the nearest at or below and picks (ties -> lower i).
+__global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4c(const uint8_t *__restrict__ mask, i64 nlines, int nx,
+                                                            int16_t *__restrict__ di) {
+    __shared__ int segL[32][4 * XG + 1], segF[32][4 * XG + 1];
+    const int c = threadIdx.x, y = threadIdx.y;
+    const i64 l0 = blockIdx.x * (4ll * XG) + 4 * c;
+    const bool valid = l0 < nlines;
+    const i64 S = nlines;
+    const int row0 = y * 32;
+    uint32_t bits[4] = {0, 0, 0, 0};
+    {
+        uint32_t v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const int x = row0 + u;
+            v[u] = (valid && x < nx) ? __ldg((const uint32_t *)(mask + (i64)x * S + l0)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const uint32_t nzb = ((v[u] & 0x7f7f7f7fu) + 0x7f7f7f7fu) | v[u];  // bit 7 of each byte: byte != 0
+#pragma unroll
+            for (int q = 0; q < 4; ++q) bits[q] |= ((nzb >> (8 * q + 7)) & 1u) << u;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        segL[y][4 * c + q] = bits[q] ? row0 + 31 - __clz(bits[q]) : -1;
+        segF[y][4 * c + q] = bits[q] ? row0 + __ffs(bits[q]) - 1 : -1;
+    }
+    __syncthreads();
+    if (!valid) return;
+    constexpr int BIG = 1 << 20, CAP = 0x7fff;  // CAP: "no foreground on this side" (nx <= 1024)
+    const int nrows = min(32, nx - row0);
+    int last[4], nxt[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        int lc = -1, rc = -1;
+        for (int yy = y - 1; yy >= 0; --yy)
+            if (segL[yy][4 * c + q] >= 0) { lc = segL[yy][4 * c + q]; break; }
+        for (int yy = y + 1; yy < 32; ++yy)
+            if (segF[yy][4 * c + q] >= 0) { rc = segF[yy][4 * c + q]; break; }
+        last[q] = lc >= 0 ? lc : -BIG;
+        nxt[q] = rc >= 0 ? rc : BIG;
+    }
+    // backward: distance to the nearest foreground at or above, parked in di
+#pragma unroll 8
+    for (int u = 31; u >= 0; --u) {
+        if (u >= nrows) continue;
+        const int x = row0 + u;
+        uint32_t d[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((bits[q] >> u) & 1u) nxt[q] = x;
+            d[q] = (uint32_t)min(nxt[q] - x, CAP);
+        }
+        *(uint2 *)(di + (i64)x * S + l0) = make_uint2(d[0] | (d[1] << 16), d[2] | (d[3] << 16));
+    }
+    // forward: nearest at or below, pick (ties -> lower i)
+#pragma unroll 8
+    for (int u = 0; u < 32; ++u) {
+        if (u >= nrows) break;
+        const int x = row0 + u;
+        const uint2 rp = *(const uint2 *)(di + (i64)x * S + l0);
+        const uint32_t rw[4] = {rp.x & 0xffffu, rp.x >> 16, rp.y & 0xffffu, rp.y >> 16};
+        uint32_t d[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((bits[q] >> u) & 1u) last[q] = x;
+            const int ld = min(x - last[q], CAP), rd = (int)rw[q];
+            const int dv = ld <= rd ? -ld : rd;
+            d[q] = (uint16_t)(min(ld, rd) >= CAP ? NONE16 : (int16_t)dv);
+        }
+        *(uint2 *)(di + (i64)x * S + l0) = make_uint2(d[0] | (d[1] << 16), d[2] | (d[3] << 16));
+    }
+}
+
 // ---------------------------------------------------------------------------
 // pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di)
 // ---------------------------------------------------------------------------
@@ -455,9 +535,8 @@ __global__ void __launch_bounds__(LTB) edt_y_build(int16_t *__restrict__ di, i64
 #define GOF(pl) sq(__dmul_rn((double)(int16_t)(pl), dx))
     int K = 0, tp = 0, bp = 0;
     double tg = 0.0, bg = 0.0;
-    for (int x0 = 0; x0 < ny; x0 += PFB) {
-        int16_t v[PFB];
-        __syncwarp(wm);
+    // batch x0 + PFB is loaded before batch x0 is consumed (double buffer)
+    auto load = [&](int x0, int16_t (&v)[PFB]) {
         const int16_t *p = line + (i64)x0 * nz;
         if (x0 + PFB <= ny) {
 #pragma unroll
@@ -466,6 +545,16 @@ __global__ void __launch_bounds__(LTB) edt_y_build(int16_t *__restrict__ di, i64
 #pragma unroll
             for (int u = 0; u < PFB; ++u) v[u] = x0 + u < ny ? __ldg(p + u * nz) : NONE16;
         }
+    };
+    int16_t vn[PFB];
+    __syncwarp(wm);
+    load(0, vn);
+    for (int x0 = 0; x0 < ny; x0 += PFB) {
+        int16_t v[PFB];
+#pragma unroll
+        for (int u = 0; u < PFB; ++u) v[u] = vn[u];
+        __syncwarp(wm);
+        if (x0 + PFB < ny) load(x0 + PFB, vn);
 #pragma unroll
         for (int u = 0; u < PFB; ++u) {
             if (v[u] == NONE16) continue;
@@ -1051,9 +1140,10 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     uint32_t *spill = (uint32_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
     const i64 lx = ny * nz, ly = nx * nz, lz = nx * ny;
     if (nx <= 1024 && lx % 4 == 0 && ((uintptr_t)mask & 3) == 0 && ((uintptr_t)di & 7) == 0) {
-        // A/B knob: CT_EDT_XV=1 selects edt_pass_x_seg4b (measured slower: 137 vs 99 us on C2)
-        static const bool xv1 = getenv("CT_EDT_XV") && atoi(getenv("CT_EDT_XV")) == 1;
-        if (!xv1) edt_pass_x_seg4<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
+        // A/B knob CT_EDT_XV: 0 edt_pass_x_seg4 (99 us on C2), 1 edt_pass_x_seg4b (137 us), 2 edt_pass_x_seg4c (105 us)
+        static const int xv = getenv("CT_EDT_XV") ? atoi(getenv("CT_EDT_XV")) : 0;
+        if (xv == 2) edt_pass_x_seg4c<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
+        else if (xv == 0) edt_pass_x_seg4<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
         else edt_pass_x_seg4b<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
     } else if (nx <= 1024) {
         edt_pass_x_seg<1><<<(unsigned)((lx + 31) / 32), dim3(32, 32), 0, s>>>(mask, lx, (int)nx, di);
