@@ -1025,19 +1025,20 @@ __global__ void __launch_bounds__(ZLN) edt_pass_zq(const int32_t *__restrict__ i
 // entries, packed offsets for the first SCZ; deeper entries re-read their
 // offsets from the line, which stays in L1/L2), and forms the distances in the
 // sweep itself, four voxels per 32-byte store (one full sector per lane).
-// 128 B of SMEM per line: 32 warps per SM.  Same predicates and arithmetic
+// 192 B of SMEM per line (with the switch points): 32 warps per SM.  Same predicates and arithmetic
 // as edt_pass_zp (bit-identical output).
 __device__ __forceinline__ void st_v4(double *p, double a, double b, double c, double d) {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
-constexpr int ZRT = 256;  // threads (lines) per CTA
+constexpr int ZRT = 128;  // threads (lines) per CTA
 template <int NZ, int SCZ>
-__global__ void __launch_bounds__(ZRT, 4) edt_pass_zr(const int32_t *__restrict__ in, i64 nlines, double dx,
+__global__ void __launch_bounds__(ZRT, 8) edt_pass_zr(const int32_t *__restrict__ in, i64 nlines, double dx,
                                                       double dy, double dz, double *__restrict__ out) {
     __shared__ double czt[2 * NZ];          // czt[d + NZ] = sq(d * dz)
     __shared__ uint8_t posS[NZ][ZRT];       // stack positions
     __shared__ int32_t pkS[SCZ][ZRT];       // packed offsets of the first SCZ entries
+    __shared__ uint8_t swS[NZ][ZRT];        // switch points of the envelope entries
     for (int d = threadIdx.x; d < 2 * NZ; d += ZRT) czt[d] = sq(__dmul_rn((double)(d - NZ), dz));
     __syncthreads();
     const i64 l = blockIdx.x * (i64)ZRT + threadIdx.x;
@@ -1083,24 +1084,37 @@ __global__ void __launch_bounds__(ZRT, 4) edt_pass_zr(const int32_t *__restrict_
         return;
     }
     int e = 0;
-    int cp = posS[0][t], np = K > 1 ? posS[1][t] : 0;
-    double cg = gyz(pk_ld(0, cp), dx, dy), ng = K > 1 ? gyz(pk_ld(1, np), dx, dy) : 0.0;
-    int sw = K > 1 ? first_past(0, NZ, np, ng, cp, cg, d2) : NZ;
+    int cp = posS[0][t];
+    double cg = gyz(pk_ld(0, cp), dx, dy);
+    // switch points first, per entry (a loop of at most K - 1 trips per lane
+    // instead of a divergent test inside the voxel loop): the sweep moves past
+    // entry e at sw_e = first_past(sw_{e-1}, ...), sw_{-1} = 0 -- exactly where
+    // the voxel-by-voxel sweep of edt_pass_zp switches
+    {
+        int p = cp, sw = 0;
+        double pg = cg;
+        for (int e2 = 0; e2 + 1 < K; ++e2) {
+            const int q = posS[e2 + 1][t];
+            const double qg = gyz(pk_ld(e2 + 1, q), dx, dy);
+            sw = first_past(sw, NZ, q, qg, p, pg, d2);
+            swS[e2][t] = (uint8_t)sw;
+            p = q;
+            pg = qg;
+        }
+    }
+    int sw = K > 1 ? swS[0][t] : NZ;
     for (int x0 = 0; x0 < NZ; x0 += 4) {
         double r[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int x = x0 + u;
-            while (x >= sw) {
-                ++e;
-                cp = np; cg = ng;
-                if (e + 1 < K) {
-                    np = posS[e + 1][t];
-                    ng = gyz(pk_ld(e + 1, np), dx, dy);
-                    sw = first_past(x, NZ, np, ng, cp, cg, d2);
-                } else {
-                    sw = NZ;
-                }
+            if (x >= sw) {
+                do {
+                    ++e;
+                    sw = e + 1 < K ? swS[e][t] : NZ;
+                } while (x >= sw);
+                cp = posS[e][t];
+                cg = gyz(pk_ld(e, cp), dx, dy);
             }
             r[u] = __dsqrt_rn(__dadd_rn(cg, czt[cp - x + NZ]));
         }
