@@ -216,6 +216,15 @@ int ct_voxel_runs(const int32_t *voxels, const ct_cell *table, const int64_t *co
 int ct_mrf(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz, void *work, double *state,
            uint64_t *hist, void *stream);
 
+/* ct_mrf for the fused pipeline: the first-step decision is certified
+ * without the exact sigma_hat when ||delta sign(S)|| = delta sqrt(nnz) exceeds
+ * the upper bound sqrt(mean(L^2))/sqrt(42) >= std(L)/sqrt(42) of the
+ * reference's estimate (denoise.py:100-114, 172-176), with a 2^-20 relative
+ * margin; state[1] is then NaN and state[2] = 2 (sigma skipped).  Otherwise
+ * (and for non-u8 input) the state equals ct_mrf's. */
+int ct_mrf_decide(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz, void *work, double *state,
+                  uint64_t *hist, void *stream);
+
 /* One synchronous MRF iteration (denoise.py:172): next = cur + delta *
  * sign(S(cur)); cur == NULL means the input.  out2 (device): [0] ||next -
  * input|| (pairwise order; exact for integer data), [1] moved voxels.

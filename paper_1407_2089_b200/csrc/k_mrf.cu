@@ -316,7 +316,9 @@ __global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__re
 
 // fold 2^D partials pairwise (complete binary tree above depth D); partial
 // has room for 2 * 2^D values (ping-pong halves).
-__global__ void __launch_bounds__(1024) pw_fold(double *partial, int D, double *out) {
+__global__ void __launch_bounds__(1024) pw_fold(double *partial, int D, double *out,
+                                                const unsigned long long *skip = nullptr) {
+    if (skip && *skip) return;
     const i64 m = 1ll << D;
     double *src = partial, *dst = partial + m;
     for (i64 w = m; w > 1; w >>= 1) {
@@ -472,7 +474,9 @@ __device__ __forceinline__ void load8<int32_t>(const int32_t *p, double (&x)[8])
 template <typename LT>
 __global__ void __launch_bounds__(PWV_T) pw_subtree_lap(const LT *__restrict__ lap, const double *__restrict__ meanp,
                                                         i64 n, int D, double *__restrict__ partial,
-                                                        const __grid_constant__ PwvTabs tabs) {
+                                                        const __grid_constant__ PwvTabs tabs,
+                                                        const unsigned long long *skip) {
+    if (skip && *skip) return;
     __shared__ double val[2 * PWV_LEAVES];
     i64 off, len;
     pw_node(n, D, blockIdx.x, off, len);
@@ -520,7 +524,8 @@ __global__ void __launch_bounds__(PWV_T) pw_subtree_lap(const LT *__restrict__ l
 
 // returns 1 when the shapes do not fit the tables (caller falls back)
 template <typename LT>
-int pairwise_sum_lap(const LT *lap, const double *mean, i64 n, double *partial, double *out, cudaStream_t s) {
+int pairwise_sum_lap(const LT *lap, const double *mean, i64 n, double *partial, double *out, cudaStream_t s,
+                     const unsigned long long *skip = nullptr) {
     if (n < 8 || ((uintptr_t)lap & 15) != 0 || n >= (1ll << 31)) return 1;
     const int D = pwv_depth(n);
     static thread_local i64 cached_n = -1;
@@ -554,9 +559,9 @@ int pairwise_sum_lap(const LT *lap, const double *mean, i64 n, double *partial, 
         for (int i = 0; i < ns && ok; ++i) ok = pwv_table(tabs, i, (int)sizes[i]);
     }
     if (!ok) return 1;
-    pw_subtree_lap<LT><<<(unsigned)(1ll << D), PWV_T, 0, s>>>(lap, mean, n, D, partial, tabs);
+    pw_subtree_lap<LT><<<(unsigned)(1ll << D), PWV_T, 0, s>>>(lap, mean, n, D, partial, tabs, skip);
     if (int st = ct::check_launch("pw_subtree_lap")) return -st;
-    pw_fold<<<1, 1024, 0, s>>>(partial, D, out);
+    pw_fold<<<1, 1024, 0, s>>>(partial, D, out, skip);
     if (int st = ct::check_launch("pw_fold")) return -st;
     return 0;
 }
@@ -564,7 +569,7 @@ int pairwise_sum_lap(const LT *lap, const double *mean, i64 n, double *partial, 
 // state words
 enum { S_DELTA = 0, S_SIGMA, S_SIGMA_STATUS, S_NNZ, S_NORM, S_DECISION, S_SUM1, S_SUM2, S_SUM3, S_WORDS };
 // scalar words (u64) in the workspace
-enum { W_NNZ = 0, W_BEST_BITS, W_MOVED, W_LAPSUM, W_WORDS = 8 };
+enum { W_NNZ = 0, W_BEST_BITS, W_MOVED, W_LAPSUM, W_LAPSQ, W_SKIP, W_WORDS = 8 };
 
 // ---------------------------------------------------------------------------
 // Streaming statistics pass (integer input): a CTA owns MJ rows (j) x all k
@@ -800,11 +805,17 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
 // owns MJ4 = 256 / (NZ/4) rows and walks MIPER planes along i with the same
 // 3-plane SMEM ring.  Edge neighbours are clamped exactly like the scalar
 // kernels (j, i by the clamped row/plane loads; k by byte replication).
-template <int NZ>
+// MODE 0: histogram, #{sign sum != 0}, Laplacian sum and the Laplacians
+// (lap) for the exact pairwise sigma_hat.  MODE 1 (certified quick decision,
+// ct_mrf_decide): as 0 but the Laplacians are only summed and squared-summed
+// (W_LAPSQ), not stored.  MODE 2: the fallback of MODE 1 -- Laplacians
+// only, and nothing at all when the quick decision certified (scal[W_SKIP]).
+template <int NZ, int MODE = 0>
 __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__ v, int nx, int ny,
                                                      unsigned long long *__restrict__ ghist,
                                                      unsigned long long *__restrict__ scal,
                                                      int16_t *__restrict__ lap) {
+    if (MODE == 2 && *(volatile unsigned long long *)&scal[W_SKIP]) return;
     constexpr int W = NZ / 4;               // words per row
     constexpr int MJ4 = 256 / W;            // rows per CTA
     constexpr int PW = (MJ4 + 2) * W;       // staged words per plane
@@ -852,6 +863,7 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
     uint32_t xm = ring[2][o];
     unsigned nnz = 0;
     long long lsum = 0;
+    unsigned long long lsq = 0;
     const bool jin = own && j < ny, jint = j > 0 && j < ny - 1;
     int cs = 0, ns = 1, fs = 2;
     for (int i = i0; i < i1; ++i) {
@@ -887,20 +899,26 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
             nb0 = (uint32_t)(s6 - 6 * c1) & 0xffffu;
         }
         if (jin) {
-            nnz += __popc(__vcmpne4(pos, neg)) >> 3;
-            atomicAdd(&wh[c & 0xff], 1u);
-            atomicAdd(&wh[(c >> 8) & 0xff], 1u);
-            atomicAdd(&wh[(c >> 16) & 0xff], 1u);
-            atomicAdd(&wh[c >> 24], 1u);
+            if (MODE != 2) {
+                nnz += __popc(__vcmpne4(pos, neg)) >> 3;
+                atomicAdd(&wh[c & 0xff], 1u);
+                atomicAdd(&wh[(c >> 8) & 0xff], 1u);
+                atomicAdd(&wh[(c >> 16) & 0xff], 1u);
+                atomicAdd(&wh[c >> 24], 1u);
+            }
             if (jint && i > 0 && i < nx - 1) {
                 // elements k-1 for k = 4kw+1 .. 4kw+4 (two aligned 32-bit words)
                 const uint32_t e0 = __byte_perm(w01, w23, 0x5432), e1 = __byte_perm(w23, nb0, 0x5432);
+                const int a0 = (int16_t)(e0 & 0xffff), a1 = (int16_t)(e0 >> 16);
+                const int b0 = (int16_t)(e1 & 0xffff), b1 = (int16_t)(e1 >> 16);
                 uint32_t *dst = (uint32_t *)(lap + ((size_t)(i - 1) * my + (j - 1)) * mz + 4 * kw);
-                dst[0] = e0;
-                lsum += (int)(int16_t)(e0 & 0xffff) + (int)(int16_t)(e0 >> 16);
+                if (MODE != 1) dst[0] = e0;
+                if (MODE != 2) lsum += a0 + a1;
+                if (MODE == 1) lsq += (unsigned)(a0 * a0 + a1 * a1);
                 if (kw < W - 1) {
-                    dst[1] = e1;
-                    lsum += (int)(int16_t)(e1 & 0xffff) + (int)(int16_t)(e1 >> 16);
+                    if (MODE != 1) dst[1] = e1;
+                    if (MODE != 2) lsum += b0 + b1;
+                    if (MODE == 1) lsq += (unsigned)(b0 * b0 + b1 * b1);
                 }
             }
         }
@@ -911,14 +929,17 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
         __syncthreads();
         const int t = cs; cs = ns; ns = fs; fs = t;
     }
+    if (MODE == 2) return;
     unsigned long long nnz64 = nnz;
     for (int q = 16; q; q >>= 1) {
         nnz64 += __shfl_xor_sync(0xffffffffu, nnz64, q);
         lsum += __shfl_xor_sync(0xffffffffu, lsum, q);
+        if (MODE == 1) lsq += __shfl_xor_sync(0xffffffffu, lsq, q);
     }
     if ((threadIdx.x & 31) == 0) {
         atomicAdd(&scal[W_NNZ], nnz64);
         atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
+        if (MODE == 1) atomicAdd(&scal[W_LAPSQ], lsq);
     }
     __syncthreads();
     unsigned tt = 0;
@@ -990,8 +1011,36 @@ __global__ void lap_mean(double *state, const long long *sum, i64 n) {
     state[S_SUM1] = __ddiv_rn((double)*sum, (double)n);
 }
 
+// Certified first-step decision without sigma_hat (ct_mrf_decide).  The
+// reference stops before its first step iff ||delta sign(S)|| > sigma_hat
+// (denoise.py:172-176); for integer input the norm is sqrt(delta^2 nnz)
+// exactly, and sigma_hat = std(L)/sqrt(42) <= sqrt(sum L^2 / n)/sqrt(42)
+// (the variance about the mean never exceeds the mean square).  When the
+// norm beats that bound (with a 2^-20 relative margin for the reference's
+// float64 rounding of std) the decision is 0 without the exact pairwise sum;
+// a constant grid (delta 0) is decided too.  Otherwise scal[W_SKIP] stays 0
+// and the exact kernels that follow (guarded by it) compute sigma_hat.
+__global__ void mrf_quick(double *state, i64 n_interior, unsigned long long *scal) {
+    const unsigned long long nnz = scal[W_NNZ];
+    const double delta = state[S_DELTA];
+    const double norm = __dsqrt_rn(__dmul_rn(__dmul_rn(delta, delta), (double)nnz));
+    const double bound = __dmul_rn(__ddiv_rn(__dsqrt_rn(__ddiv_rn((double)scal[W_LAPSQ], (double)n_interior)),
+                                             __dsqrt_rn(42.0)), 1.0 + 0x1p-20);
+    if (n_interior >= 2 && (delta == 0.0 || norm > bound)) {
+        state[S_NNZ] = (double)nnz;
+        state[S_SUM1] = __ddiv_rn((double)(long long)scal[W_LAPSUM], (double)n_interior);
+        state[S_SUM3] = __dmul_rn(__dmul_rn(delta, delta), (double)nnz);
+        state[S_NORM] = norm;
+        state[S_SIGMA] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not computed
+        state[S_SIGMA_STATUS] = 2.0;                  // skipped (decision certified)
+        state[S_DECISION] = delta == 0.0 ? 2.0 : 0.0;
+        scal[W_SKIP] = 1;
+    }
+}
+
 // int_path: norm^2 = delta^2 * nnz (exact); else state[S_SUM3] holds the tree sum
 __global__ void mrf_decide(double *state, i64 n_interior, const unsigned long long *scal, int int_path) {
+    if (scal[W_SKIP]) return;  // certified by mrf_quick
     if (n_interior < 2) {
         state[S_SIGMA] = 0.0;
         state[S_SIGMA_STATUS] = 1.0;
@@ -1086,7 +1135,8 @@ MrfWork mrf_carve(void *work, i64 n, int dtype, i64 ni) {
 }
 
 template <typename T>
-int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint64_t *hist, cudaStream_t s) {
+int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint64_t *hist, cudaStream_t s,
+            bool quick = false) {
     const i64 mx = nx - 2 > 0 ? nx - 2 : 0, my = ny - 2 > 0 ? ny - 2 : 0, mz = nz - 2 > 0 ? nz - 2 : 0;
     const i64 ni = mx * my * mz;
     using LT = typename std::conditional<sizeof(T) == 1, int16_t, int32_t>::type;
@@ -1095,11 +1145,39 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
     if (sizeof(T) == 1 && (nz == 32 || nz == 64 || nz == 96 || nz == 128) && ((uintptr_t)v & 3) == 0 &&
         ((uintptr_t)lap & 3) == 0 &&
         nx * ny * nz < (1ll << 31) && getenv("CT_MRF_SCALAR") == nullptr) {
-        auto kern = nz == 32 ? mrf_stream_v4<32> : nz == 64 ? mrf_stream_v4<64> : nz == 96 ? mrf_stream_v4<96>
-                                                                                      : mrf_stream_v4<128>;
         const i64 b4 = ((ny + 256 / (nz / 4) - 1) / (256 / (nz / 4))) * ((nx + MIPER - 1) / MIPER);
-        kern<<<(unsigned)b4, 256, 0, s>>>((const uint8_t *)v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal,
-                                          (int16_t *)lap);
+        auto launch = [&](auto kern) {
+            kern<<<(unsigned)b4, 256, 0, s>>>((const uint8_t *)v, (int)nx, (int)ny, (unsigned long long *)hist,
+                                              w.scal, (int16_t *)lap);
+        };
+        if (quick && ni >= 2) {
+            // certified decision first; the Laplacians are stored (MODE 2) only if it fails
+            if (nz == 32) launch(mrf_stream_v4<32, 1>);
+            else if (nz == 64) launch(mrf_stream_v4<64, 1>);
+            else if (nz == 96) launch(mrf_stream_v4<96, 1>);
+            else launch(mrf_stream_v4<128, 1>);
+            if (int st = ct::check_launch("mrf_stream_v4")) return st;
+            delta_from_hist<<<1, 1024, 0, s>>>(hist, 256, state);
+            mrf_quick<<<1, 1, 0, s>>>(state, ni, w.scal);
+            if (nz == 32) launch(mrf_stream_v4<32, 2>);
+            else if (nz == 64) launch(mrf_stream_v4<64, 2>);
+            else if (nz == 96) launch(mrf_stream_v4<96, 2>);
+            else launch(mrf_stream_v4<128, 2>);
+            if (int st = ct::check_launch("mrf_stream_v4 (exact sigma)")) return st;
+            lap_mean<<<1, 1, 0, s>>>(state, (const long long *)&w.scal[W_LAPSUM], ni);
+            const int vs = pairwise_sum_lap<LT>(lap, &state[S_SUM1], ni, w.partial, &state[S_SUM2], s, &w.scal[W_SKIP]);
+            if (vs < 0) return -vs;
+            if (vs == 1) {
+                LapArrSq<LT> f{lap, &state[S_SUM1]};
+                if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s)) return st;
+            }
+            mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 1);
+            return ct::check_launch("mrf_decide");
+        }
+        if (nz == 32) launch(mrf_stream_v4<32>);
+        else if (nz == 64) launch(mrf_stream_v4<64>);
+        else if (nz == 96) launch(mrf_stream_v4<96>);
+        else launch(mrf_stream_v4<128>);
         if (int st = ct::check_launch("mrf_stream_v4")) return st;
     } else if ((nz == 32 || nz == 64 || nz == 128) && ((uintptr_t)v & 3) == 0 && nx * ny * nz < (1ll << 31)) {
         auto kern = nz == 32 ? mrf_stream_nz<T, LT, 32> : nz == 64 ? mrf_stream_nz<T, LT, 64> : mrf_stream_nz<T, LT, 128>;
@@ -1195,6 +1273,23 @@ extern "C" int ct_mrf(const void *in, int dtype, int64_t nx, int64_t ny, int64_t
             ct::set_error("unsupported dtype %d", dtype);
             return CT_ERR_UNSUPPORTED;
     }
+}
+
+// ct_mrf with a certified first-step decision (see mrf_quick): identical
+// state except that sigma_hat (state[1]) is NaN with status state[2] = 2 when
+// the decision was certified without it.  Non-u8 / unsupported shapes run the
+// full ct_mrf.
+extern "C" int ct_mrf_decide(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz, void *work,
+                             double *state, uint64_t *hist, void *stream) {
+    if (dtype != CT_U8 || nx <= 0 || ny <= 0 || nz <= 0 || nx * ny * nz >= (1ll << 31) || !hist)
+        return ct_mrf(in, dtype, nx, ny, nz, work, state, hist, stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    const i64 n = nx * ny * nz;
+    MrfWork w = mrf_carve(work, n, dtype, interior(nx, ny, nz));
+    cudaMemsetAsync(state, 0, S_WORDS * sizeof(double), s);
+    cudaMemsetAsync(w.scal, 0, W_WORDS * 8, s);
+    cudaMemsetAsync(&w.scal[W_BEST_BITS], 0xff, 8, s);
+    return mrf_int<uint8_t>((const uint8_t *)in, nx, ny, nz, w, state, hist, s, true);
 }
 
 extern "C" int ct_mrf_step(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *cur,

@@ -209,7 +209,7 @@ class FramePipeline:
         s = _dev.stream_handle()
         self.vhist.zero_()
         e = self._t0()
-        call("ct_mrf", raw.data_ptr(), self.code, nx, ny, nz, self.mwork.data_ptr(), self.state.data_ptr(),
+        call("ct_mrf_decide", raw.data_ptr(), self.code, nx, ny, nz, self.mwork.data_ptr(), self.state.data_ptr(),
              self.vhist.data_ptr(), s)
         self._t1("K7 mrf", e)
         e = self._t0()

@@ -470,3 +470,43 @@ def test_packed_rows_closing_and_ccl(cuda, oracle, shape):
         np.testing.assert_array_equal(outs[0][1], outs[1][1])
         if outs[0][2] is not None:
             np.testing.assert_array_equal(outs[0][2], outs[1][2])
+
+
+@pytest.mark.parametrize("shape", [(40, 36, 64), (16, 16, 32), (20, 18, 96), (12, 14, 70)])
+def test_mrf_decide_certified_vs_exact(cuda, oracle, shape):
+    """ct_mrf_decide (fused pipeline) against ct_mrf and the oracle: same
+    decision, delta, nnz and norm on volumes that stop before the first step
+    (certified without sigma_hat: NaN, status 2), iterate (uniform noise: the
+    bound cannot decide, so the exact sigma_hat is computed) or are constant."""
+    from paper_1407_2089_b200._lib import call, workspace_bytes
+    from paper_1407_2089_b200 import _dev
+
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx + ny + nz)
+    ramp = np.add.outer(np.add.outer(np.arange(nx), np.arange(ny)), np.arange(nz)) % 50
+    vols = {"ramp": (ramp + rng.integers(0, 9, shape)).astype(np.uint8),
+            "noise": rng.integers(0, 256, shape).astype(np.uint8),
+            "const": np.full(shape, 7, np.uint8)}
+    s = _dev.stream_handle()
+    for name, v in vols.items():
+        dv = torch.from_numpy(v).cuda()
+        states = []
+        for fn in ("ct_mrf", "ct_mrf_decide"):
+            work = torch.empty(workspace_bytes(4, nx, ny, nz, 1), dtype=torch.uint8, device="cuda")
+            state = torch.zeros(9, dtype=torch.float64, device="cuda")
+            hist = torch.zeros(65536, dtype=torch.int64, device="cuda")
+            call(fn, dv.data_ptr(), 1, nx, ny, nz, work.data_ptr(), state.data_ptr(), hist.data_ptr(), s)
+            torch.cuda.synchronize()
+            states.append((state.cpu().numpy(), hist.cpu().numpy()))
+        (a, ha), (b, hb) = states
+        np.testing.assert_array_equal(ha, hb)
+        o = oracle.mrf(v)
+        assert a[5] == b[5], (name, a, b)                 # decision
+        assert a[0] == b[0] == o["delta"]                 # delta
+        assert a[3] == b[3] and a[4] == b[4]              # nnz, first-step norm
+        if b[2] == 2.0:                                   # certified: sigma skipped
+            assert np.isnan(b[1]) and a[5] in (0.0, 2.0)
+        else:
+            assert a[1] == b[1] == o["sigma_hat"] and a[2] == b[2]
+        if a[5] == 1.0:
+            assert b[2] != 2.0                            # iterating volume: exact path taken
