@@ -800,6 +800,13 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
     }
 }
 
+// per byte: bit 7 set iff a > b (unsigned), other bits clear.  s7 = [a_lo >
+// b_lo] from (a & 0x7f) + (127 - b_lo); then a > b = (a7 & ~b7) | (a7 == b7 & s7).
+__device__ __forceinline__ uint32_t gt_hi(uint32_t a, uint32_t b) {
+    const uint32_t s = (a & 0x7f7f7f7fu) + (~b & 0x7f7f7f7fu);
+    return ((a & ~b) | (~(a ^ b) & s)) & 0x80808080u;
+}
+
 // u8 input, nz == NZ: 4 voxels per thread as one 32-bit word (SIMD byte
 // compares for the sign sum, packed 16-bit lanes for the Laplacian).  A CTA
 // owns MJ4 = 256 / (NZ/4) rows and walks MIPER planes along i with the same
@@ -807,9 +814,10 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
 // kernels (j, i by the clamped row/plane loads; k by byte replication).
 // MODE 0: histogram, #{sign sum != 0}, Laplacian sum and the Laplacians
 // (lap) for the exact pairwise sigma_hat.  MODE 1 (certified quick decision,
-// ct_mrf_decide): as 0 but the Laplacians are only summed and squared-summed
-// (W_LAPSQ), not stored.  MODE 2: the fallback of MODE 1 -- Laplacians
-// only, and nothing at all when the quick decision certified (scal[W_SKIP]).
+// ct_mrf_decide): histogram, #{sign sum != 0} and the sum of squared forward
+// differences E (W_LAPSQ) of the sigma bound -- no Laplacians.  MODE 2: the
+// fallback of MODE 1 -- Laplacians and their sum only, and nothing at all
+// when the quick decision certified (scal[W_SKIP]).
 template <int NZ, int MODE = 0>
 __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__ v, int nx, int ny,
                                                      unsigned long long *__restrict__ ghist,
@@ -863,15 +871,45 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
     uint32_t xm = ring[2][o];
     unsigned nnz = 0;
     long long lsum = 0;
-    unsigned long long lsq = 0;
     const bool jin = own && j < ny, jint = j > 0 && j < ny - 1;
     int cs = 0, ns = 1, fs = 2;
+    // MODE 1: the x-direction comparisons of plane i against i+1 are reused
+    // as plane i+1's comparisons against its i-1 neighbour (gxm, lxm)
+    uint32_t gxm = 0, lxm = 0;
+    if (MODE == 1) {
+        const uint32_t c0 = ring[0][o];
+        gxm = gt_hi(xm, c0);
+        lxm = gt_hi(c0, xm);
+    }
+    unsigned esq = 0;  // MODE 1: sum of squared forward differences (edge term of the sigma bound)
     for (int i = i0; i < i1; ++i) {
         load_plane(i + 3, regs);  // planes i+2 (regs2) and i+3 (regs) in flight while plane i is processed
         const uint32_t c = ring[cs][o], xp = ring[ns][o];
         const uint32_t ym = ring[cs][o - W], yp = ring[cs][o + W];
         const uint32_t wl = kw > 0 ? ring[cs][o - 1] : c << 24, wr = kw < W - 1 ? ring[cs][o + 1] : c >> 24;
         const uint32_t zm = __funnelshift_l(wl, c, 8), zp = __funnelshift_r(c, wr, 8);
+        if constexpr (MODE == 1) {
+            // sign sum != 0 per byte <=> #(+1 terms) != #(-1 terms) <=> pos ^ neg != 0 (both <= 6)
+            const uint32_t gxp = gt_hi(c, xp), lxp = gt_hi(xp, c);
+            const uint32_t pos = ((gxm >> 7) + (gxp >> 7)) + ((gt_hi(ym, c) >> 7) + (gt_hi(c, yp) >> 7)) +
+                                 ((gt_hi(zm, c) >> 7) + (gt_hi(c, zp) >> 7));
+            const uint32_t neg = ((lxm >> 7) + (lxp >> 7)) + ((gt_hi(c, ym) >> 7) + (gt_hi(yp, c) >> 7)) +
+                                 ((gt_hi(c, zm) >> 7) + (gt_hi(zp, c) >> 7));
+            gxm = gxp;
+            lxm = lxp;
+            if (jin) {
+                nnz += __popc(((pos ^ neg) + 0x7f7f7f7fu) & 0x80808080u);
+                atomicAdd(&wh[c & 0xff], 1u);
+                atomicAdd(&wh[(c >> 8) & 0xff], 1u);
+                atomicAdd(&wh[(c >> 16) & 0xff], 1u);
+                atomicAdd(&wh[c >> 24], 1u);
+                // clamped neighbours make the boundary differences 0
+                const uint32_t dx4 = __vabsdiffu4(c, xp), dy4 = __vabsdiffu4(c, yp), dz4 = __vabsdiffu4(c, zp);
+                esq = __dp4a(dx4, dx4, esq);
+                esq = __dp4a(dy4, dy4, esq);
+                esq = __dp4a(dz4, dz4, esq);
+            }
+        } else {
         // sign sum != 0 per byte: #(+1 terms) != #(-1 terms)
         const uint32_t one = 0x01010101u;
         const uint32_t pos = (__vcmpgtu4(xm, c) & one) + (__vcmpgtu4(c, xp) & one) + (__vcmpgtu4(ym, c) & one) +
@@ -899,7 +937,7 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
             nb0 = (uint32_t)(s6 - 6 * c1) & 0xffffu;
         }
         if (jin) {
-            if (MODE != 2) {
+            if (MODE == 0) {
                 nnz += __popc(__vcmpne4(pos, neg)) >> 3;
                 atomicAdd(&wh[c & 0xff], 1u);
                 atomicAdd(&wh[(c >> 8) & 0xff], 1u);
@@ -909,18 +947,15 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
             if (jint && i > 0 && i < nx - 1) {
                 // elements k-1 for k = 4kw+1 .. 4kw+4 (two aligned 32-bit words)
                 const uint32_t e0 = __byte_perm(w01, w23, 0x5432), e1 = __byte_perm(w23, nb0, 0x5432);
-                const int a0 = (int16_t)(e0 & 0xffff), a1 = (int16_t)(e0 >> 16);
-                const int b0 = (int16_t)(e1 & 0xffff), b1 = (int16_t)(e1 >> 16);
                 uint32_t *dst = (uint32_t *)(lap + ((size_t)(i - 1) * my + (j - 1)) * mz + 4 * kw);
-                if (MODE != 1) dst[0] = e0;
-                if (MODE != 2) lsum += a0 + a1;
-                if (MODE == 1) lsq += (unsigned)(a0 * a0 + a1 * a1);
+                dst[0] = e0;
+                lsum += (int)(int16_t)(e0 & 0xffff) + (int)(int16_t)(e0 >> 16);
                 if (kw < W - 1) {
-                    if (MODE != 1) dst[1] = e1;
-                    if (MODE != 2) lsum += b0 + b1;
-                    if (MODE == 1) lsq += (unsigned)(b0 * b0 + b1 * b1);
+                    dst[1] = e1;
+                    lsum += (int)(int16_t)(e1 & 0xffff) + (int)(int16_t)(e1 >> 16);
                 }
             }
+        }
         }
         xm = c;
         store_plane(fs, regs2);
@@ -929,18 +964,18 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
         __syncthreads();
         const int t = cs; cs = ns; ns = fs; fs = t;
     }
-    if (MODE == 2) return;
-    unsigned long long nnz64 = nnz;
+    unsigned long long nnz64 = nnz, esq64 = esq;
     for (int q = 16; q; q >>= 1) {
         nnz64 += __shfl_xor_sync(0xffffffffu, nnz64, q);
         lsum += __shfl_xor_sync(0xffffffffu, lsum, q);
-        if (MODE == 1) lsq += __shfl_xor_sync(0xffffffffu, lsq, q);
+        if (MODE == 1) esq64 += __shfl_xor_sync(0xffffffffu, esq64, q);
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&scal[W_NNZ], nnz64);
-        atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
-        if (MODE == 1) atomicAdd(&scal[W_LAPSQ], lsq);
+        if (MODE != 2) atomicAdd(&scal[W_NNZ], nnz64);
+        if (MODE != 1) atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
+        if (MODE == 1) atomicAdd(&scal[W_LAPSQ], esq64);
     }
+    if (MODE == 2) return;
     __syncthreads();
     unsigned tt = 0;
 #pragma unroll
@@ -1015,7 +1050,10 @@ __global__ void lap_mean(double *state, const long long *sum, i64 n) {
 // reference stops before its first step iff ||delta sign(S)|| > sigma_hat
 // (denoise.py:172-176); for integer input the norm is sqrt(delta^2 nnz)
 // exactly, and sigma_hat = std(L)/sqrt(42) <= sqrt(sum L^2 / n)/sqrt(42)
-// (the variance about the mean never exceeds the mean square).  When the
+// (variance <= mean square) <= sqrt(12 E / n)/sqrt(42): L = sum of the six
+// (neighbour - centre) differences, so L^2 <= 6 * sum of their squares
+// (Cauchy-Schwarz), and over the interior every grid edge is counted at most
+// twice -- E = sum over all forward edges of the squared difference.  When the
 // norm beats that bound (with a 2^-20 relative margin for the reference's
 // float64 rounding of std) the decision is 0 without the exact pairwise sum;
 // a constant grid (delta 0) is decided too.  Otherwise scal[W_SKIP] stays 0
@@ -1024,11 +1062,10 @@ __global__ void mrf_quick(double *state, i64 n_interior, unsigned long long *sca
     const unsigned long long nnz = scal[W_NNZ];
     const double delta = state[S_DELTA];
     const double norm = __dsqrt_rn(__dmul_rn(__dmul_rn(delta, delta), (double)nnz));
-    const double bound = __dmul_rn(__ddiv_rn(__dsqrt_rn(__ddiv_rn((double)scal[W_LAPSQ], (double)n_interior)),
+    const double bound = __dmul_rn(__ddiv_rn(__dsqrt_rn(__ddiv_rn(12.0 * (double)scal[W_LAPSQ], (double)n_interior)),
                                              __dsqrt_rn(42.0)), 1.0 + 0x1p-20);
     if (n_interior >= 2 && (delta == 0.0 || norm > bound)) {
         state[S_NNZ] = (double)nnz;
-        state[S_SUM1] = __ddiv_rn((double)(long long)scal[W_LAPSUM], (double)n_interior);
         state[S_SUM3] = __dmul_rn(__dmul_rn(delta, delta), (double)nnz);
         state[S_NORM] = norm;
         state[S_SIGMA] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not computed
