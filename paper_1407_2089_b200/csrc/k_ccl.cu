@@ -709,7 +709,7 @@ __global__ void tab_relabel(int32_t *labels, const int32_t *__restrict__ fg, con
 // One warp per kept cell: bbox scan in C order with ballots (no block
 // barriers); the centroid is the row-sequential float64 sum of numpy's
 // mean(axis=0), accumulated by lane 0 in list order via shuffles.
-constexpr int TVB = 8;  // chunks of 32 candidates in flight per warp
+constexpr int TVB = 8;  // chunks of 32 candidates per round; the next round's labels are in flight
 __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ labels, i64 ny, i64 nz,
                                                     const int64_t *__restrict__ counters, ct_cell *table,
                                                     int32_t *__restrict__ voxels, double dx, double dy, double dz) {
@@ -720,29 +720,37 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
     const i64 w0 = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
     for (i64 r = w0; r < nk; r += nw) {
         const int lo0 = table[r].bbox_lo[0], lo1 = table[r].bbox_lo[1], lo2 = table[r].bbox_lo[2];
-        const int bi = table[r].bbox_hi[0] - lo0 + 1, bj = table[r].bbox_hi[1] - lo1 + 1,
-                  bk = table[r].bbox_hi[2] - lo2 + 1;
+        const unsigned bi = table[r].bbox_hi[0] - lo0 + 1, bj = table[r].bbox_hi[1] - lo1 + 1,
+                       bk = table[r].bbox_hi[2] - lo2 + 1;
         const i64 off = table[r].voxel_offset;
-        const i64 nbox = (i64)bi * bj * bk;
+        const unsigned nbox = bi * bj * bk;  // < 2^31 (volumes < 2^31 voxels)
+        const unsigned bjk = bj * bk;
         i64 written = 0;
         double sx = 0.0, sy = 0.0, sz = 0.0;
-        for (i64 q00 = 0; q00 < nbox; q00 += 32 * TVB) {
-            // labels of TVB chunks in flight, then ballots / list / sums in order
-            int32_t pv[TVB], lv[TVB];
-            int av[TVB], bv[TVB], cv[TVB];
+        // candidate q -> linear index (32-bit index math; q < nbox)
+        auto lin = [&](unsigned q) -> int32_t {
+            const unsigned a = q / bjk, rem = q - a * bjk, b = rem / bk, c = rem - b * bk;
+            return (int32_t)(((i64)(lo0 + (int)a) * ny + (lo1 + (int)b)) * nz + (lo2 + (int)c));
+        };
+        int32_t pn[TVB], ln[TVB];  // next round: linear indices and labels in flight
+        auto fetch = [&](unsigned q0, int32_t (&pv)[TVB], int32_t (&lv)[TVB]) {
 #pragma unroll
             for (int u = 0; u < TVB; ++u) {
-                const i64 q = q00 + 32 * u + lane;
-                pv[u] = 0; lv[u] = -2; av[u] = bv[u] = cv[u] = 0;
+                const unsigned q = q0 + 32 * u + lane;
+                pv[u] = 0;
+                lv[u] = -2;
                 if (q < nbox) {
-                    cv[u] = (int)(q % bk);
-                    const i64 t2 = q / bk;
-                    bv[u] = (int)(t2 % bj);
-                    av[u] = (int)(t2 / bj);
-                    pv[u] = (int32_t)(((i64)(lo0 + av[u]) * ny + (lo1 + bv[u])) * nz + (lo2 + cv[u]));
+                    pv[u] = lin(q);
                     lv[u] = __ldg(labels + pv[u]);
                 }
             }
+        };
+        fetch(0, pn, ln);
+        for (unsigned q00 = 0; q00 < nbox; q00 += 32 * TVB) {
+            int32_t pv[TVB], lv[TVB];
+#pragma unroll
+            for (int u = 0; u < TVB; ++u) { pv[u] = pn[u]; lv[u] = ln[u]; }
+            if (q00 + 32 * TVB < nbox) fetch(q00 + 32 * TVB, pn, ln);
 #pragma unroll
             for (int u = 0; u < TVB; ++u) {
                 const bool hit = lv[u] == (int32_t)r;
@@ -752,10 +760,12 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
                 // slots, then lane 0 continues the row-sequential sum
                 const int nh = __popc(m);
                 if (hit) {
+                    const unsigned q = q00 + 32 * u + lane;
+                    const unsigned a = q / bjk, rem = q - a * bjk, b = rem / bk, c = rem - b * bk;
                     double *slot = cs + 3 * __popc(m & ((1u << lane) - 1));
-                    slot[0] = __dmul_rn((double)(lo0 + av[u]), dx);
-                    slot[1] = __dmul_rn((double)(lo1 + bv[u]), dy);
-                    slot[2] = __dmul_rn((double)(lo2 + cv[u]), dz);
+                    slot[0] = __dmul_rn((double)(lo0 + (int)a), dx);
+                    slot[1] = __dmul_rn((double)(lo1 + (int)b), dy);
+                    slot[2] = __dmul_rn((double)(lo2 + (int)c), dz);
                 }
                 __syncwarp();
                 if (lane == 0) {

@@ -510,5 +510,5 @@ def test_mrf_decide_certified_vs_exact(cuda, oracle, shape):
             assert a[1] == b[1] == o["sigma_hat"] and a[2] == b[2]
         if a[5] == 1.0:
             assert b[2] != 2.0                            # iterating volume: exact path taken
-        if name == "ramp":
+        if name == "ramp" and nz in (32, 64, 96, 128):  # (other nz: the generic stream, no quick path)
             assert b[2] == 2.0                            # smooth + noise: certified without sigma_hat
