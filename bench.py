@@ -484,6 +484,8 @@ def run_e2e(args, pipe, spec, sp, dev, world, s_cell, s_vess):
     val = world * args.steps * 2 * nvox / (ms / 1e3)
     return {"value": val, "unit": UNIT, "h2d_bytes_per_step": 2 * nvox,
             "d2h_bytes_per_step": int(rbytes), "ms_per_step": ms / args.steps,
+            # the H2D of the raw frames over PCIe is the e2e bound once the device step is shorter
+            "h2d_gbs": 2 * nvox / (ms / args.steps / 1e3) / 1e9,
             "note": "pinned host frames, H2D up to two time points ahead of compute (3 device slots, one copy "
                     f"stream per channel); per step D2H of counters, first {rows} table rows and the vessel "
                     "state, read on the host while the next time point runs"}
