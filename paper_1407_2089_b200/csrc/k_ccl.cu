@@ -663,6 +663,60 @@ __global__ void __launch_bounds__(256) tab_rank_keys(const int64_t *__restrict__
     w.sb[r] = w.sa[e];
 }
 
+// Rank + voxel offset + table row in one pass, one warp per kept cell (all
+// SMs; replaces tab_rank_keys + the single-CTA tab_emit, which was bound by
+// one SM's memory pipe): rank = #{keys < k}, voxel offset = sum of the counts
+// of those keys (= the exclusive scan in rank order), lanes split the key
+// range; the 128-byte row is written by 16 lanes, one field each.
+__global__ void __launch_bounds__(256) tab_rank_emit(int64_t *counters, TabWork w, double vv, i64 id_start,
+                                                     ct_cell *table) {
+    __shared__ u64 key[RK];
+    __shared__ uint32_t cnt[RK];
+    const i64 nk = counters[CT_CNT_KEPT];
+    if (nk > RK || (i64)blockIdx.x * 8 >= nk) return;
+    for (i64 e = threadIdx.x; e < nk; e += 256) {
+        const int c = w.sa[e];
+        key[e] = order_key(w, c);
+        cnt[e] = w.count[c];
+    }
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31;
+    const i64 e = (i64)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (e >= nk) return;
+    const u64 k = key[e];
+    unsigned r = 0;
+    u64 v = 0;
+    for (int f = (int)lane; f < (int)nk; f += 32) {
+        const bool lt = key[f] < k;
+        r += lt;
+        v += lt ? cnt[f] : 0u;
+    }
+    for (int o = 16; o; o >>= 1) {
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    const int c = w.sa[e];
+    if (lane == 0) {
+        w.rank[c] = (int32_t)r;
+        w.sb[r] = c;
+        if ((i64)r == nk - 1) counters[CT_CNT_KEPT_VOXELS] = (int64_t)(v + cnt[e]);
+    }
+    if (lane < 16) {
+        int64_t f;
+        switch (lane) {
+            case 0: f = id_start + (i64)r; break;
+            case 1: f = (int64_t)cnt[e]; break;
+            case 2: f = w.root[c]; break;
+            case 3: case 4: case 5: case 6: case 7: case 8: f = w.bbox[6 * c + (lane - 3)]; break;
+            case 9: f = (int64_t)w.isum[c]; break;
+            case 13: f = __double_as_longlong(__dmul_rn((double)cnt[e], vv)); break;
+            case 14: f = (int64_t)v; break;
+            default: f = 0; break;  // centroid (tab_voxels_w), reserved
+        }
+        reinterpret_cast<int64_t *>(table + r)[lane] = f;
+    }
+}
+
 // table rows in rank order, voxel offsets by an exclusive scan (one CTA)
 __global__ void __launch_bounds__(1024) tab_emit(int64_t *counters, TabWork w, double vv, i64 id_start,
                                                  ct_cell *table) {
@@ -939,8 +993,13 @@ extern "C" int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz
     if (int st = ct::check_launch("tab_stats")) return st;
     cudaMemsetAsync(&counters[CT_CNT_KEPT], 0, sizeof(int64_t), s);
     tab_keep<<<CT_NUM_SMS * 2, 256, 0, s>>>(counters, w, cap, vv, min_volume_um3);
-    tab_rank_keys<<<(unsigned)((std::min<i64>(cap, RK) + 255) / 256), 256, 0, s>>>(counters, w);
-    tab_emit<<<1, 1024, 0, s>>>(counters, w, vv, id_start, table);
+    static const bool emit1 = getenv("CT_TAB_EMIT1") != nullptr;  // A/B knob: the previous two-kernel form
+    if (emit1) {
+        tab_rank_keys<<<(unsigned)((std::min<i64>(cap, RK) + 255) / 256), 256, 0, s>>>(counters, w);
+        tab_emit<<<1, 1024, 0, s>>>(counters, w, vv, id_start, table);
+    } else {
+        tab_rank_emit<<<(unsigned)((std::min<i64>(cap, RK) + 7) / 8), 256, 0, s>>>(counters, w, vv, id_start, table);
+    }
     tab_rank<<<1, RT, 0, s>>>(counters, w, cap, N, vv, min_volume_um3, id_start, table);
     if (int st = ct::check_launch("tab_rank")) return st;
     tab_relabel<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters, w);
