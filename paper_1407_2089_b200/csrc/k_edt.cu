@@ -231,6 +231,36 @@ __global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4(const uint8_t *__rest
         for (int yy = y + 1; yy < 32; ++yy)
             if (segF[yy][4 * c + q] >= 0) { rc[q] = segF[yy][4 * c + q]; break; }
     }
+    // segments without foreground in their own rows (most of a sparse mask):
+    // the nearest foreground is lc or rc for every row, no bit scans
+    if (!(bits[0] | bits[1] | bits[2] | bits[3])) {
+        if (max(max(lc[0], lc[1]), max(lc[2], lc[3])) < 0 && max(max(rc[0], rc[1]), max(rc[2], rc[3])) < 0) {
+            const uint32_t none2 = (uint32_t)(uint16_t)NONE16 * 0x10001u;  // no foreground on the lines at all
+#pragma unroll 8
+            for (int u = 0; u < 32; ++u) {
+                const int x = row0 + u;
+                if (x >= nx) break;
+                *(uint2 *)(di + (i64)x * S + l0) = make_uint2(none2, none2);
+            }
+            return;
+        }
+#pragma unroll 4
+        for (int u = 0; u < 32; ++u) {
+            const int x = row0 + u;
+            if (x >= nx) break;
+            uint32_t packed[2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                int best = lc[q];
+                if (rc[q] >= 0 && (best < 0 || rc[q] - x < x - best)) best = rc[q];
+                const uint32_t d = (uint16_t)(best < 0 ? NONE16 : (int16_t)(best - x));
+                if (q & 1) packed[q >> 1] |= d << 16;
+                else packed[q >> 1] = d;
+            }
+            *(uint2 *)(di + (i64)x * S + l0) = make_uint2(packed[0], packed[1]);
+        }
+        return;
+    }
 #pragma unroll 4
     for (int u = 0; u < 32; ++u) {
         const int x = row0 + u;

@@ -512,3 +512,15 @@ def test_mrf_decide_certified_vs_exact(cuda, oracle, shape):
             assert b[2] != 2.0                            # iterating volume: exact path taken
         if name == "ramp" and nz in (32, 64, 96, 128):  # (other nz: the generic stream, no quick path)
             assert b[2] == 2.0                            # smooth + noise: certified without sigma_hat
+
+
+@pytest.mark.parametrize("shape,density", [((200, 24, 64), 1e-3), ((130, 20, 32), 3e-4), ((1024, 4, 64), 2e-5)])
+def test_edt_sparse_masks_vs_oracle(cuda, oracle, shape, density):
+    """EDT on sparse masks: pass-x segments with no foreground of their own
+    (nearest from neighbouring segments only), whole lines without foreground
+    (NONE throughout), and lines whose only foreground is far away -- bit-exact
+    against the oracle."""
+    rng = np.random.default_rng(int(1 / density))
+    m = rng.random(shape) < density
+    m[0, 0, 0] = True  # never empty
+    np.testing.assert_array_equal(S.distance_map(m, ANISO).values, oracle.edt(m, ANISO.as_array()))
