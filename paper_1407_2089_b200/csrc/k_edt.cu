@@ -14,10 +14,12 @@
 //            sites are sparse after pass x (only columns that hold foreground),
 //            so each thread's stack lives in SMEM (global spill past 16).
 //                                                           2 B in, 4 B (dj,di) out
-//   pass z : per (i,j) line along the contiguous k (nz <= 128): a CTA stages
-//            128 whole lines in SMEM (coalesced), runs the envelope of
-//            (di*dx)^2 + (dj*dy)^2 + ((k-q)*dz)^2 per thread entirely in SMEM
-//            and writes the float64 distances back coalesced.  4 B in, 8 B out
+//   pass z : per (i,j) line along the contiguous k (nz in {32, 64, 96}): one
+//            thread streams its line from global memory, builds the envelope
+//            of (di*dx)^2 + (dj*dy)^2 + ((k-q)*dz)^2 with its stack in SMEM,
+//            computes the switch points per entry, then sweeps the voxels
+//            forming the float64 distances (32-byte stores; edt_pass_zr).
+//            Other nz: SMEM-staged lines (edt_pass_z).      4 B in, 8 B out
 // Lines of passes x and y map to consecutive k across a warp (coalesced).  The
 // envelope uses division-free predicates; arithmetic is identical to
 // oracle/ct_oracle.c ora_edt, so results match it bit for bit; equidistant
@@ -279,160 +281,6 @@ __global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4(const uint8_t *__rest
             else packed[q >> 1] = d;
         }
         *(uint2 *)(di + (i64)x * S + l0) = make_uint2(packed[0], packed[1]);
-    }
-}
-
-// Same pass, leaner per-row work (edt_pass_x_seg4 was ALU bound: two masks,
-// clz and ffs per voxel and line): the nearest foreground at or below the row
-// is carried forward (one bit test and select per voxel) and the nearest at or
-// above is recomputed by ffs only after the walk passes it, i.e. once per
-// foreground voxel.  Rows fully unrolled.
-__global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4b(const uint8_t *__restrict__ mask, i64 nlines, int nx,
-                                                            int16_t *__restrict__ di) {
-    __shared__ int segL[32][4 * XG + 1], segF[32][4 * XG + 1];
-    const int c = threadIdx.x, y = threadIdx.y;
-    const i64 l0 = blockIdx.x * (4ll * XG) + 4 * c;
-    const bool valid = l0 < nlines;
-    const i64 S = nlines;
-    const int row0 = y * 32;
-    uint32_t bits[4] = {0, 0, 0, 0};
-    {
-        uint32_t v[32];
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-            const int x = row0 + u;
-            v[u] = (valid && x < nx) ? __ldg((const uint32_t *)(mask + (i64)x * S + l0)) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-            // nonzero bytes -> bit 7 of each byte, then gather the 4 flags
-            const uint32_t nzb = ((v[u] & 0x7f7f7f7fu) + 0x7f7f7f7fu) | v[u];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) bits[q] |= ((nzb >> (8 * q + 7)) & 1u) << u;
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        segL[y][4 * c + q] = bits[q] ? row0 + 31 - __clz(bits[q]) : -1;
-        segF[y][4 * c + q] = bits[q] ? row0 + __ffs(bits[q]) - 1 : -1;
-    }
-    __syncthreads();
-    if (!valid) return;
-    int last[4], nxt[4], rcv[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        int lc = -1, rc = -1;
-        for (int yy = y - 1; yy >= 0; --yy)
-            if (segL[yy][4 * c + q] >= 0) { lc = segL[yy][4 * c + q]; break; }
-        for (int yy = y + 1; yy < 32; ++yy)
-            if (segF[yy][4 * c + q] >= 0) { rc = segF[yy][4 * c + q]; break; }
-        last[q] = lc;
-        rcv[q] = rc < 0 ? INT_MAX / 2 : rc;
-        nxt[q] = bits[q] ? row0 + __ffs(bits[q]) - 1 : rc;
-        if (nxt[q] < 0) nxt[q] = INT_MAX / 2;  // no foreground above: never closer
-    }
-    const int nrows = min(32, nx - row0);
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-        if (u >= nrows) break;
-        const int x = row0 + u;
-        uint32_t d[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t b = bits[q];
-            if ((b >> u) & 1u) {
-                last[q] = x;
-                nxt[q] = x;
-            } else if (x > nxt[q]) {  // walked past the nearest foreground above: next one
-                // (none left in this segment: the first of the next non-empty one)
-                const uint32_t rem = u < 31 ? b >> (u + 1) : 0u;
-                nxt[q] = rem ? x + __ffs(rem) : rcv[q];
-            }
-            int best = last[q];
-            if (nxt[q] < INT_MAX / 2 && (best < 0 || nxt[q] - x < x - best)) best = nxt[q];
-            d[q] = (uint16_t)(best < 0 ? NONE16 : (int16_t)(best - x));
-        }
-        *(uint2 *)(di + (i64)x * S + l0) = make_uint2(d[0] | (d[1] << 16), d[2] | (d[3] << 16));
-    }
-}
-
-// Same pass without clz / ffs (edt_pass_x_seg4 is XU bound: two bit scans per
-// voxel and line): a backward sweep over the segment's rows carries the
-// nearest foreground at or above each row and parks the distances in the
-// output rows (the thread's own 8-byte words; re-read from L2), then a forward
-// sweep carries the nearest at or below and picks (ties -> lower i).
-__global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4c(const uint8_t *__restrict__ mask, i64 nlines, int nx,
-                                                            int16_t *__restrict__ di) {
-    __shared__ int segL[32][4 * XG + 1], segF[32][4 * XG + 1];
-    const int c = threadIdx.x, y = threadIdx.y;
-    const i64 l0 = blockIdx.x * (4ll * XG) + 4 * c;
-    const bool valid = l0 < nlines;
-    const i64 S = nlines;
-    const int row0 = y * 32;
-    uint32_t bits[4] = {0, 0, 0, 0};
-    {
-        uint32_t v[32];
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-            const int x = row0 + u;
-            v[u] = (valid && x < nx) ? __ldg((const uint32_t *)(mask + (i64)x * S + l0)) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-            const uint32_t nzb = ((v[u] & 0x7f7f7f7fu) + 0x7f7f7f7fu) | v[u];  // bit 7 of each byte: byte != 0
-#pragma unroll
-            for (int q = 0; q < 4; ++q) bits[q] |= ((nzb >> (8 * q + 7)) & 1u) << u;
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        segL[y][4 * c + q] = bits[q] ? row0 + 31 - __clz(bits[q]) : -1;
-        segF[y][4 * c + q] = bits[q] ? row0 + __ffs(bits[q]) - 1 : -1;
-    }
-    __syncthreads();
-    if (!valid) return;
-    constexpr int BIG = 1 << 20, CAP = 0x7fff;  // CAP: "no foreground on this side" (nx <= 1024)
-    const int nrows = min(32, nx - row0);
-    int last[4], nxt[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        int lc = -1, rc = -1;
-        for (int yy = y - 1; yy >= 0; --yy)
-            if (segL[yy][4 * c + q] >= 0) { lc = segL[yy][4 * c + q]; break; }
-        for (int yy = y + 1; yy < 32; ++yy)
-            if (segF[yy][4 * c + q] >= 0) { rc = segF[yy][4 * c + q]; break; }
-        last[q] = lc >= 0 ? lc : -BIG;
-        nxt[q] = rc >= 0 ? rc : BIG;
-    }
-    // backward: distance to the nearest foreground at or above, parked in di
-#pragma unroll 8
-    for (int u = 31; u >= 0; --u) {
-        if (u >= nrows) continue;
-        const int x = row0 + u;
-        uint32_t d[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if ((bits[q] >> u) & 1u) nxt[q] = x;
-            d[q] = (uint32_t)min(nxt[q] - x, CAP);
-        }
-        *(uint2 *)(di + (i64)x * S + l0) = make_uint2(d[0] | (d[1] << 16), d[2] | (d[3] << 16));
-    }
-    // forward: nearest at or below, pick (ties -> lower i)
-#pragma unroll 8
-    for (int u = 0; u < 32; ++u) {
-        if (u >= nrows) break;
-        const int x = row0 + u;
-        const uint2 rp = *(const uint2 *)(di + (i64)x * S + l0);
-        const uint32_t rw[4] = {rp.x & 0xffffu, rp.x >> 16, rp.y & 0xffffu, rp.y >> 16};
-        uint32_t d[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if ((bits[q] >> u) & 1u) last[q] = x;
-            const int ld = min(x - last[q], CAP), rd = (int)rw[q];
-            const int dv = ld <= rd ? -ld : rd;
-            d[q] = (uint16_t)(min(ld, rd) >= CAP ? NONE16 : (int16_t)dv);
-        }
-        *(uint2 *)(di + (i64)x * S + l0) = make_uint2(d[0] | (d[1] << 16), d[2] | (d[3] << 16));
     }
 }
 
@@ -882,171 +730,6 @@ __global__ void __launch_bounds__(ZLN) edt_pass_zp(const int32_t *__restrict__ i
     }
 }
 
-// Pass z, third form.  Same envelope and arithmetic as edt_pass_zp; the
-// distance phase is reworked (it was ~40% of the kernel's instructions):
-//   * each thread forms 4 consecutive voxels of a line (one 32-bit SMEM load
-//     of their feature positions, two 16-byte stores); the site cost
-//     gyz(site) is formed once per distinct feature among the 4;
-//   * the z term sq((f - x) * dz) comes from a CTA table over f - x in
-//     (-NZ, NZ) (same operations, so the same bits).
-// GD = true: the load phase forms every element's cost (t0 + t1) as float64
-// into SMEM (voxel-parallel), so neither the envelope nor the distance phase
-// converts or multiplies offsets; it costs 8 instead of 4 SMEM bytes per
-// element (fewer lines per SM).
-template <int NZ, int ZLN, bool GD>
-constexpr size_t zq_smem() {
-    return (size_t)ZLN * (NZ + 1) * (GD ? 8 : 4) + 2 * (size_t)ZLN * (NZ + 4) + (size_t)(2 * NZ) * 8;
-}
-
-template <int NZ, int ZLN, bool GD>
-__global__ void __launch_bounds__(ZLN) edt_pass_zq(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
-                                                  double dz, double *__restrict__ out) {
-    constexpr int S = NZ + 1;   // padded line stride (conflict-free)
-    constexpr int SB = NZ + 4;  // byte rows (multiple of 4: 32-bit loads of 4 positions)
-    extern __shared__ __align__(16) unsigned char zsm[];
-    double *czt = (double *)zsm;                       // [2 NZ]: czt[d + NZ] = sq(d * dz)
-    double *gd = czt + 2 * NZ;                         // GD: [ZLN][S] costs
-    int32_t *ps = (int32_t *)(czt + 2 * NZ);           // !GD: [ZLN][S] packed offsets
-    uint8_t *stk = (uint8_t *)(czt + 2 * NZ) + (size_t)ZLN * S * (GD ? 8 : 4);
-    uint8_t *fid = stk + ZLN * SB;
-
-    for (int d = threadIdx.x; d < 2 * NZ; d += ZLN) czt[d] = sq(__dmul_rn((double)(d - NZ), dz));
-    const i64 l0 = blockIdx.x * (i64)ZLN;
-    const int nl = (int)min((i64)ZLN, nlines - l0);
-    const int32_t *src = in + l0 * NZ;
-    constexpr int T4 = ZLN * NZ / 4;
-    for (int i0 = threadIdx.x; i0 < T4; i0 += 8 * ZLN) {
-        int4 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int q = i0 + u * ZLN;
-            if (q < T4 && q * 4 < nl * NZ) v[u] = __ldg((const int4 *)src + q);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int q = i0 + u * ZLN;
-            if (q < T4 && q * 4 < nl * NZ) {
-                const int idx = q * 4, g = idx / NZ, k = idx - g * NZ;
-                if constexpr (GD) {
-                    double *d = gd + g * S + k;
-                    d[0] = v[u].x == NONE32 ? INFINITY : gyz(v[u].x, dx, dy);
-                    d[1] = v[u].y == NONE32 ? INFINITY : gyz(v[u].y, dx, dy);
-                    d[2] = v[u].z == NONE32 ? INFINITY : gyz(v[u].z, dx, dy);
-                    d[3] = v[u].w == NONE32 ? INFINITY : gyz(v[u].w, dx, dy);
-                } else {
-                    int32_t *d = ps + g * S + k;
-                    d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    const double d2 = __dmul_rn(dz, dz);
-    const int t = threadIdx.x;
-    if (t < nl) {
-        uint8_t *st = stk + t * SB;
-        uint8_t *fo = fid + t * SB;
-        int K = 0, tp = 0, bp = 0;
-        double tg = 0.0, bg = 0.0;
-        if constexpr (GD) {
-            const double *G = gd + t * S;
-            double gnx = G[0];
-            for (int x = 0; x < NZ; ++x) {
-                const double gx = gnx;
-                gnx = x + 1 < NZ ? G[x + 1] : INFINITY;  // next element in flight
-                if (gx == INFINITY) continue;
-                while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-                    --K;
-                    tp = bp;
-                    tg = bg;
-                    if (K >= 2) {
-                        bp = st[K - 2];
-                        bg = G[bp];
-                    }
-                }
-                st[K++] = (uint8_t)x;
-                bp = tp; bg = tg; tp = x; tg = gx;
-            }
-        } else {
-            const int32_t *P = ps + t * S;
-            int32_t pcur = P[0];
-            for (int x = 0; x < NZ; ++x) {
-                const int32_t px = pcur;
-                pcur = x + 1 < NZ ? P[x + 1] : NONE32;
-                if (px == NONE32) continue;
-                const double gx = gyz(px, dx, dy);
-                while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-                    --K;
-                    tp = bp;
-                    tg = bg;
-                    if (K >= 2) {
-                        bp = st[K - 2];
-                        bg = gyz(P[bp], dx, dy);
-                    }
-                }
-                st[K++] = (uint8_t)x;
-                bp = tp; bg = tg; tp = x; tg = gx;
-            }
-        }
-        if (K == 0) {
-            for (int x = 0; x < NZ; x += 4) *(uint32_t *)(fo + x) = 0xffffffffu;
-        } else {
-            auto G = [&](int x) -> double {
-                if constexpr (GD) return gd[t * S + x];
-                else return gyz(ps[t * S + x], dx, dy);
-            };
-            int e = 0;
-            int cp = st[0], np = K > 1 ? st[1] : 0;
-            double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
-            int sw = K > 1 ? first_past(0, NZ, np, ng, cp, cg, d2) : NZ;
-            int x = 0;
-            for (;;) {
-                for (; x < sw; ++x) fo[x] = (uint8_t)cp;
-                if (x >= NZ) break;
-                ++e;
-                cp = np; cg = ng;
-                if (e + 1 < K) {
-                    np = st[e + 1];
-                    ng = G(np);
-                    sw = first_past(x, NZ, np, ng, cp, cg, d2);
-                } else {
-                    sw = NZ;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    // distances: thread = 4 consecutive voxels of one line
-    double *dst = out + l0 * NZ;
-    constexpr int NQ = NZ / 4;
-    const int totq = nl * NQ;
-#pragma unroll 2
-    for (int iq = threadIdx.x; iq < totq; iq += ZLN) {
-        const int g = iq / NQ, x0 = (iq - g * NQ) * 4;
-        const uint32_t f4 = *(const uint32_t *)(fid + g * SB + x0);
-        double r[4];
-        int fprev = -1;
-        double gprev = 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int f = (f4 >> (8 * u)) & 0xff;
-            if (f == 255) {
-                r[u] = INFINITY;
-                continue;
-            }
-            if (f != fprev) {
-                if constexpr (GD) gprev = gd[g * S + f];
-                else gprev = gyz(ps[g * S + f], dx, dy);
-                fprev = f;
-            }
-            r[u] = __dsqrt_rn(__dadd_rn(gprev, czt[f - (x0 + u) + NZ]));
-        }
-        double2 *o = (double2 *)(dst + (i64)g * NZ + x0);
-        o[0] = make_double2(r[0], r[1]);
-        o[1] = make_double2(r[2], r[3]);
-    }
-}
-
 // Pass z, register-streamed form.  ncu on edt_pass_zp: the thread-per-line
 // envelope is latency bound (wait stalls, 16 warps/SM) and the SMEM staging of
 // whole lines (396 B per line) is what caps the warps.  Here a thread streams
@@ -1184,11 +867,9 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     uint32_t *spill = (uint32_t *)((char *)pk + (((size_t)N * 4 + 255) & ~(size_t)255));
     const i64 lx = ny * nz, ly = nx * nz, lz = nx * ny;
     if (nx <= 1024 && lx % 4 == 0 && ((uintptr_t)mask & 3) == 0 && ((uintptr_t)di & 7) == 0) {
-        // A/B knob CT_EDT_XV: 0 edt_pass_x_seg4 (99 us on C2), 1 edt_pass_x_seg4b (137 us), 2 edt_pass_x_seg4c (105 us)
-        static const int xv = getenv("CT_EDT_XV") ? atoi(getenv("CT_EDT_XV")) : 0;
-        if (xv == 2) edt_pass_x_seg4c<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
-        else if (xv == 0) edt_pass_x_seg4<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
-        else edt_pass_x_seg4b<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
+        // (tried: bit scans only after passing a foreground, and a backward sweep
+        // parking right distances in the output -- both slower, 137 / 105 us vs 99)
+        edt_pass_x_seg4<<<(unsigned)((lx + 4 * XG - 1) / (4 * XG)), dim3(XG, 32), 0, s>>>(mask, lx, (int)nx, di);
     } else if (nx <= 1024) {
         edt_pass_x_seg<1><<<(unsigned)((lx + 31) / 32), dim3(32, 32), 0, s>>>(mask, lx, (int)nx, di);
     } else if (nx <= 4096) {
@@ -1223,24 +904,17 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             kern<<<(unsigned)((lz + zln - 1) / zln), zln, smem, s>>>(pk, lz, dx, dy, dz, out);
         };
-        static const int zv = getenv("CT_EDT_ZV") ? atoi(getenv("CT_EDT_ZV")) : 3;  // pass-z form (A/B knob)
+        static const int zv = getenv("CT_EDT_ZV") ? atoi(getenv("CT_EDT_ZV")) : 3;  // pass-z form (A/B knob: 0 = edt_pass_zp)
+        // (tried: 4-voxel distance phase over SMEM-staged lines, with packed offsets or float64 costs -- 490 / 654 us vs 468 for zp)
         if (zv == 0) {
             if (nz == 64) launch(edt_pass_zp<64, ZL>, ZL, zp_smem<64, ZL>());
             else if (nz == 32) launch(edt_pass_zp<32, ZL>, ZL, zp_smem<32, ZL>());
             else launch(edt_pass_zp<96, 64>, 64, zp_smem<96, 64>());
-        } else if (zv == 1) {
-            if (nz == 64) launch(edt_pass_zq<64, 128, false>, 128, zq_smem<64, 128, false>());
-            else if (nz == 32) launch(edt_pass_zq<32, 128, false>, 128, zq_smem<32, 128, false>());
-            else launch(edt_pass_zq<96, 64, false>, 64, zq_smem<96, 64, false>());
-        } else if (zv == 3) {
+        } else {
             const unsigned g = (unsigned)((lz + ZRT - 1) / ZRT);
             if (nz == 64) edt_pass_zr<64, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
             else if (nz == 32) edt_pass_zr<32, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
             else edt_pass_zr<96, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
-        } else {
-            if (nz == 64) launch(edt_pass_zq<64, 64, true>, 64, zq_smem<64, 64, true>());
-            else if (nz == 32) launch(edt_pass_zq<32, 128, true>, 128, zq_smem<32, 128, true>());
-            else launch(edt_pass_zq<96, 32, true>, 32, zq_smem<96, 32, true>());
         }
         return ct::check_launch("edt_pass_z");
     }
