@@ -504,6 +504,52 @@ __global__ void fix_p1(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz, con
     }
 }
 
+// Same phase 1 for nz % 32 == 0, rx <= 64: a warp's 32 values share (entry,
+// tt) and read consecutive kk, so the warp first stages the (2rx+1) x 32 raw
+// values of its taps in SMEM (one 32-element row chunk per lane and load
+// round, all in flight together) and then runs scipy's accumulation from SMEM
+// -- the per-thread form waited on one memory round trip per 8 taps.
+constexpr int FXR = 64;  // max rx of the staged form
+template <typename Traw>
+__global__ void __launch_bounds__(128) fix_p1s(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz,
+                                               const double *__restrict__ w, int rx, int ry,
+                                               const unsigned long long *__restrict__ fix, long long cap,
+                                               long long capF, double *__restrict__ P1) {
+    __shared__ Traw buf[4][(2 * FXR + 1) * 32];
+    const long long F = min(min((long long)fix[0], cap), capF);
+    const i64 RJ = 2 * ry + 1, per = RJ * nz, S = ny * nz, tot = F * per;
+    const unsigned lane = threadIdx.x & 31;
+    Traw *b = buf[threadIdx.x >> 5];
+    const int nr = 2 * rx + 1;
+    for (i64 e0 = blockIdx.x * (i64)blockDim.x + (threadIdx.x & ~31u); e0 < tot; e0 += (i64)gridDim.x * blockDim.x) {
+        const i64 f = e0 / per, rem = e0 - f * per, tt = rem / nz, kk0 = rem - tt * nz;  // kk0 % 32 == 0
+        const i64 p = (i64)fix[2 + f];
+        const i64 j = (p / nz) % ny, i = p / S;
+        const i64 jj = ct::clampi(j + tt - ry, 0, ny - 1);
+        const Traw *col = raw + jj * nz + kk0;
+        // lane r stages tap row r (clamped), 32 consecutive values
+        for (int r = (int)lane; r < nr; r += 32) {
+            const Traw *src = col + ct::clampi(i - rx + r, 0, nx - 1) * S;
+            if constexpr (sizeof(Traw) == 1) {
+                const uint4 a = __ldg((const uint4 *)src), c = __ldg((const uint4 *)src + 1);
+                *(uint4 *)(b + r * 32) = a;
+                *(uint4 *)(b + r * 32 + 16) = c;
+            } else {
+#pragma unroll
+                for (int q = 0; q < 32; ++q) b[r * 32 + q] = src[q];
+            }
+        }
+        __syncwarp();
+        const Traw *cb = b + lane;
+        double acc = __dmul_rn(ct::to_f64(cb[rx * 32]), w[0]);
+        for (int d = rx; d >= 1; --d)
+            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(ct::to_f64(cb[(rx - d) * 32]), ct::to_f64(cb[(rx + d) * 32])),
+                                           w[d]));
+        if (e0 + lane < tot) P1[e0 + lane] = acc;
+        __syncwarp();
+    }
+}
+
 // phases 2+3: one CTA (nz threads) per entry: P2 line in SMEM, then pass z +
 // residual at the voxel
 template <typename Traw, typename Tq>
@@ -546,6 +592,48 @@ __global__ void fix_p2q(const Traw *__restrict__ raw, i64 nz, const double *__re
     }
 }
 
+// Same phases 2+3 with the entry's whole P1 cone ((2ry+1) x nz doubles)
+// copied into SMEM by cp.async first (every load in flight at once; the
+// per-thread form waited one L2 round trip per 8 taps), nz % 2 == 0.
+template <typename Traw, typename Tq>
+__global__ void __launch_bounds__(128) fix_p2q_s(const Traw *__restrict__ raw, i64 nz, const double *__restrict__ wy,
+                                                 int ry, const double *__restrict__ wz, int rz,
+                                                 const unsigned long long *__restrict__ fix, long long cap,
+                                                 long long capF, const double *__restrict__ P1, Tq *__restrict__ q_out) {
+    extern __shared__ __align__(16) double cone[];  // [(2ry+1) * nz], then line[nz]
+    const long long F = min(min((long long)fix[0], cap), capF);
+    const int per = (2 * ry + 1) * (int)nz;
+    double *line = cone + per;
+    const int kk = threadIdx.x;
+    for (long long f = blockIdx.x; f < F; f += gridDim.x) {
+        __syncthreads();
+        const double *src = P1 + f * per;
+        for (int q = threadIdx.x; q < per / 2; q += blockDim.x) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(cone + 2 * q);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + 2 * q) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        if (kk < nz) {
+            const double *c = cone + kk;
+            double acc = __dmul_rn(c[ry * nz], wy[0]);
+            for (int d = ry; d >= 1; --d)
+                acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(c[(ry - d) * nz], c[(ry + d) * nz]), wy[d]));
+            line[kk] = acc;
+        }
+        __syncthreads();
+        if (kk == 0) {
+            const i64 p = (i64)fix[2 + f], k = p % nz;
+            double acc = __dmul_rn(line[k], wz[0]);
+            for (int d = rz; d >= 1; --d)
+                acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(line[ct::clampi(k - d, 0, nz - 1)],
+                                                         line[ct::clampi(k + d, 0, nz - 1)]), wz[d]));
+            const double dd = __dadd_rn(ct::to_f64(raw[p]), -acc);
+            q_out[p] = (Tq)rint(dd < 0.0 ? 0.0 : dd);
+        }
+    }
+}
+
 // fix-up of a certified fast path: grid-wide phases for the first capF
 // entries (scratch = the dead K1 workspace), per-CTA fallback for the rest
 template <typename Traw>
@@ -555,8 +643,17 @@ int launch_fixup(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int r
     const i64 per = (2 * (i64)ry + 1) * nz;
     const long long capF = nz <= 128 ? (long long)(work_bytes / ((size_t)per * sizeof(double))) : 0;
     double *P1 = (double *)work;
-    fix_p1<Traw><<<CT_NUM_SMS * 8, 256, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
-    fix_p2q<Traw, Traw><<<CT_NUM_SMS * 2, 128, 0, s>>>(raw, nz, wy, ry, wz, rz, fix, cap, capF, P1, q);
+    if (nz % 32 == 0 && rx <= FXR && ((uintptr_t)raw & 15) == 0 && getenv("CT_FIX_P1_PLAIN") == nullptr)
+        fix_p1s<Traw><<<CT_NUM_SMS * 16, 128, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
+    else
+        fix_p1<Traw><<<CT_NUM_SMS * 8, 256, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
+    const size_t csm = ((size_t)per + nz) * sizeof(double);
+    if (nz % 2 == 0 && nz <= 128 && csm <= 200 * 1024 && getenv("CT_FIX_P1_PLAIN") == nullptr) {
+        cudaFuncSetAttribute(fix_p2q_s<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+        fix_p2q_s<Traw, Traw><<<CT_NUM_SMS * 2, 128, csm, s>>>(raw, nz, wy, ry, wz, rz, fix, cap, capF, P1, q);
+    } else {
+        fix_p2q<Traw, Traw><<<CT_NUM_SMS * 2, 128, 0, s>>>(raw, nz, wy, ry, wz, rz, fix, cap, capF, P1, q);
+    }
     if (int st = ct::check_launch("fixup phases")) return st;
     const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
     cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
