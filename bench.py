@@ -316,6 +316,15 @@ def run_ours(args):
                 "unit_note": "int8 tensor ops (multiply + add = 2), dense",
                 "peak_source": "2 x measured dense bf16 (" + pk["source"] + "): B200 int8 dense = 2x bf16",
                 "work_per_voxel": {"int8_macs": k1_macs, "useful_taps": (2 * rx + 1) + (2 * ry + 1) + (2 * rz + 1)}}
+        # SURVEY 8d's algorithmic figure for K1: the reference's float64 ops
+        # (3 (rx + ry + rz) + 3 per voxel), against the measured FP64 DADD/DMUL
+        # rate of this GPU -- the roofline a float64 implementation would face
+        alg = 3 * (rx + ry + rz) + 3
+        fp64_pk = measured_fp64_peak(dev)
+        alg_tf = alg * nvox / (ms_dom / 1e3) / 1e12
+        roof["algorithmic"] = {"fp64_ops_per_voxel": alg, "achieved_tflops": alg_tf,
+                               "fp64_peak_measured_tflops": fp64_pk,
+                               "frac_of_fp64_peak": alg_tf / fp64_pk if fp64_pk == fp64_pk else None}
     else:
         b = bpv.get(dom) or 1
         achieved = b * nvox / (ms_dom / 1e3) / 1e9
