@@ -278,17 +278,21 @@ def _materialize(ct: CellTable, dims, spacing: VoxelSpacing, frame: int, with_hu
     _, ny, nz = dims
     lin = ct.voxels[:nv].to(torch.int64)
     coords = torch.stack((lin // (ny * nz), (lin // nz) % ny, lin % nz), dim=1).cpu().numpy()
+    # columns as Python scalars / one (n, 3) array up front: per-row structured
+    # field access dominated the host side of materialisation
+    offs, cnts = rows["voxel_offset"].tolist(), rows["count"].tolist()
+    ids, vols = rows["id"].tolist(), rows["volume_um3"].tolist()
+    cents = np.array(rows["centroid_um"], dtype=np.float64)
     dets = []
-    for r in rows:
-        off, c = int(r["voxel_offset"]), int(r["count"])
-        vox = coords[off : off + c]
+    for k in range(len(offs)):
+        vox = coords[offs[k] : offs[k] + cnts[k]]
         dets.append(
             Detection(
-                id=int(r["id"]),
+                id=ids[k],
                 frame=frame,
                 voxels=vox,
-                centroid_um=np.array(r["centroid_um"], dtype=np.float64),
-                volume_um3=float(r["volume_um3"]),
+                centroid_um=cents[k],
+                volume_um3=vols[k],
                 hull=compute_hull(vox, spacing) if with_hull else None,
             )
         )
