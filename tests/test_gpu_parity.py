@@ -524,3 +524,26 @@ def test_edt_sparse_masks_vs_oracle(cuda, oracle, shape, density):
     m = rng.random(shape) < density
     m[0, 0, 0] = True  # never empty
     np.testing.assert_array_equal(S.distance_map(m, ANISO).values, oracle.edt(m, ANISO.as_array()))
+
+
+@pytest.mark.parametrize("n_keep_min", [0.0, 1.5])
+def test_many_components_vs_oracle(cuda, oracle, n_keep_min):
+    """More kept cells than the multi-CTA rank path holds (4096): ~16k isolated
+    voxels on a lattice plus random clusters, so the single-CTA radix-sort
+    path orders them; with a volume filter (1.5 um^3 drops the single voxels)
+    the kept set falls back under 4096.  Ids, voxel lists, centroids and
+    volumes against the oracle (API path: detections_from_mask)."""
+    rng = np.random.default_rng(77)
+    shape = (64, 64, 32)
+    m = np.zeros(shape, dtype=bool)
+    m[::2, ::2, ::2] = True                                   # 16384 isolated voxels
+    for _ in range(40):                                       # clusters merging lattice points
+        c = rng.integers(2, 60, 3) % np.array(shape)
+        m[c[0]:c[0] + 3, c[1]:c[1] + 3, c[2]:c[2] + 2] = True
+    d_gpu = S.detections_from_mask(m, ANISO, frame=0, min_volume_um3=n_keep_min)
+    d_ora = oracle.detections(m, ANISO.as_array(), min_volume_um3=n_keep_min)
+    assert len(d_gpu) == len(d_ora) and (n_keep_min > 0 or len(d_gpu) > 4096)
+    for a, b in zip(d_gpu, d_ora):
+        assert a.id == b.id and a.volume_um3 == b.volume_um3
+        np.testing.assert_array_equal(a.voxels, b.voxels)
+        np.testing.assert_array_equal(a.centroid_um, b.centroid_um)
