@@ -174,9 +174,13 @@ int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, int32_t *l
              int64_t *counters, void *stream);
 
 /* K5 on packed z-rows (ct_threshold_close_rows output, nz <= 128): same
- * outputs as ct_ccl26 (ref segment.py:254) without re-reading a byte mask. */
+ * outputs as ct_ccl26 (ref segment.py:254) without re-reading a byte mask.
+ * flags: CT_LABELS_PREFILLED = labels already hold -1 everywhere (the caller
+ * filled them, e.g. on a side stream off the critical path); else the call
+ * fills them. */
+#define CT_LABELS_PREFILLED 1
 int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t nz, int32_t *labels, int32_t *fg_list,
-                  int64_t *counters, void *stream);
+                  int64_t *counters, int flags, void *stream);
 
 /* K6 -- ref segment.py:242-276 detections_from_mask minus the hull: volume
  * filter count*((dx*dy)*dz) >= min_volume (float64), rank by (-count, root),

@@ -70,7 +70,7 @@ SIGNATURES = {
     "ct_closing": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P, _P]),
     "ct_ccl26": (_INT, [_P, _I64, _I64, _I64, _P, _P, _P, _P]),
     "ct_threshold_close_rows": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
-    "ct_ccl26_rows": (_INT, [_P, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "ct_ccl26_rows": (_INT, [_P, _I64, _I64, _I64, _P, _P, _P, _INT, _P]),
     "ct_cell_table": (
         _INT,
         [_P, _I64, _I64, _I64, _P, _P, _P, _INT, _D, _D, _D, _D, _I64, _I64, _P, _P, _P, _P],

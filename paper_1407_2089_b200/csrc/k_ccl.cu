@@ -938,7 +938,7 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
 }
 
 extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t nz, int32_t *labels,
-                             int32_t *fg_list, int64_t *counters, void *stream) {
+                             int32_t *fg_list, int64_t *counters, int flags, void *stream) {
     if (nx <= 0 || ny <= 0 || nz <= 0) {
         ct::set_error("empty mask");
         return CT_ERR_PARAM;
@@ -949,7 +949,8 @@ extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t n
     }
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(counters, 0, CT_CNT_WORDS * sizeof(int64_t), s);
-    cudaMemsetAsync(labels, 0xff, (size_t)(nx * ny * nz) * sizeof(int32_t), s);  // background = -1
+    if (!(flags & CT_LABELS_PREFILLED))  // else the caller filled labels with -1 (e.g. on a side stream)
+        cudaMemsetAsync(labels, 0xff, (size_t)(nx * ny * nz) * sizeof(int32_t), s);  // background = -1
     const i64 nrows = nx * ny;
     const int g = (int)min((nrows + 255) / 256, (i64)CT_NUM_SMS * 16);
     auto run = [&](auto tag) -> int {

@@ -114,6 +114,9 @@ class FramePipeline:
             self.rows_path = cr == 1 and nz <= 128 and nz % 4 == 0
             self.crows = E(nx * ny * (1 if nz <= 64 else 2), torch.int64) if self.rows_path else None
             self.mask = None if self.rows_path else E(self.dims, torch.uint8)
+            if self.rows_path:
+                self._side = torch.cuda.Stream(dev)
+                self._ev_free, self._ev_filled = torch.cuda.Event(), torch.cuda.Event()
         if vessel:
             self.mwork = E(workspace_bytes(4, nx, ny, nz, self.code), torch.uint8)
             self.state = Z(9, torch.float64)
@@ -161,6 +164,16 @@ class FramePipeline:
         nx, ny, nz = self.dims
         s = _dev.stream_handle()
         rx, ry, rz = self.r
+        if self.rows_path:
+            # the label volume's background fill (N int32, HBM bound) runs on a
+            # side stream while K1/K2 (tensor / ALU bound) run, instead of
+            # inside K5 on the critical path; K5 waits for it
+            cur = torch.cuda.current_stream(self.device)
+            self._ev_free.record(cur)  # previous frame's label consumers are done
+            self._side.wait_event(self._ev_free)
+            with torch.cuda.stream(self._side):
+                self.labels.fill_(-1)
+            self._ev_filled.record(self._side)
         self.hist.zero_()
         e = self._t0()
         if self.exact_k1:
@@ -189,8 +202,9 @@ class FramePipeline:
         self._t1("K4 threshold+close", e)
         e = self._t0()
         if self.rows_path:
+            torch.cuda.current_stream(self.device).wait_event(self._ev_filled)
             call("ct_ccl26_rows", self.crows.data_ptr(), nx, ny, nz, self.labels.data_ptr(), self.fg.data_ptr(),
-                 self.counters.data_ptr(), s)
+                 self.counters.data_ptr(), 1, s)  # CT_LABELS_PREFILLED
         else:
             call("ct_ccl26", self.mask.data_ptr(), nx, ny, nz, self.labels.data_ptr(), self.fg.data_ptr(),
                  self.counters.data_ptr(), s)

@@ -462,7 +462,11 @@ def test_packed_rows_closing_and_ccl(cuda, oracle, shape):
             labels = torch.empty(shape, dtype=torch.int32, device="cuda")
             fg = torch.empty(nx * ny * nz, dtype=torch.int32, device="cuda")
             cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
-            call(name, src.data_ptr(), nx, ny, nz, labels.data_ptr(), fg.data_ptr(), cnt.data_ptr(), s)
+            if name == "ct_ccl26_rows":  # labels pre-filled by the caller (flag 1)
+                labels.fill_(-1)
+                call(name, src.data_ptr(), nx, ny, nz, labels.data_ptr(), fg.data_ptr(), cnt.data_ptr(), 1, s)
+            else:
+                call(name, src.data_ptr(), nx, ny, nz, labels.data_ptr(), fg.data_ptr(), cnt.data_ptr(), s)
             torch.cuda.synchronize()
             c = cnt.cpu().numpy()
             outs.append((labels.cpu().numpy(), c, np.sort(fg[: int(c[0])].cpu().numpy()) if c[0] else None))
