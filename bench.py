@@ -222,18 +222,28 @@ def run_ours(args):
     gathered = torch.zeros(world, dtype=torch.int64, device=dev)
     torch.cuda.synchronize()
 
-    def step(i, timing=False, coll=True):
+    # Time points are queued back to back: each channel's stream runs its
+    # frames in order (its buffers are reused frame to frame), the two
+    # channels share no buffers, so the vessel work of time point t may still
+    # run while the cell work of t+1 starts.  The timed region ends with both
+    # streams joined.  (CT_STEP_JOIN=1: join both streams after every step.)
+    join_each = os.environ.get("CT_STEP_JOIN", "0") == "1"
+
+    def step(i, timing=False, coll=True, first=True):
         t, rc, rv = inputs[i % ring]
         main = torch.cuda.current_stream()
-        s_cell.wait_stream(main)
-        s_vess.wait_stream(main)
+        if join_each or first:
+            s_cell.wait_stream(main)
+            s_vess.wait_stream(main)
         with torch.cuda.stream(s_cell):
             pipe.cell(rc, frame=t, id_start=0)
             counts_dev.copy_(pipe.counters[2:3])
         with torch.cuda.stream(s_vess):
             pipe.vessel(rv)
-        main.wait_stream(s_cell)
-        main.wait_stream(s_vess)
+        if join_each:
+            main.wait_stream(s_vess)
+        if join_each or (world > 1 and coll):
+            main.wait_stream(s_cell)  # the collectives read this step's cell results
         if world > 1 and coll:
             # the frame's detection count (global ids) and its per-cell records, over NCCL
             dist.all_gather_into_tensor(gathered, counts_dev)
@@ -261,7 +271,10 @@ def run_ours(args):
     clocks.mark("t0")
     e0.record()
     for i in range(args.steps):
-        step(args.warmup + i)
+        step(args.warmup + i, first=(i == 0))
+    main_s = torch.cuda.current_stream()
+    main_s.wait_stream(s_cell)
+    main_s.wait_stream(s_vess)
     e1.record()
     torch.cuda.synchronize()
     clocks.mark("t1")
