@@ -20,10 +20,10 @@
 //                 stable LSD radix sort by (-count, root) (segment.py:257),
 //                 ids, voxel offsets (exclusive scan).
 //   tab_relabel : labels[p] = rank of p's kept cell or -1.
-//   tab_voxels  : one CTA per kept cell walks its bbox in C order, emitting
-//                 the ordered voxel list (segment.py:207-217) with a block
-//                 scan; thread 0 then forms the centroid by the row-sequential
-//                 float64 sum numpy's mean(axis=0) performs (segment.py:260).
+//   tab_voxels_w: one warp per kept cell walks its bbox in C order, emitting
+//                 the ordered voxel list (segment.py:207-217) with ballots;
+//                 lane 0 forms the centroid by the row-sequential float64
+//                 sum numpy's mean(axis=0) performs (segment.py:260).
 #include <algorithm>
 #include <cstdlib>
 
@@ -128,7 +128,6 @@ __global__ void __launch_bounds__(LK *LJ) ccl_local(const uint8_t *__restrict__ 
                                                     int32_t *__restrict__ labels, int32_t *__restrict__ fg,
                                                     int64_t *__restrict__ counters) {
     __shared__ int L[LN];
-    const int tid = threadIdx.y * LK + threadIdx.x;
     const i64 tk = (nz + LK - 1) / LK, tj = (ny + LJ - 1) / LJ, ti = (nx + LI - 1) / LI;
     const i64 ntiles = tk * tj * ti;
     const int c = threadIdx.x, b = threadIdx.y;
@@ -842,58 +841,6 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
             table[r].centroid_um[1] = __ddiv_rn(sy, n);
             table[r].centroid_um[2] = __ddiv_rn(sz, n);
         }
-    }
-}
-
-constexpr int VT = 256;
-
-__global__ void __launch_bounds__(VT) tab_voxels(const int32_t *__restrict__ labels, i64 ny, i64 nz,
-                                                 const int64_t *__restrict__ counters, ct_cell *table,
-                                                 int32_t *__restrict__ voxels, double dx, double dy, double dz) {
-    __shared__ u64 sh[VT / 32 + 1];
-    const i64 nk = counters[CT_CNT_KEPT];
-    for (i64 r = blockIdx.x; r < nk; r += gridDim.x) {
-        const ct_cell cell = table[r];
-        const i64 bi = cell.bbox_hi[0] - cell.bbox_lo[0] + 1, bj = cell.bbox_hi[1] - cell.bbox_lo[1] + 1,
-                  bk = cell.bbox_hi[2] - cell.bbox_lo[2] + 1;
-        const i64 nbox = bi * bj * bk;
-        i64 written = 0;
-        for (i64 q0 = 0; q0 < nbox; q0 += VT) {
-            const i64 q = q0 + threadIdx.x;
-            int32_t p = 0;
-            bool hit = false;
-            if (q < nbox) {
-                const i64 c = q % bk, b = (q / bk) % bj, a = q / (bk * bj);
-                p = (int32_t)(((cell.bbox_lo[0] + a) * ny + (cell.bbox_lo[1] + b)) * nz + (cell.bbox_lo[2] + c));
-                hit = labels[p] == (int32_t)r;
-            }
-            u64 v = hit;
-            const u64 tot = block_excl_scan(v, sh);
-            if (hit) voxels[cell.voxel_offset + written + (i64)v] = p;
-            written += (i64)tot;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            // numpy: physical_coordinates(vox).mean(axis=0) -> row-sequential sum / n
-            double sx = 0.0, sy = 0.0, sz = 0.0;
-            const int32_t *list = voxels + cell.voxel_offset;
-            const uint32_t uny = (uint32_t)ny, unz = (uint32_t)nz;
-            for (i64 e = 0; e < cell.count; ++e) {
-                const uint32_t p = (uint32_t)list[e];
-                const uint32_t row = p / unz, kk = p - row * unz;
-                const uint32_t ii = row / uny, jj = row - ii * uny;
-                const double px = __dmul_rn((double)ii, dx);
-                const double py = __dmul_rn((double)jj, dy);
-                const double pz = __dmul_rn((double)kk, dz);
-                if (e == 0) { sx = px; sy = py; sz = pz; }
-                else { sx = __dadd_rn(sx, px); sy = __dadd_rn(sy, py); sz = __dadd_rn(sz, pz); }
-            }
-            const double n = (double)cell.count;
-            table[r].centroid_um[0] = __ddiv_rn(sx, n);
-            table[r].centroid_um[1] = __ddiv_rn(sy, n);
-            table[r].centroid_um[2] = __ddiv_rn(sz, n);
-        }
-        __syncthreads();
     }
 }
 
