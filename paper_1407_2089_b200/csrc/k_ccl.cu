@@ -16,9 +16,11 @@
 //   tab_roots   : compact the roots (component index c, any order).
 //   tab_stats   : per component count / bbox / intensity sum (warp-aggregated
 //                 integer atomics: order-independent, deterministic).
-//   tab_rank    : one CTA: volume filter in float64 (segment.py:253-255),
-//                 stable LSD radix sort by (-count, root) (segment.py:257),
-//                 ids, voxel offsets (exclusive scan).
+//   tab_keep +  : volume filter in float64 (segment.py:253-255); then one warp
+//   tab_rank_emit per kept cell: rank by (-count, root) (segment.py:257) = the
+//                 number of smaller keys, voxel offset = their count sum, and
+//                 the cell's table row (<= 4096 kept cells);
+//   tab_rank    : above that, one CTA: stable LSD radix sort, ids, offsets.
 //   tab_relabel : labels[p] = rank of p's kept cell or -1.
 //   tab_voxels_w: one warp per kept cell walks its bbox in C order, emitting
 //                 the ordered voxel list (segment.py:207-217) with ballots;
