@@ -16,9 +16,11 @@
 //       A = the tap band (128 x 256, Toeplitz, constant) held in TMEM;
 //       B = 256 input rows (clamped at the edges = mode "nearest") x 32
 //       columns of a byte plane, MN-major in shared memory.
-//   pass z (contiguous axis, nz in {32, 64}): D[line][out k] = A[line][in k] * B[in k][out k]
-//       A = 128 lines x nz bytes, K-major; B = the taps with the clamped
-//       boundary folded in (nz x nz, constant), K-major; both in SMEM.
+//   pass z (contiguous axis, nz in {32, 64, 96}): D[line][out k] = A[line][in k] * B[in k][out k]
+//       A = 128 lines x nz bytes, K-major; B = the taps that land inside the
+//       line (nz x nz, constant), K-major; both in SMEM.  The taps beyond the
+//       line ends (mode "nearest": the edge values) are exact integer edge
+//       terms added in the epilogue on the CUDA cores.
 // Operand tiles are staged with cp.async several tiles ahead, and each
 // tile's epilogue (from registers) overlaps the next tile's MMAs.
 //   Limb pairs (a, b) with a + b >= 2 (data limb a, weight limb b) are kept;
