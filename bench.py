@@ -551,16 +551,28 @@ def run_materialized(args, pipe, spec, dev, world):
         dets = pipe.finish_cell(res, materialize=True, with_hull=False)
         mask, dmap = pipe.finish_vessel(vres, dv)
         ndet = len(dets)
+        return dets
 
     one(0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for i in range(steps):
-        one(i + 1)
+        dets = one(i + 1)
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3
+    # hulls, reported separately: host Qhull of the last frame's
+    # detections, over worker processes (segment.compute_hulls; pool warmed first)
+    from paper_1407_2089_b200 import segment as S
+
+    vox = [d.voxels for d in dets]
+    S.compute_hulls(vox[: S.HULL_POOL_MIN], pipe.spacing)
+    th = time.perf_counter()
+    S.compute_hulls(vox, pipe.spacing)
+    hull_ms = (time.perf_counter() - th) * 1e3
     return {"value": world * steps * 2 * nvox / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps,
             "steps": steps, "detections_per_step": ndet,
+            "hulls": {"ms_per_step": hull_ms, "procs": int(os.environ.get("CT_HULL_PROCS", min(16, os.cpu_count() or 1))),
+                      "note": "host Qhull (as the reference), identical calls spread over worker processes"},
             "note": "host wall clock (the result is host Python objects): H2D both channels, pipeline, "
                     "Detection list (no hulls) + vessel (mask, device-resident DistanceMap), sequential"}
 

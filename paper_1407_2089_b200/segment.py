@@ -226,6 +226,41 @@ def compute_hull(voxels: np.ndarray, spacing: VoxelSpacing) -> HullMesh:
     return HullMesh(vertices_um=np.unique(points, axis=0), facets=np.empty((0, 3), dtype=np.int64), flat=True)
 
 
+# Hulls stay host Qhull; scipy's Qhull holds the GIL, so a frame's
+# many small hulls are spread over worker processes (identical calls, identical
+# results, original order).  Below HULL_POOL_MIN cells the pool is not worth
+# its start-up; CT_HULL_PROCS=0 forces the serial loop.
+HULL_POOL_MIN = 256
+_hull_pool = None
+
+
+def _hull_chunk(args):
+    vox_list, spacing = args
+    return [compute_hull(v, spacing) for v in vox_list]
+
+
+def compute_hulls(vox_list, spacing: VoxelSpacing) -> list:
+    """compute_hull for every voxel array of a frame, in order."""
+    import os
+
+    global _hull_pool
+    procs = int(os.environ.get("CT_HULL_PROCS", str(min(16, os.cpu_count() or 1))))
+    if procs <= 1 or len(vox_list) < HULL_POOL_MIN:
+        return [compute_hull(v, spacing) for v in vox_list]
+    if _hull_pool is None:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+
+        import atexit
+
+        # forkserver: workers never inherit this process's CUDA context
+        _hull_pool = ProcessPoolExecutor(max_workers=procs, mp_context=mp.get_context("forkserver"))
+        atexit.register(_hull_pool.shutdown)
+    step = max(16, len(vox_list) // (4 * procs))
+    chunks = [(vox_list[i:i + step], spacing) for i in range(0, len(vox_list), step)]
+    return [h for part in _hull_pool.map(_hull_chunk, chunks) for h in part]
+
+
 @dataclass
 class CellTable:
     """Device-resident result of K5+K6 for one frame."""
@@ -283,20 +318,10 @@ def _materialize(ct: CellTable, dims, spacing: VoxelSpacing, frame: int, with_hu
     offs, cnts = rows["voxel_offset"].tolist(), rows["count"].tolist()
     ids, vols = rows["id"].tolist(), rows["volume_um3"].tolist()
     cents = np.array(rows["centroid_um"], dtype=np.float64)
-    dets = []
-    for k in range(len(offs)):
-        vox = coords[offs[k] : offs[k] + cnts[k]]
-        dets.append(
-            Detection(
-                id=ids[k],
-                frame=frame,
-                voxels=vox,
-                centroid_um=cents[k],
-                volume_um3=vols[k],
-                hull=compute_hull(vox, spacing) if with_hull else None,
-            )
-        )
-    return dets
+    voxs = [coords[offs[k] : offs[k] + cnts[k]] for k in range(len(offs))]
+    hulls = compute_hulls(voxs, spacing) if with_hull else [None] * len(voxs)
+    return [Detection(id=ids[k], frame=frame, voxels=voxs[k], centroid_um=cents[k], volume_um3=vols[k],
+                      hull=hulls[k]) for k in range(len(voxs))]
 
 
 def _detections_dev(mask: torch.Tensor, spacing, frame, min_volume_um3, id_start, with_hull=True):

@@ -551,3 +551,30 @@ def test_many_components_vs_oracle(cuda, oracle, n_keep_min):
         assert a.id == b.id and a.volume_um3 == b.volume_um3
         np.testing.assert_array_equal(a.voxels, b.voxels)
         np.testing.assert_array_equal(a.centroid_um, b.centroid_um)
+
+
+def test_parallel_hulls_match_serial(cuda):
+    """compute_hulls over worker processes (frames with >= HULL_POOL_MIN
+    cells) returns exactly the serial compute_hull results, in order."""
+    import os
+
+    rng = np.random.default_rng(5)
+    vox = []
+    for _ in range(S.HULL_POOL_MIN + 40):
+        r = rng.uniform(1.0, 4.5)
+        g = np.mgrid[-5:6, -5:6, -5:6].reshape(3, -1).T
+        v = g[((g - rng.uniform(0, 1, 3)) ** 2).sum(1) <= r * r].astype(np.int64) + 10
+        vox.append(v[:rng.integers(1, len(v) + 1)])  # includes < 4 points and flat sets
+    par = S.compute_hulls(vox, ANISO)
+    os.environ["CT_HULL_PROCS"] = "0"
+    try:
+        ser = S.compute_hulls(vox, ANISO)
+    finally:
+        del os.environ["CT_HULL_PROCS"]
+    assert len(par) == len(ser)
+    for a, b in zip(par, ser):
+        assert a.flat == b.flat
+        np.testing.assert_array_equal(a.vertices_um, b.vertices_um)
+        np.testing.assert_array_equal(a.facets, b.facets)
+        if not a.flat:
+            np.testing.assert_array_equal(a.equations, b.equations)
