@@ -263,8 +263,16 @@ def test_large_frame_properties(cuda):
     rawv = synth.generate(spec, 5, synth.VESSEL)
     vres = pipe_v = FramePipeline(spec.dims, spec.dtype, ANISO, cell=False).vessel(rawv)
     assert int(vres.state[5]) == 0
+    assert float(vres.state[2]) == 2.0  # decision certified without the exact sigma_hat
     assert torch.all(vres.distance[vres.mask.bool()] == 0)
     assert torch.all(vres.distance[~vres.mask.bool()] > 0)
+    # the drop-in API path (exact sigma_hat, float64 grid, float histogram)
+    # reaches the same decision, mask and distance map at full size
+    st = D.mrf_denoise_state(VoxelGrid(values=rawv, spacing=ANISO))
+    assert st.iteration == 0 and st.sigma_hat > 0
+    m_api, dm_api = S.segment_vessel_channel(D.mrf_denoise(VoxelGrid(values=rawv, spacing=ANISO)))
+    assert torch.equal(m_api.to(torch.uint8), vres.mask)
+    assert torch.equal(dm_api.values, vres.distance)
 
 
 def _q_exact_and_fast(raw, spacing, sigma_um, eps=0.0, cap=1 << 20):
