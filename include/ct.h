@@ -72,7 +72,9 @@ typedef struct ct_cell {
     double centroid_um[3]; /* row-sequential mean of idx*spacing (segment.py:260) */
     double volume_um3;     /* count * voxel_volume (segment.py:267)             */
     int64_t voxel_offset;  /* start of this cell's voxels in the voxel list     */
-    int64_t reserved;
+    double mean_intensity; /* intensity_sum / count as float64 = numpy
+                            * intensity[voxels].mean() (north star's per-cell
+                            * mean intensity; NaN if no intensity given)      */
 } ct_cell;
 
 const char *ct_version(void);
@@ -95,7 +97,7 @@ int ct_gaussian_residual(const void *raw, int raw_dtype, int64_t nx, int64_t ny,
                          double *bg_out, double *residual_out, void *q_out, int q_dtype, void *stream);
 
 /* K1 fast path of the fused pipeline: q = rint(max(raw - bg, 0)) for U8/U16
- * raw, CERTIFIED exact.  U8 volumes with nz in {32, 64}, rx, ry <= 64 and
+ * raw, CERTIFIED exact.  U8 volumes with nz in {32, 64, 96}, rx, ry <= 64 and
  * rz <= 64 run on the tensor cores (tcgen05 int8 MMA: taps as 35-bit
  * integers in 8-bit limbs, intermediates as 32-bit fixed point, exact int32
  * accumulation; k_gauss_tc.cu); other inputs accumulate bg by FP64 FMA.
@@ -103,21 +105,22 @@ int ct_gaussian_residual(const void *raw, int raw_dtype, int64_t nx, int64_t ny,
  * scipy's float64 result) of a half-integer are listed in fix (device: [0]
  * count, [1] overflow, [2..2+fix_cap) linear indices) and recomputed in
  * scipy's exact order by a fix-up kernel, so q is bit-identical to
- * ct_gaussian_residual's.  fix[1] != 0 (list overflow) means q is not
- * certified: rerun ct_gaussian_residual.  eps_override > 0 replaces the
- * bound (tests force the fix-up path with it).  Falls back to the exact path
- * when no tiled kernel applies.  work: ct_workspace_bytes(0,...). */
+ * ct_gaussian_residual's.  When the list overflows (fix[1] != 0) the whole
+ * volume is recomputed in scipy's order in the same stream (no host round
+ * trip), so q is exact in every case.  eps_override > 0 replaces the bound
+ * (tests force the fix-up path with it).  path: 0 auto (tensor cores where
+ * the shape fits), 1 FP64 FMA only, 2 tensor cores only (CT_ERR_UNSUPPORTED
+ * when the shape does not fit).  Falls back to the exact path when no tiled
+ * kernel applies.  work: ct_workspace_bytes(0,...).
+ * (Replaces the q = rint(denoise_cell_channel(raw)) part of ref
+ * denoise.py:84-88 on the fused path.) */
 int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry,
                   int rz, void *work, void *q_out, unsigned long long *fix, int64_t fix_cap, double eps_override,
-                  void *stream);
+                  int path, void *stream);
 
-/* Selects ct_gaussian_q's fast path (process-wide): 0 auto, 1 FP64 FMA
- * only, 2 tensor cores only (CT_ERR_UNSUPPORTED when the shape does not fit). */
-int ct_set_k1_path(int mode);
-
-/* Which arithmetic ct_gaussian_q uses for this shape under the current mode:
+/* Which arithmetic ct_gaussian_q uses for this shape and path argument:
  * 2 tensor cores, 1 FP64 FMA (both certified; informational). */
-int ct_k1_path(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz);
+int ct_k1_path(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz, int path);
 
 /* float64 copy of a U8/U16/F64 volume (ref denoise.py:84, :158 astype). */
 int ct_to_f64(const void *in, int dtype, int64_t n, double *out, void *stream);
@@ -184,8 +187,8 @@ int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t nz, int32_t 
 
 /* K6 -- ref segment.py:242-276 detections_from_mask minus the hull: volume
  * filter count*((dx*dy)*dz) >= min_volume (float64), rank by (-count, root),
- * ids from id_start, C-order voxel lists, row-sequential centroids, bbox and
- * intensity sums.  On return labels[p] = rank (0-based) of p's kept cell,
+ * ids from id_start, C-order voxel lists, row-sequential centroids, bbox,
+ * intensity sums and mean intensities.  On return labels[p] = rank (0-based) of p's kept cell,
  * else -1 (canonical label volume); table[rank] filled for rank < n_kept;
  * voxels[] = concatenated C-order linear indices (capacity nx*ny*nz).
  * intensity: optional U8/U16 volume for intensity_sum.  cap = component

@@ -39,7 +39,7 @@ CELL_DTYPE = np.dtype(
         ("centroid_um", "<f8", (3,)),
         ("volume_um3", "<f8"),
         ("voxel_offset", "<i8"),
-        ("reserved", "<i8"),
+        ("mean_intensity", "<f8"),
     ]
 )
 assert CELL_DTYPE.itemsize == 128
@@ -58,10 +58,9 @@ SIGNATURES = {
     "ct_last_error": (ctypes.c_char_p, []),
     "ct_workspace_bytes": (_SZ, [_INT, _I64, _I64, _I64, _I64]),
     "ct_gaussian_residual": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _P, _INT, _P]),
-    "ct_gaussian_q": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _I64, _D, _P]),
-    "ct_set_k1_path": (_INT, [_INT]),
+    "ct_gaussian_q": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _I64, _D, _INT, _P]),
     "ct_voxel_runs": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P]),
-    "ct_k1_path": (_INT, [_INT, _I64, _I64, _I64, _INT, _INT, _INT]),
+    "ct_k1_path": (_INT, [_INT, _I64, _I64, _I64, _INT, _INT, _INT, _INT]),
     "ct_to_f64": (_INT, [_P, _INT, _I64, _P, _P]),
     "ct_median": (_INT, [_P, _INT, _I64, _I64, _I64, _INT, _P, _P, _P]),
     "ct_histogram": (_INT, [_P, _INT, _I64, _P, _P]),
@@ -141,8 +140,8 @@ def exported_symbols() -> list[str]:
 # kernels each entry point launches (memsets excluded); used for the
 # bench's gpu_launches count
 LAUNCHES = {
-    "ct_gaussian_residual": 3, "ct_gaussian_q": 7, "ct_to_f64": 1, "ct_median": 1, "ct_histogram": 1, "ct_otsu": 1,
-    "ct_threshold_close": 2, "ct_closing": 2, "ct_ccl26": 4, "ct_threshold_close_rows": 2, "ct_ccl26_rows": 4, "ct_cell_table": 7, "ct_voxel_runs": 3, "ct_mrf": 5, "ct_mrf_decide": 8,
+    "ct_gaussian_residual": 3, "ct_gaussian_q": 8, "ct_to_f64": 1, "ct_median": 1, "ct_histogram": 1, "ct_otsu": 1,
+    "ct_threshold_close": 2, "ct_closing": 2, "ct_ccl26": 4, "ct_threshold_close_rows": 2, "ct_ccl26_rows": 4, "ct_cell_table": 6, "ct_voxel_runs": 3, "ct_mrf": 5, "ct_mrf_decide": 8,
     "ct_mrf_step": 4, "ct_sign_sum": 1, "ct_edt": 4, "ct_synth_frame": 3,
 }
 launch_counter = {"enabled": False, "count": 0}

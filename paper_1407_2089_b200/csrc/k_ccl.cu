@@ -463,8 +463,15 @@ __global__ void tab_stats(const int32_t *__restrict__ labels, i64 ny, i64 nz, co
     }
 }
 
+// per-cell mean intensity: the numpy mean of the cell's integer intensities
+// (raw[voxels].mean(): the float64 sum of integers < 2^53 is exact in any
+// order, so the mean is one correctly rounded division); NaN without intensity
+__device__ __forceinline__ double mean_intensity(u64 isum, u64 count, bool has_int) {
+    return has_int ? __ddiv_rn((double)isum, (double)count) : __longlong_as_double(0x7ff8000000000000ll);
+}
+
 constexpr int RT = 512;    // tab_rank threads
-constexpr int RK = 4096;   // kept cells ordered by the multi-CTA path (tab_keep / tab_rank_keys / tab_emit)
+constexpr int RK = 4096;   // kept cells ordered by the multi-CTA path (tab_keep / tab_rank_emit)
 constexpr int RD = 16;     // radix digits (4 bits)
 
 __device__ __forceinline__ u64 sort_key(const TabWork &w, int c, u64 maxc, int rbits) {
@@ -495,13 +502,13 @@ __device__ u64 block_excl_scan(u64 &v, u64 *sh) {
     return total;
 }
 
-__global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64 cap, i64 N, double vv,
+__global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64 cap, i64 N, double vv, bool has_int,
                                                double min_volume, i64 id_start, ct_cell *table) {
     __shared__ uint32_t hcnt[RD][RT];
     __shared__ u64 sh[RT / 32 + 1];
     __shared__ u64 s_maxc;
     const int tid = threadIdx.x;
-    if (counters[CT_CNT_KEPT] <= RK) return;  // ordered by tab_rank_keys / tab_emit
+    if (counters[CT_CNT_KEPT] <= RK) return;  // ordered by tab_rank_emit
     i64 nc = counters[CT_CNT_COMPONENTS];
     if (nc > cap) nc = cap;
     if (counters[CT_CNT_OVERFLOW]) nc = 0;
@@ -612,7 +619,7 @@ __global__ void __launch_bounds__(RT) tab_rank(int64_t *counters, TabWork w, i64
         r.centroid_um[0] = r.centroid_um[1] = r.centroid_um[2] = 0.0;
         r.volume_um3 = __dmul_rn((double)r.count, vv);
         r.voxel_offset = (int64_t)voff;
-        r.reserved = 0;
+        r.mean_intensity = mean_intensity(w.isum[c], w.count[c], has_int);
         table[e] = r;
         voff += w.count[c];
     }
@@ -649,28 +656,13 @@ __global__ void tab_keep(int64_t *counters, TabWork w, i64 cap, double vv, doubl
     }
 }
 
-// rank of each kept cell = number of smaller keys (keys are unique); all keys in SMEM
-__global__ void __launch_bounds__(256) tab_rank_keys(const int64_t *__restrict__ counters, TabWork w) {
-    __shared__ u64 key[RK];
-    const i64 nk = counters[CT_CNT_KEPT];
-    if (nk > RK || (i64)blockIdx.x * 256 >= nk) return;
-    for (i64 e = threadIdx.x; e < nk; e += 256) key[e] = order_key(w, w.sa[e]);
-    __syncthreads();
-    const i64 e = (i64)blockIdx.x * 256 + threadIdx.x;
-    if (e >= nk) return;
-    const u64 k = key[e];
-    int r = 0;
-    for (int f = 0; f < (int)nk; ++f) r += key[f] < k;
-    w.sb[r] = w.sa[e];
-}
-
 // Rank + voxel offset + table row in one pass, one warp per kept cell (all
 // SMs; replaces tab_rank_keys + the single-CTA tab_emit, which was bound by
 // one SM's memory pipe): rank = #{keys < k}, voxel offset = sum of the counts
 // of those keys (= the exclusive scan in rank order), lanes split the key
 // range; the 128-byte row is written by 16 lanes, one field each.
 __global__ void __launch_bounds__(256) tab_rank_emit(int64_t *counters, TabWork w, double vv, i64 id_start,
-                                                     ct_cell *table) {
+                                                     bool has_int, ct_cell *table) {
     __shared__ u64 key[RK];
     __shared__ uint32_t cnt[RK];
     const i64 nk = counters[CT_CNT_KEPT];
@@ -712,45 +704,11 @@ __global__ void __launch_bounds__(256) tab_rank_emit(int64_t *counters, TabWork 
             case 9: f = (int64_t)w.isum[c]; break;
             case 13: f = __double_as_longlong(__dmul_rn((double)cnt[e], vv)); break;
             case 14: f = (int64_t)v; break;
-            default: f = 0; break;  // centroid (tab_voxels_w), reserved
+            case 15: f = __double_as_longlong(mean_intensity(w.isum[c], cnt[e], has_int)); break;
+            default: f = 0; break;  // centroid (tab_voxels_w)
         }
         reinterpret_cast<int64_t *>(table + r)[lane] = f;
     }
-}
-
-// table rows in rank order, voxel offsets by an exclusive scan (one CTA)
-__global__ void __launch_bounds__(1024) tab_emit(int64_t *counters, TabWork w, double vv, i64 id_start,
-                                                 ct_cell *table) {
-    __shared__ u64 sh[1024 / 32 + 1];
-    const i64 nk = counters[CT_CNT_KEPT];
-    if (nk > RK) return;
-    const int tid = threadIdx.x;
-    const i64 chunk = (nk + 1023) / 1024;
-    const i64 e0 = min((i64)tid * chunk, nk), e1 = min(e0 + chunk, nk);
-    u64 vox = 0;
-    for (i64 e = e0; e < e1; ++e) vox += w.count[w.sb[e]];
-    u64 voff = vox;
-    const u64 total_vox = block_excl_scan(voff, sh);
-    for (i64 e = e0; e < e1; ++e) {
-        const int c = w.sb[e];
-        w.rank[c] = (int32_t)e;
-        ct_cell r;
-        r.id = id_start + e;
-        r.count = w.count[c];
-        r.root = w.root[c];
-        for (int a = 0; a < 3; ++a) {
-            r.bbox_lo[a] = w.bbox[6 * c + a];
-            r.bbox_hi[a] = w.bbox[6 * c + 3 + a];
-        }
-        r.intensity_sum = (int64_t)w.isum[c];
-        r.centroid_um[0] = r.centroid_um[1] = r.centroid_um[2] = 0.0;
-        r.volume_um3 = __dmul_rn((double)r.count, vv);
-        r.voxel_offset = (int64_t)voff;
-        r.reserved = 0;
-        table[e] = r;
-        voff += w.count[c];
-    }
-    if (tid == 0) counters[CT_CNT_KEPT_VOXELS] = (int64_t)total_vox;
 }
 
 __global__ void tab_relabel(int32_t *labels, const int32_t *__restrict__ fg, const int64_t *__restrict__ counters,
@@ -863,7 +821,7 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(counters, 0, CT_CNT_WORDS * sizeof(int64_t), s);
     cudaMemsetAsync(labels, 0xff, (size_t)(nx * ny * nz) * sizeof(int32_t), s);  // background = -1
-    if (nz <= 128 && getenv("CT_CCL_TILES") == nullptr) {
+    if (nz <= 128) {  // run-based union-find on z-rows; the tile form covers nz > 128
         const i64 nrows = nx * ny;
         const int g = (int)min((nrows + 255) / 256, (i64)CT_NUM_SMS * 16);
         auto run = [&](auto tag) -> int {
@@ -943,14 +901,10 @@ extern "C" int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz
     if (int st = ct::check_launch("tab_stats")) return st;
     cudaMemsetAsync(&counters[CT_CNT_KEPT], 0, sizeof(int64_t), s);
     tab_keep<<<CT_NUM_SMS * 2, 256, 0, s>>>(counters, w, cap, vv, min_volume_um3);
-    static const bool emit1 = getenv("CT_TAB_EMIT1") != nullptr;  // A/B knob: the previous two-kernel form
-    if (emit1) {
-        tab_rank_keys<<<(unsigned)((std::min<i64>(cap, RK) + 255) / 256), 256, 0, s>>>(counters, w);
-        tab_emit<<<1, 1024, 0, s>>>(counters, w, vv, id_start, table);
-    } else {
-        tab_rank_emit<<<(unsigned)((std::min<i64>(cap, RK) + 7) / 8), 256, 0, s>>>(counters, w, vv, id_start, table);
-    }
-    tab_rank<<<1, RT, 0, s>>>(counters, w, cap, N, vv, min_volume_um3, id_start, table);
+    const bool has_int = intensity != nullptr;
+    tab_rank_emit<<<(unsigned)((std::min<i64>(cap, RK) + 7) / 8), 256, 0, s>>>(counters, w, vv, id_start, has_int,
+                                                                              table);
+    tab_rank<<<1, RT, 0, s>>>(counters, w, cap, N, vv, has_int, min_volume_um3, id_start, table);
     if (int st = ct::check_launch("tab_rank")) return st;
     tab_relabel<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters, w);
     if (int st = ct::check_launch("tab_relabel")) return st;

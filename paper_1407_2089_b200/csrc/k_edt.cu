@@ -285,97 +285,8 @@ __global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4(const uint8_t *__rest
 }
 
 // ---------------------------------------------------------------------------
-// pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di)
-// ---------------------------------------------------------------------------
-// blockIdx.y = output segment: every segment's threads build the line's whole
-// envelope (cheap: sites are sparse after pass x) and emit only their part of
-// the line, which multiplies the parallelism of the long output walk.
-__global__ void __launch_bounds__(LT) edt_pass_y(const int16_t *__restrict__ di, i64 nlines, int ny, int nz, double dx,
-                                                 double dy, int32_t *__restrict__ out, uint32_t *__restrict__ spill) {
-    __shared__ uint32_t stk[SC][LT];  // entry = (position << 16) | payload (di as uint16)
-    const i64 l = blockIdx.x * (i64)LT + threadIdx.x;
-    const int nseg = gridDim.y, seg = blockIdx.y;
-    const int xs0 = (int)((i64)ny * seg / nseg), xs1 = (int)((i64)ny * (seg + 1) / nseg);
-    spill += (size_t)seg * nlines * (ny > SC ? ny - SC : 0);  // private spill stacks per segment
-    // lanes run data-dependent envelope loops; reconverge (wm) before every
-    // batched load and every store so the warp's accesses stay coalesced
-    const unsigned wm = __ballot_sync(0xffffffffu, l < nlines);
-    if (l >= nlines) return;
-    const i64 base = (l / nz) * (i64)ny * nz + (l % nz);
-    const double d2 = __dmul_rn(dy, dy);
-    // explicit shared / global accesses (no generic pointers)
-    auto ent_ld = [&](int e) -> uint32_t { return e < SC ? stk[e][threadIdx.x] : spill[(i64)(e - SC) * nlines + l]; };
-    auto ent_st = [&](int e, uint32_t v) {
-        if (e < SC) stk[e][threadIdx.x] = v;
-        else spill[(i64)(e - SC) * nlines + l] = v;
-    };
-#define GOF(pl) sq(__dmul_rn((double)(int16_t)(pl), dx))
-    int K = 0, tp = 0, bp = 0;
-    double tg = 0.0, bg = 0.0;
-    for (int x0 = 0; x0 < ny; x0 += PF) {
-        int16_t v[PF];
-        __syncwarp(wm);
-#pragma unroll
-        for (int u = 0; u < PF; ++u) v[u] = x0 + u < ny ? di[base + (i64)(x0 + u) * nz] : NONE16;
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int x = x0 + u;
-            if (x >= ny) break;
-            if (v[u] == NONE16) continue;
-            const double gx = GOF(v[u]);
-            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-                --K;
-                tp = bp;
-                tg = bg;
-                if (K >= 2) {
-                    const uint32_t e = ent_ld(K - 2);
-                    bp = (int)(e >> 16);
-                    bg = GOF(e & 0xffff);
-                }
-            }
-            ent_st(K, ((uint32_t)x << 16) | (uint16_t)v[u]);
-            bp = tp; bg = tg; tp = x; tg = gx;
-            ++K;
-        }
-    }
-    int e = 0, cp = 0, np = 0;
-    int16_t cpl = 0, npl = 0;
-    double cg = 0.0, ng = 0.0;
-    if (K) {
-        const uint32_t c0 = ent_ld(0);
-        cp = (int)(c0 >> 16); cpl = (int16_t)(c0 & 0xffff); cg = GOF(cpl);
-        if (K > 1) {
-            const uint32_t c1 = ent_ld(1);
-            np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
-        }
-    }
-    // sw = first x at which the envelope has moved past site cp
-    int sw = (K > 1) ? first_past(0, ny, np, ng, cp, cg, d2) : ny;
-    int32_t *o = out + base + (i64)xs0 * nz;
-    for (int x = xs0; x < xs1; ++x, o += nz) {
-        int32_t r = NONE32;
-        if (K) {
-            while (x >= sw) {
-                ++e;
-                cp = np; cpl = npl; cg = ng;
-                if (e + 1 < K) {
-                    const uint32_t c1 = ent_ld(e + 1);
-                    np = (int)(c1 >> 16); npl = (int16_t)(c1 & 0xffff); ng = GOF(npl);
-                    sw = first_past(x, ny, np, ng, cp, cg, d2);
-                } else {
-                    sw = ny;
-                }
-            }
-            r = pack(cp - x, cpl);
-        }
-        __syncwarp(wm);
-        *o = r;
-    }
-#undef GOF
-}
-
-// ---------------------------------------------------------------------------
-// pass y in two kernels (parallelism: only nx*nz lines exist, too few threads
+// pass y: envelope along j; sites di != NONE, cost (di*dx)^2; out (dj, di),
+// in two kernels (parallelism: only nx*nz lines exist, too few threads
 // for one-thread-per-line sweeps of ny outputs):
 //   build  : thread per line (64-thread CTAs spread the lines evenly over the
 //            SMs), loads PFB deep with compile-time strides; the envelope
@@ -619,127 +530,16 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
     }
 }
 
-// Same pass with the packed (dj, di) offsets kept in SMEM instead of the
-// float64 costs (costs recomputed on use by gyz, same operations): 4 + 1
-// bytes per element instead of 8 + 1, so ~1.8x more lines per SM.  Split in
-// two phases: (1) one thread per line builds the envelope and sweeps it,
-// writing only the chosen feature position per voxel (u8, SMEM); (2) all
-// threads form the float64 distances voxel-parallel -- the correctly rounded
-// sqrt off the sequential chain, stores coalesced along k.
-template <int NZ, int ZLN>
-constexpr size_t zp_smem() {
-    return (size_t)ZLN * (NZ + 1) * 4 + 2 * (size_t)ZLN * (NZ + 4);
-}
-
-template <int NZ, int ZLN = ZL>  // ZLN lines per CTA
-__global__ void __launch_bounds__(ZLN) edt_pass_zp(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
-                                                  double dz, double *__restrict__ out) {
-    constexpr int S = NZ + 1;   // padded line stride (conflict-free)
-    constexpr int SB = NZ + 4;  // byte rows: 4-byte pad keeps per-thread rows in distinct banks
-    extern __shared__ __align__(16) unsigned char zsm[];
-    int32_t *ps = (int32_t *)zsm;
-    uint8_t *stk = zsm + (size_t)ZLN * S * 4;
-    uint8_t *fid = stk + ZLN * SB;
-
-    const i64 l0 = blockIdx.x * (i64)ZLN;
-    const int nl = (int)min((i64)ZLN, nlines - l0);
-    const int32_t *src = in + l0 * NZ;
-    constexpr int T4 = ZLN * NZ / 4;
-    for (int i0 = threadIdx.x; i0 < T4; i0 += 8 * ZLN) {
-        int4 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int q = i0 + u * ZLN;
-            if (q < T4 && q * 4 < nl * NZ) v[u] = __ldg((const int4 *)src + q);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int q = i0 + u * ZLN;
-            if (q < T4 && q * 4 < nl * NZ) {
-                const int idx = q * 4, g = idx / NZ, k = idx - g * NZ;
-                int32_t *d = ps + g * S + k;
-                d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
-            }
-        }
-    }
-    __syncthreads();
-    const double d2 = __dmul_rn(dz, dz);
-    const int t = threadIdx.x;
-    if (t < nl) {
-        const int32_t *P = ps + t * S;
-        auto G = [&](int x) -> double { return gyz(P[x], dx, dy); };
-        uint8_t *st = stk + t * SB;
-        uint8_t *fo = fid + t * SB;
-        int K = 0, tp = 0, bp = 0;
-        double tg = 0.0, bg = 0.0;
-        int32_t pcur = P[0];
-        for (int x = 0; x < NZ; ++x) {
-            const int32_t pnx = x + 1 < NZ ? P[x + 1] : NONE32;  // next element in flight
-            const int32_t px = pcur;
-            pcur = pnx;
-            if (px == NONE32) continue;
-            const double gx = gyz(px, dx, dy);
-            while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
-                --K;
-                tp = bp;
-                tg = bg;
-                if (K >= 2) {
-                    bp = st[K - 2];
-                    bg = G(bp);
-                }
-            }
-            st[K++] = (uint8_t)x;
-            bp = tp; bg = tg; tp = x; tg = gx;
-        }
-        if (K == 0) {
-            for (int x = 0; x < NZ; ++x) fo[x] = 255;
-        } else {
-            int e = 0;
-            int cp = st[0], np = K > 1 ? st[1] : 0;
-            double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
-            {  // jump to each switch point
-                int sw = K > 1 ? first_past(0, NZ, np, ng, cp, cg, d2) : NZ;
-                int x = 0;
-                for (;;) {
-                    for (; x < sw; ++x) fo[x] = (uint8_t)cp;
-                    if (x >= NZ) break;
-                    ++e;
-                    cp = np; cg = ng;
-                    if (e + 1 < K) {
-                        np = st[e + 1];
-                        ng = G(np);
-                        sw = first_past(x, NZ, np, ng, cp, cg, d2);
-                    } else {
-                        sw = NZ;
-                    }
-                }
-            }
-        }
-    }
-    __syncthreads();
-    // phase 2: voxel-parallel distances, warp-contiguous along k
-    double *dst = out + l0 * NZ;
-    const int tot = nl * NZ;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < tot; idx += ZLN) {
-        const int g = idx / NZ, x = idx - g * NZ;
-        const int f = fid[g * SB + x];
-        double r = INFINITY;
-        if (f != 255) r = __dsqrt_rn(__dadd_rn(gyz(ps[g * S + f], dx, dy), sq(__dmul_rn((double)(f - x), dz))));
-        dst[idx] = r;
-    }
-}
-
-// Pass z, register-streamed form.  ncu on edt_pass_zp: the thread-per-line
-// envelope is latency bound (wait stalls, 16 warps/SM) and the SMEM staging of
-// whole lines (396 B per line) is what caps the warps.  Here a thread streams
+// Pass z, register-streamed form.  ncu on the SMEM-staged form (edt_pass_z):
+// the thread-per-line envelope is latency bound (wait stalls, 16 warps/SM) and
+// the SMEM staging of whole lines (396 B per line) is what caps the warps.  Here a thread streams
 // its own line from global memory (two 16-byte loads per 8 elements, the next
 // chunk in flight), keeps only the envelope stack in SMEM (positions for all
 // entries, packed offsets for the first SCZ; deeper entries re-read their
 // offsets from the line, which stays in L1/L2), and forms the distances in the
 // sweep itself, four voxels per 32-byte store (one full sector per lane).
 // 192 B of SMEM per line (with the switch points): 32 warps per SM.  Same predicates and arithmetic
-// as edt_pass_zp (bit-identical output).
+// as edt_pass_z (bit-identical output).
 __device__ __forceinline__ void st_v4(double *p, double a, double b, double c, double d) {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
@@ -802,7 +602,7 @@ __global__ void __launch_bounds__(ZRT, 8) edt_pass_zr(const int32_t *__restrict_
     // switch points first, per entry (a loop of at most K - 1 trips per lane
     // instead of a divergent test inside the voxel loop): the sweep moves past
     // entry e at sw_e = first_past(sw_{e-1}, ...), sw_{-1} = 0 -- exactly where
-    // the voxel-by-voxel sweep of edt_pass_zp switches
+    // the voxel-by-voxel sweep of edt_pass_z switches
     {
         int p = cp, sw = 0;
         double pg = cg;
@@ -835,6 +635,54 @@ __global__ void __launch_bounds__(ZRT, 8) edt_pass_zr(const int32_t *__restrict_
     }
 }
 
+// Pass z for long lines (nz > 128, up to 32767): the edt_pass_z envelope and
+// sweep with the costs recomputed from the packed offsets on use and the
+// stack in global memory (the int16 pass-x buffer, dead after pass y: one
+// entry per voxel at most).  Thread per line; same predicates, same order.
+__global__ void __launch_bounds__(128) edt_pass_z_long(const int32_t *__restrict__ in, i64 nlines, int nz, double dx,
+                                                       double dy, double dz, int16_t *__restrict__ stack,
+                                                       double *__restrict__ out) {
+    const i64 l = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+    if (l >= nlines) return;
+    const int32_t *line = in + l * nz;
+    int16_t *st = stack + l * nz;
+    auto G = [&](int x) { const int32_t pl = line[x]; return pl == NONE32 ? INFINITY : gyz(pl, dx, dy); };
+    const double d2 = __dmul_rn(dz, dz);
+    int K = 0, tp = 0, bp = 0;
+    double tg = 0.0, bg = 0.0;
+    for (int x = 0; x < nz; ++x) {
+        const double gx = G(x);
+        if (gx == INFINITY) continue;
+        while (K >= 2 && env_pop(x, gx, tp, tg, bp, bg, d2)) {
+            --K;
+            tp = bp;
+            tg = bg;
+            if (K >= 2) {
+                bp = st[K - 2];
+                bg = G(bp);
+            }
+        }
+        st[K++] = (int16_t)x;
+        bp = tp; bg = tg; tp = x; tg = gx;
+    }
+    double *dst = out + l * nz;
+    if (K == 0) {
+        for (int x = 0; x < nz; ++x) dst[x] = INFINITY;
+        return;
+    }
+    int e = 0;
+    int cp = st[0], np = K > 1 ? st[1] : 0;
+    double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
+    for (int x = 0; x < nz; ++x) {
+        while (e + 1 < K && env_past(x, np, ng, cp, cg, d2)) {
+            ++e;
+            cp = np; cg = ng;
+            if (e + 1 < K) { np = st[e + 1]; ng = G(np); }
+        }
+        dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
+    }
+}
+
 inline size_t zsmem(int nz) {
     const int S = nz + 1;
     return (size_t)ZL * S * 8 + (size_t)ZL * nz + 16;
@@ -856,8 +704,9 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         ct::set_error("mask has no voxels");
         return CT_ERR_PARAM;
     }
-    if (nx > 32767 || ny > 32767 || nz > 128) {
-        ct::set_error("EDT supports nx, ny < 32768 and nz <= 128 (packed int16 offsets, SMEM z lines)");
+    if (nx > 32767 || ny > 32767 || nz > 32767) {
+        ct::set_error("EDT supports extents < 32768 (packed int16 offsets); got (%lld, %lld, %lld)", (long long)nx,
+                      (long long)ny, (long long)nz);
         return CT_ERR_UNSUPPORTED;
     }
     cudaStream_t s = (cudaStream_t)stream;
@@ -878,20 +727,15 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         edt_pass_x<<<(unsigned)((lx + LT - 1) / LT), LT, 0, s>>>(mask, lx, (int)nx, di);
     }
     if (int st = ct::check_launch("edt_pass_x")) return st;
-    static const bool y1 = getenv("CT_EDT_Y1") != nullptr;  // one-kernel pass y (A/B knob)
-    if (y1) {
-        edt_pass_y<<<dim3((unsigned)((ly + LT - 1) / LT), YSEG), LT, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, pk, spill);
-        if (int st = ct::check_launch("edt_pass_y")) return st;
-    } else {
+    {
         uint32_t *head = spill + (size_t)YSEG * ly * (ny > SC ? ny - SC : 0);
         int32_t *kc = (int32_t *)(head + (size_t)SC * ly);
         int16_t *swh = (int16_t *)(kc + ly);
         int16_t *est = swh + (size_t)SC * ly;
         const unsigned gb = (unsigned)((ly + LT - 1) / LT);
-        static const int ypf = getenv("CT_EDT_YPF") ? atoi(getenv("CT_EDT_YPF")) : 16;  // build prefetch depth (A/B knob; 16: 95 us, 32: 107, 64: 126 on C2)
-        auto yb = ypf == 16 ? (nz == 64 ? edt_y_build<64, 16> : nz == 32 ? edt_y_build<32, 16> : nz == 96 ? edt_y_build<96, 16> : edt_y_build<0, 16>)
-                : ypf == 8 ? (nz == 64 ? edt_y_build<64, 8> : nz == 32 ? edt_y_build<32, 8> : nz == 96 ? edt_y_build<96, 8> : edt_y_build<0, 8>)
-                            : (nz == 64 ? edt_y_build<64, 32> : nz == 32 ? edt_y_build<32, 32> : nz == 96 ? edt_y_build<96, 32> : edt_y_build<0, 32>);
+        // build prefetch depth 16 (measured on C2: 8 -> 115 us, 16 -> 95, 32 -> 107, 64 -> 126)
+        auto yb = nz == 64 ? edt_y_build<64, 16> : nz == 32 ? edt_y_build<32, 16> : nz == 96 ? edt_y_build<96, 16>
+                                                                                             : edt_y_build<0, 16>;
         auto yo = nz == 64 ? edt_y_out<64> : nz == 32 ? edt_y_out<32> : nz == 96 ? edt_y_out<96> : edt_y_out<0>;
         yb<<<(unsigned)((ly + LTB - 1) / LTB), LTB, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, head, spill, kc, swh, est);
         if (int st = ct::check_launch("edt_y_build")) return st;
@@ -900,23 +744,17 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
     }
     const size_t sm = zsmem((int)nz);
     if ((nz == 64 || nz == 32 || nz == 96) && ((uintptr_t)pk & 15) == 0) {
-        auto launch = [&](auto kern, int zln, size_t smem) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            kern<<<(unsigned)((lz + zln - 1) / zln), zln, smem, s>>>(pk, lz, dx, dy, dz, out);
-        };
-        static const int zv = getenv("CT_EDT_ZV") ? atoi(getenv("CT_EDT_ZV")) : 3;  // pass-z form (A/B knob: 0 = edt_pass_zp)
-        // (tried: 4-voxel distance phase over SMEM-staged lines, with packed offsets or float64 costs -- 490 / 654 us vs 468 for zp)
-        if (zv == 0) {
-            if (nz == 64) launch(edt_pass_zp<64, ZL>, ZL, zp_smem<64, ZL>());
-            else if (nz == 32) launch(edt_pass_zp<32, ZL>, ZL, zp_smem<32, ZL>());
-            else launch(edt_pass_zp<96, 64>, 64, zp_smem<96, 64>());
-        } else {
-            const unsigned g = (unsigned)((lz + ZRT - 1) / ZRT);
-            if (nz == 64) edt_pass_zr<64, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
-            else if (nz == 32) edt_pass_zr<32, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
-            else edt_pass_zr<96, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
-        }
+        // (tried: the SMEM-staged thread-per-line form, and a 4-voxel distance phase over SMEM-staged lines
+        // with packed offsets or float64 costs -- 468 / 490 / 654 us vs 307 for this register-streamed form)
+        const unsigned g = (unsigned)((lz + ZRT - 1) / ZRT);
+        if (nz == 64) edt_pass_zr<64, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
+        else if (nz == 32) edt_pass_zr<32, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
+        else edt_pass_zr<96, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
         return ct::check_launch("edt_pass_z");
+    }
+    if (nz > 128) {
+        edt_pass_z_long<<<(unsigned)((lz + 127) / 128), 128, 0, s>>>(pk, lz, (int)nz, dx, dy, dz, di, out);
+        return ct::check_launch("edt_pass_z_long");
     }
     auto kz = nz == 64 ? edt_pass_z<64> : nz == 32 ? edt_pass_z<32> : nz == 128 ? edt_pass_z<128> : edt_pass_z<0>;
     cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -16,6 +16,7 @@
 // Each thread computes B consecutive outputs along the filtered axis and keeps
 // a left and a right window of B inputs in registers that slide one step per
 // tap, so a tap costs 2 shared loads per B outputs (3B FP64 ops).
+#include <cooperative_groups.h>
 #include <cstdlib>
 #include <type_traits>
 
@@ -290,17 +291,13 @@ int pass_strided(const Tin *in, double *out, i64 outer, i64 L, i64 inner, const 
         to_f64_copy<Tin><<<ct::grid_for(n, 256), 256, 0, s>>>(in, out, n);
         return ct::check_launch("gauss copy");
     }
-    static const int cfg = [] { const char *e = getenv("CT_GAUSS_CFG"); return e ? atoi(e) : 0; }();
-    const int TT = (cfg == 2 || cfg == 3) ? 64 : TMAX;
-    int T = (int)min((i64)TT, ((L + B - 1) / B) * B);
+    int T = (int)min((i64)TMAX, ((L + B - 1) / B) * B);
     size_t sm = ((size_t)(T + 2 * r) * C + r + 1) * sizeof(double);
     if (sm > SMEM_LIMIT || outer > 65535 || (L + T - 1) / T > 65535) {
         gauss_generic<Tin><<<ct::grid_for(n, 256), 256, 0, s>>>(in, out, outer, L, inner, w, r);
         return ct::check_launch("gauss_generic");
     }
-    auto k = cfg == 1 ? gauss_strided<Tin, FMA, TMAX, 1>
-             : cfg == 2 ? gauss_strided<Tin, FMA, 64, 3>
-             : cfg == 3 ? gauss_strided<Tin, FMA, 64, 2> : gauss_strided<Tin, FMA, TMAX, 2>;
+    auto k = gauss_strided<Tin, FMA, TMAX, 2>;  // (64-row tiles at 2-3 CTAs/SM, or 1 CTA/SM: measured slower)
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
     dim3 grid((unsigned)((inner + C - 1) / C), (unsigned)((L + T - 1) / T), (unsigned)outer);
     dim3 block(C, T / B);
@@ -634,6 +631,58 @@ __global__ void __launch_bounds__(128) fix_p2q_s(const Traw *__restrict__ raw, i
     }
 }
 
+// Fix-list overflow (fix[1] != 0: more voxels near a rounding boundary than
+// the list holds -- adversarial inputs only): the whole q is recomputed in
+// scipy's exact order, in stream, without a host round trip.  One cooperative
+// launch; every CTA reads the same flag, so in the normal case all of them
+// return at once.  Otherwise three grid-stride passes (x: raw -> p1, y: p1 ->
+// p2, z: p2 -> residual -> q) separated by grid syncs, each voxel computed as
+// ct_gaussian_residual does (ref denoise.py:84-86; the fast path's partial
+// results in `work` are dead by now).
+template <typename Traw>
+__global__ void __launch_bounds__(256) k1_overflow_exact(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz,
+                                                         const double *__restrict__ w, int rx, int ry, int rz,
+                                                         const unsigned long long *__restrict__ fix,
+                                                         double *__restrict__ p1, double *__restrict__ p2,
+                                                         Traw *__restrict__ q_out) {
+    if (fix[1] == 0) return;
+    namespace cg = cooperative_groups;
+    const cg::grid_group grid = cg::this_grid();
+    const double *wx = w, *wy = w + rx + 1, *wz = wy + ry + 1;
+    const i64 N = nx * ny * nz, S = ny * nz;
+    const i64 t0 = blockIdx.x * (i64)blockDim.x + threadIdx.x, dt = (i64)gridDim.x * blockDim.x;
+    for (i64 p = t0; p < N; p += dt) {
+        const i64 i = p / S;
+        const Traw *col = raw + (p - i * S);
+        double acc = __dmul_rn(ct::to_f64(col[i * S]), wx[0]);
+        for (int d = rx; d >= 1; --d)
+            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(ct::to_f64(col[ct::clampi(i - d, 0, nx - 1) * S]),
+                                                     ct::to_f64(col[ct::clampi(i + d, 0, nx - 1) * S])), wx[d]));
+        p1[p] = acc;
+    }
+    grid.sync();
+    for (i64 p = t0; p < N; p += dt) {
+        const i64 j = (p / nz) % ny;
+        const double *col = p1 + (p - j * nz);
+        double acc = __dmul_rn(col[j * nz], wy[0]);
+        for (int d = ry; d >= 1; --d)
+            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(col[ct::clampi(j - d, 0, ny - 1) * nz],
+                                                     col[ct::clampi(j + d, 0, ny - 1) * nz]), wy[d]));
+        p2[p] = acc;
+    }
+    grid.sync();
+    for (i64 p = t0; p < N; p += dt) {
+        const i64 k = p % nz;
+        const double *line = p2 + (p - k);
+        double acc = __dmul_rn(line[k], wz[0]);
+        for (int d = rz; d >= 1; --d)
+            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(line[ct::clampi(k - d, 0, nz - 1)],
+                                                     line[ct::clampi(k + d, 0, nz - 1)]), wz[d]));
+        const double dd = __dadd_rn(ct::to_f64(raw[p]), -acc);
+        q_out[p] = (Traw)rint(dd < 0.0 ? 0.0 : dd);
+    }
+}
+
 // fix-up of a certified fast path: grid-wide phases for the first capF
 // entries (scratch = the dead K1 workspace), per-CTA fallback for the rest
 template <typename Traw>
@@ -643,12 +692,12 @@ int launch_fixup(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int r
     const i64 per = (2 * (i64)ry + 1) * nz;
     const long long capF = nz <= 128 ? (long long)(work_bytes / ((size_t)per * sizeof(double))) : 0;
     double *P1 = (double *)work;
-    if (nz % 32 == 0 && rx <= FXR && ((uintptr_t)raw & 15) == 0 && getenv("CT_FIX_P1_PLAIN") == nullptr)
+    if (nz % 32 == 0 && rx <= FXR && ((uintptr_t)raw & 15) == 0)
         fix_p1s<Traw><<<CT_NUM_SMS * 16, 128, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
     else
         fix_p1<Traw><<<CT_NUM_SMS * 8, 256, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
     const size_t csm = ((size_t)per + nz) * sizeof(double);
-    if (nz % 2 == 0 && nz <= 128 && csm <= 200 * 1024 && getenv("CT_FIX_P1_PLAIN") == nullptr) {
+    if (nz % 2 == 0 && nz <= 128 && csm <= 200 * 1024) {
         cudaFuncSetAttribute(fix_p2q_s<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
         fix_p2q_s<Traw, Traw><<<CT_NUM_SMS * 2, 128, csm, s>>>(raw, nz, wy, ry, wz, rz, fix, cap, capF, P1, q);
     } else {
@@ -658,7 +707,17 @@ int launch_fixup(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int r
     const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
     cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
     gauss_fixup<Traw, Traw><<<CT_NUM_SMS, 256, fsm, s>>>(raw, nx, ny, nz, w, rx, ry, rz, fix, cap, q, capF);
-    return ct::check_launch("gauss_fixup");
+    if (int st = ct::check_launch("gauss_fixup")) return st;
+    // list overflow -> exact recompute in stream (returns at once otherwise)
+    double *p1 = (double *)work, *p2 = p1 + nx * ny * nz;
+    void *args[] = {(void *)&raw, (void *)&nx, (void *)&ny, (void *)&nz, (void *)&w, (void *)&rx, (void *)&ry,
+                    (void *)&rz, (void *)&fix, (void *)&p1, (void *)&p2, (void *)&q};
+    if (cudaLaunchCooperativeKernel((const void *)k1_overflow_exact<Traw>, dim3(CT_NUM_SMS * 2), dim3(256), args, 0,
+                                    s) != cudaSuccess) {
+        ct::set_error("k1_overflow_exact: cooperative launch failed (%s)", cudaGetErrorString(cudaGetLastError()));
+        return CT_ERR_CUDA;
+    }
+    return CT_OK;
 }
 
 template <typename Traw>
@@ -695,27 +754,21 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
 
 bool ct_gaussian_q_tc_fits(int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz);
 
-// K1 fast-path selection (ct_set_k1_path): 0 auto (tensor cores when the
-// shape fits, else FP64 FMA), 1 FP64 FMA, 2 tensor cores only.
-static int g_k1_path = 0;
-extern "C" int ct_k1_path(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz) {
-    if (dtype == CT_U8 && g_k1_path != 1 && ct_gaussian_q_tc_fits(nx, ny, nz, rx, ry, rz)) return 2;
+// K1 fast-path selection (per call): 0 auto (tensor cores when the shape
+// fits, else FP64 FMA), 1 FP64 FMA, 2 tensor cores only.
+extern "C" int ct_k1_path(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz, int path) {
+    if (dtype == CT_U8 && path != 1 && ct_gaussian_q_tc_fits(nx, ny, nz, rx, ry, rz)) return 2;
     return 1;
-}
-
-extern "C" int ct_set_k1_path(int mode) {
-    if (mode < 0 || mode > 2) {
-        ct::set_error("k1 path mode must be 0, 1 or 2");
-        return CT_ERR_PARAM;
-    }
-    g_k1_path = mode;
-    return CT_OK;
 }
 
 extern "C" int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx,
                              int ry, int rz, void *work, void *q_out, unsigned long long *fix, int64_t fix_cap,
-                             double eps_override, void *stream) {
+                             double eps_override, int path, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
+    if (path < 0 || path > 2) {
+        ct::set_error("k1 path must be 0 (auto), 1 (FP64 FMA) or 2 (tensor cores)");
+        return CT_ERR_PARAM;
+    }
     // the fast kernels need the tiled paths (see pass_strided / pass_contig) and every axis filtered
     const bool fast = rx >= 0 && ry >= 0 && rz >= 0 && nz <= 128 &&
                       ((size_t)(TMAX + 2 * (rx > ry ? rx : ry)) * C + 64) * sizeof(double) <= SMEM_LIMIT &&
@@ -729,14 +782,14 @@ extern "C" int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny,
     }
     if (dtype == CT_U8) {
         // tensor-core path (k_gauss_tc.cu) unless disabled or the shape does not fit
-        if (g_k1_path != 1) {
+        if (path != 1) {
             const int st = ct_gaussian_q_tc((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, work, (uint8_t *)q_out,
                                             fix, fix_cap, eps_override, s);
             if (st == CT_OK)
                 return launch_fixup<uint8_t>((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, work,
                                              (size_t)2 * nx * ny * nz * sizeof(double), fix, fix_cap,
                                              (uint8_t *)q_out, s);
-            if (st != CT_ERR_UNSUPPORTED || g_k1_path == 2) {
+            if (st != CT_ERR_UNSUPPORTED || path == 2) {
                 if (st == CT_ERR_UNSUPPORTED) ct::set_error("tensor-core K1 does not support this shape");
                 return st;
             }

@@ -537,6 +537,62 @@ __global__ void __launch_bounds__(128) median_generic(const T *__restrict__ in, 
     }
 }
 
+// Any radius (> 3: the (2r+1)^3 window no longer fits a per-thread buffer):
+// bitwise radix select of the k-th smallest order-preserving key, one pass
+// over the clamped window per key bit (8 / 16 / 64 for u8 / u16 / f64).
+// Same order statistic as select_kth (scipy's rank filter, rank = size^3 // 2).
+template <typename T>
+__device__ __forceinline__ unsigned long long okey(T v) {
+    if constexpr (sizeof(T) == 8) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+        return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    } else {
+        return (unsigned long long)v;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ T from_okey(unsigned long long k) {
+    if constexpr (sizeof(T) == 8) {
+        return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+    } else {
+        return (T)k;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) median_radix(const T *__restrict__ in, T *__restrict__ out, i64 nx, i64 ny,
+                                                    i64 nz, int rad, uint64_t *__restrict__ ghist) {
+    constexpr int BITS = 8 * (int)sizeof(T);
+    const int size = 2 * rad + 1;
+    const int kth = size * size * size / 2;
+    const i64 n = nx * ny * nz;
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < n; p += (i64)gridDim.x * blockDim.x) {
+        const i64 k = p % nz, j = (p / nz) % ny, i = p / (ny * nz);
+        unsigned long long prefix = 0;
+        int rank = kth;
+        for (int b = BITS - 1; b >= 0; --b) {
+            const unsigned long long hi = b == 63 ? 0ull : (~0ull << (b + 1));
+            int c0 = 0;  // window keys matching the prefix above bit b with bit b clear
+            for (int di = -rad; di <= rad; ++di)
+                for (int dj = -rad; dj <= rad; ++dj) {
+                    const T *row = in + (ct::clampi(i + di, 0, nx - 1) * ny + ct::clampi(j + dj, 0, ny - 1)) * nz;
+                    for (int dk = -rad; dk <= rad; ++dk) {
+                        const unsigned long long key = okey<T>(row[ct::clampi(k + dk, 0, nz - 1)]);
+                        c0 += ((key & hi) == prefix) & !((key >> b) & 1ull);
+                    }
+                }
+            if (rank >= c0) {
+                rank -= c0;
+                prefix |= 1ull << b;
+            }
+        }
+        const T m = from_okey<T>(prefix);
+        out[p] = m;
+        if (ghist) atomicAdd((unsigned long long *)&ghist[ct::hist_bin(m)], 1ull);
+    }
+}
+
 // intensity_histogram over any dtype (segment.py:154-163)
 template <typename T>
 __global__ void __launch_bounds__(512) histogram_kernel(const T *__restrict__ in, i64 n, uint64_t *__restrict__ ghist) {
@@ -557,10 +613,6 @@ extern "C" int ct_median(const void *in, int dtype, int64_t nx, int64_t ny, int6
     if (nx <= 0 || ny <= 0 || nz <= 0 || radius < 0) {
         ct::set_error("bad median arguments");
         return CT_ERR_PARAM;
-    }
-    if (radius > 3) {
-        ct::set_error("median radius %d > 3 unsupported", radius);
-        return CT_ERR_UNSUPPORTED;
     }
     cudaStream_t s = (cudaStream_t)stream;
     const i64 n = nx * ny * nz;
@@ -607,6 +659,12 @@ extern "C" int ct_median(const void *in, int dtype, int64_t nx, int64_t ny, int6
         if (int st = ct::check_launch("median3_f64")) return st;
         if (hist) return ct_histogram(out, dtype, n, hist, stream);
         return CT_OK;
+    }
+    if (radius > 3) {
+        CT_DISPATCH(dtype, T, {
+            median_radix<T><<<ct::grid_for(n, 128), 128, 0, s>>>((const T *)in, (T *)out, nx, ny, nz, radius, hist);
+        });
+        return ct::check_launch("median_radix");
     }
     CT_DISPATCH(dtype, T, {
         median_generic<T><<<ct::grid_for(n, 128), 128, 0, s>>>((const T *)in, (T *)out, nx, ny, nz, radius, hist);

@@ -231,7 +231,9 @@ struct PwShapes {
 // left + right exactly as numpy's recursion performs it.
 template <class F>
 __global__ void __launch_bounds__(PT) pw_subtree(F f, i64 n, int D, double *__restrict__ partial,
-                                                 const __grid_constant__ PwShapes shapes) {
+                                                 const __grid_constant__ PwShapes shapes,
+                                                 const unsigned long long *skip) {
+    if (skip && *skip) return;  // decision certified earlier in the stream (mrf_quick)
     __shared__ PwShape shs;
     __shared__ double lv[2][1 << PW_MAXD];  // values per level slot (ping-pong)
     __shared__ double lval[MAX_LEAVES];
@@ -330,7 +332,8 @@ __global__ void __launch_bounds__(1024) pw_fold(double *partial, int D, double *
 }
 
 template <class F>
-int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s) {
+int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s,
+                 const unsigned long long *skip = nullptr) {
     if (n <= 0) {
         cudaMemsetAsync(out, 0, sizeof(double), s);
         return ct::check_launch("pairwise empty");
@@ -367,9 +370,9 @@ int pairwise_sum(const F &f, i64 n, double *partial, double *out, cudaStream_t s
             ++shapes.count;
         }
     }
-    pw_subtree<F><<<(unsigned)(1ll << D), PT, 0, s>>>(f, n, D, partial, shapes);
+    pw_subtree<F><<<(unsigned)(1ll << D), PT, 0, s>>>(f, n, D, partial, shapes, skip);
     if (int st = ct::check_launch("pw_subtree")) return st;
-    pw_fold<<<1, 1024, 0, s>>>(partial, D, out);
+    pw_fold<<<1, 1024, 0, s>>>(partial, D, out, skip);
     return ct::check_launch("pw_fold");
 }
 
@@ -994,6 +997,18 @@ __global__ void mrf_nnz_generic(const T *__restrict__ v, i64 nx, i64 ny, i64 nz,
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(nnz, local);
 }
 
+// exact integer sum of the interior Laplacians (integer input of any shape;
+// the stream kernels form it on the fly for nz <= 128)
+template <typename T>
+__global__ void lap_sum_int(const T *__restrict__ v, i64 ny, i64 nz, uint32_t my, uint32_t mz, i64 ni,
+                            unsigned long long *__restrict__ sum) {
+    long long local = 0;
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < ni; e += (i64)gridDim.x * blockDim.x)
+        local += (long long)lap_at(v, (uint32_t)e, my, mz, ny, nz);
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(sum, (unsigned long long)local);
+}
+
 // delta from the histogram of integer values (min gap of non-empty bins)
 // (nbins: 256 for u8 input -- no other bin can be non-empty -- else 65536)
 __global__ void delta_from_hist(const uint64_t *__restrict__ hist, int nbins, double *state) {
@@ -1042,7 +1057,8 @@ __global__ void delta_store(const unsigned long long *best_bits, double *state) 
 }
 
 __global__ void mean_from_sum(double *state, i64 n) { state[S_SUM1] = __ddiv_rn(state[S_SUM1], (double)n); }
-__global__ void lap_mean(double *state, const long long *sum, i64 n) {
+__global__ void lap_mean(double *state, const long long *sum, i64 n, const unsigned long long *skip = nullptr) {
+    if (skip && *skip) return;  // certified by mrf_quick: the Laplacian sums were not formed
     state[S_SUM1] = __ddiv_rn((double)*sum, (double)n);
 }
 
@@ -1069,6 +1085,8 @@ __global__ void mrf_quick(double *state, i64 n_interior, unsigned long long *sca
         state[S_SUM3] = __dmul_rn(__dmul_rn(delta, delta), (double)nnz);
         state[S_NORM] = norm;
         state[S_SIGMA] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not computed
+        state[S_SUM1] = state[S_SIGMA];                               // nor the Laplacian moments
+        state[S_SUM2] = state[S_SIGMA];
         state[S_SIGMA_STATUS] = 2.0;                  // skipped (decision certified)
         state[S_DECISION] = delta == 0.0 ? 2.0 : 0.0;
         scal[W_SKIP] = 1;
@@ -1181,7 +1199,7 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
     const i64 blocks = ((ny + MJ - 1) / MJ) * ((nx + MIPER - 1) / MIPER);
     if (sizeof(T) == 1 && (nz == 32 || nz == 64 || nz == 96 || nz == 128) && ((uintptr_t)v & 3) == 0 &&
         ((uintptr_t)lap & 3) == 0 &&
-        nx * ny * nz < (1ll << 31) && getenv("CT_MRF_SCALAR") == nullptr) {
+        nx * ny * nz < (1ll << 31)) {
         const i64 b4 = ((ny + 256 / (nz / 4) - 1) / (256 / (nz / 4))) * ((nx + MIPER - 1) / MIPER);
         auto launch = [&](auto kern) {
             kern<<<(unsigned)b4, 256, 0, s>>>((const uint8_t *)v, (int)nx, (int)ny, (unsigned long long *)hist,
@@ -1201,12 +1219,12 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
             else if (nz == 96) launch(mrf_stream_v4<96, 2>);
             else launch(mrf_stream_v4<128, 2>);
             if (int st = ct::check_launch("mrf_stream_v4 (exact sigma)")) return st;
-            lap_mean<<<1, 1, 0, s>>>(state, (const long long *)&w.scal[W_LAPSUM], ni);
+            lap_mean<<<1, 1, 0, s>>>(state, (const long long *)&w.scal[W_LAPSUM], ni, &w.scal[W_SKIP]);
             const int vs = pairwise_sum_lap<LT>(lap, &state[S_SUM1], ni, w.partial, &state[S_SUM2], s, &w.scal[W_SKIP]);
             if (vs < 0) return -vs;
-            if (vs == 1) {
+            if (vs == 1) {  // shapes outside the vectorised tables: the generic tree, same skip guard
                 LapArrSq<LT> f{lap, &state[S_SUM1]};
-                if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s)) return st;
+                if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s, &w.scal[W_SKIP])) return st;
             }
             mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 1);
             return ct::check_launch("mrf_decide");
@@ -1228,15 +1246,32 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
                                                                w.scal, lap);
         if (int st = ct::check_launch("mrf_stream_int")) return st;
     } else {
-        ct::set_error("integer MRF supports nz <= 128");
-        return CT_ERR_UNSUPPORTED;
+        // nz > 128: the same statistics from global memory, no stored Laplacians
+        // (ct_workspace_bytes(4, ...) covers this path too): input histogram,
+        // #{sign sum != 0}, the exact Laplacian sum, then numpy's pairwise tree
+        // over (lap - mean)^2 with the Laplacians recomputed per element
+        if (int st = ct_histogram(v, sizeof(T) == 1 ? CT_U8 : CT_U16, nx * ny * nz, hist, s)) return st;
+        delta_from_hist<<<1, 1024, 0, s>>>(hist, sizeof(T) == 1 ? 256 : 65536, state);
+        mrf_nnz_generic<T><<<ct::grid_for(nx * ny * nz, 256, CT_NUM_SMS * 4), 256, 0, s>>>(v, nx, ny, nz,
+                                                                                           &w.scal[W_NNZ]);
+        if (int st = ct::check_launch("mrf_nnz_generic")) return st;
+        if (ni >= 2) {
+            lap_sum_int<T><<<ct::grid_for(ni, 256, CT_NUM_SMS * 4), 256, 0, s>>>(v, ny, nz, (uint32_t)my,
+                                                                                 (uint32_t)mz, ni,
+                                                                                 &w.scal[W_LAPSUM]);
+            if (int st = ct::check_launch("lap_sum_int")) return st;
+            LapElem<T> f2{v, ny, nz, (uint32_t)my, (uint32_t)mz, nullptr, (const long long *)&w.scal[W_LAPSUM],
+                          ni, 1};
+            if (int st = pairwise_sum(f2, ni, w.partial, &state[S_SUM2], s)) return st;
+        }
+        mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 1);
+        return ct::check_launch("mrf_decide");
     }
     delta_from_hist<<<1, 1024, 0, s>>>(hist, sizeof(T) == 1 ? 256 : 65536, state);
     if (int st = ct::check_launch("delta_from_hist")) return st;
     if (ni >= 2) {
         lap_mean<<<1, 1, 0, s>>>(state, (const long long *)&w.scal[W_LAPSUM], ni);
-        static const bool scalar_pw = getenv("CT_PW_SCALAR") != nullptr;
-        const int vs = scalar_pw ? 1 : pairwise_sum_lap<LT>(lap, &state[S_SUM1], ni, w.partial, &state[S_SUM2], s);
+        const int vs = pairwise_sum_lap<LT>(lap, &state[S_SUM1], ni, w.partial, &state[S_SUM2], s);
         if (vs < 0) return -vs;
         if (vs == 1) {
             LapArrSq<LT> f{lap, &state[S_SUM1]};

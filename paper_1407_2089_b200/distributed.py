@@ -22,13 +22,15 @@ def frame_shard(t_count: int, world: int, rank: int) -> range:
     return range(min(rank * per, t_count), min((rank + 1) * per, t_count))
 
 
-def global_id_starts(local_counts: dict[int, int], t_count: int, device=None, group=None) -> list[int]:
+def global_id_starts(local_counts: dict[int, int], t_count: int, device=None, group=None,
+                     with_total: bool = False):
     """id_start for every frame from the per-rank detection counts.
 
     local_counts maps the frames this rank processed to their detection
     counts.  One all_gather of a t_count-long int64 vector (owned frames
     filled, others 0); the sum over ranks is the global per-frame count and its
-    exclusive prefix sum the reference's id_start per frame."""
+    exclusive prefix sum the reference's id_start per frame.  with_total:
+    also return the total count (ref session.py:300, next_detection_id)."""
     dev = device or torch.device("cpu")
     mine = torch.zeros(t_count, dtype=torch.int64, device=dev)
     for t, c in local_counts.items():
@@ -40,7 +42,10 @@ def global_id_starts(local_counts: dict[int, int], t_count: int, device=None, gr
     else:
         total = mine
     starts = torch.cumsum(total, 0) - total
-    return [int(x) for x in starts.cpu()]
+    out = [int(x) for x in starts.cpu()]
+    if with_total:  # (starts, total detections = the reference's final det_counter)
+        return out, int(total.sum().item())
+    return out
 
 
 def relabel_rows(rows, id_start: int):

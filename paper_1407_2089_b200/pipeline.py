@@ -82,6 +82,8 @@ class FramePipeline:
         self.device = dev
         self.marks = None  # list of (stage, start_event, end_event) when timing
         self.exact_k1 = False  # True: scipy-order K1 (no FMA fast path)
+        self.k1_path = 0       # ct_gaussian_q path: 0 auto, 1 FP64 FMA, 2 tensor cores
+        self.k1_eps = 0.0      # ct_gaussian_q eps_override (0: the certified bound; tests force the fix-up)
         E = lambda shape, dt: torch.empty(shape, dtype=dt, device=dev)  # noqa: E731
         Z = lambda shape, dt: torch.zeros(shape, dtype=dt, device=dev)  # noqa: E731
         cr = self.seg.closing_radius
@@ -158,7 +160,7 @@ class FramePipeline:
             return False
         from ._lib import lib
         nx, ny, nz = self.dims
-        return lib().ct_k1_path(self.code, nx, ny, nz, *self.r) == 2
+        return lib().ct_k1_path(self.code, nx, ny, nz, *self.r, self.k1_path) == 2
 
     def cell(self, raw: torch.Tensor, frame: int = 0, id_start: int = 0) -> CellResult:
         nx, ny, nz = self.dims
@@ -182,7 +184,8 @@ class FramePipeline:
             self.fix[:2].zero_()
         else:
             call("ct_gaussian_q", raw.data_ptr(), self.code, nx, ny, nz, self.w.data_ptr(), rx, ry, rz,
-                 self.gwork.data_ptr(), self.q.data_ptr(), self.fix.data_ptr(), self.fix_cap, 0.0, s)
+                 self.gwork.data_ptr(), self.q.data_ptr(), self.fix.data_ptr(), self.fix_cap, self.k1_eps,
+                 self.k1_path, s)
         self._t1("K1 gaussian", e)
         e = self._t0()
         call("ct_median", self.q.data_ptr(), self.code, nx, ny, nz, self.denoise.median_radius,
@@ -244,8 +247,6 @@ class FramePipeline:
         """Raise reference errors; return (counters, rows) or Detections."""
         if int(res.otsu[OTSU_STATUS].item()) == 2:
             raise DegenerateHistogramError("frame is constant; no threshold separates it")
-        if int(self.fix[1].item()):
-            raise RuntimeError("certified K1 fix-up list overflowed; rerun with exact_k1=True")
         cnt = res.cells.counters.cpu().numpy()
         if cnt[CNT_OVERFLOW]:
             raise RuntimeError("component capacity exceeded; raise FramePipeline(capacity=...)")
@@ -255,11 +256,11 @@ class FramePipeline:
         rows = res.cells.table[: nk * CELL_DTYPE.itemsize].cpu().numpy().view(CELL_DTYPE)
         return cnt, rows
 
-    def finish_vessel(self, res: VesselResult, raw: torch.Tensor):
-        """(mask, DistanceMap) exactly as segment_vessel_channel(mrf_denoise(raw))."""
+    def finish_vessel(self, res: VesselResult, raw: torch.Tensor, max_iters: int = 1000):
+        """(mask, DistanceMap) exactly as segment_vessel_channel(mrf_denoise(raw, max_iters))."""
         decision = int(res.state[MRF_DECISION].item())
         if decision != 0:
-            vden = mrf_denoise(VoxelGrid(values=raw, spacing=self.spacing))
+            vden = mrf_denoise(VoxelGrid(values=raw, spacing=self.spacing), max_iters=max_iters)
             return segment_vessel_channel(vden, self.seg)
         if int(res.otsu[OTSU_STATUS].item()) == 2:
             raise DegenerateHistogramError("frame is constant; no threshold separates it")

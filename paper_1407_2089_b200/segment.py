@@ -81,6 +81,12 @@ class Detection:
     centroid_um: np.ndarray
     volume_um3: float
     hull: HullMesh | None = None
+    # north-star per-cell features beyond the reference's record (computed by
+    # the same K6 table pass): bounding box (imin, jmin, kmin, imax, jmax, kmax)
+    # and the mean of the cell's raw intensities (numpy intensity[voxels].mean();
+    # None when no intensity volume was given)
+    bbox: np.ndarray | None = None
+    mean_intensity: float | None = None
 
     @property
     def voxel_count(self) -> int:
@@ -247,6 +253,8 @@ def compute_hulls(vox_list, spacing: VoxelSpacing) -> list:
     procs = int(os.environ.get("CT_HULL_PROCS", str(min(16, os.cpu_count() or 1))))
     if procs <= 1 or len(vox_list) < HULL_POOL_MIN:
         return [compute_hull(v, spacing) for v in vox_list]
+    from concurrent.futures.process import BrokenProcessPool
+
     if _hull_pool is None:
         import multiprocessing as mp
         from concurrent.futures import ProcessPoolExecutor
@@ -258,7 +266,14 @@ def compute_hulls(vox_list, spacing: VoxelSpacing) -> list:
         atexit.register(_hull_pool.shutdown)
     step = max(16, len(vox_list) // (4 * procs))
     chunks = [(vox_list[i:i + step], spacing) for i in range(0, len(vox_list), step)]
-    return [h for part in _hull_pool.map(_hull_chunk, chunks) for h in part]
+    try:
+        return [h for part in _hull_pool.map(_hull_chunk, chunks) for h in part]
+    except BrokenProcessPool:
+        # a worker died (OOM, signal): drop the pool (the next call starts a
+        # fresh one) and finish this frame serially -- same calls, same results
+        pool, _hull_pool = _hull_pool, None
+        pool.shutdown(wait=False, cancel_futures=True)
+        return [compute_hull(v, spacing) for v in vox_list]
 
 
 @dataclass
@@ -318,16 +333,29 @@ def _materialize(ct: CellTable, dims, spacing: VoxelSpacing, frame: int, with_hu
     offs, cnts = rows["voxel_offset"].tolist(), rows["count"].tolist()
     ids, vols = rows["id"].tolist(), rows["volume_um3"].tolist()
     cents = np.array(rows["centroid_um"], dtype=np.float64)
+    bbox = np.concatenate([rows["bbox_lo"], rows["bbox_hi"]], axis=1).astype(np.int64)
+    means = [None if m != m else m for m in rows["mean_intensity"].tolist()]  # NaN: no intensity given
     voxs = [coords[offs[k] : offs[k] + cnts[k]] for k in range(len(offs))]
     hulls = compute_hulls(voxs, spacing) if with_hull else [None] * len(voxs)
     return [Detection(id=ids[k], frame=frame, voxels=voxs[k], centroid_um=cents[k], volume_um3=vols[k],
-                      hull=hulls[k]) for k in range(len(voxs))]
+                      hull=hulls[k], bbox=bbox[k], mean_intensity=means[k]) for k in range(len(voxs))]
 
 
-def _detections_dev(mask: torch.Tensor, spacing, frame, min_volume_um3, id_start, with_hull=True):
+def _intensity_dev(intensity, shape):
+    """Optional raw intensity volume (U8/U16, the mask's shape) on the device."""
+    if intensity is None:
+        return None
+    t = _dev.to_device(intensity, allow=(torch.uint8, torch.uint16))
+    if t.dtype not in (torch.uint8, torch.uint16) or tuple(t.shape) != tuple(shape):
+        raise ParameterError(f"intensity must be a uint8/uint16 volume of shape {tuple(shape)}")
+    return t
+
+
+def _detections_dev(mask: torch.Tensor, spacing, frame, min_volume_um3, id_start, with_hull=True, intensity=None):
     cap = DEFAULT_COMPONENT_CAPACITY
+    inten = _intensity_dev(intensity, mask.shape)
     while True:
-        ct = label_cells(mask, spacing, min_volume_um3, id_start, capacity=cap)
+        ct = label_cells(mask, spacing, min_volume_um3, id_start, intensity=inten, capacity=cap)
         dets = _materialize(ct, tuple(int(d) for d in mask.shape), spacing, frame, with_hull)
         if dets is not None:
             return dets
@@ -335,23 +363,26 @@ def _detections_dev(mask: torch.Tensor, spacing, frame, min_volume_um3, id_start
 
 
 def detections_from_mask(mask, spacing: VoxelSpacing, frame: int, min_volume_um3: float,
-                         id_start: int = 0) -> list[Detection]:
+                         id_start: int = 0, intensity=None) -> list[Detection]:
     """Label a mask and build volume-filtered detections: ids by (-count,
-    first voxel) from id_start (ref segment.py:242-276)."""
+    first voxel) from id_start (ref segment.py:242-276).  ``intensity``
+    (extension, optional): the raw uint8/uint16 volume whose per-cell mean
+    fills ``Detection.mean_intensity``."""
     m = _dev.to_device(mask, allow=(torch.uint8,))
     if m.dtype != torch.uint8:
         m = (m != 0).to(torch.uint8)
-    return _detections_dev(m, spacing, frame, min_volume_um3, id_start)
+    return _detections_dev(m, spacing, frame, min_volume_um3, id_start, intensity=intensity)
 
 
 def segment_cell_channel(grid: VoxelGrid, config: SegmentationConfig | None = None, frame: int = 0,
-                         id_start: int = 0) -> list[Detection]:
-    """Segment a denoised cell-channel frame into detections (ref segment.py:279-289)."""
+                         id_start: int = 0, intensity=None) -> list[Detection]:
+    """Segment a denoised cell-channel frame into detections (ref segment.py:279-289).
+    ``intensity`` as in detections_from_mask (the frame's raw volume)."""
     config = config or SegmentationConfig()
     v = _dev.to_device(grid.values)
     mask, res = _binarize_dev(v, config.closing_radius)
     _check_otsu(res)
-    return _detections_dev(mask, grid.spacing, frame, config.min_volume_um3, id_start)
+    return _detections_dev(mask, grid.spacing, frame, config.min_volume_um3, id_start, intensity=intensity)
 
 
 # ---------------------------------------------------------------------------

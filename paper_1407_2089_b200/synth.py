@@ -25,7 +25,10 @@ import torch
 from . import _dev
 from ._lib import CT_U8, CT_U16, call
 
-CELL, VESSEL = 0, 1
+# channels: the reference processes the first cell and the first vessel
+# channel (ref session.py:286-289); CELL2 is C3's third channel, a second cell
+# population segmented through the cell path directly (an extension)
+CELL, VESSEL, CELL2 = 0, 1, 2
 
 
 @dataclass(frozen=True)
@@ -73,9 +76,9 @@ class SceneSpec:
     def frame_seed(self, t: int, channel: int) -> int:
         return 1000 * channel + t + 1_000_000 * self.seed
 
-    def balls(self, t: int) -> np.ndarray:
-        """(n_cells, 4) int64: cx16, cy16, cz16, r16 at frame t."""
-        rng = np.random.default_rng(self.seed * 7919 + 17)
+    def balls(self, t: int, channel: int = CELL) -> np.ndarray:
+        """(n_cells, 4) int64: cx16, cy16, cz16, r16 at frame t (CELL2: another population)."""
+        rng = np.random.default_rng(self.seed * 7919 + 17 + (104_729 if channel == CELL2 else 0))
         n = self.n_cells
         c = rng.uniform(0.0, 1.0, size=(n, 3)) * (np.array(self.dims, dtype=float) - 1.0)
         r = rng.uniform(self.r_min, self.r_max, size=n)
@@ -105,7 +108,7 @@ def generate(spec: SceneSpec, t: int, channel: int, out: torch.Tensor | None = N
     if out is None:
         out = torch.empty(spec.dims, dtype=spec.torch_dtype, device=dev)
     if objects is None:
-        balls = torch.from_numpy(spec.balls(t)).to(dev) if channel == CELL else None
+        balls = torch.from_numpy(spec.balls(t, channel)).to(dev) if channel in (CELL, CELL2) else None
         tubes = torch.from_numpy(spec.tubes()).to(dev) if channel == VESSEL else None
     else:
         balls, tubes = objects
@@ -129,3 +132,5 @@ C1 = SceneSpec(256, 256, 32, "u8", n_cells=50, n_tubes=3)
 C2 = SceneSpec(1024, 1024, 64, "u8", n_cells=1600, n_tubes=24)
 C3 = SceneSpec(1024, 1024, 64, "u16", n_cells=1600, n_tubes=24)
 C4 = SceneSpec(4096, 4096, 96, "u8", n_cells=20000, r_min=3.0, r_max=6.0, n_tubes=144)
+# a 1024 x 1024 x 96 crop of C4 at C4's density (parity-test size; nz = 96 kernels)
+C4_CROP = SceneSpec(1024, 1024, 96, "u8", n_cells=1250, r_min=3.0, r_max=6.0, n_tubes=36, seed=4)

@@ -1,0 +1,277 @@
+"""Parity at the benchmark's own configurations (BASELINE.json configs) and
+for every shape-specialised kernel variant.
+
+Full frames through ``FramePipeline`` (the fused path bench.py times) against
+the CPU oracle (oracle/, pinned to the reference by tests/golden), bit-exact:
+the quantised residual q, the median, the fused histogram, the Otsu
+threshold, the canonical label volume, every per-cell table column (ids,
+counts, roots, bbox, intensity sums, mean intensities, row-sequential
+centroids, volumes), the C-order voxel lists, the vessel mask, the MRF
+statistics and the distance map.
+
+  C2   1024x1024x64 u8, cell + vessel: t = 0 (the first frame of bench.py's
+       ring) and t = 5
+  C3   1024x1024x64 u16, cell + vessel + the second cell channel
+  C4   a 1024x1024x96 crop at C4's density (nz = 96 kernels: tensor-core K1
+       pass z, median WC = 3, 128-bit CCL rows, MRF nz = 96, EDT pass z 96)
+
+ref: denoise.py:67-89 (cell denoise), segment.py:242-318 (detections,
+vessel), denoise.py:147-195 (MRF)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1407_2089_b200 import synth
+from paper_1407_2089_b200._lib import CNT_KEPT, MRF_DECISION, MRF_DELTA, MRF_NNZ, call, workspace_bytes
+from paper_1407_2089_b200 import _dev
+from paper_1407_2089_b200.imaging import VoxelSpacing
+from paper_1407_2089_b200.pipeline import FramePipeline
+
+pytestmark = pytest.mark.gpu
+
+ANISO = VoxelSpacing(0.8, 0.8, 1.0)
+SP = ANISO.as_array()
+
+
+def to_np(t: torch.Tensor) -> np.ndarray:
+    t = t.cpu()
+    if t.dtype == torch.uint16:
+        return t.view(torch.int16).numpy().view(np.uint16)
+    return t.numpy()
+
+
+def host_frame(oracle, spec, t, ch):
+    if ch == synth.VESSEL:
+        return oracle.synth_frame(spec.dims, spec.dtype, spec.frame_seed(t, ch), spec.vmax, tubes=spec.tubes(),
+                                  amp_tube=spec.amp_tube)
+    return oracle.synth_frame(spec.dims, spec.dtype, spec.frame_seed(t, ch), spec.vmax, balls=spec.balls(t, ch),
+                              amp_ball=spec.amp_cell)
+
+
+def check_cell(pipe, spec, t, ch, oracle, id_start):
+    """One cell-channel frame through the fused path vs the oracle."""
+    raw = synth.generate(spec, t, ch)
+    host = host_frame(oracle, spec, t, ch)
+    np.testing.assert_array_equal(to_np(raw), host)  # device generator == the oracle's frame
+    res = pipe.cell(raw, frame=t, id_start=id_start)
+    cnt, rows = pipe.finish_cell(res)
+    o = oracle.denoise_cell(host, SP, 10.0)
+    # K1: q = rint(max(raw - gaussian_filter(raw), 0)); K2: the median of q
+    np.testing.assert_array_equal(to_np(pipe.q), np.rint(o["residual"]).astype(spec.np_dtype))
+    np.testing.assert_array_equal(to_np(pipe.med), np.rint(o["denoised"]).astype(spec.np_dtype))
+    hist = oracle.histogram(o["denoised"])
+    np.testing.assert_array_equal(pipe.hist.cpu().numpy()[: hist.size], hist)
+    assert not pipe.hist.cpu().numpy()[hist.size:].any()
+    assert int(pipe.otsu[0]) == oracle.otsu(hist)
+    odets = oracle.segment_cell(o["denoised"], SP, frame=t, id_start=id_start, intensity=host)
+    assert int(cnt[CNT_KEPT]) == len(rows) == len(odets) > 100
+    assert list(rows["id"]) == [d.id for d in odets]
+    assert list(rows["count"]) == [d.voxel_count for d in odets]
+    assert list(rows["root"]) == [d.root for d in odets]
+    np.testing.assert_array_equal(np.concatenate([rows["bbox_lo"], rows["bbox_hi"]], axis=1),
+                                  np.array([d.bbox for d in odets]))
+    np.testing.assert_array_equal(rows["intensity_sum"], np.array([d.intensity_sum for d in odets]))
+    hostf = host.ravel()
+    nx, ny, nz = spec.dims
+    lin_all = np.concatenate([(d.voxels[:, 0] * ny + d.voxels[:, 1]) * nz + d.voxels[:, 2] for d in odets])
+    means = np.array([hostf[(d.voxels[:, 0] * ny + d.voxels[:, 1]) * nz + d.voxels[:, 2]].mean() for d in odets])
+    np.testing.assert_array_equal(rows["mean_intensity"], means)  # numpy's own mean, bit for bit
+    np.testing.assert_array_equal(rows["centroid_um"], np.array([d.centroid_um for d in odets]))
+    np.testing.assert_array_equal(rows["volume_um3"], np.array([d.volume_um3 for d in odets]))
+    # C-order voxel lists, concatenated in id order
+    np.testing.assert_array_equal(pipe.voxels[: lin_all.size].cpu().numpy().astype(np.int64), lin_all)
+    np.testing.assert_array_equal(rows["voxel_offset"], np.concatenate([[0], np.cumsum(rows["count"])[:-1]]))
+    # canonical label volume: rank of the kept cell, -1 elsewhere
+    lab = np.full(nx * ny * nz, -1, np.int32)
+    lab[lin_all] = np.repeat(np.arange(len(odets), dtype=np.int32), [d.voxel_count for d in odets])
+    np.testing.assert_array_equal(pipe.labels.cpu().numpy().ravel(), lab)
+    return res, odets
+
+
+def check_vessel(pipe, spec, t, oracle):
+    raw = synth.generate(spec, t, synth.VESSEL)
+    host = host_frame(oracle, spec, t, synth.VESSEL)
+    np.testing.assert_array_equal(to_np(raw), host)
+    vres = pipe.vessel(raw)
+    mask, dm = pipe.finish_vessel(vres, raw)
+    st = oracle.mrf(host)
+    assert st["iteration"] == 0
+    state = vres.state.cpu().numpy()
+    assert state[MRF_DECISION] == 0.0 and state[MRF_DELTA] == st["delta"]
+    ss = oracle.sign_sum(host)
+    assert state[MRF_NNZ] == np.count_nonzero(ss)
+    om, odist, empty = oracle.segment_vessel(st["current"], SP)
+    assert not empty and 0.001 < om.mean() < 0.5
+    np.testing.assert_array_equal(mask.cpu().numpy(), om)
+    np.testing.assert_array_equal(dm.values.cpu().numpy(), odist)  # same envelope arithmetic: bit-exact
+
+
+@pytest.fixture(scope="module")
+def c2_pipe(cuda):
+    return FramePipeline(synth.C2.dims, "u8", ANISO)
+
+
+@pytest.mark.parametrize("t", [0, 5])
+def test_c2_time_point_vs_oracle(c2_pipe, oracle, t):
+    """The bench workload: full C2 time points, both channels (t = 0 is the
+    first frame of bench.py's input ring)."""
+    assert c2_pipe.k1_path_tc  # the tensor-core K1 the bench times
+    check_cell(c2_pipe, synth.C2, t, synth.CELL, oracle, id_start=1000 * t)
+    check_vessel(c2_pipe, synth.C2, t, oracle)
+
+
+def test_c3_time_point_vs_oracle(cuda, oracle):
+    """C3: 1024x1024x64 u16 (12-bit), three channels -- cell, vessel, and the
+    second cell channel (segmented through the cell path)."""
+    spec = synth.C3
+    pipe = FramePipeline(spec.dims, "u16", ANISO)
+    _, d1 = check_cell(pipe, spec, 2, synth.CELL, oracle, id_start=0)
+    check_vessel(pipe, spec, 2, oracle)
+    _, d2 = check_cell(pipe, spec, 2, synth.CELL2, oracle, id_start=len(d1))
+    assert d2[0].id == len(d1)
+
+
+def test_c4_crop_nz96_vs_oracle(cuda, oracle):
+    """nz = 96 kernels at C4's cell density (1024x1024x96 crop)."""
+    spec = synth.C4_CROP
+    pipe = FramePipeline(spec.dims, "u8", ANISO)
+    assert pipe.k1_path_tc and pipe.rows_path
+    check_cell(pipe, spec, 1, synth.CELL, oracle, id_start=7)
+    check_vessel(pipe, spec, 1, oracle)
+
+
+# ---------------------------------------------------------------------------
+# shape-specialised kernel variants vs the oracle
+# ---------------------------------------------------------------------------
+def _median(v: np.ndarray, rad: int):
+    t = torch.from_numpy(v if v.dtype != np.uint16 else v.view(np.int16)).cuda()
+    if v.dtype == np.uint16:
+        t = t.view(torch.uint16)
+    out = torch.empty_like(t)
+    hist = torch.zeros(65536, dtype=torch.int64, device=t.device)
+    call("ct_median", t.data_ptr(), _dev.ct_code(t), *v.shape, rad, out.data_ptr(), hist.data_ptr(),
+         _dev.stream_handle())
+    return to_np(out), hist.cpu().numpy()
+
+
+def _scene(rng, shape, vmax):
+    """Smooth blobs + noise (runs of equal values, like real q volumes) or noise."""
+    nx, ny, nz = shape
+    g = np.add.outer(np.add.outer(np.sin(np.arange(nx) / 3.0), np.cos(np.arange(ny) / 5.0)),
+                     np.sin(np.arange(nz) / 4.0))
+    return np.clip((g + 3) / 6 * vmax * 0.6 + rng.integers(0, max(2, vmax // 20), shape), 0, vmax)
+
+
+@pytest.mark.parametrize("nz", [32, 64, 96, 128, 40])
+@pytest.mark.parametrize("nxy", [(40, 36), (17, 19)])
+def test_median_u8_nz_variants_vs_oracle(cuda, oracle, nz, nxy):
+    """median3_bits<u8, 8, WC> for nz = 32/64/96/128 (WC = 1..4: the bench's
+    nz = 64 kernel is WC = 2) and the generic WC = 0 (nz = 40), full and
+    partial tiles, with the fused histogram."""
+    rng = np.random.default_rng(nz * 7 + nxy[0])
+    shape = (*nxy, nz)
+    for v in (rng.integers(0, 256, shape).astype(np.uint8), _scene(rng, shape, 255).astype(np.uint8),
+              (rng.random(shape) < 0.1).astype(np.uint8) * 200):
+        got, hist = _median(v, 1)
+        ref = oracle.median(v.astype(np.float64), 1)
+        np.testing.assert_array_equal(got.astype(np.float64), ref)
+        np.testing.assert_array_equal(hist, np.bincount(ref.astype(np.int64).ravel(), minlength=65536))
+
+
+@pytest.mark.parametrize("nz", [32, 64, 96, 128, 150])
+def test_median_u16_variants_vs_oracle(cuda, oracle, nz):
+    """median3_bits<u16, 16> (nz <= 128) and median3_int (nz > 128), 12-bit and
+    full 16-bit values."""
+    rng = np.random.default_rng(nz)
+    shape = (21, 18, nz)
+    for vmax in (4095, 65535):
+        v = _scene(rng, shape, vmax).astype(np.uint16)
+        got, hist = _median(v, 1)
+        ref = oracle.median(v.astype(np.float64), 1)
+        np.testing.assert_array_equal(got.astype(np.float64), ref)
+        np.testing.assert_array_equal(hist, np.bincount(ref.astype(np.int64).ravel(), minlength=65536))
+
+
+@pytest.mark.parametrize("rad", [4, 5])
+def test_median_large_radius_vs_oracle(cuda, oracle, rad):
+    """radius > 3 (median_radix, any window size) for every dtype."""
+    rng = np.random.default_rng(rad)
+    shape = (11, 9, 13)
+    for v in (rng.integers(0, 256, shape).astype(np.uint8), rng.integers(0, 4096, shape).astype(np.uint16),
+              rng.normal(3.0, 2.0, shape).clip(0)):
+        got, _ = _median(v, rad)
+        np.testing.assert_array_equal(got.astype(np.float64), oracle.median(v.astype(np.float64), rad))
+
+
+def test_denoise_api_large_median_radius(cuda, oracle):
+    """denoise_cell_channel with median_radius 4 (the reference accepts any r >= 1)."""
+    from paper_1407_2089_b200 import denoise as D
+    from paper_1407_2089_b200.imaging import VoxelGrid
+
+    v = np.random.default_rng(3).integers(0, 256, (30, 26, 20)).astype(np.uint8)
+    g = D.denoise_cell_channel(VoxelGrid(values=v, spacing=VoxelSpacing(1.0, 1.0, 1.0)),
+                               D.CellDenoiseParams(3.0, median_radius=4))
+    np.testing.assert_array_equal(g.values, oracle.denoise_cell(v, (1.0, 1.0, 1.0), 3.0, 4)["denoised"])
+
+
+@pytest.mark.parametrize("shape", [(20, 18, 150), (9, 11, 257)])
+def test_long_z_lines_vs_oracle(cuda, oracle, shape):
+    """nz > 128: CCL tile path, EDT pass z for long lines, the integer MRF's
+    global-memory statistics, closing -- all through the drop-in API."""
+    from paper_1407_2089_b200 import denoise as D
+    from paper_1407_2089_b200 import segment as S
+    from paper_1407_2089_b200.imaging import VoxelGrid
+
+    rng = np.random.default_rng(sum(shape))
+    for thr in (0.6, 0.93):
+        m = rng.random(shape) > thr
+        np.testing.assert_array_equal(S.morphological_closing(m, 1), oracle.closing(m, 1))
+        d_gpu = S.detections_from_mask(m, ANISO, frame=0, min_volume_um3=0.0)
+        d_ora = oracle.detections(m, SP, min_volume_um3=0.0)
+        assert [d.id for d in d_gpu] == [d.id for d in d_ora]
+        for a, b in zip(d_gpu, d_ora):
+            np.testing.assert_array_equal(a.voxels, b.voxels)
+            np.testing.assert_array_equal(a.centroid_um, b.centroid_um)
+        np.testing.assert_array_equal(S.distance_map(m, ANISO).values, oracle.edt(m, SP))
+    ramp = np.add.outer(np.add.outer(np.arange(shape[0]), np.arange(shape[1])), np.arange(shape[2])) % 50
+    for v in ((ramp + rng.integers(0, 9, shape)).astype(np.uint8), rng.integers(0, 256, shape).astype(np.uint8),
+              (ramp * 40 + rng.integers(0, 300, shape)).astype(np.uint16)):
+        st = D.mrf_denoise_state(VoxelGrid(values=v, spacing=ANISO))
+        o = oracle.mrf(v)
+        assert (st.sigma_hat, st.delta, st.iteration, st.converged) == \
+            (o["sigma_hat"], o["delta"], o["iteration"], o["converged"])
+        np.testing.assert_array_equal(np.asarray(st.current.values, dtype=np.float64), o["current"])
+
+
+@pytest.mark.parametrize("shape", [(24, 40, 64), (14, 18, 96), (9, 11, 20)])
+def test_ccl_rows_callee_fills_labels(cuda, oracle, shape):
+    """ct_ccl26_rows with flags = 0 (the call fills the -1 background itself)
+    equals the byte-mask CCL (only the pre-filled form was tested)."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx + ny + nz)
+    v = (rng.random(shape) * 255).astype(np.uint8)
+    dv = torch.from_numpy(v).cuda()
+    otsu = torch.tensor([170, 0, 0, 0], dtype=torch.int64, device="cuda")
+    work = torch.empty(workspace_bytes(1, nx, ny, nz, 1), dtype=torch.uint8, device="cuda")
+    W = 1 if nz <= 64 else 2
+    rows = torch.zeros(nx * ny * W, dtype=torch.int64, device="cuda")
+    mask = torch.empty(shape, dtype=torch.uint8, device="cuda")
+    s = _dev.stream_handle()
+    call("ct_threshold_close_rows", dv.data_ptr(), 1, nx, ny, nz, otsu.data_ptr(), 0, mask.data_ptr(),
+         rows.data_ptr(), work.data_ptr(), s)
+    outs = []
+    for flags in (None, 0):
+        labels = torch.full(shape, 12345, dtype=torch.int32, device="cuda")  # garbage: the call must fill
+        fg = torch.empty(nx * ny * nz, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
+        if flags is None:
+            call("ct_ccl26", mask.data_ptr(), nx, ny, nz, labels.data_ptr(), fg.data_ptr(), cnt.data_ptr(), s)
+        else:
+            call("ct_ccl26_rows", rows.data_ptr(), nx, ny, nz, labels.data_ptr(), fg.data_ptr(), cnt.data_ptr(),
+                 flags, s)
+        outs.append((labels.cpu().numpy(), cnt.cpu().numpy()))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    lab, n = oracle.label26(mask.cpu().numpy())
+    assert outs[1][1][1] == n

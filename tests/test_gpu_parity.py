@@ -275,7 +275,7 @@ def test_large_frame_properties(cuda):
     assert torch.equal(dm_api.values, vres.distance)
 
 
-def _q_exact_and_fast(raw, spacing, sigma_um, eps=0.0, cap=1 << 20):
+def _q_exact_and_fast(raw, spacing, sigma_um, eps=0.0, cap=1 << 20, path=0):
     from paper_1407_2089_b200 import _dev
     from paper_1407_2089_b200._lib import call
 
@@ -291,68 +291,105 @@ def _q_exact_and_fast(raw, spacing, sigma_um, eps=0.0, cap=1 << 20):
     call("ct_gaussian_residual", raw.data_ptr(), code, nx, ny, nz, w.data_ptr(), rx, ry, rz, work.data_ptr(), None,
          None, q1.data_ptr(), code, s)
     call("ct_gaussian_q", raw.data_ptr(), code, nx, ny, nz, w.data_ptr(), rx, ry, rz, work.data_ptr(),
-         q2.data_ptr(), fix.data_ptr(), cap, eps, s)
+         q2.data_ptr(), fix.data_ptr(), cap, eps, path, s)
     return q1, q2, fix[:2].cpu().numpy()
-
-
-def _k1_path(mode):
-    from paper_1407_2089_b200._lib import call
-    call("ct_set_k1_path", mode)
 
 
 @pytest.mark.parametrize("mode", [1, 0])  # FP64 FMA, auto (tensor cores where the shape fits)
 def test_certified_fast_k1_matches_exact(cuda, mode):
-    _k1_path(mode)
-    try:
-        for spec in (synth.C1, synth.SceneSpec(128, 96, 48, "u16", n_cells=20, seed=4),
-                     synth.SceneSpec(160, 96, 64, "u8", n_cells=30, seed=9)):
-            raw = synth.generate(spec, 2, synth.CELL)
-            q1, q2, fx = _q_exact_and_fast(raw, ANISO, 10.0)
-            assert fx[1] == 0
-            assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
-    finally:
-        _k1_path(0)
+    for spec in (synth.C1, synth.SceneSpec(128, 96, 48, "u16", n_cells=20, seed=4),
+                 synth.SceneSpec(160, 96, 64, "u8", n_cells=30, seed=9)):
+        raw = synth.generate(spec, 2, synth.CELL)
+        q1, q2, fx = _q_exact_and_fast(raw, ANISO, 10.0, path=mode)
+        assert fx[1] == 0
+        assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
 
 
 @pytest.mark.parametrize("sigma,shape,seed", [(10.0, (256, 192, 64), 1), (6.0, (200, 64, 32), 2),
                                               (12.0, (130, 130, 64), 3), (3.0, (64, 32, 32), 4),
                                               (10.0, (96, 64, 96), 5)])
 def test_tensor_core_k1_matches_exact(cuda, sigma, shape, seed):
-    # tensor-core K1 alone (mode 2) on noise and on a synthetic scene, incl.
+    # tensor-core K1 alone (path 2) on noise and on a synthetic scene, incl.
     # row counts that are not multiples of the 128-row tile
-    _k1_path(2)
-    try:
-        rng = np.random.default_rng(seed)
-        noise = torch.from_numpy(rng.integers(0, 256, size=shape, dtype=np.uint8)).cuda()
-        scene = synth.generate(synth.SceneSpec(*shape, "u8", n_cells=40, seed=seed), 1, synth.CELL)
-        for raw in (noise, scene):
-            q1, q2, fx = _q_exact_and_fast(raw, ANISO, sigma)
-            assert fx[1] == 0
-            assert fx[0] < 0.001 * raw.numel(), fx
-            assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
-    finally:
-        _k1_path(0)
+    rng = np.random.default_rng(seed)
+    noise = torch.from_numpy(rng.integers(0, 256, size=shape, dtype=np.uint8)).cuda()
+    scene = synth.generate(synth.SceneSpec(*shape, "u8", n_cells=40, seed=seed), 1, synth.CELL)
+    for raw in (noise, scene):
+        q1, q2, fx = _q_exact_and_fast(raw, ANISO, sigma, path=2)
+        assert fx[1] == 0
+        assert fx[0] < 0.001 * raw.numel(), fx
+        assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
 
 
-def test_certified_fixup_recomputes_exactly(cuda):
-    # eps 0.6 flags every voxel: the fix-up kernel alone must reproduce K1
+def test_tensor_core_k1_rejects_unfit_shape(cuda):
+    """path 2 (tensor cores only) on a shape the TC kernels do not cover is an
+    error, not a silent fallback; path 0 falls back to the FP64 FMA kernels."""
+    from paper_1407_2089_b200._lib import LibctError, lib
+
+    raw = torch.from_numpy(np.random.default_rng(1).integers(0, 256, (40, 36, 20), dtype=np.uint8)).cuda()
+    assert lib().ct_k1_path(1, 40, 36, 20, 12, 12, 10, 0) == 1
+    assert lib().ct_k1_path(1, 64, 32, 32, 12, 12, 10, 0) == 2
+    assert lib().ct_k1_path(1, 64, 32, 32, 12, 12, 10, 1) == 1
+    with pytest.raises(LibctError):
+        _q_exact_and_fast(raw, ANISO, 3.0, path=2)
+    q1, q2, fx = _q_exact_and_fast(raw, ANISO, 3.0, path=0)
+    assert torch.equal(q1, q2)
+    with pytest.raises(Exception):
+        _q_exact_and_fast(raw, ANISO, 3.0, path=3)
+
+
+@pytest.mark.parametrize("shape", [(40, 36, 20), (24, 20, 33), (12, 20, 128)])
+def test_certified_fixup_recomputes_exactly(cuda, shape):
+    # eps 0.6 flags every voxel: the fix-up kernels alone must reproduce K1
+    # (nz = 20: plain pass-x cone; nz = 33: odd z, the unstaged pass y/z; nz = 128: the widest staged cone)
     rng = np.random.default_rng(12)
-    v = torch.from_numpy(rng.integers(0, 256, size=(40, 36, 20), dtype=np.uint8)).cuda()
+    v = torch.from_numpy(rng.integers(0, 256, size=shape, dtype=np.uint8)).cuda()
     q1, q2, fx = _q_exact_and_fast(v, ANISO, 3.0, eps=0.6)
     assert fx[0] == v.numel() and fx[1] == 0
     assert torch.equal(q1, q2)
+
+
+def test_certified_fixup_tensor_cores(cuda):
     # tensor-core path: everything with residual > -0.1 is flagged and fixed
-    _k1_path(2)
-    try:
-        v2 = torch.from_numpy(rng.integers(0, 256, size=(40, 36, 32), dtype=np.uint8)).cuda()
-        q1, q2, fx = _q_exact_and_fast(v2, ANISO, 3.0, eps=0.6)
-        assert fx[0] > v2.numel() // 3 and fx[1] == 0
-        assert torch.equal(q1, q2)
-    finally:
-        _k1_path(0)
-    # overflow is reported when the list is too small
-    _, _, fx = _q_exact_and_fast(v, ANISO, 3.0, eps=0.6, cap=10)
-    assert fx[1] == 1
+    rng = np.random.default_rng(13)
+    v2 = torch.from_numpy(rng.integers(0, 256, size=(40, 36, 32), dtype=np.uint8)).cuda()
+    q1, q2, fx = _q_exact_and_fast(v2, ANISO, 3.0, eps=0.6, path=2)
+    assert fx[0] > v2.numel() // 3 and fx[1] == 0
+    assert torch.equal(q1, q2)
+
+
+@pytest.mark.parametrize("path,dtype", [(2, np.uint8), (1, np.uint8), (1, np.uint16)])
+def test_fix_list_overflow_recomputed_in_stream(cuda, path, dtype):
+    """Fix list too small (10 entries for thousands of flagged voxels): the
+    overflow flag is set and q is still exact -- the in-stream cooperative
+    recompute (k1_overflow_exact) replaced every voxel in scipy's order."""
+    rng = np.random.default_rng(14)
+    shape = (40, 36, 32)
+    v = rng.integers(0, 256 if dtype == np.uint8 else 4096, size=shape).astype(dtype)
+    t = torch.from_numpy(v if dtype == np.uint8 else v.view(np.int16)).cuda()
+    if dtype == np.uint16:
+        t = t.view(torch.uint16)
+    q1, q2, fx = _q_exact_and_fast(t, ANISO, 3.0, eps=0.6, cap=10, path=path)
+    assert fx[1] == 1 and fx[0] > 10
+    assert torch.equal(q1, q2)
+
+
+def test_fix_list_overflow_fused_pipeline(cuda, oracle):
+    """FramePipeline with a tiny fix list on a C1 frame: the fused result
+    still equals the oracle (no exception, no host-side rerun)."""
+    spec = synth.C1
+    pipe = FramePipeline(spec.dims, spec.dtype, ANISO)
+    pipe.fix_cap = 4
+    pipe.k1_eps = 0.6  # flag every voxel with residual > -0.1: the list must overflow
+    raw = synth.generate(spec, 1, synth.CELL)
+    res = pipe.cell(raw, frame=1)
+    cnt, rows = pipe.finish_cell(res)
+    assert int(pipe.fix[1]) == 1
+    host = raw.cpu().numpy()
+    o = oracle.denoise_cell(host, ANISO.as_array(), 10.0)
+    np.testing.assert_array_equal(pipe.q.cpu().numpy(), np.rint(o["residual"]).astype(np.uint8))
+    odets = oracle.segment_cell(o["denoised"], ANISO.as_array(), frame=1)
+    assert [int(r["count"]) for r in rows] == [d.voxel_count for d in odets]
 
 
 def _ref_encode_runs(voxels):
