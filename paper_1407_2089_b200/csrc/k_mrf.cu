@@ -638,6 +638,7 @@ __global__ void __launch_bounds__(256) mrf_stream_int(const T *__restrict__ v, i
     __syncthreads();
     int prev[MAXP];
     for (int q = 0; q < np_; ++q) prev[q] = ring[2 * PL + (pj[q] + 1) * nz + pk[q]];
+    __syncthreads();  // plane i0-1 read by all before iteration i0 stores into its slot
     unsigned long long nnz = 0;
     long long lsum = 0;
     for (i64 i = i0; i < i1; ++i) {
@@ -748,6 +749,7 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
     int prev[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) prev[p] = ring[2][(jt + p * RP + 1) * NZ + k];
+    __syncthreads();  // plane i0-1 read by all before iteration i0 stores into its slot
     unsigned nnz = 0;
     long long lsum = 0;
     int cs = 0, ns = 1, fs = 2;
@@ -831,7 +833,12 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
     constexpr int MJ4 = 256 / W;            // rows per CTA
     constexpr int PW = (MJ4 + 2) * W;       // staged words per plane
     constexpr int LW = (PW + 255) / 256;
-    __shared__ uint32_t ring[3][PW];
+    // plane ring: i-1, i, i+1 and the slot plane i+2 is stored into.  When
+    // rows do not tile the warps (NZ = 96) the Laplacian path reads plane i-1
+    // from the ring (nb0 below), so the write slot must be a fourth one (the
+    // store is not behind a barrier); otherwise it is plane i-1's slot.
+    constexpr int NSLOT = (32 % W == 0) ? 3 : 4;
+    __shared__ uint32_t ring[NSLOT][PW];
     __shared__ uint32_t hsm[8 * 256];
     uint32_t *wh = hsm + (threadIdx.x >> 5) * 256;
     for (int b = threadIdx.x; b < 8 * 256; b += 256) hsm[b] = 0;
@@ -875,7 +882,7 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
     unsigned nnz = 0;
     long long lsum = 0;
     const bool jin = own && j < ny, jint = j > 0 && j < ny - 1;
-    int cs = 0, ns = 1, fs = 2;
+    int cs = 0, ns = 1, fs = 2, ws = NSLOT == 4 ? 3 : 2;  // fs: plane i-1, ws: write slot
     // MODE 1: the x-direction comparisons of plane i against i+1 are reused
     // as plane i+1's comparisons against its i-1 neighbour (gxm, lxm)
     uint32_t gxm = 0, lxm = 0;
@@ -884,6 +891,9 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
         gxm = gt_hi(xm, c0);
         lxm = gt_hi(c0, xm);
     }
+    // every thread has read plane i0-1 (slot 2) before the first iteration's
+    // store may replace it (NSLOT = 3: the write slot of iteration i0 is slot 2)
+    __syncthreads();
     unsigned esq = 0;  // MODE 1: sum of squared forward differences (edge term of the sigma bound)
     for (int i = i0; i < i1; ++i) {
         load_plane(i + 3, regs);  // planes i+2 (regs2) and i+3 (regs) in flight while plane i is processed
@@ -961,11 +971,13 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
         }
         }
         xm = c;
-        store_plane(fs, regs2);
+        store_plane(ws, regs2);
 #pragma unroll
         for (int q = 0; q < LW; ++q) regs2[q] = regs[q];
         __syncthreads();
-        const int t = cs; cs = ns; ns = fs; fs = t;
+        const int t = fs;
+        fs = cs; cs = ns; ns = ws;
+        ws = NSLOT == 4 ? t : fs;
     }
     unsigned long long nnz64 = nnz, esq64 = esq;
     for (int q = 16; q; q >>= 1) {

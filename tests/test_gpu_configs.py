@@ -273,5 +273,44 @@ def test_ccl_rows_callee_fills_labels(cuda, oracle, shape):
         outs.append((labels.cpu().numpy(), cnt.cpu().numpy()))
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     np.testing.assert_array_equal(outs[0][1], outs[1][1])
-    lab, n = oracle.label26(mask.cpu().numpy())
-    assert outs[1][1][1] == n
+    m = mask.cpu().numpy()
+    lab, n = oracle.label26(m)
+    got = outs[1][0].ravel()
+    assert outs[1][1][0] == m.sum()                                   # foreground voxels
+    assert int((got == np.arange(got.size)).sum()) == n               # one root per component
+    # same partition as the oracle's labels (label = min voxel index of the component)
+    olab = lab.ravel()
+    fgm = olab > 0
+    order = np.flatnonzero(fgm)
+    mins = np.full(n + 1, got.size, dtype=np.int64)
+    np.minimum.at(mins, olab[order], order)
+    np.testing.assert_array_equal(got[fgm], mins[olab[fgm]])
+    assert np.all(got[~fgm] == -1)
+
+
+@pytest.mark.parametrize("nz", [32, 64, 96, 128, 70])
+def test_mrf_statistics_repeatable_vs_oracle(cuda, oracle, nz):
+    """ct_mrf (exact sigma_hat) and ct_mrf_decide (certified decision), 6
+    times each on the same volume: every run equals the oracle (delta, nnz,
+    sigma_hat / decision).  Guards the plane-ring kernels against the
+    ordering hazard fixed in round 2 (a fast warp's first ring store could
+    replace plane i0-1 before a slow warp had read it)."""
+    shape = (256, 200, nz)
+    spec = synth.SceneSpec(*shape, "u8", n_cells=10, n_tubes=12, seed=3)
+    v = synth.generate(spec, 0, synth.VESSEL)
+    host = to_np(v)
+    o = oracle.mrf(host)
+    nnz = np.count_nonzero(oracle.sign_sum(host))
+    nx, ny, _ = shape
+    s = _dev.stream_handle()
+    for fn in ("ct_mrf", "ct_mrf_decide"):
+        for _ in range(6):
+            work = torch.empty(workspace_bytes(4, nx, ny, nz, 1), dtype=torch.uint8, device="cuda")
+            state = torch.zeros(9, dtype=torch.float64, device="cuda")
+            hist = torch.zeros(65536, dtype=torch.int64, device="cuda")
+            call(fn, v.data_ptr(), 1, nx, ny, nz, work.data_ptr(), state.data_ptr(), hist.data_ptr(), s)
+            st = state.cpu().numpy()
+            assert st[MRF_DELTA] == o["delta"] and st[MRF_NNZ] == nnz, (fn, st)
+            if fn == "ct_mrf" or st[2] != 2.0:
+                assert st[1] == o["sigma_hat"], (fn, st)
+            assert st[MRF_DECISION] == 0.0
