@@ -21,10 +21,15 @@
 //       line (nz x nz, constant), K-major; both in SMEM.  The taps beyond the
 //       line ends (mode "nearest": the edge values) are exact integer edge
 //       terms added in the epilogue on the CUDA cores.
-// Operand tiles are staged with cp.async several tiles ahead, and each
+// Pass x is warp-specialised: a TMA producer warp stages the B boxes
+// (cp.async.bulk.tensor, mbarrier complete_tx) into a 6-deep ring, one warp
+// issues the MMAs, 16 epilogue warps drain TMEM (tc_pass_xy_ws).  Passes y
+// and z stage their operands with cp.async several tiles ahead, and each
 // tile's epilogue (from registers) overlaps the next tile's MMAs.
 //   Limb pairs (a, b) with a + b >= 2 (data limb a, weight limb b) are kept;
 //   pairs of equal a + b share an accumulator (5 accumulators).
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -120,7 +125,7 @@ __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, u
 }
 
 // ---------------------------------------------------------------------------
-// Passes x and y.  NPIN = 1 (raw u8 input; pairs (0,b), accumulator b, shift
+// Passes x and y, synchronous form (launched for pass y).  NPIN = 1 (raw u8 input; pairs (0,b), accumulator b, shift
 // 8b; output S >> 11) or 4 (byte planes of P1; pairs a+b >= 2, accumulator
 // a+b-2, shift 8(a+b-2); output S >> 19).  Volume viewed as [outer][L][inner].
 // ---------------------------------------------------------------------------
@@ -308,6 +313,238 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     __syncthreads();
     tc::fence_after();
     if (wp == 0) tc::tmem_dealloc(base, 512);
+}
+
+// ---------------------------------------------------------------------------
+// Passes x and y, warp-specialised (launched for pass x):
+//   warp 0      TMA producer: one cp.async.bulk.tensor box per tile (256
+//               input rows x TN columns of every byte plane) into a ring of
+//               SSTG shared-memory stages (full / empty mbarriers);
+//   warp 1      TMEM owner and MMA issuer: the tap band A lives in TMEM
+//               columns [0, 256); ASTG accumulator sets follow, so MMA(k+1)
+//               runs while the epilogue drains set k (afull / aempty);
+//               rows of a box that fall outside [0, L) arrive zero-filled and
+//               are replaced by the edge row (mode "nearest") before the MMAs;
+//   warps 2..9  epilogue: TMEM -> registers, combine the limb accumulators in
+//               exact 64-bit integers, split into the next pass's byte planes,
+//               8-byte stores (warp w reads TMEM lane quarter w % 4, half
+//               (w - 2) / 4 of the tile's columns).
+// Same integer arithmetic as tc_pass_xy (bit-identical planes).
+// ---------------------------------------------------------------------------
+constexpr int WS_EPI = 16;                 // epilogue warps (4 per TMEM lane quarter)
+constexpr int WS_NT = 32 * (2 + WS_EPI);   // 576 threads
+
+__device__ __forceinline__ void epi_bar() {  // named barrier 1: the epilogue warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * WS_EPI) : "memory");
+}
+
+template <int NPIN, int TN, int SSTG, int ASTG>
+__global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant__ CUtensorMap tmap, int L, int inner,
+                                                          int outer, const TcParams *__restrict__ prm, int axis, int r,
+                                                          uint8_t *__restrict__ out, long long plane_out) {
+    constexpr int NACC = NPIN == 1 ? 4 : 5;
+    constexpr int CH = TN / 16;                     // 16-byte chunks per row (one TMA box each)
+    constexpr int PB = KXY * 16;                    // bytes per plane per chunk: [KXY][16]
+    constexpr int CB = NPIN * PB;                   // bytes per chunk (all planes)
+    constexpr int SB = CH * CB;                     // bytes per stage, [CH][NPIN][KXY][16]
+    constexpr uint32_t LBO = 128, SBO = CB;         // MN-major: 8 K-rows = 128 B; next 16 columns = CB
+    constexpr int CW = TN / 4;                      // columns per epilogue thread (4 column groups)
+    constexpr int OROW = TN + 16;                   // padded staged output row (bytes)
+    constexpr int OBUF = 4 * TM * OROW;             // staged output tile: [4 planes][128 rows]
+    constexpr int CPR = TN / 16;                    // 16-byte chunks per output row
+    static_assert(256 + ASTG * NACC * TN <= 512, "TMEM: band + accumulator sets");
+    extern __shared__ __align__(1024) uint8_t sm[];  // [SSTG][SB] operand stages, [2][OBUF] output tiles
+    uint8_t *sout = sm + SSTG * SB;
+    __shared__ uint64_t full[SSTG], empty[SSTG], afull[ASTG], aempty[ASTG];
+    __shared__ uint32_t tbase;
+    __shared__ long long Qs[PMAX];
+    const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
+    if (wp == 1) tc::tmem_alloc(&tbase, 512);
+    for (int j = t; j < PMAX; j += WS_NT) Qs[j] = prm->Q[axis][j];
+    if (t == 0) {
+        for (int i = 0; i < SSTG; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < ASTG; ++i) {
+            tc::mbar_init(&afull[i], 1);
+            tc::mbar_init(&aempty[i], WS_EPI);
+        }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmap);
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t base = tbase;
+    // epilogue warp e = wp - 2: TMEM lane quarter q = wp % 4 (hardware rule),
+    // column group cg = e / 4; it writes band limb cg of its rows into TMEM
+    const int e_w = wp - 2, q = wp & 3, cg = e_w >> 2, m = 32 * q + lane;
+    const uint32_t la = base + ((uint32_t)(32 * q) << 16);
+    if (wp >= 2) {
+        const int b = cg;
+        for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int kk = 4 * (c0 + i) + e, j = kk - r - m;
+                    const uint32_t byte = (j >= -r && j <= r) ? limb(Qs[j < 0 ? -j : j], b) : 0u;
+                    word |= byte << (8 * e);
+                }
+                v[i] = word;
+            }
+            tc::tmem_st8(la + b * 64 + c0, v);
+        }
+        tc::tmem_st_wait();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+
+    const int nti = (L + TM - 1) / TM, ncb = inner / TN;
+    const long long ntiles = (long long)outer * nti * ncb;
+    const long long t0 = blockIdx.x, gs = gridDim.x;
+    const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
+    auto coords = [&](long long k, int &o, int &ti, int &cb) {
+        const unsigned tl = (unsigned)(t0 + k * gs), r2 = tl / (unsigned)ncb;
+        cb = (int)(tl - r2 * (unsigned)ncb);
+        o = (int)(r2 / (unsigned)nti);
+        ti = (int)(r2 - (unsigned)o * (unsigned)nti);
+    };
+    if (wp == 0) {
+        // ---- TMA producer ----
+        for (long long k = 0; k < nmine; ++k) {
+            const int s = (int)(k % SSTG);
+            tc::mbar_wait(&empty[s], (uint32_t)((k / SSTG) & 1) ^ 1u);
+            if (lane == 0) {
+                int o, ti, cb;
+                coords(k, o, ti, cb);
+                tc::mbar_expect_tx(&full[s], SB);
+                uint8_t *dst = sm + s * SB;
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    if constexpr (NPIN == 1)
+                        tc::tma_load_2d(dst + c * CB, &tmap, cb * TN + 16 * c, ti * TM - r, &full[s]);
+                    else
+                        tc::tma_load_4d(dst + c * CB, &tmap, cb * TN + 16 * c, ti * TM - r, o, 0, &full[s]);
+                }
+            }
+            __syncwarp();
+        }
+    } else if (wp == 1) {
+        // ---- MMA issuer ----
+        const uint32_t idesc = tc::idesc_i8(TM, TN, false, false, false, true);
+        for (long long k = 0; k < nmine; ++k) {
+            const int s = (int)(k % SSTG), a = (int)(k % ASTG);
+            tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
+            int o, ti, cb;
+            coords(k, o, ti, cb);
+            const int g0 = ti * TM - r;  // global row of box row 0
+            if (g0 < 0 || g0 + KXY > L) {
+                // box rows outside [0, L) came back zero-filled: clamp to the edge rows
+                uint8_t *st = sm + s * SB;
+                const int lo = -g0, hi = L - 1 - g0;
+                for (int e = lane; e < CH * NPIN * KXY; e += 32) {
+                    const int kk = e % KXY, pc = e / KXY;
+                    const int src = kk < lo ? lo : (kk > hi ? hi : -1);
+                    if (src >= 0) *(uint4 *)(st + (pc * KXY + kk) * 16) = *(const uint4 *)(st + (pc * KXY + src) * 16);
+                }
+                tc::fence_async_smem();
+                __syncwarp();
+            }
+            tc::mbar_wait(&aempty[a], (uint32_t)((k / ASTG) & 1) ^ 1u);
+            tc::fence_after();
+            if (tc::elect_one()) {
+                const uint64_t d0 = tc::smem_desc(tc::smem_u32(sm + s * SB), LBO, SBO);
+                bool first[NACC];
+#pragma unroll
+                for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
+#pragma unroll
+                for (int da = 0; da < NPIN; ++da)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int acc = NPIN == 1 ? b : da + b - 2;
+                        if (acc < 0) continue;
+#pragma unroll
+                        for (int ks = 0; ks < KXY / 32; ++ks)
+                            tc::mma_i8_ts(base + 256 + (a * NACC + acc) * TN, base + b * 64 + ks * 8,
+                                          d0 + (uint64_t)((da * PB + ks * 4 * LBO) >> 4), idesc,
+                                          first[acc] && ks == 0 ? 0u : 1u);
+                        first[acc] = false;
+                    }
+                tc::mma_commit(&empty[s]);  // stage s free once these MMAs have read it
+                tc::mma_commit(&afull[a]);  // accumulator set a complete
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---- epilogue: row m, columns [h, h + CW) of every tile ----
+        const int h = CW * cg;
+        const int et = t - 64;  // 0 .. 32 * WS_EPI - 1
+        // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
+        const int shift_out = NPIN == 1 ? prm->fw[axis] - FD : prm->fw[axis] - 16;
+        // coalesced store of a staged output tile: 4 planes x 128 rows x TN bytes
+        auto flush = [&](long long k, const uint8_t *ob) {
+            int o, ti, cb;
+            coords(k, o, ti, cb);
+#pragma unroll
+            for (int q2 = 0; q2 < (4 * TM * CPR + 32 * WS_EPI - 1) / (32 * WS_EPI); ++q2) {
+                const int e = et + 32 * WS_EPI * q2;
+                if (e >= 4 * TM * CPR) break;
+                const int pa = e / (CPR * TM), mm = (e / CPR) % TM, hh = e % CPR;
+                const int i = ti * TM + mm;
+                if (i < L)
+                    *(uint4 *)(out + pa * plane_out + ((long long)o * L + i) * inner + (long long)cb * TN + 16 * hh) =
+                        *(const uint4 *)(ob + (pa * TM + mm) * OROW + 16 * hh);
+            }
+        };
+        for (long long k = 0; k < nmine; ++k) {
+            const int a = (int)(k % ASTG);
+            tc::mbar_wait(&afull[a], (uint32_t)((k / ASTG) & 1));
+            tc::fence_after();
+            uint32_t v[NACC][CW];
+#pragma unroll
+            for (int acc = 0; acc < NACC; ++acc) {
+                if constexpr (CW % 8 == 0) {
+#pragma unroll
+                    for (int g8 = 0; g8 < CW; g8 += 8)
+                        tc::tmem_ld8(la + 256 + (a * NACC + acc) * TN + h + g8,
+                                     *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
+                } else {
+                    tc::tmem_ld4(la + 256 + (a * NACC + acc) * TN + h, *reinterpret_cast<uint32_t(*)[4]>(&v[acc][0]));
+                }
+            }
+            tc::tmem_ld_wait();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&aempty[a]);  // MMA(k + ASTG) may overwrite set a
+            uint8_t *ob = sout + (int)(k & 1) * OBUF;
+#pragma unroll
+            for (int g4 = 0; g4 < CW; g4 += 4) {
+                uint32_t ov[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    long long S = 0;
+#pragma unroll
+                    for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][g4 + c] << (8 * acc);
+                    ov[c] = (uint32_t)(S >> shift_out);
+                }
+                uint32_t pl[4];
+                planes4(ov[0], ov[1], ov[2], ov[3], pl);
+#pragma unroll
+                for (int pa = 0; pa < 4; ++pa) *(uint32_t *)(ob + (pa * TM + m) * OROW + h + g4) = pl[pa];
+            }
+            epi_bar();  // tile k staged (and tile k-1's flush, issued before, finished by every thread)
+            flush(k, ob);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (wp == 1) tc::tmem_dealloc(base, 512);
 }
 
 // ---------------------------------------------------------------------------
@@ -562,6 +799,20 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
 
 }  // namespace
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda);
+// the pointer is looked up once per process (idempotent)
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }();
+    return fn;
+}
+
 // TC path of ct_gaussian_q (u8).  Returns CT_ERR_UNSUPPORTED when the shape
 // does not fit (the caller then uses the SIMT FMA path).  work: >= 8 N bytes
 // (byte planes of P1 and P2) + sizeof(TcParams).
@@ -583,16 +834,37 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
     tc_prep<<<1, 96, 0, s>>>(w, rx, ry, rz, 255.0, eps_override, prm);
     if (int st = ct::check_launch("tc_prep")) return st;
-    // pass x: [1][nx][ny*nz]
+    // pass x: warp-specialised, operands staged by TMA
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tma_encoder();
+    if (!encode) {
+        ct::set_error("cuTensorMapEncodeTiled unavailable (driver entry point)");
+        return CT_ERR_CUDA;
+    }
+    // pass x: [1][nx][ny*nz]; box = 16 bytes x 256 x-rows, TX / 16 boxes per tile
     {
-        const size_t sm = 6 * 1 * KXY * TNX + 2 * 4 * TM * (TNX + 16) + 1024;
-        cudaFuncSetAttribute(tc_pass_xy<1, 6, TNX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TNX);
-        tc_pass_xy<1, 6, TNX><<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(
-            raw, 0, (int)nx, (int)(ny * nz), 1, prm, 0, rx, p1, N);
+        constexpr int TX = 64, SS = 6, AS = 1;
+        CUtensorMap tm;
+        const cuuint64_t dims[2] = {(cuuint64_t)(ny * nz), (cuuint64_t)nx};
+        const cuuint64_t strides[1] = {(cuuint64_t)(ny * nz)};
+        const cuuint32_t box[2] = {16, KXY}, es[2] = {1, 1};
+        if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)raw, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            ct::set_error("tensor map (pass x) rejected");
+            return CT_ERR_UNSUPPORTED;
+        }
+        auto kx = tc_pass_xy_ws<1, TX, SS, AS>;
+        const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * 4 * TM * (TX + 16) + 1024;
+        cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TX);
+        kx<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tm, (int)nx, (int)(ny * nz), 1, prm, 0, rx,
+                                                                        p1, N);
         if (int st = ct::check_launch("tc_pass_x")) return st;
     }
-    // pass y: [nx][ny][nz]
+    // pass y: [nx][ny][nz] x 4 planes, the synchronous form (cp.async staging):
+    // measured faster than the warp-specialised TMA form here -- 263 us vs 296
+    // (TN = 32, one accumulator set) / 373 (TN = 16, three sets) on C2: the
+    // MMAs read the tap band A from TMEM, and narrower tiles only add MMAs
     {
         const size_t sm = 5 * 4 * KXY * TNY + 2 * 4 * TM * (TNY + 16) + 1024;
         cudaFuncSetAttribute(tc_pass_xy<4, 5, TNY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
