@@ -230,8 +230,32 @@ __device__ __forceinline__ uint32_t nib_transpose8(uint32_t y, unsigned sub) {
     return y;
 }
 
-// WC > 0: nz == 32 * WC at compile time (u8: planes built by in-register
-// transposes from 32-bit loads instead of per-bit ballots)
+// 16x16 transpose of 2-bit elements across the 16 lanes of a half warp (lane
+// s holds row s; afterwards lane s holds element s of every lane's row, row t
+// at element t)
+__device__ __forceinline__ uint32_t pair_transpose16(uint32_t y, unsigned sub) {
+#pragma unroll
+    for (int s = 8; s >= 1; s >>= 1) {
+        const uint32_t m = s == 8 ? 0x0000ffffu : (s == 4 ? 0x00ff00ffu : (s == 2 ? 0x0f0f0f0fu : 0x33333333u));
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, y, s);
+        y = (sub & s) ? ((y & ~m) | ((o & ~m) >> (2 * s))) : ((y & m) | ((o & m) << (2 * s)));
+    }
+    return y;
+}
+
+// two u16 values (low half, high half) -> bit 2b + e = value e's bit b
+__device__ __forceinline__ uint32_t zip16(uint32_t x) {
+    x = (x & 0xff0000ffu) | ((x & 0x00ff0000u) >> 8) | ((x & 0x0000ff00u) << 8);
+    x = (x & 0xf00ff00fu) | ((x & 0x0f000f00u) >> 4) | ((x & 0x00f000f0u) << 4);
+    x = (x & 0xc3c3c3c3u) | ((x & 0x30303030u) >> 2) | ((x & 0x0c0c0c0cu) << 2);
+    x = (x & 0x99999999u) | ((x & 0x44444444u) >> 1) | ((x & 0x22222222u) << 1);
+    return x;
+}
+
+// WC > 0: nz == 32 * WC at compile time (planes built by in-register
+// transposes from 32-bit loads instead of per-bit ballots: u8 4 voxels per
+// lane, nibble transposes over 8 lanes; u16 2 voxels per lane, pair
+// transposes over 16 lanes)
 template <typename T, int NB, int WC = 0>
 __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T *__restrict__ out, i64 nx, i64 ny,
                                                     int nz_, uint64_t *__restrict__ ghist) {
@@ -267,7 +291,46 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
         const i64 i0 = (tile / tj) * BTI, j0 = (tile % tj) * BTJ;
         __syncthreads();
         if (threadIdx.x == 0) *s_any = 0;
-        if constexpr (NB == 8 && WC > 0) {
+        if constexpr (NB == 16 && WC > 0) {
+            // clamped row offsets of the tile's input rows, once per tile
+            __shared__ long long roff16[(BTI + 2) * (BTJ + 2)];
+            for (int r = threadIdx.x; r < RI * RJ; r += 256) {
+                const int ri = r / RJ, rj = r - ri * RJ;
+                const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
+                roff16[r] = (i * ny + j) * nz;
+            }
+            __syncthreads();
+            // phase A (u16): a half warp per (row, word) unit, lane s loads
+            // voxels 2s, 2s+1 of the word; zip16 + pair_transpose16 leave lane
+            // s with plane s of the word
+            const unsigned sub = lane & 15;
+            const int half = (int)(lane >> 4);
+            unsigned anyw = 0;
+            constexpr int UB = 4;  // units in flight per half warp
+            for (int u0 = 2 * wid + half; u0 < NW; u0 += 16 * UB) {
+                uint32_t x[UB];
+#pragma unroll
+                for (int qq = 0; qq < UB; ++qq) {
+                    const int u = u0 + 16 * qq;
+                    x[qq] = 0u;
+                    if (u < NW) {
+                        const int r = u / W, w = u - r * W;
+                        x[qq] = __ldg((const uint32_t *)(in + roff16[r] + 32 * w) + sub);
+                    }
+                }
+#pragma unroll
+                for (int qq = 0; qq < UB; ++qq) {
+                    const int u = u0 + 16 * qq;
+                    const uint32_t y = pair_transpose16(zip16(x[qq]), sub);
+                    if (u < NW) {
+                        pc[sub * NW + u] = y;
+                        anyw |= y ? (1u << sub) : 0u;
+                    }
+                }
+            }
+            anyw = __reduce_or_sync(0xffffffffu, anyw);
+            if (lane == 0 && anyw) atomicOr(s_any, anyw);
+        } else if constexpr (NB == 8 && WC > 0) {
             // clamped row offsets of the tile's input rows, once per tile
             // (the per-load clamp / divide was a third of phase A)
             __shared__ long long roff[(BTI + 2) * (BTJ + 2)];
@@ -442,16 +505,48 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                     hi8[g] = planes_to_bytes(med[8 % NB], med[9 % NB], med[10 % NB], med[11 % NB], med[12 % NB],
                                              med[13 % NB], med[14 % NB], med[15 % NB], g);
                 }
+                // 16-bit outputs: pairs packed into words, 16-byte stores when the
+                // 32 voxels are whole and aligned; the histogram counts runs of
+                // equal values along z (medians of residuals are mostly 0 and
+                // smooth, and 32 lanes adding to one SMEM bin serialise)
+                uint32_t pw[16];
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    if (q >= nv) break;
-                    const int v = (int)(((lo8[q >> 3] >> (8 * (q & 7))) & 0xFF) |
-                                        (((hi8[q >> 3] >> (8 * (q & 7))) & 0xFF) << 8));
-                    out[p0 + q] = (T)v;
-                    if (ghist) {
-                        if (v < 4096) atomicAdd(&sh16[v], 1u);
-                        else atomicAdd((unsigned long long *)&ghist[v], 1ull);
+                for (int q = 0; q < 32; q += 2) {
+                    const uint32_t a = (uint32_t)(((lo8[q >> 3] >> (8 * (q & 7))) & 0xFF) |
+                                                  (((hi8[q >> 3] >> (8 * (q & 7))) & 0xFF) << 8));
+                    const uint32_t b = (uint32_t)(((lo8[q >> 3] >> (8 * ((q + 1) & 7))) & 0xFF) |
+                                                  (((hi8[q >> 3] >> (8 * ((q + 1) & 7))) & 0xFF) << 8));
+                    pw[q >> 1] = a | (b << 16);
+                }
+                if (nv == 32 && (p0 & 7) == 0) {
+                    uint4 *dst = reinterpret_cast<uint4 *>(out + p0);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q)
+                        if (q < nv) out[p0 + q] = (T)((pw[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+                }
+                if (ghist) {
+                    int cur = -1;
+                    unsigned run = 0;
+                    auto add = [&](int v, unsigned c) {
+                        if (v < 4096) atomicAdd(&sh16[v], c);
+                        else atomicAdd((unsigned long long *)&ghist[v], (unsigned long long)c);
+                    };
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        if (q >= nv) break;
+                        const int v = (int)((pw[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+                        if (v == cur) {
+                            ++run;
+                        } else {
+                            if (run) add(cur, run);
+                            cur = v;
+                            run = 1;
+                        }
                     }
+                    if (run) add(cur, run);
                 }
             }
         }
@@ -638,9 +733,13 @@ extern "C" int ct_median(const void *in, int dtype, int64_t nx, int64_t ny, int6
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             k<<<grid, 256, sm, s>>>((const uint8_t *)in, (uint8_t *)out, nx, ny, (int)nz, hist);
         } else {
-            cudaFuncSetAttribute(median3_bits<uint16_t, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            median3_bits<uint16_t, 16><<<grid, 256, sm, s>>>((const uint16_t *)in, (uint16_t *)out, nx, ny, (int)nz,
-                                                             hist);
+            const bool al4 = ((uintptr_t)in & 3) == 0;
+            auto k = (al4 && nz == 64) ? median3_bits<uint16_t, 16, 2>
+                     : (al4 && nz == 32) ? median3_bits<uint16_t, 16, 1>
+                     : (al4 && nz == 96) ? median3_bits<uint16_t, 16, 3>
+                     : (al4 && nz == 128) ? median3_bits<uint16_t, 16, 4> : median3_bits<uint16_t, 16, 0>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k<<<grid, 256, sm, s>>>((const uint16_t *)in, (uint16_t *)out, nx, ny, (int)nz, hist);
         }
         return ct::check_launch("median3_bits");
     }

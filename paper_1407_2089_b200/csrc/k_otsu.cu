@@ -7,11 +7,11 @@
 // with numpy int64 arrays (two's-complement wrap for huge N), keeps the
 // candidates score >= best*(1-1e-9) (or every t when best <= 0), and decides
 // among them exactly with Python integers (a^2/b compared cross-multiplied,
-// strict improvement -> lowest t).  Here: one CTA of 1024 threads; each
-// thread owns a contiguous chunk of bins (prefix sums via a block scan of
-// chunk totals), pass A finds best, pass B applies the candidate filter and
-// the exact comparison with 128-bit a and 384-bit products, and a block
-// reduction keeps the lowest winning t.
+// strict improvement -> lowest t).  Here: one CTA (256 or 1024 threads)
+// visits the bins in rounds of consecutive bins (coalesced; prefix sums by a
+// block scan per round plus a carry), pass A finds best, pass B applies the
+// candidate filter and the exact comparison with 128-bit a and 384-bit
+// products, and a block reduction keeps the lowest winning t.
 #include "ct_common.cuh"
 
 namespace {
@@ -81,11 +81,78 @@ __device__ void merge(Cand &x, const Cand &y) {
     else if (!better(x, y) && y.t < x.t) x = y;
 }
 
+// candidate t (score within the reference's 1e-9 cut): exact a^2 / b against
+// the best so far -- a = s0*w1 - s1*w0 (Python ints), b = w0*w1; ascending t,
+// strict improvement only
+__device__ __noinline__ void consider(Cand &mine, i64 t, u64 w0, u64 s0, u64 W, u64 S) {
+    const u64 w1 = W - w0, s1 = S - s0;
+    const __int128 a = (__int128)(i64)s0 * (__int128)(i64)w1 - (__int128)(i64)s1 * (__int128)(i64)w0;
+    const unsigned __int128 bb = (unsigned __int128)((__int128)(i64)w0 * (__int128)(i64)w1);
+    if (bb == 0) return;
+    const unsigned __int128 ua = a < 0 ? (unsigned __int128)(-a) : (unsigned __int128)a;
+    Cand c;
+    c.t = t;
+    const u64 al[2] = {(u64)ua, (u64)(ua >> 64)};
+    U384 a2 = mul_limbs(al, 2, al);
+    for (int i = 0; i < 4; ++i) c.a2[i] = a2.w[i];
+    c.b[0] = (u64)bb;
+    c.b[1] = (u64)(bb >> 64);
+    if (better(c, mine)) mine = c;
+}
+
+// block-wide inclusive scan of (w, s) pairs (wrap arithmetic); returns the
+// block totals.  Warp scans, then warp 0 scans the NT/32 warp totals; three
+// barriers, two shared loads per thread.  Scratch: NT/32 pairs.
+template <int NT>
+__device__ __forceinline__ void block_scan2(u64 &w, u64 &s, u64 *sw, u64 *ss, u64 &tw, u64 &ts) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 a = __shfl_up_sync(0xffffffffu, w, o), b = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) {
+            w += a;
+            s += b;
+        }
+    }
+    __syncthreads();  // previous round's readers of sw/ss are done
+    if (lane == 31) {
+        sw[wid] = w;
+        ss[wid] = s;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        u64 a = lane < NW ? sw[lane] : 0, b = lane < NW ? ss[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < NW; o <<= 1) {
+            const u64 x = __shfl_up_sync(0xffffffffu, a, o), y = __shfl_up_sync(0xffffffffu, b, o);
+            if (lane >= o) {
+                a += x;
+                b += y;
+            }
+        }
+        if (lane < NW) {
+            sw[lane] = a;  // inclusive prefix of the warp totals
+            ss[lane] = b;
+        }
+    }
+    __syncthreads();
+    if (wid > 0) {
+        w += sw[wid - 1];
+        s += ss[wid - 1];
+    }
+    tw = sw[NW - 1];
+    ts = ss[NW - 1];
+}
+
+// Bins are visited in rounds of NT consecutive bins (thread tid takes bin
+// R*NT + tid: coalesced reads, no per-thread serial chain); the prefix sums
+// w0, s0 at each bin come from a block scan per round plus the running carry.
 template <int NT>  // threads (256 when the caller fixes 256 bins, else 1024)
 __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ hist, i64 nbins_given,
                                                   i64 *__restrict__ result) {
     constexpr int NW = NT / 32;
-    __shared__ u64 s_w[NT], s_s[NT];
+    __shared__ u64 s_w[NW], s_s[NW];
     __shared__ double s_best[NW];
     __shared__ i64 s_cnt[NW];
     __shared__ int s_hi;
@@ -95,41 +162,44 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     __syncthreads();
     i64 nb = nbins_given;
     if (nb <= 0) {
-        for (int b = 256 + tid; b < 65536; b += NT)
-            if (hist[b]) s_hi = 1;
+        int hi = 0;
+        for (int b = 256 + tid; b < 65536; b += NT) hi |= hist[b] != 0;
+        if (__any_sync(0xffffffffu, hi) && (tid & 31) == 0) s_hi = 1;
         __syncthreads();
         nb = s_hi ? 65536 : 256;
     }
-    const i64 chunk = (nb + NT - 1) / NT;
-    const i64 b0 = min((i64)tid * chunk, nb), b1 = min(b0 + chunk, nb);
-    // chunk totals
-    u64 cw = 0, cs = 0;
+    const i64 rounds = (nb + NT - 1) / NT;
+    // totals and the non-empty bin count
+    u64 W = 0, S = 0;
     i64 nzc = 0;
-    for (i64 b = b0; b < b1; ++b) {
-        const u64 h = hist[b];
-        cw += h;
-        cs += h * (u64)b;
-        nzc += h != 0;
-    }
-    s_w[tid] = cw;
-    s_s[tid] = cs;
-    // nonzero count
-    for (int o = 16; o; o >>= 1) nzc += __shfl_xor_sync(0xffffffffu, nzc, o);
-    if ((tid & 31) == 0) s_cnt[tid >> 5] = nzc;
-    __syncthreads();
-    // inclusive scan of chunk totals (Hillis-Steele on SMEM, wrap arithmetic)
-    for (int off = 1; off < NT; off <<= 1) {
-        u64 aw = 0, as = 0;
-        if (tid >= off) { aw = s_w[tid - off]; as = s_s[tid - off]; }
+    {
+        u64 cw = 0, cs = 0;
+        for (i64 R = 0; R < rounds; ++R) {
+            const i64 b = R * NT + tid;
+            const u64 h = b < nb ? hist[b] : 0;
+            cw += h;
+            cs += h * (u64)b;
+            nzc += h != 0;
+        }
+        for (int o = 16; o; o >>= 1) {
+            cw += __shfl_xor_sync(0xffffffffu, cw, o);
+            cs += __shfl_xor_sync(0xffffffffu, cs, o);
+            nzc += __shfl_xor_sync(0xffffffffu, nzc, o);
+        }
+        if ((tid & 31) == 0) {
+            s_w[tid >> 5] = cw;
+            s_s[tid >> 5] = cs;
+            s_cnt[tid >> 5] = nzc;
+        }
         __syncthreads();
-        s_w[tid] += aw;
-        s_s[tid] += as;
-        __syncthreads();
+        nzc = 0;
+        for (int i = 0; i < NW; ++i) {
+            W += s_w[i];
+            S += s_s[i];
+            nzc += s_cnt[i];
+        }
     }
-    const u64 W = s_w[NT - 1], S = s_s[NT - 1];
-    const u64 pre_w = tid ? s_w[tid - 1] : 0, pre_s = tid ? s_s[tid - 1] : 0;
-    i64 nonzero = 0;
-    for (int i = 0; i < NW; ++i) nonzero += s_cnt[i];
+    const i64 nonzero = nzc;
     if (nonzero < 2 || nb < 2) {
         if (tid == 0) {
             result[CT_OTSU_T] = 0;
@@ -139,23 +209,45 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
         }
         return;
     }
+    auto score = [&](u64 w0, u64 s0) -> double {
+        const u64 w1 = W - w0, s1 = S - s0;
+        const i64 num_i = (i64)(s0 * w1 - s1 * w0);
+        const i64 den_i = (i64)(w0 * w1);
+        double num = (double)num_i;
+        num = __dmul_rn(num, num);
+        const double den = (double)den_i;
+        return den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+    };
     // pass A: best float score over t in [0, nb-2]
     double best = -INFINITY;
+    // the bins of RB rounds are loaded up front (independent loads in flight),
+    // then scanned round by round: a load per barrier-separated round would
+    // put its full latency on the critical path
+    constexpr int RB = 8;
+    u64 hb[RB];
+    auto load_batch = [&](i64 R0) {
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const i64 t = (R0 + u) * NT + tid;
+            hb[u] = (R0 + u < rounds && t < nb) ? hist[t] : 0;
+        }
+    };
     {
-        u64 w0 = pre_w, s0 = pre_s;
-        for (i64 t = b0; t < b1; ++t) {
-            const u64 h = hist[t];
-            w0 += h;
-            s0 += h * (u64)t;
-            if (t >= nb - 1) break;
-            const u64 w1 = W - w0, s1 = S - s0;
-            const i64 num_i = (i64)(s0 * w1 - s1 * w0);
-            const i64 den_i = (i64)(w0 * w1);
-            double num = (double)num_i;
-            num = __dmul_rn(num, num);
-            const double den = (double)den_i;
-            const double sc = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
-            best = fmax(best, sc);
+        u64 cw = 0, cs = 0;
+        for (i64 R0 = 0; R0 < rounds; R0 += RB) {
+            load_batch(R0);
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                if (R0 + u >= rounds) break;  // uniform
+                const i64 t = (R0 + u) * NT + tid;
+                u64 w0 = hb[u], s0 = hb[u] * (u64)t, tw, ts;
+                block_scan2<NT>(w0, s0, s_w, s_s, tw, ts);
+                w0 += cw;
+                s0 += cs;
+                cw += tw;
+                cs += ts;
+                if (t < nb - 1) best = fmax(best, score(w0, s0));
+            }
         }
     }
     for (int o = 16; o; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
@@ -164,41 +256,30 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     best = s_best[0];
     for (int i = 1; i < NW; ++i) best = fmax(best, s_best[i]);
     const double cut = __dmul_rn(best, 1.0 - 1e-9);
-    // pass B: candidates, exact comparison
+    // pass B: candidates, exact comparison (each thread sees its bins in ascending t)
     Cand mine;
     mine.t = -1;
     {
-        u64 w0 = pre_w, s0 = pre_s;
-        for (i64 t = b0; t < b1; ++t) {
-            const u64 h = hist[t];
-            w0 += h;
-            s0 += h * (u64)t;
-            if (t >= nb - 1) break;
-            const u64 w1 = W - w0, s1 = S - s0;
-            bool cand = true;
-            if (!(best <= 0.0)) {
-                const i64 num_i = (i64)(s0 * w1 - s1 * w0);
-                const i64 den_i = (i64)(w0 * w1);
-                double num = (double)num_i;
-                num = __dmul_rn(num, num);
-                const double den = (double)den_i;
-                const double sc = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
-                cand = sc >= cut;
+        u64 cw = 0, cs = 0;
+        auto visit = [&](i64 t, u64 w0, u64 s0) {
+            if (t >= nb - 1) return;
+            if (!(best <= 0.0) && !(score(w0, s0) >= cut)) return;
+            consider(mine, t, w0, s0, W, S);  // rare: out of line
+        };
+        for (i64 R0 = 0; R0 < rounds; R0 += RB) {
+            load_batch(R0);
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                if (R0 + u >= rounds) break;  // uniform
+                const i64 t = (R0 + u) * NT + tid;
+                u64 w0 = hb[u], s0 = hb[u] * (u64)t, tw, ts;
+                block_scan2<NT>(w0, s0, s_w, s_s, tw, ts);
+                w0 += cw;
+                s0 += cs;
+                cw += tw;
+                cs += ts;
+                visit(t, w0, s0);
             }
-            if (!cand) continue;
-            // exact: a = s0*w1 - s1*w0 (Python ints), b = w0*w1
-            const __int128 a = (__int128)(i64)s0 * (__int128)(i64)w1 - (__int128)(i64)s1 * (__int128)(i64)w0;
-            const unsigned __int128 bb = (unsigned __int128)((__int128)(i64)w0 * (__int128)(i64)w1);
-            if (bb == 0) continue;
-            const unsigned __int128 ua = a < 0 ? (unsigned __int128)(-a) : (unsigned __int128)a;
-            Cand c;
-            c.t = t;
-            const u64 al[2] = {(u64)ua, (u64)(ua >> 64)};
-            U384 a2 = mul_limbs(al, 2, al);
-            for (int i = 0; i < 4; ++i) c.a2[i] = a2.w[i];
-            c.b[0] = (u64)bb;
-            c.b[1] = (u64)(bb >> 64);
-            if (better(c, mine)) mine = c;  // ascending t: strict improvement only
         }
     }
     // warp then block reduction (exact, ties -> lower t)
