@@ -20,6 +20,14 @@ It relies on two exact identities, verified by the parity tests:
     input's; any other decision is finished through the drop-in API
     (``finish_vessel``), which reproduces the reference in every case.
 Data-dependent errors (DegenerateHistogramError) surface in ``finish_*``.
+
+Stream contract: every launch goes to the current torch stream, and a
+result's buffers (labels, table, voxel lists, mask, distance) are reused by
+the next ``cell()`` / ``vessel()`` call of the same pipeline.  A result is
+valid only for work ordered after it on the launching stream; the next
+frame's label background fill (side stream) waits on an event recorded on
+that stream at the next ``cell()`` call, so a consumer on any other stream
+must make the launching stream wait for it first.
 """
 
 from __future__ import annotations
