@@ -457,7 +457,7 @@ def run_ours(args):
     rx, ry, rz = pipe.r
     b = 1 if spec.dtype == "u8" else 2
     k1_tc = pipe.k1_path_tc
-    k1_macs = (4 * 256 + 13 * 256 + 13 * spec.nz) if k1_tc else None  # limb-pair MMAs (see k_gauss_tc.cu)
+    k1_macs = (4 * 256 * b + 13 * 256 + 13 * spec.nz) if k1_tc else None  # limb-pair MMAs (see k_gauss_tc.cu)
     bpv = {"K1 gaussian": 2 * b, "K2 median+hist": 2 * b,
            "K4 threshold+close": (b + 0.125) if pipe.rows_path else (b + 1), "K5 ccl": 0.125 if pipe.rows_path else 1,
            "K6 table": None, "K7 mrf": b, "K3+K4 vessel otsu+close": b + 1, "K8 edt": 9}

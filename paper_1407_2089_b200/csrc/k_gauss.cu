@@ -307,7 +307,7 @@ int pass_strided(const Tin *in, double *out, i64 outer, i64 L, i64 inner, const 
 
 template <typename Traw, typename Tq>
 int pass_contig(const double *in, i64 nlines, i64 L, const double *w, int r, const Traw *raw, double *bg_out,
-                double *res_out, Tq *q_out, cudaStream_t s) {
+                double *res_out, Tq *q_out, double *scratch, cudaStream_t s) {
     const i64 n = nlines * L;
     if (r >= 0) {
         int S = (int)(((L + B - 1) / B) * B + 2 * r);
@@ -325,12 +325,8 @@ int pass_contig(const double *in, i64 nlines, i64 L, const double *w, int r, con
             return ct::check_launch("gauss_contig");
         }
     }
-    // generic: filter into res_out-or-bg scratch, then epilogue
-    double *tmp = bg_out ? bg_out : res_out;
-    if (!tmp) {
-        ct::set_error("generic contiguous pass needs bg or residual output");
-        return CT_ERR_UNSUPPORTED;
-    }
+    // generic: filter into bg_out, res_out or the caller's scratch (N doubles), then epilogue
+    double *tmp = bg_out ? bg_out : res_out ? res_out : scratch;
     if (r < 0) {
         cudaMemcpyAsync(tmp, in, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
     } else {
@@ -349,7 +345,7 @@ int gaussian_residual(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, 
     const double *wx = w, *wy = w + (rx >= 0 ? rx + 1 : 0), *wz = wy + (ry >= 0 ? ry + 1 : 0);
     if (int st = pass_strided<Traw>(raw, p1, 1, nx, ny * nz, wx, rx, s)) return st;
     if (int st = pass_strided<double>(p1, p2, nx, ny, nz, wy, ry, s)) return st;
-    return pass_contig<Traw, Tq>(p2, nx * ny, nz, wz, rz, raw, bg_out, res_out, q_out, s);
+    return pass_contig<Traw, Tq>(p2, nx * ny, nz, wz, rz, raw, bg_out, res_out, q_out, p1, s);  // p1 is dead here
 }
 
 }  // namespace
@@ -748,16 +744,17 @@ int gaussian_q_fast(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, in
 
 }  // namespace
 
-int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry, int rz,
-                     void *work, uint8_t *q, unsigned long long *fix, int64_t cap, double eps_override,
+int ct_gaussian_q_tc(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry,
+                     int rz, void *work, void *q, unsigned long long *fix, int64_t cap, double eps_override,
                      cudaStream_t s);
 
-bool ct_gaussian_q_tc_fits(int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz);
+bool ct_gaussian_q_tc_fits(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz);
 
 // K1 fast-path selection (per call): 0 auto (tensor cores when the shape
 // fits, else FP64 FMA), 1 FP64 FMA, 2 tensor cores only.
 extern "C" int ct_k1_path(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz, int path) {
-    if (dtype == CT_U8 && path != 1 && ct_gaussian_q_tc_fits(nx, ny, nz, rx, ry, rz)) return 2;
+    // auto: u8 only for now (u16 flags too many voxels for the exact fix-up at 32-bit intermediates)
+    if ((path == 2 || (path == 0 && dtype == CT_U8)) && ct_gaussian_q_tc_fits(dtype, nx, ny, nz, rx, ry, rz)) return 2;
     return 1;
 }
 
@@ -780,23 +777,25 @@ extern "C" int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny,
         return ct_gaussian_residual(raw, dtype, nx, ny, nz, w, rx, ry, rz, work, nullptr, nullptr, q_out, dtype,
                                     stream);
     }
-    if (dtype == CT_U8) {
-        // tensor-core path (k_gauss_tc.cu) unless disabled or the shape does not fit
-        if (path != 1) {
-            const int st = ct_gaussian_q_tc((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, work, (uint8_t *)q_out,
-                                            fix, fix_cap, eps_override, s);
-            if (st == CT_OK)
-                return launch_fixup<uint8_t>((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, work,
-                                             (size_t)2 * nx * ny * nz * sizeof(double), fix, fix_cap,
-                                             (uint8_t *)q_out, s);
-            if (st != CT_ERR_UNSUPPORTED || path == 2) {
-                if (st == CT_ERR_UNSUPPORTED) ct::set_error("tensor-core K1 does not support this shape");
-                return st;
-            }
+    // tensor-core path (k_gauss_tc.cu) unless disabled or the shape does not fit
+    if (path == 2 || (path == 0 && dtype == CT_U8)) {
+        const int st = ct_gaussian_q_tc(raw, dtype, nx, ny, nz, w, rx, ry, rz, work, q_out, fix, fix_cap,
+                                        eps_override, s);
+        if (st == CT_OK) {
+            const size_t wb = (size_t)2 * nx * ny * nz * sizeof(double);
+            return dtype == CT_U8 ? launch_fixup<uint8_t>((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, work, wb,
+                                                          fix, fix_cap, (uint8_t *)q_out, s)
+                                  : launch_fixup<uint16_t>((const uint16_t *)raw, nx, ny, nz, w, rx, ry, rz, work,
+                                                           wb, fix, fix_cap, (uint16_t *)q_out, s);
         }
+        if (st != CT_ERR_UNSUPPORTED || path == 2) {
+            if (st == CT_ERR_UNSUPPORTED) ct::set_error("tensor-core K1 does not support this shape");
+            return st;
+        }
+    }
+    if (dtype == CT_U8)
         return gaussian_q_fast<uint8_t>((const uint8_t *)raw, nx, ny, nz, w, rx, ry, rz, (double *)work,
                                         (uint8_t *)q_out, fix, fix_cap, 255.0, eps_override, s);
-    }
     return gaussian_q_fast<uint16_t>((const uint16_t *)raw, nx, ny, nz, w, rx, ry, rz, (double *)work,
                                      (uint16_t *)q_out, fix, fix_cap, 65535.0, eps_override, s);
 }

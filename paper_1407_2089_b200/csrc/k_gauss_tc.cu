@@ -50,16 +50,35 @@ constexpr int PMAX = 65;       // max taps per side + 1
 struct TcParams {
     long long Q[3][PMAX];  // integer taps per axis (Q[axis][|j|] = rint(w_j 2^fw[axis]))
     int fw[3];             // weight scale bits per axis (<= FW, four 8-bit limbs)
-    long long eps;         // certification threshold in units of 2^-(fw[2] + 8)
+    int fd;                // fractional bits of the 32-bit intermediates: 32 - bits(vmax), in [16, FD]
+    long long eps;         // certification threshold in units of 2^-(fw[2] + fd - 16)
+    unsigned vmax;         // u16: the frame's maximum (tc_vmax); u8: 255
 };
+
+// u16 frames: the maximum sets the intermediates' integer bits (P1, P2 <=
+// vmax), so 12-bit data keeps 20 fractional bits instead of 16
+__global__ void __launch_bounds__(256) tc_vmax(const uint4 *__restrict__ raw, long long n16, TcParams *prm) {
+    uint32_t m = 0;
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n16; i += (long long)gridDim.x * 256) {
+        const uint4 v = raw[i];
+        m = max(m, __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w)));
+    }
+    m = max(m & 0xffffu, m >> 16);
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(&prm->vmax, m);
+}
 
 // ---------------------------------------------------------------------------
 // Setup: integer taps and the certified error bound (one warp per axis).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int rx, int ry, int rz, double vmax,
+__global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int rx, int ry, int rz, int u8,
                                                double eps_override, TcParams *prm) {
     // warp a handles axis a: lane-parallel taps, warp reductions
     const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned vm = u8 ? 255u : prm->vmax;  // tc_vmax ran before (u16)
+    const double vmax = (double)vm;
+    // P <= vmax (1 + (2r+1) 2^-fw) < 2^bits(vmax): 32 - bits integer bits left for the fraction
+    const int fd = min(FD, max(16, 32 - (vm ? 32 - __clz(vm) : 0)));
     const int rr[3] = {rx, ry, rz};
     const double *ws = a == 0 ? w : (a == 1 ? w + rx + 1 : w + rx + 1 + ry + 1);
     const int r = rr[a];
@@ -92,7 +111,7 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
     // inputs of passes y, z are bounded by vmax up to the taps' sum rounding)
     // plus, for y and z, the dropped limb pairs (a+b <= 1: (0,0), (1,0), (0,1))
     double b = dq / scale * vmax * 1.001;
-    if (a > 0) b += 255.0 * (qsum0 * ldexp(1.0, -fw - FD) + (qsum0 + qsum1) * ldexp(1.0, 8 - fw - FD));
+    if (a > 0) b += 255.0 * (qsum0 * ldexp(1.0, -fw - fd) + (qsum0 + qsum1) * ldexp(1.0, 8 - fw - fd));
     __shared__ double bs[3];
     __shared__ int fws[3];
     if (lane == 0) {
@@ -102,11 +121,13 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        prm->fd = fd;
+        prm->vmax = vm;
+        const int zs = fws[2] + fd - 16;  // scale bits of the final sum
         double bound = bs[0] + bs[1] + bs[2];
-        bound += 2.0 * ldexp(1.0, -FD);                              // truncation of P1, P2
-        bound += 4.0 * ldexp(1.0, -(fws[2] + 8));                    // floor of pass z edge terms
+        bound += 2.0 * ldexp(1.0, -fd);                               // truncation of P1, P2
+        bound += 4.0 * ldexp(1.0, -zs);                               // floor of pass z edge terms
         bound += 4.0 * (rx + ry + rz + 12) * ldexp(1.0, -53) * vmax;  // scipy float64 order + residual
-        const int zs = fws[2] + 8;  // scale bits of the final sum
         prm->eps = (long long)ceil(bound * 1.25 * ldexp(1.0, zs)) + 16;
         if (eps_override > 0.0) prm->eps = (long long)ceil(eps_override * ldexp(1.0, zs));
     }
@@ -158,7 +179,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     __syncthreads();
     tc::fence_after();
     // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
-    const int shift_out = NPIN == 1 ? prm->fw[axis] - FD : prm->fw[axis] - 16;
+    const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 16;
     const uint32_t base = tbase;
     const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
     // A (taps) into TMEM columns [0, 256): limb b = cg at 64 b; row m
@@ -338,20 +359,27 @@ __device__ __forceinline__ void epi_bar() {  // named barrier 1: the epilogue wa
     asm volatile("bar.sync 1, %0;" ::"n"(32 * WS_EPI) : "memory");
 }
 
-template <int NPIN, int TN, int SSTG, int ASTG>
+// DB = bytes per input voxel: 2 for raw u16 (pass x), read as a byte matrix
+// of twice the width -- column 2c holds the low bytes of voxel c, column
+// 2c + 1 the high bytes, so the MMA yields both limb sums and the epilogue
+// combines S(c) = D[2c] + 256 D[2c + 1] (no de-interleave pass).
+template <int NPIN, int TN, int SSTG, int ASTG, int DB = 1>
 __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant__ CUtensorMap tmap, int L, int inner,
                                                           int outer, const TcParams *__restrict__ prm, int axis, int r,
                                                           uint8_t *__restrict__ out, long long plane_out) {
+    static_assert(DB == 1 || NPIN == 1, "u16 input only for the raw pass");
     constexpr int NACC = NPIN == 1 ? 4 : 5;
     constexpr int CH = TN / 16;                     // 16-byte chunks per row (one TMA box each)
     constexpr int PB = KXY * 16;                    // bytes per plane per chunk: [KXY][16]
     constexpr int CB = NPIN * PB;                   // bytes per chunk (all planes)
     constexpr int SB = CH * CB;                     // bytes per stage, [CH][NPIN][KXY][16]
     constexpr uint32_t LBO = 128, SBO = CB;         // MN-major: 8 K-rows = 128 B; next 16 columns = CB
-    constexpr int CW = TN / 4;                      // columns per epilogue thread (4 column groups)
-    constexpr int OROW = TN + 16;                   // padded staged output row (bytes)
+    constexpr int CW = TN / 4;                      // (byte) columns per epilogue thread (4 column groups)
+    constexpr int TV = TN / DB;                     // voxels per tile row
+    constexpr int OROW = TV + 16;                   // padded staged output row (bytes)
     constexpr int OBUF = 4 * TM * OROW;             // staged output tile: [4 planes][128 rows]
-    constexpr int CPR = TN / 16;                    // 16-byte chunks per output row
+    constexpr int CPR = TV / 16;                    // 16-byte chunks per output row
+    const long long inner_v = inner / DB;           // voxels per input row
     static_assert(256 + ASTG * NACC * TN <= 512, "TMEM: band + accumulator sets");
     extern __shared__ __align__(1024) uint8_t sm[];  // [SSTG][SB] operand stages, [2][OBUF] output tiles
     uint8_t *sout = sm + SSTG * SB;
@@ -485,8 +513,8 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
         const int h = CW * cg;
         const int et = t - 64;  // 0 .. 32 * WS_EPI - 1
         // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
-        const int shift_out = NPIN == 1 ? prm->fw[axis] - FD : prm->fw[axis] - 16;
-        // coalesced store of a staged output tile: 4 planes x 128 rows x TN bytes
+        const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 16;
+        // coalesced store of a staged output tile: 4 planes x 128 rows x TV bytes
         auto flush = [&](long long k, const uint8_t *ob) {
             int o, ti, cb;
             coords(k, o, ti, cb);
@@ -497,7 +525,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                 const int pa = e / (CPR * TM), mm = (e / CPR) % TM, hh = e % CPR;
                 const int i = ti * TM + mm;
                 if (i < L)
-                    *(uint4 *)(out + pa * plane_out + ((long long)o * L + i) * inner + (long long)cb * TN + 16 * hh) =
+                    *(uint4 *)(out + pa * plane_out + ((long long)o * L + i) * inner_v + (long long)cb * TV + 16 * hh) =
                         *(const uint4 *)(ob + (pa * TM + mm) * OROW + 16 * hh);
             }
         };
@@ -523,19 +551,23 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
             if (lane == 0) tc::mbar_arrive(&aempty[a]);  // MMA(k + ASTG) may overwrite set a
             uint8_t *ob = sout + (int)(k & 1) * OBUF;
 #pragma unroll
-            for (int g4 = 0; g4 < CW; g4 += 4) {
+            for (int g4 = 0; g4 < CW; g4 += 4 * DB) {
                 uint32_t ov[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     long long S = 0;
 #pragma unroll
-                    for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][g4 + c] << (8 * acc);
+                    for (int acc = 0; acc < NACC; ++acc) {
+                        long long d = v[acc][g4 + DB * c];
+                        if constexpr (DB == 2) d += (long long)v[acc][g4 + 2 * c + 1] << 8;
+                        S += d << (8 * acc);
+                    }
                     ov[c] = (uint32_t)(S >> shift_out);
                 }
                 uint32_t pl[4];
                 planes4(ov[0], ov[1], ov[2], ov[3], pl);
 #pragma unroll
-                for (int pa = 0; pa < 4; ++pa) *(uint32_t *)(ob + (pa * TM + m) * OROW + h + g4) = pl[pa];
+                for (int pa = 0; pa < 4; ++pa) *(uint32_t *)(ob + (pa * TM + m) * OROW + (h + g4) / DB) = pl[pa];
             }
             epi_bar();  // tile k staged (and tile k-1's flush, issued before, finished by every thread)
             flush(k, ob);
@@ -554,21 +586,27 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
 // (mode "nearest"), so the epilogue adds x[0] E0[n] + x[nz-1] EL[n] with the
 // integer tail sums E0[n] = sum_{j < -n} Q_|j|, EL[n] = sum_{j > nz-1-n} Q_j.
 // ---------------------------------------------------------------------------
-template <int NZ, int STAGES>
+template <int NZ, int STAGES, typename Traw = uint8_t>
 __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ in, long long plane, long long nlines,
                                                     const TcParams *__restrict__ prm, int r,
-                                                    const uint8_t *__restrict__ raw, uint8_t *__restrict__ q,
+                                                    const Traw *__restrict__ raw, Traw *__restrict__ q,
                                                     unsigned long long *__restrict__ fix, long long cap) {
+    constexpr int RB = (int)sizeof(Traw);       // raw / q bytes per voxel
+    constexpr int VPW = 4 / RB;                 // voxels per 32-bit word
+    static_assert(NZ <= 64 || RB == 1, "u16 pass z: nz in {32, 64}");
     constexpr int NCH = NZ / 16;                // 16-byte chunks per line
     constexpr uint32_t LBO = 128, SBO = NCH * 128;
     constexpr int ABUF = TM * NZ;               // bytes per plane per buffer
+    constexpr int RBUF = ABUF * RB;             // bytes of a raw / q tile
     constexpr int BW = NZ * NZ;                 // bytes per weight limb
-    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [STAGES][4][ABUF] data, [STAGES][ABUF] raw,
-                                                     // [2][ABUF] q tile
+    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [STAGES][4][ABUF] data, [STAGES][RBUF] raw,
+                                                     // [2][RBUF] q tile
     uint8_t *sw = sm;
     uint8_t *sa = sm + 4 * BW;
     uint8_t *sr = sa + STAGES * 4 * ABUF;
-    uint8_t *sq = sr + STAGES * ABUF;
+    uint8_t *sq = sr + STAGES * RBUF;
+    const uint8_t *rawb = (const uint8_t *)raw;
+    uint8_t *qb8 = (uint8_t *)q;
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
     __shared__ long long Qs[PMAX], Ts[PMAX + 1];
@@ -601,7 +639,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         Et[n] = make_uint4((uint32_t)(e0 >> 16), (uint32_t)(e0 & 0xffff), (uint32_t)(el >> 16), (uint32_t)(el & 0xffff));
     }
     const long long eps = prm->eps;
-    const int zs = prm->fw[2] + 8;  // S has scale 2^zs
+    const int zs = prm->fw[2] + prm->fd - 16;  // S has scale 2^zs
     const long long half = 1ll << (zs - 1), one = 1ll << zs, fmask = one - 1;
     const uint32_t base = tbase;
     const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
@@ -620,7 +658,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
                 for (int a = 0; a < 4; ++a)
                     tc::cp_async16(sa + (buf * 4 + a) * ABUF + tc::kmajor_off(l, 16 * c, LBO, SBO),
                                    in + a * plane + (l0 + l) * NZ + 16 * c);
-                tc::cp_async16(sr + buf * ABUF + l * NZ + 16 * c, raw + (l0 + l) * NZ + 16 * c);
+#pragma unroll
+                for (int j = 0; j < RB; ++j)
+                    tc::cp_async16(sr + buf * RBUF + (l * NZ + 16 * c) * RB + 16 * j,
+                                   rawb + ((l0 + l) * NZ + 16 * c) * RB + 16 * j);
             }
         }
         tc::cp_commit();
@@ -629,8 +670,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     // coalesced store of a staged q tile (lines are contiguous in global)
     auto flush = [&](long long tile, const uint8_t *qb) {
         const long long l0 = tile * TM;
-        const int nbytes = (int)min((long long)TM, nlines - l0) * NZ;
-        for (int e = 16 * t; e < nbytes; e += 16 * NT) *(uint4 *)(q + l0 * NZ + e) = *(const uint4 *)(qb + e);
+        const int nbytes = (int)min((long long)TM, nlines - l0) * NZ * RB;
+        for (int e = 16 * t; e < nbytes; e += 16 * NT) *(uint4 *)(qb8 + l0 * NZ * RB + e) = *(const uint4 *)(qb + e);
     };
     // same software pipeline as tc_pass_xy
     const long long t0 = blockIdx.x, gs = gridDim.x;
@@ -689,13 +730,13 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         // rounding boundaries R = (k + 1/2) 2^zs (k >= 0) are T = (k+1) 2^zs,
         // flagged when T is within eps of one of them
         const long long T = (long long)(((unsigned long long)raw8 << zs) - S) + half;
-        const uint32_t qv = T > 0 ? (uint32_t)(T >> zs) : 0u;
+        const uint32_t qv = T > 0 ? (uint32_t)(T >> zs) : 0u;  // <= raw8
         if (T >= one - eps && ((T + eps) & fmask) <= 2 * eps) {
             const unsigned long long at = atomicAdd(&fix[0], 1ull);
             if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
             else fix[1] = 1;
         }
-        return qv & 0xffu;
+        return qv;
     };
     auto edges = [&](long long k, uint32_t &x0, uint32_t &xl) {
         const uint8_t *ab = sa + (int)(k % STAGES) * 4 * ABUF;
@@ -722,10 +763,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         tc::tmem_ld_wait();
         // raw and the line's edge values of tile k (slot k % STAGES) before the slot is restaged
         const long long l = (t0 + k * gs) * TM + m;
-        const uint8_t *rl = sr + (int)(k % STAGES) * ABUF + m * NZ + h0;
-        uint32_t rw[CW / 4];
+        const uint8_t *rl = sr + (int)(k % STAGES) * RBUF + (m * NZ + h0) * RB;
+        uint32_t rw[CW / VPW];
 #pragma unroll
-        for (int c4 = 0; c4 < CW / 4; ++c4) rw[c4] = *(const uint32_t *)(rl + 4 * c4);
+        for (int c4 = 0; c4 < CW / VPW; ++c4) rw[c4] = *(const uint32_t *)(rl + 4 * c4);
         uint32_t x0, xl;
         edges(k, x0, xl);
         tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
@@ -736,19 +777,21 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         if (k + 1 < nmine) issue(k + 1);
         if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
         else tc::cp_commit();
-        if (k > 0) flush(t0 + (k - 1) * gs, sq + (int)((k - 1) & 1) * ABUF);
-        uint32_t qw[CW / 4];
+        if (k > 0) flush(t0 + (k - 1) * gs, sq + (int)((k - 1) & 1) * RBUF);
+        constexpr uint32_t VM = RB == 1 ? 0xffu : 0xffffu;
+        uint32_t qw[CW / VPW];
 #pragma unroll
-        for (int c4 = 0; c4 < CW / 4; ++c4) qw[c4] = 0;
+        for (int c4 = 0; c4 < CW / VPW; ++c4) qw[c4] = 0;
         if (l < nlines) {
 #pragma unroll
             for (int c = 0; c < CW; ++c)
-                qw[c >> 2] |= qbyte(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], c,
-                                    (rw[c >> 2] >> (8 * (c & 3))) & 0xff, x0, xl, l) << (8 * (c & 3));
+                qw[c / VPW] |= qbyte(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], c,
+                                     (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM, x0, xl, l)
+                               << (8 * RB * (c % VPW));
         }
-        uint8_t *qb = sq + (int)(k & 1) * ABUF + m * NZ + h0;
+        uint8_t *qb = sq + (int)(k & 1) * RBUF + (m * NZ + h0) * RB;
 #pragma unroll
-        for (int c4 = 0; c4 < CW / 4; c4 += 2) *(uint2 *)(qb + 4 * c4) = make_uint2(qw[c4], qw[c4 + 1]);
+        for (int c4 = 0; c4 < CW / VPW; c4 += 2) *(uint2 *)(qb + 4 * c4) = make_uint2(qw[c4], qw[c4 + 1]);
     }
     } else {
     // long lines (NZ = 96): the accumulators do not fit in registers at once,
@@ -790,7 +833,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     }
     }
     __syncthreads();
-    if (nmine > 0) flush(t0 + (nmine - 1) * gs, sq + (int)((nmine - 1) & 1) * ABUF);
+    if (nmine > 0) flush(t0 + (nmine - 1) * gs, sq + (int)((nmine - 1) & 1) * RBUF);
     tc::cp_wait_all();
     __syncthreads();
     tc::fence_after();
@@ -813,39 +856,40 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
     return fn;
 }
 
-// TC path of ct_gaussian_q (u8).  Returns CT_ERR_UNSUPPORTED when the shape
-// does not fit (the caller then uses the SIMT FMA path).  work: >= 8 N bytes
-// (byte planes of P1 and P2) + sizeof(TcParams).
-bool ct_gaussian_q_tc_fits(int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz) {
-    return (nz == 32 || nz == 64 || nz == 96) && rx >= 0 && ry >= 0 && rz >= 0 && rx <= (KXY - TM) / 2 && ry <= (KXY - TM) / 2 &&
-           rz < PMAX && (ny * nz) % TNX == 0 && nz % TNY == 0 && nx * ny * nz < (1ll << 31);
+// TC path of ct_gaussian_q (u8, u16).  Returns CT_ERR_UNSUPPORTED when the
+// shape does not fit (the caller then uses the SIMT FMA path).  work: >= 8 N
+// bytes (byte planes of P1 and P2) + sizeof(TcParams).
+bool ct_gaussian_q_tc_fits(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz) {
+    const bool u16 = dtype == CT_U16;
+    if (dtype != CT_U8 && !u16) return false;
+    return (nz == 32 || nz == 64 || (nz == 96 && !u16)) && rx >= 0 && ry >= 0 && rz >= 0 && rx <= (KXY - TM) / 2 &&
+           ry <= (KXY - TM) / 2 && rz < PMAX && (ny * nz) % TNX == 0 && nz % TNY == 0 &&
+           nx * ny * nz < (1ll << 31);
 }
 
-int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry, int rz,
-                     void *work, uint8_t *q, unsigned long long *fix, int64_t cap, double eps_override,
-                     cudaStream_t s) {
-    if (!ct_gaussian_q_tc_fits(nx, ny, nz, rx, ry, rz) || ((uintptr_t)raw & 15)) return CT_ERR_UNSUPPORTED;
+namespace {
+
+template <typename Traw>
+int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz, uint8_t *p1,
+                  uint8_t *p2, TcParams *prm, Traw *q, unsigned long long *fix, int64_t cap, cudaStream_t s) {
+    constexpr int RB = (int)sizeof(Traw);
     const long long N = nx * ny * nz;
     // persistent grids: one CTA per SM (capping it to leave SMs to the concurrent vessel stream measured
     // slower: 140 / 132 / 120 SMs -> 1.744 / 1.750 / 1.810 ms per C2 step vs 1.744)
     const int nsm = CT_NUM_SMS;
-    uint8_t *p1 = (uint8_t *)work, *p2 = p1 + 4 * N;
-    TcParams *prm = (TcParams *)(p2 + 4 * N);
-    cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
-    tc_prep<<<1, 96, 0, s>>>(w, rx, ry, rz, 255.0, eps_override, prm);
-    if (int st = ct::check_launch("tc_prep")) return st;
-    // pass x: warp-specialised, operands staged by TMA
     PFN_cuTensorMapEncodeTiled_v12000 encode = tma_encoder();
     if (!encode) {
         ct::set_error("cuTensorMapEncodeTiled unavailable (driver entry point)");
         return CT_ERR_CUDA;
     }
-    // pass x: [1][nx][ny*nz]; box = 16 bytes x 256 x-rows, TX / 16 boxes per tile
+    // pass x: warp-specialised, operands staged by TMA.  The raw volume as a
+    // byte matrix [nx][ny nz RB]; box = 16 bytes x 256 x-rows, TX / 16 boxes
+    // per tile (u16: TX bytes = TX / 2 voxels, both byte limbs)
     {
         constexpr int TX = 64, SS = 6, AS = 1;
         CUtensorMap tm;
-        const cuuint64_t dims[2] = {(cuuint64_t)(ny * nz), (cuuint64_t)nx};
-        const cuuint64_t strides[1] = {(cuuint64_t)(ny * nz)};
+        const cuuint64_t dims[2] = {(cuuint64_t)(ny * nz * RB), (cuuint64_t)nx};
+        const cuuint64_t strides[1] = {(cuuint64_t)(ny * nz * RB)};
         const cuuint32_t box[2] = {16, KXY}, es[2] = {1, 1};
         if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)raw, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -853,12 +897,12 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
             ct::set_error("tensor map (pass x) rejected");
             return CT_ERR_UNSUPPORTED;
         }
-        auto kx = tc_pass_xy_ws<1, TX, SS, AS>;
-        const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * 4 * TM * (TX + 16) + 1024;
+        auto kx = tc_pass_xy_ws<1, TX, SS, AS, RB>;
+        const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * 4 * TM * (TX / RB + 16) + 1024;
         cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        const long long tiles = ((nx + TM - 1) / TM) * (ny * nz / TX);
-        kx<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tm, (int)nx, (int)(ny * nz), 1, prm, 0, rx,
-                                                                        p1, N);
+        const long long tiles = ((nx + TM - 1) / TM) * (ny * nz * RB / TX);
+        kx<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tm, (int)nx, (int)(ny * nz * RB), 1, prm, 0,
+                                                                        rx, p1, N);
         if (int st = ct::check_launch("tc_pass_x")) return st;
     }
     // pass y: [nx][ny][nz] x 4 planes, the synchronous form (cp.async staging):
@@ -876,14 +920,44 @@ int ct_gaussian_q_tc(const uint8_t *raw, int64_t nx, int64_t ny, int64_t nz, con
     // pass z + epilogue
     {
         const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
-        const int stg = nz == 96 ? 2 : 4;
-        const size_t sm = 4 * nz * nz + (size_t)stg * (4 * TM * nz + TM * nz) + 2 * TM * nz + 1024;
-        auto kz = nz == 64 ? tc_pass_z<64, 4> : nz == 96 ? tc_pass_z<96, 2> : tc_pass_z<32, 4>;
+        const int stg = RB == 2 ? 3 : nz == 96 ? 2 : 4;
+        const size_t sm = 4 * nz * nz + (size_t)stg * (4 * TM * nz + TM * nz * RB) + 2 * TM * nz * RB + 1024;
+        void (*kz)(const uint8_t *, long long, long long, const TcParams *, int, const Traw *, Traw *,
+                   unsigned long long *, long long);
+        if constexpr (RB == 2)
+            kz = nz == 64 ? tc_pass_z<64, 3, Traw> : tc_pass_z<32, 3, Traw>;
+        else
+            kz = nz == 64 ? tc_pass_z<64, 4, Traw> : nz == 96 ? tc_pass_z<96, 2, Traw> : tc_pass_z<32, 4, Traw>;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         kz<<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
         if (int st = ct::check_launch("tc_pass_z")) return st;
     }
     return CT_OK;
+}
+
+}  // namespace
+
+int ct_gaussian_q_tc(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t nz, const double *w, int rx, int ry,
+                     int rz, void *work, void *q, unsigned long long *fix, int64_t cap, double eps_override,
+                     cudaStream_t s) {
+    if (!ct_gaussian_q_tc_fits(dtype, nx, ny, nz, rx, ry, rz) || ((uintptr_t)raw & 15)) return CT_ERR_UNSUPPORTED;
+    const long long N = nx * ny * nz;
+    uint8_t *p1 = (uint8_t *)work, *p2 = p1 + 4 * N;
+    TcParams *prm = (TcParams *)(p2 + 4 * N);
+    cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
+    const bool u8 = dtype == CT_U8;
+    if (!u8) {
+        cudaMemsetAsync(&prm->vmax, 0, sizeof(unsigned), s);
+        tc_vmax<<<CT_NUM_SMS * 4, 256, 0, s>>>((const uint4 *)raw, N * 2 / 16, prm);  // N * 2 % 16 == 0 (nz % 32)
+        if (int st = ct::check_launch("tc_vmax")) return st;
+    }
+    tc_prep<<<1, 96, 0, s>>>(w, rx, ry, rz, u8 ? 1 : 0, eps_override, prm);
+    if (int st = ct::check_launch("tc_prep")) return st;
+    if (u8)
+        return gaussian_q_tc<uint8_t>((const uint8_t *)raw, nx, ny, nz, rx, ry, rz, p1, p2, prm, (uint8_t *)q, fix,
+                                      cap, s);
+    return gaussian_q_tc<uint16_t>((const uint16_t *)raw, nx, ny, nz, rx, ry, rz, p1, p2, prm, (uint16_t *)q, fix,
+                                   cap, s);
 }
 
 size_t ct_gaussian_q_tc_work(int64_t nx, int64_t ny, int64_t nz) {

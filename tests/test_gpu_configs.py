@@ -314,3 +314,50 @@ def test_mrf_statistics_repeatable_vs_oracle(cuda, oracle, nz):
             if fn == "ct_mrf" or st[2] != 2.0:
                 assert st[1] == o["sigma_hat"], (fn, st)
             assert st[MRF_DECISION] == 0.0
+
+
+UNIT = VoxelSpacing(1.0, 1.0, 1.0)
+
+
+@pytest.mark.parametrize("dims,dt,sigma,radius", [
+    ((128, 128, 128), "u8", 1.0, 1), ((128, 128, 128), "u16", 2.0, 2), ((128, 128, 128), "u8", 4.0, 3),
+    ((96, 64, 160), "u8", 3.0, 2), ((64, 48, 256), "u16", 4.0, 1), ((128, 96, 64), "u16", 3.0, 3)])
+def test_c5_sweep_points_vs_oracle(cuda, oracle, dims, dt, sigma, radius):
+    """BASELINE configs[4] (C5 sweep): unit spacing, sigma 1-4 voxels, median
+    radius 1-3, u8 / u16, incl. nz > 128 (the generic z pass and byte-mask
+    CCL) -- the fused path vs the oracle: q, median, histogram, threshold,
+    detections, label volume and the vessel channel."""
+    from paper_1407_2089_b200.denoise import CellDenoiseParams
+
+    n = dims[0] * dims[1] * dims[2]
+    spec = synth.SceneSpec(*dims, dt, n_cells=max(10, n * 50 // (256 * 256 * 32)),
+                           n_tubes=max(3, 3 * dims[1] * dims[2] // (256 * 32)), seed=5)
+    pipe = FramePipeline(dims, dt, UNIT, denoise=CellDenoiseParams(sigma, radius))
+    sp = UNIT.as_array()
+    raw = synth.generate(spec, 0, synth.CELL)
+    host = host_frame(oracle, spec, 0, synth.CELL)
+    np.testing.assert_array_equal(to_np(raw), host)
+    cnt, rows = pipe.finish_cell(pipe.cell(raw, frame=0))
+    o = oracle.denoise_cell(host, sp, sigma, radius)
+    np.testing.assert_array_equal(to_np(pipe.q), np.rint(o["residual"]).astype(spec.np_dtype))
+    np.testing.assert_array_equal(to_np(pipe.med), np.rint(o["denoised"]).astype(spec.np_dtype))
+    hist = oracle.histogram(o["denoised"])
+    np.testing.assert_array_equal(pipe.hist.cpu().numpy()[: hist.size], hist)
+    assert int(pipe.otsu[0]) == oracle.otsu(hist)
+    odets = oracle.segment_cell(o["denoised"], sp, frame=0, intensity=host)
+    assert len(rows) == len(odets) > 0
+    assert list(rows["count"]) == [d.voxel_count for d in odets]
+    assert list(rows["root"]) == [d.root for d in odets]
+    np.testing.assert_array_equal(rows["centroid_um"], np.array([d.centroid_um for d in odets]))
+    nx, ny, nz = dims
+    lab = np.full(n, -1, np.int32)
+    for i, d in enumerate(odets):
+        lab[(d.voxels[:, 0] * ny + d.voxels[:, 1]) * nz + d.voxels[:, 2]] = i
+    np.testing.assert_array_equal(pipe.labels.cpu().numpy().ravel(), lab)
+    vraw = synth.generate(spec, 0, synth.VESSEL)
+    vhost = host_frame(oracle, spec, 0, synth.VESSEL)
+    mask, dm = pipe.finish_vessel(pipe.vessel(vraw), vraw)
+    st = oracle.mrf(vhost)
+    om, odist, _ = oracle.segment_vessel(st["current"] if st["current"] is not None else vhost, sp)
+    np.testing.assert_array_equal(mask.cpu().numpy(), om)
+    np.testing.assert_array_equal(dm.values.cpu().numpy(), odist)

@@ -321,6 +321,28 @@ def test_tensor_core_k1_matches_exact(cuda, sigma, shape, seed):
         assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
 
 
+@pytest.mark.parametrize("vmax,shape,sigma,seed", [(4095, (256, 128, 64), 10.0, 21), (65535, (130, 64, 64), 10.0, 22),
+                                                   (200, (96, 64, 32), 6.0, 23), (4095, (64, 192, 32), 3.0, 24)])
+def test_tensor_core_k1_u16_matches_exact(cuda, vmax, shape, sigma, seed):
+    """u16 tensor-core K1 (byte-interleaved pass x, fraction bits from the
+    frame's maximum: 20 for 12-bit data, 16 at full range, 24 when the
+    maximum is <= 255) on noise and on a synthetic 12-bit scene vs the
+    scipy-order exact path."""
+    from paper_1407_2089_b200._lib import lib
+
+    assert lib().ct_k1_path(2, *shape, 12, 12, 10, 2) == 2
+    rng = np.random.default_rng(seed)
+    noise = torch.from_numpy(rng.integers(0, vmax + 1, size=shape).astype(np.uint16).view(np.int16)).cuda()
+    raws = [noise.view(torch.uint16)]
+    if vmax == 4095:
+        raws.append(synth.generate(synth.SceneSpec(*shape, "u16", n_cells=40, seed=seed), 1, synth.CELL))
+    for raw in raws:
+        q1, q2, fx = _q_exact_and_fast(raw, ANISO, sigma, path=2)
+        assert fx[1] == 0
+        assert fx[0] < 0.001 * raw.numel(), fx
+        assert torch.equal(q1, q2), f"{int((q1 != q2).sum())} voxels differ; flagged {fx[0]}"
+
+
 def test_tensor_core_k1_rejects_unfit_shape(cuda):
     """path 2 (tensor cores only) on a shape the TC kernels do not cover is an
     error, not a silent fallback; path 0 falls back to the FP64 FMA kernels."""
