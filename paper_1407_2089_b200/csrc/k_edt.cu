@@ -14,7 +14,7 @@
 //            sites are sparse after pass x (only columns that hold foreground),
 //            so each thread's stack lives in SMEM (global spill past 16).
 //                                                           2 B in, 4 B (dj,di) out
-//   pass z : per (i,j) line along the contiguous k (nz in {32, 64, 96}): one
+//   pass z : per (i,j) line along the contiguous k (nz in {32, 64, 96, 128}): one
 //            thread streams its line from global memory, builds the envelope
 //            of (di*dx)^2 + (dj*dy)^2 + ((k-q)*dz)^2 with its stack in SMEM,
 //            computes the switch points per entry, then sweeps the voxels
@@ -735,21 +735,23 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         const unsigned gb = (unsigned)((ly + LT - 1) / LT);
         // build prefetch depth 16 (measured on C2: 8 -> 115 us, 16 -> 95, 32 -> 107, 64 -> 126)
         auto yb = nz == 64 ? edt_y_build<64, 16> : nz == 32 ? edt_y_build<32, 16> : nz == 96 ? edt_y_build<96, 16>
-                                                                                             : edt_y_build<0, 16>;
-        auto yo = nz == 64 ? edt_y_out<64> : nz == 32 ? edt_y_out<32> : nz == 96 ? edt_y_out<96> : edt_y_out<0>;
+                  : nz == 128 ? edt_y_build<128, 16> : edt_y_build<0, 16>;
+        auto yo = nz == 64 ? edt_y_out<64> : nz == 32 ? edt_y_out<32> : nz == 96 ? edt_y_out<96>
+                  : nz == 128 ? edt_y_out<128> : edt_y_out<0>;
         yb<<<(unsigned)((ly + LTB - 1) / LTB), LTB, 0, s>>>(di, ly, (int)ny, (int)nz, dx, dy, head, spill, kc, swh, est);
         if (int st = ct::check_launch("edt_y_build")) return st;
         yo<<<dim3(gb, YS), LT, 0, s>>>(di, ly, (int)ny, (int)nz, head, spill, kc, swh, est, pk);
         if (int st = ct::check_launch("edt_y_out")) return st;
     }
     const size_t sm = zsmem((int)nz);
-    if ((nz == 64 || nz == 32 || nz == 96) && ((uintptr_t)pk & 15) == 0) {
+    if ((nz == 64 || nz == 32 || nz == 96 || nz == 128) && ((uintptr_t)pk & 15) == 0) {
         // (tried: the SMEM-staged thread-per-line form, and a 4-voxel distance phase over SMEM-staged lines
         // with packed offsets or float64 costs -- 468 / 490 / 654 us vs 307 for this register-streamed form)
         const unsigned g = (unsigned)((lz + ZRT - 1) / ZRT);
         if (nz == 64) edt_pass_zr<64, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
         else if (nz == 32) edt_pass_zr<32, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
-        else edt_pass_zr<96, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
+        else if (nz == 96) edt_pass_zr<96, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
+        else edt_pass_zr<128, 16><<<g, ZRT, 0, s>>>(pk, lz, dx, dy, dz, out);
         return ct::check_launch("edt_pass_z");
     }
     if (nz > 128) {

@@ -753,8 +753,7 @@ bool ct_gaussian_q_tc_fits(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx
 // K1 fast-path selection (per call): 0 auto (tensor cores when the shape
 // fits, else FP64 FMA), 1 FP64 FMA, 2 tensor cores only.
 extern "C" int ct_k1_path(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz, int path) {
-    // auto: u8 only for now (u16 flags too many voxels for the exact fix-up at 32-bit intermediates)
-    if ((path == 2 || (path == 0 && dtype == CT_U8)) && ct_gaussian_q_tc_fits(dtype, nx, ny, nz, rx, ry, rz)) return 2;
+    if (path != 1 && ct_gaussian_q_tc_fits(dtype, nx, ny, nz, rx, ry, rz)) return 2;
     return 1;
 }
 
@@ -778,7 +777,7 @@ extern "C" int ct_gaussian_q(const void *raw, int dtype, int64_t nx, int64_t ny,
                                     stream);
     }
     // tensor-core path (k_gauss_tc.cu) unless disabled or the shape does not fit
-    if (path == 2 || (path == 0 && dtype == CT_U8)) {
+    if (path != 1) {
         const int st = ct_gaussian_q_tc(raw, dtype, nx, ny, nz, w, rx, ry, rz, work, q_out, fix, fix_cap,
                                         eps_override, s);
         if (st == CT_OK) {

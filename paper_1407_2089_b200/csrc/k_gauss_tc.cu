@@ -71,14 +71,16 @@ __global__ void __launch_bounds__(256) tc_vmax(const uint4 *__restrict__ raw, lo
 // ---------------------------------------------------------------------------
 // Setup: integer taps and the certified error bound (one warp per axis).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int rx, int ry, int rz, int u8,
+__global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int rx, int ry, int rz, int u8, int np,
                                                double eps_override, TcParams *prm) {
     // warp a handles axis a: lane-parallel taps, warp reductions
     const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned vm = u8 ? 255u : prm->vmax;  // tc_vmax ran before (u16)
     const double vmax = (double)vm;
-    // P <= vmax (1 + (2r+1) 2^-fw) < 2^bits(vmax): 32 - bits integer bits left for the fraction
-    const int fd = min(FD, max(16, 32 - (vm ? 32 - __clz(vm) : 0)));
+    // P <= vmax (1 + (2r+1) 2^-fw) < 2^bits(vmax): 8 np - bits integer bits left for the fraction
+    // (4 planes: <= 24; 5 planes: <= 28 -- 12-bit data keeps 28, full 16-bit 24)
+    const int fd = min(np == 4 ? FD : 28, max(16, 8 * np - (vm ? 32 - __clz(vm) : 0)));
+    const int lop = np - 2;  // kept limb pairs a + b >= lop
     const int rr[3] = {rx, ry, rz};
     const double *ws = a == 0 ? w : (a == 1 ? w + rx + 1 : w + rx + 1 + ry + 1);
     const int r = rr[a];
@@ -86,10 +88,11 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
     for (int j = lane; j <= r; j += 32) wmax = fmax(wmax, ws[j]);
     for (int o = 16; o; o >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
     wmax *= 1.0000001;
-    int fw = FW;
+    // pass z: fw <= 36 keeps the edge tail sums < 2^35 (16 pieces < 2^32, see tc_pass_z)
+    int fw = a == 2 ? 36 : FW;
     while (fw > 24 && wmax * ldexp(1.0, fw) >= 4294967295.0) --fw;
     const double scale = ldexp(1.0, fw);
-    double dq = 0.0, qsum0 = 0.0, qsum1 = 0.0;
+    double dq = 0.0, qsum[3] = {0.0, 0.0, 0.0};  // qsum[b] = sum_j |limb b of Q_j| over taps -r..r
     for (int j = lane; j < PMAX; j += 32) {
         long long q = 0;
         if (j <= r) {
@@ -97,21 +100,25 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
             q = __double2ll_rn(x);
             const double mult = j ? 2.0 : 1.0;  // taps -j and +j
             dq += mult * fabs((double)q - x);   // exact difference
-            qsum0 += mult * (double)(q & 0xff);
-            qsum1 += mult * (double)((q >> 8) & 0xff);
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb) qsum[bb] += mult * (double)((q >> (8 * bb)) & 0xff);
         }
         prm->Q[a][j] = q;
     }
     for (int o = 16; o; o >>= 1) {
         dq += __shfl_xor_sync(0xffffffffu, dq, o);
-        qsum0 += __shfl_xor_sync(0xffffffffu, qsum0, o);
-        qsum1 += __shfl_xor_sync(0xffffffffu, qsum1, o);
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) qsum[bb] += __shfl_xor_sync(0xffffffffu, qsum[bb], o);
     }
     // per-axis bound: weight rounding sum_j |Q_j 2^-fw - w_j| * max input (the
     // inputs of passes y, z are bounded by vmax up to the taps' sum rounding)
-    // plus, for y and z, the dropped limb pairs (a+b <= 1: (0,0), (1,0), (0,1))
+    // plus, for y and z, the dropped limb pairs a + b < lop (data limbs <= 255)
     double b = dq / scale * vmax * 1.001;
-    if (a > 0) b += 255.0 * (qsum0 * ldexp(1.0, -fw - fd) + (qsum0 + qsum1) * ldexp(1.0, 8 - fw - fd));
+    if (a == 2)  // pass z: every output column also holds 32 edge-tap pieces (limbs <= 255)
+        for (int bb = 0; bb < 3; ++bb) qsum[bb] += 32.0 * 255.0;
+    if (a > 0)
+        for (int da = 0; da < lop; ++da)
+            for (int bb = 0; da + bb < lop; ++bb) b += 255.0 * qsum[bb] * ldexp(1.0, 8 * (da + bb) - fw - fd);
     __shared__ double bs[3];
     __shared__ int fws[3];
     if (lane == 0) {
@@ -123,15 +130,19 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
     if (threadIdx.x == 0) {
         prm->fd = fd;
         prm->vmax = vm;
-        const int zs = fws[2] + fd - 16;  // scale bits of the final sum
+        const int zs = fws[2] + fd - 8 * lop;  // scale bits of the final sum
         double bound = bs[0] + bs[1] + bs[2];
         bound += 2.0 * ldexp(1.0, -fd);                               // truncation of P1, P2
-        bound += 4.0 * ldexp(1.0, -zs);                               // floor of pass z edge terms
         bound += 4.0 * (rx + ry + rz + 12) * ldexp(1.0, -53) * vmax;  // scipy float64 order + residual
         prm->eps = (long long)ceil(bound * 1.25 * ldexp(1.0, zs)) + 16;
         if (eps_override > 0.0) prm->eps = (long long)ceil(eps_override * ldexp(1.0, zs));
     }
 }
+
+// lowest kept limb-pair sum (data limb a + weight limb b) for NP data planes:
+// 4 planes (u8: 24 fractional bits) keep a + b >= 2, 5 planes (u16: 40-bit
+// intermediates, 24-28 fractional bits) keep a + b >= 3; both 5 accumulators
+__host__ __device__ constexpr int lo_pair(int np) { return np == 1 ? 0 : np - 2; }
 
 __device__ __forceinline__ uint32_t limb(long long q, int b) { return (uint32_t)((q >> (8 * b)) & 0xff); }
 
@@ -150,17 +161,19 @@ __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, u
 // 8b; output S >> 11) or 4 (byte planes of P1; pairs a+b >= 2, accumulator
 // a+b-2, shift 8(a+b-2); output S >> 19).  Volume viewed as [outer][L][inner].
 // ---------------------------------------------------------------------------
-template <int NPIN, int STAGES, int TN>  // TN: columns per tile (32 or 64)
+// NPIN = 5 (u16 frames): 40-bit intermediates, pairs a + b >= 3 (lo_pair), still 5 accumulators.
+template <int NPIN, int STAGES, int TN, int NPO = 4>  // TN: columns per tile (32 or 64); NPO: output planes
 __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ in, long long plane_in, int L,
                                                      int inner, int outer, const TcParams *__restrict__ prm, int axis,
                                                      int r, uint8_t *__restrict__ out, long long plane_out) {
     constexpr int NACC = NPIN == 1 ? 4 : 5;
+    constexpr int LOP = lo_pair(NPIN);
     constexpr uint32_t LBO = (TN / 16) * 128, SBO = 128;                // MN-major B
     constexpr int BUF = KXY * TN;                                       // bytes per plane per buffer
     constexpr int OROW = TN + 16;                                       // padded output row (bytes)
     constexpr int CPR = TN / 16;                                        // 16-byte chunks per row
     constexpr int CW = TN / 4;                                          // columns per thread (epilogue)
-    constexpr int OBUF = 4 * TM * OROW;                                 // output tile: [4 planes][128 rows]
+    constexpr int OBUF = NPO * TM * OROW;                               // output tile: [NPO planes][128 rows]
     extern __shared__ __align__(1024) uint8_t sm[];                     // [STAGES][NPIN][BUF], [2][OBUF]
     uint8_t *sout = sm + STAGES * NPIN * BUF;
     __shared__ uint32_t tbase;
@@ -179,7 +192,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     __syncthreads();
     tc::fence_after();
     // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
-    const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 16;
+    const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * LOP;
     const uint32_t base = tbase;
     const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
     // A (taps) into TMEM columns [0, 256): limb b = cg at 64 b; row m
@@ -217,10 +230,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         int o, ti, cb;
         tile_coords(tile, o, ti, cb);
 #pragma unroll
-        for (int q2 = 0; q2 < 4 * TM * CPR / NT; ++q2) {
+        for (int q2 = 0; q2 < (NPO * TM * CPR + NT - 1) / NT; ++q2) {
             const int e = t + NT * q2, a = e / (CPR * TM), mm = (e / CPR) & (TM - 1), hh = e % CPR;
             const int i = ti * TM + mm;
-            if (i < L)
+            if (e < NPO * TM * CPR && i < L)
                 *(uint4 *)(out + a * plane_out + ((long long)o * L + i) * inner + (long long)cb * TN + 16 * hh) =
                     *(const uint4 *)(ob + (a * TM + mm) * OROW + 16 * hh);
         }
@@ -261,7 +274,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
             for (int a = 0; a < NPIN; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    const int acc = NPIN == 1 ? b : a + b - 2;
+                    const int acc = NPIN == 1 ? b : a + b - LOP;
                     if (acc < 0) continue;
 #pragma unroll
                     for (int ks = 0; ks < KXY / 32; ++ks)
@@ -313,19 +326,22 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         uint8_t *ob = sout + (int)(k & 1) * OBUF;
 #pragma unroll
         for (int g8 = 0; g8 < CW; g8 += 8) {
-            uint32_t ov[8];
+            uint32_t ov[8], o4[2] = {0u, 0u};
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 long long S = 0;
 #pragma unroll
                 for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][g8 + c] << (8 * acc);
-                ov[c] = (uint32_t)(S >> shift_out);
+                const unsigned long long o = (unsigned long long)(S >> shift_out);
+                ov[c] = (uint32_t)o;
+                if constexpr (NPO == 5) o4[c >> 2] |= (uint32_t)((o >> 32) & 0xff) << (8 * (c & 3));
             }
             uint32_t lo[4], hi[4];
             planes4(ov[0], ov[1], ov[2], ov[3], lo);
             planes4(ov[4], ov[5], ov[6], ov[7], hi);
 #pragma unroll
             for (int a = 0; a < 4; ++a) *(uint2 *)(ob + (a * TM + m) * OROW + h + g8) = make_uint2(lo[a], hi[a]);
+            if constexpr (NPO == 5) *(uint2 *)(ob + (4 * TM + m) * OROW + h + g8) = make_uint2(o4[0], o4[1]);
         }
     }
     __syncthreads();
@@ -363,7 +379,7 @@ __device__ __forceinline__ void epi_bar() {  // named barrier 1: the epilogue wa
 // of twice the width -- column 2c holds the low bytes of voxel c, column
 // 2c + 1 the high bytes, so the MMA yields both limb sums and the epilogue
 // combines S(c) = D[2c] + 256 D[2c + 1] (no de-interleave pass).
-template <int NPIN, int TN, int SSTG, int ASTG, int DB = 1>
+template <int NPIN, int TN, int SSTG, int ASTG, int DB = 1, int NPO = 4>
 __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant__ CUtensorMap tmap, int L, int inner,
                                                           int outer, const TcParams *__restrict__ prm, int axis, int r,
                                                           uint8_t *__restrict__ out, long long plane_out) {
@@ -377,7 +393,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     constexpr int CW = TN / 4;                      // (byte) columns per epilogue thread (4 column groups)
     constexpr int TV = TN / DB;                     // voxels per tile row
     constexpr int OROW = TV + 16;                   // padded staged output row (bytes)
-    constexpr int OBUF = 4 * TM * OROW;             // staged output tile: [4 planes][128 rows]
+    constexpr int OBUF = NPO * TM * OROW;           // staged output tile: [NPO planes][128 rows]
     constexpr int CPR = TV / 16;                    // 16-byte chunks per output row
     const long long inner_v = inner / DB;           // voxels per input row
     static_assert(256 + ASTG * NACC * TN <= 512, "TMEM: band + accumulator sets");
@@ -494,7 +510,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                 for (int da = 0; da < NPIN; ++da)
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
-                        const int acc = NPIN == 1 ? b : da + b - 2;
+                        const int acc = NPIN == 1 ? b : da + b - lo_pair(NPIN);
                         if (acc < 0) continue;
 #pragma unroll
                         for (int ks = 0; ks < KXY / 32; ++ks)
@@ -513,15 +529,15 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
         const int h = CW * cg;
         const int et = t - 64;  // 0 .. 32 * WS_EPI - 1
         // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
-        const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 16;
-        // coalesced store of a staged output tile: 4 planes x 128 rows x TV bytes
+        const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * lo_pair(NPIN);
+        // coalesced store of a staged output tile: NPO planes x 128 rows x TV bytes
         auto flush = [&](long long k, const uint8_t *ob) {
             int o, ti, cb;
             coords(k, o, ti, cb);
 #pragma unroll
-            for (int q2 = 0; q2 < (4 * TM * CPR + 32 * WS_EPI - 1) / (32 * WS_EPI); ++q2) {
+            for (int q2 = 0; q2 < (NPO * TM * CPR + 32 * WS_EPI - 1) / (32 * WS_EPI); ++q2) {
                 const int e = et + 32 * WS_EPI * q2;
-                if (e >= 4 * TM * CPR) break;
+                if (e >= NPO * TM * CPR) break;
                 const int pa = e / (CPR * TM), mm = (e / CPR) % TM, hh = e % CPR;
                 const int i = ti * TM + mm;
                 if (i < L)
@@ -552,7 +568,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
             uint8_t *ob = sout + (int)(k & 1) * OBUF;
 #pragma unroll
             for (int g4 = 0; g4 < CW; g4 += 4 * DB) {
-                uint32_t ov[4];
+                uint32_t ov[4], o4 = 0;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     long long S = 0;
@@ -562,12 +578,15 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                         if constexpr (DB == 2) d += (long long)v[acc][g4 + 2 * c + 1] << 8;
                         S += d << (8 * acc);
                     }
-                    ov[c] = (uint32_t)(S >> shift_out);
+                    const unsigned long long o = (unsigned long long)(S >> shift_out);
+                    ov[c] = (uint32_t)o;
+                    if constexpr (NPO == 5) o4 |= (uint32_t)((o >> 32) & 0xff) << (8 * c);
                 }
                 uint32_t pl[4];
                 planes4(ov[0], ov[1], ov[2], ov[3], pl);
 #pragma unroll
                 for (int pa = 0; pa < 4; ++pa) *(uint32_t *)(ob + (pa * TM + m) * OROW + (h + g4) / DB) = pl[pa];
+                if constexpr (NPO == 5) *(uint32_t *)(ob + (4 * TM + m) * OROW + (h + g4) / DB) = o4;
             }
             epi_bar();  // tile k staged (and tile k-1's flush, issued before, finished by every thread)
             flush(k, ob);
@@ -580,37 +599,48 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
-// Pass z + residual + quantisation + certification.  NZ in {32, 64}.  The
+// Pass z + residual + quantisation + certification.  NZ in {32, 64, 96}.  The
 // whole line is one tile: the MMA applies the taps that land inside the line
-// (B[n][k] = Q_|k-n|); the taps beyond either end all read the edge value
-// (mode "nearest"), so the epilogue adds x[0] E0[n] + x[nz-1] EL[n] with the
-// integer tail sums E0[n] = sum_{j < -n} Q_|j|, EL[n] = sum_{j > nz-1-n} Q_j.
+// (B[n][k] = Q_|k-n|), and the taps beyond either end, which all read the
+// edge value (mode "nearest"), come from one more K = 32 block: A holds the
+// line's edge values x0 (16 slots) and x_{nz-1} (16 slots) -- written into
+// TMEM by the line's owner thread, so no SMEM and no proxy fence -- and B the
+// tail sums E0[n] = sum_{j > n} Q_j and EL[n] = sum_{j >= nz-n} Q_j split into
+// 16 pieces < 2^32 each (fw_z <= 36 keeps E < 2^35).  The epilogue is then
+// pure accumulator arithmetic:
+//   S = sum_acc v[acc] 2^(8 acc),  V = S - 2^(zs-1)
+//   q = max(raw - ceil(V / 2^zs), 0)                  (= rint(max(raw - bg, 0)))
+//   flag iff (eps - V) mod 2^zs <= 2 eps and raw 2^zs - V >= 2^zs - eps
 // ---------------------------------------------------------------------------
-template <int NZ, int STAGES, typename Traw = uint8_t>
+template <int NZ, int STAGES, typename Traw = uint8_t, int NP = 4>  // NP: planes of P2 (4, or 5 for u16)
 __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ in, long long plane, long long nlines,
                                                     const TcParams *__restrict__ prm, int r,
                                                     const Traw *__restrict__ raw, Traw *__restrict__ q,
                                                     unsigned long long *__restrict__ fix, long long cap) {
     constexpr int RB = (int)sizeof(Traw);       // raw / q bytes per voxel
     constexpr int VPW = 4 / RB;                 // voxels per 32-bit word
+    constexpr int LOP = lo_pair(NP), SPL = 8 * LOP;  // kept pairs a + b >= LOP; S has scale 2^(fd + fw - SPL)
     static_assert(NZ <= 64 || RB == 1, "u16 pass z: nz in {32, 64}");
     constexpr int NCH = NZ / 16;                // 16-byte chunks per line
-    constexpr uint32_t LBO = 128, SBO = NCH * 128;
+    constexpr uint32_t LBO = 128, SBO = NCH * 128, SBOE = 256;  // K-major: data / taps (K = NZ), edge block (K = 32)
     constexpr int ABUF = TM * NZ;               // bytes per plane per buffer
     constexpr int RBUF = ABUF * RB;             // bytes of a raw / q tile
     constexpr int BW = NZ * NZ;                 // bytes per weight limb
-    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [STAGES][4][ABUF] data, [STAGES][RBUF] raw,
-                                                     // [2][RBUF] q tile
+    constexpr int BE = NZ * 32;                 // bytes per weight limb, edge block
+    constexpr int ACOL = 5 * NZ;                // TMEM: accumulators [0, ACOL), edge A slots after
+    static_assert(ACOL + NP * 8 <= 512, "TMEM");
+    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [4][BE] edge taps, [STAGES][NP][ABUF] data,
+                                                     // [STAGES][RBUF] raw, [2][RBUF] q tile
     uint8_t *sw = sm;
-    uint8_t *sa = sm + 4 * BW;
-    uint8_t *sr = sa + STAGES * 4 * ABUF;
+    uint8_t *swe = sm + 4 * BW;
+    uint8_t *sa = swe + 4 * BE;
+    uint8_t *sr = sa + STAGES * NP * ABUF;
     uint8_t *sq = sr + STAGES * RBUF;
     const uint8_t *rawb = (const uint8_t *)raw;
     uint8_t *qb8 = (uint8_t *)q;
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
     __shared__ long long Qs[PMAX], Ts[PMAX + 1];
-    __shared__ uint4 Et[NZ];  // edge tail sums split at 2^16: {E0 >> 16, E0 & 0xffff, EL >> 16, EL & 0xffff}
     const int t = threadIdx.x, wp = t >> 5, m = t & (TM - 1), cg = t >> 7;
     if (wp == 0) tc::tmem_alloc(&tbase, 512);
     for (int j = t; j < PMAX; j += NT) Qs[j] = j <= r ? prm->Q[2][j] : 0;
@@ -626,7 +656,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         for (int j = PMAX - 1; j >= 0; --j) Ts[j] = Ts[j + 1] + Qs[j];
     }
     __syncthreads();
-    // taps inside the line, K-major; edge tail sums
+    // taps inside the line, K-major; edge taps: B[s][n] = piece s of E0[n] (s < 16) / of EL[n] (s >= 16)
     for (int e = t; e < NZ * NZ; e += NT) {
         const int n = e / NZ, k = e - n * NZ;
         const int d = k > n ? k - n : n - k;
@@ -634,16 +664,20 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
 #pragma unroll
         for (int b = 0; b < 4; ++b) sw[b * BW + tc::kmajor_off(n, k, LBO, SBO)] = (uint8_t)limb(qv, b);
     }
-    for (int n = t; n < NZ; n += NT) {
-        const long long e0 = n + 1 <= PMAX ? Ts[n + 1] : 0, el = NZ - n <= PMAX ? Ts[NZ - n] : 0;
-        Et[n] = make_uint4((uint32_t)(e0 >> 16), (uint32_t)(e0 & 0xffff), (uint32_t)(el >> 16), (uint32_t)(el & 0xffff));
+    for (int e = t; e < NZ * 32; e += NT) {
+        const int n = e >> 5, sl = e & 31, s16 = sl & 15;
+        const long long E = sl < 16 ? (n + 1 <= PMAX ? Ts[n + 1] : 0) : (NZ - n <= PMAX ? Ts[NZ - n] : 0);
+        const long long pc = E / 16 + (s16 < E % 16 ? 1 : 0);  // < 2^32
+#pragma unroll
+        for (int b = 0; b < 4; ++b) swe[b * BE + tc::kmajor_off(n, sl, LBO, SBOE)] = (uint8_t)limb(pc, b);
     }
     const long long eps = prm->eps;
-    const int zs = prm->fw[2] + prm->fd - 16;  // S has scale 2^zs
+    const int zs = prm->fw[2] + prm->fd - SPL;  // S has scale 2^zs
     const long long half = 1ll << (zs - 1), one = 1ll << zs, fmask = one - 1;
     const uint32_t base = tbase;
     const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
     const long long ntiles = (nlines + TM - 1) / TM;
+    const long long t0 = blockIdx.x, gs = gridDim.x;
     const uint32_t idesc = tc::idesc_i8(TM, NZ, false, false, false, false);
 
     // data planes (K-major canonical) and raw (plain) of a tile via cp.async
@@ -655,8 +689,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
             const int e = t + NT * q2, l = e / NCH, c = e - l * NCH;
             if (e < TM * NCH && l < nl) {
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
-                    tc::cp_async16(sa + (buf * 4 + a) * ABUF + tc::kmajor_off(l, 16 * c, LBO, SBO),
+                for (int a = 0; a < NP; ++a)
+                    tc::cp_async16(sa + (buf * NP + a) * ABUF + tc::kmajor_off(l, 16 * c, LBO, SBO),
                                    in + a * plane + (l0 + l) * NZ + 16 * c);
 #pragma unroll
                 for (int j = 0; j < RB; ++j)
@@ -666,6 +700,29 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         }
         tc::cp_commit();
     };
+    // edge A block of tile k (TMEM columns ACOL + 8 a): the owner thread of
+    // line m (warps 0-3, one per TMEM lane quarter) loads the line's two edge
+    // values of every plane and stores them as 16 + 16 byte slots -- between
+    // the completion of MMA(k-1) and the barrier before MMA(k) is issued, so
+    // one copy suffices
+    uint8_t ex[2 * NP];
+    auto edge_load = [&](long long k) {
+        const long long l = (t0 + k * gs) * TM + m;
+#pragma unroll
+        for (int a = 0; a < NP; ++a) {
+            ex[2 * a] = l < nlines ? in[a * plane + l * NZ] : 0;
+            ex[2 * a + 1] = l < nlines ? in[a * plane + l * NZ + NZ - 1] : 0;
+        }
+    };
+    auto edge_store = [&]() {
+#pragma unroll
+        for (int a = 0; a < NP; ++a) {
+            const uint32_t w0 = 0x01010101u * ex[2 * a], wl = 0x01010101u * ex[2 * a + 1];
+            const uint32_t v[8] = {w0, w0, w0, w0, wl, wl, wl, wl};
+            tc::tmem_st8(lane_addr + ACOL + a * 8, v);
+        }
+        tc::tmem_st_wait();
+    };
 
     // coalesced store of a staged q tile (lines are contiguous in global)
     auto flush = [&](long long tile, const uint8_t *qb) {
@@ -674,25 +731,28 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         for (int e = 16 * t; e < nbytes; e += 16 * NT) *(uint4 *)(qb8 + l0 * NZ * RB + e) = *(const uint4 *)(qb + e);
     };
     // same software pipeline as tc_pass_xy
-    const long long t0 = blockIdx.x, gs = gridDim.x;
     const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
     auto issue = [&](long long k) {
         if (wp != 0) return;
-        const uint64_t a0 = tc::smem_desc(tc::smem_u32(sa + (int)(k % STAGES) * 4 * ABUF), LBO, SBO);
+        const uint64_t a0 = tc::smem_desc(tc::smem_u32(sa + (int)(k % STAGES) * NP * ABUF), LBO, SBO);
         const uint64_t b0 = tc::smem_desc(tc::smem_u32(sw), LBO, SBO);
+        const uint64_t be = tc::smem_desc(tc::smem_u32(swe), LBO, SBOE);
+        const uint32_t ae = base + ACOL;
         if (tc::elect_one()) {
             bool first[5] = {true, true, true, true, true};
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < NP; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    const int acc = a + b - 2;
+                    const int acc = a + b - LOP;
                     if (acc < 0) continue;
 #pragma unroll
                     for (int ks = 0; ks < NZ / 32; ++ks)
                         tc::mma_i8_ss(base + NZ * acc, a0 + (uint64_t)((a * ABUF + ks * 2 * LBO) >> 4),
                                       b0 + (uint64_t)((b * BW + ks * 2 * LBO) >> 4), idesc,
                                       first[acc] && ks == 0 ? 0u : 1u);
+                    // the edge taps: A from TMEM (8 columns = 32 K bytes per plane)
+                    tc::mma_i8_ts(base + NZ * acc, ae + a * 8, be + (uint64_t)((b * BE) >> 4), idesc, 1u);
                     first[acc] = false;
                 }
             tc::mma_commit(&mbar);
@@ -705,6 +765,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         else tc::cp_commit();
     }
     if (nmine > 0) {
+        if (cg == 0) {
+            edge_load(0);
+            edge_store();
+        }
         tc::cp_wait_group<STAGES - 1>();
         tc::fence_async_smem();
         tc::fence_before();
@@ -715,42 +779,30 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     uint32_t phase = 0;
     constexpr int CW = NZ / 4;  // columns per thread
     const int h0 = cg * CW;
-    // q of one voxel (column h0 + c of line l) from its 5 accumulator words,
-    // the raw byte and the line's edge values; flags it for the fix-up
-    auto qbyte = [&](const uint32_t v0, const uint32_t v1, const uint32_t v2, const uint32_t v3, const uint32_t v4,
-                     int c, uint32_t raw8, uint32_t x0, uint32_t xl, long long l) -> uint32_t {
-        // S = sum_acc v[acc] 2^(8 acc) (IMAD.WIDE chain) + edge taps
-        const uint4 e = Et[h0 + c];
-        const unsigned long long lo = (unsigned long long)x0 * e.y + (unsigned long long)xl * e.w;
-        unsigned long long S = (unsigned long long)v0 + (unsigned long long)v1 * 0x100ull +
-                               (unsigned long long)v2 * 0x10000ull + (unsigned long long)v3 * 0x1000000ull +
-                               ((unsigned long long)v4 << 32);
-        S += (unsigned long long)x0 * e.x + (unsigned long long)xl * e.z + (lo >> 16);
-        // T = R + 2^(zs-1), R = raw 2^zs - S: q = max(T, 0) >> zs; the
-        // rounding boundaries R = (k + 1/2) 2^zs (k >= 0) are T = (k+1) 2^zs,
-        // flagged when T is within eps of one of them
-        const long long T = (long long)(((unsigned long long)raw8 << zs) - S) + half;
-        const uint32_t qv = T > 0 ? (uint32_t)(T >> zs) : 0u;  // <= raw8
-        if (T >= one - eps && ((T + eps) & fmask) <= 2 * eps) {
+    // q of one voxel (column h0 + c of line l) from its 5 accumulator words
+    // and the raw value; flags it for the fix-up
+    auto qval = [&](const uint32_t v0, const uint32_t v1, const uint32_t v2, const uint32_t v3, const uint32_t v4,
+                    int c, uint32_t rv, long long l) -> uint32_t {
+        const unsigned long long S = (unsigned long long)v0 + (unsigned long long)v1 * 0x100ull +
+                                     (unsigned long long)v2 * 0x10000ull + (unsigned long long)v3 * 0x1000000ull +
+                                     ((unsigned long long)v4 << 32);
+        const long long V = (long long)S - half;
+        const int bgq = (int)((V + fmask) >> zs);  // ceil(V / 2^zs): the background rounded for this raw grid
+        const int qv = (int)rv - bgq;
+        // rounding boundaries of raw - bg at half-integers k + 1/2 (k >= 0):
+        // T = raw 2^zs - V within eps of a multiple of 2^zs, T >= 2^zs - eps
+        if ((unsigned long long)((eps - V) & fmask) <= (unsigned long long)(2 * eps) &&
+            ((long long)rv << zs) - V >= one - eps) {
             const unsigned long long at = atomicAdd(&fix[0], 1ull);
             if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
             else fix[1] = 1;
         }
-        return qv;
-    };
-    auto edges = [&](long long k, uint32_t &x0, uint32_t &xl) {
-        const uint8_t *ab = sa + (int)(k % STAGES) * 4 * ABUF;
-        const uint32_t o0 = tc::kmajor_off(m, 0, LBO, SBO), ol = tc::kmajor_off(m, NZ - 1, LBO, SBO);
-        x0 = xl = 0;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            x0 |= (uint32_t)ab[a * ABUF + o0] << (8 * a);
-            xl |= (uint32_t)ab[a * ABUF + ol] << (8 * a);
-        }
+        return qv > 0 ? (uint32_t)qv : 0u;
     };
     if constexpr (NZ <= 64) {
-    // accumulators -> registers, barrier, MMA(k+1), then the epilogue of k
+    // accumulators -> registers, edges of tile k+1, barrier, MMA(k+1), then the epilogue of k
     for (long long k = 0; k < nmine; ++k) {
+        if (cg == 0 && k + 1 < nmine) edge_load(k + 1);
         tc::mbar_wait(&mbar, phase);
         phase ^= 1;
         tc::fence_after();
@@ -761,14 +813,13 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
             for (int g8 = 0; g8 < CW; g8 += 8)
                 tc::tmem_ld8(lane_addr + NZ * acc + h0 + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
         tc::tmem_ld_wait();
-        // raw and the line's edge values of tile k (slot k % STAGES) before the slot is restaged
+        if (cg == 0 && k + 1 < nmine) edge_store();  // MMA(k) has completed, MMA(k+1) not yet issued
+        // raw of tile k (slot k % STAGES) before the slot is restaged
         const long long l = (t0 + k * gs) * TM + m;
         const uint8_t *rl = sr + (int)(k % STAGES) * RBUF + (m * NZ + h0) * RB;
         uint32_t rw[CW / VPW];
 #pragma unroll
         for (int c4 = 0; c4 < CW / VPW; ++c4) rw[c4] = *(const uint32_t *)(rl + 4 * c4);
-        uint32_t x0, xl;
-        edges(k, x0, xl);
         tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
         tc::fence_async_smem();
         tc::fence_before();
@@ -785,8 +836,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         if (l < nlines) {
 #pragma unroll
             for (int c = 0; c < CW; ++c)
-                qw[c / VPW] |= qbyte(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], c,
-                                     (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM, x0, xl, l)
+                qw[c / VPW] |= qval(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], c,
+                                    (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM, l)
                                << (8 * RB * (c % VPW));
         }
         uint8_t *qb = sq + (int)(k & 1) * RBUF + (m * NZ + h0) * RB;
@@ -797,13 +848,12 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     // long lines (NZ = 96): the accumulators do not fit in registers at once,
     // so the epilogue drains them in 8-column chunks before MMA(k+1) is issued
     for (long long k = 0; k < nmine; ++k) {
+        if (cg == 0 && k + 1 < nmine) edge_load(k + 1);
         tc::mbar_wait(&mbar, phase);
         phase ^= 1;
         tc::fence_after();
         const long long l = (t0 + k * gs) * TM + m;
         const uint8_t *rl = sr + (int)(k % STAGES) * ABUF + m * NZ + h0;
-        uint32_t x0, xl;
-        edges(k, x0, xl);
         uint8_t *qb = sq + (int)(k & 1) * ABUF + m * NZ + h0;
 #pragma unroll
         for (int g8 = 0; g8 < CW; g8 += 8) {
@@ -816,11 +866,12 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
             if (l < nlines) {
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
-                    qw[c >> 2] |= qbyte(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], g8 + c,
-                                        ((c < 4 ? r0w : r1w) >> (8 * (c & 3))) & 0xff, x0, xl, l) << (8 * (c & 3));
+                    qw[c >> 2] |= qval(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], g8 + c,
+                                       ((c < 4 ? r0w : r1w) >> (8 * (c & 3))) & 0xff, l) << (8 * (c & 3));
             }
             *(uint2 *)(qb + g8) = make_uint2(qw[0], qw[1]);
         }
+        if (cg == 0 && k + 1 < nmine) edge_store();
         tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
         tc::fence_async_smem();
         tc::fence_before();
@@ -835,6 +886,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     __syncthreads();
     if (nmine > 0) flush(t0 + (nmine - 1) * gs, sq + (int)((nmine - 1) & 1) * RBUF);
     tc::cp_wait_all();
+    tc::fence_before();
     __syncthreads();
     tc::fence_after();
     if (wp == 0) tc::tmem_dealloc(base, 512);
@@ -869,10 +921,13 @@ bool ct_gaussian_q_tc_fits(int dtype, int64_t nx, int64_t ny, int64_t nz, int rx
 
 namespace {
 
+// NP byte planes per intermediate: 4 for u8 (24 fractional bits), 5 for u16
+// (40-bit intermediates: 28 fractional bits for 12-bit data, 24 at full range)
 template <typename Traw>
 int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz, uint8_t *p1,
                   uint8_t *p2, TcParams *prm, Traw *q, unsigned long long *fix, int64_t cap, cudaStream_t s) {
     constexpr int RB = (int)sizeof(Traw);
+    constexpr int NP = RB == 1 ? 4 : 5;
     const long long N = nx * ny * nz;
     // persistent grids: one CTA per SM (capping it to leave SMs to the concurrent vessel stream measured
     // slower: 140 / 132 / 120 SMs -> 1.744 / 1.750 / 1.810 ms per C2 step vs 1.744)
@@ -897,8 +952,8 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
             ct::set_error("tensor map (pass x) rejected");
             return CT_ERR_UNSUPPORTED;
         }
-        auto kx = tc_pass_xy_ws<1, TX, SS, AS, RB>;
-        const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * 4 * TM * (TX / RB + 16) + 1024;
+        auto kx = tc_pass_xy_ws<1, TX, SS, AS, RB, NP>;
+        const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * NP * TM * (TX / RB + 16) + 1024;
         cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = ((nx + TM - 1) / TM) * (ny * nz * RB / TX);
         kx<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tm, (int)nx, (int)(ny * nz * RB), 1, prm, 0,
@@ -910,22 +965,25 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
     // (TN = 32, one accumulator set) / 373 (TN = 16, three sets) on C2: the
     // MMAs read the tap band A from TMEM, and narrower tiles only add MMAs
     {
-        const size_t sm = 5 * 4 * KXY * TNY + 2 * 4 * TM * (TNY + 16) + 1024;
-        cudaFuncSetAttribute(tc_pass_xy<4, 5, TNY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        constexpr int YS = NP == 4 ? 5 : 4;  // operand stages (SMEM: 5 planes x 4 stages + output tiles)
+        auto ky = tc_pass_xy<NP, YS, TNY, NP>;
+        const size_t sm = (size_t)YS * NP * KXY * TNY + 2 * NP * TM * (TNY + 16) + 1024;
+        cudaFuncSetAttribute(ky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TNY);
-        tc_pass_xy<4, 5, TNY><<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(
-            p1, N, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2, N);
+        ky<<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(p1, N, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2,
+                                                                   N);
         if (int st = ct::check_launch("tc_pass_y")) return st;
     }
     // pass z + epilogue
     {
         const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
         const int stg = RB == 2 ? 3 : nz == 96 ? 2 : 4;
-        const size_t sm = 4 * nz * nz + (size_t)stg * (4 * TM * nz + TM * nz * RB) + 2 * TM * nz * RB + 1024;
+        const size_t sm = 4 * nz * nz + 4 * nz * 32 + (size_t)stg * (NP * TM * nz + TM * nz * RB) + 2 * TM * nz * RB +
+                          1024;
         void (*kz)(const uint8_t *, long long, long long, const TcParams *, int, const Traw *, Traw *,
                    unsigned long long *, long long);
         if constexpr (RB == 2)
-            kz = nz == 64 ? tc_pass_z<64, 3, Traw> : tc_pass_z<32, 3, Traw>;
+            kz = nz == 64 ? tc_pass_z<64, 3, Traw, 5> : tc_pass_z<32, 3, Traw, 5>;
         else
             kz = nz == 64 ? tc_pass_z<64, 4, Traw> : nz == 96 ? tc_pass_z<96, 2, Traw> : tc_pass_z<32, 4, Traw>;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -942,8 +1000,9 @@ int ct_gaussian_q_tc(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t
                      cudaStream_t s) {
     if (!ct_gaussian_q_tc_fits(dtype, nx, ny, nz, rx, ry, rz) || ((uintptr_t)raw & 15)) return CT_ERR_UNSUPPORTED;
     const long long N = nx * ny * nz;
-    uint8_t *p1 = (uint8_t *)work, *p2 = p1 + 4 * N;
-    TcParams *prm = (TcParams *)(p2 + 4 * N);
+    const int np = dtype == CT_U8 ? 4 : 5;
+    uint8_t *p1 = (uint8_t *)work, *p2 = p1 + np * N;
+    TcParams *prm = (TcParams *)(p2 + np * N);
     cudaMemsetAsync(fix, 0, 2 * sizeof(unsigned long long), s);
     const bool u8 = dtype == CT_U8;
     if (!u8) {
@@ -951,7 +1010,7 @@ int ct_gaussian_q_tc(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t
         tc_vmax<<<CT_NUM_SMS * 4, 256, 0, s>>>((const uint4 *)raw, N * 2 / 16, prm);  // N * 2 % 16 == 0 (nz % 32)
         if (int st = ct::check_launch("tc_vmax")) return st;
     }
-    tc_prep<<<1, 96, 0, s>>>(w, rx, ry, rz, u8 ? 1 : 0, eps_override, prm);
+    tc_prep<<<1, 96, 0, s>>>(w, rx, ry, rz, u8 ? 1 : 0, np, eps_override, prm);
     if (int st = ct::check_launch("tc_prep")) return st;
     if (u8)
         return gaussian_q_tc<uint8_t>((const uint8_t *)raw, nx, ny, nz, rx, ry, rz, p1, p2, prm, (uint8_t *)q, fix,
@@ -960,6 +1019,6 @@ int ct_gaussian_q_tc(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t
                                    cap, s);
 }
 
-size_t ct_gaussian_q_tc_work(int64_t nx, int64_t ny, int64_t nz) {
-    return (size_t)8 * nx * ny * nz + sizeof(TcParams) + 256;
+size_t ct_gaussian_q_tc_work(int64_t nx, int64_t ny, int64_t nz) {  // <= the 16 N bytes ct_gaussian_q takes
+    return (size_t)10 * nx * ny * nz + sizeof(TcParams) + 256;
 }

@@ -13,6 +13,8 @@
 // pairs are one aligned LDS.32 plus one PRMT each.  The output histogram is
 // accumulated per CTA in SMEM (warp-aggregated with __match_any_sync) and
 // flushed once per persistent CTA.
+#include <type_traits>
+
 #include "ct_common.cuh"
 
 namespace {
@@ -632,6 +634,155 @@ __global__ void __launch_bounds__(128) median_generic(const T *__restrict__ in, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// r >= 2, integer volumes: sliding-window histograms (Huang's running median
+// in 3-D).  A thread owns one (i, j) column and walks k = 0 .. nz-1: the
+// window multiset {in[clamp(i+di), clamp(j+dj), clamp(k+dk)]} moves by one
+// z-plane per step -- (2r+1)^2 values leave, (2r+1)^2 enter, and pairs that
+// leave and enter with the same value (flat background) cost nothing.  The
+// thread's private histogram (u16 counters in SMEM, [bin][thread] so a warp's
+// accesses are conflict-free whatever the bins) and a running (m, #below m)
+// pair give the size^3 // 2 order statistic after a few bin steps.
+//   u8:  256 bins.
+//   u16: the high byte in 256 coarse bins (running median bin h, rank rho
+//        inside it) and a 256-bin fine histogram of the low bytes of the
+//        values in bin h, rebuilt from the window when h moves (rare on
+//        smooth data), with its own running position.
+// A CTA owns NTC consecutive j of one i; the input rows it needs are staged
+// in SMEM per z-chunk of ZC outputs with coalesced loads and an odd word
+// stride per row (the per-thread reads of neighbouring columns hit distinct
+// banks) -- direct global reads were one L1 wavefront per lane.  The output
+// histogram is counted from runs of equal outputs along z.  Same order
+// statistic as median_generic (scipy's rank filter, mode "nearest").
+// ---------------------------------------------------------------------------
+constexpr int SZC = 32;  // outputs per z-chunk
+
+template <typename T, int R>
+struct SlideCfg {
+    static constexpr int D = 2 * R + 1;
+    static constexpr int NTC = sizeof(T) == 1 ? 64 : 32;         // columns (threads) per CTA
+    static constexpr int ZS = SZC + 2 * R + 1;                   // staged z-extent per chunk
+    static constexpr int W0 = (ZS * (int)sizeof(T) + 3) / 4;     // words per staged row
+    static constexpr int RW = W0 | 1;                            // odd word stride
+    static constexpr int ROWS = D * (NTC + 2 * R);               // staged rows
+    static constexpr size_t HIST = (sizeof(T) == 2 ? 2 : 1) * 256 * NTC * 2;
+    static constexpr size_t SMEM = HIST + (size_t)ROWS * RW * 4;
+};
+
+template <typename T, int R>
+__global__ void __launch_bounds__(SlideCfg<T, R>::NTC) median_slide(const T *__restrict__ in, T *__restrict__ out,
+                                                                  i64 nx, i64 ny, i64 nz,
+                                                                  uint64_t *__restrict__ ghist) {
+    using C = SlideCfg<T, R>;
+    constexpr int D = C::D, KTH = D * D * D / 2, NTC = C::NTC, ZS = C::ZS, RW = C::RW;
+    constexpr bool U16 = sizeof(T) == 2;
+    extern __shared__ __align__(16) unsigned char ssm[];
+    uint16_t *hc = (uint16_t *)ssm;                             // [256][NTC] direct (u8) / coarse (u16)
+    uint16_t *hf = hc + 256 * NTC;                              // [256][NTC] fine (u16)
+    uint32_t *stg = (uint32_t *)(ssm + C::HIST);                // [ROWS][RW] words
+    const int t = threadIdx.x;
+    auto H = [&](int b) -> uint16_t & { return hc[b * NTC + t]; };
+    auto F = [&](int b) -> uint16_t & { return hf[b * NTC + t]; };
+    const i64 jt = (ny + NTC - 1) / NTC, ntiles = nx * jt;
+    auto flush_run = [&](int v, unsigned c) {
+        if (ghist && c) atomicAdd((unsigned long long *)&ghist[v], (unsigned long long)c);
+    };
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const i64 i = tile / jt, j0 = (tile - i * jt) * NTC, j = j0 + t;
+        const bool live = j < ny;
+        // staged row (di, dj) of this thread: rows [di][NTC + 2R], column t + dj
+        auto sval = [&](int di, int dj, int u) -> int {  // staged z offset u
+            const T *row = (const T *)(stg + (di * (NTC + 2 * R) + t + dj) * RW);
+            return (int)row[u];
+        };
+        for (int b = 0; b < 256; ++b) H(b) = 0;
+        if constexpr (U16)
+            for (int b = 0; b < 256; ++b) F(b) = 0;
+        int m = 0, below = 0, hcur = 0, mf = 0, belowf = 0;
+        int run_v = -1;
+        unsigned run_n = 0;
+        for (i64 k0 = 0; k0 < nz; k0 += SZC) {
+            // stage z in [k0 - R - 1, k0 - R - 1 + ZS) (clamped) of the tile's rows
+            __syncthreads();
+            const i64 zb = k0 - R - 1;
+            for (int e = t; e < C::ROWS * ZS; e += NTC) {
+                const int r = e / ZS, u = e - r * ZS;
+                const int di = r / (NTC + 2 * R), dj = r - di * (NTC + 2 * R);
+                const i64 ii = ct::clampi(i + di - R, 0, nx - 1), jj = ct::clampi(j0 + dj - R, 0, ny - 1);
+                const i64 kk = ct::clampi(zb + u, 0, nz - 1);
+                ((T *)(stg + r * RW))[u] = in[(ii * ny + jj) * nz + kk];
+            }
+            __syncthreads();
+            if (!live) continue;
+            if (k0 == 0) {  // window of k = 0: z offsets R+1-R .. R+1+R in the chunk
+                for (int dk = 0; dk < D; ++dk)
+#pragma unroll
+                    for (int e = 0; e < D * D; ++e) {
+                        const int v = sval(e / D, e % D, 1 + dk);
+                        ++H(U16 ? v >> 8 : v);
+                        if (U16 && (v >> 8) == 0) ++F(v & 255);
+                    }
+            }
+            const int kend = (int)min((i64)SZC, nz - k0);
+            for (int kc = 0; kc < kend; ++kc) {
+                const i64 k = k0 + kc;
+                if (k > 0) {  // leaves: z = k - 1 - R (offset kc), enters: z = k + R (offset kc + 2R + 1)
+#pragma unroll
+                    for (int e = 0; e < D * D; ++e) {
+                        const int vo = sval(e / D, e % D, kc), vn = sval(e / D, e % D, kc + 2 * R + 1);
+                        if (vo == vn) continue;
+                        const int bo = U16 ? vo >> 8 : vo, bn = U16 ? vn >> 8 : vn;
+                        --H(bo);
+                        ++H(bn);
+                        below += (bn < m) - (bo < m);
+                        if constexpr (U16) {
+                            if (bo == hcur) {
+                                --F(vo & 255);
+                                belowf -= (vo & 255) < mf;
+                            }
+                            if (bn == hcur) {
+                                ++F(vn & 255);
+                                belowf += (vn & 255) < mf;
+                            }
+                        }
+                    }
+                }
+                // the bin holding rank KTH: below <= KTH < below + H(m)
+                while (below + (int)H(m) <= KTH) below += H(m++);
+                while (below > KTH) below -= H(--m);
+                int med = m;
+                if constexpr (U16) {
+                    if (m != hcur) {  // re-describe the fine histogram for the new bin (window z offsets kc+1 ..)
+                        for (int b = 0; b < 256; ++b) F(b) = 0;
+                        for (int dk = 0; dk < D; ++dk)
+#pragma unroll
+                            for (int e = 0; e < D * D; ++e) {
+                                const int v = sval(e / D, e % D, kc + 1 + dk);
+                                if ((v >> 8) == m) ++F(v & 255);
+                            }
+                        hcur = m;
+                        mf = 0;
+                        belowf = 0;
+                    }
+                    const int rho = KTH - below;
+                    while (belowf + (int)F(mf) <= rho) belowf += F(mf++);
+                    while (belowf > rho) belowf -= F(--mf);
+                    med = (m << 8) | mf;
+                }
+                out[(i * ny + j) * nz + k] = (T)med;
+                if (med == run_v) {
+                    ++run_n;
+                } else {
+                    flush_run(run_v, run_n);
+                    run_v = med;
+                    run_n = 1;
+                }
+            }
+        }
+        if (live) flush_run(run_v, run_n);
+    }
+}
+
 // Any radius (> 3: the (2r+1)^3 window no longer fits a per-thread buffer):
 // bitwise radix select of the k-th smallest order-preserving key, one pass
 // over the clamped window per key bit (8 / 16 / 64 for u8 / u16 / f64).
@@ -758,6 +909,23 @@ extern "C" int ct_median(const void *in, int dtype, int64_t nx, int64_t ny, int6
         if (int st = ct::check_launch("median3_f64")) return st;
         if (hist) return ct_histogram(out, dtype, n, hist, stream);
         return CT_OK;
+    }
+    if (radius >= 2 && radius <= 3 && (dtype == CT_U8 || dtype == CT_U16)) {
+        auto launch = [&](auto kern, size_t sm, int ntc, auto *typed_in) {
+            using TT = std::remove_pointer_t<decltype(typed_in)>;
+            const i64 tiles = nx * ((ny + ntc - 1) / ntc);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            kern<<<(unsigned)min(tiles, (i64)CT_NUM_SMS * 16), ntc, sm, s>>>((const TT *)in, (TT *)out, nx, ny, nz,
+                                                                              hist);
+        };
+        if (dtype == CT_U8) {
+            if (radius == 2) launch(median_slide<uint8_t, 2>, SlideCfg<uint8_t, 2>::SMEM, SlideCfg<uint8_t, 2>::NTC, (uint8_t *)nullptr);
+            else launch(median_slide<uint8_t, 3>, SlideCfg<uint8_t, 3>::SMEM, SlideCfg<uint8_t, 3>::NTC, (uint8_t *)nullptr);
+        } else {
+            if (radius == 2) launch(median_slide<uint16_t, 2>, SlideCfg<uint16_t, 2>::SMEM, SlideCfg<uint16_t, 2>::NTC, (uint16_t *)nullptr);
+            else launch(median_slide<uint16_t, 3>, SlideCfg<uint16_t, 3>::SMEM, SlideCfg<uint16_t, 3>::NTC, (uint16_t *)nullptr);
+        }
+        return ct::check_launch("median_slide");
     }
     if (radius > 3) {
         CT_DISPATCH(dtype, T, {

@@ -12,6 +12,8 @@
 // block scan per round plus a carry), pass A finds best, pass B applies the
 // candidate filter and the exact comparison with 128-bit a and 384-bit
 // products, and a block reduction keeps the lowest winning t.
+#include <climits>
+
 #include "ct_common.cuh"
 
 namespace {
@@ -169,34 +171,56 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
         nb = s_hi ? 65536 : 256;
     }
     const i64 rounds = (nb + NT - 1) / NT;
-    // totals and the non-empty bin count
+    // totals, the non-empty bin count and the first / last non-empty bin.
+    // Bins below the first or above the last non-empty one have w0 = 0 or
+    // w1 = 0: score 0 and b = w0 w1 = 0, so they never win (nor change best
+    // when a positive score exists) -- the scored rounds are [R_lo, R_hi]
+    // (12-bit data in 65536 bins: 4 rounds instead of 64).
     u64 W = 0, S = 0;
-    i64 nzc = 0;
+    i64 nzc = 0, R_lo = 0, R_hi = -1;
     {
         u64 cw = 0, cs = 0;
+        int lo = INT_MAX, hi = -1;
         for (i64 R = 0; R < rounds; ++R) {
             const i64 b = R * NT + tid;
             const u64 h = b < nb ? hist[b] : 0;
             cw += h;
             cs += h * (u64)b;
             nzc += h != 0;
+            if (h) {
+                lo = min(lo, (int)b);
+                hi = (int)b;
+            }
         }
         for (int o = 16; o; o >>= 1) {
             cw += __shfl_xor_sync(0xffffffffu, cw, o);
             cs += __shfl_xor_sync(0xffffffffu, cs, o);
             nzc += __shfl_xor_sync(0xffffffffu, nzc, o);
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
         }
+        __shared__ int s_lo[NW], s_hi2[NW];
         if ((tid & 31) == 0) {
             s_w[tid >> 5] = cw;
             s_s[tid >> 5] = cs;
             s_cnt[tid >> 5] = nzc;
+            s_lo[tid >> 5] = lo;
+            s_hi2[tid >> 5] = hi;
         }
         __syncthreads();
         nzc = 0;
+        lo = INT_MAX;
+        hi = -1;
         for (int i = 0; i < NW; ++i) {
             W += s_w[i];
             S += s_s[i];
             nzc += s_cnt[i];
+            lo = min(lo, s_lo[i]);
+            hi = max(hi, s_hi2[i]);
+        }
+        if (hi >= 0) {
+            R_lo = lo / NT;
+            R_hi = hi / NT;
         }
     }
     const i64 nonzero = nzc;
@@ -234,11 +258,11 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     };
     {
         u64 cw = 0, cs = 0;
-        for (i64 R0 = 0; R0 < rounds; R0 += RB) {
+        for (i64 R0 = R_lo; R0 <= R_hi; R0 += RB) {
             load_batch(R0);
 #pragma unroll
             for (int u = 0; u < RB; ++u) {
-                if (R0 + u >= rounds) break;  // uniform
+                if (R0 + u > R_hi) break;  // uniform
                 const i64 t = (R0 + u) * NT + tid;
                 u64 w0 = hb[u], s0 = hb[u] * (u64)t, tw, ts;
                 block_scan2<NT>(w0, s0, s_w, s_s, tw, ts);
@@ -266,11 +290,11 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
             if (!(best <= 0.0) && !(score(w0, s0) >= cut)) return;
             consider(mine, t, w0, s0, W, S);  // rare: out of line
         };
-        for (i64 R0 = 0; R0 < rounds; R0 += RB) {
+        for (i64 R0 = R_lo; R0 <= R_hi; R0 += RB) {
             load_batch(R0);
 #pragma unroll
             for (int u = 0; u < RB; ++u) {
-                if (R0 + u >= rounds) break;  // uniform
+                if (R0 + u > R_hi) break;  // uniform
                 const i64 t = (R0 + u) * NT + tid;
                 u64 w0 = hb[u], s0 = hb[u] * (u64)t, tw, ts;
                 block_scan2<NT>(w0, s0, s_w, s_s, tw, ts);

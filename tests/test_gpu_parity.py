@@ -324,13 +324,13 @@ def test_tensor_core_k1_matches_exact(cuda, sigma, shape, seed):
 @pytest.mark.parametrize("vmax,shape,sigma,seed", [(4095, (256, 128, 64), 10.0, 21), (65535, (130, 64, 64), 10.0, 22),
                                                    (200, (96, 64, 32), 6.0, 23), (4095, (64, 192, 32), 3.0, 24)])
 def test_tensor_core_k1_u16_matches_exact(cuda, vmax, shape, sigma, seed):
-    """u16 tensor-core K1 (byte-interleaved pass x, fraction bits from the
-    frame's maximum: 20 for 12-bit data, 16 at full range, 24 when the
-    maximum is <= 255) on noise and on a synthetic 12-bit scene vs the
+    """u16 tensor-core K1 (byte-interleaved pass x, 40-bit intermediates in
+    5 byte planes with fraction bits from the frame's maximum: 28 for 12-bit
+    data, 24 at full range) on noise and on a synthetic 12-bit scene vs the
     scipy-order exact path."""
     from paper_1407_2089_b200._lib import lib
 
-    assert lib().ct_k1_path(2, *shape, 12, 12, 10, 2) == 2
+    assert lib().ct_k1_path(2, *shape, 12, 12, 10, 0) == 2
     rng = np.random.default_rng(seed)
     noise = torch.from_numpy(rng.integers(0, vmax + 1, size=shape).astype(np.uint16).view(np.int16)).cuda()
     raws = [noise.view(torch.uint16)]
