@@ -358,6 +358,13 @@ def run_ours(args):
     # step read this step's table and counters on the main stream; the next
     # step's cell work waits for them (coll_done) before overwriting those
     # buffers.  The timed region ends with both streams joined.
+    graphs = {}  # (ring slot, channel) -> CUDA graph of that frame's launches (after warm-up)
+    graph_launches = {}
+
+    def cell_body(raws, t, k, ch):
+        pipe.cell(raws[ch], frame=t, id_start=0)
+        counts_dev[k:k + 1].copy_(pipe.counters[2:3])
+
     def step(i, coll=True, first=True):
         t, raws = inputs[i % ring]
         main = torch.cuda.current_stream()
@@ -368,15 +375,24 @@ def run_ours(args):
             s_cell.wait_event(coll_done)
         with torch.cuda.stream(s_cell):
             for k, ch in enumerate(cell_chs):
-                pipe.cell(raws[ch], frame=t, id_start=0)
-                counts_dev[k:k + 1].copy_(pipe.counters[2:3])
+                g = graphs.get((i % ring, ch))
+                if g is not None:
+                    g.replay()
+                    _lib.launch_counter["count"] += graph_launches[(i % ring, ch)] * _lib.launch_counter["enabled"]
+                else:
+                    cell_body(raws, t, k, ch)
                 if world > 1 and coll and k + 1 < len(cell_chs):
                     # the records of this channel leave before the next cell channel reuses the table
                     main.wait_stream(s_cell)
                     gather_tables(pipe.table, pipe.counters[2], max_rows=GATHER_ROWS)
                     s_cell.wait_stream(main)
         with torch.cuda.stream(s_vess):
-            pipe.vessel(raws[synth.VESSEL])
+            g = graphs.get((i % ring, synth.VESSEL))
+            if g is not None:
+                g.replay()
+                _lib.launch_counter["count"] += graph_launches[(i % ring, synth.VESSEL)] * _lib.launch_counter["enabled"]
+            else:
+                pipe.vessel(raws[synth.VESSEL])
         if world > 1 and coll:
             main.wait_stream(s_cell)  # the collectives read this step's cell results
             # the frame's detection counts (global ids) and its per-cell records, over NCCL
@@ -389,6 +405,26 @@ def run_ours(args):
     torch.cuda.synchronize()
     # correctness guard: the fused path's decisions must be the fast ones
     assert int(pipe.state[5].item()) == 0, "MRF needed iterations: bench workload assumption broken"
+    if not args.no_graphs:
+        # one CUDA graph per (input slot, channel): a step is then one replay per
+        # channel on that channel's stream (no per-kernel host launches)
+        for sl in range(ring):
+            t, raws = inputs[sl]
+            for k, ch in enumerate(cell_chs):
+                c0 = _lib.launch_counter["count"]
+                _lib.launch_counter["enabled"] = True
+                graphs[(sl, ch)] = pipe.capture(lambda: cell_body(raws, t, k, ch))
+                graph_launches[(sl, ch)] = _lib.launch_counter["count"] - c0
+                _lib.launch_counter["enabled"] = False
+            c0 = _lib.launch_counter["count"]
+            _lib.launch_counter["enabled"] = True
+            graphs[(sl, synth.VESSEL)] = pipe.capture(lambda: pipe.vessel(raws[synth.VESSEL]))
+            graph_launches[(sl, synth.VESSEL)] = _lib.launch_counter["count"] - c0
+            _lib.launch_counter["enabled"] = False
+        for i in range(max(2, ring)):
+            step(i)
+        torch.cuda.synchronize()
+        log(f"captured {len(graphs)} CUDA graphs ({sum(graph_launches.values()) // ring} libct launches per step)")
 
     if world > 1:
         dist.barrier()
@@ -521,6 +557,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": spec.dtype, "data": "synthetic",
             "config": {"workload": desc, "global_batch": world, "parallelism": f"frame-sharded dp{world}",
                        "frames_per_s": world * args.steps / (ms_max / 1e3),
+                       "launch": "eager" if args.no_graphs else "CUDA graph per (frame slot, channel), replayed on "
+                                                                "the channel's stream",
                        "l2": f"inputs larger than L2: {nch * nvox * b / 1e6:.0f} MB/step from a ring of {ring} "
                              "distinct time points, plus GB-scale intermediates"},
             "parity": None if parity is None else parity["ok"], "parity_detail": parity,
@@ -713,7 +751,23 @@ def run_e2e(args, pipe, spec, channels, dev, world, s_cell, s_vess):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     val = world * args.steps * nch * nvox / (ms / 1e3)
+    # the link alone: the same per-step H2D copies back to back, no compute
+    # (the roofline of e2e once the device step is shorter than the copy)
+    torch.cuda.synchronize()
+    a.record()
+    for sc in s_copy.values():
+        sc.wait_event(a)
+    for i in range(args.steps):
+        for ch in channels:
+            with torch.cuda.stream(s_copy[ch]):
+                dbuf[i % NS][ch].copy_(host[i % nring][ch], non_blocking=True)
+    for sc in s_copy.values():
+        torch.cuda.current_stream().wait_stream(sc)
+    b.record()
+    torch.cuda.synchronize()
+    link_gbs = nch * nvox * esz * args.steps / (a.elapsed_time(b) / 1e3) / 1e9
     return {"value": val, "unit": UNIT, "h2d_bytes_per_step": nch * nvox * esz,
+            "h2d_link_gbs": link_gbs, "frac_of_link": (nch * nvox * esz / (ms / args.steps / 1e3) / 1e9) / link_gbs,
             "d2h_bytes_per_step": int(rbytes), "ms_per_step": ms / args.steps,
             # the H2D of the raw frames over PCIe is the e2e bound once the device step is shorter
             "h2d_gbs": nch * nvox * esz / (ms / args.steps / 1e3) / 1e9,
@@ -797,6 +851,7 @@ def main():
     ap.add_argument("--cpu-baseline-crop", type=int, default=None,
                     help="x-slices of the cpu_baseline sample (default: the full frame for C2, 256 for C3)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of per-frame CUDA graphs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -179,9 +179,13 @@ int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, int32_t *l
 /* K5 on packed z-rows (ct_threshold_close_rows output, nz <= 128): same
  * outputs as ct_ccl26 (ref segment.py:254) without re-reading a byte mask.
  * flags: CT_LABELS_PREFILLED = labels already hold -1 everywhere (the caller
- * filled them, e.g. on a side stream off the critical path); else the call
- * fills them. */
+ * filled them); CT_LABELS_RESET = labels hold -1 everywhere except at
+ * fg_list[0 .. counters[CT_CNT_FG]) as left by the previous ct_ccl26_rows /
+ * ct_cell_table calls on these same buffers (a frame loop: the call resets
+ * just those voxels, O(foreground) instead of O(volume)); else the call
+ * fills labels with -1. */
 #define CT_LABELS_PREFILLED 1
+#define CT_LABELS_RESET 2
 int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t nz, int32_t *labels, int32_t *fg_list,
                   int64_t *counters, int flags, void *stream);
 

@@ -844,6 +844,16 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
     return ct::check_launch("ccl_flatten");
 }
 
+// CT_LABELS_RESET: the previous frame's foreground (its fg list, count in
+// counters[CT_CNT_FG]) goes back to -1 -- the only voxels ccl / cell table
+// wrote -- before the counters are cleared
+__global__ void __launch_bounds__(256) ccl_reset_prev(int32_t *__restrict__ labels,
+                                                      const int32_t *__restrict__ fg_list,
+                                                      const int64_t *__restrict__ counters) {
+    const i64 n = counters[CT_CNT_FG];
+    for (i64 e = blockIdx.x * 256ll + threadIdx.x; e < n; e += (i64)gridDim.x * 256) labels[fg_list[e]] = -1;
+}
+
 extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t nz, int32_t *labels,
                              int32_t *fg_list, int64_t *counters, int flags, void *stream) {
     if (nx <= 0 || ny <= 0 || nz <= 0) {
@@ -855,8 +865,12 @@ extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t n
         return CT_ERR_UNSUPPORTED;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    if (flags & CT_LABELS_RESET) {
+        ccl_reset_prev<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters);
+        if (int st = ct::check_launch("ccl_reset_prev")) return st;
+    }
     cudaMemsetAsync(counters, 0, CT_CNT_WORDS * sizeof(int64_t), s);
-    if (!(flags & CT_LABELS_PREFILLED))  // else the caller filled labels with -1 (e.g. on a side stream)
+    if (!(flags & (CT_LABELS_PREFILLED | CT_LABELS_RESET)))  // else labels hold -1 already / after the reset
         cudaMemsetAsync(labels, 0xff, (size_t)(nx * ny * nz) * sizeof(int32_t), s);  // background = -1
     const i64 nrows = nx * ny;
     const int g = (int)min((nrows + 255) / 256, (i64)CT_NUM_SMS * 16);

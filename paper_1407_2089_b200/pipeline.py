@@ -23,11 +23,11 @@ Data-dependent errors (DegenerateHistogramError) surface in ``finish_*``.
 
 Stream contract: every launch goes to the current torch stream, and a
 result's buffers (labels, table, voxel lists, mask, distance) are reused by
-the next ``cell()`` / ``vessel()`` call of the same pipeline.  A result is
-valid only for work ordered after it on the launching stream; the next
-frame's label background fill (side stream) waits on an event recorded on
-that stream at the next ``cell()`` call, so a consumer on any other stream
-must make the launching stream wait for it first.
+the next ``cell()`` / ``vessel()`` call of the same pipeline (the next
+frame's K5 first resets the previous frame's foreground labels to -1).  A
+result is valid only until that call, for work ordered after it on the
+launching stream; a consumer on any other stream must make the launching
+stream wait for it first.
 """
 
 from __future__ import annotations
@@ -125,8 +125,10 @@ class FramePipeline:
             self.crows = E(nx * ny * (1 if nz <= 64 else 2), torch.int64) if self.rows_path else None
             self.mask = None if self.rows_path else E(self.dims, torch.uint8)
             if self.rows_path:
-                self._side = torch.cuda.Stream(dev)
-                self._ev_free, self._ev_filled = torch.cuda.Event(), torch.cuda.Event()
+                # -1 everywhere once; afterwards each frame's K5 resets only the
+                # previous frame's foreground (CT_LABELS_RESET: fg list + count
+                # kept in fg / counters), not the whole volume
+                self.labels.fill_(-1)
         if vessel:
             self.mwork = E(workspace_bytes(4, nx, ny, nz, self.code), torch.uint8)
             self.state = Z(9, torch.float64)
@@ -174,16 +176,6 @@ class FramePipeline:
         nx, ny, nz = self.dims
         s = _dev.stream_handle()
         rx, ry, rz = self.r
-        if self.rows_path:
-            # the label volume's background fill (N int32, HBM bound) runs on a
-            # side stream while K1/K2 (tensor / ALU bound) run, instead of
-            # inside K5 on the critical path; K5 waits for it
-            cur = torch.cuda.current_stream(self.device)
-            self._ev_free.record(cur)  # previous frame's label consumers are done
-            self._side.wait_event(self._ev_free)
-            with torch.cuda.stream(self._side):
-                self.labels.fill_(-1)
-            self._ev_filled.record(self._side)
         self.hist.zero_()
         e = self._t0()
         if self.exact_k1:
@@ -213,9 +205,8 @@ class FramePipeline:
         self._t1("K4 threshold+close", e)
         e = self._t0()
         if self.rows_path:
-            torch.cuda.current_stream(self.device).wait_event(self._ev_filled)
             call("ct_ccl26_rows", self.crows.data_ptr(), nx, ny, nz, self.labels.data_ptr(), self.fg.data_ptr(),
-                 self.counters.data_ptr(), 1, s)  # CT_LABELS_PREFILLED
+                 self.counters.data_ptr(), 2, s)  # CT_LABELS_RESET
         else:
             call("ct_ccl26", self.mask.data_ptr(), nx, ny, nz, self.labels.data_ptr(), self.fg.data_ptr(),
                  self.counters.data_ptr(), s)
@@ -249,6 +240,26 @@ class FramePipeline:
              self.dist.data_ptr(), s)
         self._t1("K8 edt", e)
         return VesselResult(mask=self.vmask, distance=self.dist, state=self.state, otsu=self.votsu)
+
+    # -- CUDA graphs ---------------------------------------------------------
+    def capture(self, fn) -> "torch.cuda.CUDAGraph":
+        """Capture ``fn()`` -- e.g. ``lambda: pipe.cell(raw)`` or
+        ``lambda: pipe.vessel(raw)`` -- as a CUDA graph: every launch of the
+        frame (torch's and libct's) in one graph.  ``graph.replay()`` on a
+        stream re-runs the frame on the same buffers and input address with no
+        per-kernel host launch cost, in that stream's order (so a cell graph
+        replayed on one stream and a vessel graph on another overlap as the
+        eager launches do).  Run ``fn`` once eagerly before capturing (module
+        load, function attributes); results are read as after ``cell`` /
+        ``vessel``."""
+        assert self.marks is None, "stage timing marks cannot be captured"
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.graph(g, stream=side, capture_error_mode="relaxed"):
+            fn()
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        return g
 
     # -- host-side completion (synchronises) --------------------------------
     def finish_cell(self, res: CellResult, materialize: bool = False, with_hull: bool = False):

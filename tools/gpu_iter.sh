@@ -7,4 +7,6 @@ case "$2" in *bench2*) timeout 600 python bench.py --no-cpu-baseline --steps 100
 case "$2" in *sweep*) timeout 900 python tools/sweep_c5.py > gpurun_out/c5_sweep.jsonl 2> gpurun_out/c5_sweep.txt;; esac
 case "$2" in *stages3*) python tools/profile_stages.py --config C3 --reps 3 > gpurun_out/stages_c3.log 2>&1;
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python tools/profile_stages.py --config C3 --reps 1 > gpurun_out/ncu_c3.log 2>&1;; esac
+case "$2" in *stages2*) python tools/profile_stages.py --reps 3 > gpurun_out/stages_c2.log 2>&1;
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python tools/profile_stages.py --reps 1 > gpurun_out/ncu_c2.log 2>&1;; esac
 exit 0
