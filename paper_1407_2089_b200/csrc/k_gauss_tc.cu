@@ -47,6 +47,13 @@ constexpr int KXY = 256;       // input rows per tile (passes x, y): TM + 2r <= 
 constexpr int NT = 512;        // threads per CTA: 16 warps = 4 TMEM sub-partitions x 4 column groups
 constexpr int PMAX = 65;       // max taps per side + 1
 
+// lowest kept limb-pair sum (data limb a + weight limb b) for NP data planes
+// and NL weight limbs: u8 (4 planes, 24 fractional bits; 4 limbs, taps < 2^32)
+// keeps a + b >= 2; u16 (5 planes: 40-bit intermediates, 24-28 fractional
+// bits; 5 limbs: taps < 2^40, the weight rounding 2^8 finer) keeps a + b >= 4;
+// always 5 accumulators (a + b = LOP .. LOP + 4)
+__host__ __device__ constexpr int lo_pair(int np, int nl = 4) { return np == 1 ? 0 : np + nl - 6; }
+
 struct TcParams {
     long long Q[3][PMAX];  // integer taps per axis (Q[axis][|j|] = rint(w_j 2^fw[axis]))
     int fw[3];             // weight scale bits per axis (<= FW, four 8-bit limbs)
@@ -72,7 +79,7 @@ __global__ void __launch_bounds__(256) tc_vmax(const uint4 *__restrict__ raw, lo
 // Setup: integer taps and the certified error bound (one warp per axis).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int rx, int ry, int rz, int u8, int np,
-                                               double eps_override, TcParams *prm) {
+                                               int nl, double eps_override, TcParams *prm) {
     // warp a handles axis a: lane-parallel taps, warp reductions
     const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned vm = u8 ? 255u : prm->vmax;  // tc_vmax ran before (u16)
@@ -80,7 +87,7 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
     // P <= vmax (1 + (2r+1) 2^-fw) < 2^bits(vmax): 8 np - bits integer bits left for the fraction
     // (4 planes: <= 24; 5 planes: <= 28 -- 12-bit data keeps 28, full 16-bit 24)
     const int fd = min(np == 4 ? FD : 28, max(16, 8 * np - (vm ? 32 - __clz(vm) : 0)));
-    const int lop = np - 2;  // kept limb pairs a + b >= lop
+    const int lop = lo_pair(np, nl);  // kept limb pairs a + b >= lop
     const int rr[3] = {rx, ry, rz};
     const double *ws = a == 0 ? w : (a == 1 ? w + rx + 1 : w + rx + 1 + ry + 1);
     const int r = rr[a];
@@ -88,11 +95,13 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
     for (int j = lane; j <= r; j += 32) wmax = fmax(wmax, ws[j]);
     for (int o = 16; o; o >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
     wmax *= 1.0000001;
-    // pass z: fw <= 36 keeps the edge tail sums < 2^35 (16 pieces < 2^32, see tc_pass_z)
-    int fw = a == 2 ? 36 : FW;
-    while (fw > 24 && wmax * ldexp(1.0, fw) >= 4294967295.0) --fw;
+    // taps Q_j < 2^(8 nl); pass z: fw <= 36 + 8 (nl - 4) keeps the edge tail
+    // sums < 16 * 2^(8 nl - 1) (16 pieces, see tc_pass_z)
+    const double qmax = ldexp(1.0, 8 * nl) - 1.0;
+    int fw = a == 2 ? 36 + 8 * (nl - 4) : FW + 8 * (nl - 4);
+    while (fw > 24 && wmax * ldexp(1.0, fw) >= qmax) --fw;
     const double scale = ldexp(1.0, fw);
-    double dq = 0.0, qsum[3] = {0.0, 0.0, 0.0};  // qsum[b] = sum_j |limb b of Q_j| over taps -r..r
+    double dq = 0.0, qsum[4] = {0.0, 0.0, 0.0, 0.0};  // qsum[b] = sum_j limb b of Q_j over taps -r..r
     for (int j = lane; j < PMAX; j += 32) {
         long long q = 0;
         if (j <= r) {
@@ -101,24 +110,25 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
             const double mult = j ? 2.0 : 1.0;  // taps -j and +j
             dq += mult * fabs((double)q - x);   // exact difference
 #pragma unroll
-            for (int bb = 0; bb < 3; ++bb) qsum[bb] += mult * (double)((q >> (8 * bb)) & 0xff);
+            for (int bb = 0; bb < 4; ++bb) qsum[bb] += mult * (double)((q >> (8 * bb)) & 0xff);
         }
         prm->Q[a][j] = q;
     }
     for (int o = 16; o; o >>= 1) {
         dq += __shfl_xor_sync(0xffffffffu, dq, o);
 #pragma unroll
-        for (int bb = 0; bb < 3; ++bb) qsum[bb] += __shfl_xor_sync(0xffffffffu, qsum[bb], o);
+        for (int bb = 0; bb < 4; ++bb) qsum[bb] += __shfl_xor_sync(0xffffffffu, qsum[bb], o);
     }
     // per-axis bound: weight rounding sum_j |Q_j 2^-fw - w_j| * max input (the
     // inputs of passes y, z are bounded by vmax up to the taps' sum rounding)
     // plus, for y and z, the dropped limb pairs a + b < lop (data limbs <= 255)
     double b = dq / scale * vmax * 1.001;
     if (a == 2)  // pass z: every output column also holds 32 edge-tap pieces (limbs <= 255)
-        for (int bb = 0; bb < 3; ++bb) qsum[bb] += 32.0 * 255.0;
+        for (int bb = 0; bb < 4; ++bb) qsum[bb] += 32.0 * 255.0;
     if (a > 0)
         for (int da = 0; da < lop; ++da)
-            for (int bb = 0; da + bb < lop; ++bb) b += 255.0 * qsum[bb] * ldexp(1.0, 8 * (da + bb) - fw - fd);
+            for (int bb = 0; da + bb < lop && bb < nl; ++bb)
+                b += 255.0 * qsum[bb] * ldexp(1.0, 8 * (da + bb) - fw - fd);
     __shared__ double bs[3];
     __shared__ int fws[3];
     if (lane == 0) {
@@ -139,10 +149,7 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
     }
 }
 
-// lowest kept limb-pair sum (data limb a + weight limb b) for NP data planes:
-// 4 planes (u8: 24 fractional bits) keep a + b >= 2, 5 planes (u16: 40-bit
-// intermediates, 24-28 fractional bits) keep a + b >= 3; both 5 accumulators
-__host__ __device__ constexpr int lo_pair(int np) { return np == 1 ? 0 : np - 2; }
+
 
 __device__ __forceinline__ uint32_t limb(long long q, int b) { return (uint32_t)((q >> (8 * b)) & 0xff); }
 
@@ -162,12 +169,15 @@ __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, u
 // a+b-2, shift 8(a+b-2); output S >> 19).  Volume viewed as [outer][L][inner].
 // ---------------------------------------------------------------------------
 // NPIN = 5 (u16 frames): 40-bit intermediates, pairs a + b >= 3 (lo_pair), still 5 accumulators.
-template <int NPIN, int STAGES, int TN, int NPO = 4>  // TN: columns per tile (32 or 64); NPO: output planes
+template <int NPIN, int STAGES, int TN, int NPO = 4, int NL = 4>  // TN: columns per tile; NPO: output planes;
+                                                                     // NL: weight limbs
 __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ in, long long plane_in, int L,
                                                      int inner, int outer, const TcParams *__restrict__ prm, int axis,
                                                      int r, uint8_t *__restrict__ out, long long plane_out) {
-    constexpr int NACC = NPIN == 1 ? 4 : 5;
-    constexpr int LOP = lo_pair(NPIN);
+    constexpr int NACC = NPIN == 1 ? NL : 5;
+    constexpr int LOP = lo_pair(NPIN, NL);
+    constexpr int AB = 64 * NL;  // TMEM columns of the tap band (64 per limb)
+    static_assert(AB + NACC * TN <= 512, "TMEM: band + accumulators");
     constexpr uint32_t LBO = (TN / 16) * 128, SBO = 128;                // MN-major B
     constexpr int BUF = KXY * TN;                                       // bytes per plane per buffer
     constexpr int OROW = TN + 16;                                       // padded output row (bytes)
@@ -195,9 +205,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * LOP;
     const uint32_t base = tbase;
     const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
-    // A (taps) into TMEM columns [0, 256): limb b = cg at 64 b; row m
-    {
-        const int b = cg;
+    // A (taps) into TMEM columns [0, AB): limb b (column group cg, cg + 4) at 64 b; row m
+    for (int b = cg; b < NL; b += 4) {
         for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
             uint32_t v[8];
 #pragma unroll
@@ -273,12 +282,12 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
 #pragma unroll
             for (int a = 0; a < NPIN; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
+                for (int b = 0; b < NL; ++b) {
                     const int acc = NPIN == 1 ? b : a + b - LOP;
-                    if (acc < 0) continue;
+                    if (acc < 0 || acc >= NACC) continue;
 #pragma unroll
                     for (int ks = 0; ks < KXY / 32; ++ks)
-                        tc::mma_i8_ts(base + 256 + TN * acc, base + b * 64 + ks * 8,
+                        tc::mma_i8_ts(base + AB + TN * acc, base + b * 64 + ks * 8,
                                       d0 + (uint64_t)((a * BUF + ks * 4 * LBO) >> 4), idesc,
                                       first[acc] && ks == 0 ? 0u : 1u);
                     first[acc] = false;
@@ -311,7 +320,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         for (int acc = 0; acc < NACC; ++acc)
 #pragma unroll
             for (int g8 = 0; g8 < CW; g8 += 8)
-                tc::tmem_ld8(lane_addr + 256 + TN * acc + h + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
+                tc::tmem_ld8(lane_addr + AB + TN * acc + h + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
         tc::tmem_ld_wait();
         tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
         tc::fence_async_smem();
@@ -379,12 +388,13 @@ __device__ __forceinline__ void epi_bar() {  // named barrier 1: the epilogue wa
 // of twice the width -- column 2c holds the low bytes of voxel c, column
 // 2c + 1 the high bytes, so the MMA yields both limb sums and the epilogue
 // combines S(c) = D[2c] + 256 D[2c + 1] (no de-interleave pass).
-template <int NPIN, int TN, int SSTG, int ASTG, int DB = 1, int NPO = 4>
+template <int NPIN, int TN, int SSTG, int ASTG, int DB = 1, int NPO = 4, int NL = 4>
 __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant__ CUtensorMap tmap, int L, int inner,
                                                           int outer, const TcParams *__restrict__ prm, int axis, int r,
                                                           uint8_t *__restrict__ out, long long plane_out) {
     static_assert(DB == 1 || NPIN == 1, "u16 input only for the raw pass");
-    constexpr int NACC = NPIN == 1 ? 4 : 5;
+    constexpr int NACC = NPIN == 1 ? NL : 5;
+    constexpr int AB = 64 * NL;  // TMEM columns of the tap band
     constexpr int CH = TN / 16;                     // 16-byte chunks per row (one TMA box each)
     constexpr int PB = KXY * 16;                    // bytes per plane per chunk: [KXY][16]
     constexpr int CB = NPIN * PB;                   // bytes per chunk (all planes)
@@ -396,7 +406,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     constexpr int OBUF = NPO * TM * OROW;           // staged output tile: [NPO planes][128 rows]
     constexpr int CPR = TV / 16;                    // 16-byte chunks per output row
     const long long inner_v = inner / DB;           // voxels per input row
-    static_assert(256 + ASTG * NACC * TN <= 512, "TMEM: band + accumulator sets");
+    static_assert(AB + ASTG * NACC * TN <= 512, "TMEM: band + accumulator sets");
     extern __shared__ __align__(1024) uint8_t sm[];  // [SSTG][SB] operand stages, [2][OBUF] output tiles
     uint8_t *sout = sm + SSTG * SB;
     __shared__ uint64_t full[SSTG], empty[SSTG], afull[ASTG], aempty[ASTG];
@@ -425,8 +435,8 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     // column group cg = e / 4; it writes band limb cg of its rows into TMEM
     const int e_w = wp - 2, q = wp & 3, cg = e_w >> 2, m = 32 * q + lane;
     const uint32_t la = base + ((uint32_t)(32 * q) << 16);
-    if (wp >= 2) {
-        const int b = cg;
+    if (wp >= 2)
+    for (int b = cg; b < NL; b += 4) {
         for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
             uint32_t v[8];
 #pragma unroll
@@ -509,12 +519,12 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
 #pragma unroll
                 for (int da = 0; da < NPIN; ++da)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int acc = NPIN == 1 ? b : da + b - lo_pair(NPIN);
-                        if (acc < 0) continue;
+                    for (int b = 0; b < NL; ++b) {
+                        const int acc = NPIN == 1 ? b : da + b - lo_pair(NPIN, NL);
+                        if (acc < 0 || acc >= NACC) continue;
 #pragma unroll
                         for (int ks = 0; ks < KXY / 32; ++ks)
-                            tc::mma_i8_ts(base + 256 + (a * NACC + acc) * TN, base + b * 64 + ks * 8,
+                            tc::mma_i8_ts(base + AB + (a * NACC + acc) * TN, base + b * 64 + ks * 8,
                                           d0 + (uint64_t)((da * PB + ks * 4 * LBO) >> 4), idesc,
                                           first[acc] && ks == 0 ? 0u : 1u);
                         first[acc] = false;
@@ -529,7 +539,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
         const int h = CW * cg;
         const int et = t - 64;  // 0 .. 32 * WS_EPI - 1
         // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
-        const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * lo_pair(NPIN);
+        const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * lo_pair(NPIN, NL);
         // coalesced store of a staged output tile: NPO planes x 128 rows x TV bytes
         auto flush = [&](long long k, const uint8_t *ob) {
             int o, ti, cb;
@@ -555,10 +565,10 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                 if constexpr (CW % 8 == 0) {
 #pragma unroll
                     for (int g8 = 0; g8 < CW; g8 += 8)
-                        tc::tmem_ld8(la + 256 + (a * NACC + acc) * TN + h + g8,
+                        tc::tmem_ld8(la + AB + (a * NACC + acc) * TN + h + g8,
                                      *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
                 } else {
-                    tc::tmem_ld4(la + 256 + (a * NACC + acc) * TN + h, *reinterpret_cast<uint32_t(*)[4]>(&v[acc][0]));
+                    tc::tmem_ld4(la + AB + (a * NACC + acc) * TN + h, *reinterpret_cast<uint32_t(*)[4]>(&v[acc][0]));
                 }
             }
             tc::tmem_ld_wait();
@@ -612,14 +622,14 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
 //   q = max(raw - ceil(V / 2^zs), 0)                  (= rint(max(raw - bg, 0)))
 //   flag iff (eps - V) mod 2^zs <= 2 eps and raw 2^zs - V >= 2^zs - eps
 // ---------------------------------------------------------------------------
-template <int NZ, int STAGES, typename Traw = uint8_t, int NP = 4>  // NP: planes of P2 (4, or 5 for u16)
+template <int NZ, int STAGES, typename Traw = uint8_t, int NP = 4, int NL = 4>  // NP: planes of P2, NL: weight limbs
 __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ in, long long plane, long long nlines,
                                                     const TcParams *__restrict__ prm, int r,
                                                     const Traw *__restrict__ raw, Traw *__restrict__ q,
                                                     unsigned long long *__restrict__ fix, long long cap) {
     constexpr int RB = (int)sizeof(Traw);       // raw / q bytes per voxel
     constexpr int VPW = 4 / RB;                 // voxels per 32-bit word
-    constexpr int LOP = lo_pair(NP), SPL = 8 * LOP;  // kept pairs a + b >= LOP; S has scale 2^(fd + fw - SPL)
+    constexpr int LOP = lo_pair(NP, NL), SPL = 8 * LOP;  // kept pairs a + b >= LOP; S has scale 2^(fd + fw - SPL)
     static_assert(NZ <= 64 || RB == 1, "u16 pass z: nz in {32, 64}");
     constexpr int NCH = NZ / 16;                // 16-byte chunks per line
     constexpr uint32_t LBO = 128, SBO = NCH * 128, SBOE = 256;  // K-major: data / taps (K = NZ), edge block (K = 32)
@@ -629,11 +639,11 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     constexpr int BE = NZ * 32;                 // bytes per weight limb, edge block
     constexpr int ACOL = 5 * NZ;                // TMEM: accumulators [0, ACOL), edge A slots after
     static_assert(ACOL + NP * 8 <= 512, "TMEM");
-    extern __shared__ __align__(1024) uint8_t sm[];  // [4][BW] taps, [4][BE] edge taps, [STAGES][NP][ABUF] data,
+    extern __shared__ __align__(1024) uint8_t sm[];  // [NL][BW] taps, [NL][BE] edge taps, [STAGES][NP][ABUF] data,
                                                      // [STAGES][RBUF] raw, [2][RBUF] q tile
     uint8_t *sw = sm;
-    uint8_t *swe = sm + 4 * BW;
-    uint8_t *sa = swe + 4 * BE;
+    uint8_t *swe = sm + NL * BW;
+    uint8_t *sa = swe + NL * BE;
     uint8_t *sr = sa + STAGES * NP * ABUF;
     uint8_t *sq = sr + STAGES * RBUF;
     const uint8_t *rawb = (const uint8_t *)raw;
@@ -662,14 +672,14 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         const int d = k > n ? k - n : n - k;
         const long long qv = d < PMAX ? Qs[d] : 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) sw[b * BW + tc::kmajor_off(n, k, LBO, SBO)] = (uint8_t)limb(qv, b);
+        for (int b = 0; b < NL; ++b) sw[b * BW + tc::kmajor_off(n, k, LBO, SBO)] = (uint8_t)limb(qv, b);
     }
     for (int e = t; e < NZ * 32; e += NT) {
         const int n = e >> 5, sl = e & 31, s16 = sl & 15;
         const long long E = sl < 16 ? (n + 1 <= PMAX ? Ts[n + 1] : 0) : (NZ - n <= PMAX ? Ts[NZ - n] : 0);
-        const long long pc = E / 16 + (s16 < E % 16 ? 1 : 0);  // < 2^32
+        const long long pc = E / 16 + (s16 < E % 16 ? 1 : 0);  // < 2^(8 NL)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) swe[b * BE + tc::kmajor_off(n, sl, LBO, SBOE)] = (uint8_t)limb(pc, b);
+        for (int b = 0; b < NL; ++b) swe[b * BE + tc::kmajor_off(n, sl, LBO, SBOE)] = (uint8_t)limb(pc, b);
     }
     const long long eps = prm->eps;
     const int zs = prm->fw[2] + prm->fd - SPL;  // S has scale 2^zs
@@ -743,9 +753,9 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
 #pragma unroll
             for (int a = 0; a < NP; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
+                for (int b = 0; b < NL; ++b) {
                     const int acc = a + b - LOP;
-                    if (acc < 0) continue;
+                    if (acc < 0 || acc > 4) continue;
 #pragma unroll
                     for (int ks = 0; ks < NZ / 32; ++ks)
                         tc::mma_i8_ss(base + NZ * acc, a0 + (uint64_t)((a * ABUF + ks * 2 * LBO) >> 4),
@@ -927,7 +937,7 @@ template <typename Traw>
 int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, int ry, int rz, uint8_t *p1,
                   uint8_t *p2, TcParams *prm, Traw *q, unsigned long long *fix, int64_t cap, cudaStream_t s) {
     constexpr int RB = (int)sizeof(Traw);
-    constexpr int NP = RB == 1 ? 4 : 5;
+    constexpr int NP = RB == 1 ? 4 : 5, NL = NP;  // intermediate planes, weight limbs
     const long long N = nx * ny * nz;
     // persistent grids: one CTA per SM (capping it to leave SMs to the concurrent vessel stream measured
     // slower: 140 / 132 / 120 SMs -> 1.744 / 1.750 / 1.810 ms per C2 step vs 1.744)
@@ -941,7 +951,7 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
     // byte matrix [nx][ny nz RB]; box = 16 bytes x 256 x-rows, TX / 16 boxes
     // per tile (u16: TX bytes = TX / 2 voxels, both byte limbs)
     {
-        constexpr int TX = 64, SS = 6, AS = 1;
+        constexpr int TX = NL == 4 ? 64 : 32, SS = 6, AS = 1;  // TMEM: 64 NL band columns + NL TX accumulators
         CUtensorMap tm;
         const cuuint64_t dims[2] = {(cuuint64_t)(ny * nz * RB), (cuuint64_t)nx};
         const cuuint64_t strides[1] = {(cuuint64_t)(ny * nz * RB)};
@@ -952,7 +962,7 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
             ct::set_error("tensor map (pass x) rejected");
             return CT_ERR_UNSUPPORTED;
         }
-        auto kx = tc_pass_xy_ws<1, TX, SS, AS, RB, NP>;
+        auto kx = tc_pass_xy_ws<1, TX, SS, AS, RB, NP, NL>;
         const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * NP * TM * (TX / RB + 16) + 1024;
         cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = ((nx + TM - 1) / TM) * (ny * nz * RB / TX);
@@ -966,7 +976,7 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
     // MMAs read the tap band A from TMEM, and narrower tiles only add MMAs
     {
         constexpr int YS = NP == 4 ? 5 : 4;  // operand stages (SMEM: 5 planes x 4 stages + output tiles)
-        auto ky = tc_pass_xy<NP, YS, TNY, NP>;
+        auto ky = tc_pass_xy<NP, YS, TNY, NP, NL>;
         const size_t sm = (size_t)YS * NP * KXY * TNY + 2 * NP * TM * (TNY + 16) + 1024;
         cudaFuncSetAttribute(ky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TNY);
@@ -977,13 +987,13 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
     // pass z + epilogue
     {
         const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
-        const int stg = RB == 2 ? 3 : nz == 96 ? 2 : 4;
-        const size_t sm = 4 * nz * nz + 4 * nz * 32 + (size_t)stg * (NP * TM * nz + TM * nz * RB) + 2 * TM * nz * RB +
-                          1024;
+        const int stg = RB == 2 ? 2 : nz == 96 ? 2 : 4;
+        const size_t sm = NL * nz * nz + NL * nz * 32 + (size_t)stg * (NP * TM * nz + TM * nz * RB) +
+                          2 * TM * nz * RB + 1024;
         void (*kz)(const uint8_t *, long long, long long, const TcParams *, int, const Traw *, Traw *,
                    unsigned long long *, long long);
         if constexpr (RB == 2)
-            kz = nz == 64 ? tc_pass_z<64, 3, Traw, 5> : tc_pass_z<32, 3, Traw, 5>;
+            kz = nz == 64 ? tc_pass_z<64, 2, Traw, 5, 5> : tc_pass_z<32, 2, Traw, 5, 5>;
         else
             kz = nz == 64 ? tc_pass_z<64, 4, Traw> : nz == 96 ? tc_pass_z<96, 2, Traw> : tc_pass_z<32, 4, Traw>;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1010,7 +1020,7 @@ int ct_gaussian_q_tc(const void *raw, int dtype, int64_t nx, int64_t ny, int64_t
         tc_vmax<<<CT_NUM_SMS * 4, 256, 0, s>>>((const uint4 *)raw, N * 2 / 16, prm);  // N * 2 % 16 == 0 (nz % 32)
         if (int st = ct::check_launch("tc_vmax")) return st;
     }
-    tc_prep<<<1, 96, 0, s>>>(w, rx, ry, rz, u8 ? 1 : 0, np, eps_override, prm);
+    tc_prep<<<1, 96, 0, s>>>(w, rx, ry, rz, u8 ? 1 : 0, np, np, eps_override, prm);
     if (int st = ct::check_launch("tc_prep")) return st;
     if (u8)
         return gaussian_q_tc<uint8_t>((const uint8_t *)raw, nx, ny, nz, rx, ry, rz, p1, p2, prm, (uint8_t *)q, fix,

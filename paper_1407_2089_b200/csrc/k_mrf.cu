@@ -693,11 +693,16 @@ __global__ void __launch_bounds__(256) mrf_stream_int(const T *__restrict__ v, i
 // Same pass specialised for nz == NZ (32, 64, 128): thread t owns column
 // k = t % NZ of rows t / NZ + p * (256 / NZ); planes staged as raw T in SMEM
 // via 32-bit vector loads; 32-bit indexing (volumes < 2^31 voxels).
-template <typename T, typename LT, int NZ>
+// MODE as in mrf_stream_v4: 0 = histogram, #{sign sum != 0}, Laplacian sum
+// and Laplacians; 1 = histogram, #{sign sum != 0} and E = sum of squared
+// forward differences (the certified decision's bound, ct_mrf_decide), no
+// Laplacians; 2 = Laplacians and their sum only, nothing when certified.
+template <typename T, typename LT, int NZ, int MODE = 0>
 __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, int nx, int ny,
                                                      unsigned long long *__restrict__ ghist,
                                                      unsigned long long *__restrict__ scal,
                                                      LT *__restrict__ lap) {
+    if (MODE == 2 && *(volatile unsigned long long *)&scal[W_SKIP]) return;
     constexpr int RP = 256 / NZ;           // rows per thread sweep
     constexpr int P = MJ / RP;             // positions per thread
     constexpr int PL = (MJ + 2) * NZ;      // staged plane elements
@@ -752,6 +757,7 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
     __syncthreads();  // plane i0-1 read by all before iteration i0 stores into its slot
     unsigned nnz = 0;
     long long lsum = 0;
+    unsigned long long esq = 0;  // MODE 1 (clamped neighbours make boundary differences 0)
     int cs = 0, ns = 1, fs = 2;
     for (int i = i0; i < i1; ++i) {
         load_plane(i + 2, regs);  // in flight while plane i is processed
@@ -766,17 +772,22 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
                 const int xm = prev[p], xp = X[o];
                 const int ym = C[o - NZ], yp = C[o + NZ];
                 const int zm = k > 0 ? C[o - 1] : c, zp = k < NZ - 1 ? C[o + 1] : c;
-                const int sgs = ((xm > c) - (xm < c)) + ((c > xp) - (c < xp)) + ((ym > c) - (ym < c)) +
-                                ((c > yp) - (c < yp)) + ((zm > c) - (zm < c)) + ((c > zp) - (c < zp));
-                nnz += sgs != 0;
-                if (iint && j > 0 && j < ny - 1 && k > 0 && k < NZ - 1) {
+                if (MODE != 2) {
+                    const int sgs = ((xm > c) - (xm < c)) + ((c > xp) - (c < xp)) + ((ym > c) - (ym < c)) +
+                                    ((c > yp) - (c < yp)) + ((zm > c) - (zm < c)) + ((c > zp) - (c < zp));
+                    nnz += sgs != 0;
+                    if (BYTE || c < 4096) atomicAdd(&wh[c], 1u);
+                    else atomicAdd(&ghist[c], 1ull);
+                }
+                if (MODE == 1) {
+                    const long long dx = xp - c, dy = yp - c, dz = zp - c;
+                    esq += (unsigned long long)(dx * dx + dy * dy + dz * dz);
+                } else if (iint && j > 0 && j < ny - 1 && k > 0 && k < NZ - 1) {
                     const int l = (xm + xp + ym + yp + zm + zp) - 6 * c;
                     lsum += l;
                     lap[((unsigned)(i - 1) * (unsigned)my + (unsigned)(j - 1)) * (unsigned)mz + (unsigned)(k - 1)] =
                         (LT)l;
                 }
-                if (BYTE || c < 4096) atomicAdd(&wh[c], 1u);
-                else atomicAdd(&ghist[c], 1ull);
                 prev[p] = c;
             }
         }
@@ -788,11 +799,14 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
     for (int o = 16; o; o >>= 1) {
         nnz64 += __shfl_xor_sync(0xffffffffu, nnz64, o);
         lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        esq += __shfl_xor_sync(0xffffffffu, esq, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&scal[W_NNZ], nnz64);
-        atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
+        if (MODE != 2) atomicAdd(&scal[W_NNZ], nnz64);
+        if (MODE != 1) atomicAdd(&scal[W_LAPSUM], (unsigned long long)lsum);
+        if (MODE == 1) atomicAdd(&scal[W_LAPSQ], esq);
     }
+    if (MODE == 2) return;
     __syncthreads();
     if (BYTE) {
         unsigned t = 0;
@@ -1247,6 +1261,28 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
         else launch(mrf_stream_v4<128>);
         if (int st = ct::check_launch("mrf_stream_v4")) return st;
     } else if ((nz == 32 || nz == 64 || nz == 128) && ((uintptr_t)v & 3) == 0 && nx * ny * nz < (1ll << 31)) {
+        if (quick && ni >= 2) {
+            // certified decision first (MODE 1); Laplacians (MODE 2) only if it fails
+            auto k1 = nz == 32 ? mrf_stream_nz<T, LT, 32, 1> : nz == 64 ? mrf_stream_nz<T, LT, 64, 1>
+                                                                         : mrf_stream_nz<T, LT, 128, 1>;
+            auto k2 = nz == 32 ? mrf_stream_nz<T, LT, 32, 2> : nz == 64 ? mrf_stream_nz<T, LT, 64, 2>
+                                                                         : mrf_stream_nz<T, LT, 128, 2>;
+            k1<<<(unsigned)blocks, 256, 0, s>>>(v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal, lap);
+            if (int st = ct::check_launch("mrf_stream_nz")) return st;
+            delta_from_hist<<<1, 1024, 0, s>>>(hist, sizeof(T) == 1 ? 256 : 65536, state);
+            mrf_quick<<<1, 1, 0, s>>>(state, ni, w.scal);
+            k2<<<(unsigned)blocks, 256, 0, s>>>(v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal, lap);
+            if (int st = ct::check_launch("mrf_stream_nz (exact sigma)")) return st;
+            lap_mean<<<1, 1, 0, s>>>(state, (const long long *)&w.scal[W_LAPSUM], ni, &w.scal[W_SKIP]);
+            const int vs = pairwise_sum_lap<LT>(lap, &state[S_SUM1], ni, w.partial, &state[S_SUM2], s, &w.scal[W_SKIP]);
+            if (vs < 0) return -vs;
+            if (vs == 1) {
+                LapArrSq<LT> f{lap, &state[S_SUM1]};
+                if (int st = pairwise_sum(f, ni, w.partial, &state[S_SUM2], s, &w.scal[W_SKIP])) return st;
+            }
+            mrf_decide<<<1, 1, 0, s>>>(state, ni, w.scal, 1);
+            return ct::check_launch("mrf_decide");
+        }
         auto kern = nz == 32 ? mrf_stream_nz<T, LT, 32> : nz == 64 ? mrf_stream_nz<T, LT, 64> : mrf_stream_nz<T, LT, 128>;
         kern<<<(unsigned)blocks, 256, 0, s>>>(v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal, lap);
         if (int st = ct::check_launch("mrf_stream_nz")) return st;
@@ -1365,7 +1401,7 @@ extern "C" int ct_mrf(const void *in, int dtype, int64_t nx, int64_t ny, int64_t
 // full ct_mrf.
 extern "C" int ct_mrf_decide(const void *in, int dtype, int64_t nx, int64_t ny, int64_t nz, void *work,
                              double *state, uint64_t *hist, void *stream) {
-    if (dtype != CT_U8 || nx <= 0 || ny <= 0 || nz <= 0 || nx * ny * nz >= (1ll << 31) || !hist)
+    if ((dtype != CT_U8 && dtype != CT_U16) || nx <= 0 || ny <= 0 || nz <= 0 || nx * ny * nz >= (1ll << 31) || !hist)
         return ct_mrf(in, dtype, nx, ny, nz, work, state, hist, stream);
     cudaStream_t s = (cudaStream_t)stream;
     const i64 n = nx * ny * nz;
@@ -1373,6 +1409,8 @@ extern "C" int ct_mrf_decide(const void *in, int dtype, int64_t nx, int64_t ny, 
     cudaMemsetAsync(state, 0, S_WORDS * sizeof(double), s);
     cudaMemsetAsync(w.scal, 0, W_WORDS * 8, s);
     cudaMemsetAsync(&w.scal[W_BEST_BITS], 0xff, 8, s);
+    if (dtype == CT_U16)
+        return mrf_int<uint16_t>((const uint16_t *)in, nx, ny, nz, w, state, hist, s, true);
     return mrf_int<uint8_t>((const uint8_t *)in, nx, ny, nz, w, state, hist, s, true);
 }
 

@@ -165,7 +165,13 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     i64 nb = nbins_given;
     if (nb <= 0) {
         int hi = 0;
-        for (int b = 256 + tid; b < 65536; b += NT) hi |= hist[b] != 0;
+        for (int b0 = 256; b0 < 65536; b0 += 8 * NT) {  // 8 independent loads in flight
+            u64 hv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) hv[u] = b0 + u * NT + tid < 65536 ? hist[b0 + u * NT + tid] : 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) hi |= hv[u] != 0;
+        }
         if (__any_sync(0xffffffffu, hi) && (tid & 31) == 0) s_hi = 1;
         __syncthreads();
         nb = s_hi ? 65536 : 256;
@@ -181,15 +187,24 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     {
         u64 cw = 0, cs = 0;
         int lo = INT_MAX, hi = -1;
-        for (i64 R = 0; R < rounds; ++R) {
-            const i64 b = R * NT + tid;
-            const u64 h = b < nb ? hist[b] : 0;
-            cw += h;
-            cs += h * (u64)b;
-            nzc += h != 0;
-            if (h) {
-                lo = min(lo, (int)b);
-                hi = (int)b;
+        for (i64 R0 = 0; R0 < rounds; R0 += 8) {  // 8 independent loads in flight (65536 bins: 64 rounds)
+            u64 hv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const i64 b = (R0 + u) * NT + tid;
+                hv[u] = (R0 + u < rounds && b < nb) ? hist[b] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const i64 b = (R0 + u) * NT + tid;
+                const u64 h = hv[u];
+                cw += h;
+                cs += h * (u64)b;
+                nzc += h != 0;
+                if (h) {
+                    lo = min(lo, (int)b);
+                    hi = (int)b;
+                }
             }
         }
         for (int o = 16; o; o >>= 1) {
