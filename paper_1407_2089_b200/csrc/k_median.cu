@@ -13,9 +13,15 @@
 // pairs are one aligned LDS.32 plus one PRMT each.  The output histogram is
 // accumulated per CTA in SMEM (warp-aggregated with __match_any_sync) and
 // flushed once per persistent CTA.
+#include <cudaTypedefs.h>
+
+#include <cstring>
 #include <type_traits>
 
 #include "ct_common.cuh"
+#include "tc_common.cuh"
+
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder();  // k_gauss_tc.cu
 
 namespace {
 
@@ -258,10 +264,15 @@ __device__ __forceinline__ uint32_t zip16(uint32_t x) {
 // transposes from 32-bit loads instead of per-bit ballots: u8 4 voxels per
 // lane, nibble transposes over 8 lanes; u16 2 voxels per lane, pair
 // transposes over 16 lanes)
-template <typename T, int NB, int WC = 0>
+// TMA (WC > 0): the tile's (BTI+2) x (BTJ+2) input rows arrive as one 3-D
+// cp.async.bulk.tensor box ([i][j][z], rows out of the volume zero-filled and
+// then replaced by their clamped rows in SMEM), issued for the next tile as
+// soon as this tile's planes are built, so the load overlaps phases B and C.
+template <typename T, int NB, int WC = 0, bool TMA_IN = false>
 __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T *__restrict__ out, i64 nx, i64 ny,
-                                                    int nz_, uint64_t *__restrict__ ghist) {
-    extern __shared__ __align__(16) unsigned char dsm[];
+                                                    int nz_, uint64_t *__restrict__ ghist,
+                                                    const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) unsigned char dsm[];
     const int nz = WC > 0 ? 32 * WC : nz_;
     const int W = WC > 0 ? WC : (nz + 31) >> 5;
     const int RI = BTI + 2, RJ = BTJ + 2;
@@ -288,20 +299,58 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
     const int units = BTI * BTJ * W;
     const int last_w = (nz - 1) >> 5, last_pos = (nz - 1) & 31;
     int since_flush = 0;
+    // TMA input box: [RI][RJ][nz] elements after the planes and the histogram
+    constexpr int TBOX = TMA_IN ? (BTI + 2) * (BTJ + 2) * 32 * WC * (int)sizeof(T) : 0;
+    const T *tbuf = (const T *)(dsm + ((pbytes + (BYTE ? ct::ByteHist256::kBytes : 4096 * 4) + 127) & ~(size_t)127));
+    __shared__ uint64_t tbar;
+    uint32_t tphase = 0;
+    auto tma_issue = [&](i64 tile) {  // one thread
+        const int i0 = (int)((tile / tj) * BTI), j0 = (int)((tile % tj) * BTJ);
+        tc::fence_async_smem();  // earlier generic reads of the buffer before the async-proxy write
+        tc::mbar_expect_tx(&tbar, TBOX);
+        tc::tma_load_3d((void *)tbuf, &tmap, 0, j0 - 1, i0 - 1, &tbar);
+    };
+    if constexpr (TMA_IN) {
+        if (threadIdx.x == 0) {
+            tc::mbar_init(&tbar, 1);
+            tc::mbar_fence_init();
+            tc::tma_prefetch_desc(&tmap);
+            if ((i64)blockIdx.x < ntiles) tma_issue(blockIdx.x);
+        }
+        __syncthreads();
+    }
     const int per_thread = (units + 255) / 256;
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 i0 = (tile / tj) * BTI, j0 = (tile % tj) * BTJ;
         __syncthreads();
         if (threadIdx.x == 0) *s_any = 0;
         if constexpr (NB == 16 && WC > 0) {
-            // clamped row offsets of the tile's input rows, once per tile
+            // clamped row offsets of the tile's input rows, once per tile (TMA:
+            // rows in SMEM, out-of-volume rows replaced by their clamped rows)
             __shared__ long long roff16[(BTI + 2) * (BTJ + 2)];
-            for (int r = threadIdx.x; r < RI * RJ; r += 256) {
-                const int ri = r / RJ, rj = r - ri * RJ;
-                const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
-                roff16[r] = (i * ny + j) * nz;
+            if constexpr (TMA_IN) {
+                tc::mbar_wait(&tbar, tphase);
+                tphase ^= 1;
+                if (i0 == 0 || j0 == 0 || i0 + BTI >= nx || j0 + BTJ >= ny) {
+                    constexpr int RWD = 32 * WC * (int)sizeof(T) / 4;  // words per row
+                    uint32_t *tb = (uint32_t *)tbuf;
+                    for (int e = threadIdx.x; e < RI * RJ * RWD; e += 256) {
+                        const int r = e / RWD, wd = e - r * RWD, ri = r / RJ, rj = r - ri * RJ;
+                        const int ci = (int)(ct::clampi(i0 + ri - 1, 0, nx - 1) - (i0 - 1));
+                        const int cj = (int)(ct::clampi(j0 + rj - 1, 0, ny - 1) - (j0 - 1));
+                        if (ci != ri || cj != rj) tb[r * RWD + wd] = tb[(ci * RJ + cj) * RWD + wd];
+                    }
+                }
+                for (int r = threadIdx.x; r < RI * RJ; r += 256) roff16[r] = (long long)r * nz;
+            } else {
+                for (int r = threadIdx.x; r < RI * RJ; r += 256) {
+                    const int ri = r / RJ, rj = r - ri * RJ;
+                    const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
+                    roff16[r] = (i * ny + j) * nz;
+                }
             }
             __syncthreads();
+            const T *src16 = TMA_IN ? tbuf : in;
             // phase A (u16): a half warp per (row, word) unit, lane s loads
             // voxels 2s, 2s+1 of the word; zip16 + pair_transpose16 leave lane
             // s with plane s of the word
@@ -317,7 +366,8 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                     x[qq] = 0u;
                     if (u < NW) {
                         const int r = u / W, w = u - r * W;
-                        x[qq] = __ldg((const uint32_t *)(in + roff16[r] + 32 * w) + sub);
+                        x[qq] = TMA_IN ? *((const uint32_t *)(src16 + roff16[r] + 32 * w) + sub)
+                                       : __ldg((const uint32_t *)(in + roff16[r] + 32 * w) + sub);
                     }
                 }
 #pragma unroll
@@ -334,14 +384,33 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
             if (lane == 0 && anyw) atomicOr(s_any, anyw);
         } else if constexpr (NB == 8 && WC > 0) {
             // clamped row offsets of the tile's input rows, once per tile
-            // (the per-load clamp / divide was a third of phase A)
+            // (the per-load clamp / divide was a third of phase A); with TMA the
+            // rows are in SMEM: wait for the box, replace the rows outside the
+            // volume (zero-filled) by their clamped rows
             __shared__ long long roff[(BTI + 2) * (BTJ + 2)];
-            for (int r = threadIdx.x; r < RI * RJ; r += 256) {
-                const int ri = r / RJ, rj = r - ri * RJ;
-                const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
-                roff[r] = (i * ny + j) * nz;
+            if constexpr (TMA_IN) {
+                tc::mbar_wait(&tbar, tphase);
+                tphase ^= 1;
+                if (i0 == 0 || j0 == 0 || i0 + BTI >= nx || j0 + BTJ >= ny) {
+                    constexpr int RWD = 32 * WC * (int)sizeof(T) / 4;  // words per row
+                    uint32_t *tb = (uint32_t *)tbuf;
+                    for (int e = threadIdx.x; e < RI * RJ * RWD; e += 256) {
+                        const int r = e / RWD, wd = e - r * RWD, ri = r / RJ, rj = r - ri * RJ;
+                        const int ci = (int)(ct::clampi(i0 + ri - 1, 0, nx - 1) - (i0 - 1));
+                        const int cj = (int)(ct::clampi(j0 + rj - 1, 0, ny - 1) - (j0 - 1));
+                        if (ci != ri || cj != rj) tb[r * RWD + wd] = tb[(ci * RJ + cj) * RWD + wd];
+                    }
+                }
+                for (int r = threadIdx.x; r < RI * RJ; r += 256) roff[r] = (long long)r * nz;
+            } else {
+                for (int r = threadIdx.x; r < RI * RJ; r += 256) {
+                    const int ri = r / RJ, rj = r - ri * RJ;
+                    const i64 i = ct::clampi(i0 + ri - 1, 0, nx - 1), j = ct::clampi(j0 + rj - 1, 0, ny - 1);
+                    roff[r] = (i * ny + j) * nz;
+                }
             }
             __syncthreads();
+            const T *src = TMA_IN ? tbuf : in;
             // phase A (u8, nz = 32 WC): each lane loads 4 voxels (32 bits); a row
             // is 8 WC lanes; t4x8 + a nibble transpose over the 8 lanes of a
             // word leave lane s with plane s of that word
@@ -357,7 +426,8 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                     const int r = r0 + q * 8 * RPW + lrow;
                     x[q] = 0u;
                     if (r < NR && lrow < RPW)  // (WC = 3: lanes 24-31 idle)
-                        x[q] = __ldg((const uint32_t *)(in + roff[r]) + (lane % LPR));
+                        x[q] = TMA_IN ? *((const uint32_t *)(src + roff[r]) + (lane % LPR))
+                                      : __ldg((const uint32_t *)(in + roff[r]) + (lane % LPR));
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -408,6 +478,9 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
             }
         }
         __syncthreads();
+        // the planes are built: the next tile's input box may overwrite the TMA buffer
+        if constexpr (TMA_IN)
+            if (threadIdx.x == 0 && tile + gridDim.x < ntiles) tma_issue(tile + gridDim.x);
         // phase B: shifted versions (k-1 and k+1 neighbours, clamp-to-edge)
         for (int e = threadIdx.x; e < NB * NW; e += 256) {
             const int u = e % NW;
@@ -870,27 +943,51 @@ extern "C" int ct_median(const void *in, int dtype, int64_t nx, int64_t ny, int6
     }
     if (radius == 1 && (dtype == CT_U8 || dtype == CT_U16) && nz <= 128) {
         const int W = (int)((nz + 31) / 32);
+        const size_t es = dtype == CT_U8 ? 1 : 2;
         const size_t NW = (size_t)(BTI + 2) * (BTJ + 2) * W;
         const size_t pbytes = ((size_t)3 * (dtype == CT_U8 ? 8 : 16) * NW * 4 + 16 + 15) & ~(size_t)15;
-        const size_t sm = pbytes + (dtype == CT_U8 ? ct::ByteHist256::kBytes : 4096 * 4);
+        size_t sm = pbytes + (dtype == CT_U8 ? ct::ByteHist256::kBytes : 4096 * 4);
         const i64 tiles = ((nx + BTI - 1) / BTI) * ((ny + BTJ - 1) / BTJ);
         const int grid = (int)min(tiles, (i64)CT_NUM_SMS * 2);
+        const bool al4 = ((uintptr_t)in & 3) == 0;
+        // nz = 32 WC: the tile's input rows by TMA (3-D box [BTI+2][BTJ+2][nz])
+        CUtensorMap tm;
+        memset(&tm, 0, sizeof(tm));
+        bool tma = (nz == 32 || nz == 64 || nz == 96 || nz == 128) && ((uintptr_t)in & 15) == 0 &&
+                   nx < (1 << 30) && ny < (1 << 30);
+        if (tma) {
+            PFN_cuTensorMapEncodeTiled_v12000 encode = tma_encoder();
+            const cuuint64_t dims[3] = {(cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)nx};
+            const cuuint64_t strides[2] = {(cuuint64_t)(nz * es), (cuuint64_t)(ny * nz * es)};
+            const cuuint32_t box[3] = {(cuuint32_t)nz, BTJ + 2, BTI + 2}, est[3] = {1, 1, 1};
+            tma = encode && encode(&tm, es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                                   (void *)in, dims, strides, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+        if (tma) sm = ((sm + 127) & ~(size_t)127) + (size_t)(BTI + 2) * (BTJ + 2) * nz * es;
         if (dtype == CT_U8) {
-            const bool al4 = ((uintptr_t)in & 3) == 0;
-            auto k = (al4 && nz == 64) ? median3_bits<uint8_t, 8, 2>
-                     : (al4 && nz == 32) ? median3_bits<uint8_t, 8, 1>
-                     : (al4 && nz == 96) ? median3_bits<uint8_t, 8, 3>
-                     : (al4 && nz == 128) ? median3_bits<uint8_t, 8, 4> : median3_bits<uint8_t, 8, 0>;
+            auto k = !al4 ? median3_bits<uint8_t, 8, 0>
+                     : !tma ? median3_bits<uint8_t, 8, 0>
+                     : nz == 64 ? median3_bits<uint8_t, 8, 2, true>
+                     : nz == 32 ? median3_bits<uint8_t, 8, 1, true>
+                     : nz == 96 ? median3_bits<uint8_t, 8, 3, true> : median3_bits<uint8_t, 8, 4, true>;
+            if (al4 && !tma && nz % 32 == 0)
+                k = nz == 64 ? median3_bits<uint8_t, 8, 2> : nz == 32 ? median3_bits<uint8_t, 8, 1>
+                    : nz == 96 ? median3_bits<uint8_t, 8, 3> : median3_bits<uint8_t, 8, 4>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k<<<grid, 256, sm, s>>>((const uint8_t *)in, (uint8_t *)out, nx, ny, (int)nz, hist);
+            k<<<grid, 256, sm, s>>>((const uint8_t *)in, (uint8_t *)out, nx, ny, (int)nz, hist, tm);
         } else {
-            const bool al4 = ((uintptr_t)in & 3) == 0;
-            auto k = (al4 && nz == 64) ? median3_bits<uint16_t, 16, 2>
-                     : (al4 && nz == 32) ? median3_bits<uint16_t, 16, 1>
-                     : (al4 && nz == 96) ? median3_bits<uint16_t, 16, 3>
-                     : (al4 && nz == 128) ? median3_bits<uint16_t, 16, 4> : median3_bits<uint16_t, 16, 0>;
+            auto k = !al4 ? median3_bits<uint16_t, 16, 0>
+                     : !tma ? median3_bits<uint16_t, 16, 0>
+                     : nz == 64 ? median3_bits<uint16_t, 16, 2, true>
+                     : nz == 32 ? median3_bits<uint16_t, 16, 1, true>
+                     : nz == 96 ? median3_bits<uint16_t, 16, 3, true> : median3_bits<uint16_t, 16, 4, true>;
+            if (al4 && !tma && nz % 32 == 0)
+                k = nz == 64 ? median3_bits<uint16_t, 16, 2> : nz == 32 ? median3_bits<uint16_t, 16, 1>
+                    : nz == 96 ? median3_bits<uint16_t, 16, 3> : median3_bits<uint16_t, 16, 4>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k<<<grid, 256, sm, s>>>((const uint16_t *)in, (uint16_t *)out, nx, ny, (int)nz, hist);
+            k<<<grid, 256, sm, s>>>((const uint16_t *)in, (uint16_t *)out, nx, ny, (int)nz, hist, tm);
         }
         return ct::check_launch("median3_bits");
     }

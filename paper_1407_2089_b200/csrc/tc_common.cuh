@@ -145,6 +145,14 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tmap, 
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(mbar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tmap, int c0, int c1, int c2,
+                                            uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(mbar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *tmap, int c0, int c1, int c2, int c3,
                                             uint64_t *mbar) {
     asm volatile(
