@@ -226,29 +226,42 @@ __device__ __forceinline__ uint32_t t4x8(uint32_t x) {
     return x;
 }
 
+// Butterfly steps of the in-register transposes below.  Lane groups exchange
+// halves with the partner lane (shfl xor s); a lane whose bit s is clear keeps
+// its low parts and takes the partner's low parts shifted up, a lane with
+// bit s set keeps its high parts and takes the partner's high parts shifted
+// down.  Byte and half-word steps are one PRMT with a per-lane selector,
+// nibble / 2-bit steps two SELs and a LOP3 -- no per-step branch (ncu: the
+// select-by-branch form was 45% of the u16 median's stalls).
+template <int SH, uint32_t M>
+__device__ __forceinline__ uint32_t bfly_sel(uint32_t y, uint32_t o, bool hi) {  // SH-bit parts, mask M = low parts
+    const uint32_t a = hi ? (o >> SH) : y, b = hi ? y : (o << SH);
+    return (a & M) | (b & ~M);
+}
+
 // 8x8 nibble transpose across the 8 lanes of a group (lane s holds row s):
 // afterwards lane s holds nibble s of every lane's row (row t at nibble t).
 __device__ __forceinline__ uint32_t nib_transpose8(uint32_t y, unsigned sub) {
-#pragma unroll
-    for (int s = 4; s >= 1; s >>= 1) {
-        const uint32_t m = s == 4 ? 0x0000ffffu : (s == 2 ? 0x00ff00ffu : 0x0f0f0f0fu);
-        const uint32_t o = __shfl_xor_sync(0xffffffffu, y, s);
-        y = (sub & s) ? ((y & ~m) | ((o & ~m) >> (4 * s))) : ((y & m) | ((o & m) << (4 * s)));
-    }
-    return y;
+    uint32_t o = __shfl_xor_sync(0xffffffffu, y, 4);
+    y = __byte_perm(y, o, (sub & 4) ? 0x3276 : 0x5410);  // 16-bit parts
+    o = __shfl_xor_sync(0xffffffffu, y, 2);
+    y = __byte_perm(y, o, (sub & 2) ? 0x3715 : 0x6240);  // bytes
+    o = __shfl_xor_sync(0xffffffffu, y, 1);
+    return bfly_sel<4, 0x0f0f0f0fu>(y, o, sub & 1);      // nibbles
 }
 
 // 16x16 transpose of 2-bit elements across the 16 lanes of a half warp (lane
 // s holds row s; afterwards lane s holds element s of every lane's row, row t
 // at element t)
 __device__ __forceinline__ uint32_t pair_transpose16(uint32_t y, unsigned sub) {
-#pragma unroll
-    for (int s = 8; s >= 1; s >>= 1) {
-        const uint32_t m = s == 8 ? 0x0000ffffu : (s == 4 ? 0x00ff00ffu : (s == 2 ? 0x0f0f0f0fu : 0x33333333u));
-        const uint32_t o = __shfl_xor_sync(0xffffffffu, y, s);
-        y = (sub & s) ? ((y & ~m) | ((o & ~m) >> (2 * s))) : ((y & m) | ((o & m) << (2 * s)));
-    }
-    return y;
+    uint32_t o = __shfl_xor_sync(0xffffffffu, y, 8);
+    y = __byte_perm(y, o, (sub & 8) ? 0x3276 : 0x5410);  // 16-bit parts
+    o = __shfl_xor_sync(0xffffffffu, y, 4);
+    y = __byte_perm(y, o, (sub & 4) ? 0x3715 : 0x6240);  // bytes
+    o = __shfl_xor_sync(0xffffffffu, y, 2);
+    y = bfly_sel<4, 0x0f0f0f0fu>(y, o, sub & 2);         // nibbles
+    o = __shfl_xor_sync(0xffffffffu, y, 1);
+    return bfly_sel<2, 0x33333333u>(y, o, sub & 1);      // 2-bit elements
 }
 
 // two u16 values (low half, high half) -> bit 2b + e = value e's bit b

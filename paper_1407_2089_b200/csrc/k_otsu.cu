@@ -285,7 +285,8 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
                 s0 += cs;
                 cw += tw;
                 cs += ts;
-                if (t < nb - 1) best = fmax(best, score(w0, s0));
+                // an empty bin t repeats bin t-1's (w0, s0), hence its score
+                if (t < nb - 1 && (hb[u] != 0 || t == 0)) best = fmax(best, score(w0, s0));
             }
         }
     }
@@ -300,8 +301,11 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
     mine.t = -1;
     {
         u64 cw = 0, cs = 0;
-        auto visit = [&](i64 t, u64 w0, u64 s0) {
+        auto visit = [&](i64 t, u64 w0, u64 s0, u64 h) {
             if (t >= nb - 1) return;
+            // an empty bin t > 0 has bin t-1's (w0, s0): the same exact a^2/b,
+            // and the lower t wins ties -- never a strict improvement
+            if (h == 0 && t > 0) return;
             if (!(best <= 0.0) && !(score(w0, s0) >= cut)) return;
             consider(mine, t, w0, s0, W, S);  // rare: out of line
         };
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(NT) otsu_kernel(const uint64_t *__restrict__ h
                 s0 += cs;
                 cw += tw;
                 cs += ts;
-                visit(t, w0, s0);
+                visit(t, w0, s0, hb[u]);
             }
         }
     }
