@@ -418,7 +418,13 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     constexpr uint32_t LBO = 128, SBO = CB;         // MN-major: 8 K-rows = 128 B; next 16 columns = CB
     constexpr int CW = TN / 4;                      // (byte) columns per epilogue thread (4 column groups)
     constexpr int TV = TN / DB;                     // voxels per tile row
-    constexpr int OROW = TV + 16;                   // padded staged output row (bytes)
+    // staged output rows: DB = 1 (TV = 64): unpadded, 16-byte chunks XOR-swizzled
+    // by (row >> 1) & 3 -- a thread's 16-byte chunk stores (rows m) and the
+    // flush's chunk loads (rows mm, mm+1) then hit distinct banks (the padded
+    // layout cost 2-4-way conflicts, ~20% of pass x's stall samples);
+    // DB = 2 (TV = 16): one chunk per row, padded
+    constexpr bool SWZ = DB == 1 && TV == 64;
+    constexpr int OROW = SWZ ? TV : TV + 16;        // staged output row (bytes)
     constexpr int OBUF = NPO * TM * OROW;           // staged output tile: [NPO planes][128 rows]
     constexpr int CPR = TV / 16;                    // 16-byte chunks per output row
     const long long inner_v = inner / DB;           // voxels per input row
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                 const int i = ti * TM + mm;
                 if (i < L)
                     *(uint4 *)(out + pa * plane_out + ((long long)o * L + i) * inner_v + (long long)cb * TV + 16 * hh) =
-                        *(const uint4 *)(ob + (pa * TM + mm) * OROW + 16 * hh);
+                        *(const uint4 *)(ob + (pa * TM + mm) * OROW + 16 * (SWZ ? (hh ^ ((mm >> 1) & 3)) : hh));
             }
         };
         for (long long k = 0; k < nmine; ++k) {
@@ -594,6 +600,8 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
             if (lane == 0) tc::mbar_arrive(&aempty[a]);  // MMA(k + ASTG) may overwrite set a
             uint8_t *ob = sout + (int)(k & 1) * OBUF;
 #pragma unroll
+            uint32_t pw[NPO][4];  // SWZ: the thread's 16 columns of every plane, stored as one chunk
+#pragma unroll
             for (int g4 = 0; g4 < CW; g4 += 4 * DB) {
                 uint32_t ov[4], o4 = 0;
 #pragma unroll
@@ -612,8 +620,22 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                 uint32_t pl[4];
                 planes4(ov[0], ov[1], ov[2], ov[3], pl);
 #pragma unroll
-                for (int pa = 0; pa < 4; ++pa) *(uint32_t *)(ob + (pa * TM + m) * OROW + (h + g4) / DB) = pl[pa];
-                if constexpr (NPO == 5) *(uint32_t *)(ob + (4 * TM + m) * OROW + (h + g4) / DB) = o4;
+                if constexpr (SWZ) {
+#pragma unroll
+                    for (int pa = 0; pa < 4; ++pa) pw[pa][g4 / 4] = pl[pa];
+                    if constexpr (NPO == 5) pw[4][g4 / 4] = o4;
+                } else {
+#pragma unroll
+                    for (int pa = 0; pa < 4; ++pa) *(uint32_t *)(ob + (pa * TM + m) * OROW + (h + g4) / DB) = pl[pa];
+                    if constexpr (NPO == 5) *(uint32_t *)(ob + (4 * TM + m) * OROW + (h + g4) / DB) = o4;
+                }
+            }
+            if constexpr (SWZ) {
+                static_assert(!SWZ || CW == 16, "one 16-byte chunk per thread and plane");
+#pragma unroll
+                for (int pa = 0; pa < NPO; ++pa)
+                    *(uint4 *)(ob + (pa * TM + m) * OROW + 16 * (cg ^ ((m >> 1) & 3))) =
+                        make_uint4(pw[pa][0], pw[pa][1], pw[pa][2], pw[pa][3]);
             }
             epi_bar();  // tile k staged (and tile k-1's flush, issued before, finished by every thread)
             flush(k, ob);
@@ -968,7 +990,7 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
     // byte matrix [nx][ny nz RB]; box = 16 bytes x 256 x-rows, TX / 16 boxes
     // per tile (u16: TX bytes = TX / 2 voxels, both byte limbs)
     {
-        constexpr int TX = NL == 4 ? 64 : 32, SS = 6, AS = 1;  // TMEM: 64 NL band columns + NL TX accumulators
+        constexpr int TX = NL == 4 ? 64 : 32, SS = 6, AS = 1;  // TMEM: 64 NL band columns + NL TX accumulators (TX = 32 with two accumulator sets measured slower: 158 vs 138 us)
         CUtensorMap tm;
         const cuuint64_t dims[2] = {(cuuint64_t)(ny * nz * RB), (cuuint64_t)nx};
         const cuuint64_t strides[1] = {(cuuint64_t)(ny * nz * RB)};
