@@ -57,6 +57,24 @@ __host__ __device__ constexpr int lo_pair(int np, int nl = 4) { return np == 1 ?
 // n / d for a divisor fixed per kernel (round-up multiply-shift, exact for
 // every 32-bit n): the tile-coordinate divisions were ~20% of pass y's
 // instructions as plain 32-bit divides.
+// Tap band rows for TMEM: tb[b][128 + x] = limb b of Q_|x - r| for 0 <= x <= 2r
+// (0 elsewhere), so band word c of row m (K bytes 4c .. 4c+3, tap index
+// kk - r - m) is the 4 bytes at tb[b][128 + 4c - m]: two aligned loads and a
+// funnel shift instead of four compare-and-lookup byte builds.
+constexpr int TBW = 392;  // bytes per limb row (128 + 256 + pad)
+__device__ __forceinline__ void tap_rows(uint8_t (*tb)[TBW], const long long *Q, int r, int nl) {
+    for (int e = threadIdx.x; e < nl * TBW; e += blockDim.x) {
+        const int b = e / TBW, x = e - b * TBW - 128;
+        const int j = x - r;
+        tb[b][e - b * TBW] = (x >= 0 && x <= 2 * r) ? (uint8_t)((Q[j < 0 ? -j : j] >> (8 * b)) & 0xff) : 0;
+    }
+}
+__device__ __forceinline__ uint32_t band_word(const uint8_t *tbb, int c, int m) {
+    const int o = 128 + 4 * c - m;  // 1 .. 380
+    const uint32_t *w = (const uint32_t *)(tbb + (o & ~3));
+    return __funnelshift_r(w[0], w[1], 8 * (o & 3));
+}
+
 struct FastDiv {
     uint32_t d, m, s;
     __device__ explicit FastDiv(uint32_t d_) : d(d_) {
@@ -221,22 +239,17 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     const uint32_t base = tbase;
     const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
     // A (taps) into TMEM columns [0, AB): limb b (column group cg, cg + 4) at 64 b; row m
-    for (int b = cg; b < NL; b += 4) {
-        for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
-            uint32_t v[8];
+    {
+        __shared__ __align__(16) uint8_t tb[NL][TBW];
+        tap_rows(tb, prm->Q[axis], r, NL);
+        __syncthreads();
+        for (int b = cg; b < NL; b += 4)
+            for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
+                uint32_t v[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                uint32_t word = 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int kk = 4 * (c0 + i) + e, j = kk - r - m;
-                    const uint32_t byte = (j >= -r && j <= r) ? limb(Qs[j < 0 ? -j : j], b) : 0u;
-                    word |= byte << (8 * e);
-                }
-                v[i] = word;
+                for (int i = 0; i < 8; ++i) v[i] = band_word(tb[b], c0 + i, m);
+                tc::tmem_st8(lane_addr + b * 64 + c0, v);
             }
-            tc::tmem_st8(lane_addr + b * 64 + c0, v);
-        }
     }
     tc::tmem_st_wait();
 
@@ -457,24 +470,20 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     // column group cg = e / 4; it writes band limb cg of its rows into TMEM
     const int e_w = wp - 2, q = wp & 3, cg = e_w >> 2, m = 32 * q + lane;
     const uint32_t la = base + ((uint32_t)(32 * q) << 16);
-    if (wp >= 2)
-    for (int b = cg; b < NL; b += 4) {
-        for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
-            uint32_t v[8];
+    {
+        __shared__ __align__(16) uint8_t tb[NL][TBW];
+        tap_rows(tb, prm->Q[axis], r, NL);
+        __syncthreads();
+        if (wp >= 2) {
+            for (int b = cg; b < NL; b += 4)
+                for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
+                    uint32_t v[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                uint32_t word = 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int kk = 4 * (c0 + i) + e, j = kk - r - m;
-                    const uint32_t byte = (j >= -r && j <= r) ? limb(Qs[j < 0 ? -j : j], b) : 0u;
-                    word |= byte << (8 * e);
+                    for (int i = 0; i < 8; ++i) v[i] = band_word(tb[b], c0 + i, m);
+                    tc::tmem_st8(la + b * 64 + c0, v);
                 }
-                v[i] = word;
-            }
-            tc::tmem_st8(la + b * 64 + c0, v);
+            tc::tmem_st_wait();
         }
-        tc::tmem_st_wait();
     }
     tc::fence_before();
     __syncthreads();
