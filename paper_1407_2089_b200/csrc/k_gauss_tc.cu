@@ -75,6 +75,12 @@ __device__ __forceinline__ uint32_t band_word(const uint8_t *tbb, int c, int m) 
     return __funnelshift_r(w[0], w[1], 8 * (o & 3));
 }
 
+// 16-byte chunk hh of a staged row whose 8-byte units are XOR-swizzled by key
+__device__ __forceinline__ uint4 swz_chunk(const uint8_t *row, int hh, int key) {
+    const uint4 v = *(const uint4 *)(row + 16 * (hh ^ (key >> 1)));
+    return (key & 1) ? make_uint4(v.z, v.w, v.x, v.y) : v;
+}
+
 struct FastDiv {
     uint32_t d, m, s;
     __device__ explicit FastDiv(uint32_t d_) : d(d_) {
@@ -213,7 +219,13 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     static_assert(AB + NACC * TN <= 512, "TMEM: band + accumulators");
     constexpr uint32_t LBO = (TN / 16) * 128, SBO = 128;                // MN-major B
     constexpr int BUF = KXY * TN;                                       // bytes per plane per buffer
-    constexpr int OROW = TN + 16;                                       // padded output row (bytes)
+    // staged output rows (TN = 32): unpadded, the four 8-byte units of a row
+    // XOR-swizzled by (row >> 2) & 3 -- the epilogue's 8-byte stores (32
+    // consecutive rows, one unit) and the flush's 16-byte loads (4 rows x 2
+    // chunks) hit distinct banks; a chunk whose halves the swizzle swapped
+    // (odd key) is swapped back after the load
+    constexpr bool SWZ = TN == 32;
+    constexpr int OROW = SWZ ? TN : TN + 16;                            // output row (bytes)
     constexpr int CPR = TN / 16;                                        // 16-byte chunks per row
     constexpr int CW = TN / 4;                                          // columns per thread (epilogue)
     constexpr int OBUF = NPO * TM * OROW;                               // output tile: [NPO planes][128 rows]
@@ -273,7 +285,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
             const int i = ti * TM + mm;
             if (e < NPO * TM * CPR && i < L)
                 *(uint4 *)(out + a * plane_out + ((long long)o * L + i) * inner + (long long)cb * TN + 16 * hh) =
-                    *(const uint4 *)(ob + (a * TM + mm) * OROW + 16 * hh);
+                    SWZ ? swz_chunk(ob + (a * TM + mm) * OROW, hh, (mm >> 2) & 3)
+                        : *(const uint4 *)(ob + (a * TM + mm) * OROW + 16 * hh);
         }
     };
     // stage the B operand of a tile (cp.async): NPIN planes x 256 rows x 32 bytes
@@ -378,8 +391,9 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
             planes4(ov[0], ov[1], ov[2], ov[3], lo);
             planes4(ov[4], ov[5], ov[6], ov[7], hi);
 #pragma unroll
-            for (int a = 0; a < 4; ++a) *(uint2 *)(ob + (a * TM + m) * OROW + h + g8) = make_uint2(lo[a], hi[a]);
-            if constexpr (NPO == 5) *(uint2 *)(ob + (4 * TM + m) * OROW + h + g8) = make_uint2(o4[0], o4[1]);
+            const int uo = SWZ ? 8 * (((h + g8) >> 3) ^ ((m >> 2) & 3)) : h + g8;  // byte offset of the 8-byte unit
+            for (int a = 0; a < 4; ++a) *(uint2 *)(ob + (a * TM + m) * OROW + uo) = make_uint2(lo[a], hi[a]);
+            if constexpr (NPO == 5) *(uint2 *)(ob + (4 * TM + m) * OROW + uo) = make_uint2(o4[0], o4[1]);
         }
     }
     __syncthreads();
