@@ -768,6 +768,14 @@ __global__ void __launch_bounds__(SlideCfg<T, R>::NTC) median_slide(const T *__r
     uint32_t *stg = (uint32_t *)(ssm + C::HIST);                // [ROWS][RW] words
     const int t = threadIdx.x;
     auto H = [&](int b) -> uint16_t & { return hc[b * NTC + t]; };
+    // +-1 on a u16 counter as a 32-bit shared-memory reduction on the word that
+    // holds it (RED: the thread does not wait for it; program order keeps the
+    // later reads of its own counters after it; counts never underflow, so no
+    // borrow crosses into the neighbour's half)
+    auto hadd = [&](uint16_t *h, int b, int d) {
+        const int idx = b * NTC + t;
+        atomicAdd((unsigned *)h + (idx >> 1), (unsigned)d << (16 * (idx & 1)));
+    };
     auto F = [&](int b) -> uint16_t & { return hf[b * NTC + t]; };
     const i64 jt = (ny + NTC - 1) / NTC, ntiles = nx * jt;
     auto flush_run = [&](int v, unsigned c) {
@@ -791,12 +799,25 @@ __global__ void __launch_bounds__(SlideCfg<T, R>::NTC) median_slide(const T *__r
             // stage z in [k0 - R - 1, k0 - R - 1 + ZS) (clamped) of the tile's rows
             __syncthreads();
             const i64 zb = k0 - R - 1;
-            for (int e = t; e < C::ROWS * ZS; e += NTC) {
-                const int r = e / ZS, u = e - r * ZS;
-                const int di = r / (NTC + 2 * R), dj = r - di * (NTC + 2 * R);
-                const i64 ii = ct::clampi(i + di - R, 0, nx - 1), jj = ct::clampi(j0 + dj - R, 0, ny - 1);
-                const i64 kk = ct::clampi(zb + u, 0, nz - 1);
-                ((T *)(stg + r * RW))[u] = in[(ii * ny + jj) * nz + kk];
+            // 8 independent loads in flight per thread (one at a time, the
+            // staging was latency bound: ~12 dependent global loads per output)
+            constexpr int TOT = C::ROWS * ZS, UNR = 8;
+            for (int e0 = t; e0 < TOT; e0 += NTC * UNR) {
+                T v[UNR];
+#pragma unroll
+                for (int q = 0; q < UNR; ++q) {
+                    const int e = e0 + q * NTC;
+                    const int r = e / ZS, u = e - r * ZS;
+                    const int di = r / (NTC + 2 * R), dj = r - di * (NTC + 2 * R);
+                    const i64 ii = ct::clampi(i + di - R, 0, nx - 1), jj = ct::clampi(j0 + dj - R, 0, ny - 1);
+                    const i64 kk = ct::clampi(zb + u, 0, nz - 1);
+                    v[q] = e < TOT ? in[(ii * ny + jj) * nz + kk] : (T)0;
+                }
+#pragma unroll
+                for (int q = 0; q < UNR; ++q) {
+                    const int e = e0 + q * NTC;
+                    if (e < TOT) ((T *)(stg + (e / ZS) * RW))[e % ZS] = v[q];
+                }
             }
             __syncthreads();
             if (!live) continue;
@@ -818,16 +839,16 @@ __global__ void __launch_bounds__(SlideCfg<T, R>::NTC) median_slide(const T *__r
                         const int vo = sval(e / D, e % D, kc), vn = sval(e / D, e % D, kc + 2 * R + 1);
                         if (vo == vn) continue;
                         const int bo = U16 ? vo >> 8 : vo, bn = U16 ? vn >> 8 : vn;
-                        --H(bo);
-                        ++H(bn);
+                        hadd(hc, bo, -1);
+                        hadd(hc, bn, 1);
                         below += (bn < m) - (bo < m);
                         if constexpr (U16) {
                             if (bo == hcur) {
-                                --F(vo & 255);
+                                hadd(hf, vo & 255, -1);
                                 belowf -= (vo & 255) < mf;
                             }
                             if (bn == hcur) {
-                                ++F(vn & 255);
+                                hadd(hf, vn & 255, 1);
                                 belowf += (vn & 255) < mf;
                             }
                         }
