@@ -262,15 +262,16 @@ class FramePipeline:
         return g
 
     # -- host-side completion (synchronises) --------------------------------
-    def finish_cell(self, res: CellResult, materialize: bool = False, with_hull: bool = False):
-        """Raise reference errors; return (counters, rows) or Detections."""
+    def finish_cell(self, res: CellResult, materialize: bool = False, with_hull: bool = False, table=None):
+        """Raise reference errors; return (counters, rows) or Detections
+        (``table``: the (counters, rows) pair of an earlier call, not re-read)."""
         if int(res.otsu[OTSU_STATUS].item()) == 2:
             raise DegenerateHistogramError("frame is constant; no threshold separates it")
         cnt = res.cells.counters.cpu().numpy()
         if cnt[CNT_OVERFLOW]:
             raise RuntimeError("component capacity exceeded; raise FramePipeline(capacity=...)")
         if materialize:
-            return _materialize(res.cells, self.dims, self.spacing, res.frame, with_hull)
+            return _materialize(res.cells, self.dims, self.spacing, res.frame, with_hull, table)
         nk = int(cnt[CNT_KEPT])
         rows = res.cells.table[: nk * CELL_DTYPE.itemsize].cpu().numpy().view(CELL_DTYPE)
         return cnt, rows

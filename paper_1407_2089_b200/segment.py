@@ -320,25 +320,28 @@ def read_table(ct: CellTable):
     return cnt, rows
 
 
-def _materialize(ct: CellTable, dims, spacing: VoxelSpacing, frame: int, with_hull: bool = True):
-    cnt, rows = read_table(ct)
+def _materialize(ct: CellTable, dims, spacing: VoxelSpacing, frame: int, with_hull: bool = True, table=None):
+    """Detection objects of a cell table (``table`` = a (counters, rows) pair
+    already read back, else read here)."""
+    cnt, rows = table if table is not None else read_table(ct)
     if cnt[CNT_OVERFLOW]:
         return None
     nv = int(cnt[CNT_KEPT_VOXELS])
     _, ny, nz = dims
     lin = ct.voxels[:nv].to(torch.int64)
     coords = torch.stack((lin // (ny * nz), (lin // nz) % ny, lin % nz), dim=1).cpu().numpy()
-    # columns as Python scalars / one (n, 3) array up front: per-row structured
-    # field access dominated the host side of materialisation
-    offs, cnts = rows["voxel_offset"].tolist(), rows["count"].tolist()
+    # one C-level split into per-cell views (the voxel lists are concatenated
+    # in id order) and positional construction: per-row field access and
+    # keyword dataclass init dominated the host side of materialisation
+    cnts = rows["count"].astype(np.int64)
+    voxs = np.split(coords, np.cumsum(cnts)[:-1]) if len(cnts) else []
     ids, vols = rows["id"].tolist(), rows["volume_um3"].tolist()
-    cents = np.array(rows["centroid_um"], dtype=np.float64)
-    bbox = np.concatenate([rows["bbox_lo"], rows["bbox_hi"]], axis=1).astype(np.int64)
+    cents = list(np.array(rows["centroid_um"], dtype=np.float64))
+    bbox = list(np.concatenate([rows["bbox_lo"], rows["bbox_hi"]], axis=1).astype(np.int64))
     means = [None if m != m else m for m in rows["mean_intensity"].tolist()]  # NaN: no intensity given
-    voxs = [coords[offs[k] : offs[k] + cnts[k]] for k in range(len(offs))]
     hulls = compute_hulls(voxs, spacing) if with_hull else [None] * len(voxs)
-    return [Detection(id=ids[k], frame=frame, voxels=voxs[k], centroid_um=cents[k], volume_um3=vols[k],
-                      hull=hulls[k], bbox=bbox[k], mean_intensity=means[k]) for k in range(len(voxs))]
+    return [Detection(i, frame, v, c, vol, h, b, m)
+            for i, v, c, vol, h, b, m in zip(ids, voxs, cents, vols, hulls, bbox, means)]
 
 
 def _intensity_dev(intensity, shape):

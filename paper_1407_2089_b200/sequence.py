@@ -134,57 +134,124 @@ def assemble(local: list[FrameOut], t_count: int, group=None, gather_rows: str =
 
 
 def segment_frames(frames, load_cell, load_vessel=None, spacing=None, denoise_params=None, seg_config=None,
-                   mrf_max_iters: int = 1000, materialize: bool = True, with_hull: bool = True, pipe=None):
+                   mrf_max_iters: int = 1000, materialize: bool = True, with_hull: bool = True, pipe=None,
+                   depth: int = 2, on_frame=None):
     """The GPU half: every frame t in ``frames`` through the fused pipeline.
 
-    load_cell(t) / load_vessel(t) return the raw frame (numpy array or CUDA
-    tensor, uint8/uint16, (nx, ny, nz)).  Returns [FrameOut] with ids from 0.
-    The cell and vessel channels of a frame run on two streams; the host
-    reads a frame's results (rows, voxel lists) while nothing else is queued,
-    as the reference consumes them frame by frame."""
-    from . import _dev
-    from .pipeline import FramePipeline
+    load_cell(t) / load_vessel(t) return the raw frame (numpy array, pinned
+    host tensor or CUDA tensor, uint8/uint16, (nx, ny, nz)).  Returns
+    [FrameOut] with ids from 0, in frame order.
 
+    Pipelined ``depth`` frames deep (one FramePipeline per slot): frame t+1's
+    H2D copy and kernels are queued before the host reads frame t's results
+    (rows, voxel lists, Detection objects, hulls), so the host side of frame
+    t overlaps the device side of frame t+1.  The cell and vessel channels of
+    a frame run on two streams; a frame's completion is an event pair, and
+    its results are read on a host-side stream that waits only for those
+    events.  ``pipe`` (depth 1 only) reuses a caller's FramePipeline.
+    ``on_frame(fo)``: a streaming consumer -- each FrameOut is handed over as
+    soon as it is read back and not kept (the returned list is empty), so its
+    device copies are released frame by frame."""
+    from collections import deque
+
+    from . import _dev
     from .errors import ParameterError
+    from .pipeline import FramePipeline
 
     if spacing is None:
         raise ParameterError("segment_frames needs the experiment's voxel spacing")
-    out = []
+    depth = 1 if pipe is not None else max(1, int(depth))
     dev = _dev.require_cuda()
     s_cell = torch.cuda.Stream(dev, priority=-1)
     s_vess = torch.cuda.Stream(dev)
-    for t in frames:
-        raw_c = _dev.to_device(load_cell(t), allow=(torch.uint8, torch.uint16))
-        raw_v = _dev.to_device(load_vessel(t), allow=(torch.uint8, torch.uint16)) if load_vessel else None
-        for r in (raw_c, raw_v):
-            if r is not None and r.dtype not in (torch.uint8, torch.uint16):
+    s_copy = torch.cuda.Stream(dev)
+    s_host = torch.cuda.Stream(dev)
+    pipes = [pipe] if pipe is not None else []
+    slots = {}  # (slot, channel) -> device input buffer, reused every depth frames
+
+    def stage(x, key):
+        """Raw frame -> CUDA tensor: device tensors as they are, host frames
+        copied on s_copy into the slot's preallocated buffer (async from
+        pinned memory; allocating per frame made every copy wait for the
+        allocator)."""
+        if x is None:
+            return None
+        if not isinstance(x, torch.Tensor):
+            a = np.ascontiguousarray(np.asarray(x))
+            if a.dtype not in (np.uint8, np.uint16):
                 raise ParameterError("raw frames must be uint8 or uint16 (ref imaging.py:211-220 TIFF frames); "
                                      "run float grids through denoise/segment directly")
-        if pipe is None:
+            x = torch.from_numpy(a.view(np.int16)).view(torch.uint16) if a.dtype == np.uint16 else torch.from_numpy(a)
+        if x.dtype not in (torch.uint8, torch.uint16):
+            raise ParameterError("raw frames must be uint8 or uint16 (ref imaging.py:211-220 TIFF frames); "
+                                 "run float grids through denoise/segment directly")
+        if x.is_cuda:
+            return x.contiguous()
+        buf = slots.get(key)
+        if buf is None or buf.shape != x.shape or buf.dtype != x.dtype:
+            buf = slots[key] = torch.empty(x.shape, dtype=x.dtype, device=dev)
+        with torch.cuda.stream(s_copy):
+            buf.copy_(x, non_blocking=x.is_pinned())
+        return buf
+
+    def launch(k, t):
+        raw_c = stage(load_cell(t), (k % depth, 0))
+        raw_v = stage(load_vessel(t), (k % depth, 1)) if load_vessel else None
+        while len(pipes) <= k % depth:
             dt = "u8" if raw_c.dtype == torch.uint8 else "u16"
-            pipe = FramePipeline(tuple(raw_c.shape), dt, spacing, denoise_params, seg_config,
-                                 vessel=load_vessel is not None, device=dev)
-        main = torch.cuda.current_stream(dev)
-        s_cell.wait_stream(main)
-        s_vess.wait_stream(main)
+            pipes.append(FramePipeline(tuple(raw_c.shape), dt, spacing, denoise_params, seg_config,
+                                       vessel=load_vessel is not None, device=dev))
+        p = pipes[k % depth]
+        copied = torch.cuda.Event()
+        copied.record(s_copy)
+        s_cell.wait_event(copied)
+        s_vess.wait_event(copied)
         with torch.cuda.stream(s_cell):
-            cres = pipe.cell(raw_c, frame=t, id_start=0)
-        vres = None
+            cres = p.cell(raw_c, frame=t, id_start=0)
+            ev_c = torch.cuda.Event()
+            ev_c.record(s_cell)
+        vres, ev_v = None, None
         if raw_v is not None:
             with torch.cuda.stream(s_vess):
-                vres = pipe.vessel(raw_v)
-        main.wait_stream(s_cell)
-        main.wait_stream(s_vess)
-        cnt, rows = pipe.finish_cell(cres)
-        dets = pipe.finish_cell(cres, materialize=True, with_hull=with_hull) if materialize else None
-        fo = FrameOut(t=t, rows=rows, detections=dets)
-        if vres is not None:
-            mask, dmap = pipe.finish_vessel(vres, raw_v, max_iters=mrf_max_iters)
-            # the buffers are reused by the next frame: keep this frame's own copies
-            fo.vessel_mask = mask.clone()
-            dmap.values = dmap.values.clone()
-            fo.distance_map = dmap
-        out.append(fo)
+                vres = p.vessel(raw_v)
+                ev_v = torch.cuda.Event()
+                ev_v.record(s_vess)
+        return (t, p, raw_c, raw_v, cres, vres, ev_c, ev_v)
+
+    def finish(item):
+        t, p, raw_c, raw_v, cres, vres, ev_c, ev_v = item
+        with torch.cuda.stream(s_host):
+            s_host.wait_event(ev_c)
+            if ev_v is not None:
+                s_host.wait_event(ev_v)
+            cnt, rows = p.finish_cell(cres)
+            dets = p.finish_cell(cres, materialize=True, with_hull=with_hull, table=(cnt, rows)) if materialize else None
+            fo = FrameOut(t=t, rows=rows, detections=dets)
+            if vres is not None:
+                mask, dmap = p.finish_vessel(vres, raw_v, max_iters=mrf_max_iters)
+                # the slot's buffers are reused by a later frame: keep this frame's own
+                # copy of the map (the bool mask is already a new tensor)
+                fo.vessel_mask = mask
+                dmap.values = dmap.values.clone()
+                fo.distance_map = dmap
+            done = torch.cuda.Event()
+            done.record(s_host)
+        # the slot's next frame (k + depth) reads nothing of this one, but its
+        # input copy and kernels overwrite these buffers: they wait for the
+        # host's reads and copies
+        s_copy.wait_event(done)
+        s_cell.wait_event(done)
+        s_vess.wait_event(done)
+        return fo
+
+    out, inflight = [], deque()
+    emit = on_frame if on_frame is not None else out.append
+    for k, t in enumerate(frames):
+        inflight.append(launch(k, t))
+        if len(inflight) == depth:  # frame k+1 goes in before frame k-depth+1 is read back
+            emit(finish(inflight.popleft()))
+    while inflight:
+        emit(finish(inflight.popleft()))
     return out
 
 

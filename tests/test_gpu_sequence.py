@@ -18,8 +18,10 @@ pytestmark = pytest.mark.gpu
 ANISO = VoxelSpacing(0.8, 0.8, 1.0)
 
 
-@pytest.mark.parametrize("dtype", ["u8", "u16"])
-def test_segment_sequence_matches_reference_loop(cuda, dtype):
+@pytest.mark.parametrize("dtype,loader", [("u8", "numpy"), ("u16", "numpy"), ("u8", "pinned"), ("u16", "cuda")])
+def test_segment_sequence_matches_reference_loop(cuda, dtype, loader):
+    """Pipelined two frames deep (frame t+1 queued before frame t is read
+    back); numpy loaders copy synchronously, pinned / CUDA ones run async."""
     spec = synth.SceneSpec(128, 96, 32, dtype, n_cells=25, n_tubes=3, seed=21)
     T = 5
     frames_c = {t: synth.generate(spec, t, synth.CELL).cpu() for t in range(T)}
@@ -28,8 +30,17 @@ def test_segment_sequence_matches_reference_loop(cuda, dtype):
     def np_frame(x):
         return x.view(torch.int16).numpy().view(np.uint16) if x.dtype == torch.uint16 else x.numpy()
 
-    res = segment_sequence(lambda t: np_frame(frames_c[t]), T, load_vessel=lambda t: np_frame(frames_v[t]),
-                           spacing=ANISO, with_hull=True)
+    if loader == "numpy":
+        lc, lv = (lambda t: np_frame(frames_c[t])), (lambda t: np_frame(frames_v[t]))
+    elif loader == "pinned":
+        pc = {t: x.pin_memory() for t, x in frames_c.items()}
+        pv = {t: x.pin_memory() for t, x in frames_v.items()}
+        lc, lv = pc.__getitem__, pv.__getitem__
+    else:
+        dc = {t: x.cuda() for t, x in frames_c.items()}
+        dv = {t: x.cuda() for t, x in frames_v.items()}
+        lc, lv = dc.__getitem__, dv.__getitem__
+    res = segment_sequence(lc, T, load_vessel=lv, spacing=ANISO, with_hull=True)
     # the reference loop (session.py:295-306) through the drop-in API
     det_counter = 0
     params, seg = D.CellDenoiseParams(), S.SegmentationConfig()
