@@ -233,12 +233,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     uint8_t *sout = sm + STAGES * NPIN * BUF;
     __shared__ uint32_t tbase;
     __shared__ uint64_t mbar;
-    __shared__ long long Qs[PMAX];
     // thread t: TMEM row (lane) m = t % 128 of sub-partition (t / 32) % 4,
     // column group cg = t / 128
     const int t = threadIdx.x, wp = t >> 5, m = t & (TM - 1), cg = t >> 7;
     if (wp == 0) tc::tmem_alloc(&tbase, 512);
-    for (int j = t; j < PMAX; j += NT) Qs[j] = prm->Q[axis][j];
     if (t == 0) {
         tc::mbar_init(&mbar, 1);
         tc::mbar_fence_init();
@@ -460,10 +458,8 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     uint8_t *sout = sm + SSTG * SB;
     __shared__ uint64_t full[SSTG], empty[SSTG], afull[ASTG], aempty[ASTG];
     __shared__ uint32_t tbase;
-    __shared__ long long Qs[PMAX];
     const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
     if (wp == 1) tc::tmem_alloc(&tbase, 512);
-    for (int j = t; j < PMAX; j += WS_NT) Qs[j] = prm->Q[axis][j];
     if (t == 0) {
         for (int i = 0; i < SSTG; ++i) {
             tc::mbar_init(&full[i], 1);
