@@ -19,6 +19,21 @@ void set_error(const char *fmt, ...);
 // Return CT_ERR_CUDA (with message) if the last launch failed.
 int check_launch(const char *what);
 
+// n / d for a divisor fixed per kernel or per work item (round-up
+// multiply-shift, exact for every 32-bit n): runtime 32-bit divides were ~20%
+// of the instructions of the K1 tile loops and of the K6 bounding-box walk.
+struct FastDiv {
+    uint32_t d, m, s;
+    __device__ explicit FastDiv(uint32_t d_) : d(d_) {
+        s = 0;
+        while ((1ull << s) < d) ++s;
+        m = (uint32_t)(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return (uint32_t)(((unsigned long long)__umulhi(n, m) + n) >> s);
+    }
+};
+
 __host__ __device__ inline i64 clampi(i64 v, i64 lo, i64 hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 inline int grid_for(i64 n, int block, int max_blocks = CT_NUM_SMS * 16) {

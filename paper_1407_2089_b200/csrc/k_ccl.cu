@@ -738,11 +738,12 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
         const i64 off = table[r].voxel_offset;
         const unsigned nbox = bi * bj * bk;  // < 2^31 (volumes < 2^31 voxels)
         const unsigned bjk = bj * bk;
+        const ct::FastDiv fjk(bjk), fk(bk);
         i64 written = 0;
         double sx = 0.0, sy = 0.0, sz = 0.0;
         // candidate q -> linear index (32-bit index math; q < nbox)
         auto lin = [&](unsigned q) -> int32_t {
-            const unsigned a = q / bjk, rem = q - a * bjk, b = rem / bk, c = rem - b * bk;
+            const unsigned a = fjk.div(q), rem = q - a * bjk, b = fk.div(rem), c = rem - b * bk;
             return (int32_t)(((i64)(lo0 + (int)a) * ny + (lo1 + (int)b)) * nz + (lo2 + (int)c));
         };
         int32_t pn[TVB], ln[TVB];  // next round: linear indices and labels in flight
@@ -774,7 +775,7 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
                 const int nh = __popc(m);
                 if (hit) {
                     const unsigned q = q00 + 32 * u + lane;
-                    const unsigned a = q / bjk, rem = q - a * bjk, b = rem / bk, c = rem - b * bk;
+                    const unsigned a = fjk.div(q), rem = q - a * bjk, b = fk.div(rem), c = rem - b * bk;
                     double *slot = cs + 3 * __popc(m & ((1u << lane) - 1));
                     slot[0] = __dmul_rn((double)(lo0 + (int)a), dx);
                     slot[1] = __dmul_rn((double)(lo1 + (int)b), dy);

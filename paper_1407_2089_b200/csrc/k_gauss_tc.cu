@@ -54,9 +54,6 @@ constexpr int PMAX = 65;       // max taps per side + 1
 // always 5 accumulators (a + b = LOP .. LOP + 4)
 __host__ __device__ constexpr int lo_pair(int np, int nl = 4) { return np == 1 ? 0 : np + nl - 6; }
 
-// n / d for a divisor fixed per kernel (round-up multiply-shift, exact for
-// every 32-bit n): the tile-coordinate divisions were ~20% of pass y's
-// instructions as plain 32-bit divides.
 // Tap band rows for TMEM: tb[b][128 + x] = limb b of Q_|x - r| for 0 <= x <= 2r
 // (0 elsewhere), so band word c of row m (K bytes 4c .. 4c+3, tap index
 // kk - r - m) is the 4 bytes at tb[b][128 + 4c - m]: two aligned loads and a
@@ -80,18 +77,6 @@ __device__ __forceinline__ uint4 swz_chunk(const uint8_t *row, int hh, int key) 
     const uint4 v = *(const uint4 *)(row + 16 * (hh ^ (key >> 1)));
     return (key & 1) ? make_uint4(v.z, v.w, v.x, v.y) : v;
 }
-
-struct FastDiv {
-    uint32_t d, m, s;
-    __device__ explicit FastDiv(uint32_t d_) : d(d_) {
-        s = 0;
-        while ((1ull << s) < d) ++s;
-        m = (uint32_t)(((1ull << 32) * ((1ull << s) - d)) / d + 1);
-    }
-    __device__ __forceinline__ uint32_t div(uint32_t n) const {
-        return (uint32_t)(((unsigned long long)__umulhi(n, m) + n) >> s);
-    }
-};
 
 struct TcParams {
     long long Q[3][PMAX];  // integer taps per axis (Q[axis][|j|] = rint(w_j 2^fw[axis]))
@@ -266,7 +251,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     const int nti = (L + TM - 1) / TM, ncb = inner / TN;
     const long long ntiles = (long long)outer * nti * ncb;
     const uint32_t idesc = tc::idesc_i8(TM, TN, false, false, false, true);
-    const FastDiv fd_cb((unsigned)ncb), fd_ti((unsigned)nti);
+    const ct::FastDiv fd_cb((unsigned)ncb), fd_ti((unsigned)nti);
     auto tile_coords = [&](long long tile, int &o, int &ti, int &cb) {
         const unsigned tl = (unsigned)tile, r2 = fd_cb.div(tl);
         cb = (int)(tl - r2 * (unsigned)ncb);
@@ -503,7 +488,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     const long long ntiles = (long long)outer * nti * ncb;
     const long long t0 = blockIdx.x, gs = gridDim.x;
     const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
-    const FastDiv fd_cb((unsigned)ncb), fd_ti((unsigned)nti);
+    const ct::FastDiv fd_cb((unsigned)ncb), fd_ti((unsigned)nti);
     auto coords = [&](long long k, int &o, int &ti, int &cb) {
         const unsigned tl = (unsigned)(t0 + k * gs), r2 = fd_cb.div(tl);
         cb = (int)(tl - r2 * (unsigned)ncb);
