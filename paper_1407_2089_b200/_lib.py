@@ -16,7 +16,8 @@ import numpy as np
 from .errors import ParameterError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libct.so")
+# CT_LIB=debug loads the bounds-checked build (csrc: make debug), test tooling only
+LIB_PATH = os.path.join(_HERE, "libct_debug.so" if os.environ.get("CT_LIB") == "debug" else "libct.so")
 
 CT_U8, CT_U16, CT_I32, CT_F64 = 1, 2, 4, 8
 CT_OK, CT_ERR_PARAM, CT_ERR_CUDA, CT_ERR_UNSUPPORTED, CT_ERR_IO = 0, 1, 3, 4, 5

@@ -12,6 +12,24 @@ typedef uint64_t u64;
 
 #define CT_NUM_SMS 148
 
+// Device-side bounds checks of the debug build (make debug -> libct_debug.so,
+// -DCT_DEBUG; loaded when CT_LIB=debug): a failed check prints the site and
+// traps, so the launch fails with an error instead of corrupting memory.  The
+// stand-in for compute-sanitizer, which is closed on the GPU pool.  No-ops in
+// the product build.
+#ifdef CT_DEBUG
+#define CT_DCHECK(cond)                                                                  \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            printf("CT_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                            \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define CT_DCHECK(cond) ((void)0)
+#endif
+
 namespace ct {
 
 void set_error(const char *fmt, ...);

@@ -347,7 +347,10 @@ __global__ void ccl_run_emit(const uint8_t *__restrict__ mask, const R *__restri
             const R mr = run_mask(w, s);
             rem &= ~mr;
             const int32_t root = (int32_t)find_g(labels, (int)(r * nz + s));
-            for (R m = mr; m; m &= m - 1) fg[base + e++] = (int32_t)(r * nz + ct::rffs(m) - 1);
+            for (R m = mr; m; m &= m - 1) {
+                CT_DCHECK(base + e < nrows * (i64)nz);
+                fg[base + e++] = (int32_t)(r * nz + ct::rffs(m) - 1);
+            }
             // run starts hold the union-find links until every thread's find is done:
             // write the run's other voxels now, the start in a second sweep
             for (R m = mr & (mr - 1); m; m &= m - 1) labels[r * nz + ct::rffs(m) - 1] = root;
@@ -715,8 +718,10 @@ __global__ void tab_relabel(int32_t *labels, const int32_t *__restrict__ fg, con
                             TabWork w) {
     const i64 nfg = counters[CT_CNT_FG];
     const bool over = counters[CT_CNT_OVERFLOW] != 0;
-    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < nfg; e += (i64)gridDim.x * blockDim.x)
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < nfg; e += (i64)gridDim.x * blockDim.x) {
+        CT_DCHECK(over || (w.comp[e] >= 0 && w.comp[e] < counters[CT_CNT_COMPONENTS]));
         labels[fg[e]] = over ? -1 : w.rank[w.comp[e]];
+    }
 }
 
 // One warp per kept cell: bbox scan in C order with ballots (no block
@@ -769,6 +774,7 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
             for (int u = 0; u < TVB; ++u) {
                 const bool hit = lv[u] == (int32_t)r;
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
+                CT_DCHECK(!hit || written + __popc(m) <= table[r].count);  // a cell's list never outgrows its count
                 if (hit) voxels[off + written + __popc(m & ((1u << lane) - 1))] = pv[u];
                 // hits' coordinates compacted in list order into the warp's SMEM
                 // slots, then lane 0 continues the row-sequential sum
@@ -852,7 +858,10 @@ __global__ void __launch_bounds__(256) ccl_reset_prev(int32_t *__restrict__ labe
                                                       const int32_t *__restrict__ fg_list,
                                                       const int64_t *__restrict__ counters) {
     const i64 n = counters[CT_CNT_FG];
-    for (i64 e = blockIdx.x * 256ll + threadIdx.x; e < n; e += (i64)gridDim.x * 256) labels[fg_list[e]] = -1;
+    for (i64 e = blockIdx.x * 256ll + threadIdx.x; e < n; e += (i64)gridDim.x * 256) {
+        CT_DCHECK(fg_list[e] >= 0);
+        labels[fg_list[e]] = -1;
+    }
 }
 
 extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t nz, int32_t *labels,

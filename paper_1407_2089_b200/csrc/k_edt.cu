@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(ZRT, 8) edt_pass_zr(const int32_t *__restrict_
                     bg = gyz(pk_ld(K - 2, bp), dx, dy);
                 }
             }
+            CT_DCHECK(K < NZ);
             posS[K][t] = (uint8_t)x;
             if (K < SCZ) pkS[K][t] = px;
             ++K;
@@ -629,6 +630,7 @@ __global__ void __launch_bounds__(ZRT, 8) edt_pass_zr(const int32_t *__restrict_
                 cp = posS[e][t];
                 cg = gyz(pk_ld(e, cp), dx, dy);
             }
+            CT_DCHECK(cp - x + NZ >= 0 && cp - x + NZ < 2 * NZ);
             r[u] = __dsqrt_rn(__dadd_rn(cg, czt[cp - x + NZ]));
         }
         st_v4(dst + x0, r[0], r[1], r[2], r[3]);

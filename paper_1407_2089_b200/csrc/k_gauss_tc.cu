@@ -847,6 +847,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         if ((unsigned long long)((eps - V) & fmask) <= (unsigned long long)(2 * eps) &&
             ((long long)rv << zs) - V >= one - eps) {
             const unsigned long long at = atomicAdd(&fix[0], 1ull);
+            CT_DCHECK(l < nlines && h0 + c < NZ);
             if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
             else fix[1] = 1;
         }

@@ -563,6 +563,7 @@ __global__ void __launch_bounds__(256) median3_bits(const T *__restrict__ in, T 
                 for (int e = 0; e < 27; ++e) eq[e] &= ~(wv[e] ^ mb);
             }
             const i64 p0 = (i * ny + j) * nz + 32 * w;
+            CT_DCHECK(i < nx && j < ny && 32 * w < nz);
             const int nv = min(32, nz - 32 * w);
             if (NB == 8) {
                 u64 g8[4];
@@ -816,6 +817,7 @@ __global__ void __launch_bounds__(SlideCfg<T, R>::NTC) median_slide(const T *__r
 #pragma unroll
                 for (int q = 0; q < UNR; ++q) {
                     const int e = e0 + q * NTC;
+                    CT_DCHECK(e >= TOT || e / ZS < C::ROWS);
                     if (e < TOT) ((T *)(stg + (e / ZS) * RW))[e % ZS] = v[q];
                 }
             }
@@ -876,6 +878,7 @@ __global__ void __launch_bounds__(SlideCfg<T, R>::NTC) median_slide(const T *__r
                     while (belowf > rho) belowf -= F(--mf);
                     med = (m << 8) | mf;
                 }
+                CT_DCHECK(med >= 0 && med < (U16 ? 65536 : 256) && i < nx && j < ny);
                 out[(i * ny + j) * nz + k] = (T)med;
                 if (med == run_v) {
                     ++run_n;

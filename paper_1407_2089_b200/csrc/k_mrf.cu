@@ -785,6 +785,7 @@ __global__ void __launch_bounds__(256) mrf_stream_nz(const T *__restrict__ v, in
                 } else if (iint && j > 0 && j < ny - 1 && k > 0 && k < NZ - 1) {
                     const int l = (xm + xp + ym + yp + zm + zp) - 6 * c;
                     lsum += l;
+                    CT_DCHECK(i - 1 < nx - 2 && j - 1 < my && k - 1 < mz);
                     lap[((unsigned)(i - 1) * (unsigned)my + (unsigned)(j - 1)) * (unsigned)mz + (unsigned)(k - 1)] =
                         (LT)l;
                 }
