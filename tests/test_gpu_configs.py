@@ -361,3 +361,46 @@ def test_c5_sweep_points_vs_oracle(cuda, oracle, dims, dt, sigma, radius):
     om, odist, _ = oracle.segment_vessel(st["current"] if st["current"] is not None else vhost, sp)
     np.testing.assert_array_equal(mask.cpu().numpy(), om)
     np.testing.assert_array_equal(dm.values.cpu().numpy(), odist)
+
+
+def test_cuda_graph_replay_matches_eager(cuda, oracle):
+    """bench.py's timed loop replays per-frame CUDA graphs (FramePipeline.capture):
+    replays on two streams, alternating two captured input frames, give the
+    same results as the eager launches -- q, median, label volume, the cell
+    table, the vessel mask and distance map -- and the cell results equal the
+    oracle's."""
+    spec = synth.SceneSpec(256, 192, 64, "u8", n_cells=120, n_tubes=9, seed=11)
+    pipe = FramePipeline(spec.dims, "u8", ANISO)
+    raws = [{ch: synth.generate(spec, t, ch) for ch in (synth.CELL, synth.VESSEL)} for t in range(2)]
+    ref = []
+    for r in raws:  # eager results (also the warm-up capture needs)
+        cnt, rows = pipe.finish_cell(pipe.cell(r[synth.CELL]))
+        vres = pipe.vessel(r[synth.VESSEL])
+        torch.cuda.synchronize()
+        ref.append((pipe.q.clone(), pipe.med.clone(), pipe.labels.clone(), rows.copy(), vres.mask.clone(),
+                    vres.distance.clone()))
+    gc = [pipe.capture(lambda r=r: pipe.cell(r[synth.CELL])) for r in raws]
+    gv = [pipe.capture(lambda r=r: pipe.vessel(r[synth.VESSEL])) for r in raws]
+    s_cell = torch.cuda.Stream(priority=-1)
+    s_vess = torch.cuda.Stream()
+    for step in range(5):
+        i = step % 2
+        s_cell.wait_stream(torch.cuda.current_stream())
+        s_vess.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_cell):
+            gc[i].replay()
+        with torch.cuda.stream(s_vess):
+            gv[i].replay()
+        torch.cuda.current_stream().wait_stream(s_cell)
+        torch.cuda.current_stream().wait_stream(s_vess)
+        torch.cuda.synchronize()
+        q, med, lab, rows, vm, vd = ref[i]
+        assert torch.equal(pipe.q, q) and torch.equal(pipe.med, med) and torch.equal(pipe.labels, lab)
+        nk = len(rows)
+        got = pipe.table[: nk * rows.itemsize].cpu().numpy().view(rows.dtype)
+        assert got.tobytes() == rows.tobytes()
+        assert torch.equal(pipe.vmask, vm) and torch.equal(pipe.dist, vd)
+    host = host_frame(oracle, spec, 1, synth.CELL)
+    o = oracle.denoise_cell(host, SP, 10.0)
+    odets = oracle.segment_cell(o["denoised"], SP, frame=1, intensity=host)
+    assert [int(c) for c in ref[1][3]["count"]] == [d.voxel_count for d in odets]
