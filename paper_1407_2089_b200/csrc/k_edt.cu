@@ -344,6 +344,12 @@ __global__ void __launch_bounds__(LTB) edt_y_build(int16_t *__restrict__ di, i64
         for (int u = 0; u < PFB; ++u) v[u] = vn[u];
         __syncwarp(wm);
         if (x0 + PFB < ny) load(x0 + PFB, vn);
+        // most (i, k) lines see no foreground in most x-columns after pass x:
+        // skip a batch with no site in one test instead of one branch per entry
+        uint32_t any = 0;
+#pragma unroll
+        for (int u = 0; u < PFB; ++u) any |= (uint32_t)(uint16_t)v[u] ^ 0x8000u;
+        if (!any) continue;
 #pragma unroll
         for (int u = 0; u < PFB; ++u) {
             if (v[u] == NONE16) continue;
@@ -569,6 +575,12 @@ __global__ void __launch_bounds__(ZRT, 8) edt_pass_zr(const int32_t *__restrict_
             na = __ldg((const int4 *)(line + c + 8));
             nb = __ldg((const int4 *)(line + c + 12));
         }
+        // z-slices without foreground carry NONE32 in every line: skip such a
+        // batch in one test
+        uint32_t any = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) any |= (uint32_t)v[u] ^ 0x80000000u;
+        if (!any) continue;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int32_t px = v[u];
