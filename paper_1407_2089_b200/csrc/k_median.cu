@@ -747,12 +747,15 @@ constexpr int SZC = 32;  // outputs per z-chunk
 template <typename T, int R>
 struct SlideCfg {
     static constexpr int D = 2 * R + 1;
-    static constexpr int NTC = sizeof(T) == 1 ? 64 : 32;         // columns (threads) per CTA
+    // counters: a bin holds at most (2r+1)^3 window values -- 125 at r = 2 fits
+    // a byte (half the SMEM per column: more columns per SM), 343 at r = 3 not
+    using CT = typename std::conditional<(D * D * D < 256), uint8_t, uint16_t>::type;
+    static constexpr int NTC = sizeof(T) == 1 ? (sizeof(CT) == 1 ? 128 : 64) : (sizeof(CT) == 1 ? 64 : 32);
     static constexpr int ZS = SZC + 2 * R + 1;                   // staged z-extent per chunk
     static constexpr int W0 = (ZS * (int)sizeof(T) + 3) / 4;     // words per staged row
     static constexpr int RW = W0 | 1;                            // odd word stride
     static constexpr int ROWS = D * (NTC + 2 * R);               // staged rows
-    static constexpr size_t HIST = (sizeof(T) == 2 ? 2 : 1) * 256 * NTC * 2;
+    static constexpr size_t HIST = (sizeof(T) == 2 ? 2 : 1) * 256 * NTC * sizeof(CT);
     static constexpr size_t SMEM = HIST + (size_t)ROWS * RW * 4;
 };
 
@@ -764,20 +767,23 @@ __global__ void __launch_bounds__(SlideCfg<T, R>::NTC) median_slide(const T *__r
     constexpr int D = C::D, KTH = D * D * D / 2, NTC = C::NTC, ZS = C::ZS, RW = C::RW;
     constexpr bool U16 = sizeof(T) == 2;
     extern __shared__ __align__(16) unsigned char ssm[];
-    uint16_t *hc = (uint16_t *)ssm;                             // [256][NTC] direct (u8) / coarse (u16)
-    uint16_t *hf = hc + 256 * NTC;                              // [256][NTC] fine (u16)
+    using CT = typename C::CT;
+    CT *hc = (CT *)ssm;                                         // [256][NTC] direct (u8) / coarse (u16)
+    CT *hf = hc + 256 * NTC;                                    // [256][NTC] fine (u16)
     uint32_t *stg = (uint32_t *)(ssm + C::HIST);                // [ROWS][RW] words
     const int t = threadIdx.x;
-    auto H = [&](int b) -> uint16_t & { return hc[b * NTC + t]; };
-    // +-1 on a u16 counter as a 32-bit shared-memory reduction on the word that
-    // holds it (RED: the thread does not wait for it; program order keeps the
-    // later reads of its own counters after it; counts never underflow, so no
-    // borrow crosses into the neighbour's half)
-    auto hadd = [&](uint16_t *h, int b, int d) {
+    auto H = [&](int b) -> CT & { return hc[b * NTC + t]; };
+    // +-1 on a counter.  u16 counters: a 32-bit shared-memory reduction on the
+    // word that holds it (RED: the thread does not wait for it; program order
+    // keeps the later reads of its own counters after it; counts never
+    // underflow, so no borrow crosses into the neighbour's half).  u8 counters:
+    // a plain byte read-modify-write (four columns share a word)
+    auto hadd = [&](CT *h, int b, int d) {
         const int idx = b * NTC + t;
-        atomicAdd((unsigned *)h + (idx >> 1), (unsigned)d << (16 * (idx & 1)));
+        if constexpr (sizeof(CT) == 2) atomicAdd((unsigned *)h + (idx >> 1), (unsigned)d << (16 * (idx & 1)));
+        else h[idx] = (CT)(h[idx] + d);
     };
-    auto F = [&](int b) -> uint16_t & { return hf[b * NTC + t]; };
+    auto F = [&](int b) -> CT & { return hf[b * NTC + t]; };
     const i64 jt = (ny + NTC - 1) / NTC, ntiles = nx * jt;
     auto flush_run = [&](int v, unsigned c) {
         if (ghist && c) atomicAdd((unsigned long long *)&ghist[v], (unsigned long long)c);
@@ -800,25 +806,35 @@ __global__ void __launch_bounds__(SlideCfg<T, R>::NTC) median_slide(const T *__r
             // stage z in [k0 - R - 1, k0 - R - 1 + ZS) (clamped) of the tile's rows
             __syncthreads();
             const i64 zb = k0 - R - 1;
-            // 8 independent loads in flight per thread (one at a time, the
-            // staging was latency bound: ~12 dependent global loads per output)
-            constexpr int TOT = C::ROWS * ZS, UNR = 8;
-            for (int e0 = t; e0 < TOT; e0 += NTC * UNR) {
-                T v[UNR];
+            // a warp per staged row (clamped row pointer once per row), lanes
+            // along z (coalesced), ROWS / (warps) rows per warp with the
+            // loads of two rows in flight; per-element index math was ~30% of
+            // this kernel's instructions
+            {
+                constexpr int NWARP = NTC / 32, RPW = 2;  // rows per warp iteration
+                static_assert(ZS <= 64, "two lanes' worth of z per row");
+                const int lane = t & 31, wid = t >> 5;
+                const int k0c = (int)ct::clampi(zb + lane, 0, nz - 1), k1c = (int)ct::clampi(zb + 32 + lane, 0, nz - 1);
+                for (int r0 = wid * RPW; r0 < C::ROWS; r0 += NWARP * RPW) {
+                    T v[RPW][2];
 #pragma unroll
-                for (int q = 0; q < UNR; ++q) {
-                    const int e = e0 + q * NTC;
-                    const int r = e / ZS, u = e - r * ZS;
-                    const int di = r / (NTC + 2 * R), dj = r - di * (NTC + 2 * R);
-                    const i64 ii = ct::clampi(i + di - R, 0, nx - 1), jj = ct::clampi(j0 + dj - R, 0, ny - 1);
-                    const i64 kk = ct::clampi(zb + u, 0, nz - 1);
-                    v[q] = e < TOT ? in[(ii * ny + jj) * nz + kk] : (T)0;
-                }
+                    for (int q = 0; q < RPW; ++q) {
+                        const int r = r0 + q;
+                        const int di = r / (NTC + 2 * R), dj = r - di * (NTC + 2 * R);
+                        const T *row = in + (ct::clampi(i + di - R, 0, nx - 1) * ny +
+                                             ct::clampi(j0 + dj - R, 0, ny - 1)) * nz;
+                        v[q][0] = (r < C::ROWS && lane < ZS) ? row[k0c] : (T)0;
+                        v[q][1] = (r < C::ROWS && 32 + lane < ZS) ? row[k1c] : (T)0;
+                    }
 #pragma unroll
-                for (int q = 0; q < UNR; ++q) {
-                    const int e = e0 + q * NTC;
-                    CT_DCHECK(e >= TOT || e / ZS < C::ROWS);
-                    if (e < TOT) ((T *)(stg + (e / ZS) * RW))[e % ZS] = v[q];
+                    for (int q = 0; q < RPW; ++q) {
+                        const int r = r0 + q;
+                        if (r < C::ROWS) {
+                            T *dst = (T *)(stg + r * RW);
+                            if (lane < ZS) dst[lane] = v[q][0];
+                            if (32 + lane < ZS) dst[32 + lane] = v[q][1];
+                        }
+                    }
                 }
             }
             __syncthreads();
