@@ -80,6 +80,11 @@ typedef struct ct_cell {
 const char *ct_version(void);
 const char *ct_last_error(void);
 
+/* Stream-ordered fill of `bytes` bytes at dst with the byte `value` (the
+ * "caller zeroes" step of the accumulating histogram outputs, and the label
+ * volume's -1 background, without a framework memset). */
+int ct_memset(void *dst, int value, int64_t bytes, void *stream);
+
 /* Bytes of device workspace an entry point needs for an (nx,ny,nz) volume.
  * which: 0 ct_gaussian_residual, 1 ct_closing (radius>1), 2 ct_ccl26 +
  * ct_cell_table (per component capacity `cap`), 3 ct_edt, 4 ct_mrf. */

@@ -57,6 +57,7 @@ _P, _I64, _U64, _D, _INT, _SZ = (
 SIGNATURES = {
     "ct_version": (ctypes.c_char_p, []),
     "ct_last_error": (ctypes.c_char_p, []),
+    "ct_memset": (_INT, [_P, _INT, _I64, _P]),
     "ct_workspace_bytes": (_SZ, [_INT, _I64, _I64, _I64, _I64]),
     "ct_gaussian_residual": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _P, _INT, _P]),
     "ct_gaussian_q": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _INT, _INT, _INT, _P, _P, _P, _I64, _D, _INT, _P]),
@@ -142,8 +143,8 @@ def exported_symbols() -> list[str]:
 # bench's gpu_launches count
 LAUNCHES = {
     "ct_gaussian_residual": 3, "ct_gaussian_q": 8, "ct_to_f64": 1, "ct_median": 1, "ct_histogram": 1, "ct_otsu": 1,
-    "ct_threshold_close": 2, "ct_closing": 2, "ct_ccl26": 4, "ct_threshold_close_rows": 2, "ct_ccl26_rows": 4, "ct_cell_table": 6, "ct_voxel_runs": 3, "ct_mrf": 5, "ct_mrf_decide": 8,
-    "ct_mrf_step": 4, "ct_sign_sum": 1, "ct_edt": 4, "ct_synth_frame": 3,
+    "ct_threshold_close": 2, "ct_closing": 2, "ct_ccl26": 4, "ct_threshold_close_rows": 2, "ct_ccl26_rows": 5, "ct_cell_table": 6, "ct_voxel_runs": 3, "ct_mrf": 5, "ct_mrf_decide": 8,
+    "ct_mrf_step": 4, "ct_sign_sum": 1, "ct_edt": 4, "ct_synth_frame": 3, "ct_memset": 0,
 }
 launch_counter = {"enabled": False, "count": 0}
 

@@ -34,6 +34,16 @@ extern "C" const char *ct_version(void) { return "libct 0.1 sm_100a"; }
 
 extern "C" const char *ct_last_error(void) { return ct::g_err; }
 
+extern "C" int ct_memset(void *dst, int value, int64_t bytes, void *stream) {
+    if (bytes < 0 || (bytes > 0 && !dst)) {
+        ct::set_error("ct_memset: bad destination");
+        return CT_ERR_PARAM;
+    }
+    if (bytes && cudaMemsetAsync(dst, value, (size_t)bytes, (cudaStream_t)stream) != cudaSuccess)
+        return ct::check_launch("ct_memset");
+    return CT_OK;
+}
+
 extern "C" size_t ct_workspace_bytes(int which, int64_t nx, int64_t ny, int64_t nz, int64_t cap) {
     const int64_t N = nx * ny * nz;
     switch (which) {

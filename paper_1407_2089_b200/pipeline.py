@@ -128,7 +128,7 @@ class FramePipeline:
                 # -1 everywhere once; afterwards each frame's K5 resets only the
                 # previous frame's foreground (CT_LABELS_RESET: fg list + count
                 # kept in fg / counters), not the whole volume
-                self.labels.fill_(-1)
+                call("ct_memset", self.labels.data_ptr(), 0xFF, self.labels.numel() * 4, _dev.stream_handle())
         if vessel:
             self.mwork = E(workspace_bytes(4, nx, ny, nz, self.code), torch.uint8)
             self.state = Z(9, torch.float64)
@@ -176,7 +176,8 @@ class FramePipeline:
         nx, ny, nz = self.dims
         s = _dev.stream_handle()
         rx, ry, rz = self.r
-        self.hist.zero_()
+        # only the bins the median can touch: 256 for u8 (the reference's nbins), all 65536 for u16
+        call("ct_memset", self.hist.data_ptr(), 0, (256 if self.code == 1 else 65536) * 8, s)
         e = self._t0()
         if self.exact_k1:
             call("ct_gaussian_residual", raw.data_ptr(), self.code, nx, ny, nz, self.w.data_ptr(), rx, ry, rz,
@@ -223,7 +224,7 @@ class FramePipeline:
     def vessel(self, raw: torch.Tensor) -> VesselResult:
         nx, ny, nz = self.dims
         s = _dev.stream_handle()
-        self.vhist.zero_()
+        call("ct_memset", self.vhist.data_ptr(), 0, (256 if self.code == 1 else 65536) * 8, s)
         e = self._t0()
         call("ct_mrf_decide", raw.data_ptr(), self.code, nx, ny, nz, self.mwork.data_ptr(), self.state.data_ptr(),
              self.vhist.data_ptr(), s)
