@@ -462,6 +462,23 @@ def run_ours(args):
     total_vox = world * args.steps * nch * nvox
     value = total_vox / (ms_max / 1e3)
 
+    # --- overlapped per-stage times: the timed loop replays graphs (no
+    # per-stage events inside them), so the same two-stream schedule runs
+    # eagerly for a few steps with CUDA events around each stage on its stream
+    if not stage_ms:
+        pipe.marks = []
+        g_saved = dict(graphs)
+        graphs.clear()
+        for i in range(min(2 * ring, args.steps)):
+            step(args.warmup + i, coll=False, first=(i == 0))
+        main_s = torch.cuda.current_stream()
+        main_s.wait_stream(s_cell)
+        main_s.wait_stream(s_vess)
+        torch.cuda.synchronize()
+        stage_ms = pipe.stage_times_ms()
+        pipe.marks = None
+        graphs.update(g_saved)
+
     # --- serialized pass (one stream) for clean per-kernel times ----------
     pipe.marks = []
     for i in range(min(3, args.steps)):
@@ -534,7 +551,9 @@ def run_ours(args):
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"], "algorithmic_bytes_per_voxel": bb}
     roof.update({"stage": dom, "ms_serial": ms_dom, "ms_overlapped": stage_ms.get(dom),
-                 "timing": "CUDA events around the stage on its stream, serialized pass (3 time points)",
+                 "timing": "CUDA events around the stage on its stream inside bench.py: ms_serial = serialized pass "
+                           "(3 time points, the roofline's duration), ms_overlapped = the two-stream schedule of the "
+                           "timed loop run eagerly (2 x ring time points; the timed loop itself replays graphs)",
                  "traffic": ncu_traffic(dom, args.config),
                  "traffic_note": "DRAM bytes of the stage's kernels per volume, ncu launch list (profiles/)",
                  "share_of_step_serial": per_tp[dom] / sum(per_tp.values())})
