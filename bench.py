@@ -584,8 +584,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": spec.dtype, "data": "synthetic",
             "config": {"workload": desc, "global_batch": world, "parallelism": f"frame-sharded dp{world}",
                        "frames_per_s": world * args.steps / (ms_max / 1e3),
-                       "launch": "eager" if args.no_graphs else "CUDA graph per (frame slot, channel), replayed on "
-                                                                "the channel's stream",
+                       "launch": "CUDA graph per (frame slot, channel), replayed on the channel's stream"
+                                 if graphs else "eager",
                        "l2": f"inputs larger than L2: {nch * nvox * b / 1e6:.0f} MB/step from a ring of {ring} "
                              "distinct time points, plus GB-scale intermediates"},
             "parity": None if parity is None else parity["ok"], "parity_detail": parity,
