@@ -135,7 +135,7 @@ def assemble(local: list[FrameOut], t_count: int, group=None, gather_rows: str =
 
 def segment_frames(frames, load_cell, load_vessel=None, spacing=None, denoise_params=None, seg_config=None,
                    mrf_max_iters: int = 1000, materialize: bool = True, with_hull: bool = True, pipe=None,
-                   depth: int = 2, on_frame=None):
+                   depth: int = 2, on_frame=None, pipes=None):
     """The GPU half: every frame t in ``frames`` through the fused pipeline.
 
     load_cell(t) / load_vessel(t) return the raw frame (numpy array, pinned
@@ -148,7 +148,9 @@ def segment_frames(frames, load_cell, load_vessel=None, spacing=None, denoise_pa
     t overlaps the device side of frame t+1.  The cell and vessel channels of
     a frame run on two streams; a frame's completion is an event pair, and
     its results are read on a host-side stream that waits only for those
-    events.  ``pipe`` (depth 1 only) reuses a caller's FramePipeline.
+    events.  ``pipe`` (depth 1 only) reuses a caller's FramePipeline;
+    ``pipes`` (a list, filled on first use) keeps the slot pipelines across
+    calls (no per-call allocation of their buffers).
     ``on_frame(fo)``: a streaming consumer -- each FrameOut is handed over as
     soon as it is read back and not kept (the returned list is empty), so its
     device copies are released frame by frame."""
@@ -166,7 +168,10 @@ def segment_frames(frames, load_cell, load_vessel=None, spacing=None, denoise_pa
     s_vess = torch.cuda.Stream(dev)
     s_copy = torch.cuda.Stream(dev)
     s_host = torch.cuda.Stream(dev)
-    pipes = [pipe] if pipe is not None else []
+    if pipes is None:
+        pipes = [pipe] if pipe is not None else []
+    elif pipe is not None and not pipes:
+        pipes.append(pipe)
     slots = {}  # (slot, channel) -> device input buffer, reused every depth frames
 
     def stage(x, key):
