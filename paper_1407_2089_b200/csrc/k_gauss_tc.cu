@@ -821,6 +821,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         if (cg == 0) {
             edge_load(0);
             edge_store();
+            if (nmine > 1) edge_load(1);  // the edges are loaded one tile ahead of their store
         }
         tc::cp_wait_group<STAGES - 1>();
         tc::fence_async_smem();
@@ -834,8 +835,8 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     const int h0 = cg * CW;
     // q of one voxel (column h0 + c of line l) from its 5 accumulator words
     // and the raw value; flags it for the fix-up
-    auto qval = [&](const uint32_t v0, const uint32_t v1, const uint32_t v2, const uint32_t v3, const uint32_t v4,
-                    int c, uint32_t rv, long long l) -> uint32_t {
+    auto qslow = [&](const uint32_t v0, const uint32_t v1, const uint32_t v2, const uint32_t v3, const uint32_t v4,
+                     int c, uint32_t rv, long long l) -> uint32_t {
         const unsigned long long S = (unsigned long long)v0 + (unsigned long long)v1 * 0x100ull +
                                      (unsigned long long)v2 * 0x10000ull + (unsigned long long)v3 * 0x1000000ull +
                                      ((unsigned long long)v4 << 32);
@@ -853,10 +854,35 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         }
         return qv > 0 ? (uint32_t)qv : 0u;
     };
+    // The common case in 32-bit words.  With Y = S + half + eps (= V + 2^zs +
+    // eps) the certification test above is (Y mod 2^zs) <= 2 eps, and when it
+    // fails Y >> zs equals ceil(V / 2^zs) (no borrow from the low bits).  For
+    // 32 <= zs < 64 and 2 eps < 2^32: Y's high word hi, low word lo; the test
+    // is (hi & hmask) == 0 && lo <= 2 eps, bgq = hi >> (zs - 32).  Other
+    // parameters make the test always pass (every voxel takes qslow).  Y is
+    // assembled with three 32 x 32 -> 64-bit multiply-adds (IMAD.WIDE).
+    const bool fast = zs >= 32 && zs < 64 && 2 * eps < (1ll << 32);
+    const unsigned long long Cy = (unsigned long long)(half + eps);
+    const uint32_t hmask = fast ? (uint32_t)((1ull << (zs - 32)) - 1) : 0u, hsh = fast ? (uint32_t)(zs - 32) : 0u;
+    const uint32_t lot = fast ? (uint32_t)(2 * eps) : 0xffffffffu;
+    auto qval = [&](const uint32_t v0, const uint32_t v1, const uint32_t v2, const uint32_t v3, const uint32_t v4,
+                    int c, uint32_t rv, long long l) -> uint32_t {
+        unsigned long long Y = (((unsigned long long)v4 << 32) | v0) + Cy;
+        Y += (unsigned long long)v1 * 0x100u;
+        Y += (unsigned long long)v2 * 0x10000u;
+        Y += (unsigned long long)v3 * 0x1000000u;
+        const uint32_t hi = (uint32_t)(Y >> 32), lo = (uint32_t)Y;
+        const bool live = l < nlines;
+        const bool near = live && (hi & hmask) == 0 && lo <= lot;
+        if (__builtin_expect(__any_sync(0xffffffffu, near), 0)) {
+            if (near) return qslow(v0, v1, v2, v3, v4, c, rv, l);
+        }
+        const int qv = (int)rv - (int)(hi >> hsh);
+        return live && qv > 0 ? (uint32_t)qv : 0u;
+    };
     if constexpr (NZ <= 64) {
     // accumulators -> registers, edges of tile k+1, barrier, MMA(k+1), then the epilogue of k
     for (long long k = 0; k < nmine; ++k) {
-        if (cg == 0 && k + 1 < nmine) edge_load(k + 1);
         tc::mbar_wait(&mbar, phase);
         phase ^= 1;
         tc::fence_after();
@@ -867,7 +893,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
             for (int g8 = 0; g8 < CW; g8 += 8)
                 tc::tmem_ld8(lane_addr + NZ * acc + h0 + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
         tc::tmem_ld_wait();
-        if (cg == 0 && k + 1 < nmine) edge_store();  // MMA(k) has completed, MMA(k+1) not yet issued
+        if (cg == 0 && k + 1 < nmine) {  // MMA(k) has completed, MMA(k+1) not yet issued
+            edge_store();
+            if (k + 2 < nmine) edge_load(k + 2);
+        }
         // raw of tile k (slot k % STAGES) before the slot is restaged
         const long long l = (t0 + k * gs) * TM + m;
         const uint8_t *rl = sr + (int)(k % STAGES) * RBUF + (m * NZ + h0) * RB;
@@ -887,13 +916,12 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
         uint32_t qw[CW / VPW];
 #pragma unroll
         for (int c4 = 0; c4 < CW / VPW; ++c4) qw[c4] = 0;
-        if (l < nlines) {
+        // all lanes run qval (its vote is warp-wide); lines past the end yield 0
 #pragma unroll
-            for (int c = 0; c < CW; ++c)
-                qw[c / VPW] |= qval(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], c,
-                                    (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM, l)
-                               << (8 * RB * (c % VPW));
-        }
+        for (int c = 0; c < CW; ++c)
+            qw[c / VPW] |= qval(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], c,
+                                (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM, l)
+                           << (8 * RB * (c % VPW));
         uint8_t *qb = sq + (int)(k & 1) * RBUF + (m * NZ + h0) * RB;
 #pragma unroll
         for (int c4 = 0; c4 < CW / VPW; c4 += 2) *(uint2 *)(qb + 4 * c4) = make_uint2(qw[c4], qw[c4 + 1]);
@@ -902,7 +930,6 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     // long lines (NZ = 96): the accumulators do not fit in registers at once,
     // so the epilogue drains them in 8-column chunks before MMA(k+1) is issued
     for (long long k = 0; k < nmine; ++k) {
-        if (cg == 0 && k + 1 < nmine) edge_load(k + 1);
         tc::mbar_wait(&mbar, phase);
         phase ^= 1;
         tc::fence_after();
@@ -917,15 +944,16 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
             tc::tmem_ld_wait();
             const uint32_t r0w = *(const uint32_t *)(rl + g8), r1w = *(const uint32_t *)(rl + g8 + 4);
             uint32_t qw[2] = {0, 0};
-            if (l < nlines) {
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    qw[c >> 2] |= qval(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], g8 + c,
-                                       ((c < 4 ? r0w : r1w) >> (8 * (c & 3))) & 0xff, l) << (8 * (c & 3));
-            }
+            for (int c = 0; c < 8; ++c)
+                qw[c >> 2] |= qval(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], g8 + c,
+                                   ((c < 4 ? r0w : r1w) >> (8 * (c & 3))) & 0xff, l) << (8 * (c & 3));
             *(uint2 *)(qb + g8) = make_uint2(qw[0], qw[1]);
         }
-        if (cg == 0 && k + 1 < nmine) edge_store();
+        if (cg == 0 && k + 1 < nmine) {
+            edge_store();
+            if (k + 2 < nmine) edge_load(k + 2);
+        }
         tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
         tc::fence_async_smem();
         tc::fence_before();
@@ -944,6 +972,275 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
     __syncthreads();
     tc::fence_after();
     if (wp == 0) tc::tmem_dealloc(base, 512);
+}
+
+// ---------------------------------------------------------------------------
+// Pass z, warp-specialised (NZ in {32, 64, 96}).  Same arithmetic as
+// tc_pass_z; the roles are split so that no CTA-wide barrier couples them
+// (ncu on tc_pass_z: 39% issue active, the largest stall the __syncthreads
+// that gates each MMA behind the slowest epilogue warp):
+//   warp 0     TMA producer: per tile NCH boxes {16 B, 128 lines, NP planes}
+//              of P2 -> chunk c at c * NP * 2048 (plane a at + a * 2048, line
+//              l at + 16 l: the K-major no-swizzle layout with LBO = NP * 2048,
+//              SBO = 128) and the raw tile {NZ * RB bytes, 128 lines};
+//   warp 1     MMA issuer: waits the stage, the drained accumulators and the
+//              tile's edge block; commits to the stage's `empty` and to `afull`;
+//   warps 2-17 epilogue (TMEM lane quarter wp % 4, column group (wp - 2) / 4):
+//              drain the 5 accumulators in 8-column groups, release them
+//              (aempty), the cg = 0 warps then write the next tile's edge block
+//              into TMEM from its staged planes (efull), then q and the
+//              certification (IMAD.WIDE form, rare lanes through the exact
+//              test) with 16-byte stores straight to global memory.
+// One accumulator set (5 NZ columns) + one edge block (NP x 8 columns): the
+// edge block of tile k+1 is written after afull(k), i.e. after MMA(k) read it.
+// ---------------------------------------------------------------------------
+template <int NZ, int SSTG, typename Traw = uint8_t, int NP = 4, int NL = 4>
+__global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__ CUtensorMap tmp,
+                                                         const __grid_constant__ CUtensorMap tmr, long long nlines,
+                                                         const TcParams *__restrict__ prm, int r,
+                                                         Traw *__restrict__ q, unsigned long long *__restrict__ fix,
+                                                         long long cap) {
+    constexpr int RB = (int)sizeof(Traw);
+    constexpr int LOP = lo_pair(NP, NL), SPL = 8 * LOP;
+    constexpr int NCH = NZ / 16;
+    constexpr uint32_t LBOB = 128, SBOB = NCH * 128, SBOE = 256;  // taps (K-major, as tc_pass_z)
+    constexpr uint32_t PLB = TM * 16;                                // bytes per plane per chunk
+    constexpr uint32_t LBOA = NP * PLB, SBOA = 128;                  // staged data planes
+    constexpr int DB = NCH * NP * PLB;                               // data bytes per stage
+    constexpr int RBT = TM * NZ * RB;                                // raw bytes per stage
+    constexpr int SB = DB + RBT;
+    constexpr int BW = NZ * NZ, BE = NZ * 32;
+    constexpr int ACOL = 5 * NZ;
+    static_assert(ACOL + NP * 8 <= 512, "TMEM");
+    static_assert(NZ % 32 == 0 && NZ <= 96, "pass z tile");
+    constexpr int CW = NZ / 4;  // columns per epilogue thread
+    extern __shared__ __align__(1024) uint8_t sm[];  // [SSTG][SB] stages, [NL][BW] taps, [NL][BE] edge taps
+    uint8_t *sw = sm + SSTG * SB;
+    uint8_t *swe = sw + NL * BW;
+    __shared__ uint64_t full[SSTG], empty[SSTG], afull, aempty, efull;
+    __shared__ uint32_t tbase;
+    __shared__ long long Qs[PMAX], Ts[PMAX + 1];
+    const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
+    if (wp == 1) tc::tmem_alloc(&tbase, 512);
+    for (int j = t; j < PMAX; j += WS_NT) Qs[j] = j <= r ? prm->Q[2][j] : 0;
+    if (t == 0) {
+        for (int i = 0; i < SSTG; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1 + WS_EPI);  // the MMA commit + every epilogue warp (raw read)
+        }
+        tc::mbar_init(&afull, 1);
+        tc::mbar_init(&aempty, WS_EPI);
+        tc::mbar_init(&efull, 4);
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmp);
+        tc::tma_prefetch_desc(&tmr);
+    }
+    __syncthreads();
+    if (t == 0) {
+        Ts[PMAX] = 0;
+        for (int j = PMAX - 1; j >= 0; --j) Ts[j] = Ts[j + 1] + Qs[j];
+    }
+    __syncthreads();
+    for (int e = t; e < NZ * NZ; e += WS_NT) {
+        const int n = e / NZ, k = e - n * NZ;
+        const int d = k > n ? k - n : n - k;
+        const long long qv = d < PMAX ? Qs[d] : 0;
+#pragma unroll
+        for (int b = 0; b < NL; ++b) sw[b * BW + tc::kmajor_off(n, k, LBOB, SBOB)] = (uint8_t)limb(qv, b);
+    }
+    for (int e = t; e < NZ * 32; e += WS_NT) {
+        const int n = e >> 5, sl = e & 31, s16 = sl & 15;
+        const long long E = sl < 16 ? (n + 1 <= PMAX ? Ts[n + 1] : 0) : (NZ - n <= PMAX ? Ts[NZ - n] : 0);
+        const long long pc = E / 16 + (s16 < E % 16 ? 1 : 0);
+#pragma unroll
+        for (int b = 0; b < NL; ++b) swe[b * BE + tc::kmajor_off(n, sl, LBOB, SBOE)] = (uint8_t)limb(pc, b);
+    }
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t base = tbase;
+    const long long ntiles = (nlines + TM - 1) / TM;
+    const long long t0 = blockIdx.x, gs = gridDim.x;
+    const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
+
+    if (wp == 0) {
+        // ---- TMA producer ----
+        for (long long k = 0; k < nmine; ++k) {
+            const int s = (int)(k % SSTG);
+            tc::mbar_wait(&empty[s], (uint32_t)((k / SSTG) & 1) ^ 1u);
+            if (lane == 0) {
+                const int l0 = (int)((t0 + k * gs) * TM);
+                uint8_t *dst = sm + s * SB;
+                tc::mbar_expect_tx(&full[s], SB);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) tc::tma_load_3d(dst + c * NP * PLB, &tmp, 16 * c, l0, 0, &full[s]);
+                tc::tma_load_2d(dst + DB, &tmr, 0, l0, &full[s]);
+            }
+            __syncwarp();
+        }
+    } else if (wp == 1) {
+        // ---- MMA issuer ----
+        const uint32_t idesc = tc::idesc_i8(TM, NZ, false, false, false, false);
+        const uint64_t b0 = tc::smem_desc(tc::smem_u32(sw), LBOB, SBOB);
+        const uint64_t be = tc::smem_desc(tc::smem_u32(swe), LBOB, SBOE);
+        for (long long k = 0; k < nmine; ++k) {
+            const int s = (int)(k % SSTG);
+            tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
+            tc::mbar_wait(&aempty, (uint32_t)(k & 1) ^ 1u);
+            tc::mbar_wait(&efull, (uint32_t)(k & 1));
+            tc::fence_after();
+            if (tc::elect_one()) {
+                const uint64_t a0 = tc::smem_desc(tc::smem_u32(sm + s * SB), LBOA, SBOA);
+                bool first[5] = {true, true, true, true, true};
+#pragma unroll
+                for (int a = 0; a < NP; ++a)
+#pragma unroll
+                    for (int b = 0; b < NL; ++b) {
+                        const int acc = a + b - LOP;
+                        if (acc < 0 || acc > 4) continue;
+#pragma unroll
+                        for (int ks = 0; ks < NZ / 32; ++ks)
+                            tc::mma_i8_ss(base + NZ * acc, a0 + (uint64_t)((a * PLB + ks * 2 * LBOA) >> 4),
+                                          b0 + (uint64_t)((b * BW + ks * 2 * LBOB) >> 4), idesc,
+                                          first[acc] && ks == 0 ? 0u : 1u);
+                        tc::mma_i8_ts(base + NZ * acc, base + ACOL + a * 8, be + (uint64_t)((b * BE) >> 4), idesc, 1u);
+                        first[acc] = false;
+                    }
+                tc::mma_commit(&empty[s]);
+                tc::mma_commit(&afull);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---- epilogue: line m of every tile, columns [h0, h0 + CW) ----
+        const int qq = wp & 3, cg = (wp - 2) >> 2, m = 32 * qq + lane, h0 = cg * CW;
+        const uint32_t la = base + ((uint32_t)(32 * qq) << 16);
+        const long long eps = prm->eps;
+        const int zs = prm->fw[2] + prm->fd - SPL;
+        const long long half = 1ll << (zs - 1), one = 1ll << zs, fmask = one - 1;
+        const bool fast = zs >= 32 && zs < 64 && 2 * eps < (1ll << 32);
+        const unsigned long long Cy = (unsigned long long)(half + eps);
+        const uint32_t hmask = fast ? (uint32_t)((1ull << (zs - 32)) - 1) : 0u, hsh = fast ? (uint32_t)(zs - 32) : 0u;
+        const uint32_t lot = fast ? (uint32_t)(2 * eps) : 0xffffffffu;
+        // the edge block of tile k (cg = 0 warps): staged edge bytes -> TMEM slots
+        auto edge = [&](long long k) {
+            const int s = (int)(k % SSTG);
+            tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
+            const uint8_t *st = sm + s * SB + m * 16;
+#pragma unroll
+            for (int a = 0; a < NP; ++a) {
+                const uint32_t w0 = 0x01010101u * st[a * PLB], wl = 0x01010101u * st[(NCH - 1) * NP * PLB + a * PLB + 15];
+                const uint32_t v[8] = {w0, w0, w0, w0, wl, wl, wl, wl};
+                tc::tmem_st8(la + ACOL + a * 8, v);
+            }
+            tc::tmem_st_wait();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&efull);
+        };
+        if (cg == 0 && nmine > 0) edge(0);
+        // exact test and quantisation of one voxel from S (rare lanes)
+        auto qslow = [&](unsigned long long S, int c, uint32_t rv, long long l) -> uint32_t {
+            const long long V = (long long)S - half;
+            const int bgq = (int)((V + fmask) >> zs);
+            const int qv = (int)rv - bgq;
+            if ((unsigned long long)((eps - V) & fmask) <= (unsigned long long)(2 * eps) &&
+                ((long long)rv << zs) - V >= one - eps) {
+                const unsigned long long at = atomicAdd(&fix[0], 1ull);
+                CT_DCHECK(l < nlines && h0 + c < NZ);
+                if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
+                else fix[1] = 1;
+            }
+            return qv > 0 ? (uint32_t)qv : 0u;
+        };
+        for (long long k = 0; k < nmine; ++k) {
+            const int s = (int)(k % SSTG);
+            const long long l = (t0 + k * gs) * TM + m;
+            const bool live = l < nlines;
+            tc::mbar_wait(&afull, (uint32_t)(k & 1));
+            tc::fence_after();
+            // Y = S + half + eps per column, from the accumulators in 8-column groups
+            uint32_t yh[CW], yl[CW];
+#pragma unroll
+            for (int g8 = 0; g8 < CW; g8 += 8) {
+                uint32_t v[5][8];
+#pragma unroll
+                for (int acc = 0; acc < 5; ++acc) tc::tmem_ld8(la + NZ * acc + h0 + g8, v[acc]);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    unsigned long long Y = (((unsigned long long)v[4][c] << 32) | v[0][c]) + Cy;
+                    Y += (unsigned long long)v[1][c] * 0x100u;
+                    Y += (unsigned long long)v[2][c] * 0x10000u;
+                    Y += (unsigned long long)v[3][c] * 0x1000000u;
+                    yh[g8 + c] = (uint32_t)(Y >> 32);
+                    yl[g8 + c] = (uint32_t)Y;
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&aempty);  // MMA(k+1) may overwrite the accumulators
+            if (cg == 0 && k + 1 < nmine) edge(k + 1);
+            // raw of the tile (stage s, already landed: MMA(k) consumed it), then release the stage
+            tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
+            // the thread's CW * RB raw / q bytes move in 16-byte chunks (8-byte when
+            // h0 * RB is not 16-aligned: NZ = 96)
+            constexpr int QW = CW * RB / 4;  // 32-bit words
+            static_assert(CW * RB % 8 == 0, "raw row chunk");
+            uint32_t rw[QW];
+            const uint8_t *rl = sm + s * SB + DB + (m * NZ + h0) * RB;
+            if constexpr (CW * RB % 16 == 0) {
+#pragma unroll
+                for (int i = 0; i < QW / 4; ++i) {
+                    const uint4 x = *(const uint4 *)(rl + 16 * i);
+                    rw[4 * i] = x.x; rw[4 * i + 1] = x.y; rw[4 * i + 2] = x.z; rw[4 * i + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < QW / 2; ++i) {
+                    const uint2 x = *(const uint2 *)(rl + 8 * i);
+                    rw[2 * i] = x.x; rw[2 * i + 1] = x.y;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&empty[s]);
+            constexpr int VPW = 4 / RB;
+            constexpr uint32_t VM = RB == 1 ? 0xffu : 0xffffu;
+            uint32_t qw[QW];
+#pragma unroll
+            for (int i = 0; i < QW; ++i) qw[i] = 0;
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+                const uint32_t rv = (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM;
+                const bool near = live && (yh[c] & hmask) == 0 && yl[c] <= lot;
+                uint32_t qv;
+                if (__builtin_expect(__any_sync(0xffffffffu, near), 0) && near) {
+                    const unsigned long long Y = ((unsigned long long)yh[c] << 32) | yl[c];
+                    qv = qslow(Y - Cy, c, rv, l);
+                } else {
+                    const int d = (int)rv - (int)(yh[c] >> hsh);
+                    qv = live && d > 0 ? (uint32_t)d : 0u;
+                }
+                qw[c / VPW] |= qv << (8 * RB * (c % VPW));
+            }
+            if (live) {
+                uint8_t *dst = (uint8_t *)q + (l * NZ + h0) * RB;
+                if constexpr (CW * RB % 16 == 0) {
+#pragma unroll
+                    for (int i = 0; i < QW / 4; ++i)
+                        *(uint4 *)(dst + 16 * i) = make_uint4(qw[4 * i], qw[4 * i + 1], qw[4 * i + 2], qw[4 * i + 3]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < QW / 2; ++i) *(uint2 *)(dst + 8 * i) = make_uint2(qw[2 * i], qw[2 * i + 1]);
+                }
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (wp == 1) tc::tmem_dealloc(base, 512);
 }
 
 }  // namespace
@@ -1028,8 +1325,41 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
                                                                    N);
         if (int st = ct::check_launch("tc_pass_y")) return st;
     }
-    // pass z + epilogue
+    // pass z + epilogue: warp-specialised, operands by TMA
     {
+        const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
+        CUtensorMap tp, tr;
+        const cuuint64_t pdims[3] = {(cuuint64_t)nz, (cuuint64_t)lines, (cuuint64_t)NP};
+        const cuuint64_t pstr[2] = {(cuuint64_t)nz, (cuuint64_t)N};
+        const cuuint32_t pbox[3] = {16, TM, NP}, es3[3] = {1, 1, 1};
+        const cuuint64_t rdims[2] = {(cuuint64_t)(nz * RB), (cuuint64_t)lines};
+        const cuuint64_t rstr[1] = {(cuuint64_t)(nz * RB)};
+        const cuuint32_t rbox[2] = {(cuuint32_t)(nz * RB), TM}, es2[2] = {1, 1};
+        if (encode(&tp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)p2, pdims, pstr, pbox, es3,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+            encode(&tr, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)raw, rdims, rstr, rbox, es2,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            ct::set_error("tensor map (pass z) rejected");
+            return CT_ERR_UNSUPPORTED;
+        }
+        void (*kz)(const CUtensorMap, const CUtensorMap, long long, const TcParams *, int, Traw *,
+                   unsigned long long *, long long);
+        int stg;
+        if constexpr (RB == 2) {
+            stg = 3;
+            kz = nz == 64 ? tc_pass_z_ws<64, 3, Traw, 5, 5> : tc_pass_z_ws<32, 3, Traw, 5, 5>;
+        } else {
+            stg = nz == 96 ? 2 : 4;
+            kz = nz == 64 ? tc_pass_z_ws<64, 4, Traw> : nz == 96 ? tc_pass_z_ws<96, 2, Traw> : tc_pass_z_ws<32, 4, Traw>;
+        }
+        const size_t sm = (size_t)stg * (NP * TM * nz + TM * nz * RB) + NL * nz * nz + NL * nz * 32 + 1024;
+        cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kz<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tp, tr, lines, prm, rz, q, fix, cap);
+        if (int st = ct::check_launch("tc_pass_z")) return st;
+    }
+    if (false) {
         const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
         const int stg = RB == 2 ? 2 : nz == 96 ? 2 : 4;
         const size_t sm = NL * nz * nz + NL * nz * 32 + (size_t)stg * (NP * TM * nz + TM * nz * RB) +
