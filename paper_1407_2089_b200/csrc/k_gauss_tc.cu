@@ -994,6 +994,24 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ i
 // One accumulator set (5 NZ columns) + one edge block (NP x 8 columns): the
 // edge block of tile k+1 is written after afull(k), i.e. after MMA(k) read it.
 // ---------------------------------------------------------------------------
+// The exact test and quantisation of one pass-z voxel from S (tc_pass_z's
+// qval): out of line, so the rare lanes that need it cost the fast epilogue
+// no registers.
+__device__ __noinline__ uint32_t qz_exact(const TcParams *__restrict__ prm, int spl, unsigned long long S, uint32_t rv,
+                                          unsigned long long idx, unsigned long long *__restrict__ fix, long long cap) {
+    const long long eps = prm->eps;
+    const int zs = prm->fw[2] + prm->fd - spl;
+    const long long half = 1ll << (zs - 1), one = 1ll << zs, fmask = one - 1;
+    const long long V = (long long)S - half;
+    const int qv = (int)rv - (int)((V + fmask) >> zs);
+    if ((unsigned long long)((eps - V) & fmask) <= (unsigned long long)(2 * eps) && ((long long)rv << zs) - V >= one - eps) {
+        const unsigned long long at = atomicAdd(&fix[0], 1ull);
+        if ((long long)at < cap) fix[2 + at] = idx;
+        else fix[1] = 1;
+    }
+    return qv > 0 ? (uint32_t)qv : 0u;
+}
+
 template <int NZ, int SSTG, typename Traw = uint8_t, int NP = 4, int NL = 4>
 __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__ CUtensorMap tmp,
                                                          const __grid_constant__ CUtensorMap tmr, long long nlines,
@@ -1116,13 +1134,17 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
         // ---- epilogue: line m of every tile, columns [h0, h0 + CW) ----
         const int qq = wp & 3, cg = (wp - 2) >> 2, m = 32 * qq + lane, h0 = cg * CW;
         const uint32_t la = base + ((uint32_t)(32 * qq) << 16);
+        // Y = S + half + eps: the certification test is (Y mod 2^zs) <= 2 eps and,
+        // when it fails, Y >> zs = ceil((S - half) / 2^zs) (see tc_pass_z).  For
+        // 32 <= zs < 64 and 2 eps < 2^32 the fast path reads bgq from Y's high
+        // word and tests the top 32 fractional bits conservatively; otherwise
+        // (fth = ~0) every voxel takes the exact path
         const long long eps = prm->eps;
         const int zs = prm->fw[2] + prm->fd - SPL;
-        const long long half = 1ll << (zs - 1), one = 1ll << zs, fmask = one - 1;
         const bool fast = zs >= 32 && zs < 64 && 2 * eps < (1ll << 32);
-        const unsigned long long Cy = (unsigned long long)(half + eps);
-        const uint32_t hmask = fast ? (uint32_t)((1ull << (zs - 32)) - 1) : 0u, hsh = fast ? (uint32_t)(zs - 32) : 0u;
-        const uint32_t lot = fast ? (uint32_t)(2 * eps) : 0xffffffffu;
+        const unsigned long long Cy = (unsigned long long)((1ll << (zs - 1)) + eps);
+        const uint32_t hsh = fast ? (uint32_t)(zs - 32) : 0u;
+        const uint32_t fth = fast ? (uint32_t)((2 * eps) >> hsh) : 0xffffffffu;
         // the edge block of tile k (cg = 0 warps): staged edge bytes -> TMEM slots
         auto edge = [&](long long k) {
             const int s = (int)(k % SSTG);
@@ -1140,20 +1162,6 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
             if (lane == 0) tc::mbar_arrive(&efull);
         };
         if (cg == 0 && nmine > 0) edge(0);
-        // exact test and quantisation of one voxel from S (rare lanes)
-        auto qslow = [&](unsigned long long S, int c, uint32_t rv, long long l) -> uint32_t {
-            const long long V = (long long)S - half;
-            const int bgq = (int)((V + fmask) >> zs);
-            const int qv = (int)rv - bgq;
-            if ((unsigned long long)((eps - V) & fmask) <= (unsigned long long)(2 * eps) &&
-                ((long long)rv << zs) - V >= one - eps) {
-                const unsigned long long at = atomicAdd(&fix[0], 1ull);
-                CT_DCHECK(l < nlines && h0 + c < NZ);
-                if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
-                else fix[1] = 1;
-            }
-            return qv > 0 ? (uint32_t)qv : 0u;
-        };
         for (long long k = 0; k < nmine; ++k) {
             const int s = (int)(k % SSTG);
             const long long l = (t0 + k * gs) * TM + m;
@@ -1205,24 +1213,50 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
             }
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&empty[s]);
+            // fast path for every column: bgq = Y >> zs, q = max(raw - bgq, 0) as
+            // SIMD bytes (u8) / halves (u16); a conservative certification test on
+            // the top 32 fractional bits (bits [zs - 32, zs) of Y, one funnel
+            // shift) marks lanes that need the exact test below
             constexpr int VPW = 4 / RB;
             constexpr uint32_t VM = RB == 1 ? 0xffu : 0xffffu;
             uint32_t qw[QW];
+            bool anyn = false;
 #pragma unroll
-            for (int i = 0; i < QW; ++i) qw[i] = 0;
+            for (int i = 0; i < QW; ++i) {
+                uint32_t bw;
+                if constexpr (RB == 1) {
+                    uint32_t b[4];
 #pragma unroll
-            for (int c = 0; c < CW; ++c) {
-                const uint32_t rv = (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM;
-                const bool near = live && (yh[c] & hmask) == 0 && yl[c] <= lot;
-                uint32_t qv;
-                if (__builtin_expect(__any_sync(0xffffffffu, near), 0) && near) {
-                    const unsigned long long Y = ((unsigned long long)yh[c] << 32) | yl[c];
-                    qv = qslow(Y - Cy, c, rv, l);
+                    for (int u = 0; u < 4; ++u) {
+                        const int c = 4 * i + u;
+                        anyn |= __funnelshift_r(yl[c], yh[c], hsh) <= fth;
+                        b[u] = yh[c] >> hsh;
+                    }
+                    bw = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+                    qw[i] = __vsubus4(rw[i], bw);
                 } else {
-                    const int d = (int)rv - (int)(yh[c] >> hsh);
-                    qv = live && d > 0 ? (uint32_t)d : 0u;
+                    uint32_t b[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int c = 2 * i + u;
+                        anyn |= __funnelshift_r(yl[c], yh[c], hsh) <= fth;
+                        b[u] = yh[c] >> hsh;
+                    }
+                    bw = __byte_perm(b[0], b[1], 0x5410);
+                    qw[i] = __vsubus2(rw[i], bw);
                 }
-                qw[c / VPW] |= qv << (8 * RB * (c % VPW));
+            }
+            if (__builtin_expect(__any_sync(0xffffffffu, anyn && live), 0)) {
+#pragma unroll
+                for (int c = 0; c < CW; ++c) {
+                    if (live && __funnelshift_r(yl[c], yh[c], hsh) <= fth) {
+                        const uint32_t rv = (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM;
+                        const unsigned long long Y = ((unsigned long long)yh[c] << 32) | yl[c];
+                        const uint32_t qv = qz_exact(prm, SPL, Y - Cy, rv, (unsigned long long)(l * NZ + h0 + c), fix, cap);
+                        const int sh = 8 * RB * (c % VPW);
+                        qw[c / VPW] = (qw[c / VPW] & ~(VM << sh)) | (qv << sh);
+                    }
+                }
             }
             if (live) {
                 uint8_t *dst = (uint8_t *)q + (l * NZ + h0) * RB;
