@@ -1029,13 +1029,17 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
     constexpr int SB = DB + RBT;
     constexpr int BW = NZ * NZ, BE = NZ * 32;
     constexpr int ACOL = 5 * NZ;
-    static_assert(ACOL + NP * 8 <= 512, "TMEM");
+    // edge blocks: two slots when they fit (tile k+2's block is written right
+    // after afull(k), off the MMA's critical path; needs SSTG >= 3 so that its
+    // stage is not the one the writer still holds), else one (tile k+1's)
+    constexpr int ES = ACOL + 2 * NP * 8 <= 512 && SSTG >= 3 ? 2 : 1;
+    static_assert(ACOL + ES * NP * 8 <= 512, "TMEM");
     static_assert(NZ % 32 == 0 && NZ <= 96, "pass z tile");
     constexpr int CW = NZ / 4;  // columns per epilogue thread
     extern __shared__ __align__(1024) uint8_t sm[];  // [SSTG][SB] stages, [NL][BW] taps, [NL][BE] edge taps
     uint8_t *sw = sm + SSTG * SB;
     uint8_t *swe = sw + NL * BW;
-    __shared__ uint64_t full[SSTG], empty[SSTG], afull, aempty, efull;
+    __shared__ uint64_t full[SSTG], empty[SSTG], afull, aempty, efull[ES];
     __shared__ uint32_t tbase;
     __shared__ long long Qs[PMAX], Ts[PMAX + 1];
     const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
@@ -1048,7 +1052,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
         }
         tc::mbar_init(&afull, 1);
         tc::mbar_init(&aempty, WS_EPI);
-        tc::mbar_init(&efull, 4);
+        for (int i = 0; i < ES; ++i) tc::mbar_init(&efull[i], 4);
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&tmp);
         tc::tma_prefetch_desc(&tmr);
@@ -1106,7 +1110,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
             const int s = (int)(k % SSTG);
             tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
             tc::mbar_wait(&aempty, (uint32_t)(k & 1) ^ 1u);
-            tc::mbar_wait(&efull, (uint32_t)(k & 1));
+            tc::mbar_wait(&efull[k % ES], (uint32_t)((k / ES) & 1));
             tc::fence_after();
             if (tc::elect_one()) {
                 const uint64_t a0 = tc::smem_desc(tc::smem_u32(sm + s * SB), LBOA, SBOA);
@@ -1122,7 +1126,8 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
                             tc::mma_i8_ss(base + NZ * acc, a0 + (uint64_t)((a * PLB + ks * 2 * LBOA) >> 4),
                                           b0 + (uint64_t)((b * BW + ks * 2 * LBOB) >> 4), idesc,
                                           first[acc] && ks == 0 ? 0u : 1u);
-                        tc::mma_i8_ts(base + NZ * acc, base + ACOL + a * 8, be + (uint64_t)((b * BE) >> 4), idesc, 1u);
+                        tc::mma_i8_ts(base + NZ * acc, base + ACOL + (int)(k % ES) * NP * 8 + a * 8,
+                                      be + (uint64_t)((b * BE) >> 4), idesc, 1u);
                         first[acc] = false;
                     }
                 tc::mma_commit(&empty[s]);
@@ -1154,28 +1159,26 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
             for (int a = 0; a < NP; ++a) {
                 const uint32_t w0 = 0x01010101u * st[a * PLB], wl = 0x01010101u * st[(NCH - 1) * NP * PLB + a * PLB + 15];
                 const uint32_t v[8] = {w0, w0, w0, w0, wl, wl, wl, wl};
-                tc::tmem_st8(la + ACOL + a * 8, v);
+                tc::tmem_st8(la + ACOL + (int)(k % ES) * NP * 8 + a * 8, v);
             }
             tc::tmem_st_wait();
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&efull);
+            if (lane == 0) tc::mbar_arrive(&efull[k % ES]);
         };
-        if (cg == 0 && nmine > 0) edge(0);
+        if (cg == 0)
+            for (int k = 0; k < ES && k < nmine; ++k) edge(k);
         for (long long k = 0; k < nmine; ++k) {
             const int s = (int)(k % SSTG);
             const long long l = (t0 + k * gs) * TM + m;
             const bool live = l < nlines;
             tc::mbar_wait(&afull, (uint32_t)(k & 1));
             tc::fence_after();
-            // Y = S + half + eps per column, from the accumulators in 8-column groups
+            // Y = S + half + eps per column.  CW <= 16: all accumulator words are
+            // loaded, then released (MMA(k+1) waits only for the loads), then
+            // combined; CW = 24 (NZ = 96): in 8-column groups (registers)
             uint32_t yh[CW], yl[CW];
-#pragma unroll
-            for (int g8 = 0; g8 < CW; g8 += 8) {
-                uint32_t v[5][8];
-#pragma unroll
-                for (int acc = 0; acc < 5; ++acc) tc::tmem_ld8(la + NZ * acc + h0 + g8, v[acc]);
-                tc::tmem_ld_wait();
+            auto ycomb = [&](const uint32_t(&v)[5][8], int g8) {
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     unsigned long long Y = (((unsigned long long)v[4][c] << 32) | v[0][c]) + Cy;
@@ -1185,11 +1188,33 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
                     yh[g8 + c] = (uint32_t)(Y >> 32);
                     yl[g8 + c] = (uint32_t)Y;
                 }
+            };
+            if constexpr (CW <= 16) {
+                uint32_t v[CW / 8][5][8];
+#pragma unroll
+                for (int g = 0; g < CW / 8; ++g)
+#pragma unroll
+                    for (int acc = 0; acc < 5; ++acc) tc::tmem_ld8(la + NZ * acc + h0 + 8 * g, v[g][acc]);
+                tc::tmem_ld_wait();
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&aempty);  // MMA(k+1) may overwrite the accumulators
+#pragma unroll
+                for (int g = 0; g < CW / 8; ++g) ycomb(v[g], 8 * g);
+            } else {
+#pragma unroll
+                for (int g8 = 0; g8 < CW; g8 += 8) {
+                    uint32_t v[5][8];
+#pragma unroll
+                    for (int acc = 0; acc < 5; ++acc) tc::tmem_ld8(la + NZ * acc + h0 + g8, v[acc]);
+                    tc::tmem_ld_wait();
+                    ycomb(v, g8);
+                }
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&aempty);
             }
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&aempty);  // MMA(k+1) may overwrite the accumulators
-            if (cg == 0 && k + 1 < nmine) edge(k + 1);
+            if (cg == 0 && k + ES < nmine) edge(k + ES);
             // raw of the tile (stage s, already landed: MMA(k) consumed it), then release the stage
             tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
             // the thread's CW * RB raw / q bytes move in 16-byte chunks (8-byte when
