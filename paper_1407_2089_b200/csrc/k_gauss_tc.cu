@@ -177,6 +177,39 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
 
 __device__ __forceinline__ uint32_t limb(long long q, int b) { return (uint32_t)((q >> (8 * b)) & 0xff); }
 
+// S += v 2^k for a compile-time k (after unrolling): one IMAD.WIDE.U32 below
+// 2^32, a high-word add above
+__device__ __forceinline__ void acc_pow2(unsigned long long &S, uint32_t v, int k) {
+    if (k < 32) S += (unsigned long long)v * (uint32_t)(1u << k);
+    else S += (unsigned long long)v << k;
+}
+
+// Mixed-radix cursor over a CTA's tiles: tile t0 + k gs has digits (o, ti,
+// cb) (cb fastest); advancing by gs adds gs's digits with carries, so the
+// per-tile coordinates cost no division.
+struct TileCur {
+    int o, ti, cb, go, gti, gcb, nti, ncb;
+    __device__ TileCur(long long t0, long long gs, int nti_, int ncb_) : nti(nti_), ncb(ncb_) {
+        long long r = t0 / ncb;
+        cb = (int)(t0 - r * ncb);
+        ti = (int)(r % nti);
+        o = (int)(r / nti);
+        r = gs / ncb;
+        gcb = (int)(gs - r * ncb);
+        gti = (int)(r % nti);
+        go = (int)(r / nti);
+    }
+    __device__ __forceinline__ void next() {
+        cb += gcb;
+        int c = cb >= ncb;
+        if (c) cb -= ncb;
+        ti += gti + c;
+        c = ti >= nti;
+        if (c) ti -= nti;
+        o += go + c;
+    }
+};
+
 // byte a of four u32 values -> one u32 (plane words), all four planes
 __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3, uint32_t (&p)[4]) {
     const uint32_t l01 = __byte_perm(o0, o1, 0x5140), h01 = __byte_perm(o0, o1, 0x7362);
@@ -251,17 +284,12 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     const int nti = (L + TM - 1) / TM, ncb = inner / TN;
     const long long ntiles = (long long)outer * nti * ncb;
     const uint32_t idesc = tc::idesc_i8(TM, TN, false, false, false, true);
-    const ct::FastDiv fd_cb((unsigned)ncb), fd_ti((unsigned)nti);
-    auto tile_coords = [&](long long tile, int &o, int &ti, int &cb) {
-        const unsigned tl = (unsigned)tile, r2 = fd_cb.div(tl);
-        cb = (int)(tl - r2 * (unsigned)ncb);
-        o = (int)fd_ti.div(r2);
-        ti = (int)(r2 - (unsigned)o * (unsigned)nti);
-    };
-    // coalesced store of a staged output tile: 4 planes x 128 rows x 32 bytes
-    auto flush = [&](long long tile, const uint8_t *ob) {
-        int o, ti, cb;
-        tile_coords(tile, o, ti, cb);
+    const long long t0 = blockIdx.x, gs = gridDim.x;
+    TileCur scur(t0, gs, nti, ncb), fcur(t0, gs, nti, ncb);  // next tile to stage / to flush
+    // coalesced store of the next staged output tile: 4 planes x 128 rows x 32 bytes
+    auto flush = [&](const uint8_t *ob) {
+        const int o = fcur.o, ti = fcur.ti, cb = fcur.cb;
+        fcur.next();
 #pragma unroll
         for (int q2 = 0; q2 < (NPO * TM * CPR + NT - 1) / NT; ++q2) {
             const int e = t + NT * q2, a = e / (CPR * TM), mm = (e / CPR) & (TM - 1), hh = e % CPR;
@@ -272,10 +300,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
                         : *(const uint4 *)(ob + (a * TM + mm) * OROW + 16 * hh);
         }
     };
-    // stage the B operand of a tile (cp.async): NPIN planes x 256 rows x 32 bytes
-    auto stage = [&](long long tile, int buf) {
-        int o, ti, cb;
-        tile_coords(tile, o, ti, cb);
+    // stage the B operand of the next tile (cp.async): NPIN planes x 256 rows x 32 bytes
+    auto stage = [&](int buf) {
+        const int o = scur.o, ti = scur.ti, cb = scur.cb;
+        scur.next();
         const int i0 = ti * TM;
 #pragma unroll
         for (int p = 0; p < NPIN; ++p)
@@ -294,7 +322,6 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     // MMA(k) completes its accumulators are read into registers, a barrier
     // frees TMEM, MMA(k+1) is issued, and the epilogue of tile k (combine +
     // stores) runs from registers while MMA(k+1) executes.
-    const long long t0 = blockIdx.x, gs = gridDim.x;
     const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
     // MMA issue: warp 0, one elected lane; descriptors = one base + constants
     auto issue = [&](long long k) {
@@ -323,7 +350,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
     };
 #pragma unroll
     for (int k = 0; k < STAGES; ++k) {
-        if (k < nmine) stage(t0 + k * gs, k);
+        if (k < nmine) stage(k);
         else tc::cp_commit();
     }
     if (nmine > 0) {
@@ -353,9 +380,9 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         __syncthreads();
         tc::fence_after();
         if (k + 1 < nmine) issue(k + 1);
-        if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
+        if (k + STAGES < nmine) stage((int)(k % STAGES));
         else tc::cp_commit();
-        if (k > 0) flush(t0 + (k - 1) * gs, sout + (int)((k - 1) & 1) * OBUF);
+        if (k > 0) flush(sout + (int)((k - 1) & 1) * OBUF);
         // epilogue of tile k: row m, columns [h, h + CW) -> staged output
         uint8_t *ob = sout + (int)(k & 1) * OBUF;
 #pragma unroll
@@ -363,10 +390,10 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
             uint32_t ov[8], o4[2] = {0u, 0u};
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                long long S = 0;
+                unsigned long long S = 0;
 #pragma unroll
-                for (int acc = 0; acc < NACC; ++acc) S += (long long)v[acc][g8 + c] << (8 * acc);
-                const unsigned long long o = (unsigned long long)(S >> shift_out);
+                for (int acc = 0; acc < NACC; ++acc) acc_pow2(S, v[acc][g8 + c], 8 * acc);
+                const unsigned long long o = S >> shift_out;
                 ov[c] = (uint32_t)o;
                 if constexpr (NPO == 5) o4[c >> 2] |= (uint32_t)((o >> 32) & 0xff) << (8 * (c & 3));
             }
@@ -380,7 +407,7 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
         }
     }
     __syncthreads();
-    if (nmine > 0) flush(t0 + (nmine - 1) * gs, sout + (int)((nmine - 1) & 1) * OBUF);
+    if (nmine > 0) flush(sout + (int)((nmine - 1) & 1) * OBUF);
     tc::cp_wait_all();
     __syncthreads();
     tc::fence_after();
@@ -488,21 +515,15 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     const long long ntiles = (long long)outer * nti * ncb;
     const long long t0 = blockIdx.x, gs = gridDim.x;
     const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
-    const ct::FastDiv fd_cb((unsigned)ncb), fd_ti((unsigned)nti);
-    auto coords = [&](long long k, int &o, int &ti, int &cb) {
-        const unsigned tl = (unsigned)(t0 + k * gs), r2 = fd_cb.div(tl);
-        cb = (int)(tl - r2 * (unsigned)ncb);
-        o = (int)fd_ti.div(r2);
-        ti = (int)(r2 - (unsigned)o * (unsigned)nti);
-    };
+    TileCur cur(t0, gs, nti, ncb);  // each role walks its tiles k = 0, 1, ... in order
     if (wp == 0) {
         // ---- TMA producer ----
         for (long long k = 0; k < nmine; ++k) {
             const int s = (int)(k % SSTG);
             tc::mbar_wait(&empty[s], (uint32_t)((k / SSTG) & 1) ^ 1u);
+            const int o = cur.o, ti = cur.ti, cb = cur.cb;
+            cur.next();
             if (lane == 0) {
-                int o, ti, cb;
-                coords(k, o, ti, cb);
                 tc::mbar_expect_tx(&full[s], SB);
                 uint8_t *dst = sm + s * SB;
 #pragma unroll
@@ -521,8 +542,8 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
         for (long long k = 0; k < nmine; ++k) {
             const int s = (int)(k % SSTG), a = (int)(k % ASTG);
             tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
-            int o, ti, cb;
-            coords(k, o, ti, cb);
+            const int ti = cur.ti;
+            cur.next();
             const int g0 = ti * TM - r;  // global row of box row 0
             if (g0 < 0 || g0 + KXY > L) {
                 // box rows outside [0, L) came back zero-filled: clamp to the edge rows
@@ -568,9 +589,9 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
         // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
         const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * lo_pair(NPIN, NL);
         // coalesced store of a staged output tile: NPO planes x 128 rows x TV bytes
-        auto flush = [&](long long k, const uint8_t *ob) {
-            int o, ti, cb;
-            coords(k, o, ti, cb);
+        auto flush = [&](const uint8_t *ob) {
+            const int o = cur.o, ti = cur.ti, cb = cur.cb;
+            cur.next();
 #pragma unroll
             for (int q2 = 0; q2 < (NPO * TM * CPR + 32 * WS_EPI - 1) / (32 * WS_EPI); ++q2) {
                 const int e = et + 32 * WS_EPI * q2;
@@ -610,14 +631,13 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                 uint32_t ov[4], o4 = 0;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    long long S = 0;
+                    unsigned long long S = 0;
 #pragma unroll
                     for (int acc = 0; acc < NACC; ++acc) {
-                        long long d = v[acc][g4 + DB * c];
-                        if constexpr (DB == 2) d += (long long)v[acc][g4 + 2 * c + 1] << 8;
-                        S += d << (8 * acc);
+                        acc_pow2(S, v[acc][g4 + DB * c], 8 * acc);
+                        if constexpr (DB == 2) acc_pow2(S, v[acc][g4 + 2 * c + 1], 8 * acc + 8);
                     }
-                    const unsigned long long o = (unsigned long long)(S >> shift_out);
+                    const unsigned long long o = S >> shift_out;
                     ov[c] = (uint32_t)o;
                     if constexpr (NPO == 5) o4 |= (uint32_t)((o >> 32) & 0xff) << (8 * c);
                 }
@@ -642,7 +662,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                         make_uint4(pw[pa][0], pw[pa][1], pw[pa][2], pw[pa][3]);
             }
             epi_bar();  // tile k staged (and tile k-1's flush, issued before, finished by every thread)
-            flush(k, ob);
+            flush(ob);
         }
     }
     tc::fence_before();
