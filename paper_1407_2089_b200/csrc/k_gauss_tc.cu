@@ -14,18 +14,19 @@
 //
 //   pass x, y (strided axes): D[out row][col] = A[out row][in row] * B[in row][col]
 //       A = the tap band (128 x 256, Toeplitz, constant) held in TMEM;
-//       B = 256 input rows (clamped at the edges = mode "nearest") x 32
+//       B = 256 input rows (clamped at the edges = mode "nearest") x TN
 //       columns of a byte plane, MN-major in shared memory.
 //   pass z (contiguous axis, nz in {32, 64, 96}): D[line][out k] = A[line][in k] * B[in k][out k]
 //       A = 128 lines x nz bytes, K-major; B = the taps that land inside the
 //       line (nz x nz, constant), K-major; both in SMEM.  The taps beyond the
-//       line ends (mode "nearest": the edge values) are exact integer edge
-//       terms added in the epilogue on the CUDA cores.
-// Pass x is warp-specialised: a TMA producer warp stages the B boxes
-// (cp.async.bulk.tensor, mbarrier complete_tx) into a 6-deep ring, one warp
-// issues the MMAs, 16 epilogue warps drain TMEM (tc_pass_xy_ws).  Passes y
-// and z stage their operands with cp.async several tiles ahead, and each
-// tile's epilogue (from registers) overlaps the next tile's MMAs.
+//       line ends (mode "nearest": the edge values) are one more K = 32
+//       block: A = the lines' edge values in TMEM, B = the tail tap sums.
+// All three passes are warp-specialised and persistent (one CTA per SM): a
+// TMA producer warp stages the operand boxes (cp.async.bulk.tensor, mbarrier
+// complete_tx) into a ring, one warp issues the MMAs, 16 epilogue warps drain
+// TMEM, so each tile's epilogue overlaps the next tile's MMAs (passes x, y:
+// tc_pass_xy_ws, with an edge-fixer warp for the clamped rows; pass z:
+// tc_pass_z_ws).
 //   Limb pairs (a, b) with a + b >= 2 (data limb a, weight limb b) are kept;
 //   pairs of equal a + b share an accumulator (5 accumulators).
 #include <cudaTypedefs.h>
@@ -44,7 +45,6 @@ constexpr int TM = 128;        // output rows per tile (passes x, y) / lines per
 constexpr int TNX = 64;        // columns per tile, pass x (4 accumulators: 256 + 4*64 TMEM columns)
 constexpr int TNY = 32;        // columns per tile, pass y (5 accumulators: 256 + 5*32)
 constexpr int KXY = 256;       // input rows per tile (passes x, y): TM + 2r <= 256
-constexpr int NT = 512;        // threads per CTA: 16 warps = 4 TMEM sub-partitions x 4 column groups
 constexpr int PMAX = 65;       // max taps per side + 1
 
 // lowest kept limb-pair sum (data limb a + weight limb b) for NP data planes
@@ -72,11 +72,6 @@ __device__ __forceinline__ uint32_t band_word(const uint8_t *tbb, int c, int m) 
     return __funnelshift_r(w[0], w[1], 8 * (o & 3));
 }
 
-// 16-byte chunk hh of a staged row whose 8-byte units are XOR-swizzled by key
-__device__ __forceinline__ uint4 swz_chunk(const uint8_t *row, int hh, int key) {
-    const uint4 v = *(const uint4 *)(row + 16 * (hh ^ (key >> 1)));
-    return (key & 1) ? make_uint4(v.z, v.w, v.x, v.y) : v;
-}
 
 struct TcParams {
     long long Q[3][PMAX];  // integer taps per axis (Q[axis][|j|] = rint(w_j 2^fw[axis]))
@@ -221,200 +216,6 @@ __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, u
 }
 
 // ---------------------------------------------------------------------------
-// Passes x and y, synchronous form (launched for pass y).  NPIN = 1 (raw u8 input; pairs (0,b), accumulator b, shift
-// 8b; output S >> 11) or 4 (byte planes of P1; pairs a+b >= 2, accumulator
-// a+b-2, shift 8(a+b-2); output S >> 19).  Volume viewed as [outer][L][inner].
-// ---------------------------------------------------------------------------
-// NPIN = 5 (u16 frames): 40-bit intermediates, pairs a + b >= 3 (lo_pair), still 5 accumulators.
-template <int NPIN, int STAGES, int TN, int NPO = 4, int NL = 4>  // TN: columns per tile; NPO: output planes;
-                                                                     // NL: weight limbs
-__global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ in, long long plane_in, int L,
-                                                     int inner, int outer, const TcParams *__restrict__ prm, int axis,
-                                                     int r, uint8_t *__restrict__ out, long long plane_out) {
-    constexpr int NACC = NPIN == 1 ? NL : 5;
-    constexpr int LOP = lo_pair(NPIN, NL);
-    constexpr int AB = 64 * NL;  // TMEM columns of the tap band (64 per limb)
-    static_assert(AB + NACC * TN <= 512, "TMEM: band + accumulators");
-    constexpr uint32_t LBO = (TN / 16) * 128, SBO = 128;                // MN-major B
-    constexpr int BUF = KXY * TN;                                       // bytes per plane per buffer
-    // staged output rows (TN = 32): unpadded, the four 8-byte units of a row
-    // XOR-swizzled by (row >> 2) & 3 -- the epilogue's 8-byte stores (32
-    // consecutive rows, one unit) and the flush's 16-byte loads (4 rows x 2
-    // chunks) hit distinct banks; a chunk whose halves the swizzle swapped
-    // (odd key) is swapped back after the load
-    constexpr bool SWZ = TN == 32;
-    constexpr int OROW = SWZ ? TN : TN + 16;                            // output row (bytes)
-    constexpr int CPR = TN / 16;                                        // 16-byte chunks per row
-    constexpr int CW = TN / 4;                                          // columns per thread (epilogue)
-    constexpr int OBUF = NPO * TM * OROW;                               // output tile: [NPO planes][128 rows]
-    extern __shared__ __align__(1024) uint8_t sm[];                     // [STAGES][NPIN][BUF], [2][OBUF]
-    uint8_t *sout = sm + STAGES * NPIN * BUF;
-    __shared__ uint32_t tbase;
-    __shared__ uint64_t mbar;
-    // thread t: TMEM row (lane) m = t % 128 of sub-partition (t / 32) % 4,
-    // column group cg = t / 128
-    const int t = threadIdx.x, wp = t >> 5, m = t & (TM - 1), cg = t >> 7;
-    if (wp == 0) tc::tmem_alloc(&tbase, 512);
-    if (t == 0) {
-        tc::mbar_init(&mbar, 1);
-        tc::mbar_fence_init();
-    }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
-    const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * LOP;
-    const uint32_t base = tbase;
-    const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
-    // A (taps) into TMEM columns [0, AB): limb b (column group cg, cg + 4) at 64 b; row m
-    {
-        __shared__ __align__(16) uint8_t tb[NL][TBW];
-        tap_rows(tb, prm->Q[axis], r, NL);
-        __syncthreads();
-        for (int b = cg; b < NL; b += 4)
-            for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
-                uint32_t v[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = band_word(tb[b], c0 + i, m);
-                tc::tmem_st8(lane_addr + b * 64 + c0, v);
-            }
-    }
-    tc::tmem_st_wait();
-
-    const int nti = (L + TM - 1) / TM, ncb = inner / TN;
-    const long long ntiles = (long long)outer * nti * ncb;
-    const uint32_t idesc = tc::idesc_i8(TM, TN, false, false, false, true);
-    const long long t0 = blockIdx.x, gs = gridDim.x;
-    TileCur scur(t0, gs, nti, ncb), fcur(t0, gs, nti, ncb);  // next tile to stage / to flush
-    // coalesced store of the next staged output tile: 4 planes x 128 rows x 32 bytes
-    auto flush = [&](const uint8_t *ob) {
-        const int o = fcur.o, ti = fcur.ti, cb = fcur.cb;
-        fcur.next();
-#pragma unroll
-        for (int q2 = 0; q2 < (NPO * TM * CPR + NT - 1) / NT; ++q2) {
-            const int e = t + NT * q2, a = e / (CPR * TM), mm = (e / CPR) & (TM - 1), hh = e % CPR;
-            const int i = ti * TM + mm;
-            if (e < NPO * TM * CPR && i < L)
-                *(uint4 *)(out + a * plane_out + ((long long)o * L + i) * inner + (long long)cb * TN + 16 * hh) =
-                    SWZ ? swz_chunk(ob + (a * TM + mm) * OROW, hh, (mm >> 2) & 3)
-                        : *(const uint4 *)(ob + (a * TM + mm) * OROW + 16 * hh);
-        }
-    };
-    // stage the B operand of the next tile (cp.async): NPIN planes x 256 rows x 32 bytes
-    auto stage = [&](int buf) {
-        const int o = scur.o, ti = scur.ti, cb = scur.cb;
-        scur.next();
-        const int i0 = ti * TM;
-#pragma unroll
-        for (int p = 0; p < NPIN; ++p)
-#pragma unroll
-            for (int q = 0; q < CPR * KXY / NT; ++q) {
-                const int e = t + NT * q, kk = e / CPR, g = e % CPR;
-                const int ii = min(max(i0 - r + kk, 0), L - 1);
-                tc::cp_async16(sm + (buf * NPIN + p) * BUF + tc::mnmajor_off(kk, 16 * g, LBO, SBO),
-                               in + p * plane_in + ((long long)o * L + ii) * inner + (long long)cb * TN + 16 * g);
-            }
-        tc::cp_commit();
-    };
-
-    // Software pipeline over this CTA's tiles k = 0, 1, ... (tile t0 + k gs):
-    // STAGES tiles are staged ahead by cp.async (slot k % STAGES); after
-    // MMA(k) completes its accumulators are read into registers, a barrier
-    // frees TMEM, MMA(k+1) is issued, and the epilogue of tile k (combine +
-    // stores) runs from registers while MMA(k+1) executes.
-    const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
-    // MMA issue: warp 0, one elected lane; descriptors = one base + constants
-    auto issue = [&](long long k) {
-        if (wp != 0) return;
-        const uint64_t d0 = tc::smem_desc(tc::smem_u32(sm + (int)(k % STAGES) * NPIN * BUF), LBO, SBO);
-        if (tc::elect_one()) {
-            bool first[NACC];
-#pragma unroll
-            for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
-#pragma unroll
-            for (int a = 0; a < NPIN; ++a)
-#pragma unroll
-                for (int b = 0; b < NL; ++b) {
-                    const int acc = NPIN == 1 ? b : a + b - LOP;
-                    if (acc < 0 || acc >= NACC) continue;
-#pragma unroll
-                    for (int ks = 0; ks < KXY / 32; ++ks)
-                        tc::mma_i8_ts(base + AB + TN * acc, base + b * 64 + ks * 8,
-                                      d0 + (uint64_t)((a * BUF + ks * 4 * LBO) >> 4), idesc,
-                                      first[acc] && ks == 0 ? 0u : 1u);
-                    first[acc] = false;
-                }
-            tc::mma_commit(&mbar);
-        }
-        __syncwarp();
-    };
-#pragma unroll
-    for (int k = 0; k < STAGES; ++k) {
-        if (k < nmine) stage(k);
-        else tc::cp_commit();
-    }
-    if (nmine > 0) {
-        tc::cp_wait_group<STAGES - 1>();
-        tc::fence_async_smem();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-        issue(0);
-    }
-    uint32_t phase = 0;
-    const int h = CW * cg;
-    for (long long k = 0; k < nmine; ++k) {
-        tc::mbar_wait(&mbar, phase);
-        phase ^= 1;
-        tc::fence_after();
-        uint32_t v[NACC][CW];
-#pragma unroll
-        for (int acc = 0; acc < NACC; ++acc)
-#pragma unroll
-            for (int g8 = 0; g8 < CW; g8 += 8)
-                tc::tmem_ld8(lane_addr + AB + TN * acc + h + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
-        tc::tmem_ld_wait();
-        tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
-        tc::fence_async_smem();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-        if (k + 1 < nmine) issue(k + 1);
-        if (k + STAGES < nmine) stage((int)(k % STAGES));
-        else tc::cp_commit();
-        if (k > 0) flush(sout + (int)((k - 1) & 1) * OBUF);
-        // epilogue of tile k: row m, columns [h, h + CW) -> staged output
-        uint8_t *ob = sout + (int)(k & 1) * OBUF;
-#pragma unroll
-        for (int g8 = 0; g8 < CW; g8 += 8) {
-            uint32_t ov[8], o4[2] = {0u, 0u};
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                unsigned long long S = 0;
-#pragma unroll
-                for (int acc = 0; acc < NACC; ++acc) acc_pow2(S, v[acc][g8 + c], 8 * acc);
-                const unsigned long long o = S >> shift_out;
-                ov[c] = (uint32_t)o;
-                if constexpr (NPO == 5) o4[c >> 2] |= (uint32_t)((o >> 32) & 0xff) << (8 * (c & 3));
-            }
-            uint32_t lo[4], hi[4];
-            planes4(ov[0], ov[1], ov[2], ov[3], lo);
-            planes4(ov[4], ov[5], ov[6], ov[7], hi);
-#pragma unroll
-            const int uo = SWZ ? 8 * (((h + g8) >> 3) ^ ((m >> 2) & 3)) : h + g8;  // byte offset of the 8-byte unit
-            for (int a = 0; a < 4; ++a) *(uint2 *)(ob + (a * TM + m) * OROW + uo) = make_uint2(lo[a], hi[a]);
-            if constexpr (NPO == 5) *(uint2 *)(ob + (4 * TM + m) * OROW + uo) = make_uint2(o4[0], o4[1]);
-        }
-    }
-    __syncthreads();
-    if (nmine > 0) flush(sout + (int)((nmine - 1) & 1) * OBUF);
-    tc::cp_wait_all();
-    __syncthreads();
-    tc::fence_after();
-    if (wp == 0) tc::tmem_dealloc(base, 512);
-}
-
-// ---------------------------------------------------------------------------
 // Passes x and y, warp-specialised (launched for pass x):
 //   warp 0      TMA producer: one cp.async.bulk.tensor box per tile (256
 //               input rows x TN columns of every byte plane) into a ring of
@@ -422,16 +223,20 @@ __global__ void __launch_bounds__(NT, 1) tc_pass_xy(const uint8_t *__restrict__ 
 //   warp 1      TMEM owner and MMA issuer: the tap band A lives in TMEM
 //               columns [0, 256); ASTG accumulator sets follow, so MMA(k+1)
 //               runs while the epilogue drains set k (afull / aempty);
-//               rows of a box that fall outside [0, L) arrive zero-filled and
-//               are replaced by the edge row (mode "nearest") before the MMAs;
-//   warps 2..9  epilogue: TMEM -> registers, combine the limb accumulators in
+//   warp 2      edge fixer: rows of a box that fall outside [0, L) arrive
+//               zero-filled; it replaces them by the edge row (mode "nearest")
+//               and releases the stage to the MMA warp (ready) -- off the MMA
+//               warp's critical path (when the MMA warp did it, the 2 of 8
+//               tiles per column at the volume's faces stalled the tensor pipe);
+//   warps 3..18 epilogue: TMEM -> registers, combine the limb accumulators in
 //               exact 64-bit integers, split into the next pass's byte planes,
-//               8-byte stores (warp w reads TMEM lane quarter w % 4, half
-//               (w - 2) / 4 of the tile's columns).
+//               staged, coalesced 16-byte stores (warp w reads TMEM lane
+//               quarter w % 4, column group (w - 3) / 4).
 // Same integer arithmetic as tc_pass_xy (bit-identical planes).
 // ---------------------------------------------------------------------------
 constexpr int WS_EPI = 16;                 // epilogue warps (4 per TMEM lane quarter)
-constexpr int WS_NT = 32 * (2 + WS_EPI);   // 576 threads
+constexpr int WS_NT = 32 * (2 + WS_EPI);   // 576 threads (pass z)
+constexpr int WSX_NT = 32 * (3 + WS_EPI);  // 608 threads (passes x, y: + the edge fixer)
 
 __device__ __forceinline__ void epi_bar() {  // named barrier 1: the epilogue warps only
     asm volatile("bar.sync 1, %0;" ::"n"(32 * WS_EPI) : "memory");
@@ -442,7 +247,7 @@ __device__ __forceinline__ void epi_bar() {  // named barrier 1: the epilogue wa
 // 2c + 1 the high bytes, so the MMA yields both limb sums and the epilogue
 // combines S(c) = D[2c] + 256 D[2c + 1] (no de-interleave pass).
 template <int NPIN, int TN, int SSTG, int ASTG, int DB = 1, int NPO = 4, int NL = 4>
-__global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant__ CUtensorMap tmap, int L, int inner,
+__global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant__ CUtensorMap tmap, int L, int inner,
                                                           int outer, const TcParams *__restrict__ prm, int axis, int r,
                                                           uint8_t *__restrict__ out, long long plane_out) {
     static_assert(DB == 1 || NPIN == 1, "u16 input only for the raw pass");
@@ -468,13 +273,14 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     static_assert(AB + ASTG * NACC * TN <= 512, "TMEM: band + accumulator sets");
     extern __shared__ __align__(1024) uint8_t sm[];  // [SSTG][SB] operand stages, [2][OBUF] output tiles
     uint8_t *sout = sm + SSTG * SB;
-    __shared__ uint64_t full[SSTG], empty[SSTG], afull[ASTG], aempty[ASTG];
+    __shared__ uint64_t full[SSTG], ready[SSTG], empty[SSTG], afull[ASTG], aempty[ASTG];
     __shared__ uint32_t tbase;
     const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
     if (wp == 1) tc::tmem_alloc(&tbase, 512);
     if (t == 0) {
         for (int i = 0; i < SSTG; ++i) {
             tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&ready[i], 1);
             tc::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < ASTG; ++i) {
@@ -490,13 +296,13 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     const uint32_t base = tbase;
     // epilogue warp e = wp - 2: TMEM lane quarter q = wp % 4 (hardware rule),
     // column group cg = e / 4; it writes band limb cg of its rows into TMEM
-    const int e_w = wp - 2, q = wp & 3, cg = e_w >> 2, m = 32 * q + lane;
+    const int e_w = wp - 3, q = wp & 3, cg = e_w >> 2, m = 32 * q + lane;
     const uint32_t la = base + ((uint32_t)(32 * q) << 16);
     {
         __shared__ __align__(16) uint8_t tb[NL][TBW];
         tap_rows(tb, prm->Q[axis], r, NL);
         __syncthreads();
-        if (wp >= 2) {
+        if (wp >= 3) {
             for (int b = cg; b < NL; b += 4)
                 for (int c0 = 0; c0 < KXY / 4; c0 += 8) {
                     uint32_t v[8];
@@ -536,11 +342,10 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
             }
             __syncwarp();
         }
-    } else if (wp == 1) {
-        // ---- MMA issuer ----
-        const uint32_t idesc = tc::idesc_i8(TM, TN, false, false, false, true);
+    } else if (wp == 2) {
+        // ---- edge fixer ----
         for (long long k = 0; k < nmine; ++k) {
-            const int s = (int)(k % SSTG), a = (int)(k % ASTG);
+            const int s = (int)(k % SSTG);
             tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
             const int ti = cur.ti;
             cur.next();
@@ -555,8 +360,16 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
                     if (src >= 0) *(uint4 *)(st + (pc * KXY + kk) * 16) = *(const uint4 *)(st + (pc * KXY + src) * 16);
                 }
                 tc::fence_async_smem();
-                __syncwarp();
             }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&ready[s]);
+        }
+    } else if (wp == 1) {
+        // ---- MMA issuer ----
+        const uint32_t idesc = tc::idesc_i8(TM, TN, false, false, false, true);
+        for (long long k = 0; k < nmine; ++k) {
+            const int s = (int)(k % SSTG), a = (int)(k % ASTG);
+            tc::mbar_wait(&ready[s], (uint32_t)((k / SSTG) & 1));
             tc::mbar_wait(&aempty[a], (uint32_t)((k / ASTG) & 1) ^ 1u);
             tc::fence_after();
             if (tc::elect_one()) {
@@ -585,7 +398,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     } else {
         // ---- epilogue: row m, columns [h, h + CW) of every tile ----
         const int h = CW * cg;
-        const int et = t - 64;  // 0 .. 32 * WS_EPI - 1
+        const int et = t - 96;  // 0 .. 32 * WS_EPI - 1
         // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
         const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * lo_pair(NPIN, NL);
         // coalesced store of a staged output tile: NPO planes x 128 rows x TV bytes
@@ -671,349 +484,6 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_xy_ws(const __grid_constant_
     if (wp == 1) tc::tmem_dealloc(base, 512);
 }
 
-// ---------------------------------------------------------------------------
-// Pass z + residual + quantisation + certification.  NZ in {32, 64, 96}.  The
-// whole line is one tile: the MMA applies the taps that land inside the line
-// (B[n][k] = Q_|k-n|), and the taps beyond either end, which all read the
-// edge value (mode "nearest"), come from one more K = 32 block: A holds the
-// line's edge values x0 (16 slots) and x_{nz-1} (16 slots) -- written into
-// TMEM by the line's owner thread, so no SMEM and no proxy fence -- and B the
-// tail sums E0[n] = sum_{j > n} Q_j and EL[n] = sum_{j >= nz-n} Q_j split into
-// 16 pieces < 2^32 each (fw_z <= 36 keeps E < 2^35).  The epilogue is then
-// pure accumulator arithmetic:
-//   S = sum_acc v[acc] 2^(8 acc),  V = S - 2^(zs-1)
-//   q = max(raw - ceil(V / 2^zs), 0)                  (= rint(max(raw - bg, 0)))
-//   flag iff (eps - V) mod 2^zs <= 2 eps and raw 2^zs - V >= 2^zs - eps
-// ---------------------------------------------------------------------------
-template <int NZ, int STAGES, typename Traw = uint8_t, int NP = 4, int NL = 4>  // NP: planes of P2, NL: weight limbs
-__global__ void __launch_bounds__(NT, 1) tc_pass_z(const uint8_t *__restrict__ in, long long plane, long long nlines,
-                                                    const TcParams *__restrict__ prm, int r,
-                                                    const Traw *__restrict__ raw, Traw *__restrict__ q,
-                                                    unsigned long long *__restrict__ fix, long long cap) {
-    constexpr int RB = (int)sizeof(Traw);       // raw / q bytes per voxel
-    constexpr int VPW = 4 / RB;                 // voxels per 32-bit word
-    constexpr int LOP = lo_pair(NP, NL), SPL = 8 * LOP;  // kept pairs a + b >= LOP; S has scale 2^(fd + fw - SPL)
-    static_assert(NZ <= 64 || RB == 1, "u16 pass z: nz in {32, 64}");
-    constexpr int NCH = NZ / 16;                // 16-byte chunks per line
-    constexpr uint32_t LBO = 128, SBO = NCH * 128, SBOE = 256;  // K-major: data / taps (K = NZ), edge block (K = 32)
-    constexpr int ABUF = TM * NZ;               // bytes per plane per buffer
-    constexpr int RBUF = ABUF * RB;             // bytes of a raw / q tile
-    constexpr int BW = NZ * NZ;                 // bytes per weight limb
-    constexpr int BE = NZ * 32;                 // bytes per weight limb, edge block
-    constexpr int ACOL = 5 * NZ;                // TMEM: accumulators [0, ACOL), edge A slots after
-    static_assert(ACOL + NP * 8 <= 512, "TMEM");
-    extern __shared__ __align__(1024) uint8_t sm[];  // [NL][BW] taps, [NL][BE] edge taps, [STAGES][NP][ABUF] data,
-                                                     // [STAGES][RBUF] raw, [2][RBUF] q tile
-    uint8_t *sw = sm;
-    uint8_t *swe = sm + NL * BW;
-    uint8_t *sa = swe + NL * BE;
-    uint8_t *sr = sa + STAGES * NP * ABUF;
-    uint8_t *sq = sr + STAGES * RBUF;
-    const uint8_t *rawb = (const uint8_t *)raw;
-    uint8_t *qb8 = (uint8_t *)q;
-    __shared__ uint32_t tbase;
-    __shared__ uint64_t mbar;
-    __shared__ long long Qs[PMAX], Ts[PMAX + 1];
-    const int t = threadIdx.x, wp = t >> 5, m = t & (TM - 1), cg = t >> 7;
-    if (wp == 0) tc::tmem_alloc(&tbase, 512);
-    for (int j = t; j < PMAX; j += NT) Qs[j] = j <= r ? prm->Q[2][j] : 0;
-    if (t == 0) {
-        tc::mbar_init(&mbar, 1);
-        tc::mbar_fence_init();
-    }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (t == 0) {  // tail sums T[m] = sum_{j >= m} Q_j
-        Ts[PMAX] = 0;
-        for (int j = PMAX - 1; j >= 0; --j) Ts[j] = Ts[j + 1] + Qs[j];
-    }
-    __syncthreads();
-    // taps inside the line, K-major; edge taps: B[s][n] = piece s of E0[n] (s < 16) / of EL[n] (s >= 16)
-    for (int e = t; e < NZ * NZ; e += NT) {
-        const int n = e / NZ, k = e - n * NZ;
-        const int d = k > n ? k - n : n - k;
-        const long long qv = d < PMAX ? Qs[d] : 0;
-#pragma unroll
-        for (int b = 0; b < NL; ++b) sw[b * BW + tc::kmajor_off(n, k, LBO, SBO)] = (uint8_t)limb(qv, b);
-    }
-    for (int e = t; e < NZ * 32; e += NT) {
-        const int n = e >> 5, sl = e & 31, s16 = sl & 15;
-        const long long E = sl < 16 ? (n + 1 <= PMAX ? Ts[n + 1] : 0) : (NZ - n <= PMAX ? Ts[NZ - n] : 0);
-        const long long pc = E / 16 + (s16 < E % 16 ? 1 : 0);  // < 2^(8 NL)
-#pragma unroll
-        for (int b = 0; b < NL; ++b) swe[b * BE + tc::kmajor_off(n, sl, LBO, SBOE)] = (uint8_t)limb(pc, b);
-    }
-    const long long eps = prm->eps;
-    const int zs = prm->fw[2] + prm->fd - SPL;  // S has scale 2^zs
-    const long long half = 1ll << (zs - 1), one = 1ll << zs, fmask = one - 1;
-    const uint32_t base = tbase;
-    const uint32_t lane_addr = base + ((uint32_t)((wp & 3) * 32) << 16);
-    const long long ntiles = (nlines + TM - 1) / TM;
-    const long long t0 = blockIdx.x, gs = gridDim.x;
-    const uint32_t idesc = tc::idesc_i8(TM, NZ, false, false, false, false);
-
-    // data planes (K-major canonical) and raw (plain) of a tile via cp.async
-    auto stage = [&](long long tile, int buf) {
-        const long long l0 = tile * TM;
-        const int nl = (int)min((long long)TM, nlines - l0);
-#pragma unroll
-        for (int q2 = 0; q2 < (TM * NCH + NT - 1) / NT; ++q2) {
-            const int e = t + NT * q2, l = e / NCH, c = e - l * NCH;
-            if (e < TM * NCH && l < nl) {
-#pragma unroll
-                for (int a = 0; a < NP; ++a)
-                    tc::cp_async16(sa + (buf * NP + a) * ABUF + tc::kmajor_off(l, 16 * c, LBO, SBO),
-                                   in + a * plane + (l0 + l) * NZ + 16 * c);
-#pragma unroll
-                for (int j = 0; j < RB; ++j)
-                    tc::cp_async16(sr + buf * RBUF + (l * NZ + 16 * c) * RB + 16 * j,
-                                   rawb + ((l0 + l) * NZ + 16 * c) * RB + 16 * j);
-            }
-        }
-        tc::cp_commit();
-    };
-    // edge A block of tile k (TMEM columns ACOL + 8 a): the owner thread of
-    // line m (warps 0-3, one per TMEM lane quarter) loads the line's two edge
-    // values of every plane and stores them as 16 + 16 byte slots -- between
-    // the completion of MMA(k-1) and the barrier before MMA(k) is issued, so
-    // one copy suffices
-    uint8_t ex[2 * NP];
-    auto edge_load = [&](long long k) {
-        const long long l = (t0 + k * gs) * TM + m;
-#pragma unroll
-        for (int a = 0; a < NP; ++a) {
-            ex[2 * a] = l < nlines ? in[a * plane + l * NZ] : 0;
-            ex[2 * a + 1] = l < nlines ? in[a * plane + l * NZ + NZ - 1] : 0;
-        }
-    };
-    auto edge_store = [&]() {
-#pragma unroll
-        for (int a = 0; a < NP; ++a) {
-            const uint32_t w0 = 0x01010101u * ex[2 * a], wl = 0x01010101u * ex[2 * a + 1];
-            const uint32_t v[8] = {w0, w0, w0, w0, wl, wl, wl, wl};
-            tc::tmem_st8(lane_addr + ACOL + a * 8, v);
-        }
-        tc::tmem_st_wait();
-    };
-
-    // coalesced store of a staged q tile (lines are contiguous in global)
-    auto flush = [&](long long tile, const uint8_t *qb) {
-        const long long l0 = tile * TM;
-        const int nbytes = (int)min((long long)TM, nlines - l0) * NZ * RB;
-        for (int e = 16 * t; e < nbytes; e += 16 * NT) *(uint4 *)(qb8 + l0 * NZ * RB + e) = *(const uint4 *)(qb + e);
-    };
-    // same software pipeline as tc_pass_xy
-    const long long nmine = t0 < ntiles ? (ntiles - 1 - t0) / gs + 1 : 0;
-    auto issue = [&](long long k) {
-        if (wp != 0) return;
-        const uint64_t a0 = tc::smem_desc(tc::smem_u32(sa + (int)(k % STAGES) * NP * ABUF), LBO, SBO);
-        const uint64_t b0 = tc::smem_desc(tc::smem_u32(sw), LBO, SBO);
-        const uint64_t be = tc::smem_desc(tc::smem_u32(swe), LBO, SBOE);
-        const uint32_t ae = base + ACOL;
-        if (tc::elect_one()) {
-            bool first[5] = {true, true, true, true, true};
-#pragma unroll
-            for (int a = 0; a < NP; ++a)
-#pragma unroll
-                for (int b = 0; b < NL; ++b) {
-                    const int acc = a + b - LOP;
-                    if (acc < 0 || acc > 4) continue;
-#pragma unroll
-                    for (int ks = 0; ks < NZ / 32; ++ks)
-                        tc::mma_i8_ss(base + NZ * acc, a0 + (uint64_t)((a * ABUF + ks * 2 * LBO) >> 4),
-                                      b0 + (uint64_t)((b * BW + ks * 2 * LBO) >> 4), idesc,
-                                      first[acc] && ks == 0 ? 0u : 1u);
-                    // the edge taps: A from TMEM (8 columns = 32 K bytes per plane)
-                    tc::mma_i8_ts(base + NZ * acc, ae + a * 8, be + (uint64_t)((b * BE) >> 4), idesc, 1u);
-                    first[acc] = false;
-                }
-            tc::mma_commit(&mbar);
-        }
-        __syncwarp();
-    };
-#pragma unroll
-    for (int k = 0; k < STAGES; ++k) {
-        if (k < nmine) stage(t0 + k * gs, k);
-        else tc::cp_commit();
-    }
-    if (nmine > 0) {
-        if (cg == 0) {
-            edge_load(0);
-            edge_store();
-            if (nmine > 1) edge_load(1);  // the edges are loaded one tile ahead of their store
-        }
-        tc::cp_wait_group<STAGES - 1>();
-        tc::fence_async_smem();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-        issue(0);
-    }
-    uint32_t phase = 0;
-    constexpr int CW = NZ / 4;  // columns per thread
-    const int h0 = cg * CW;
-    // q of one voxel (column h0 + c of line l) from its 5 accumulator words
-    // and the raw value; flags it for the fix-up
-    auto qslow = [&](const uint32_t v0, const uint32_t v1, const uint32_t v2, const uint32_t v3, const uint32_t v4,
-                     int c, uint32_t rv, long long l) -> uint32_t {
-        const unsigned long long S = (unsigned long long)v0 + (unsigned long long)v1 * 0x100ull +
-                                     (unsigned long long)v2 * 0x10000ull + (unsigned long long)v3 * 0x1000000ull +
-                                     ((unsigned long long)v4 << 32);
-        const long long V = (long long)S - half;
-        const int bgq = (int)((V + fmask) >> zs);  // ceil(V / 2^zs): the background rounded for this raw grid
-        const int qv = (int)rv - bgq;
-        // rounding boundaries of raw - bg at half-integers k + 1/2 (k >= 0):
-        // T = raw 2^zs - V within eps of a multiple of 2^zs, T >= 2^zs - eps
-        if ((unsigned long long)((eps - V) & fmask) <= (unsigned long long)(2 * eps) &&
-            ((long long)rv << zs) - V >= one - eps) {
-            const unsigned long long at = atomicAdd(&fix[0], 1ull);
-            CT_DCHECK(l < nlines && h0 + c < NZ);
-            if ((long long)at < cap) fix[2 + at] = (unsigned long long)(l * NZ + h0 + c);
-            else fix[1] = 1;
-        }
-        return qv > 0 ? (uint32_t)qv : 0u;
-    };
-    // The common case in 32-bit words.  With Y = S + half + eps (= V + 2^zs +
-    // eps) the certification test above is (Y mod 2^zs) <= 2 eps, and when it
-    // fails Y >> zs equals ceil(V / 2^zs) (no borrow from the low bits).  For
-    // 32 <= zs < 64 and 2 eps < 2^32: Y's high word hi, low word lo; the test
-    // is (hi & hmask) == 0 && lo <= 2 eps, bgq = hi >> (zs - 32).  Other
-    // parameters make the test always pass (every voxel takes qslow).  Y is
-    // assembled with three 32 x 32 -> 64-bit multiply-adds (IMAD.WIDE).
-    const bool fast = zs >= 32 && zs < 64 && 2 * eps < (1ll << 32);
-    const unsigned long long Cy = (unsigned long long)(half + eps);
-    const uint32_t hmask = fast ? (uint32_t)((1ull << (zs - 32)) - 1) : 0u, hsh = fast ? (uint32_t)(zs - 32) : 0u;
-    const uint32_t lot = fast ? (uint32_t)(2 * eps) : 0xffffffffu;
-    auto qval = [&](const uint32_t v0, const uint32_t v1, const uint32_t v2, const uint32_t v3, const uint32_t v4,
-                    int c, uint32_t rv, long long l) -> uint32_t {
-        unsigned long long Y = (((unsigned long long)v4 << 32) | v0) + Cy;
-        Y += (unsigned long long)v1 * 0x100u;
-        Y += (unsigned long long)v2 * 0x10000u;
-        Y += (unsigned long long)v3 * 0x1000000u;
-        const uint32_t hi = (uint32_t)(Y >> 32), lo = (uint32_t)Y;
-        const bool live = l < nlines;
-        const bool near = live && (hi & hmask) == 0 && lo <= lot;
-        if (__builtin_expect(__any_sync(0xffffffffu, near), 0)) {
-            if (near) return qslow(v0, v1, v2, v3, v4, c, rv, l);
-        }
-        const int qv = (int)rv - (int)(hi >> hsh);
-        return live && qv > 0 ? (uint32_t)qv : 0u;
-    };
-    if constexpr (NZ <= 64) {
-    // accumulators -> registers, edges of tile k+1, barrier, MMA(k+1), then the epilogue of k
-    for (long long k = 0; k < nmine; ++k) {
-        tc::mbar_wait(&mbar, phase);
-        phase ^= 1;
-        tc::fence_after();
-        uint32_t v[5][CW];
-#pragma unroll
-        for (int acc = 0; acc < 5; ++acc)
-#pragma unroll
-            for (int g8 = 0; g8 < CW; g8 += 8)
-                tc::tmem_ld8(lane_addr + NZ * acc + h0 + g8, *reinterpret_cast<uint32_t(*)[8]>(&v[acc][g8]));
-        tc::tmem_ld_wait();
-        if (cg == 0 && k + 1 < nmine) {  // MMA(k) has completed, MMA(k+1) not yet issued
-            edge_store();
-            if (k + 2 < nmine) edge_load(k + 2);
-        }
-        // raw of tile k (slot k % STAGES) before the slot is restaged
-        const long long l = (t0 + k * gs) * TM + m;
-        const uint8_t *rl = sr + (int)(k % STAGES) * RBUF + (m * NZ + h0) * RB;
-        uint32_t rw[CW / VPW];
-#pragma unroll
-        for (int c4 = 0; c4 < CW / VPW; ++c4) rw[c4] = *(const uint32_t *)(rl + 4 * c4);
-        tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
-        tc::fence_async_smem();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-        if (k + 1 < nmine) issue(k + 1);
-        if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
-        else tc::cp_commit();
-        if (k > 0) flush(t0 + (k - 1) * gs, sq + (int)((k - 1) & 1) * RBUF);
-        constexpr uint32_t VM = RB == 1 ? 0xffu : 0xffffu;
-        uint32_t qw[CW / VPW];
-#pragma unroll
-        for (int c4 = 0; c4 < CW / VPW; ++c4) qw[c4] = 0;
-        // all lanes run qval (its vote is warp-wide); lines past the end yield 0
-#pragma unroll
-        for (int c = 0; c < CW; ++c)
-            qw[c / VPW] |= qval(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], c,
-                                (rw[c / VPW] >> (8 * RB * (c % VPW))) & VM, l)
-                           << (8 * RB * (c % VPW));
-        uint8_t *qb = sq + (int)(k & 1) * RBUF + (m * NZ + h0) * RB;
-#pragma unroll
-        for (int c4 = 0; c4 < CW / VPW; c4 += 2) *(uint2 *)(qb + 4 * c4) = make_uint2(qw[c4], qw[c4 + 1]);
-    }
-    } else {
-    // long lines (NZ = 96): the accumulators do not fit in registers at once,
-    // so the epilogue drains them in 8-column chunks before MMA(k+1) is issued
-    for (long long k = 0; k < nmine; ++k) {
-        tc::mbar_wait(&mbar, phase);
-        phase ^= 1;
-        tc::fence_after();
-        const long long l = (t0 + k * gs) * TM + m;
-        const uint8_t *rl = sr + (int)(k % STAGES) * ABUF + m * NZ + h0;
-        uint8_t *qb = sq + (int)(k & 1) * ABUF + m * NZ + h0;
-#pragma unroll
-        for (int g8 = 0; g8 < CW; g8 += 8) {
-            uint32_t v[5][8];
-#pragma unroll
-            for (int acc = 0; acc < 5; ++acc) tc::tmem_ld8(lane_addr + NZ * acc + h0 + g8, v[acc]);
-            tc::tmem_ld_wait();
-            const uint32_t r0w = *(const uint32_t *)(rl + g8), r1w = *(const uint32_t *)(rl + g8 + 4);
-            uint32_t qw[2] = {0, 0};
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                qw[c >> 2] |= qval(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], g8 + c,
-                                   ((c < 4 ? r0w : r1w) >> (8 * (c & 3))) & 0xff, l) << (8 * (c & 3));
-            *(uint2 *)(qb + g8) = make_uint2(qw[0], qw[1]);
-        }
-        if (cg == 0 && k + 1 < nmine) {
-            edge_store();
-            if (k + 2 < nmine) edge_load(k + 2);
-        }
-        tc::cp_wait_group<STAGES - 2>();  // tile k+1 landed
-        tc::fence_async_smem();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-        if (k + 1 < nmine) issue(k + 1);
-        if (k + STAGES < nmine) stage(t0 + (k + STAGES) * gs, (int)(k % STAGES));
-        else tc::cp_commit();
-        if (k > 0) flush(t0 + (k - 1) * gs, sq + (int)((k - 1) & 1) * ABUF);
-    }
-    }
-    __syncthreads();
-    if (nmine > 0) flush(t0 + (nmine - 1) * gs, sq + (int)((nmine - 1) & 1) * RBUF);
-    tc::cp_wait_all();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (wp == 0) tc::tmem_dealloc(base, 512);
-}
-
-// ---------------------------------------------------------------------------
-// Pass z, warp-specialised (NZ in {32, 64, 96}).  Same arithmetic as
-// tc_pass_z; the roles are split so that no CTA-wide barrier couples them
-// (ncu on tc_pass_z: 39% issue active, the largest stall the __syncthreads
-// that gates each MMA behind the slowest epilogue warp):
-//   warp 0     TMA producer: per tile NCH boxes {16 B, 128 lines, NP planes}
-//              of P2 -> chunk c at c * NP * 2048 (plane a at + a * 2048, line
-//              l at + 16 l: the K-major no-swizzle layout with LBO = NP * 2048,
-//              SBO = 128) and the raw tile {NZ * RB bytes, 128 lines};
-//   warp 1     MMA issuer: waits the stage, the drained accumulators and the
-//              tile's edge block; commits to the stage's `empty` and to `afull`;
-//   warps 2-17 epilogue (TMEM lane quarter wp % 4, column group (wp - 2) / 4):
-//              drain the 5 accumulators in 8-column groups, release them
-//              (aempty), the cg = 0 warps then write the next tile's edge block
-//              into TMEM from its staged planes (efull), then q and the
-//              certification (IMAD.WIDE form, rare lanes through the exact
-//              test) with 16-byte stores straight to global memory.
-// One accumulator set (5 NZ columns) + one edge block (NP x 8 columns): the
-// edge block of tile k+1 is written after afull(k), i.e. after MMA(k) read it.
-// ---------------------------------------------------------------------------
 // The exact test and quantisation of one pass-z voxel from S (tc_pass_z's
 // qval): out of line, so the rare lanes that need it cost the fast epilogue
 // no registers.
@@ -1386,22 +856,31 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
         const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * NP * TM * (TX / RB + 16) + 1024;
         cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = ((nx + TM - 1) / TM) * (ny * nz * RB / TX);
-        kx<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tm, (int)nx, (int)(ny * nz * RB), 1, prm, 0,
+        kx<<<(unsigned)std::min<long long>(tiles, nsm), WSX_NT, sm, s>>>(tm, (int)nx, (int)(ny * nz * RB), 1, prm, 0,
                                                                         rx, p1, N);
         if (int st = ct::check_launch("tc_pass_x")) return st;
     }
-    // pass y: [nx][ny][nz] x 4 planes, the synchronous form (cp.async staging):
-    // measured faster than the warp-specialised TMA form here -- 263 us vs 296
-    // (TN = 32, one accumulator set) / 373 (TN = 16, three sets) on C2: the
-    // MMAs read the tap band A from TMEM, and narrower tiles only add MMAs
+    // pass y: [nx][ny][nz] x NP planes, warp-specialised like pass x: one 4-D
+    // box {16 B, 256 rows, 1, NP planes} per 16-byte column chunk, the edge
+    // fixer warp clamps the rows outside [0, ny)
     {
-        constexpr int YS = NP == 4 ? 5 : 4;  // operand stages (SMEM: 5 planes x 4 stages + output tiles)
-        auto ky = tc_pass_xy<NP, YS, TNY, NP, NL>;
-        const size_t sm = (size_t)YS * NP * KXY * TNY + 2 * NP * TM * (TNY + 16) + 1024;
+        constexpr int SS = NP == 4 ? 5 : 4;  // operand stages
+        CUtensorMap tm;
+        const cuuint64_t dims[4] = {(cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)nx, (cuuint64_t)NP};
+        const cuuint64_t strides[3] = {(cuuint64_t)nz, (cuuint64_t)(ny * nz), (cuuint64_t)N};
+        const cuuint32_t box[4] = {16, KXY, 1, NP}, es[4] = {1, 1, 1, 1};
+        if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, (void *)p1, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            ct::set_error("tensor map (pass y) rejected");
+            return CT_ERR_UNSUPPORTED;
+        }
+        auto ky = tc_pass_xy_ws<NP, TNY, SS, 1, 1, NP, NL>;
+        const size_t sm = (size_t)SS * NP * KXY * TNY + 2 * NP * TM * (TNY + 16) + 1024;
         cudaFuncSetAttribute(ky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TNY);
-        ky<<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(p1, N, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2,
-                                                                   N);
+        ky<<<(unsigned)std::min<long long>(tiles, nsm), WSX_NT, sm, s>>>(tm, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2,
+                                                                         N);
         if (int st = ct::check_launch("tc_pass_y")) return st;
     }
     // pass z + epilogue: warp-specialised, operands by TMA
@@ -1436,21 +915,6 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
         const size_t sm = (size_t)stg * (NP * TM * nz + TM * nz * RB) + NL * nz * nz + NL * nz * 32 + 1024;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         kz<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tp, tr, lines, prm, rz, q, fix, cap);
-        if (int st = ct::check_launch("tc_pass_z")) return st;
-    }
-    if (false) {
-        const long long lines = nx * ny, tiles = (lines + TM - 1) / TM;
-        const int stg = RB == 2 ? 2 : nz == 96 ? 2 : 4;
-        const size_t sm = NL * nz * nz + NL * nz * 32 + (size_t)stg * (NP * TM * nz + TM * nz * RB) +
-                          2 * TM * nz * RB + 1024;
-        void (*kz)(const uint8_t *, long long, long long, const TcParams *, int, const Traw *, Traw *,
-                   unsigned long long *, long long);
-        if constexpr (RB == 2)
-            kz = nz == 64 ? tc_pass_z<64, 2, Traw, 5, 5> : tc_pass_z<32, 2, Traw, 5, 5>;
-        else
-            kz = nz == 64 ? tc_pass_z<64, 4, Traw> : nz == 96 ? tc_pass_z<96, 2, Traw> : tc_pass_z<32, 4, Traw>;
-        cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        kz<<<(unsigned)std::min<long long>(tiles, nsm), NT, sm, s>>>(p2, N, lines, prm, rz, raw, q, fix, cap);
         if (int st = ct::check_launch("tc_pass_z")) return st;
     }
     return CT_OK;
