@@ -247,9 +247,10 @@ __device__ __forceinline__ void epi_bar() {  // named barrier 1: the epilogue wa
 // 2c + 1 the high bytes, so the MMA yields both limb sums and the epilogue
 // combines S(c) = D[2c] + 256 D[2c + 1] (no de-interleave pass).
 template <int NPIN, int TN, int SSTG, int ASTG, int DB = 1, int NPO = 4, int NL = 4>
-__global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant__ CUtensorMap tmap, int L, int inner,
-                                                          int outer, const TcParams *__restrict__ prm, int axis, int r,
-                                                          uint8_t *__restrict__ out, long long plane_out) {
+__global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant__ CUtensorMap tmap,
+                                                          const __grid_constant__ CUtensorMap tmo, int L, int inner,
+                                                          int outer, const TcParams *__restrict__ prm, int axis,
+                                                          int r) {
     static_assert(DB == 1 || NPIN == 1, "u16 input only for the raw pass");
     constexpr int NACC = NPIN == 1 ? NL : 5;
     constexpr int AB = 64 * NL;  // TMEM columns of the tap band
@@ -260,16 +261,17 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
     constexpr uint32_t LBO = 128, SBO = CB;         // MN-major: 8 K-rows = 128 B; next 16 columns = CB
     constexpr int CW = TN / 4;                      // (byte) columns per epilogue thread (4 column groups)
     constexpr int TV = TN / DB;                     // voxels per tile row
-    // staged output rows: DB = 1 (TV = 64): unpadded, 16-byte chunks XOR-swizzled
-    // by (row >> 1) & 3 -- a thread's 16-byte chunk stores (rows m) and the
-    // flush's chunk loads (rows mm, mm+1) then hit distinct banks (the padded
-    // layout cost 2-4-way conflicts, ~20% of pass x's stall samples);
-    // DB = 2 (TV = 16): one chunk per row, padded
-    constexpr bool SWZ = DB == 1 && TV == 64;
-    constexpr int OROW = SWZ ? TV : TV + 16;        // staged output row (bytes)
-    constexpr int OBUF = NPO * TM * OROW;           // staged output tile: [NPO planes][128 rows]
-    constexpr int CPR = TV / 16;                    // 16-byte chunks per output row
-    const long long inner_v = inner / DB;           // voxels per input row
+    // staged output tile [NPO planes][128 rows][TV bytes], stored by one TMA
+    // box per tile (tmo): rows of TV = 64 / 32 bytes in the TMA's 64B / 32B
+    // swizzle (16-byte chunk c of row m at c ^ ((m >> 1) & 3) / c ^ ((m >> 2)
+    // & 1)), so that the epilogue's row stores spread over the banks
+    constexpr int OBUF = NPO * TM * TV;
+    constexpr int VB = CW / DB;                     // output bytes per thread, row and plane (16, 8, 4)
+    static_assert(TV == 64 || TV == 32 || TV == 16, "output row");
+    auto soff = [](int m, int byte) {                // swizzled byte offset within a plane of the staged tile
+        const int c = byte >> 4, key = TV == 64 ? (m >> 1) & 3 : TV == 32 ? (m >> 2) & 1 : 0;
+        return m * TV + ((c ^ key) << 4) + (byte & 15);
+    };
     static_assert(AB + ASTG * NACC * TN <= 512, "TMEM: band + accumulator sets");
     extern __shared__ __align__(1024) uint8_t sm[];  // [SSTG][SB] operand stages, [2][OBUF] output tiles
     uint8_t *sout = sm + SSTG * SB;
@@ -289,12 +291,13 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
         }
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&tmap);
+        tc::tma_prefetch_desc(&tmo);
     }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t base = tbase;
-    // epilogue warp e = wp - 2: TMEM lane quarter q = wp % 4 (hardware rule),
+    // epilogue warp e = wp - 3: TMEM lane quarter q = wp % 4 (hardware rule),
     // column group cg = e / 4; it writes band limb cg of its rows into TMEM
     const int e_w = wp - 3, q = wp & 3, cg = e_w >> 2, m = 32 * q + lane;
     const uint32_t la = base + ((uint32_t)(32 * q) << 16);
@@ -401,21 +404,6 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
         const int et = t - 96;  // 0 .. 32 * WS_EPI - 1
         // output = S >> shift: S has scale 2^fw (x) or 2^(FD + fw - 16) (y); P has FD bits
         const int shift_out = NPIN == 1 ? prm->fw[axis] - prm->fd : prm->fw[axis] - 8 * lo_pair(NPIN, NL);
-        // coalesced store of a staged output tile: NPO planes x 128 rows x TV bytes
-        auto flush = [&](const uint8_t *ob) {
-            const int o = cur.o, ti = cur.ti, cb = cur.cb;
-            cur.next();
-#pragma unroll
-            for (int q2 = 0; q2 < (NPO * TM * CPR + 32 * WS_EPI - 1) / (32 * WS_EPI); ++q2) {
-                const int e = et + 32 * WS_EPI * q2;
-                if (e >= NPO * TM * CPR) break;
-                const int pa = e / (CPR * TM), mm = (e / CPR) % TM, hh = e % CPR;
-                const int i = ti * TM + mm;
-                if (i < L)
-                    *(uint4 *)(out + pa * plane_out + ((long long)o * L + i) * inner_v + (long long)cb * TV + 16 * hh) =
-                        *(const uint4 *)(ob + (pa * TM + mm) * OROW + 16 * (SWZ ? (hh ^ ((mm >> 1) & 3)) : hh));
-            }
-        };
         for (long long k = 0; k < nmine; ++k) {
             const int a = (int)(k % ASTG);
             tc::mbar_wait(&afull[a], (uint32_t)((k / ASTG) & 1));
@@ -437,8 +425,7 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&aempty[a]);  // MMA(k + ASTG) may overwrite set a
             uint8_t *ob = sout + (int)(k & 1) * OBUF;
-#pragma unroll
-            uint32_t pw[NPO][4];  // SWZ: the thread's 16 columns of every plane, stored as one chunk
+            uint32_t pw[NPO][VB / 4];  // the thread's VB output bytes of every plane
 #pragma unroll
             for (int g4 = 0; g4 < CW; g4 += 4 * DB) {
                 uint32_t ov[4], o4 = 0;
@@ -457,26 +444,27 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
                 uint32_t pl[4];
                 planes4(ov[0], ov[1], ov[2], ov[3], pl);
 #pragma unroll
-                if constexpr (SWZ) {
-#pragma unroll
-                    for (int pa = 0; pa < 4; ++pa) pw[pa][g4 / 4] = pl[pa];
-                    if constexpr (NPO == 5) pw[4][g4 / 4] = o4;
-                } else {
-#pragma unroll
-                    for (int pa = 0; pa < 4; ++pa) *(uint32_t *)(ob + (pa * TM + m) * OROW + (h + g4) / DB) = pl[pa];
-                    if constexpr (NPO == 5) *(uint32_t *)(ob + (4 * TM + m) * OROW + (h + g4) / DB) = o4;
-                }
+                for (int pa = 0; pa < 4; ++pa) pw[pa][g4 / (4 * DB)] = pl[pa];
+                if constexpr (NPO == 5) pw[4][g4 / (4 * DB)] = o4;
             }
-            if constexpr (SWZ) {
-                static_assert(!SWZ || CW == 16, "one 16-byte chunk per thread and plane");
 #pragma unroll
-                for (int pa = 0; pa < NPO; ++pa)
-                    *(uint4 *)(ob + (pa * TM + m) * OROW + 16 * (cg ^ ((m >> 1) & 3))) =
-                        make_uint4(pw[pa][0], pw[pa][1], pw[pa][2], pw[pa][3]);
+            for (int pa = 0; pa < NPO; ++pa) {
+                uint8_t *d = ob + pa * TM * TV + soff(m, h / DB);
+                if constexpr (VB == 16) *(uint4 *)d = make_uint4(pw[pa][0], pw[pa][1], pw[pa][2], pw[pa][3]);
+                else if constexpr (VB == 8) *(uint2 *)d = make_uint2(pw[pa][0], pw[pa][1]);
+                else *(uint32_t *)d = pw[pa][0];
             }
-            epi_bar();  // tile k staged (and tile k-1's flush, issued before, finished by every thread)
-            flush(ob);
+            tc::fence_async_smem();                 // the staged tile -> visible to the TMA store
+            if (et == 0) tc::bulk_wait_read<0>();  // tile k-1's store has read its buffer (reused by k+1)
+            epi_bar();
+            const int o = cur.o, ti = cur.ti, cb = cur.cb;
+            cur.next();
+            if (et == 0) {
+                tc::tma_store_4d(&tmo, ob, cb * TV, ti * TM, o, 0);
+                tc::bulk_commit();
+            }
         }
+        if (et == 0) tc::bulk_wait<0>();
     }
     tc::fence_before();
     __syncthreads();
@@ -808,6 +796,23 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
     return fn;
 }
 
+namespace {
+// tensor map of an intermediate's NP byte planes [plane][outer][rows][row bytes]
+// for the TMA store of 128-row x tv-byte output tiles (64B / 32B swizzle
+// matching tc_pass_xy_ws's staging)
+bool out_map(CUtensorMap *tm, PFN_cuTensorMapEncodeTiled_v12000 encode, uint8_t *base, long long row_bytes,
+             long long rows, long long outer, int np, long long plane, int tv) {
+    const cuuint64_t dims[4] = {(cuuint64_t)row_bytes, (cuuint64_t)rows, (cuuint64_t)outer, (cuuint64_t)np};
+    const cuuint64_t strides[3] = {(cuuint64_t)row_bytes, (cuuint64_t)(row_bytes * rows), (cuuint64_t)plane};
+    const cuuint32_t box[4] = {(cuuint32_t)tv, TM, 1, (cuuint32_t)np}, es[4] = {1, 1, 1, 1};
+    const CUtensorMapSwizzle sw =
+        tv == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : tv == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, (void *)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
 // TC path of ct_gaussian_q (u8, u16).  Returns CT_ERR_UNSUPPORTED when the
 // shape does not fit (the caller then uses the SIMT FMA path).  work: >= 8 N
 // bytes (byte planes of P1 and P2) + sizeof(TcParams).
@@ -852,12 +857,17 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
             ct::set_error("tensor map (pass x) rejected");
             return CT_ERR_UNSUPPORTED;
         }
+        CUtensorMap to;
+        if (!out_map(&to, encode, p1, ny * nz, nx, 1, NP, N, TX / RB)) {
+            ct::set_error("tensor map (pass x output) rejected");
+            return CT_ERR_UNSUPPORTED;
+        }
         auto kx = tc_pass_xy_ws<1, TX, SS, AS, RB, NP, NL>;
-        const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * NP * TM * (TX / RB + 16) + 1024;
+        const size_t sm = (size_t)SS * 1 * KXY * TX + 2 * NP * TM * (TX / RB) + 1024;
         cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = ((nx + TM - 1) / TM) * (ny * nz * RB / TX);
-        kx<<<(unsigned)std::min<long long>(tiles, nsm), WSX_NT, sm, s>>>(tm, (int)nx, (int)(ny * nz * RB), 1, prm, 0,
-                                                                        rx, p1, N);
+        kx<<<(unsigned)std::min<long long>(tiles, nsm), WSX_NT, sm, s>>>(tm, to, (int)nx, (int)(ny * nz * RB), 1, prm,
+                                                                        0, rx);
         if (int st = ct::check_launch("tc_pass_x")) return st;
     }
     // pass y: [nx][ny][nz] x NP planes, warp-specialised like pass x: one 4-D
@@ -875,12 +885,17 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
             ct::set_error("tensor map (pass y) rejected");
             return CT_ERR_UNSUPPORTED;
         }
+        CUtensorMap to;
+        if (!out_map(&to, encode, p2, nz, ny, nx, NP, N, TNY)) {
+            ct::set_error("tensor map (pass y output) rejected");
+            return CT_ERR_UNSUPPORTED;
+        }
         auto ky = tc_pass_xy_ws<NP, TNY, SS, 1, 1, NP, NL>;
-        const size_t sm = (size_t)SS * NP * KXY * TNY + 2 * NP * TM * (TNY + 16) + 1024;
+        const size_t sm = (size_t)SS * NP * KXY * TNY + 2 * NP * TM * TNY + 1024;
         cudaFuncSetAttribute(ky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const long long tiles = nx * ((ny + TM - 1) / TM) * (nz / TNY);
-        ky<<<(unsigned)std::min<long long>(tiles, nsm), WSX_NT, sm, s>>>(tm, (int)ny, (int)nz, (int)nx, prm, 1, ry, p2,
-                                                                         N);
+        ky<<<(unsigned)std::min<long long>(tiles, nsm), WSX_NT, sm, s>>>(tm, to, (int)ny, (int)nz, (int)nx, prm, 1,
+                                                                         ry);
         if (int st = ct::check_launch("tc_pass_y")) return st;
     }
     // pass z + epilogue: warp-specialised, operands by TMA

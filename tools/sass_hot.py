@@ -1,6 +1,6 @@
 """Stall samples per SASS instruction of one kernel in an ncu report, with the
 instruction's index so that waits of different warp roles can be told apart:
-python tools/sass_hot.py report.ncu-rep kernel_regex [top]"""
+python tools/sass_hot.py report.ncu-rep kernel_regex [top] [nth match, default 0]"""
 import csv
 import io
 import subprocess
@@ -8,16 +8,18 @@ import sys
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+nth = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 out = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{kre}", "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
-rows, h = [], None
+rows, h, seen = [], None, -1
 for r in csv.reader(io.StringIO(out)):
     if not r:
         continue
     if r[0] == "Address":
-        if h is not None:
-            break  # first kernel only
-        h = r
+        seen += 1
+        if seen > nth:
+            break
+        h = r if seen == nth else None
         continue
     if h and len(r) == len(h):
         rows.append(dict(zip(h, r)))
