@@ -254,11 +254,14 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
     static_assert(DB == 1 || NPIN == 1, "u16 input only for the raw pass");
     constexpr int NACC = NPIN == 1 ? NL : 5;
     constexpr int AB = 64 * NL;  // TMEM columns of the tap band
-    constexpr int CH = TN / 16;                     // 16-byte chunks per row (one TMA box each)
-    constexpr int PB = KXY * 16;                    // bytes per plane per chunk: [KXY][16]
-    constexpr int CB = NPIN * PB;                   // bytes per chunk (all planes)
-    constexpr int SB = CH * CB;                     // bytes per stage, [CH][NPIN][KXY][16]
-    constexpr uint32_t LBO = 128, SBO = CB;         // MN-major: 8 K-rows = 128 B; next 16 columns = CB
+    // operand stage: one TMA box per tile, [NPIN planes][KXY rows][TN bytes] in
+    // the TMA's TN-byte swizzle = the MMA's MN-major SWIZZLE_32B / 64B
+    // canonical layout (one atom across N; 8-row groups 8 TN bytes apart),
+    // full 32-byte sectors per request
+    static_assert(TN == 32 || TN == 64, "swizzled operand rows");
+    constexpr int PB = KXY * TN;                    // bytes per plane
+    constexpr int SB = NPIN * PB;                   // bytes per stage
+    constexpr uint32_t LBO = PB, SBO = 8 * TN;
     constexpr int CW = TN / 4;                      // (byte) columns per epilogue thread (4 column groups)
     constexpr int TV = TN / DB;                     // voxels per tile row
     // staged output tile [NPO planes][128 rows][TV bytes], stored by one TMA
@@ -335,13 +338,10 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
             if (lane == 0) {
                 tc::mbar_expect_tx(&full[s], SB);
                 uint8_t *dst = sm + s * SB;
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    if constexpr (NPIN == 1)
-                        tc::tma_load_2d(dst + c * CB, &tmap, cb * TN + 16 * c, ti * TM - r, &full[s]);
-                    else
-                        tc::tma_load_4d(dst + c * CB, &tmap, cb * TN + 16 * c, ti * TM - r, o, 0, &full[s]);
-                }
+                if constexpr (NPIN == 1)
+                    tc::tma_load_2d(dst, &tmap, cb * TN, ti * TM - r, &full[s]);
+                else
+                    tc::tma_load_4d(dst, &tmap, cb * TN, ti * TM - r, o, 0, &full[s]);
             }
             __syncwarp();
         }
@@ -355,12 +355,17 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
             const int g0 = ti * TM - r;  // global row of box row 0
             if (g0 < 0 || g0 + KXY > L) {
                 // box rows outside [0, L) came back zero-filled: clamp to the edge rows
+                // (16-byte chunk c of row kk sits at chunk c ^ key(kk) of the row)
                 uint8_t *st = sm + s * SB;
                 const int lo = -g0, hi = L - 1 - g0;
-                for (int e = lane; e < CH * NPIN * KXY; e += 32) {
-                    const int kk = e % KXY, pc = e / KXY;
+                constexpr int CPR = TN / 16;
+                auto key = [](int kk) { return TN == 64 ? (kk >> 1) & 3 : (kk >> 2) & 1; };
+                for (int e = lane; e < NPIN * KXY * CPR; e += 32) {
+                    const int c = e % CPR, kk = (e / CPR) % KXY, pl = e / (CPR * KXY);
                     const int src = kk < lo ? lo : (kk > hi ? hi : -1);
-                    if (src >= 0) *(uint4 *)(st + (pc * KXY + kk) * 16) = *(const uint4 *)(st + (pc * KXY + src) * 16);
+                    if (src >= 0)
+                        *(uint4 *)(st + pl * PB + kk * TN + 16 * (c ^ key(kk))) =
+                            *(const uint4 *)(st + pl * PB + src * TN + 16 * (c ^ key(src)));
                 }
                 tc::fence_async_smem();
             }
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
             tc::mbar_wait(&aempty[a], (uint32_t)((k / ASTG) & 1) ^ 1u);
             tc::fence_after();
             if (tc::elect_one()) {
-                const uint64_t d0 = tc::smem_desc(tc::smem_u32(sm + s * SB), LBO, SBO);
+                const uint64_t d0 = tc::smem_desc_sw(tc::smem_u32(sm + s * SB), LBO, SBO, TN);
                 bool first[NACC];
 #pragma unroll
                 for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
 #pragma unroll
                         for (int ks = 0; ks < KXY / 32; ++ks)
                             tc::mma_i8_ts(base + AB + (a * NACC + acc) * TN, base + b * 64 + ks * 8,
-                                          d0 + (uint64_t)((da * PB + ks * 4 * LBO) >> 4), idesc,
+                                          d0 + (uint64_t)((da * PB + ks * 32 * TN) >> 4), idesc,
                                           first[acc] && ks == 0 ? 0u : 1u);
                         first[acc] = false;
                     }
@@ -843,16 +848,17 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
         return CT_ERR_CUDA;
     }
     // pass x: warp-specialised, operands staged by TMA.  The raw volume as a
-    // byte matrix [nx][ny nz RB]; box = 16 bytes x 256 x-rows, TX / 16 boxes
-    // per tile (u16: TX bytes = TX / 2 voxels, both byte limbs)
+    // byte matrix [nx][ny nz RB]; one box of TX bytes x 256 x-rows per tile,
+    // 64B / 32B-swizzled (u16: TX bytes = TX / 2 voxels, both byte limbs)
     {
         constexpr int TX = NL == 4 ? 64 : 32, SS = 6, AS = 1;  // TMEM: 64 NL band columns + NL TX accumulators (TX = 32 with two accumulator sets measured slower: 158 vs 138 us)
         CUtensorMap tm;
         const cuuint64_t dims[2] = {(cuuint64_t)(ny * nz * RB), (cuuint64_t)nx};
         const cuuint64_t strides[1] = {(cuuint64_t)(ny * nz * RB)};
-        const cuuint32_t box[2] = {16, KXY}, es[2] = {1, 1};
+        const cuuint32_t box[2] = {TX, KXY}, es[2] = {1, 1};
         if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)raw, dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, TX == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
             ct::set_error("tensor map (pass x) rejected");
             return CT_ERR_UNSUPPORTED;
@@ -871,16 +877,16 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
         if (int st = ct::check_launch("tc_pass_x")) return st;
     }
     // pass y: [nx][ny][nz] x NP planes, warp-specialised like pass x: one 4-D
-    // box {16 B, 256 rows, 1, NP planes} per 16-byte column chunk, the edge
+    // box {32 B, 256 rows, 1, NP planes} per tile (32B swizzle), the edge
     // fixer warp clamps the rows outside [0, ny)
     {
         constexpr int SS = NP == 4 ? 5 : 4;  // operand stages
         CUtensorMap tm;
         const cuuint64_t dims[4] = {(cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)nx, (cuuint64_t)NP};
         const cuuint64_t strides[3] = {(cuuint64_t)nz, (cuuint64_t)(ny * nz), (cuuint64_t)N};
-        const cuuint32_t box[4] = {16, KXY, 1, NP}, es[4] = {1, 1, 1, 1};
+        const cuuint32_t box[4] = {TNY, KXY, 1, NP}, es[4] = {1, 1, 1, 1};
         if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, (void *)p1, dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
             ct::set_error("tensor map (pass y) rejected");
             return CT_ERR_UNSUPPORTED;

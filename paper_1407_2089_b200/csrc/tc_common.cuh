@@ -32,6 +32,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
     return d;                // base offset 0, lbo mode 0, layout 0 (no swizzle)
 }
 
+// swizzled canonical layouts (the TMA's 32B / 64B swizzle): layout type 6 / 4
+// in bits [61, 64); MN-major: one atom = 8 K-rows of 32 / 64 bytes, SBO =
+// the byte stride between 8-row groups along K, LBO = between atoms along MN
+__device__ __forceinline__ uint64_t smem_desc_sw(uint32_t saddr, uint32_t lbo, uint32_t sbo, int swz_bytes) {
+    return smem_desc(saddr, lbo, sbo) | ((uint64_t)(swz_bytes == 64 ? 4 : swz_bytes == 32 ? 6 : 0) << 61);
+}
+
 // instruction descriptor, kind::i8, int32 accumulate
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed, bool b_signed, bool a_mn_major,
                                                 bool b_mn_major) {
