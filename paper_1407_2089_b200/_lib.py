@@ -142,7 +142,7 @@ def exported_symbols() -> list[str]:
 # kernels each entry point launches (memsets excluded); used for the
 # bench's gpu_launches count
 LAUNCHES = {
-    "ct_gaussian_residual": 3, "ct_gaussian_q": 8, "ct_to_f64": 1, "ct_median": 1, "ct_histogram": 1, "ct_otsu": 1,
+    "ct_gaussian_residual": 3, "ct_gaussian_q": 7, "ct_to_f64": 1, "ct_median": 1, "ct_histogram": 1, "ct_otsu": 1,
     "ct_threshold_close": 2, "ct_closing": 2, "ct_ccl26": 4, "ct_threshold_close_rows": 2, "ct_ccl26_rows": 5, "ct_cell_table": 6, "ct_voxel_runs": 3, "ct_mrf": 5, "ct_mrf_decide": 8,
     "ct_mrf_step": 4, "ct_sign_sum": 1, "ct_edt": 4, "ct_synth_frame": 3, "ct_memset": 0,
 }

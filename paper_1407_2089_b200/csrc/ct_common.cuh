@@ -69,6 +69,17 @@ template <> struct dtype_of<double> { static constexpr int value = CT_F64; };
 __device__ __forceinline__ double to_f64(uint8_t v) { return (double)v; }
 __device__ __forceinline__ double to_f64(uint16_t v) { return (double)v; }
 __device__ __forceinline__ double to_f64(double v) { return v; }
+// exact double of an integer 0 <= v < 2^31 on the FP64 pipe (one DADD:
+// 2^52 + v built from its bits, minus 2^52) instead of an I2F.F64 on the
+// quarter-rate XU pipe
+__device__ __forceinline__ double u2d(uint32_t v) {
+    return __dadd_rn(__hiloint2double(0x43300000, (int)v), -4503599627370496.0);
+}
+// x[a] + x[b] of two raw (integer) values in double: exact, so the integer sum
+// converted once equals scipy's float64 sum of the two converted values
+__device__ __forceinline__ double pair_f64(uint8_t a, uint8_t b) { return u2d((uint32_t)a + b); }
+__device__ __forceinline__ double pair_f64(uint16_t a, uint16_t b) { return u2d((uint32_t)a + b); }
+__device__ __forceinline__ double pair_f64(double a, double b) { return __dadd_rn(a, b); }
 
 // numpy rint + clip(0, 65535) (segment.py:160-161) for the histogram bin
 __device__ __forceinline__ int hist_bin(uint8_t v) { return v; }

@@ -534,10 +534,9 @@ __global__ void __launch_bounds__(128) fix_p1s(const Traw *__restrict__ raw, i64
         }
         __syncwarp();
         const Traw *cb = b + lane;
-        double acc = __dmul_rn(ct::to_f64(cb[rx * 32]), w[0]);
+        double acc = __dmul_rn(ct::u2d(cb[rx * 32]), w[0]);
         for (int d = rx; d >= 1; --d)
-            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(ct::to_f64(cb[(rx - d) * 32]), ct::to_f64(cb[(rx + d) * 32])),
-                                           w[d]));
+            acc = __dadd_rn(acc, __dmul_rn(ct::pair_f64(cb[(rx - d) * 32], cb[(rx + d) * 32]), w[d]));
         if (e0 + lane < tot) P1[e0 + lane] = acc;
         __syncwarp();
     }
@@ -588,24 +587,40 @@ __global__ void fix_p2q(const Traw *__restrict__ raw, i64 nz, const double *__re
 // Same phases 2+3 with the entry's whole P1 cone ((2ry+1) x nz doubles)
 // copied into SMEM by cp.async first (every load in flight at once; the
 // per-thread form waited one L2 round trip per 8 taps), nz % 2 == 0.
+// Entries past the scratch (f >= capF; gauss_fixup's job in the other
+// configurations) build their cone here from raw, in the same order.
 template <typename Traw, typename Tq>
-__global__ void __launch_bounds__(128) fix_p2q_s(const Traw *__restrict__ raw, i64 nz, const double *__restrict__ wy,
+__global__ void __launch_bounds__(128) fix_p2q_s(const Traw *__restrict__ raw, i64 nx, i64 ny, i64 nz,
+                                                 const double *__restrict__ wx, int rx, const double *__restrict__ wy,
                                                  int ry, const double *__restrict__ wz, int rz,
                                                  const unsigned long long *__restrict__ fix, long long cap,
                                                  long long capF, const double *__restrict__ P1, Tq *__restrict__ q_out) {
     extern __shared__ __align__(16) double cone[];  // [(2ry+1) * nz], then line[nz]
-    const long long F = min(min((long long)fix[0], cap), capF);
+    const long long cnt = min((long long)fix[0], cap), F = min(cnt, capF);
     const int per = (2 * ry + 1) * (int)nz;
     double *line = cone + per;
     const int kk = threadIdx.x;
-    for (long long f = blockIdx.x; f < F; f += gridDim.x) {
+    for (long long f = blockIdx.x; f < cnt; f += gridDim.x) {
         __syncthreads();
-        const double *src = P1 + f * per;
-        for (int q = threadIdx.x; q < per / 2; q += blockDim.x) {
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(cone + 2 * q);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + 2 * q) : "memory");
+        if (f < F) {
+            const double *src = P1 + f * per;
+            for (int q = threadIdx.x; q < per / 2; q += blockDim.x) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(cone + 2 * q);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + 2 * q) : "memory");
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+        } else {
+            const i64 p = (i64)fix[2 + f], j = (p / nz) % ny, i = p / (ny * nz), S = ny * nz;
+            for (int e = threadIdx.x; e < per; e += blockDim.x) {
+                const i64 jj = ct::clampi(j + e / nz - ry, 0, ny - 1);
+                const Traw *col = raw + jj * nz + e % nz;
+                double acc = __dmul_rn(ct::to_f64(col[i * S]), wx[0]);
+                for (int d = rx; d >= 1; --d)
+                    acc = __dadd_rn(acc, __dmul_rn(ct::pair_f64(col[ct::clampi(i - d, 0, nx - 1) * S],
+                                                                col[ct::clampi(i + d, 0, nx - 1) * S]), wx[d]));
+                cone[e] = acc;
+            }
         }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
         __syncthreads();
         if (kk < nz) {
             const double *c = cone + kk;
@@ -694,16 +709,19 @@ int launch_fixup(const Traw *raw, i64 nx, i64 ny, i64 nz, const double *w, int r
         fix_p1<Traw><<<CT_NUM_SMS * 8, 256, 0, s>>>(raw, nx, ny, nz, wx, rx, ry, fix, cap, capF, P1);
     const size_t csm = ((size_t)per + nz) * sizeof(double);
     if (nz % 2 == 0 && nz <= 128 && csm <= 200 * 1024) {
+        // (also the entries past the scratch: no gauss_fixup launch)
         cudaFuncSetAttribute(fix_p2q_s<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-        fix_p2q_s<Traw, Traw><<<CT_NUM_SMS * 2, 128, csm, s>>>(raw, nz, wy, ry, wz, rz, fix, cap, capF, P1, q);
+        fix_p2q_s<Traw, Traw><<<CT_NUM_SMS * 2, 128, csm, s>>>(raw, nx, ny, nz, wx, rx, wy, ry, wz, rz, fix, cap, capF,
+                                                               P1, q);
+        if (int st = ct::check_launch("fixup phases")) return st;
     } else {
         fix_p2q<Traw, Traw><<<CT_NUM_SMS * 2, 128, 0, s>>>(raw, nz, wy, ry, wz, rz, fix, cap, capF, P1, q);
+        if (int st = ct::check_launch("fixup phases")) return st;
+        const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
+        cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+        gauss_fixup<Traw, Traw><<<CT_NUM_SMS, 256, fsm, s>>>(raw, nx, ny, nz, w, rx, ry, rz, fix, cap, q, capF);
+        if (int st = ct::check_launch("gauss_fixup")) return st;
     }
-    if (int st = ct::check_launch("fixup phases")) return st;
-    const size_t fsm = ((size_t)(2 * ry + 1) * nz + nz) * sizeof(double);
-    cudaFuncSetAttribute(gauss_fixup<Traw, Traw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-    gauss_fixup<Traw, Traw><<<CT_NUM_SMS, 256, fsm, s>>>(raw, nx, ny, nz, w, rx, ry, rz, fix, cap, q, capF);
-    if (int st = ct::check_launch("gauss_fixup")) return st;
     // list overflow -> exact recompute in stream (returns at once otherwise)
     double *p1 = (double *)work, *p2 = p1 + nx * ny * nz;
     void *args[] = {(void *)&raw, (void *)&nx, (void *)&ny, (void *)&nz, (void *)&w, (void *)&rx, (void *)&ry,

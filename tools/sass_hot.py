@@ -11,11 +11,16 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 nth = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 out = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{kre}", "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
-rows, h, seen = [], None, -1
+rows, h, seen, name, kname = [], None, -1, "", ""
 for r in csv.reader(io.StringIO(out)):
     if not r:
         continue
+    if r[0] == "Kernel Name":
+        name = r[1] if len(r) > 1 else ""
+        continue
     if r[0] == "Address":
+        if seen + 1 == nth:
+            kname = name
         seen += 1
         if seen > nth:
             break
@@ -25,6 +30,7 @@ for r in csv.reader(io.StringIO(out)):
         rows.append(dict(zip(h, r)))
 tot = sum(int(r["Warp Stall Sampling (All Samples)"]) for r in rows) or 1
 ins = sum(int(r["Instructions Executed"]) for r in rows) or 1
+print(kname[:100])
 print(f"{len(rows)} SASS lines, {tot} samples, {ins} warp instructions")
 for i, r in sorted(enumerate(rows), key=lambda x: -int(x[1]["Warp Stall Sampling (All Samples)"]))[:top]:
     s = int(r["Warp Stall Sampling (All Samples)"])
