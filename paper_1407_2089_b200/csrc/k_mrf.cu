@@ -1013,6 +1013,128 @@ __global__ void __launch_bounds__(256) mrf_stream_v4(const uint8_t *__restrict__
     if (tt) atomicAdd(&ghist[threadIdx.x], (unsigned long long)tt);
 }
 
+// MODE 1 of mrf_stream_v4 without the shared-memory plane ring (NZ in {32,
+// 64, 128}: a row is 8 / 16 / 32 lanes).  ncu on mrf_stream_v4<64, 1>: the
+// per-plane __syncthreads of the ring and the ring loads were ~40% of the
+// stall samples with one word per thread and plane.  Here a thread owns the
+// word (j, kw) of every plane of its slab and walks i with the x-neighbours in
+// registers; the y-neighbours (rows j -+ 1, clamped) are loaded from global
+// memory (the rows of the neighbouring lanes' words: L1 hits), the
+// z-neighbours come from the row's lanes by shuffles; plane i+1's loads are
+// in flight while plane i is processed.  No barriers inside the walk.  Same
+// per-byte arithmetic and results as mrf_stream_v4<NZ, 1>.
+// Per byte lane, bit 7 only (the other bits are don't-care until the final
+// mask): a > b is the carry out of a + ~b = maj(a7, ~b7, s7) with s = (a & 7f)
+// + (~b & 7f); both orders of a pair share the masked operands.  The six +1
+// and six -1 terms of a voxel's sign sum are counted in carry-save form (full
+// adders on whole words), and the sum is nonzero iff the two 3-bit counts
+// differ.
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+__device__ __forceinline__ void fadd(uint32_t a, uint32_t b, uint32_t c, uint32_t &s, uint32_t &cy) {
+    s = a ^ b ^ c;
+    cy = maj3(a, b, c);
+}
+// 3-bit count (b0, b1, b2) of six bit-7 flags
+__device__ __forceinline__ void count6(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3, uint32_t f4, uint32_t f5,
+                                       uint32_t &b0, uint32_t &b1, uint32_t &b2) {
+    uint32_t s1, c1, s2, c2;
+    fadd(f0, f1, f2, s1, c1);
+    fadd(f3, f4, f5, s2, c2);
+    b0 = s1 ^ s2;
+    const uint32_t c3 = s1 & s2;
+    fadd(c1, c2, c3, b1, b2);
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(256) mrf_decide_walk(const uint8_t *__restrict__ v, int nx, int ny,
+                                                       unsigned long long *__restrict__ ghist,
+                                                       unsigned long long *__restrict__ scal) {
+    constexpr int W = NZ / 4, RPC = 256 / W;  // words per row, rows per CTA
+    static_assert(W == 8 || W == 16 || W == 32, "row = whole lane segment");
+    constexpr uint32_t M7 = 0x7f7f7f7fu;
+    __shared__ uint32_t hsm[8 * 256];
+    uint32_t *wh = hsm + (threadIdx.x >> 5) * 256;
+    for (int b = threadIdx.x; b < 8 * 256; b += 256) hsm[b] = 0;
+    __syncthreads();
+    const int nJ = (ny + RPC - 1) / RPC;
+    const int j = (blockIdx.x % nJ) * RPC + (int)threadIdx.x / W, kw = (int)threadIdx.x % W;
+    const int i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
+    const bool jin = j < ny;
+    const int jc = min(j, ny - 1), jm = max(jc - 1, 0), jp = min(jc + 1, ny - 1);
+    const size_t plane_w = (size_t)ny * W;
+    // row pointers of plane i (ym, yp rows) and of plane i+2 (the centre row)
+    const uint32_t *pm = (const uint32_t *)v + (size_t)i0 * plane_w + (size_t)jm * W + kw;
+    const uint32_t *pp = pm + (size_t)(jp - jm) * W;
+    const uint32_t *pc2 = pm + (size_t)(jc - jm) * W + (size_t)(min(i0 + 2, nx - 1) - i0) * plane_w;
+    const uint32_t *pc = pm + (size_t)(jc - jm) * W;
+    uint32_t xm = __ldg(pc - (i0 > 0 ? plane_w : 0)), c = __ldg(pc), xp = __ldg(pc + (i0 + 1 < nx ? plane_w : 0));
+    uint32_t ym = __ldg(pm), yp = __ldg(pp);
+    // x-pair flags of plane i against i-1: gt(xm, c) (+1) and gt(c, xm) (-1)
+    uint32_t gxm, lxm;
+    {
+        const uint32_t cm = c & M7, nm = xm & M7;
+        gxm = maj3(xm, ~c, nm + M7 - cm);
+        lxm = maj3(c, ~xm, cm + M7 - nm);
+    }
+    unsigned nnz = 0, esq = 0;
+    for (int i = i0; i < i1; ++i) {
+        // plane i+1's loads in flight (rows clamped at the volume's faces)
+        const bool more = i + 1 < nx;
+        pm += more ? plane_w : 0;
+        pp += more ? plane_w : 0;
+        const uint32_t xp2 = __ldg(pc2), ym2 = __ldg(pm), yp2 = __ldg(pp);
+        pc2 += i + 3 < nx ? plane_w : 0;
+        const uint32_t wl0 = __shfl_up_sync(0xffffffffu, c, 1, W), wr0 = __shfl_down_sync(0xffffffffu, c, 1, W);
+        const uint32_t wl = kw > 0 ? wl0 : c << 24, wr = kw < W - 1 ? wr0 : c >> 24;
+        const uint32_t zm = __funnelshift_l(wl, c, 8), zp = __funnelshift_r(c, wr, 8);
+        const uint32_t cm = c & M7;
+        uint32_t gn[5], gc[5];  // gt(n, c), gt(c, n) for n = xp, ym, yp, zm, zp
+        const uint32_t nb[5] = {xp, ym, yp, zm, zp};
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+            const uint32_t nm = nb[u] & M7;
+            gn[u] = maj3(nb[u], ~c, nm + M7 - cm);
+            gc[u] = maj3(c, ~nb[u], cm + M7 - nm);
+        }
+        // +1: gt(xm,c), gt(c,xp), gt(ym,c), gt(c,yp), gt(zm,c), gt(c,zp); -1: the reverses
+        uint32_t p0, p1, p2, n0, n1, n2;
+        count6(gxm, gc[0], gn[1], gc[2], gn[3], gc[4], p0, p1, p2);
+        count6(lxm, gn[0], gc[1], gn[2], gc[3], gn[4], n0, n1, n2);
+        gxm = gc[0];
+        lxm = gn[0];
+        if (jin) {
+            nnz += __popc(((p0 ^ n0) | (p1 ^ n1) | (p2 ^ n2)) & 0x80808080u);
+            atomicAdd(&wh[c & 0xff], 1u);
+            atomicAdd(&wh[(c >> 8) & 0xff], 1u);
+            atomicAdd(&wh[(c >> 16) & 0xff], 1u);
+            atomicAdd(&wh[c >> 24], 1u);
+            const uint32_t dx4 = __vabsdiffu4(c, xp), dy4 = __vabsdiffu4(c, yp), dz4 = __vabsdiffu4(c, zp);
+            esq = __dp4a(dx4, dx4, esq);
+            esq = __dp4a(dy4, dy4, esq);
+            esq = __dp4a(dz4, dz4, esq);
+        }
+        xm = c;
+        c = xp;
+        xp = xp2;
+        ym = ym2;
+        yp = yp2;
+    }
+    unsigned long long nnz64 = nnz, esq64 = esq;
+    for (int q = 16; q; q >>= 1) {
+        nnz64 += __shfl_xor_sync(0xffffffffu, nnz64, q);
+        esq64 += __shfl_xor_sync(0xffffffffu, esq64, q);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&scal[W_NNZ], nnz64);
+        atomicAdd(&scal[W_LAPSQ], esq64);
+    }
+    __syncthreads();
+    unsigned tt = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tt += hsm[q * 256 + threadIdx.x];
+    if (tt) atomicAdd(&ghist[threadIdx.x], (unsigned long long)tt);
+}
+
 // float input: #{sign sum != 0} only (delta via sort; sums via the tree)
 template <typename T>
 __global__ void mrf_nnz_generic(const T *__restrict__ v, i64 nx, i64 ny, i64 nz, unsigned long long *__restrict__ nnz) {
@@ -1234,10 +1356,14 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
         };
         if (quick && ni >= 2) {
             // certified decision first; the Laplacians are stored (MODE 2) only if it fails
-            if (nz == 32) launch(mrf_stream_v4<32, 1>);
-            else if (nz == 64) launch(mrf_stream_v4<64, 1>);
+            auto walk = [&](auto kern) {
+                kern<<<(unsigned)b4, 256, 0, s>>>((const uint8_t *)v, (int)nx, (int)ny, (unsigned long long *)hist,
+                                                  w.scal);
+            };
+            if (nz == 32) walk(mrf_decide_walk<32>);
+            else if (nz == 64) walk(mrf_decide_walk<64>);
             else if (nz == 96) launch(mrf_stream_v4<96, 1>);
-            else launch(mrf_stream_v4<128, 1>);
+            else walk(mrf_decide_walk<128>);
             if (int st = ct::check_launch("mrf_stream_v4")) return st;
             delta_from_hist<<<1, 1024, 0, s>>>(hist, 256, state);
             mrf_quick<<<1, 1, 0, s>>>(state, ni, w.scal);
