@@ -19,6 +19,7 @@ KINDS = {
     "STTM": "tcgen05.st (registers -> TMEM)",
     "UTCATOMSWS": "tcgen05.alloc / dealloc (TMEM allocator)",
     "UTMALDG": "cp.async.bulk.tensor (TMA tile load)",
+    "UTMASTG": "cp.async.bulk.tensor shared -> global (TMA tile store)",
     "UBLKCP": "cp.async.bulk (bulk copy)",
     "SYNCS": "mbarrier arrive / try_wait",
     "LDGSTS": "cp.async (Ampere-style async copy)",
