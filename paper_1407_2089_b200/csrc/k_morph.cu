@@ -187,19 +187,6 @@ __global__ void __launch_bounds__(256) pack_rows_u8v(const uint8_t *__restrict__
 }
 
 template <typename R>
-__device__ __forceinline__ R rowM(const R *rows, i64 i, i64 j, i64 nx, i64 ny) {
-    return (i >= 0 && i < nx && j >= 0 && j < ny) ? rows[i * ny + j] : (R)0;
-}
-
-// dilation row D(i,j) over the whole (possibly out-of-volume) row
-template <typename R>
-__device__ __forceinline__ R rowD(const R *rows, i64 i, i64 j, i64 nx, i64 ny, R kmask) {
-    const R c = rowM(rows, i, j, nx, ny);
-    return (c | (c << 1) | (c >> 1) | rowM(rows, i - 1, j, nx, ny) | rowM(rows, i + 1, j, nx, ny) |
-            rowM(rows, i, j - 1, nx, ny) | rowM(rows, i, j + 1, nx, ny)) & kmask;
-}
-
-template <typename R>
 __global__ void __launch_bounds__(256) close1_bits(const R *__restrict__ rows, i64 nx, i64 ny, int nz,
                                                    uint8_t *__restrict__ out, R *__restrict__ out_rows) {
     __shared__ __align__(16) uint8_t stage[8][32 * ct::rbits<R>()];
@@ -209,18 +196,29 @@ __global__ void __launch_bounds__(256) close1_bits(const R *__restrict__ rows, i
     const i64 nrows = nx * ny;
     const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
     const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+    // rows = nx ny < 2^31 (checked by the caller): 32-bit row coordinates by multiply-shift
+    const ct::FastDiv fny((uint32_t)ny);
+    const int inx = (int)nx, iny = (int)ny;
+    auto M = [&](int ii, int jj) -> R {
+        return (ii >= 0 && ii < inx && jj >= 0 && jj < iny) ? rows[(i64)ii * iny + jj] : (R)0;
+    };
+    auto sh = [](R w) { return w | (w << 1) | (w >> 1); };
     for (i64 r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
         const i64 r = r0 + lane;
         R e = 0;
         if (r < nrows) {
-            const i64 i = r / ny, j = r - i * ny;
+            const int i = (int)fny.div((uint32_t)r), j = (int)r - i * iny;
+            // the 13 distinct rows of the two-step cross, each loaded once
             const R m = rows[r];
-            const R d = rowD(rows, i, j, nx, ny, kmask);
+            const R xm1 = M(i - 1, j), xp1 = M(i + 1, j), ym1 = M(i, j - 1), yp1 = M(i, j + 1);
+            const R xm2 = M(i - 2, j), xp2 = M(i + 2, j), ym2 = M(i, j - 2), yp2 = M(i, j + 2);
+            const R mm = M(i - 1, j - 1), mp = M(i - 1, j + 1), pm = M(i + 1, j - 1), pp = M(i + 1, j + 1);
+            const R d = (sh(m) | xm1 | xp1 | ym1 | yp1) & kmask;
             // cross neighbours of D; outside the volume D equals the single in-volume M
-            const R dxm = i > 0 ? rowD(rows, i - 1, j, nx, ny, kmask) : m;
-            const R dxp = i < nx - 1 ? rowD(rows, i + 1, j, nx, ny, kmask) : m;
-            const R dym = j > 0 ? rowD(rows, i, j - 1, nx, ny, kmask) : m;
-            const R dyp = j < ny - 1 ? rowD(rows, i, j + 1, nx, ny, kmask) : m;
+            const R dxm = i > 0 ? (sh(xm1) | xm2 | m | mm | mp) & kmask : m;
+            const R dxp = i < inx - 1 ? (sh(xp1) | xp2 | m | pm | pp) & kmask : m;
+            const R dym = j > 0 ? (sh(ym1) | ym2 | m | mm | pm) & kmask : m;
+            const R dyp = j < iny - 1 ? (sh(yp1) | yp2 | m | mp | pp) & kmask : m;
             const R dkm = ((d << 1) | (m & (R)1)) & kmask;    // D at k-1; k=-1 -> M(k=0)
             const R dkp = (d >> 1) | (m & top);               // D at k+1; k=nz -> M(k=nz-1)
             e = d & dxm & dxp & dym & dyp & dkm & dkp;
@@ -265,7 +263,7 @@ int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i6
         threshold_kernel<T><<<ct::grid_for(n, 256), 256, 0, s>>>(in, n, otsu, t_host, out);
         return ct::check_launch("threshold");
     }
-    if (r == 1 && nz <= 128 && nz % 4 == 0 && work && ((uintptr_t)out & 15) == 0) {
+    if (r == 1 && nz <= 128 && nz % 4 == 0 && work && ((uintptr_t)out & 15) == 0 && nx * ny < (1ll << 31)) {
         const i64 nrows = nx * ny;
         auto run = [&](auto tag) -> int {
             using R = decltype(tag);
@@ -323,8 +321,9 @@ extern "C" int ct_threshold_close_rows(const void *in, int dtype, int64_t nx, in
         ct::set_error("bad closing arguments");
         return CT_ERR_PARAM;
     }
-    if (nz > 128 || nz % 4 != 0 || ((uintptr_t)mask_out & 15) || ((uintptr_t)rows_out & 15)) {
-        ct::set_error("ct_threshold_close_rows: needs nz <= 128, nz %% 4 == 0, 16-byte aligned outputs");
+    if (nz > 128 || nz % 4 != 0 || ((uintptr_t)mask_out & 15) || ((uintptr_t)rows_out & 15) ||
+        nx * ny >= (1ll << 31)) {
+        ct::set_error("ct_threshold_close_rows: needs nz <= 128, nz %% 4 == 0, nx ny < 2^31, 16-byte aligned outputs");
         return CT_ERR_UNSUPPORTED;
     }
     cudaStream_t s = (cudaStream_t)stream;
