@@ -286,10 +286,11 @@ template <typename R, bool BITS>
 __global__ void ccl_run_union(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 nx, i64 ny, int nz,
                               int32_t *labels) {
     const i64 nrows = nx * ny;
+    const ct::FastDiv fny((uint32_t)ny);  // rows < 2^31 (labels are int32 voxel indices)
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
         const R w = load_row<R, BITS>(mask, rows, r, nz);
         if (!w) continue;
-        const i64 i = r / ny, j = r - i * ny;
+        const i64 i = fny.div((uint32_t)r), j = r - i * ny;
         const i64 nb[4] = {j > 0 ? r - 1 : -1, (i > 0 && j > 0) ? r - ny - 1 : -1, i > 0 ? r - ny : -1,
                            (i > 0 && j + 1 < ny) ? r - ny + 1 : -1};
 #pragma unroll
@@ -430,6 +431,7 @@ __global__ void tab_stats(const int32_t *__restrict__ labels, i64 ny, i64 nz, co
                           const int64_t *__restrict__ counters, TabWork w, const TI *__restrict__ intensity) {
     const i64 nfg = counters[CT_CNT_FG];
     const bool over = counters[CT_CNT_OVERFLOW] != 0;
+    const ct::FastDiv fnz((uint32_t)nz), fny((uint32_t)ny);  // voxel indices are int32 (N < 2^31)
     for (i64 e0 = blockIdx.x * (i64)blockDim.x; e0 < nfg; e0 += (i64)gridDim.x * blockDim.x) {
         const i64 e = e0 + threadIdx.x;
         int c = -1;
@@ -446,7 +448,8 @@ __global__ void tab_stats(const int32_t *__restrict__ labels, i64 ny, i64 nz, co
         if (!act) continue;
         const unsigned peers = __match_any_sync(full, c);
         const int leader = __ffs(peers) - 1;
-        const int k = (int)(p % nz), j = (int)((p / nz) % ny), i = (int)(p / (ny * nz));
+        const uint32_t pz = fnz.div((uint32_t)p), pi = fny.div(pz);
+        const int k = p - (int)(pz * (uint32_t)nz), j = (int)(pz - pi * (uint32_t)ny), i = (int)pi;
         const int imin = __reduce_min_sync(peers, i), jmin = __reduce_min_sync(peers, j),
                   kmin = __reduce_min_sync(peers, k);
         const int imax = __reduce_max_sync(peers, i), jmax = __reduce_max_sync(peers, j),
