@@ -1135,6 +1135,98 @@ __global__ void __launch_bounds__(256) mrf_decide_walk(const uint8_t *__restrict
     if (tt) atomicAdd(&ghist[threadIdx.x], (unsigned long long)tt);
 }
 
+// u16 form of mrf_decide_walk (nz in {32, 64}: a row is 16 / 32 lanes of
+// 2-voxel words): the same walk, 16-bit lanes (a > b = carry-out majority at
+// bit 15), carry-save counting, the 4096-bin SMEM histogram of mrf_stream_nz
+// (values >= 4096 to global), E in 64-bit integers.  Results equal
+// mrf_stream_nz<uint16_t, ., NZ, 1>'s.
+template <int NZ>
+__global__ void __launch_bounds__(256) mrf_decide_walk16(const uint16_t *__restrict__ v, int nx, int ny,
+                                                         unsigned long long *__restrict__ ghist,
+                                                         unsigned long long *__restrict__ scal) {
+    constexpr int W = NZ / 2, RPC = 256 / W;  // words per row, rows per CTA
+    static_assert(W == 16 || W == 32, "row = whole lane segment");
+    constexpr uint32_t M15 = 0x7fff7fffu;
+    __shared__ uint32_t hsm[4096];
+    for (int b = threadIdx.x; b < 4096; b += 256) hsm[b] = 0;
+    __syncthreads();
+    const int nJ = (ny + RPC - 1) / RPC;
+    const int j = (blockIdx.x % nJ) * RPC + (int)threadIdx.x / W, kw = (int)threadIdx.x % W;
+    const int i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
+    const bool jin = j < ny;
+    const int jc = min(j, ny - 1), jm = max(jc - 1, 0), jp = min(jc + 1, ny - 1);
+    const size_t plane_w = (size_t)ny * W;
+    const uint32_t *pm = (const uint32_t *)v + (size_t)i0 * plane_w + (size_t)jm * W + kw;
+    const uint32_t *pp = pm + (size_t)(jp - jm) * W;
+    const uint32_t *pc = pm + (size_t)(jc - jm) * W;
+    const uint32_t *pc2 = pc + (size_t)(min(i0 + 2, nx - 1) - i0) * plane_w;
+    uint32_t xm = __ldg(pc - (i0 > 0 ? plane_w : 0)), c = __ldg(pc), xp = __ldg(pc + (i0 + 1 < nx ? plane_w : 0));
+    uint32_t ym = __ldg(pm), yp = __ldg(pp);
+    uint32_t gxm, lxm;
+    {
+        const uint32_t cm = c & M15, nm = xm & M15;
+        gxm = maj3(xm, ~c, nm + M15 - cm);
+        lxm = maj3(c, ~xm, cm + M15 - nm);
+    }
+    unsigned nnz = 0;
+    unsigned long long esq = 0;
+    auto hadd = [&](uint32_t val) {
+        if (val < 4096) atomicAdd(&hsm[val], 1u);
+        else atomicAdd(&ghist[val], 1ull);
+    };
+    auto sq2 = [](uint32_t a, uint32_t b) {  // sum of the two lanes' squared differences
+        const int d0 = (int)(a & 0xffffu) - (int)(b & 0xffffu), d1 = (int)(a >> 16) - (int)(b >> 16);
+        return (unsigned long long)((long long)d0 * d0) + (unsigned long long)((long long)d1 * d1);
+    };
+    for (int i = i0; i < i1; ++i) {
+        const bool more = i + 1 < nx;
+        pm += more ? plane_w : 0;
+        pp += more ? plane_w : 0;
+        const uint32_t xp2 = __ldg(pc2), ym2 = __ldg(pm), yp2 = __ldg(pp);
+        pc2 += i + 3 < nx ? plane_w : 0;
+        const uint32_t wl0 = __shfl_up_sync(0xffffffffu, c, 1, W), wr0 = __shfl_down_sync(0xffffffffu, c, 1, W);
+        const uint32_t wl = kw > 0 ? wl0 : c << 16, wr = kw < W - 1 ? wr0 : c >> 16;
+        const uint32_t zm = __funnelshift_l(wl, c, 16), zp = __funnelshift_r(c, wr, 16);
+        const uint32_t cm = c & M15;
+        uint32_t gn[5], gc[5];
+        const uint32_t nb[5] = {xp, ym, yp, zm, zp};
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+            const uint32_t nm = nb[u] & M15;
+            gn[u] = maj3(nb[u], ~c, nm + M15 - cm);
+            gc[u] = maj3(c, ~nb[u], cm + M15 - nm);
+        }
+        uint32_t p0, p1, p2, n0, n1, n2;
+        count6(gxm, gc[0], gn[1], gc[2], gn[3], gc[4], p0, p1, p2);
+        count6(lxm, gn[0], gc[1], gn[2], gc[3], gn[4], n0, n1, n2);
+        gxm = gc[0];
+        lxm = gn[0];
+        if (jin) {
+            nnz += __popc(((p0 ^ n0) | (p1 ^ n1) | (p2 ^ n2)) & 0x80008000u);
+            hadd(c & 0xffffu);
+            hadd(c >> 16);
+            esq += sq2(c, xp) + sq2(c, yp) + sq2(c, zp);
+        }
+        xm = c;
+        c = xp;
+        xp = xp2;
+        ym = ym2;
+        yp = yp2;
+    }
+    unsigned long long nnz64 = nnz;
+    for (int q = 16; q; q >>= 1) {
+        nnz64 += __shfl_xor_sync(0xffffffffu, nnz64, q);
+        esq += __shfl_xor_sync(0xffffffffu, esq, q);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&scal[W_NNZ], nnz64);
+        atomicAdd(&scal[W_LAPSQ], esq);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 4096; b += 256)
+        if (hsm[b]) atomicAdd(&ghist[b], (unsigned long long)hsm[b]);
+}
+
 // float input: #{sign sum != 0} only (delta via sort; sums via the tree)
 template <typename T>
 __global__ void mrf_nnz_generic(const T *__restrict__ v, i64 nx, i64 ny, i64 nz, unsigned long long *__restrict__ nnz) {
@@ -1394,7 +1486,14 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
                                                                          : mrf_stream_nz<T, LT, 128, 1>;
             auto k2 = nz == 32 ? mrf_stream_nz<T, LT, 32, 2> : nz == 64 ? mrf_stream_nz<T, LT, 64, 2>
                                                                          : mrf_stream_nz<T, LT, 128, 2>;
-            k1<<<(unsigned)blocks, 256, 0, s>>>(v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal, lap);
+            if (sizeof(T) == 2 && nz <= 64) {  // barrier-free walk (u16 words of two voxels)
+                const int rpc = 256 / ((int)nz / 2);
+                const unsigned bw = (unsigned)(((ny + rpc - 1) / rpc) * ((nx + MIPER - 1) / MIPER));
+                auto kw = nz == 32 ? mrf_decide_walk16<32> : mrf_decide_walk16<64>;
+                kw<<<bw, 256, 0, s>>>((const uint16_t *)v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal);
+            } else {
+                k1<<<(unsigned)blocks, 256, 0, s>>>(v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal, lap);
+            }
             if (int st = ct::check_launch("mrf_stream_nz")) return st;
             delta_from_hist<<<1, 1024, 0, s>>>(hist, sizeof(T) == 1 ? 256 : 65536, state);
             mrf_quick<<<1, 1, 0, s>>>(state, ni, w.scal);
