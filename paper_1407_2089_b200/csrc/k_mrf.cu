@@ -1254,11 +1254,35 @@ __global__ void lap_sum_int(const T *__restrict__ v, i64 ny, i64 nz, uint32_t my
 // (nbins: 256 for u8 input -- no other bin can be non-empty -- else 65536)
 __global__ void delta_from_hist(const uint64_t *__restrict__ hist, int nbins, double *state) {
     __shared__ int prev_of[1024];
-    __shared__ int wg[32];
+    __shared__ int wg[32], wlo[32], whi[32];
     const int t = threadIdx.x;
-    const int per = (nbins + 1023) / 1024;
+    // the non-empty span first (coalesced): 12-bit data in 65536 bins scans 4096
+    int lo = INT32_MAX, hi = -1;
+#pragma unroll 16
+    for (int b = t; b < nbins; b += 1024)
+        if (hist[b]) {
+            lo = min(lo, b);
+            hi = b;
+        }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((t & 31) == 0) {
+        wlo[t >> 5] = lo;
+        whi[t >> 5] = hi;
+    }
+    __syncthreads();
+    lo = INT32_MAX;
+    hi = -1;
+    for (int i = 0; i < 32; ++i) {
+        lo = min(lo, wlo[i]);
+        hi = max(hi, whi[i]);
+    }
+    const int span = hi >= lo ? hi - lo + 1 : 0;
+    const int per = (span + 1023) / 1024, b0 = lo + t * per, b1 = min(b0 + per, hi + 1);
     int first = -1, last = -1, gap = INT32_MAX;
-    for (int b = t * per; b < min(t * per + per, nbins); ++b) {
+    for (int b = b0; b < b1; ++b) {
         if (!hist[b]) continue;
         if (last >= 0) gap = min(gap, b - last);
         if (first < 0) first = b;
