@@ -495,12 +495,15 @@ __device__ __noinline__ uint32_t qz_exact(const TcParams *__restrict__ prm, int 
     return qv > 0 ? (uint32_t)qv : 0u;
 }
 
-template <int NZ, int SSTG, typename Traw = uint8_t, int NP = 4, int NL = 4>
+// RAWG: the epilogue reads raw straight from global memory (prefetched at the
+// tile's start) instead of a staged copy, so that a 2-byte raw tile does not
+// cost a pipeline stage (u16: 4 stages of 5 planes fit, 3 with staged raw)
+template <int NZ, int SSTG, typename Traw = uint8_t, int NP = 4, int NL = 4, bool RAWG = false>
 __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__ CUtensorMap tmp,
                                                          const __grid_constant__ CUtensorMap tmr, long long nlines,
                                                          const TcParams *__restrict__ prm, int r,
-                                                         Traw *__restrict__ q, unsigned long long *__restrict__ fix,
-                                                         long long cap) {
+                                                         const Traw *__restrict__ raw, Traw *__restrict__ q,
+                                                         unsigned long long *__restrict__ fix, long long cap) {
     constexpr int RB = (int)sizeof(Traw);
     constexpr int LOP = lo_pair(NP, NL), SPL = 8 * LOP;
     constexpr int NCH = NZ / 16;
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
     constexpr uint32_t PLB = TM * 16;                                // bytes per plane per chunk
     constexpr uint32_t LBOA = NP * PLB, SBOA = 128;                  // staged data planes
     constexpr int DB = NCH * NP * PLB;                               // data bytes per stage
-    constexpr int RBT = TM * NZ * RB;                                // raw bytes per stage
+    constexpr int RBT = RAWG ? 0 : TM * NZ * RB;                     // raw bytes per stage
     constexpr int SB = DB + RBT;
     constexpr int BW = NZ * NZ, BE = NZ * 32;
     constexpr int ACOL = 5 * NZ;
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
                 tc::mbar_expect_tx(&full[s], SB);
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) tc::tma_load_3d(dst + c * NP * PLB, &tmp, 16 * c, l0, 0, &full[s]);
-                tc::tma_load_2d(dst + DB, &tmr, 0, l0, &full[s]);
+                if constexpr (!RAWG) tc::tma_load_2d(dst + DB, &tmr, 0, l0, &full[s]);
             }
             __syncwarp();
         }
@@ -655,6 +658,17 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
             const int s = (int)(k % SSTG);
             const long long l = (t0 + k * gs) * TM + m;
             const bool live = l < nlines;
+            // RAWG: the tile's raw words, in flight during the wait and the drain
+            uint32_t rg[RAWG ? CW * RB / 4 : 1];
+            if constexpr (RAWG) {
+                static_assert(CW * RB % 16 == 0, "16-byte raw loads");
+                const uint4 *src = (const uint4 *)((const uint8_t *)raw + ((live ? l : 0) * NZ + h0) * RB);
+#pragma unroll
+                for (int i = 0; i < CW * RB / 16; ++i) {
+                    const uint4 x = __ldg(src + i);
+                    rg[4 * i] = x.x; rg[4 * i + 1] = x.y; rg[4 * i + 2] = x.z; rg[4 * i + 3] = x.w;
+                }
+            }
             tc::mbar_wait(&afull, (uint32_t)(k & 1));
             tc::fence_after();
             // Y = S + half + eps per column.  CW <= 16: all accumulator words are
@@ -699,12 +713,16 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
             }
             if (cg == 0 && k + ES < nmine) edge(k + ES);
             // raw of the tile (stage s, already landed: MMA(k) consumed it), then release the stage
-            tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
             // the thread's CW * RB raw / q bytes move in 16-byte chunks (8-byte when
             // h0 * RB is not 16-aligned: NZ = 96)
             constexpr int QW = CW * RB / 4;  // 32-bit words
             static_assert(CW * RB % 8 == 0, "raw row chunk");
             uint32_t rw[QW];
+            if constexpr (RAWG) {
+#pragma unroll
+                for (int i = 0; i < QW; ++i) rw[i] = rg[i];
+            } else {
+            tc::mbar_wait(&full[s], (uint32_t)((k / SSTG) & 1));
             const uint8_t *rl = sm + s * SB + DB + (m * NZ + h0) * RB;
             if constexpr (CW * RB % 16 == 0) {
 #pragma unroll
@@ -718,6 +736,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
                     const uint2 x = *(const uint2 *)(rl + 8 * i);
                     rw[2 * i] = x.x; rw[2 * i + 1] = x.y;
                 }
+            }
             }
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&empty[s]);
@@ -923,19 +942,21 @@ int gaussian_q_tc(const Traw *raw, int64_t nx, int64_t ny, int64_t nz, int rx, i
             ct::set_error("tensor map (pass z) rejected");
             return CT_ERR_UNSUPPORTED;
         }
-        void (*kz)(const CUtensorMap, const CUtensorMap, long long, const TcParams *, int, Traw *,
+        void (*kz)(const CUtensorMap, const CUtensorMap, long long, const TcParams *, int, const Traw *, Traw *,
                    unsigned long long *, long long);
         int stg;
-        if constexpr (RB == 2) {
-            stg = 3;
-            kz = nz == 64 ? tc_pass_z_ws<64, 3, Traw, 5, 5> : tc_pass_z_ws<32, 3, Traw, 5, 5>;
+        bool rawg = false;
+        if constexpr (RB == 2) {  // u16: raw from global, 4 stages of 5 planes
+            stg = 4;
+            rawg = true;
+            kz = nz == 64 ? tc_pass_z_ws<64, 4, Traw, 5, 5, true> : tc_pass_z_ws<32, 4, Traw, 5, 5, true>;
         } else {
             stg = nz == 96 ? 2 : 4;
             kz = nz == 64 ? tc_pass_z_ws<64, 4, Traw> : nz == 96 ? tc_pass_z_ws<96, 2, Traw> : tc_pass_z_ws<32, 4, Traw>;
         }
-        const size_t sm = (size_t)stg * (NP * TM * nz + TM * nz * RB) + NL * nz * nz + NL * nz * 32 + 1024;
+        const size_t sm = (size_t)stg * (NP * TM * nz + (rawg ? 0 : TM * nz * RB)) + NL * nz * nz + NL * nz * 32 + 1024;
         cudaFuncSetAttribute(kz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        kz<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tp, tr, lines, prm, rz, q, fix, cap);
+        kz<<<(unsigned)std::min<long long>(tiles, nsm), WS_NT, sm, s>>>(tp, tr, lines, prm, rz, raw, q, fix, cap);
         if (int st = ct::check_launch("tc_pass_z")) return st;
     }
     return CT_OK;
