@@ -10,7 +10,7 @@
 // (weight rounding, truncation of intermediates, dropped limb pairs of weight
 // < 2^-43, and scipy's own float64 rounding); voxels whose residual lies
 // within that bound of a rounding boundary go to the fix list and are
-// recomputed in scipy's exact operation order (gauss_fixup in k_gauss.cu).
+// recomputed in scipy's exact operation order (fix_p1s / fix_p2q_s in k_gauss.cu).
 //
 //   pass x, y (strided axes): D[out row][col] = A[out row][in row] * B[in row][col]
 //       A = the tap band (128 x 256, Toeplitz, constant) held in TMEM;
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(96) tc_prep(const double *__restrict__ w, int 
     for (int o = 16; o; o >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
     wmax *= 1.0000001;
     // taps Q_j < 2^(8 nl); pass z: fw <= 36 + 8 (nl - 4) keeps the edge tail
-    // sums < 16 * 2^(8 nl - 1) (16 pieces, see tc_pass_z)
+    // sums < 16 * 2^(8 nl - 1) (16 pieces, see tc_pass_z_ws)
     const double qmax = ldexp(1.0, 8 * nl) - 1.0;
     int fw = a == 2 ? 36 + 8 * (nl - 4) : FW + 8 * (nl - 4);
     while (fw > 24 && wmax * ldexp(1.0, fw) >= qmax) --fw;
@@ -216,7 +216,7 @@ __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, u
 }
 
 // ---------------------------------------------------------------------------
-// Passes x and y, warp-specialised (launched for pass x):
+// Passes x and y, warp-specialised:
 //   warp 0      TMA producer: one cp.async.bulk.tensor box per tile (256
 //               input rows x TN columns of every byte plane) into a ring of
 //               SSTG shared-memory stages (full / empty mbarriers);
@@ -230,9 +230,9 @@ __device__ __forceinline__ void planes4(uint32_t o0, uint32_t o1, uint32_t o2, u
 //               tiles per column at the volume's faces stalled the tensor pipe);
 //   warps 3..18 epilogue: TMEM -> registers, combine the limb accumulators in
 //               exact 64-bit integers, split into the next pass's byte planes,
-//               staged, coalesced 16-byte stores (warp w reads TMEM lane
-//               quarter w % 4, column group (w - 3) / 4).
-// Same integer arithmetic as tc_pass_xy (bit-identical planes).
+//               staged in 64B / 32B-swizzled shared memory and stored by one
+//               TMA tensor store per tile (warp w reads TMEM lane quarter
+//               w % 4, column group (w - 3) / 4).
 // ---------------------------------------------------------------------------
 constexpr int WS_EPI = 16;                 // epilogue warps (4 per TMEM lane quarter)
 constexpr int WS_NT = 32 * (2 + WS_EPI);   // 576 threads (pass z)
@@ -477,9 +477,13 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
     if (wp == 1) tc::tmem_dealloc(base, 512);
 }
 
-// The exact test and quantisation of one pass-z voxel from S (tc_pass_z's
-// qval): out of line, so the rare lanes that need it cost the fast epilogue
-// no registers.
+// The exact test and quantisation of one pass-z voxel from its accumulator
+// sum S (scale 2^zs):  V = S - 2^(zs-1), q = max(raw - ceil(V / 2^zs), 0)
+// (= rint(max(raw - bg, 0))), and the voxel goes to the fix list iff
+// (eps - V) mod 2^zs <= 2 eps and raw 2^zs - V >= 2^zs - eps (a rounding
+// boundary within the certified error, with raw - bg possibly >= 1/2).  Out
+// of line, so the rare lanes that need it cost the fast epilogue no
+// registers.
 __device__ __noinline__ uint32_t qz_exact(const TcParams *__restrict__ prm, int spl, unsigned long long S, uint32_t rv,
                                           unsigned long long idx, unsigned long long *__restrict__ fix, long long cap) {
     const long long eps = prm->eps;
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
     constexpr int RB = (int)sizeof(Traw);
     constexpr int LOP = lo_pair(NP, NL), SPL = 8 * LOP;
     constexpr int NCH = NZ / 16;
-    constexpr uint32_t LBOB = 128, SBOB = NCH * 128, SBOE = 256;  // taps (K-major, as tc_pass_z)
+    constexpr uint32_t LBOB = 128, SBOB = NCH * 128, SBOE = 256;  // taps (K-major): in-line band, edge block
     constexpr uint32_t PLB = TM * 16;                                // bytes per plane per chunk
     constexpr uint32_t LBOA = NP * PLB, SBOA = 128;                  // staged data planes
     constexpr int DB = NCH * NP * PLB;                               // data bytes per stage
@@ -626,7 +630,7 @@ __global__ void __launch_bounds__(WS_NT, 1) tc_pass_z_ws(const __grid_constant__
         const int qq = wp & 3, cg = (wp - 2) >> 2, m = 32 * qq + lane, h0 = cg * CW;
         const uint32_t la = base + ((uint32_t)(32 * qq) << 16);
         // Y = S + half + eps: the certification test is (Y mod 2^zs) <= 2 eps and,
-        // when it fails, Y >> zs = ceil((S - half) / 2^zs) (see tc_pass_z).  For
+        // when it fails, Y >> zs = ceil((S - half) / 2^zs) (no borrow from the low bits; qz_exact).  For
         // 32 <= zs < 64 and 2 eps < 2^32 the fast path reads bgq from Y's high
         // word and tests the top 32 fractional bits conservatively; otherwise
         // (fth = ~0) every voxel takes the exact path
