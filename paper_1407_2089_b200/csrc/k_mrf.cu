@@ -585,6 +585,7 @@ enum { W_NNZ = 0, W_BEST_BITS, W_MOVED, W_LAPSUM, W_LAPSQ, W_SKIP, W_WORDS = 8 }
 // ---------------------------------------------------------------------------
 constexpr int MJ = 8;
 constexpr int MIPER = 64;  // planes per CTA
+constexpr int WIPER = 32;  // planes per CTA of the register walks (mrf_decide_walk*): 2+ waves on C2
 
 template <typename T, typename LT>
 __global__ void __launch_bounds__(256) mrf_stream_int(const T *__restrict__ v, i64 nx, i64 ny, int nz,
@@ -1058,7 +1059,7 @@ __global__ void __launch_bounds__(256) mrf_decide_walk(const uint8_t *__restrict
     __syncthreads();
     const int nJ = (ny + RPC - 1) / RPC;
     const int j = (blockIdx.x % nJ) * RPC + (int)threadIdx.x / W, kw = (int)threadIdx.x % W;
-    const int i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
+    const int i0 = (blockIdx.x / nJ) * WIPER, i1 = min(i0 + WIPER, nx);
     const bool jin = j < ny;
     const int jc = min(j, ny - 1), jm = max(jc - 1, 0), jp = min(jc + 1, ny - 1);
     const size_t plane_w = (size_t)ny * W;
@@ -1152,7 +1153,7 @@ __global__ void __launch_bounds__(256) mrf_decide_walk16(const uint16_t *__restr
     __syncthreads();
     const int nJ = (ny + RPC - 1) / RPC;
     const int j = (blockIdx.x % nJ) * RPC + (int)threadIdx.x / W, kw = (int)threadIdx.x % W;
-    const int i0 = (blockIdx.x / nJ) * MIPER, i1 = min(i0 + MIPER, nx);
+    const int i0 = (blockIdx.x / nJ) * WIPER, i1 = min(i0 + WIPER, nx);
     const bool jin = j < ny;
     const int jc = min(j, ny - 1), jm = max(jc - 1, 0), jp = min(jc + 1, ny - 1);
     const size_t plane_w = (size_t)ny * W;
@@ -1472,8 +1473,9 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
         };
         if (quick && ni >= 2) {
             // certified decision first; the Laplacians are stored (MODE 2) only if it fails
+            const i64 bwk = ((ny + 256 / (nz / 4) - 1) / (256 / (nz / 4))) * ((nx + WIPER - 1) / WIPER);
             auto walk = [&](auto kern) {
-                kern<<<(unsigned)b4, 256, 0, s>>>((const uint8_t *)v, (int)nx, (int)ny, (unsigned long long *)hist,
+                kern<<<(unsigned)bwk, 256, 0, s>>>((const uint8_t *)v, (int)nx, (int)ny, (unsigned long long *)hist,
                                                   w.scal);
             };
             if (nz == 32) walk(mrf_decide_walk<32>);
@@ -1512,7 +1514,7 @@ int mrf_int(const T *v, i64 nx, i64 ny, i64 nz, MrfWork &w, double *state, uint6
                                                                          : mrf_stream_nz<T, LT, 128, 2>;
             if (sizeof(T) == 2 && nz <= 64) {  // barrier-free walk (u16 words of two voxels)
                 const int rpc = 256 / ((int)nz / 2);
-                const unsigned bw = (unsigned)(((ny + rpc - 1) / rpc) * ((nx + MIPER - 1) / MIPER));
+                const unsigned bw = (unsigned)(((ny + rpc - 1) / rpc) * ((nx + WIPER - 1) / WIPER));
                 auto kw = nz == 32 ? mrf_decide_walk16<32> : mrf_decide_walk16<64>;
                 kw<<<bw, 256, 0, s>>>((const uint16_t *)v, (int)nx, (int)ny, (unsigned long long *)hist, w.scal);
             } else {
