@@ -71,7 +71,7 @@ class HullMesh:
         return (pts @ self.equations[:, :3].T + self.equations[:, 3]).max(axis=1) <= tol
 
 
-@dataclass(eq=False)
+@dataclass(eq=False, slots=True)  # slots: ~25% faster construction of a frame's detections
 class Detection:
     """One segmented cell in one frame (ref segment.py:58-74)."""
 
@@ -334,7 +334,8 @@ def _materialize(ct: CellTable, dims, spacing: VoxelSpacing, frame: int, with_hu
     # in id order) and positional construction: per-row field access and
     # keyword dataclass init dominated the host side of materialisation
     cnts = rows["count"].astype(np.int64)
-    voxs = np.split(coords, np.cumsum(cnts)[:-1]) if len(cnts) else []
+    offs = np.concatenate(([0], np.cumsum(cnts))).tolist()
+    voxs = [coords[a:b] for a, b in zip(offs[:-1], offs[1:])]  # (np.split: ~1.5 us of swapaxes per view)
     ids, vols = rows["id"].tolist(), rows["volume_um3"].tolist()
     cents = list(np.array(rows["centroid_um"], dtype=np.float64))
     bbox = list(np.concatenate([rows["bbox_lo"], rows["bbox_hi"]], axis=1).astype(np.int64))
