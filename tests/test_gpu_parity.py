@@ -308,7 +308,7 @@ def test_certified_fast_k1_matches_exact(cuda, mode):
 @pytest.mark.parametrize("sigma,shape,seed", [(10.0, (256, 192, 64), 1), (6.0, (200, 64, 32), 2),
                                               (12.0, (130, 130, 64), 3), (3.0, (64, 32, 32), 4),
                                               (10.0, (96, 64, 96), 5),
-                                              # ny % 128 == 0: the fused pass y + z kernel
+                                              # ny % 128 == 0, and partial row / line tiles
                                               (10.0, (256, 256, 64), 6), (6.0, (130, 128, 32), 7),
                                               (12.0, (64, 384, 64), 8), (4.0, (33, 128, 64), 9)])
 def test_tensor_core_k1_matches_exact(cuda, sigma, shape, seed):
