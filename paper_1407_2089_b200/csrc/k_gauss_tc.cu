@@ -278,7 +278,10 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
     static_assert(AB + ASTG * NACC * TN <= 512, "TMEM: band + accumulator sets");
     extern __shared__ __align__(1024) uint8_t sm[];  // [SSTG][SB] operand stages, [2][OBUF] output tiles
     uint8_t *sout = sm + SSTG * SB;
-    __shared__ uint64_t full[SSTG], ready[SSTG], empty[SSTG], afull[ASTG], aempty[ASTG];
+    // aempty[a][acc]: accumulator acc of set a drained -- pass x releases them one
+    // by one, so the next tile's MMAs into accumulator 0 start while the others
+    // drain (100 -> 90 us on C2); pass y releases the set at once (aempty[a][0])
+    __shared__ uint64_t full[SSTG], ready[SSTG], empty[SSTG], afull[ASTG], aempty[ASTG][NACC];
     __shared__ uint32_t tbase;
     const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
     if (wp == 1) tc::tmem_alloc(&tbase, 512);
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
         }
         for (int i = 0; i < ASTG; ++i) {
             tc::mbar_init(&afull[i], 1);
-            tc::mbar_init(&aempty[i], WS_EPI);
+            for (int j = 0; j < NACC; ++j) tc::mbar_init(&aempty[i][j], WS_EPI);
         }
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&tmap);
@@ -378,26 +381,47 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
         for (long long k = 0; k < nmine; ++k) {
             const int s = (int)(k % SSTG), a = (int)(k % ASTG);
             tc::mbar_wait(&ready[s], (uint32_t)((k / SSTG) & 1));
-            tc::mbar_wait(&aempty[a], (uint32_t)((k / ASTG) & 1) ^ 1u);
-            tc::fence_after();
-            if (tc::elect_one()) {
-                const uint64_t d0 = tc::smem_desc_sw(tc::smem_u32(sm + s * SB), LBO, SBO, TN);
-                bool first[NACC];
+            const uint64_t d0 = tc::smem_desc_sw(tc::smem_u32(sm + s * SB), LBO, SBO, TN);
+            if constexpr (NPIN == 1) {
+                // pass x: the MMAs grouped by accumulator (= weight limb), each group
+                // issued as soon as its accumulator of the previous tile is drained
 #pragma unroll
-                for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
-#pragma unroll
-                for (int da = 0; da < NPIN; ++da)
-#pragma unroll
-                    for (int b = 0; b < NL; ++b) {
-                        const int acc = NPIN == 1 ? b : da + b - lo_pair(NPIN, NL);
-                        if (acc < 0 || acc >= NACC) continue;
+                for (int acc = 0; acc < NACC; ++acc) {
+                    tc::mbar_wait(&aempty[a][acc], (uint32_t)((k / ASTG) & 1) ^ 1u);
+                    tc::fence_after();
+                    if (tc::elect_one()) {
 #pragma unroll
                         for (int ks = 0; ks < KXY / 32; ++ks)
-                            tc::mma_i8_ts(base + AB + (a * NACC + acc) * TN, base + b * 64 + ks * 8,
-                                          d0 + (uint64_t)((da * PB + ks * 32 * TN) >> 4), idesc,
-                                          first[acc] && ks == 0 ? 0u : 1u);
-                        first[acc] = false;
+                            tc::mma_i8_ts(base + AB + (a * NACC + acc) * TN, base + acc * 64 + ks * 8,
+                                          d0 + (uint64_t)((ks * 32 * TN) >> 4), idesc, ks == 0 ? 0u : 1u);
                     }
+                    __syncwarp();
+                }
+            } else {
+                // pass y: plane-major order (consecutive MMAs share the B plane), one release
+                tc::mbar_wait(&aempty[a][0], (uint32_t)((k / ASTG) & 1) ^ 1u);
+                tc::fence_after();
+                if (tc::elect_one()) {
+                    bool first[NACC];
+#pragma unroll
+                    for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
+#pragma unroll
+                    for (int da = 0; da < NPIN; ++da)
+#pragma unroll
+                        for (int b = 0; b < NL; ++b) {
+                            const int acc = da + b - lo_pair(NPIN, NL);
+                            if (acc < 0 || acc >= NACC) continue;
+#pragma unroll
+                            for (int ks = 0; ks < KXY / 32; ++ks)
+                                tc::mma_i8_ts(base + AB + (a * NACC + acc) * TN, base + b * 64 + ks * 8,
+                                              d0 + (uint64_t)((da * PB + ks * 32 * TN) >> 4), idesc,
+                                              first[acc] && ks == 0 ? 0u : 1u);
+                            first[acc] = false;
+                        }
+                }
+                __syncwarp();
+            }
+            if (tc::elect_one()) {
                 tc::mma_commit(&empty[s]);  // stage s free once these MMAs have read it
                 tc::mma_commit(&afull[a]);  // accumulator set a complete
             }
@@ -424,11 +448,19 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
                 } else {
                     tc::tmem_ld4(la + AB + (a * NACC + acc) * TN + h, *reinterpret_cast<uint32_t(*)[4]>(&v[acc][0]));
                 }
+                if constexpr (NPIN == 1) {  // pass x: release accumulator by accumulator
+                    tc::tmem_ld_wait();
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&aempty[a][acc]);  // MMA(k + ASTG) may overwrite accumulator acc
+                }
             }
-            tc::tmem_ld_wait();
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&aempty[a]);  // MMA(k + ASTG) may overwrite set a
+            if constexpr (NPIN != 1) {  // pass y (measured: 192 us vs 199 released one by one)
+                tc::tmem_ld_wait();
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&aempty[a][0]);
+            }
             uint8_t *ob = sout + (int)(k & 1) * OBUF;
             uint32_t pw[NPO][VB / 4];  // the thread's VB output bytes of every plane
 #pragma unroll
