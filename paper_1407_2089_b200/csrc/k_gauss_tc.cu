@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
                                                           int r) {
     static_assert(DB == 1 || NPIN == 1, "u16 input only for the raw pass");
     constexpr int NACC = NPIN == 1 ? NL : 5;
+    constexpr bool PERACC = NPIN == 1 && DB == 1;  // accumulators released one by one (pass x, u8)
     constexpr int AB = 64 * NL;  // TMEM columns of the tap band
     // operand stage: one TMA box per tile, [NPIN planes][KXY rows][TN bytes] in
     // the TMA's TN-byte swizzle = the MMA's MN-major SWIZZLE_32B / 64B
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
             const int s = (int)(k % SSTG), a = (int)(k % ASTG);
             tc::mbar_wait(&ready[s], (uint32_t)((k / SSTG) & 1));
             const uint64_t d0 = tc::smem_desc_sw(tc::smem_u32(sm + s * SB), LBO, SBO, TN);
-            if constexpr (NPIN == 1) {
+            if constexpr (PERACC) {
                 // pass x: the MMAs grouped by accumulator (= weight limb), each group
                 // issued as soon as its accumulator of the previous tile is drained
 #pragma unroll
@@ -448,14 +449,14 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
                 } else {
                     tc::tmem_ld4(la + AB + (a * NACC + acc) * TN + h, *reinterpret_cast<uint32_t(*)[4]>(&v[acc][0]));
                 }
-                if constexpr (NPIN == 1) {  // pass x: release accumulator by accumulator
+                if constexpr (PERACC) {  // pass x: release accumulator by accumulator
                     tc::tmem_ld_wait();
                     tc::fence_before();
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive(&aempty[a][acc]);  // MMA(k + ASTG) may overwrite accumulator acc
                 }
             }
-            if constexpr (NPIN != 1) {  // pass y (measured: 192 us vs 199 released one by one)
+            if constexpr (!PERACC) {  // pass y (measured: 192 us vs 199 released one by one), u16 pass x
                 tc::tmem_ld_wait();
                 tc::fence_before();
                 __syncwarp();
