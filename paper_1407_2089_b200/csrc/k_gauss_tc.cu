@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
     static_assert(DB == 1 || NPIN == 1, "u16 input only for the raw pass");
     constexpr int NACC = NPIN == 1 ? NL : 5;
     constexpr bool PERACC = NPIN == 1 && DB == 1;  // accumulators released one by one (pass x, u8)
+    constexpr int AG = 3;                           // pass y: accumulators [0, AG) released first
     constexpr int AB = 64 * NL;  // TMEM columns of the tap band
     // operand stage: one TMA box per tile, [NPIN planes][KXY rows][TN bytes] in
     // the TMA's TN-byte swizzle = the MMA's MN-major SWIZZLE_32B / 64B
@@ -399,11 +400,13 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
                     __syncwarp();
                 }
             } else {
-                // pass y: plane-major order (consecutive MMAs share the B plane), one release
+                // pass y: plane-major order (consecutive MMAs share the B plane); the
+                // accumulators are released in two groups ([0, AG) and [AG, NACC)):
+                // the pairs into the first group come first in this order
                 tc::mbar_wait(&aempty[a][0], (uint32_t)((k / ASTG) & 1) ^ 1u);
                 tc::fence_after();
                 if (tc::elect_one()) {
-                    bool first[NACC];
+                    bool first[NACC], g1 = NPIN == 1;
 #pragma unroll
                     for (int s2 = 0; s2 < NACC; ++s2) first[s2] = true;
 #pragma unroll
@@ -412,6 +415,11 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
                         for (int b = 0; b < NL; ++b) {
                             const int acc = da + b - lo_pair(NPIN, NL);
                             if (acc < 0 || acc >= NACC) continue;
+                            if (acc >= AG && !g1) {
+                                tc::mbar_wait(&aempty[a][1], (uint32_t)((k / ASTG) & 1) ^ 1u);
+                                tc::fence_after();
+                                g1 = true;
+                            }
 #pragma unroll
                             for (int ks = 0; ks < KXY / 32; ++ks)
                                 tc::mma_i8_ts(base + AB + (a * NACC + acc) * TN, base + b * 64 + ks * 8,
@@ -455,12 +463,20 @@ __global__ void __launch_bounds__(WSX_NT, 1) tc_pass_xy_ws(const __grid_constant
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive(&aempty[a][acc]);  // MMA(k + ASTG) may overwrite accumulator acc
                 }
+                if constexpr (!PERACC && NPIN > 1) {  // pass y: first group released after its loads
+                    if (acc == AG - 1) {
+                        tc::tmem_ld_wait();
+                        tc::fence_before();
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive(&aempty[a][0]);
+                    }
+                }
             }
-            if constexpr (!PERACC) {  // pass y (measured: 192 us vs 199 released one by one), u16 pass x
+            if constexpr (!PERACC) {  // pass y: the second group; u16 pass x: the whole set (aempty[a][0])
                 tc::tmem_ld_wait();
                 tc::fence_before();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&aempty[a][0]);
+                if (lane == 0) tc::mbar_arrive(&aempty[a][NPIN > 1 ? 1 : 0]);
             }
             uint8_t *ob = sout + (int)(k & 1) * OBUF;
             uint32_t pw[NPO][VB / 4];  // the thread's VB output bytes of every plane
