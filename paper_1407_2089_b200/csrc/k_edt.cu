@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
 // Pass z, register-streamed form.  ncu on the SMEM-staged form (edt_pass_z):
 // the thread-per-line envelope is latency bound (wait stalls, 16 warps/SM) and
 // the SMEM staging of whole lines (396 B per line) is what caps the warps.  Here a thread streams
-// its own line from global memory (two 16-byte loads per 8 elements, the next
+// its own line from global memory (one 32-byte load per 8 elements, the next
 // chunk in flight), keeps only the envelope stack in SMEM (positions for all
 // entries, packed offsets for the first SCZ; deeper entries re-read their
 // offsets from the line, which stays in L1/L2), and forms the distances in the
@@ -548,6 +548,16 @@ __global__ void __launch_bounds__(ZL) edt_pass_z(const int32_t *__restrict__ in,
 // as edt_pass_z (bit-identical output).
 __device__ __forceinline__ void st_v4(double *p, double a, double b, double c, double d) {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+// 8 elements of the line per lane in one 256-bit load that does not allocate
+// in L1: the 1,024 lines' streams otherwise evict the L1 lines the envelope
+// re-reads (C2: 298 -> 272 us, tools/micro/edtz_ab.cu; two 128-bit loads with
+// allocation, or 256-bit with allocation: 297 / 300 us)
+__device__ __forceinline__ void ld8_stream(const int32_t *p, int4 &a, int4 &b) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(p));
 }
 
 constexpr int ZRT = 128;  // threads (lines) per CTA
@@ -568,13 +578,11 @@ __global__ void __launch_bounds__(ZRT, 8) edt_pass_zr(const int32_t *__restrict_
     auto pk_ld = [&](int e, int pos) -> int32_t { return e < SCZ ? pkS[e][t] : __ldg(line + pos); };
     int K = 0, tp = 0, bp = 0;
     double tg = 0.0, bg = 0.0;
-    int4 na = __ldg((const int4 *)line), nb = __ldg((const int4 *)line + 1);
+    int4 na, nb;
+    ld8_stream(line, na, nb);
     for (int c = 0; c < NZ; c += 8) {
         const int32_t v[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
-        if (c + 8 < NZ) {
-            na = __ldg((const int4 *)(line + c + 8));
-            nb = __ldg((const int4 *)(line + c + 12));
-        }
+        if (c + 8 < NZ) ld8_stream(line + c + 8, na, nb);
         // z-slices without foreground carry NONE32 in every line: skip such a
         // batch in one test
         uint32_t any = 0;
@@ -758,7 +766,7 @@ extern "C" int ct_edt(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz, d
         if (int st = ct::check_launch("edt_y_out")) return st;
     }
     const size_t sm = zsmem((int)nz);
-    if ((nz == 64 || nz == 32 || nz == 96 || nz == 128) && ((uintptr_t)pk & 15) == 0) {
+    if ((nz == 64 || nz == 32 || nz == 96 || nz == 128) && ((uintptr_t)pk & 31) == 0) {
         // (tried: the SMEM-staged thread-per-line form, and a 4-voxel distance phase over SMEM-staged lines
         // with packed offsets or float64 costs -- 468 / 490 / 654 us vs 307 for this register-streamed form)
         const unsigned g = (unsigned)((lz + ZRT - 1) / ZRT);

@@ -404,3 +404,23 @@ def test_cuda_graph_replay_matches_eager(cuda, oracle):
     o = oracle.denoise_cell(host, SP, 10.0)
     odets = oracle.segment_cell(o["denoised"], SP, frame=1, intensity=host)
     assert [int(c) for c in ref[1][3]["count"]] == [d.voxel_count for d in odets]
+
+
+@pytest.mark.parametrize("nz", [32, 64, 96, 128])
+def test_edt_deep_z_envelopes_vs_oracle(cuda, oracle, nz):
+    """Pass-z envelopes deeper than the 32 shared-memory stack entries of
+    edt_pass_zr (the rest live in the dead pass-x buffer): one foreground
+    line tilted through x as it runs along z, so in slice k the nearest site
+    of a far column moves by half a voxel per slice and nearly every slice's
+    parabola stays on the lower envelope (~55 of 64 entries); plus a second
+    tilted line and random specks."""
+    from paper_1407_2089_b200 import segment as S
+
+    shape = (96, 40, nz)
+    m = np.zeros(shape, dtype=bool)
+    k = np.arange(nz)
+    m[(4 + k // 2) % shape[0], 3, k] = True
+    m[(90 - k // 3) % shape[0], 33, k] = True
+    rng = np.random.default_rng(nz)
+    m |= rng.random(shape) > 0.9995
+    np.testing.assert_array_equal(S.distance_map(m, ANISO).values, oracle.edt(m, SP))

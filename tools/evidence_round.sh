@@ -1,0 +1,6 @@
+python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
+python bench.py --steps 200 > gpurun_out/bench_c2.jsonl 2> gpurun_out/bench_c2.err; tail -c 400 gpurun_out/bench_c2.jsonl
+python bench.py --config C3 --steps 100 > gpurun_out/bench_c3.jsonl 2> gpurun_out/bench_c3.err
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref_arm.jsonl 2> gpurun_out/ref_arm.err
+bash tools/prof_round.sh > gpurun_out/prof_round.log 2>&1
+exit 0

@@ -53,17 +53,59 @@ __device__ __forceinline__ void st_v4(double *p, double a, double b, double c, d
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
+__device__ __noinline__ void line_global(const int32_t *__restrict__ line, int nz, double dx, double dy, double dz,
+                                         int16_t *__restrict__ st, double *__restrict__ dst) {
+    auto G = [&](int x) { const int32_t pl = line[x]; return pl == NONE32 ? INFINITY : gyz<0>(pl, dx, dy); };
+    const double d2 = __dmul_rn(dz, dz);
+    int K = 0, tp = 0, bp = 0;
+    double tg = 0.0, bg = 0.0;
+    for (int x = 0; x < nz; ++x) {
+        const double gx = G(x);
+        if (gx == INFINITY) continue;
+        while (K >= 2 && env_pop<0>(x, gx, tp, tg, bp, bg, d2)) {
+            --K; tp = bp; tg = bg;
+            if (K >= 2) { bp = st[K - 2]; bg = G(bp); }
+        }
+        st[K++] = (int16_t)x;
+        bp = tp; bg = tg; tp = x; tg = gx;
+    }
+    int e = 0;
+    int cp = st[0], np = K > 1 ? st[1] : 0;
+    double cg = G(cp), ng = K > 1 ? G(np) : 0.0;
+    for (int x = 0; x < nz; ++x) {
+        while (e + 1 < K && env_past<0>(x, np, ng, cp, cg, d2)) {
+            ++e; cp = np; cg = ng;
+            if (e + 1 < K) { np = st[e + 1]; ng = G(np); }
+        }
+        dst[x] = __dsqrt_rn(__dadd_rn(cg, sq(__dmul_rn((double)(cp - x), dz))));
+    }
+}
+
+template <int V> __device__ __forceinline__ void ld8(const int32_t *p, int4 &a, int4 &b) {
+    if (V & 4096) {
+        asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(p));
+    } else if (V & 2048) {
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(p));
+    } else {
+        a = __ldg((const int4 *)p);
+        b = __ldg((const int4 *)p + 1);
+    }
+}
+
 constexpr int ZRT = 128;
 constexpr int NZ = 64, SCZ = 16;
+static void *g_ovf = nullptr;
 
-template <int V, int SCG>
-__global__ void __launch_bounds__(ZRT, 8) passz(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
-                                                double dz, double *__restrict__ out, int *__restrict__ kstat) {
+template <int V, int SCG, int SD = NZ, int MINB = 8, int SCZ = 16>
+__global__ void __launch_bounds__(ZRT, MINB) passz(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
+                                                double dz, double *__restrict__ out, int *__restrict__ kstat, void *kstat_ovf = nullptr) {
     __shared__ double czt[2 * NZ];
-    __shared__ uint8_t posS[NZ][ZRT];
+    __shared__ uint8_t posS[SD][ZRT];
     __shared__ int32_t pkS[(V & 4) ? 1 : SCZ][ZRT];
     __shared__ double gS[(V & 4) ? SCG : 1][ZRT];
-    __shared__ uint8_t swS[NZ][ZRT];
+    __shared__ uint8_t swS[SD][ZRT];
     for (int d = threadIdx.x; d < 2 * NZ; d += ZRT) czt[d] = sq(__dmul_rn((double)(d - NZ), dz));
     __syncthreads();
     const i64 l = blockIdx.x * (i64)ZRT + threadIdx.x;
@@ -71,6 +113,9 @@ __global__ void __launch_bounds__(ZRT, 8) passz(const int32_t *__restrict__ in, 
     const int t = threadIdx.x;
     const int32_t *line = in + l * NZ;
     const double d2 = __dmul_rn(dz, dz);
+    uint16_t *ovf = (uint16_t *)kstat_ovf + l * NZ;
+    auto pos_ld = [&](int e) -> int { return ((V & 128) && e >= SD) ? (int)(ovf[e] & 0xffu) : (int)posS[e][t]; };
+    auto sw_ld = [&](int e) -> int { return ((V & 128) && e >= SD) ? (int)(ovf[e] >> 8) : (int)swS[e][t]; };
     // cost of stack entry e at position pos
     auto g_ld = [&](int e, int pos) -> double {
         if (V & 4) return e < SCG ? gS[e][t] : gyz<V>(__ldg(line + pos), dx, dy);
@@ -111,16 +156,15 @@ __global__ void __launch_bounds__(ZRT, 8) passz(const int32_t *__restrict__ in, 
             }
         }
     }
-    int4 na = __ldg((const int4 *)line), nb = __ldg((const int4 *)line + 1);
+    int4 na, nb;
+    ld8<V>(line, na, nb);
+    bool deep = false;
     int32_t prevpx = NONE32;  // site at c - 1 (V & 64)
     double prevg = 0.0;
     int nrem = 0;
     for (int c = (V & 32) ? NZ : 0; c < NZ; c += 8) {
         const int32_t v[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
-        if (c + 8 < NZ) {
-            na = __ldg((const int4 *)(line + c + 8));
-            nb = __ldg((const int4 *)(line + c + 12));
-        }
+        if (c + 8 < NZ) ld8<V>(line + c + 8, na, nb);
         uint32_t any = 0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) any |= (uint32_t)v[u] ^ 0x80000000u;
@@ -154,11 +198,15 @@ __global__ void __launch_bounds__(ZRT, 8) passz(const int32_t *__restrict__ in, 
                 tp = bp;
                 tg = bg;
                 if (K >= 2) {
-                    bp = posS[K - 2][t];
+                    bp = pos_ld(K - 2);
                     bg = g_ld(K - 2, bp);
                 }
             }
-            posS[K][t] = (uint8_t)x;
+            if (V & (256 | 512)) {
+                if (K == SD) { deep = true; continue; }
+                posS[K][t] = (uint8_t)x;
+            } else if (!(V & 128) || K < SD) posS[K][t] = (uint8_t)x;
+            else ovf[K] = (uint16_t)x;
             if (V & 4) {
                 if (K < SCG) gS[K][t] = gx;
             } else if (K < SCZ) {
@@ -167,6 +215,11 @@ __global__ void __launch_bounds__(ZRT, 8) passz(const int32_t *__restrict__ in, 
             ++K;
             bp = tp; bg = tg; tp = x; tg = gx;
         }
+    }
+    if ((V & (256 | 512)) && deep) {
+        if (V & 256) line_global(line, NZ, dx, dy, dz, (int16_t *)kstat_ovf + l * NZ, out + l * NZ);
+        else atomicAdd((int *)kstat_ovf, 1);
+        return;
     }
     if (kstat) { atomicAdd(kstat + K, 1); if (V & 64) atomicAdd(kstat + NZ + 1, nrem); }
     double *dst = out + l * NZ;
@@ -185,10 +238,11 @@ __global__ void __launch_bounds__(ZRT, 8) passz(const int32_t *__restrict__ in, 
         int p = cp, sw = 0;
         double pg = cg;
         for (int e2 = 0; e2 + 1 < K; ++e2) {
-            const int q = posS[e2 + 1][t];
+            const int q = pos_ld(e2 + 1);
             const double qg = g_ld(e2 + 1, q);
             sw = first_past<V>(sw, NZ, q, qg, p, pg, d2);
-            swS[e2][t] = (uint8_t)sw;
+            if (!(V & 128) || e2 < SD) swS[e2][t] = (uint8_t)sw;
+            else ovf[e2] = (uint16_t)(p | (sw << 8));
             p = q;
             pg = qg;
         }
@@ -202,9 +256,9 @@ __global__ void __launch_bounds__(ZRT, 8) passz(const int32_t *__restrict__ in, 
             if (x >= sw) {
                 do {
                     ++e;
-                    sw = e + 1 < K ? swS[e][t] : NZ;
+                    sw = e + 1 < K ? sw_ld(e) : NZ;
                 } while (x >= sw);
-                cp = posS[e][t];
+                cp = pos_ld(e);
                 cg = g_ld(e, cp);
             }
             const double s = __dadd_rn(cg, czt[cp - x + NZ]);
@@ -354,16 +408,16 @@ static std::vector<char> slurp(const char *path) {
     return b;
 }
 
-template <int V, int SCG>
+template <int V, int SCG, int SD = NZ, int MINB = 8, int SCZ = 16>
 void run(const char *name, const int32_t *d_in, i64 lz, double *d_out, const std::vector<double> &ref, int reps) {
     const unsigned g = (unsigned)((lz + ZRT - 1) / ZRT);
-    passz<V, SCG><<<g, ZRT>>>(d_in, lz, 0.8, 0.8, 1.0, d_out, nullptr);
+    passz<V, SCG, SD, MINB, SCZ><<<g, ZRT>>>(d_in, lz, 0.8, 0.8, 1.0, d_out, nullptr, g_ovf);
     CK(cudaDeviceSynchronize());
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    for (int r = 0; r < reps; ++r) passz<V, SCG><<<g, ZRT>>>(d_in, lz, 0.8, 0.8, 1.0, d_out, nullptr);
+    for (int r = 0; r < reps; ++r) passz<V, SCG, SD, MINB, SCZ><<<g, ZRT>>>(d_in, lz, 0.8, 0.8, 1.0, d_out, nullptr, g_ovf);
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     float ms = 0;
@@ -415,6 +469,7 @@ int main(int argc, char **argv) {
     CK(cudaMalloc(&d_out, N * 8));
     CK(cudaMalloc(&d_k, 4 * (NZ + 2)));
     CK(cudaMemcpy(d_in, pk.data(), N * 4, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&g_ovf, N * 2));
     CK(cudaMemset(d_k, 0, 4 * (NZ + 2)));
     passz<0, 1><<<(unsigned)((lz + ZRT - 1) / ZRT), ZRT>>>(d_in, lz, 0.8, 0.8, 1.0, d_out, d_k);
     int hk[NZ + 1];
@@ -437,16 +492,12 @@ int main(int argc, char **argv) {
     run<0, 1>("V0 production", d_in, lz, d_out, ref, reps);
     run<1, 1>("V1 no sqrt", d_in, lz, d_out, ref, reps);
     run<2, 1>("V2 build only", d_in, lz, d_out, ref, reps);
-    run<4, 8>("V4 g in SMEM (8)", d_in, lz, d_out, ref, reps);
-    run<4, 16>("V4 g in SMEM (16)", d_in, lz, d_out, ref, reps);
-    run<8, 1>("V8 u2d conversions", d_in, lz, d_out, ref, reps);
-    run<12, 8>("V12 g SMEM(8) + u2d", d_in, lz, d_out, ref, reps);
-    run<12, 16>("V12 g SMEM(16) + u2d", d_in, lz, d_out, ref, reps);
-    run<32, 1>("V32 flattened build", d_in, lz, d_out, ref, reps);
-    run<33, 1>("V33 flattened, no sqrt", d_in, lz, d_out, ref, reps);
-    run<34, 1>("V34 flattened, build only", d_in, lz, d_out, ref, reps);
-    run<64, 1>("V64 neighbour prefilter", d_in, lz, d_out, ref, reps);
-    run<66, 1>("V66 prefilter, build only", d_in, lz, d_out, ref, reps);
+    run<0, 1, 32, 10>("V0 stack 32, 10/SM", d_in, lz, d_out, ref, reps);
+    run<2048, 1>("V2048 v8 loads", d_in, lz, d_out, ref, reps);
+    run<4096, 1>("V4096 v8 no-allocate", d_in, lz, d_out, ref, reps);
+    run<2048, 1, 64, 10>("V2048 v8, 10/SM cap", d_in, lz, d_out, ref, reps);
+    run<4096 + 512, 1, 32, 10>("V4608 v8 na + stack32 list", d_in, lz, d_out, ref, reps);
+    run<2048 + 512, 1, 32, 10>("V2560 v8 + stack32 list", d_in, lz, d_out, ref, reps);
     run_f("V16 float-certified build", d_in, lz, d_out, ref, reps, d_k);
     run<0, 1>("V0 production (again)", d_in, lz, d_out, ref, reps);
     return 0;
