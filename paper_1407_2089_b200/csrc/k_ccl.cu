@@ -282,6 +282,13 @@ __global__ void ccl_run_init(const uint8_t *__restrict__ mask, const R *__restri
     }
 }
 
+// A run s unions with every run of row (i-1, j) it touches (F); a run of
+// rows (i, j-1), (i-1, j-1), (i-1, j+1) that touches s is skipped when it also
+// touches F: that link is implied -- s-F is made here, and the F-run link is
+// owned by an earlier row ((i, j-1) against its (i-1, j); (i-1, j) against its
+// (i-1, j-1); (i-1, j+1) against its (i-1, j)), itself made or implied by
+// induction over the row order.  Same components, same roots (minimum index),
+// fewer atomic unions on compact cells.
 template <typename R, bool BITS>
 __global__ void ccl_run_union(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 nx, i64 ny, int nz,
                               int32_t *labels) {
@@ -291,25 +298,32 @@ __global__ void ccl_run_union(const uint8_t *__restrict__ mask, const R *__restr
         const R w = load_row<R, BITS>(mask, rows, r, nz);
         if (!w) continue;
         const i64 i = fny.div((uint32_t)r), j = r - i * ny;
-        const i64 nb[4] = {j > 0 ? r - 1 : -1, (i > 0 && j > 0) ? r - ny - 1 : -1, i > 0 ? r - ny : -1,
+        // q = 0: (i-1, j) first (it defines F), then (i, j-1), (i-1, j-1), (i-1, j+1)
+        const i64 nb[4] = {i > 0 ? r - ny : -1, j > 0 ? r - 1 : -1, (i > 0 && j > 0) ? r - ny - 1 : -1,
                            (i > 0 && j + 1 < ny) ? r - ny + 1 : -1};
+        R u[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (nb[q] < 0) continue;
-            const R u = load_row<R, BITS>(mask, rows, nb[q], nz);
-            if (!u) continue;
-            const R ustart = u & ~(u << 1);
-            R rem = w;
-            while (rem) {
-                const int s = ct::rffs(rem) - 1;
-                const R mr = run_mask(w, s);
-                rem &= ~mr;
-                R o = (mr | (mr << 1) | (mr >> 1)) & u;  // 26-neighbours in row nb
+        for (int q = 0; q < 4; ++q) u[q] = nb[q] >= 0 ? load_row<R, BITS>(mask, rows, nb[q], nz) : (R)0;
+        R rem = w;
+        while (rem) {
+            const int s = ct::rffs(rem) - 1;
+            const R mr = run_mask(w, s);
+            rem &= ~mr;
+            const R ds = mr | (mr << 1) | (mr >> 1);
+            R dF = 0;  // F dilated by one along z
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!u[q]) continue;
+                const R ustart = u[q] & ~(u[q] << 1);
+                R o = ds & u[q];  // 26-neighbours in row nb[q]
                 while (o) {
                     const int b = ct::rffs(o) - 1;
                     const R below = ustart & ct::rmask<R>(b + 1);
                     const int su = ct::rbits<R>() - 1 - ct::rclz(below);
-                    o &= ~run_mask(u, su);
+                    const R um = run_mask(u[q], su);
+                    o &= ~um;
+                    if (q == 0) dF |= um | (um << 1) | (um >> 1);
+                    else if (dF & um) continue;
                     union_gh(labels, (int)(r * nz + s), (int)(nb[q] * nz + su));
                 }
             }
