@@ -753,6 +753,7 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
     double *cs = csm[threadIdx.x >> 5];
     const i64 nk = counters[CT_CNT_KEPT];
     const i64 w0 = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
+    const ct::FastDiv fyz((uint32_t)(ny * nz)), fz((uint32_t)nz);  // voxel index -> (i, j, k); N < 2^31
     for (i64 r = w0; r < nk; r += nw) {
         const int lo0 = table[r].bbox_lo[0], lo1 = table[r].bbox_lo[1], lo2 = table[r].bbox_lo[2];
         const unsigned bi = table[r].bbox_hi[0] - lo0 + 1, bj = table[r].bbox_hi[1] - lo1 + 1,
@@ -793,31 +794,43 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
                 CT_DCHECK(!hit || written + __popc(m) <= table[r].count);  // a cell's list never outgrows its count
                 if (hit) voxels[off + written + __popc(m & ((1u << lane) - 1))] = pv[u];
-                // hits' coordinates compacted in list order into the warp's SMEM
-                // slots, then lane 0 continues the row-sequential sum
-                const int nh = __popc(m);
-                if (hit) {
-                    const unsigned q = q00 + 32 * u + lane;
-                    const unsigned a = fjk.div(q), rem = q - a * bjk, b = fk.div(rem), c = rem - b * bk;
-                    double *slot = cs + 3 * __popc(m & ((1u << lane) - 1));
-                    slot[0] = __dmul_rn((double)(lo0 + (int)a), dx);
-                    slot[1] = __dmul_rn((double)(lo1 + (int)b), dy);
-                    slot[2] = __dmul_rn((double)(lo2 + (int)c), dz);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    int h0 = 0;
-                    if (written == 0 && nh) { sx = cs[0]; sy = cs[1]; sz = cs[2]; h0 = 1; }
-#pragma unroll 4
-                    for (int h = h0; h < nh; ++h) {
+                written += __popc(m);
+            }
+        }
+        // centroid: the row-sequential float64 sum numpy's mean(axis=0) performs,
+        // over the list just written (C order), 32 voxels per step: the lanes form
+        // the coordinates, lane 0 runs the three addition chains from SMEM (the
+        // chains inside the walk, per 32 candidates with two warp barriers,
+        // were ~half of this kernel's instructions and stalls)
+        __syncwarp();  // the warp's list writes are visible to its lanes
+        for (i64 c0 = 0; c0 < written; c0 += 32) {
+            const i64 e = c0 + lane;
+            if (e < written) {
+                const uint32_t p = (uint32_t)voxels[off + e];
+                const uint32_t a = fyz.div(p), rem = p - a * (uint32_t)(ny * nz), b = fz.div(rem), c = rem - b * (uint32_t)nz;
+                cs[3 * lane] = __dmul_rn((double)a, dx);
+                cs[3 * lane + 1] = __dmul_rn((double)b, dy);
+                cs[3 * lane + 2] = __dmul_rn((double)c, dz);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const int n = (int)min((i64)32, written - c0);
+                if (n == 32) {
+#pragma unroll
+                    for (int h = 0; h < 32; ++h) {
+                        sx = __dadd_rn(sx, cs[3 * h]);
+                        sy = __dadd_rn(sy, cs[3 * h + 1]);
+                        sz = __dadd_rn(sz, cs[3 * h + 2]);
+                    }
+                } else {
+                    for (int h = 0; h < n; ++h) {
                         sx = __dadd_rn(sx, cs[3 * h]);
                         sy = __dadd_rn(sy, cs[3 * h + 1]);
                         sz = __dadd_rn(sz, cs[3 * h + 2]);
                     }
                 }
-                __syncwarp();
-                written += nh;
             }
+            __syncwarp();
         }
         if (lane == 0) {
             const double n = (double)table[r].count;
