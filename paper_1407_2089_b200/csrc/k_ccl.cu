@@ -230,7 +230,9 @@ __global__ void ccl_flatten(int32_t *labels, const int32_t *__restrict__ fg, con
 //   ccl_run_init  : labels[run start] = run start
 //   ccl_run_union : each run unions with the runs of the 4 backward rows
 //                   (i, j-1), (i-1, j-1..j+1) that touch it in z +- 1
-//   ccl_run_emit  : labels of every run voxel = find(run start); fg list
+//   ccl_run_roots : labels[run start] = find(run start) (compression to the root:
+//                   concurrent finds only ever see ancestors)
+//   ccl_run_emit  : labels of the run's other voxels = labels[run start]; fg list
 // ---------------------------------------------------------------------------
 template <typename R>
 __device__ __forceinline__ R pack_row(const uint8_t *__restrict__ row, int nz) {
@@ -361,19 +363,17 @@ __global__ void ccl_run_emit(const uint8_t *__restrict__ mask, const R *__restri
             const int s = ct::rffs(rem) - 1;
             const R mr = run_mask(w, s);
             rem &= ~mr;
-            const int32_t root = (int32_t)find_g(labels, (int)(r * nz + s));
+            const int32_t root = labels[r * nz + s];  // ccl_run_roots ran first: the start holds its root
             for (R m = mr; m; m &= m - 1) {
                 CT_DCHECK(base + e < nrows * (i64)nz);
                 fg[base + e++] = (int32_t)(r * nz + ct::rffs(m) - 1);
             }
-            // run starts hold the union-find links until every thread's find is done:
-            // write the run's other voxels now, the start in a second sweep
             for (R m = mr & (mr - 1); m; m &= m - 1) labels[r * nz + ct::rffs(m) - 1] = root;
         }
     }
 }
 
-// final sweep: run starts take their root (after all finds of ccl_run_emit)
+// run starts take their root (before ccl_run_emit, which copies it to the run)
 template <typename R, bool BITS>
 __global__ void ccl_run_roots(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 nrows, int nz,
                               int32_t *labels) {
@@ -865,8 +865,8 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
             using R = decltype(tag);
             ccl_run_init<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels);
             ccl_run_union<R, false><<<g, 256, 0, s>>>(mask, nullptr, nx, ny, (int)nz, labels);
-            ccl_run_emit<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels, fg_list, counters);
             ccl_run_roots<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels);
+            ccl_run_emit<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels, fg_list, counters);
             return ct::check_launch("ccl_run");
         };
         return nz <= 64 ? run((unsigned long long)0) : run((ct::u128)0);
@@ -919,8 +919,8 @@ extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t n
         const R *rw = (const R *)rows;
         ccl_run_init<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels);
         ccl_run_union<R, true><<<g, 256, 0, s>>>(nullptr, rw, nx, ny, (int)nz, labels);
-        ccl_run_emit<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels, fg_list, counters);
         ccl_run_roots<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels);
+        ccl_run_emit<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels, fg_list, counters);
         return ct::check_launch("ccl_run_rows");
     };
     return nz <= 64 ? run((unsigned long long)0) : run((ct::u128)0);
