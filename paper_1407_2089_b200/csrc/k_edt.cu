@@ -200,7 +200,10 @@ constexpr int XG = 8;
 __global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4(const uint8_t *__restrict__ mask, i64 nlines, int nx,
                                                            int16_t *__restrict__ di) {
     __shared__ int segL[32][4 * XG + 1], segF[32][4 * XG + 1];
+    __shared__ uint32_t segM[4 * XG];  // per line: bit y = segment y holds foreground
     const int c = threadIdx.x, y = threadIdx.y;  // c: 4-line group, y: segment
+    if (y == 0) for (int q = 0; q < 4; ++q) segM[4 * c + q] = 0u;
+    __syncthreads();
     const i64 l0 = blockIdx.x * (4ll * XG) + 4 * c;
     const bool valid = l0 < nlines;             // nlines % 4 == 0
     const i64 S = nlines;
@@ -220,18 +223,20 @@ __global__ void __launch_bounds__(XG * 32) edt_pass_x_seg4(const uint8_t *__rest
     for (int q = 0; q < 4; ++q) {
         segL[y][4 * c + q] = bits[q] ? row0 + 31 - __clz(bits[q]) : -1;
         segF[y][4 * c + q] = bits[q] ? row0 + __ffs(bits[q]) - 1 : -1;
+        if (bits[q]) atomicOr(&segM[4 * c + q], 1u << y);
     }
     __syncthreads();
     if (!valid) return;
+    // nearest segments with foreground left / right of this one from the
+    // line's segment mask (a scan of the other 31 segments per line was most
+    // of this kernel's instructions on sparse masks)
     int lc[4], rc[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        lc[q] = -1;
-        rc[q] = -1;
-        for (int yy = y - 1; yy >= 0; --yy)
-            if (segL[yy][4 * c + q] >= 0) { lc[q] = segL[yy][4 * c + q]; break; }
-        for (int yy = y + 1; yy < 32; ++yy)
-            if (segF[yy][4 * c + q] >= 0) { rc[q] = segF[yy][4 * c + q]; break; }
+        const uint32_t sm = segM[4 * c + q];
+        const uint32_t below = sm & ((1u << y) - 1u), above = sm & ~((2u << y) - 1u);
+        lc[q] = below ? segL[31 - __clz(below)][4 * c + q] : -1;
+        rc[q] = above ? segF[__ffs(above) - 1][4 * c + q] : -1;
     }
     // segments without foreground in their own rows (most of a sparse mask):
     // the nearest foreground is lc or rc for every row, no bit scans
