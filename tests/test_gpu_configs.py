@@ -424,3 +424,66 @@ def test_edt_deep_z_envelopes_vs_oracle(cuda, oracle, nz):
     rng = np.random.default_rng(nz)
     m |= rng.random(shape) > 0.9995
     np.testing.assert_array_equal(S.distance_map(m, ANISO).values, oracle.edt(m, SP))
+
+
+@pytest.mark.parametrize("nz", [32, 64, 96, 128])
+def test_ccl_rows_vs_oracle_components(cuda, oracle, nz):
+    """ct_ccl26_rows (the fused path's K5, which skips the links to rows
+    (i, j-1), (i-1, j+-1) that a run of row (i-1, j) already implies) against
+    the oracle's 26-connected components on masks rich in diagonal-only and
+    corner-only contacts: sparse random masks, diagonal voxel chains and
+    random balls.  GPU label = the component's minimum voxel index; each mask
+    is labelled three times (run-to-run identical)."""
+    from paper_1407_2089_b200._lib import call
+
+    rng = np.random.default_rng(1000 + nz)
+    shape = (40, 48, nz)
+    nx, ny, _ = shape
+    masks = [rng.random(shape) > t for t in (0.9, 0.8, 0.7, 0.5)]
+    chains = np.zeros(shape, dtype=bool)
+    for _ in range(60):  # diagonal chains: consecutive voxels touch only at edges / corners
+        p = rng.integers(0, [nx, ny, nz])
+        d = rng.choice([-1, 1], size=3) * rng.integers(0, 2, size=3)
+        d[rng.integers(0, 3)] = rng.choice([-1, 1])
+        for _s in range(rng.integers(3, 30)):
+            if not (0 <= p[0] < nx and 0 <= p[1] < ny and 0 <= p[2] < nz):
+                break
+            chains[tuple(p)] = True
+            p = p + d
+    masks.append(chains)
+    balls = np.zeros(shape, dtype=bool)
+    ii, jj, kk = np.indices(shape)
+    for _ in range(25):
+        c, r = rng.integers(0, [nx, ny, nz]), rng.uniform(1.0, 4.0)
+        balls |= (ii - c[0]) ** 2 + (jj - c[1]) ** 2 + (kk - c[2]) ** 2 <= r * r
+    masks.append(balls | chains)
+    W = 1 if nz <= 64 else 2
+    s = _dev.stream_handle()
+    for m in masks:
+        lab, _n = oracle.label26(m)
+        flat = lab.ravel()
+        fg = flat >= 0 if flat.min() < 0 else m.ravel()
+        # expected: every foreground voxel carries its component's minimum index
+        comp = flat[fg]
+        idx = np.nonzero(fg)[0]
+        mins = {}
+        for c, i in zip(comp.tolist(), idx.tolist()):
+            if c not in mins:
+                mins[c] = i  # idx ascending: the first is the minimum
+        want = np.full(m.size, -1, dtype=np.int32)
+        want[idx] = [mins[c] for c in comp.tolist()]
+        words = np.zeros((nx * ny, W), dtype=np.uint64)
+        mb = m.reshape(nx * ny, nz)
+        for k in range(nz):
+            words[:, k // 64] |= mb[:, k].astype(np.uint64) << np.uint64(k % 64)
+        rows = torch.from_numpy(words.view(np.int64)).cuda()
+        got = []
+        for _rep in range(3):
+            labels = torch.full(shape, -1, dtype=torch.int32, device="cuda")
+            fgl = torch.empty(m.size, dtype=torch.int32, device="cuda")
+            cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
+            call("ct_ccl26_rows", rows.data_ptr(), nx, ny, nz, labels.data_ptr(), fgl.data_ptr(), cnt.data_ptr(), 1, s)
+            torch.cuda.synchronize()
+            got.append(labels.cpu().numpy().ravel())
+        for g in got:
+            np.testing.assert_array_equal(g, want)
