@@ -12,6 +12,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 
 #include <vector>
 
@@ -452,6 +453,118 @@ void run_f(const char *name, const int32_t *d_in, i64 lz, double *d_out, const s
     printf("%-28s %8.1f us  mismatches %zu  exact fallbacks %d\n", name, 1000.0 * ms / reps, bad, nf);
 }
 
+template <int V>
+__global__ void __launch_bounds__(ZRT, 8) passz_h(const int32_t *__restrict__ in, i64 nlines, double dx, double dy,
+                                                  double dz, double *__restrict__ out, int *__restrict__ dummy) {
+    __shared__ double czt[2 * NZ];
+    __shared__ uint8_t posS[NZ][ZRT];
+    __shared__ int32_t pkS[SCZ][ZRT];
+    __shared__ uint8_t swS[NZ][ZRT];
+    for (int d = threadIdx.x; d < 2 * NZ; d += ZRT) czt[d] = sq(__dmul_rn((double)(d - NZ), dz));
+    __syncthreads();
+    const i64 l = blockIdx.x * (i64)ZRT + threadIdx.x;
+    if (l >= nlines) return;
+    const int t = threadIdx.x;
+    const int32_t *line = in + l * NZ;
+    const double d2 = __dmul_rn(dz, dz);
+    auto pk_ld = [&](int e, int pos) -> int32_t { return e < SCZ ? pkS[e][t] : __ldg(line + pos); };
+    auto hof = [&](int32_t pk, int pos) -> double { return __dadd_rn(gyz<0>(pk, dx, dy), czt[pos + NZ]); };
+    int K = 0, tp = 0, bp = 0;
+    double th = 0.0, bh = 0.0;  // h of the top and of the entry below it
+    int4 na, nb;
+    ld8<4096>(line, na, nb);
+    for (int c = 0; c < NZ; c += 8) {
+        const int32_t v[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
+        if (c + 8 < NZ) ld8<4096>(line + c + 8, na, nb);
+        uint32_t any = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) any |= (uint32_t)v[u] ^ 0x80000000u;
+        if (!any) continue;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int32_t px = v[u];
+            if (px == NONE32) continue;
+            const int x = c + u;
+            const double hx = hof(px, x);
+            while (K >= 2 && __dmul_rn(__dadd_rn(hx, -th), (double)(tp - bp)) <=
+                                 __dmul_rn(__dadd_rn(th, -bh), (double)(x - tp))) {
+                --K;
+                tp = bp;
+                th = bh;
+                if (K >= 2) {
+                    bp = posS[K - 2][t];
+                    bh = hof(pk_ld(K - 2, bp), bp);
+                }
+            }
+            posS[K][t] = (uint8_t)x;
+            if (K < SCZ) pkS[K][t] = px;
+            ++K;
+            bp = tp; bh = th; tp = x; th = hx;
+        }
+    }
+    double *dst = out + l * NZ;
+    if (K == 0) {
+        for (int x = 0; x < NZ; x += 4) st_v4(dst + x, INFINITY, INFINITY, INFINITY, INFINITY);
+        return;
+    }
+    int e = 0;
+    int cp = posS[0][t];
+    double cg = gyz<0>(pk_ld(0, cp), dx, dy);
+    {
+        int p = cp, sw = 0;
+        double pg = cg;
+        for (int e2 = 0; e2 + 1 < K; ++e2) {
+            const int q = posS[e2 + 1][t];
+            const double qg = gyz<0>(pk_ld(e2 + 1, q), dx, dy);
+            sw = first_past<0>(sw, NZ, q, qg, p, pg, d2);
+            swS[e2][t] = (uint8_t)sw;
+            p = q;
+            pg = qg;
+        }
+    }
+    int sw = K > 1 ? swS[0][t] : NZ;
+    for (int x0 = 0; x0 < NZ; x0 += 4) {
+        double r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int x = x0 + u;
+            if (x >= sw) {
+                do {
+                    ++e;
+                    sw = e + 1 < K ? swS[e][t] : NZ;
+                } while (x >= sw);
+                cp = posS[e][t];
+                cg = gyz<0>(pk_ld(e, cp), dx, dy);
+            }
+            r[u] = __dsqrt_rn(__dadd_rn(cg, czt[cp - x + NZ]));
+        }
+        st_v4(dst + x0, r[0], r[1], r[2], r[3]);
+    }
+}
+
+void run_h(const char *name, const int32_t *d_in, i64 lz, double *d_out, const std::vector<double> &ref, int reps) {
+    const unsigned g = (unsigned)((lz + ZRT - 1) / ZRT);
+    passz_h<0><<<g, ZRT>>>(d_in, lz, 0.8, 0.8, 1.0, d_out, nullptr);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) passz_h<0><<<g, ZRT>>>(d_in, lz, 0.8, 0.8, 1.0, d_out, nullptr);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    std::vector<double> h(ref.size());
+    CK(cudaMemcpy(h.data(), d_out, h.size() * 8, cudaMemcpyDeviceToHost));
+    size_t bad = 0;
+    double maxd = 0;
+    for (size_t i = 0; i < h.size(); ++i) {
+        if (memcmp(&h[i], &ref[i], 8) != 0) { ++bad; maxd = fmax(maxd, fabs(h[i] - ref[i])); }
+    }
+    printf("%-28s %8.1f us  mismatches %zu (max |d| %.3g)\n", name, 1000.0 * ms / reps, bad, maxd);
+}
+
 int main(int argc, char **argv) {
     const char *dir = argc > 1 ? argv[1] : "/tmp";
     char p[512];
@@ -498,6 +611,8 @@ int main(int argc, char **argv) {
     run<2048, 1, 64, 10>("V2048 v8, 10/SM cap", d_in, lz, d_out, ref, reps);
     run<4096 + 512, 1, 32, 10>("V4608 v8 na + stack32 list", d_in, lz, d_out, ref, reps);
     run<2048 + 512, 1, 32, 10>("V2560 v8 + stack32 list", d_in, lz, d_out, ref, reps);
+    run<4096, 1>("V4096 v8 no-allocate", d_in, lz, d_out, ref, reps);
+    run_h("V-h h-form pop, v8 na", d_in, lz, d_out, ref, reps);
     run_f("V16 float-certified build", d_in, lz, d_out, ref, reps, d_k);
     run<0, 1>("V0 production (again)", d_in, lz, d_out, ref, reps);
     return 0;
