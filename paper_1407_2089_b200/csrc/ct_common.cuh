@@ -40,9 +40,11 @@ int check_launch(const char *what);
 // n / d for a divisor fixed per kernel or per work item (round-up
 // multiply-shift, exact for every 32-bit n): runtime 32-bit divides were ~20%
 // of the instructions of the K1 tile loops and of the K6 bounding-box walk.
+// Construct it on the host (kernel argument) where every thread would build
+// it: the constructor's loop and 64-bit divide were ~8% of close1_bits.
 struct FastDiv {
     uint32_t d, m, s;
-    __device__ explicit FastDiv(uint32_t d_) : d(d_) {
+    __host__ __device__ explicit FastDiv(uint32_t d_) : d(d_) {
         s = 0;
         while ((1ull << s) < d) ++s;
         m = (uint32_t)(((1ull << 32) * ((1ull << s) - d)) / d + 1);

@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(256) pack_rows_u8v(const uint8_t *__restrict__
 
 template <typename R>
 __global__ void __launch_bounds__(256) close1_bits(const R *__restrict__ rows, i64 nx, i64 ny, int nz,
-                                                   uint8_t *__restrict__ out, R *__restrict__ out_rows) {
+                                                   uint8_t *__restrict__ out, R *__restrict__ out_rows,
+                                                   const ct::FastDiv fny) {
     __shared__ __align__(16) uint8_t stage[8][32 * ct::rbits<R>()];
     const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const R kmask = ct::rmask<R>(nz);
@@ -196,8 +197,8 @@ __global__ void __launch_bounds__(256) close1_bits(const R *__restrict__ rows, i
     const i64 nrows = nx * ny;
     const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
     const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-    // rows = nx ny < 2^31 (checked by the caller): 32-bit row coordinates by multiply-shift
-    const ct::FastDiv fny((uint32_t)ny);
+    // rows = nx ny < 2^31 (checked by the caller): 32-bit row coordinates by
+    // multiply-shift (fny built on the host)
     const int inx = (int)nx, iny = (int)ny;
     auto M = [&](int ii, int jj) -> R {
         return (ii >= 0 && ii < inx && jj >= 0 && jj < iny) ? rows[(i64)ii * iny + jj] : (R)0;
@@ -208,6 +209,19 @@ __global__ void __launch_bounds__(256) close1_bits(const R *__restrict__ rows, i
         R e = 0;
         if (r < nrows) {
             const int i = (int)fny.div((uint32_t)r), j = (int)r - i * iny;
+            if (i >= 2 && i < inx - 2 && j >= 2 && j < iny - 2) {
+                // interior (all but a 2-row rim): the 13 rows at fixed offsets, no bounds tests
+                const R *p = rows + r;
+                const R m = p[0], xm1 = p[-iny], xp1 = p[iny], ym1 = p[-1], yp1 = p[1];
+                const R xm2 = p[-2 * iny], xp2 = p[2 * iny], ym2 = p[-2], yp2 = p[2];
+                const R mm = p[-iny - 1], mp = p[-iny + 1], pm = p[iny - 1], pp = p[iny + 1];
+                const R d = (sh(m) | xm1 | xp1 | ym1 | yp1) & kmask;
+                const R dxm = (sh(xm1) | xm2 | m | mm | mp) & kmask, dxp = (sh(xp1) | xp2 | m | pm | pp) & kmask;
+                const R dym = (sh(ym1) | ym2 | m | mm | pm) & kmask, dyp = (sh(yp1) | yp2 | m | mp | pp) & kmask;
+                const R dkm = ((d << 1) | (m & (R)1)) & kmask, dkp = (d >> 1) | (m & top);
+                e = d & dxm & dxp & dym & dyp & dkm & dkp;
+                if (out_rows) out_rows[r] = e;
+            } else {
             // the 13 distinct rows of the two-step cross, each loaded once
             const R m = rows[r];
             const R xm1 = M(i - 1, j), xp1 = M(i + 1, j), ym1 = M(i, j - 1), yp1 = M(i, j + 1);
@@ -223,6 +237,7 @@ __global__ void __launch_bounds__(256) close1_bits(const R *__restrict__ rows, i
             const R dkp = (d >> 1) | (m & top);               // D at k+1; k=nz -> M(k=nz-1)
             e = d & dxm & dxp & dym & dyp & dkm & dkp;
             if (out_rows) out_rows[r] = e;
+            }
         }
         if (out) {
             // bits -> bytes via SMEM, then a coalesced copy of the warp's 32 rows
@@ -276,7 +291,8 @@ int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i6
                                                                                           t_host, rows);
             if (int st = ct::check_launch("pack_rows")) return st;
             close1_bits<R><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(rows, nx, ny, (int)nz, out,
-                                                                                      (R *)rows_out);
+                                                                                      (R *)rows_out,
+                                                                                      ct::FastDiv((uint32_t)ny));
             return ct::check_launch("close1_bits");
         };
         return nz <= 64 ? run((u64)0) : run((ct::u128)0);
