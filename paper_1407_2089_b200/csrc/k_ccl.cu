@@ -293,9 +293,8 @@ __global__ void ccl_run_init(const uint8_t *__restrict__ mask, const R *__restri
 // fewer atomic unions on compact cells.
 template <typename R, bool BITS>
 __global__ void ccl_run_union(const uint8_t *__restrict__ mask, const R *__restrict__ rows, i64 nx, i64 ny, int nz,
-                              int32_t *labels) {
-    const i64 nrows = nx * ny;
-    const ct::FastDiv fny((uint32_t)ny);  // rows < 2^31 (labels are int32 voxel indices)
+                              int32_t *labels, const ct::FastDiv fny) {
+    const i64 nrows = nx * ny;  // rows < 2^31 (labels are int32 voxel indices); fny built on the host
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
         const R w = load_row<R, BITS>(mask, rows, r, nz);
         if (!w) continue;
@@ -442,10 +441,11 @@ __global__ void tab_roots(int32_t *labels, const int32_t *__restrict__ fg, int64
 
 template <typename TI>
 __global__ void tab_stats(const int32_t *__restrict__ labels, i64 ny, i64 nz, const int32_t *__restrict__ fg,
-                          const int64_t *__restrict__ counters, TabWork w, const TI *__restrict__ intensity) {
+                          const int64_t *__restrict__ counters, TabWork w, const TI *__restrict__ intensity,
+                          const ct::FastDiv fnz, const ct::FastDiv fny) {
     const i64 nfg = counters[CT_CNT_FG];
     const bool over = counters[CT_CNT_OVERFLOW] != 0;
-    const ct::FastDiv fnz((uint32_t)nz), fny((uint32_t)ny);  // voxel indices are int32 (N < 2^31)
+    // fnz, fny: built on the host (voxel indices are int32, N < 2^31)
     for (i64 e0 = blockIdx.x * (i64)blockDim.x; e0 < nfg; e0 += (i64)gridDim.x * blockDim.x) {
         const i64 e = e0 + threadIdx.x;
         int c = -1;
@@ -864,7 +864,7 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
         auto run = [&](auto tag) -> int {
             using R = decltype(tag);
             ccl_run_init<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels);
-            ccl_run_union<R, false><<<g, 256, 0, s>>>(mask, nullptr, nx, ny, (int)nz, labels);
+            ccl_run_union<R, false><<<g, 256, 0, s>>>(mask, nullptr, nx, ny, (int)nz, labels, ct::FastDiv((uint32_t)ny));
             ccl_run_roots<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels);
             ccl_run_emit<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels, fg_list, counters);
             return ct::check_launch("ccl_run");
@@ -918,7 +918,7 @@ extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t n
         using R = decltype(tag);
         const R *rw = (const R *)rows;
         ccl_run_init<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels);
-        ccl_run_union<R, true><<<g, 256, 0, s>>>(nullptr, rw, nx, ny, (int)nz, labels);
+        ccl_run_union<R, true><<<g, 256, 0, s>>>(nullptr, rw, nx, ny, (int)nz, labels, ct::FastDiv((uint32_t)ny));
         ccl_run_roots<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels);
         ccl_run_emit<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels, fg_list, counters);
         return ct::check_launch("ccl_run_rows");
@@ -941,13 +941,13 @@ extern "C" int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz
     tab_roots<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters, w, cap);
     if (int st = ct::check_launch("tab_roots")) return st;
     if (!intensity) {
-        tab_stats<uint8_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w, nullptr);
+        tab_stats<uint8_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w, nullptr, ct::FastDiv((uint32_t)nz), ct::FastDiv((uint32_t)ny));
     } else if (intensity_dtype == CT_U8) {
         tab_stats<uint8_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w,
-                                                          (const uint8_t *)intensity);
+                                                          (const uint8_t *)intensity, ct::FastDiv((uint32_t)nz), ct::FastDiv((uint32_t)ny));
     } else if (intensity_dtype == CT_U16) {
         tab_stats<uint16_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w,
-                                                           (const uint16_t *)intensity);
+                                                           (const uint16_t *)intensity, ct::FastDiv((uint32_t)nz), ct::FastDiv((uint32_t)ny));
     } else {
         ct::set_error("intensity must be U8 or U16");
         return CT_ERR_UNSUPPORTED;
