@@ -159,27 +159,37 @@ __global__ void __launch_bounds__(256) pack_rows(const T *__restrict__ in, i64 n
 }
 
 // u8, nz % 16 == 0 (<= 128): one thread per row, 16-byte loads, SIMD byte compares
-template <typename R>
-__global__ void __launch_bounds__(256) pack_rows_u8v(const uint8_t *__restrict__ in, i64 nrows, int nz,
+// NZ > 0: compile-time row length (unrolled, constant shifts); v > t per byte
+// as the carry out of v + (255 - t): an IADD and a majority LOP3 per 4 bytes
+// (__vcmpgtu4 is emulated)
+template <typename R, int NZ = 0>
+__global__ void __launch_bounds__(256) pack_rows_u8v(const uint8_t *__restrict__ in, i64 nrows, int nz_,
                                                      const int64_t *__restrict__ otsu, i64 t_host,
                                                      R *__restrict__ rows) {
+    const int nz = NZ > 0 ? NZ : nz_;
     bool empty;
     const i64 t = threshold_of(otsu, t_host, empty);
     const bool all = !empty && t < 0, none = empty || t >= 255;
-    const uint32_t tb = (uint32_t)(all || none ? 0 : t) * 0x01010101u;
+    const uint32_t kb = (uint32_t)(255 - (all || none ? 0 : t)) * 0x01010101u;  // 255 - t per byte
+    const uint32_t k7 = kb & 0x7f7f7f7fu;
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < nrows; r += (i64)gridDim.x * blockDim.x) {
         R w = 0;
         if (all) w = ct::rmask<R>(nz);
         else if (!none) {
             const uint4 *src = (const uint4 *)(in + r * nz);
-            for (int c = 0; c < nz / 16; ++c) {
+#pragma unroll
+            for (int c = 0; c < (NZ > 0 ? NZ / 16 : 8); ++c) {
+                if (NZ == 0 && c >= nz / 16) break;
                 const uint4 v = __ldg(src + c);
                 const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+                uint32_t piece = 0;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint32_t g = __vcmpgtu4(x[q], tb) & 0x80808080u;  // high bit per byte
-                    w |= (R)(((g >> 7) * 0x10204080u) >> 28) << (16 * c + 4 * q);
+                    const uint32_t cin = (x[q] & 0x7f7f7f7fu) + k7;  // bit 7 of each byte: the carry into bit 7
+                    const uint32_t g = ((x[q] & kb) | ((x[q] | kb) & cin)) & 0x80808080u;  // carry out: v > t
+                    piece |= (((g >> 7) * 0x10204080u) >> 28) << (4 * q);
                 }
+                w |= (R)piece << (16 * c);
             }
         }
         rows[r] = w;
@@ -284,8 +294,12 @@ int threshold_close(const T *in, i64 nx, i64 ny, i64 nz, const int64_t *otsu, i6
             using R = decltype(tag);
             R *rows = (R *)work;
             if (sizeof(T) == 1 && nz % 16 == 0 && ((uintptr_t)in & 15) == 0)
-                pack_rows_u8v<R><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(
-                    (const uint8_t *)in, nrows, (int)nz, otsu, t_host, rows);
+            {
+                auto k = nz == 64 ? pack_rows_u8v<R, 64> : nz == 32 ? pack_rows_u8v<R, 32>
+                         : nz == 128 ? pack_rows_u8v<R, 128> : pack_rows_u8v<R, 0>;
+                k<<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>((const uint8_t *)in, nrows, (int)nz, otsu,
+                                                                          t_host, rows);
+            }
             else
                 pack_rows<T, R><<<ct::grid_for(nrows, 256, CT_NUM_SMS * 16), 256, 0, s>>>(in, nrows, (int)nz, otsu,
                                                                                           t_host, rows);
