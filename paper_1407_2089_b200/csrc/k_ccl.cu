@@ -807,7 +807,8 @@ __global__ void __launch_bounds__(256) tab_voxels_w(const int32_t *__restrict__ 
             const i64 e = c0 + lane;
             if (e < written) {
                 const uint32_t p = (uint32_t)voxels[off + e];
-                const uint32_t a = fyz.div(p), rem = p - a * (uint32_t)(ny * nz), b = fz.div(rem), c = rem - b * (uint32_t)nz;
+                const uint32_t a = fyz.div(p), rem = p - a * (uint32_t)(ny * nz);
+                const uint32_t b = fz.div(rem), c = rem - b * (uint32_t)nz;
                 cs[3 * lane] = __dmul_rn((double)a, dx);
                 cs[3 * lane + 1] = __dmul_rn((double)b, dy);
                 cs[3 * lane + 2] = __dmul_rn((double)c, dz);
@@ -864,7 +865,8 @@ extern "C" int ct_ccl26(const uint8_t *mask, int64_t nx, int64_t ny, int64_t nz,
         auto run = [&](auto tag) -> int {
             using R = decltype(tag);
             ccl_run_init<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels);
-            ccl_run_union<R, false><<<g, 256, 0, s>>>(mask, nullptr, nx, ny, (int)nz, labels, ct::FastDiv((uint32_t)ny));
+            ccl_run_union<R, false><<<g, 256, 0, s>>>(mask, nullptr, nx, ny, (int)nz, labels,
+                                                      ct::FastDiv((uint32_t)ny));
             ccl_run_roots<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels);
             ccl_run_emit<R, false><<<g, 256, 0, s>>>(mask, nullptr, nrows, (int)nz, labels, fg_list, counters);
             return ct::check_launch("ccl_run");
@@ -918,7 +920,8 @@ extern "C" int ct_ccl26_rows(const void *rows, int64_t nx, int64_t ny, int64_t n
         using R = decltype(tag);
         const R *rw = (const R *)rows;
         ccl_run_init<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels);
-        ccl_run_union<R, true><<<g, 256, 0, s>>>(nullptr, rw, nx, ny, (int)nz, labels, ct::FastDiv((uint32_t)ny));
+        ccl_run_union<R, true><<<g, 256, 0, s>>>(nullptr, rw, nx, ny, (int)nz, labels,
+                                                 ct::FastDiv((uint32_t)ny));
         ccl_run_roots<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels);
         ccl_run_emit<R, true><<<g, 256, 0, s>>>(nullptr, rw, nrows, (int)nz, labels, fg_list, counters);
         return ct::check_launch("ccl_run_rows");
@@ -940,14 +943,15 @@ extern "C" int ct_cell_table(int32_t *labels, int64_t nx, int64_t ny, int64_t nz
     const double vv = (dx * dy) * dz;  // VoxelSpacing.voxel_volume_um3 (imaging.py:41-43)
     tab_roots<<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, fg_list, counters, w, cap);
     if (int st = ct::check_launch("tab_roots")) return st;
+    const ct::FastDiv fnz((uint32_t)nz), fny((uint32_t)ny);  // built once here, not per thread
     if (!intensity) {
-        tab_stats<uint8_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w, nullptr, ct::FastDiv((uint32_t)nz), ct::FastDiv((uint32_t)ny));
+        tab_stats<uint8_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w, nullptr, fnz, fny);
     } else if (intensity_dtype == CT_U8) {
         tab_stats<uint8_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w,
-                                                          (const uint8_t *)intensity, ct::FastDiv((uint32_t)nz), ct::FastDiv((uint32_t)ny));
+                                                          (const uint8_t *)intensity, fnz, fny);
     } else if (intensity_dtype == CT_U16) {
         tab_stats<uint16_t><<<CT_NUM_SMS * 4, 256, 0, s>>>(labels, ny, nz, fg_list, counters, w,
-                                                           (const uint16_t *)intensity, ct::FastDiv((uint32_t)nz), ct::FastDiv((uint32_t)ny));
+                                                           (const uint16_t *)intensity, fnz, fny);
     } else {
         ct::set_error("intensity must be U8 or U16");
         return CT_ERR_UNSUPPORTED;
