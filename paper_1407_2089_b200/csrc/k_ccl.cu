@@ -229,7 +229,8 @@ __global__ void ccl_flatten(int32_t *labels, const int32_t *__restrict__ fg, con
 // component root -- the minimum node -- is again its minimum voxel).
 //   ccl_run_init  : labels[run start] = run start
 //   ccl_run_union : each run unions with the runs of the 4 backward rows
-//                   (i, j-1), (i-1, j-1..j+1) that touch it in z +- 1
+//                   (i, j-1), (i-1, j-1..j+1) that touch it in z +- 1, except
+//                   links already implied through row (i-1, j) (see the kernel)
 //   ccl_run_roots : labels[run start] = find(run start) (compression to the root:
 //                   concurrent finds only ever see ancestors)
 //   ccl_run_emit  : labels of the run's other voxels = labels[run start]; fg list
