@@ -509,6 +509,9 @@ __global__ void __launch_bounds__(128) fix_p1s(const Traw *__restrict__ raw, i64
                                                const unsigned long long *__restrict__ fix, long long cap,
                                                long long capF, double *__restrict__ P1) {
     __shared__ Traw buf[4][(2 * FXR + 1) * 32];
+    __shared__ double ws[FXR + 1];  // the taps, read by every lane at every step
+    for (int d = threadIdx.x; d <= rx; d += blockDim.x) ws[d] = w[d];
+    __syncthreads();
     const long long F = min(min((long long)fix[0], cap), capF);
     const i64 RJ = 2 * ry + 1, per = RJ * nz, S = ny * nz, tot = F * per;
     const unsigned lane = threadIdx.x & 31;
@@ -534,9 +537,10 @@ __global__ void __launch_bounds__(128) fix_p1s(const Traw *__restrict__ raw, i64
         }
         __syncwarp();
         const Traw *cb = b + lane;
-        double acc = __dmul_rn(ct::u2d(cb[rx * 32]), w[0]);
+        double acc = __dmul_rn(ct::u2d(cb[rx * 32]), ws[0]);
+#pragma unroll 4
         for (int d = rx; d >= 1; --d)
-            acc = __dadd_rn(acc, __dmul_rn(ct::pair_f64(cb[(rx - d) * 32], cb[(rx + d) * 32]), w[d]));
+            acc = __dadd_rn(acc, __dmul_rn(ct::pair_f64(cb[(rx - d) * 32], cb[(rx + d) * 32]), ws[d]));
         if (e0 + lane < tot) P1[e0 + lane] = acc;
         __syncwarp();
     }
